@@ -1,0 +1,178 @@
+"""Network specifications (layer lists) for the BASELINE.json configs, and
+seeded tensors for them.  Pure data: the oracle interprets a spec with its own
+numpy definitions; the product's graph builder unrolls the same spec into a
+training-step function graph.
+
+Spec format
+  {"name", "mode": "fp32"|"bf16", "batch": b, "input": [F] or [H, W, C],
+   "classes": K, "sgd": {"lr", "momentum"},
+   "layers": [ {"type": "linear", "name", "in", "out", "features", "relu": bool},
+               {"type": "conv",   "name", "in", "out", "k", "r", "s", "stride", "pad"},
+               {"type": "bn",     "name", "in", "out", "relu": bool, "residual": tensor|None},
+               {"type": "maxpool","name", "in", "out", "r", "stride", "pad"},
+               {"type": "gap",    "name", "in", "out"} ],
+   "loss": {"type": "softmax_ce", "in": logits tensor}}
+The network input tensor is named "x"; labels are "y".  Layout: NHWC
+activations, KRSC conv weights, [out, in] linear weights.
+"""
+import numpy as np
+
+BN_EPS = 1e-5
+
+
+def mlp6(batch=8, width=256, classes=256, mode="fp32"):
+    """configs[0]: 6×Linear(256→256), ReLU after 1-5, softmax-CE over 256
+    classes, SGD-momentum 0.9, lr 0.01."""
+    layers = []
+    prev = "x"
+    for i in range(1, 7):
+        out = f"h{i}" if i < 6 else "logits"
+        layers.append({"type": "linear", "name": f"fc{i}", "in": prev, "out": out,
+                       "features": width if i < 6 else classes, "relu": i < 6})
+        prev = out
+    return {"name": "mlp6", "mode": mode, "batch": batch, "input": [width], "classes": classes,
+            "sgd": {"lr": 0.01, "momentum": 0.9}, "layers": layers,
+            "loss": {"type": "softmax_ce", "in": "logits"}}
+
+
+def resnet(depth=18, batch=8, image=224, classes=1000, mode="bf16", width=64, in_ch=8):
+    """ResNet-18/34 (basic blocks) or ResNet-50 (bottleneck) in NHWC with the
+    C=3 stem input zero-padded to `in_ch` = 8 channels."""
+    cfg = {18: ("basic", [2, 2, 2, 2]), 34: ("basic", [3, 4, 6, 3]),
+           50: ("bottleneck", [3, 4, 6, 3])}[depth]
+    kind, blocks = cfg
+    L = []
+
+    def conv(name, i, o, k, r, st, pad):
+        L.append({"type": "conv", "name": name, "in": i, "out": o, "k": k, "r": r, "s": r,
+                  "stride": st, "pad": pad})
+
+    def bn(name, i, o, relu, res=None):
+        L.append({"type": "bn", "name": name, "in": i, "out": o, "relu": relu, "residual": res})
+
+    conv("conv1", "x", "c1", width, 7, 2, 3)
+    bn("bn1", "c1", "a1", True)
+    L.append({"type": "maxpool", "name": "pool1", "in": "a1", "out": "p1", "r": 3, "stride": 2, "pad": 1})
+    prev, ch = "p1", width
+    for si, nb in enumerate(blocks):
+        planes = width * (2 ** si)
+        for bi in range(nb):
+            st = 2 if (bi == 0 and si > 0) else 1
+            pre = f"l{si + 1}b{bi}"
+            out_ch = planes * (4 if kind == "bottleneck" else 1)
+            res = prev
+            if st != 1 or ch != out_ch:
+                conv(pre + "_dsc", prev, pre + "_dy", out_ch, 1, st, 0)
+                bn(pre + "_dsbn", pre + "_dy", pre + "_ds", False)
+                res = pre + "_ds"
+            if kind == "basic":
+                conv(pre + "_c1", prev, pre + "_y1", planes, 3, st, 1)
+                bn(pre + "_bn1", pre + "_y1", pre + "_a1", True)
+                conv(pre + "_c2", pre + "_a1", pre + "_y2", planes, 3, 1, 1)
+                bn(pre + "_bn2", pre + "_y2", pre + "_out", True, res)
+            else:
+                conv(pre + "_c1", prev, pre + "_y1", planes, 1, 1, 0)
+                bn(pre + "_bn1", pre + "_y1", pre + "_a1", True)
+                conv(pre + "_c2", pre + "_a1", pre + "_y2", planes, 3, st, 1)
+                bn(pre + "_bn2", pre + "_y2", pre + "_a2", True)
+                conv(pre + "_c3", pre + "_a2", pre + "_y3", out_ch, 1, 1, 0)
+                bn(pre + "_bn3", pre + "_y3", pre + "_out", True, res)
+            prev, ch = pre + "_out", out_ch
+    L.append({"type": "gap", "name": "gap", "in": prev, "out": "feat"})
+    L.append({"type": "linear", "name": "fc", "in": "feat", "out": "logits", "features": classes,
+              "relu": False})
+    return {"name": f"resnet{depth}", "mode": mode, "batch": batch, "input": [image, image, in_ch],
+            "classes": classes, "sgd": {"lr": 0.1, "momentum": 0.9}, "layers": L,
+            "loss": {"type": "softmax_ce", "in": "logits"}}
+
+
+def tiny_resnet(batch=4, image=16, classes=10, mode="bf16"):
+    """A two-stage basic-block ResNet small enough for the fp64 oracle in
+    seconds, with every layer kind of ResNet-18 (stem 7×7/2, maxpool,
+    identity and downsample blocks, gap, fc)."""
+    spec = resnet(18, batch=batch, image=image, classes=classes, mode=mode, width=16)
+    keep = []
+    for lay in spec["layers"]:
+        if lay["name"].startswith(("l3", "l4")):
+            continue
+        keep.append(lay)
+    for lay in keep:
+        if lay["type"] == "gap":
+            lay["in"] = "l2b1_out"
+    spec["layers"] = keep
+    spec["name"] = "tiny_resnet"
+    return spec
+
+
+# ----------------------------------------------------------------------------
+# shapes and seeded tensors
+
+
+def tensor_shapes(spec):
+    """Shape of every activation tensor (without batch) and every parameter."""
+    shapes = {"x": list(spec["input"])}
+    params = {}
+    for lay in spec["layers"]:
+        t = lay["type"]
+        ish = shapes[lay["in"]]
+        if t == "linear":
+            fin = int(np.prod(ish))
+            params[lay["name"] + ".W"] = [lay["features"], fin]
+            params[lay["name"] + ".b"] = [lay["features"]]
+            shapes[lay["out"]] = [lay["features"]]
+        elif t == "conv":
+            H, W, C = ish
+            P = (H + 2 * lay["pad"] - lay["r"]) // lay["stride"] + 1
+            Q = (W + 2 * lay["pad"] - lay["s"]) // lay["stride"] + 1
+            params[lay["name"] + ".W"] = [lay["k"], lay["r"], lay["s"], C]
+            shapes[lay["out"]] = [P, Q, lay["k"]]
+        elif t == "bn":
+            C = ish[-1]
+            params[lay["name"] + ".gamma"] = [C]
+            params[lay["name"] + ".beta"] = [C]
+            shapes[lay["out"]] = list(ish)
+        elif t == "maxpool":
+            H, W, C = ish
+            P = (H + 2 * lay["pad"] - lay["r"]) // lay["stride"] + 1
+            Q = (W + 2 * lay["pad"] - lay["r"]) // lay["stride"] + 1
+            shapes[lay["out"]] = [P, Q, C]
+        elif t == "gap":
+            shapes[lay["out"]] = [ish[-1]]
+        else:
+            raise ValueError(t)
+    return shapes, params
+
+
+def make_inputs(spec, seed_x=0, seed_y=1):
+    """x ~ N(0,1) (padded stem channels are zero), y ~ U{0..classes-1}; fp32."""
+    b = spec["batch"]
+    rx = np.random.default_rng(seed_x)
+    x = rx.standard_normal([b] + list(spec["input"])).astype(np.float32)
+    if len(spec["input"]) == 3 and spec["input"][2] == 8:
+        x[..., 3:] = 0.0
+    y = np.random.default_rng(seed_y).integers(0, spec["classes"], size=b).astype(np.int32)
+    return x, y
+
+
+def make_params(spec, seed=2):
+    """Linear: W, b ~ U(±1/sqrt(fan_in)); conv: W ~ N(0, 2/fan_in) (He);
+    BN: gamma = 1, beta = 0.  All fp32."""
+    rng = np.random.default_rng(seed)
+    _, pshapes = tensor_shapes(spec)
+    out = {}
+    for name, shp in pshapes.items():
+        if name.endswith(".gamma"):
+            out[name] = np.ones(shp, np.float32)
+        elif name.endswith(".beta"):
+            out[name] = np.zeros(shp, np.float32)
+        elif len(shp) == 4:
+            fan_in = shp[1] * shp[2] * shp[3]
+            out[name] = (rng.standard_normal(shp) * np.sqrt(2.0 / fan_in)).astype(np.float32)
+        elif len(shp) == 2:
+            bound = 1.0 / np.sqrt(shp[1])
+            out[name] = rng.uniform(-bound, bound, shp).astype(np.float32)
+        else:
+            fan_in = pshapes[name[:-2] + ".W"][1]
+            bound = 1.0 / np.sqrt(fan_in)
+            out[name] = rng.uniform(-bound, bound, shp).astype(np.float32)
+    return out

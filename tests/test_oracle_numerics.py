@@ -1,0 +1,166 @@
+"""Pins of the numerics oracle (oracle/numerics.py) against things other
+than itself: library routines (torch's bf16 conversion, scipy's correlate and
+logsumexp, numpy matmul), central finite differences in float64, closed forms
+(BN output moments, one SGD step from zero momentum) and brute-force loops."""
+import copy
+
+import numpy as np
+import pytest
+import scipy.signal
+import scipy.special
+import torch
+
+from oracle import numerics as nm
+from synth import nets
+
+
+def test_round_bf16_matches_library_conversion():
+    rng = np.random.default_rng(0)
+    x = np.concatenate([rng.standard_normal(100000) * 10.0 ** rng.integers(-6, 6, 100000),
+                        [0.0, -0.0, 1.0, 1.00390625, 1.01171875, 3.0e38, -2.5]]).astype(np.float32)
+    ref = torch.from_numpy(x).to(torch.bfloat16).to(torch.float64).numpy()
+    got = nm.round_bf16(x.astype(np.float64))
+    assert np.array_equal(ref, got)
+
+
+def test_conv2d_matches_correlate_and_matmul():
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((1, 9, 11, 1))
+    w = rng.standard_normal((1, 3, 3, 1))
+    y = nm.conv2d(x, w, 1, 1)
+    ref = scipy.signal.correlate(np.pad(x[0, :, :, 0], 1), w[0, :, :, 0], mode="valid")
+    assert np.allclose(y[0, :, :, 0], ref)
+    # stride 2: every other output of the stride-1 result
+    y2 = nm.conv2d(x, w, 2, 1)
+    assert np.allclose(y2[0, :, :, 0], ref[::2, ::2])
+    # 1x1 conv == matmul over channels
+    x = rng.standard_normal((2, 5, 4, 6))
+    w = rng.standard_normal((3, 1, 1, 6))
+    assert np.allclose(nm.conv2d(x, w, 1, 0), x @ w[:, 0, 0, :].T)
+
+
+def _fd(f, arr, idx, eps=1e-6):
+    old = arr[idx]
+    arr[idx] = old + eps
+    fp = f()
+    arr[idx] = old - eps
+    fm = f()
+    arr[idx] = old
+    return (fp - fm) / (2 * eps)
+
+
+def test_conv2d_backward_finite_differences():
+    rng = np.random.default_rng(2)
+    for stride, pad, R in ((1, 1, 3), (2, 1, 3), (2, 3, 7), (2, 0, 1)):
+        x = rng.standard_normal((2, 9, 8, 3))
+        w = rng.standard_normal((4, R, R, 3))
+        y = nm.conv2d(x, w, stride, pad)
+        G = rng.standard_normal(y.shape)
+        dx, dw = nm.conv2d_backward(x, w, G, stride, pad)
+        f = lambda: float((nm.conv2d(x, w, stride, pad) * G).sum())
+        for _ in range(6):
+            i = tuple(int(rng.integers(0, s)) for s in x.shape)
+            assert abs(_fd(f, x, i) - dx[i]) < 1e-5 * (1 + abs(dx[i]))
+            j = tuple(int(rng.integers(0, s)) for s in w.shape)
+            assert abs(_fd(f, w, j) - dw[j]) < 1e-5 * (1 + abs(dw[j]))
+
+
+def test_maxpool_brute_force_and_first_max():
+    rng = np.random.default_rng(3)
+    x = np.round(rng.standard_normal((2, 7, 6, 3)), 1)   # many ties
+    out, arg = nm.maxpool(x, 3, 2, 1)
+    N, H, W, C = x.shape
+    for n in range(N):
+        for p in range(out.shape[1]):
+            for q in range(out.shape[2]):
+                for c in range(C):
+                    best, bi = -np.inf, None
+                    for i in range(3):
+                        for j in range(3):
+                            h, w_ = p * 2 - 1 + i, q * 2 - 1 + j
+                            if 0 <= h < H and 0 <= w_ < W and x[n, h, w_, c] > best:
+                                best, bi = x[n, h, w_, c], i * 3 + j
+                    assert out[n, p, q, c] == best and arg[n, p, q, c] == bi
+    G = rng.standard_normal(out.shape)
+    dx = nm.maxpool_backward(G, arg, x.shape, 3, 2, 1)
+    assert np.isclose(dx.sum(), G.sum())
+
+
+def test_softmax_ce_closed_form_and_fd():
+    rng = np.random.default_rng(4)
+    z = rng.standard_normal((5, 7)) * 3
+    y = rng.integers(0, 7, 5)
+    loss, dz = nm.softmax_ce(z, y)
+    ref = np.mean(scipy.special.logsumexp(z, axis=1) - z[np.arange(5), y])
+    assert np.isclose(loss, ref)
+    for _ in range(5):
+        i = (int(rng.integers(0, 5)), int(rng.integers(0, 7)))
+        assert abs(_fd(lambda: nm.softmax_ce(z, y)[0], z, i) - dz[i]) < 1e-7
+    assert np.allclose(dz.sum(axis=1), 0.0)
+
+
+def _fd_check_spec(spec, n_checks=12, tol=2e-5, seed=5):
+    spec = copy.deepcopy(spec)
+    spec["mode"] = "fp64"
+    x, y = nets.make_inputs(spec)
+    params = {k: v.astype(np.float64) for k, v in nets.make_params(spec).items()}
+    res = nm.train_step(spec, params, x, y)
+    rng = np.random.default_rng(seed)
+    names = sorted(params)
+    for _ in range(n_checks):
+        k = names[int(rng.integers(0, len(names)))]
+        idx = tuple(int(rng.integers(0, s)) for s in params[k].shape)
+        f = lambda: nm.train_step(spec, params, x, y)["loss"]
+        num = _fd(f, params[k], idx, eps=1e-6)
+        ana = res["grads"][k][idx]
+        assert abs(num - ana) <= tol * (abs(ana) + 1e-3), (k, idx, num, ana)
+
+
+def test_mlp_gradients_finite_differences():
+    _fd_check_spec(nets.mlp6(batch=4, width=16, classes=10), n_checks=20)
+
+
+def test_tiny_resnet_gradients_finite_differences():
+    spec = nets.tiny_resnet(batch=2, image=16, classes=5)
+    _fd_check_spec(spec, n_checks=16, tol=5e-5)
+
+
+def test_bn_output_moments_and_sgd_closed_form():
+    spec = nets.mlp6(batch=8, width=32, classes=10)
+    spec["mode"] = "fp64"
+    x, y = nets.make_inputs(spec)
+    p = nets.make_params(spec)
+    r = nm.train_step(spec, p, x, y)
+    for k in p:   # v = g, w' = w - lr g from zero momentum
+        assert np.allclose(r["momentum"][k], r["grads"][k])
+        assert np.allclose(r["params"][k], p[k] - spec["sgd"]["lr"] * r["grads"][k])
+    # BN without ReLU: per-channel output mean = beta, var = gamma^2 var/(var+eps)
+    rng = np.random.default_rng(6)
+    xin = rng.standard_normal((4, 5, 5, 3)) * 2 + 1
+    sp = {"mode": "fp64", "layers": [{"type": "bn", "name": "b", "in": "x", "out": "o", "relu": False,
+                                      "residual": None},
+                                     {"type": "gap", "name": "g", "in": "o", "out": "f"},
+                                     {"type": "linear", "name": "fc", "in": "f", "out": "logits",
+                                      "features": 2, "relu": False}],
+          "loss": {"type": "softmax_ce", "in": "logits"}, "sgd": {"lr": 0.1, "momentum": 0.9}}
+    prm = {"b.gamma": np.array([1.5, 2.0, 0.5]), "b.beta": np.array([0.1, -0.2, 0.3]),
+           "fc.W": np.zeros((2, 3)), "fc.b": np.zeros(2)}
+    out = nm.train_step(sp, prm, xin, np.array([0, 1, 0, 1]))["acts"]["o"]
+    var = xin.var(axis=(0, 1, 2))
+    assert np.allclose(out.mean(axis=(0, 1, 2)), prm["b.beta"])
+    assert np.allclose(out.var(axis=(0, 1, 2)), prm["b.gamma"] ** 2 * var / (var + nm.BN_EPS))
+
+
+def test_bf16_mode_close_to_fp64():
+    """The bf16 storage contract perturbs the fp64 step by O(bf16 eps), not more."""
+    spec = nets.tiny_resnet(batch=2, image=16, classes=5)
+    x, y = nets.make_inputs(spec)
+    p = nets.make_params(spec)
+    r16 = nm.train_step(spec, p, x, y)
+    s64 = copy.deepcopy(spec)
+    s64["mode"] = "fp64"
+    r64 = nm.train_step(s64, p, x, y)
+    errs = [nm.rel_l2(r16["grads"][k], r64["grads"][k]) for k in r64["grads"]]
+    # a bf16 rounding can flip a ReLU mask or a maxpool choice in a 2-sample
+    # batch, so single tensors may move by ~10%; the bulk stays at O(1e-2)
+    assert np.median(errs) < 0.03 and max(errs) < 0.3
