@@ -1,0 +1,650 @@
+// Executor of one out-of-core training step under a window schedule.
+//
+// Per function f_i, in the paper's order (reading Z9):
+//   wait_out[i]  compute stream waits the D2H completion of each waited
+//                variable ("waits for the Swap-out right before f_i", P:86b);
+//                its memory is released at that point
+//   in[i]        H2D stream: wait the release points of the memory the
+//                arrival reuses (static, from the allocator replay), map the
+//                chunks (VA, memoised), copy host->device (h2d) or only
+//                materialise (alloc); record ev_in
+//   f_i          compute stream waits ev_in of V̂_i, launches f_i's kernels,
+//                records ev_done[i]
+//   reserve_out  D2H stream waits ev_done[i], copies device->host
+//                ("Swap-out is reserved right after the previous function
+//                using the variable", P:86b); records ev_out
+//   free[i]      memory released at ev_done[i]
+// Addresses are fixed per arrival slot and identical every step, so after the
+// first step no driver call is made (memoised VA) and the host only issues
+// copies, event waits and kernels.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <dlfcn.h>
+#include <sstream>
+
+#include "mem.hpp"
+#include "ops.hpp"
+
+namespace oc {
+
+namespace {
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// a release point: compute event after f_j, or the D2H completion of departure d
+struct Ref {
+  enum { DONE, OUT } type;
+  uint32_t idx;
+  bool operator==(const Ref& o) const { return type == o.type && idx == o.idx; }
+};
+
+struct Slot {
+  uint32_t var = 0, fn = 0;
+  uint8_t kind = ARRIVE_H2D;
+  CUdeviceptr addr = 0;
+  Span span;                       // VA mode: fixed span of this arrival slot
+  std::vector<uint32_t> chunks;    // VA mode: chunks from the replay
+  std::vector<Ref> waits;          // release points of reused memory
+  int32_t host_dep = -1;           // departure whose D2H must land before this H2D
+};
+
+struct Dep {
+  uint32_t fn, var;
+  uint8_t dirty;
+  int32_t wait_fn;
+};
+
+struct XVar {
+  uint64_t bytes = 0;
+  bool pinned = false, persistent = false;
+  void* dev_fixed = nullptr;       // pinned variables: bound by the caller
+  int64_t host_off = -1;
+  int32_t cur_slot = -1;
+  bool need_wait = false;
+};
+
+struct XFn {
+  const OpDesc* op = nullptr;
+  std::vector<std::vector<uint32_t>> role_vars;  // per role, variables
+  std::vector<int32_t> dep_of_wait;              // parallel to wait_out: departure ids
+  std::vector<uint32_t> dep_reserve;             // departure ids reserved after f_i
+};
+
+struct Interval { double a, b; };
+
+double union_len(std::vector<Interval> v) {
+  std::sort(v.begin(), v.end(), [](const Interval& x, const Interval& y) { return x.a < y.a; });
+  double tot = 0, ca = -1e300, cb = -1e300;
+  for (auto& x : v) {
+    if (x.a > cb) { if (cb > ca) tot += cb - ca; ca = x.a; cb = x.b; }
+    else cb = std::max(cb, x.b);
+  }
+  if (cb > ca) tot += cb - ca;
+  return tot;
+}
+
+std::vector<Interval> merge(std::vector<Interval> v) {
+  std::sort(v.begin(), v.end(), [](const Interval& x, const Interval& y) { return x.a < y.a; });
+  std::vector<Interval> out;
+  for (auto& x : v) {
+    if (out.empty() || x.a > out.back().b) out.push_back(x);
+    else out.back().b = std::max(out.back().b, x.b);
+  }
+  return out;
+}
+
+double inter_len(const std::vector<Interval>& A, const std::vector<Interval>& B) {
+  auto a = merge(A), b = merge(B);
+  size_t i = 0, j = 0;
+  double t = 0;
+  while (i < a.size() && j < b.size()) {
+    double lo = std::max(a[i].a, b[j].a), hi = std::min(a[i].b, b[j].b);
+    if (hi > lo) t += hi - lo;
+    if (a[i].b < b[j].b) ++i; else ++j;
+  }
+  return t;
+}
+
+}  // namespace
+
+struct Exec {
+  int device = 0;
+  const Graph* g = nullptr;
+  const Schedule* s = nullptr;
+  MemPool* mem = nullptr;
+  cudaStream_t cs = nullptr, hs = nullptr, ds = nullptr;
+  oc_exec_options opt{};
+  std::vector<XVar> vars;
+  std::vector<XFn> fns;
+  std::vector<Slot> slots;
+  std::vector<Dep> deps;
+  std::vector<int32_t> end_deps;
+  std::vector<cudaEvent_t> ev_done, ev_in, ev_out;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+  bool have_prev = false;
+  char* host = nullptr;
+  uint64_t host_bytes = 0;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  // timeline (opt.timeline)
+  std::vector<cudaEvent_t> tl_fn0, tl_fn1, tl_in0, tl_in1, tl_out0, tl_out1;
+  std::vector<uint8_t> tl_in_used, tl_out_used;
+  // NCCL
+  void* nccl_lib = nullptr;
+  void* nccl_comm = nullptr;
+  void* nccl_allreduce = nullptr;
+  void* nccl_destroy = nullptr;
+  uint64_t step_index = 0;
+
+  Status create(int dev, const Graph* graph, const Schedule* sch, MemPool* m, const oc_streams& st,
+                const oc_exec_options* o);
+  Status run(oc_step_metrics* out);
+  void destroy();
+  void* addr_of(uint32_t v) const {
+    const XVar& x = vars[v];
+    if (x.pinned) return x.dev_fixed;
+    return x.cur_slot >= 0 ? (void*)slots[x.cur_slot].addr : nullptr;
+  }
+};
+
+Status Exec::create(int dev, const Graph* graph, const Schedule* sch, MemPool* m, const oc_streams& st,
+                    const oc_exec_options* o) {
+  device = dev;
+  g = graph;
+  s = sch;
+  mem = m;
+  cs = (cudaStream_t)st.compute;
+  hs = (cudaStream_t)st.h2d;
+  ds = (cudaStream_t)st.d2h;
+  if (o) opt = *o;
+  OC_CUDA(cudaSetDevice(dev));
+  if (s->replay.oom_fn >= 0) return Status::make(OC_E_DEVICE_OOM, "schedule's allocator replay ran out of memory");
+  const auto& am = s->alloc;
+  if (am.mode != m->model.mode) return Status::make(OC_E_ARG, "schedule and memory pool use different allocator modes");
+  if (am.mode == OC_ALLOC_VA && am.chunk_bytes != m->m_c)
+    return Status::make(OC_E_ARG, "schedule chunk size differs from the pool's");
+  const uint64_t phys = am.phys_bytes ? am.phys_bytes : (s->budget - g->pinned_bytes);
+  if (am.mode == OC_ALLOC_VA && phys / am.chunk_bytes > m->n_chunks)
+    return Status::make(OC_E_ARG, "memory pool has fewer chunks than the schedule's replay");
+  if (am.mode != OC_ALLOC_VA && m->slab_bytes < s->replay.peak_phys)
+    return Status::make(OC_E_ARG, "arena slab smaller than the schedule's peak");
+
+  // variables
+  vars.resize(g->nv());
+  for (uint32_t v = 0; v < g->nv(); ++v) {
+    vars[v].bytes = g->var_bytes[v];
+    vars[v].pinned = g->pinned[v];
+    vars[v].persistent = g->persistent[v];
+  }
+  // host copies: persistent variables and every variable ever swapped out
+  std::vector<uint8_t> needs_host(g->nv(), 0);
+  for (uint32_t v = 0; v < g->nv(); ++v) needs_host[v] = g->persistent[v] && !g->pinned[v];
+  for (auto& F : s->fn)
+    for (auto& d : F.reserve_out) needs_host[d.var] = 1;
+  host_bytes = 0;
+  for (uint32_t v = 0; v < g->nv(); ++v)
+    if (needs_host[v]) {
+      vars[v].host_off = (int64_t)host_bytes;
+      host_bytes += (g->var_bytes[v] + 255) / 256 * 256;
+    }
+  if (host_bytes) {
+    OC_CUDA(cudaHostAlloc((void**)&host, host_bytes, cudaHostAllocPortable));
+    std::memset(host, 0, host_bytes);
+  }
+
+  // departures
+  const uint32_t n = g->nf();
+  fns.resize(n);
+  for (uint32_t i = 0; i < n; ++i)
+    for (auto& d : s->fn[i].reserve_out) {
+      fns[i].dep_reserve.push_back((uint32_t)deps.size());
+      deps.push_back(Dep{i, d.var, d.dirty, d.wait_fn});
+    }
+  for (uint32_t i = 0; i < n; ++i)
+    for (uint32_t v : s->fn[i].wait_out) {
+      int32_t id = -1;
+      for (uint32_t d = 0; d < deps.size(); ++d)
+        if (deps[d].wait_fn == (int32_t)i && deps[d].var == v) { id = (int32_t)d; break; }
+      if (id < 0) return Status::make(OC_E_INVARIANT, "wait without a departure");
+      fns[i].dep_of_wait.push_back(id);
+    }
+  for (uint32_t v : s->end_wait) {
+    int32_t id = -1;
+    for (uint32_t d = 0; d < deps.size(); ++d)
+      if (deps[d].wait_fn == -1 && deps[d].var == v) { id = (int32_t)d; break; }
+    if (id < 0) return Status::make(OC_E_INVARIANT, "end wait without a departure");
+    end_deps.push_back(id);
+  }
+
+  // arrival slots and the static hazard analysis over the replay's placements
+  slots.resize(s->n_arrivals);
+  const bool va = am.mode == OC_ALLOC_VA;
+  std::vector<Ref> chunk_rel;                 // VA: last release point per chunk
+  std::vector<uint8_t> chunk_has;
+  struct Range { uint64_t a, b; Ref r; };
+  std::vector<Range> ranges;                  // arena: released byte ranges
+  if (va) { chunk_rel.resize(m->n_chunks); chunk_has.assign(m->n_chunks, 0); }
+  std::vector<int32_t> var_slot(g->nv(), -1), var_last_dep(g->nv(), -1);
+  auto release = [&](uint32_t v, Ref r) {
+    const Slot& sl = slots[var_slot[v]];
+    if (va) {
+      for (uint32_t c : sl.chunks) { chunk_rel[c] = r; chunk_has[c] = 1; }
+    } else {
+      uint64_t off = sl.addr - m->slab;
+      uint64_t al = am.align ? am.align : 512;
+      ranges.push_back(Range{off, off + (vars[v].bytes + al - 1) / al * al, r});
+    }
+    var_slot[v] = -1;
+  };
+  for (uint32_t i = 0; i < n; ++i) {
+    const FnSchedule& F = s->fn[i];
+    for (size_t k = 0; k < F.wait_out.size(); ++k) {
+      uint32_t v = F.wait_out[k];
+      release(v, Ref{Ref::OUT, (uint32_t)fns[i].dep_of_wait[k]});
+    }
+    for (const Arrival& a : F.in) {
+      Slot& sl = slots[a.slot];
+      sl.var = a.var;
+      sl.fn = i;
+      sl.kind = a.kind;
+      auto add = [&](Ref r) {
+        if (r.type == Ref::DONE && r.idx >= i) return;  // cannot happen; defensive
+        if (std::find(sl.waits.begin(), sl.waits.end(), r) == sl.waits.end()) sl.waits.push_back(r);
+      };
+      if (va) {
+        sl.chunks = a.chunks;
+        for (uint32_t c : a.chunks)
+          if (chunk_has[c]) add(chunk_rel[c]);
+        sl.span.m_r = vars[a.var].bytes;
+        sl.span.k = (uint32_t)a.chunks.size();
+        sl.span.m_a = (uint64_t)sl.span.k * m->m_c;
+        OC_TRY(m->reserve(sl.span.m_a, sl.span.va));
+        sl.addr = sl.span.va;
+      } else {
+        sl.addr = m->slab + a.offset;
+        uint64_t al = am.align ? am.align : 512;
+        uint64_t lo = a.offset, hi = a.offset + (vars[a.var].bytes + al - 1) / al * al;
+        for (size_t k = 0; k < ranges.size();) {
+          if (ranges[k].a < hi && lo < ranges[k].b) {
+            add(ranges[k].r);
+            if (lo <= ranges[k].a && ranges[k].b <= hi) { ranges[k] = ranges.back(); ranges.pop_back(); continue; }
+          }
+          ++k;
+        }
+      }
+      if (a.kind == ARRIVE_H2D && var_last_dep[a.var] >= 0) sl.host_dep = var_last_dep[a.var];
+      var_slot[a.var] = (int32_t)a.slot;
+    }
+    for (uint32_t d : fns[i].dep_reserve) var_last_dep[deps[d].var] = (int32_t)d;
+    for (uint32_t v : F.free) release(v, Ref{Ref::DONE, i});
+  }
+
+  // ops
+  size_t ws_need = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const Function& f = g->fns[i];
+    if (f.op.kind != JVal::OBJ) continue;  // a function without compute (planner-only graphs)
+    std::string kind = f.op.gets("kind");
+    const OpDesc* d = find_op(kind);
+    if (!d) {
+      Status e = Status::make(OC_E_UNSUPPORTED, "function " + f.name + ": unknown op kind '" + kind + "'");
+      e.fn = i;
+      return e;
+    }
+    fns[i].op = d;
+    const JVal* args = f.op.get("args");
+    fns[i].role_vars.resize(d->roles.size());
+    for (size_t r = 0; r < d->roles.size(); ++r) {
+      const JVal* a = args ? args->get(d->roles[r]) : nullptr;
+      if (!a || a->kind == JVal::NUL) continue;
+      std::vector<const JVal*> items;
+      if (a->kind == JVal::ARR) for (auto& x : a->arr) items.push_back(&x);
+      else items.push_back(a);
+      for (const JVal* x : items) {
+        uint32_t v = UINT32_MAX;
+        for (uint32_t j = 0; j < g->nv(); ++j)
+          if (g->var_names[j] == x->s) { v = j; break; }
+        if (v == UINT32_MAX || x->kind != JVal::STR) {
+          Status e = Status::make(OC_E_INVALID, "function " + f.name + ": role " + d->roles[r] + " names no variable");
+          e.fn = i;
+          return e;
+        }
+        bool used = std::find(f.in.begin(), f.in.end(), v) != f.in.end() ||
+                    std::find(f.out.begin(), f.out.end(), v) != f.out.end();
+        if (!used) {
+          Status e = Status::make(OC_E_INVALID, "function " + f.name + ": op reads " + x->s + " which is not in V̂_i");
+          e.fn = i;
+          e.var = v;
+          return e;
+        }
+        fns[i].role_vars[r].push_back(v);
+      }
+    }
+    const JVal* attrs = f.op.get("attrs");
+    if (d->workspace && attrs) ws_need = std::max(ws_need, d->workspace(*attrs));
+  }
+  ws_bytes = ws_need;
+  if (ws_bytes) OC_CUDA(cudaMalloc(&ws, ws_bytes));
+
+  // events
+  auto mk = [&](std::vector<cudaEvent_t>& v, size_t cnt, bool timing) -> Status {
+    v.assign(cnt, nullptr);
+    for (auto& e : v) OC_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+    return Status::ok();
+  };
+  OC_TRY(mk(ev_done, n, false));
+  OC_TRY(mk(ev_in, slots.size(), false));
+  OC_TRY(mk(ev_out, deps.size(), false));
+  OC_CUDA(cudaEventCreate(&ev_start));
+  OC_CUDA(cudaEventCreate(&ev_end));
+  if (opt.timeline) {
+    OC_TRY(mk(tl_fn0, n, true));
+    OC_TRY(mk(tl_fn1, n, true));
+    OC_TRY(mk(tl_in0, slots.size(), true));
+    OC_TRY(mk(tl_in1, slots.size(), true));
+    OC_TRY(mk(tl_out0, deps.size(), true));
+    OC_TRY(mk(tl_out1, deps.size(), true));
+  }
+  return Status::ok();
+}
+
+Status Exec::run(oc_step_metrics* out) {
+  OC_CUDA(cudaSetDevice(device));
+  for (uint32_t v = 0; v < vars.size(); ++v) {
+    if (vars[v].pinned && !vars[v].dev_fixed) {
+      Status e = Status::make(OC_E_ARG, "pinned variable " + g->var_names[v] + " has no bound device address");
+      e.var = v;
+      return e;
+    }
+    vars[v].cur_slot = -1;
+    vars[v].need_wait = false;
+  }
+  const double t_host0 = now_ms();
+  const double map0 = mem->map_us, unmap0 = mem->unmap_us;
+  uint64_t bytes_h2d = 0, bytes_d2h = 0;
+  uint32_t n_h2d = 0, n_d2h = 0, n_kernels = 0;
+  tl_in_used.assign(slots.size(), 0);
+  tl_out_used.assign(deps.size(), 0);
+
+  OC_CUDA(cudaEventRecord(ev_start, cs));
+  // the previous step (incl. its end waits) is complete on the compute stream
+  OC_CUDA(cudaStreamWaitEvent(hs, ev_start, 0));
+  OC_CUDA(cudaStreamWaitEvent(ds, ev_start, 0));
+  auto ev_of = [&](const Ref& r) { return r.type == Ref::DONE ? ev_done[r.idx] : ev_out[r.idx]; };
+  const uint32_t n = g->nf();
+  for (uint32_t i = 0; i < n; ++i) {
+    const FnSchedule& F = s->fn[i];
+    XFn& X = fns[i];
+    // (b) waits before f_i
+    for (size_t k = 0; k < X.dep_of_wait.size(); ++k) {
+      OC_CUDA(cudaStreamWaitEvent(cs, ev_out[X.dep_of_wait[k]], 0));
+      vars[F.wait_out[k]].cur_slot = -1;  // swapped out: no longer resident
+    }
+    // (a) arrivals
+    for (const Arrival& a : F.in) {
+      Slot& sl = slots[a.slot];
+      if (s->alloc.mode == OC_ALLOC_VA) OC_TRY(mem->bind(sl.span, sl.chunks));
+      for (const Ref& r : sl.waits) OC_CUDA(cudaStreamWaitEvent(hs, ev_of(r), 0));
+      if (sl.kind == ARRIVE_H2D) {
+        if (sl.host_dep >= 0) OC_CUDA(cudaStreamWaitEvent(hs, ev_out[sl.host_dep], 0));
+        XVar& xv = vars[sl.var];
+        if (opt.timeline) { OC_CUDA(cudaEventRecord(tl_in0[a.slot], hs)); tl_in_used[a.slot] = 1; }
+        OC_CUDA(cudaMemcpyAsync((void*)sl.addr, host + xv.host_off, xv.bytes, cudaMemcpyHostToDevice, hs));
+        if (opt.timeline) OC_CUDA(cudaEventRecord(tl_in1[a.slot], hs));
+        bytes_h2d += xv.bytes;
+        ++n_h2d;
+      }
+      OC_CUDA(cudaEventRecord(ev_in[a.slot], hs));
+      vars[sl.var].cur_slot = (int32_t)a.slot;
+      vars[sl.var].need_wait = true;
+    }
+    // f_i on the compute stream
+    const Function& f = g->fns[i];
+    for (int pass = 0; pass < 2; ++pass)
+      for (uint32_t v : (pass == 0 ? f.in : f.out)) {
+        XVar& xv = vars[v];
+        if (xv.pinned) continue;
+        if (xv.cur_slot < 0) {
+          Status e = Status::make(OC_E_INVARIANT, "variable " + g->var_names[v] + " not resident at " + f.name);
+          e.fn = i;
+          e.var = v;
+          return e;
+        }
+        if (xv.need_wait) {
+          OC_CUDA(cudaStreamWaitEvent(cs, ev_in[xv.cur_slot], 0));
+          xv.need_wait = false;
+        }
+      }
+    if (opt.timeline) OC_CUDA(cudaEventRecord(tl_fn0[i], cs));
+    if (X.op) {
+      OpArgs oa;
+      oa.ptr.resize(X.role_vars.size());
+      oa.bytes.resize(X.role_vars.size());
+      for (size_t r = 0; r < X.role_vars.size(); ++r)
+        for (uint32_t v : X.role_vars[r]) {
+          oa.ptr[r].push_back(addr_of(v));
+          oa.bytes[r].push_back(vars[v].bytes);
+        }
+      oa.attrs = f.op.get("attrs");
+      oa.ws = ws;
+      oa.ws_bytes = ws_bytes;
+      oa.stream = cs;
+      oa.nccl_comm = nccl_comm;
+      oa.nccl_allreduce = nccl_allreduce;
+      Status st = X.op->launch(oa);
+      if (!st.good()) {
+        st.fn = i;
+        st.msg = f.name + ": " + st.msg;
+        return st;
+      }
+      n_kernels += oa.n_kernels;
+    }
+    if (opt.timeline) OC_CUDA(cudaEventRecord(tl_fn1[i], cs));
+    OC_CUDA(cudaEventRecord(ev_done[i], cs));
+    // (c) reserved swap-outs after f_i
+    for (uint32_t d : X.dep_reserve) {
+      const Dep& D = deps[d];
+      XVar& xv = vars[D.var];
+      OC_CUDA(cudaStreamWaitEvent(ds, ev_done[i], 0));
+      if (D.dirty || !opt.elide_clean) {
+        if (opt.timeline) { OC_CUDA(cudaEventRecord(tl_out0[d], ds)); tl_out_used[d] = 1; }
+        OC_CUDA(cudaMemcpyAsync(host + xv.host_off, addr_of(D.var), xv.bytes, cudaMemcpyDeviceToHost, ds));
+        if (opt.timeline) OC_CUDA(cudaEventRecord(tl_out1[d], ds));
+        bytes_d2h += xv.bytes;
+        ++n_d2h;
+      }
+      OC_CUDA(cudaEventRecord(ev_out[d], ds));
+    }
+    // frees: nothing to issue; the memory is released at ev_done[i]
+    for (uint32_t v : F.free) vars[v].cur_slot = -1;
+  }
+  for (int32_t d : end_deps) OC_CUDA(cudaStreamWaitEvent(cs, ev_out[d], 0));
+  OC_CUDA(cudaEventRecord(ev_end, cs));
+  const double t_host1 = now_ms();
+  OC_CUDA(cudaEventSynchronize(ev_end));
+  ++step_index;
+  if (out) {
+    std::memset(out, 0, sizeof(*out));
+    float ms = 0;
+    OC_CUDA(cudaEventElapsedTime(&ms, ev_start, ev_end));
+    out->step_ms = ms;
+    out->bytes_h2d = bytes_h2d;
+    out->bytes_d2h = bytes_d2h;
+    out->n_h2d = n_h2d;
+    out->n_d2h = n_d2h;
+    out->n_kernels = n_kernels;
+    out->host_issue_ms = t_host1 - t_host0;
+    out->map_us = mem->map_us - map0;
+    out->unmap_us = mem->unmap_us - unmap0;
+    if (opt.timeline) {
+      std::vector<Interval> C, H, D, T;
+      auto iv = [&](cudaEvent_t a, cudaEvent_t b) {
+        float x = 0, y = 0;
+        cudaEventElapsedTime(&x, ev_start, a);
+        cudaEventElapsedTime(&y, ev_start, b);
+        return Interval{x, y};
+      };
+      for (uint32_t i = 0; i < n; ++i)
+        if (fns[i].op) C.push_back(iv(tl_fn0[i], tl_fn1[i]));
+      for (size_t k = 0; k < slots.size(); ++k)
+        if (tl_in_used[k]) H.push_back(iv(tl_in0[k], tl_in1[k]));
+      for (size_t k = 0; k < deps.size(); ++k)
+        if (tl_out_used[k]) D.push_back(iv(tl_out0[k], tl_out1[k]));
+      T = H;
+      T.insert(T.end(), D.begin(), D.end());
+      out->compute_busy_ms = union_len(C);
+      out->h2d_busy_ms = union_len(H);
+      out->d2h_busy_ms = union_len(D);
+      double tl = union_len(T);
+      out->overlap_frac = tl > 0 ? inter_len(T, C) / tl : 1.0;
+      out->stall_ms = out->step_ms - out->compute_busy_ms;
+    }
+  }
+  return Status::ok();
+}
+
+void Exec::destroy() {
+  cudaSetDevice(device);
+  cudaDeviceSynchronize();
+  for (auto& sl : slots) {
+    if (sl.span.va) {
+      if (!sl.span.mapped.empty()) mem->driver_unmap(sl.span);
+      mem->drv->MemAddressFree(sl.span.va, sl.span.m_a);
+    }
+  }
+  auto kill = [](std::vector<cudaEvent_t>& v) { for (auto e : v) if (e) cudaEventDestroy(e); v.clear(); };
+  kill(ev_done); kill(ev_in); kill(ev_out);
+  kill(tl_fn0); kill(tl_fn1); kill(tl_in0); kill(tl_in1); kill(tl_out0); kill(tl_out1);
+  if (ev_start) cudaEventDestroy(ev_start);
+  if (ev_end) cudaEventDestroy(ev_end);
+  if (host) cudaFreeHost(host);
+  if (ws) cudaFree(ws);
+  if (nccl_comm && nccl_destroy) ((int (*)(void*))nccl_destroy)(nccl_comm);
+}
+
+}  // namespace oc
+
+using namespace oc;
+
+struct oc_exec {
+  Exec x;
+};
+
+extern "C" {
+
+int oc_exec_create(int device, const oc_graph* g, const oc_schedule* s, oc_mem* m, const oc_streams* st,
+                   const oc_exec_options* opt, oc_exec** out, oc_err* err) {
+  if (!g || !s || !m || !st || !out) return OC_E_ARG;
+  *out = nullptr;
+  oc_exec* x = new oc_exec();
+  Status r = x->x.create(device, &g->g, &s->s, &m->p, *st, opt);
+  if (!r.good()) {
+    r.fill(err);
+    x->x.destroy();
+    delete x;
+    return r.code;
+  }
+  *out = x;
+  return OC_OK;
+}
+
+int oc_exec_bind_device(oc_exec* x, uint32_t var, void* dev_ptr, oc_err* err) {
+  if (!x || var >= x->x.vars.size() || !x->x.vars[var].pinned) {
+    Status::make(OC_E_ARG, "oc_exec_bind_device: not a pinned variable").fill(err);
+    return OC_E_ARG;
+  }
+  x->x.vars[var].dev_fixed = dev_ptr;
+  return OC_OK;
+}
+
+int oc_exec_host_ptr(oc_exec* x, uint32_t var, void** host_ptr, oc_err* err) {
+  if (!x || !host_ptr || var >= x->x.vars.size() || x->x.vars[var].host_off < 0) {
+    Status::make(OC_E_ARG, "oc_exec_host_ptr: variable has no host copy").fill(err);
+    return OC_E_ARG;
+  }
+  *host_ptr = x->x.host + x->x.vars[var].host_off;
+  return OC_OK;
+}
+
+int oc_run_step(oc_exec* x, oc_step_metrics* out, oc_err* err) {
+  if (!x) return OC_E_ARG;
+  Status st = x->x.run(out);
+  st.fill(err);
+  return st.code;
+}
+
+int oc_exec_timeline(oc_exec* xh, char* buf, size_t cap, size_t* need) {
+  if (!xh) return OC_E_ARG;
+  Exec& X = xh->x;
+  std::ostringstream o;
+  if (X.opt.timeline) {
+    auto t = [&](cudaEvent_t e) { float v = 0; cudaEventElapsedTime(&v, X.ev_start, e); return v; };
+    for (uint32_t i = 0; i < X.fns.size(); ++i)
+      if (X.fns[i].op)
+        o << "{\"t0\":" << t(X.tl_fn0[i]) << ",\"t1\":" << t(X.tl_fn1[i]) << ",\"stream\":\"compute\",\"id\":\""
+          << X.g->fns[i].name << "\"}\n";
+    for (size_t k = 0; k < X.slots.size(); ++k)
+      if (k < X.tl_in_used.size() && X.tl_in_used[k])
+        o << "{\"t0\":" << t(X.tl_in0[k]) << ",\"t1\":" << t(X.tl_in1[k]) << ",\"stream\":\"h2d\",\"id\":\""
+          << X.g->var_names[X.slots[k].var] << "\"}\n";
+    for (size_t k = 0; k < X.deps.size(); ++k)
+      if (k < X.tl_out_used.size() && X.tl_out_used[k])
+        o << "{\"t0\":" << t(X.tl_out0[k]) << ",\"t1\":" << t(X.tl_out1[k]) << ",\"stream\":\"d2h\",\"id\":\""
+          << X.g->var_names[X.deps[k].var] << "\"}\n";
+  }
+  std::string j = o.str();
+  if (need) *need = j.size();
+  if (!buf || cap < j.size() + 1) return buf ? OC_E_BUFFER_TOO_SMALL : OC_OK;
+  std::memcpy(buf, j.c_str(), j.size() + 1);
+  return OC_OK;
+}
+
+void oc_exec_destroy(oc_exec* x) {
+  if (!x) return;
+  x->x.destroy();
+  delete x;
+}
+
+// ---------------------------------------------------------------- NCCL
+typedef struct { char internal[128]; } nccl_uid;
+typedef int (*nccl_get_uid_t)(nccl_uid*);
+typedef int (*nccl_init_rank_t)(void**, int, nccl_uid, int);
+
+static void* open_nccl() {
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  return h;
+}
+
+int oc_nccl_unique_id(void* out, oc_err* err) {
+  void* h = open_nccl();
+  if (!h || !out) { Status::make(OC_E_NCCL, "libnccl.so.2 not loadable").fill(err); return OC_E_NCCL; }
+  auto f = (nccl_get_uid_t)dlsym(h, "ncclGetUniqueId");
+  if (!f) { Status::make(OC_E_NCCL, "ncclGetUniqueId missing").fill(err); return OC_E_NCCL; }
+  int r = f((nccl_uid*)out);
+  if (r) { Status s = Status::make(OC_E_NCCL, "ncclGetUniqueId failed"); s.cuda = r; s.fill(err); return OC_E_NCCL; }
+  return OC_OK;
+}
+
+int oc_exec_attach_nccl(oc_exec* xh, const void* uid, int rank, int nranks, oc_err* err) {
+  if (!xh || !uid) return OC_E_ARG;
+  Exec& X = xh->x;
+  void* h = open_nccl();
+  if (!h) { Status::make(OC_E_NCCL, "libnccl.so.2 not loadable").fill(err); return OC_E_NCCL; }
+  auto init = (nccl_init_rank_t)dlsym(h, "ncclCommInitRank");
+  X.nccl_allreduce = dlsym(h, "ncclAllReduce");
+  X.nccl_destroy = dlsym(h, "ncclCommDestroy");
+  if (!init || !X.nccl_allreduce) { Status::make(OC_E_NCCL, "NCCL symbols missing").fill(err); return OC_E_NCCL; }
+  cudaSetDevice(X.device);
+  nccl_uid id;
+  std::memcpy(&id, uid, sizeof(id));
+  int r = init(&X.nccl_comm, nranks, id, rank);
+  if (r) { Status s = Status::make(OC_E_NCCL, "ncclCommInitRank failed"); s.cuda = r; s.fill(err); return OC_E_NCCL; }
+  return OC_OK;
+}
+
+}  // extern "C"

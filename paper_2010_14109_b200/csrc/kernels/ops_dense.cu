@@ -1,0 +1,315 @@
+// Dense-layer kernels of the training step:
+// linear forward/backward, softmax cross-entropy, SGD with momentum and the
+// data-parallel gradient all-reduce.  All reductions run in a fixed order so
+// a step is bitwise reproducible whatever the swap schedule (swap
+// transparency).
+//
+// The GEMM here is a SIMT FFMA kernel: the fp32 parity mode must not use TF32
+// tensor cores, and the dense layers of the configs are tiny
+// (MLP 8×256×256, ResNet FC b×512×1000).  Convolutions — the dominant
+// contractions — run on tcgen05 (kernels/conv_tc.cu).
+#include "common.cuh"
+
+namespace oc {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
+
+// C[m,n] (+)= Σ_k A(m,k)·B(k,n), generic strides.
+//   maskA: A(m,k) is used only where mask(m,k) > 0 (ReLU'(·), same strides as A)
+//   RB:    round B to bf16 on load (bf16 copy of an fp32 master weight)
+//   bias:  per-n bias; relu: max(·,0); accumulate: C = rnd(C + acc)
+template <typename TA, typename TB, typename TC, bool RB>
+__global__ void __launch_bounds__(256) gemm_simt(int M, int N, int K, const TA* __restrict__ A, int64_t sam,
+                                                 int64_t sak, const TA* __restrict__ maskA, const TB* __restrict__ B,
+                                                 int64_t sbk, int64_t sbn, TC* C, int64_t scm, int64_t scn,
+                                                 const float* __restrict__ bias, int relu, int accumulate) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tx = tid % 16, ty = tid / 16;
+  float acc[TM][TN] = {};
+  for (int k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int e = tid + r * 256;  // 0..1023
+      int mm = e % BM, kk = e / BM;
+      int gm = m0 + mm, gk = k0 + kk;
+      float va = 0.f;
+      if (gm < M && gk < K) {
+        int64_t off = gm * sam + gk * sak;
+        va = ld_f(A + off);
+        if (maskA && !(ld_f(maskA + off) > 0.f)) va = 0.f;
+      }
+      As[kk][mm] = va;
+      int nn = e % BN, kb = e / BN;
+      int gn = n0 + nn, gk2 = k0 + kb;
+      float vb = 0.f;
+      if (gn < N && gk2 < K) {
+        vb = ld_f(B + gk2 * sbk + gn * sbn);
+        if (RB) vb = rnd<__nv_bfloat16>(vb);
+      }
+      Bs[kb][nn] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[j] = Bs[kk][tx * TN + j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    int gm = m0 + ty * TM + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      int gn = n0 + tx * TN + j;
+      if (gn >= N) continue;
+      float v = acc[i][j];
+      if (bias) v += bias[gn];
+      if (relu) v = fmaxf(v, 0.f);
+      TC* p = C + gm * scm + gn * scn;
+      if (accumulate) v = v + ld_f(p);
+      st_f(p, v);
+    }
+  }
+}
+
+template <typename TA, typename TB, typename TC, bool RB>
+Status gemm(OpArgs& a, int M, int N, int K, const TA* A, int64_t sam, int64_t sak, const TA* mask, const TB* B,
+            int64_t sbk, int64_t sbn, TC* C, int64_t scm, int64_t scn, const float* bias, bool relu, bool acc) {
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
+  gemm_simt<TA, TB, TC, RB><<<grid, 256, 0, a.stream>>>(M, N, K, A, sam, sak, mask, B, sbk, sbn, C, scm, scn, bias,
+                                                        relu ? 1 : 0, acc ? 1 : 0);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+
+// db[n] = Σ_m dz[m,n] (masked), sequential over m per column: deterministic
+template <typename T>
+__global__ void colsum(int M, int N, const T* __restrict__ dy, const T* __restrict__ mask, float* __restrict__ out) {
+  int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  float s = 0.f;
+  for (int m = 0; m < M; ++m) {
+    int64_t o = (int64_t)m * N + n;
+    float v = ld_f(dy + o);
+    if (mask && !(ld_f(mask + o) > 0.f)) v = 0.f;
+    s += v;
+  }
+  out[n] = s;
+}
+
+// ---------------------------------------------------------------- linear
+enum { L_X, L_W, L_B, L_Y };
+Status linear_fwd(OpArgs& a) {
+  const int M = (int)A(a, "M"), N = (int)A(a, "N"), K = (int)A(a, "K");
+  const bool relu = Ab(a, "relu");
+  const std::string dt = As(a, "dtype", "f32");
+  const float* w = (const float*)a.p(L_W);
+  const float* b = (const float*)a.p(L_B);
+  if (dt == "f32")
+    return gemm<float, float, float, false>(a, M, N, K, (const float*)a.p(L_X), K, 1, nullptr, w, 1, K,
+                                            (float*)a.p(L_Y), N, 1, b, relu, false);
+  if (Ab(a, "out_f32"))
+    return gemm<__nv_bfloat16, float, float, true>(a, M, N, K, (const __nv_bfloat16*)a.p(L_X), K, 1, nullptr, w,
+                                                   1, K, (float*)a.p(L_Y), N, 1, b, relu, false);
+  return gemm<__nv_bfloat16, float, __nv_bfloat16, true>(a, M, N, K, (const __nv_bfloat16*)a.p(L_X), K, 1, nullptr,
+                                                         w, 1, K, (__nv_bfloat16*)a.p(L_Y), N, 1, b, relu, false);
+}
+
+// roles: dy, y (ReLU mask source), x, w, dw, db, dx
+enum { LB_DY, LB_Y, LB_X, LB_W, LB_DW, LB_DB, LB_DX };
+Status linear_bwd(OpArgs& a) {
+  const int M = (int)A(a, "M"), N = (int)A(a, "N"), K = (int)A(a, "K");
+  const bool relu = Ab(a, "relu");
+  const std::string dt = As(a, "dtype", "f32");
+  const bool dy_f32 = dt == "f32" || Ab(a, "dy_f32");
+  float* dw = (float*)a.p(LB_DW);
+  float* db = (float*)a.p(LB_DB);
+  if (dt == "f32" || dy_f32) {
+    // dy fp32 [M,N]; mask (if any) has dy's layout and type
+    const float* dy = (const float*)a.p(LB_DY);
+    const float* mask = relu ? (const float*)a.p(LB_Y) : nullptr;
+    // dW[n,k] = Σ_m dz[m,n] x[m,k]
+    if (dt == "f32") {
+      OC_TRY((gemm<float, float, float, false>(a, N, K, M, dy, 1, N, mask, (const float*)a.p(LB_X), K, 1, dw, K, 1,
+                                               nullptr, false, false)));
+    } else {
+      // x is bf16: run with A = x^T? keep A = dz (fp32), B = x (bf16 exact)
+      OC_TRY((gemm<float, __nv_bfloat16, float, false>(a, N, K, M, dy, 1, N, mask,
+                                                       (const __nv_bfloat16*)a.p(LB_X), K, 1, dw, K, 1, nullptr,
+                                                       false, false)));
+    }
+    colsum<float><<<(N + 255) / 256, 256, 0, a.stream>>>(M, N, dy, mask, db);
+    OC_LAUNCH_CHECK(a);
+    if (a.p(LB_DX)) {
+      if (dt == "f32")
+        return gemm<float, float, float, false>(a, M, K, N, dy, N, 1, mask, (const float*)a.p(LB_W), K, 1,
+                                                (float*)a.p(LB_DX), K, 1, nullptr, false, false);
+      return gemm<float, float, __nv_bfloat16, true>(a, M, K, N, dy, N, 1, mask, (const float*)a.p(LB_W), K, 1,
+                                                     (__nv_bfloat16*)a.p(LB_DX), K, 1, nullptr, false, false);
+    }
+    return Status::ok();
+  }
+  // bf16 dy (hidden bf16 linear layers)
+  const __nv_bfloat16* dy = (const __nv_bfloat16*)a.p(LB_DY);
+  const __nv_bfloat16* mask = relu ? (const __nv_bfloat16*)a.p(LB_Y) : nullptr;
+  OC_TRY((gemm<__nv_bfloat16, __nv_bfloat16, float, false>(a, N, K, M, dy, 1, N, mask,
+                                                           (const __nv_bfloat16*)a.p(LB_X), K, 1, dw, K, 1, nullptr,
+                                                           false, false)));
+  colsum<__nv_bfloat16><<<(N + 255) / 256, 256, 0, a.stream>>>(M, N, dy, mask, db);
+  OC_LAUNCH_CHECK(a);
+  if (a.p(LB_DX))
+    return gemm<__nv_bfloat16, float, __nv_bfloat16, true>(a, M, K, N, dy, N, 1, mask, (const float*)a.p(LB_W), K,
+                                                           1, (__nv_bfloat16*)a.p(LB_DX), K, 1, nullptr, false,
+                                                           false);
+  return Status::ok();
+}
+
+// ---------------------------------------------------------------- softmax CE
+// per row: loss_m = logsumexp(z_m) − z_m[y_m]; dz = (softmax(z) − onehot)/M
+__global__ void softmax_ce_rows(int M, int N, const float* __restrict__ z, const int* __restrict__ y,
+                                float* __restrict__ row_loss, float* __restrict__ dz) {
+  const int m = blockIdx.x;
+  const float* zr = z + (int64_t)m * N;
+  __shared__ float red[32];
+  __shared__ float bcast;
+  float mx = -INFINITY;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) mx = fmaxf(mx, zr[n]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) bcast = v;
+  }
+  __syncthreads();
+  mx = bcast;
+  __syncthreads();
+  float s = 0.f;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) s += expf(zr[n] - mx);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) bcast = v;
+  }
+  __syncthreads();
+  s = bcast;
+  const int lab = y[m];
+  const float inv = 1.f / (float)M;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    float p = expf(zr[n] - mx) / s;
+    dz[(int64_t)m * N + n] = (p - (n == lab ? 1.f : 0.f)) * inv;
+  }
+  if (threadIdx.x == 0) row_loss[m] = (logf(s) + mx) - zr[lab];
+}
+
+__global__ void mean_fixed_order(int M, const float* __restrict__ v, float* __restrict__ out) {
+  double s = 0;
+  for (int m = threadIdx.x; m < M; m += 32) s += v[m];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) out[0] = (float)(s / M);
+}
+
+enum { S_LOGITS, S_LABELS, S_LOSS, S_DLOGITS };
+Status softmax_ce(OpArgs& a) {
+  const int M = (int)A(a, "M"), N = (int)A(a, "N");
+  if (a.ws_bytes < (size_t)M * 4) return Status::make(OC_E_INVARIANT, "softmax_ce: workspace too small");
+  softmax_ce_rows<<<M, 256, 0, a.stream>>>(M, N, (const float*)a.p(S_LOGITS), (const int*)a.p(S_LABELS),
+                                           (float*)a.ws, (float*)a.p(S_DLOGITS));
+  OC_LAUNCH_CHECK(a);
+  mean_fixed_order<<<1, 32, 0, a.stream>>>(M, (const float*)a.ws, (float*)a.p(S_LOSS));
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+size_t softmax_ce_ws(const JVal& at) { return (size_t)at.geti("M") * 4; }
+
+// ---------------------------------------------------------------- SGD
+// v ← μ v + g ; w ← w − lr v  (fp32 state; vectorised, grid-stride)
+__global__ void sgd_kernel(int64_t n, float* __restrict__ w, const float* __restrict__ g, float* __restrict__ v,
+                           float lr, float mu) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if ((((uintptr_t)w | (uintptr_t)g | (uintptr_t)v) & 15) == 0) {
+    int64_t n4 = n / 4;
+    for (int64_t k = i; k < n4; k += stride) {
+      float4 gw = reinterpret_cast<const float4*>(g)[k];
+      float4 vv = reinterpret_cast<float4*>(v)[k];
+      float4 ww = reinterpret_cast<float4*>(w)[k];
+      vv.x = fmaf(mu, vv.x, gw.x); vv.y = fmaf(mu, vv.y, gw.y);
+      vv.z = fmaf(mu, vv.z, gw.z); vv.w = fmaf(mu, vv.w, gw.w);
+      ww.x = fmaf(-lr, vv.x, ww.x); ww.y = fmaf(-lr, vv.y, ww.y);
+      ww.z = fmaf(-lr, vv.z, ww.z); ww.w = fmaf(-lr, vv.w, ww.w);
+      reinterpret_cast<float4*>(v)[k] = vv;
+      reinterpret_cast<float4*>(w)[k] = ww;
+    }
+    for (int64_t k = n4 * 4 + i; k < n; k += stride) {
+      float vk = fmaf(mu, v[k], g[k]);
+      v[k] = vk;
+      w[k] = fmaf(-lr, vk, w[k]);
+    }
+  } else {
+    for (int64_t k = i; k < n; k += stride) {
+      float vk = fmaf(mu, v[k], g[k]);
+      v[k] = vk;
+      w[k] = fmaf(-lr, vk, w[k]);
+    }
+  }
+}
+
+enum { G_W, G_G, G_M };
+Status sgd(OpArgs& a) {
+  const float lr = (float)Ad(a, "lr"), mu = (float)Ad(a, "momentum");
+  const size_t cnt = a.ptr[G_W].size();
+  if (a.ptr[G_G].size() != cnt || a.ptr[G_M].size() != cnt) return Status::make(OC_E_INVALID, "sgd: role lengths differ");
+  for (size_t t = 0; t < cnt; ++t) {
+    int64_t n = (int64_t)(a.bytes[G_W][t] / 4);
+    sgd_kernel<<<grid_for(n, 256, 4), 256, 0, a.stream>>>(n, (float*)a.ptr[G_W][t], (const float*)a.ptr[G_G][t],
+                                                          (float*)a.ptr[G_M][t], lr, mu);
+    OC_LAUNCH_CHECK(a);
+  }
+  return Status::ok();
+}
+
+// ---------------------------------------------------------------- all-reduce
+typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+Status allreduce(OpArgs& a) {
+  if (!a.nccl_comm) return Status::ok();  // single replica
+  auto f = (nccl_allreduce_t)a.nccl_allreduce;
+  for (size_t t = 0; t < a.ptr[0].size(); ++t) {
+    // ncclFloat32 = 7, ncclAvg = 4: mean of the replicas' gradients
+    int r = f(a.ptr[0][t], a.ptr[0][t], a.bytes[0][t] / 4, 7, 4, a.nccl_comm, a.stream);
+    if (r) { Status s = Status::make(OC_E_NCCL, "ncclAllReduce failed"); s.cuda = r; return s; }
+  }
+  return Status::ok();
+}
+
+// no compute (placeholder functions in planner-only graphs)
+Status nop(OpArgs&) { return Status::ok(); }
+
+}  // namespace
+
+extern const OpDesc kLinearFwd{"linear_fwd", {"x", "w", "b", "y"}, linear_fwd, nullptr};
+extern const OpDesc kLinearBwd{"linear_bwd", {"dy", "y", "x", "w", "dw", "db", "dx"}, linear_bwd, nullptr};
+extern const OpDesc kSoftmaxCE{"softmax_ce", {"logits", "labels", "loss", "dlogits"}, softmax_ce, softmax_ce_ws};
+extern const OpDesc kSGD{"sgd", {"w", "g", "m"}, sgd, nullptr};
+extern const OpDesc kAllreduce{"allreduce", {"bufs"}, allreduce, nullptr};
+extern const OpDesc kNop{"nop", {}, nop, nullptr};
+
+}  // namespace oc

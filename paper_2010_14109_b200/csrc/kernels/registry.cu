@@ -1,0 +1,27 @@
+// Op kind -> implementation.
+#include <string>
+#include <vector>
+
+#include "../ops.hpp"
+
+namespace oc {
+
+#define OC_OPS(X) X(kLinearFwd) X(kLinearBwd) X(kSoftmaxCE) X(kSGD) X(kAllreduce) X(kNop)
+
+#define OC_DECL(n) extern const OpDesc n;
+OC_OPS(OC_DECL)
+
+void register_ops(std::vector<const OpDesc*>& out) {
+#define OC_PUSH(n) out.push_back(&n);
+  OC_OPS(OC_PUSH)
+}
+
+const OpDesc* find_op(const std::string& kind) {
+  static std::vector<const OpDesc*> all;
+  if (all.empty()) register_ops(all);
+  for (const OpDesc* d : all)
+    if (kind == d->kind) return d;
+  return nullptr;
+}
+
+}  // namespace oc

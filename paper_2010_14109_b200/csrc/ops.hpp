@@ -1,0 +1,57 @@
+// Op registry: the compute of one function f_i (the layer kernels of the
+// training step).  An op descriptor in the graph
+// document looks like
+//   {"kind": "linear_fwd", "args": {"x": var, "w": var, ...}, "attrs": {...}}
+// `args` binds the op's roles to variables (a role may take a list of
+// variables); `attrs` holds shapes and flags.  The executor resolves roles to
+// device addresses before each launch.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "core.hpp"
+#include "cuda_util.hpp"
+
+namespace oc {
+
+struct OpArgs {
+  // one entry per role in OpDesc::roles order; list roles hold several
+  std::vector<std::vector<void*>> ptr;
+  std::vector<std::vector<uint64_t>> bytes;
+  const JVal* attrs = nullptr;
+  void* ws = nullptr;            // executor workspace (outside the budget)
+  size_t ws_bytes = 0;
+  cudaStream_t stream = nullptr;
+  void* nccl_comm = nullptr;     // attached communicator (allreduce)
+  void* nccl_allreduce = nullptr;
+  uint32_t n_kernels = 0;        // incremented by launch()
+  void* p(size_t role, size_t k = 0) const {
+    return (role < ptr.size() && k < ptr[role].size()) ? ptr[role][k] : nullptr;
+  }
+};
+
+struct OpDesc {
+  const char* kind;
+  std::vector<const char*> roles;
+  Status (*launch)(OpArgs& a);
+  size_t (*workspace)(const JVal& attrs);  // may be null
+};
+
+const OpDesc* find_op(const std::string& kind);
+void register_ops(std::vector<const OpDesc*>& out);
+
+inline int64_t A(const OpArgs& a, const char* k, int64_t d = 0) { return a.attrs ? a.attrs->geti(k, d) : d; }
+inline double Ad(const OpArgs& a, const char* k, double d = 0) { return a.attrs ? a.attrs->getd(k, d) : d; }
+inline bool Ab(const OpArgs& a, const char* k, bool d = false) { return a.attrs ? a.attrs->getb(k, d) : d; }
+inline std::string As(const OpArgs& a, const char* k, const char* d = "") { return a.attrs ? a.attrs->gets(k, d) : d; }
+
+#define OC_LAUNCH_CHECK(a)                                   \
+  do {                                                       \
+    cudaError_t e_ = cudaGetLastError();                     \
+    if (e_ != cudaSuccess) return oc::cuda_status(e_, "kernel launch"); \
+    (a).n_kernels++;                                         \
+  } while (0)
+
+}  // namespace oc
