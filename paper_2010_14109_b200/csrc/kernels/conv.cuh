@@ -1,0 +1,28 @@
+// Convolution entry points (implicit GEMM, NHWC / KRSC).
+#pragma once
+#include "common.cuh"
+
+namespace oc {
+
+struct ConvGeom {
+  int N, H, W, C, K, R, S, st, pad, P, Q;
+};
+
+inline ConvGeom conv_geom(const OpArgs& a) {
+  return ConvGeom{(int)A(a, "N"), (int)A(a, "H"), (int)A(a, "W"), (int)A(a, "C"), (int)A(a, "K"), (int)A(a, "R"),
+                  (int)A(a, "S"), (int)A(a, "stride"), (int)A(a, "pad"), (int)A(a, "P"), (int)A(a, "Q")};
+}
+inline ConvGeom conv_geom(const JVal& j) {
+  return ConvGeom{(int)j.geti("N"), (int)j.geti("H"), (int)j.geti("W"), (int)j.geti("C"), (int)j.geti("K"),
+                  (int)j.geti("R"), (int)j.geti("S"), (int)j.geti("stride"), (int)j.geti("pad"), (int)j.geti("P"),
+                  (int)j.geti("Q")};
+}
+
+// CUDA-core implicit GEMM (conv_simt.cu)
+Status conv_fprop_simt(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y);
+Status conv_dgrad_simt(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const float* w, __nv_bfloat16* dx,
+                       bool accumulate);
+Status conv_wgrad_simt(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* x, float* dw);
+size_t conv_wgrad_ws_simt(const ConvGeom& g);
+
+}  // namespace oc

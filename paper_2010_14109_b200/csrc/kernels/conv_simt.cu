@@ -1,0 +1,185 @@
+// Convolution as implicit GEMM on CUDA cores (bf16 operands, fp32 FFMA
+// accumulation) — the reference-speed fallback kept for small/odd shapes and
+// as the cross-check of the tcgen05 kernels (conv_tc.cu).  NHWC activations,
+// KRSC weights (fp32 masters rounded to bf16 on load, the act-dtype copy of
+// the numerics contract).
+//   fprop  y[m=(n,p,q), k]   = Σ_{(r,s,c)} x[n, p·st−pad+r, q·st−pad+s, c] · W[k,r,s,c]
+//   dgrad  dx[m=(n,h,w), c]  = Σ_{(r,s,k)} dy[n, (h+pad−r)/st, (w+pad−s)/st, k] · W[k,r,s,c]
+//                              (terms with a non-integer or out-of-range index vanish)
+//   wgrad  dW[k, (r,s,c)]    = Σ_{m=(n,p,q)} dy[m,k] · x[n, p·st−pad+r, q·st−pad+s, c]
+//          deterministic split-K over m: fixed partial slices, fixed-order sum
+#include "conv.cuh"
+
+namespace oc {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
+
+template <int MODE>
+__global__ void __launch_bounds__(256) conv_simt(ConvGeom g, const __nv_bfloat16* __restrict__ a_src,
+                                                 const float* __restrict__ w, const __nv_bfloat16* __restrict__ b_src,
+                                                 void* out, int accumulate, int64_t k_begin_step) {
+  // GEMM sizes
+  int64_t M, N, Kg;
+  if (MODE == 0) { M = (int64_t)g.N * g.P * g.Q; N = g.K; Kg = (int64_t)g.R * g.S * g.C; }
+  else if (MODE == 1) { M = (int64_t)g.N * g.H * g.W; N = g.C; Kg = (int64_t)g.R * g.S * g.K; }
+  else { M = g.K; N = (int64_t)g.R * g.S * g.C; Kg = (int64_t)g.N * g.P * g.Q; }
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  int64_t kb = 0, ke = Kg;
+  if (MODE == 2) {  // split-K slice z
+    kb = (int64_t)blockIdx.z * k_begin_step;
+    ke = (kb + k_begin_step < Kg) ? kb + k_begin_step : Kg;
+  }
+  float acc[TM][TN] = {};
+  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+#pragma unroll
+    for (int rep = 0; rep < 4; ++rep) {
+      const int e = tid + rep * 256;
+      {  // A tile: As[kk][mm]
+        const int mm = e % BM, kk = e / BM;
+        const int64_t gm = m0 + mm, gk = k0 + kk;
+        float v = 0.f;
+        if (gm < M && gk < ke) {
+          if (MODE == 0) {
+            const int c = (int)(gk % g.C);
+            const int64_t rs = gk / g.C;
+            const int s = (int)(rs % g.S), r = (int)(rs / g.S);
+            const int q = (int)(gm % g.Q);
+            const int64_t t = gm / g.Q;
+            const int p = (int)(t % g.P), n = (int)(t / g.P);
+            const int h = p * g.st - g.pad + r, ww = q * g.st - g.pad + s;
+            if (h >= 0 && h < g.H && ww >= 0 && ww < g.W)
+              v = __bfloat162float(a_src[(((int64_t)n * g.H + h) * g.W + ww) * g.C + c]);
+          } else if (MODE == 1) {
+            const int k = (int)(gk % g.K);
+            const int64_t rs = gk / g.K;
+            const int s = (int)(rs % g.S), r = (int)(rs / g.S);
+            const int ww = (int)(gm % g.W);
+            const int64_t t = gm / g.W;
+            const int h = (int)(t % g.H), n = (int)(t / g.H);
+            const int pn = h + g.pad - r, qn = ww + g.pad - s;
+            if (pn >= 0 && qn >= 0 && pn % g.st == 0 && qn % g.st == 0) {
+              const int p = pn / g.st, q = qn / g.st;
+              if (p < g.P && q < g.Q) v = __bfloat162float(a_src[(((int64_t)n * g.P + p) * g.Q + q) * g.K + k]);
+            }
+          } else {
+            v = __bfloat162float(a_src[gk * g.K + gm]);  // dy[m][k], GEMM row = k
+          }
+        }
+        As[kk][mm] = v;
+      }
+      {  // B tile: Bs[kk][nn]
+        const int nn = e % BN, kk = e / BN;
+        const int64_t gn = n0 + nn, gk = k0 + kk;
+        float v = 0.f;
+        if (gn < N && gk < ke) {
+          if (MODE == 0) {
+            v = rnd<__nv_bfloat16>(w[gn * Kg + gk]);
+          } else if (MODE == 1) {
+            const int k = (int)(gk % g.K);
+            const int64_t rs = gk / g.K;
+            v = rnd<__nv_bfloat16>(w[((int64_t)k * g.R * g.S + rs) * g.C + gn]);
+          } else {
+            const int c = (int)(gn % g.C);
+            const int64_t rs = gn / g.C;
+            const int s = (int)(rs % g.S), r = (int)(rs / g.S);
+            const int q = (int)(gk % g.Q);
+            const int64_t t = gk / g.Q;
+            const int p = (int)(t % g.P), n = (int)(t / g.P);
+            const int h = p * g.st - g.pad + r, ww = q * g.st - g.pad + s;
+            if (h >= 0 && h < g.H && ww >= 0 && ww < g.W)
+              v = __bfloat162float(b_src[(((int64_t)n * g.H + h) * g.W + ww) * g.C + c]);
+          }
+        }
+        Bs[kk][nn] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[j] = Bs[kk][tx * TN + j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t gm = m0 + ty * TM + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t gn = n0 + tx * TN + j;
+      if (gn >= N) continue;
+      if (MODE == 2) {
+        ((float*)out)[((int64_t)blockIdx.z * M + gm) * N + gn] = acc[i][j];
+      } else {
+        __nv_bfloat16* o = (__nv_bfloat16*)out + gm * N + gn;
+        float v = acc[i][j];
+        if (accumulate) v += __bfloat162float(*o);
+        *o = __float2bfloat16_rn(v);
+      }
+    }
+  }
+}
+
+__global__ void splitk_reduce(int splits, int64_t n, const float* __restrict__ part, float* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * n + i];
+    out[i] = s;
+  }
+}
+
+}  // namespace
+
+int wgrad_splits_simt(const ConvGeom& g) {
+  const int64_t tiles = ((g.K + BM - 1) / BM) * (((int64_t)g.R * g.S * g.C + BN - 1) / BN);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(64, 296 / std::max<int64_t>(1, tiles)));
+}
+
+Status conv_fprop_simt(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y) {
+  dim3 grid((g.K + BN - 1) / BN, (unsigned)(((int64_t)g.N * g.P * g.Q + BM - 1) / BM));
+  conv_simt<0><<<grid, 256, 0, a.stream>>>(g, x, w, nullptr, y, 0, 0);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+
+Status conv_dgrad_simt(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const float* w, __nv_bfloat16* dx,
+                       bool accumulate) {
+  dim3 grid((g.C + BN - 1) / BN, (unsigned)(((int64_t)g.N * g.H * g.W + BM - 1) / BM));
+  conv_simt<1><<<grid, 256, 0, a.stream>>>(g, dy, w, nullptr, dx, accumulate ? 1 : 0, 0);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+
+Status conv_wgrad_simt(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* x, float* dw) {
+  const int splits = wgrad_splits_simt(g);
+  const int64_t Kg = (int64_t)g.N * g.P * g.Q;
+  int64_t step = (Kg + splits - 1) / splits;
+  step = (step + BK - 1) / BK * BK;
+  const int64_t n = (int64_t)g.K * g.R * g.S * g.C;
+  if (a.ws_bytes < (size_t)(splits * n * 4)) return Status::make(OC_E_INVARIANT, "wgrad: workspace too small");
+  dim3 grid((unsigned)(((int64_t)g.R * g.S * g.C + BN - 1) / BN), (g.K + BM - 1) / BM, splits);
+  conv_simt<2><<<grid, 256, 0, a.stream>>>(g, dy, nullptr, x, a.ws, 0, step);
+  OC_LAUNCH_CHECK(a);
+  splitk_reduce<<<grid_for(n, 256, 4), 256, 0, a.stream>>>(splits, n, (const float*)a.ws, dw);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+
+size_t conv_wgrad_ws_simt(const ConvGeom& g) {
+  return (size_t)wgrad_splits_simt(g) * g.K * g.R * g.S * g.C * 4;
+}
+
+}  // namespace oc

@@ -1,0 +1,184 @@
+"""Conv-net (ResNet-shaped) training-step graph builder.
+
+Function granularity is chosen so every function's working set stays small
+(the budget floor is max_i bytes(V̂_i)):
+  conv          conv_fwd            [x, W] -> [y]
+  bn(+res,relu) bn_fwd              [y, γ, β, res] -> [out, stat]
+  stem bn+pool  bn_relu_pool_fwd    [y, γ, β] -> [pooled, stat, idx]   (the BN
+                output is never stored; idx = u8 argmax tap)
+  backward, reverse layer order (oracle/numerics.py contract):
+  bn            bn_bwd_reduce       [g, out, y, stat, γ] -> [dγ, dβ]
+                bn_bwd_apply        [g, out, y, stat, γ, dγ, dβ] -> [y := dy, g := dz]
+                (in place: y holds dy afterwards; with a residual, g holds dz,
+                which is the residual's first gradient contribution)
+  stem          pool_bn_bwd_reduce / pool_bn_bwd_apply (y := dy in place)
+  conv          conv_wgrad [dy, x] -> [dW];  conv_dgrad [dy, W, (G)] -> [G]
+                (G accumulates: first contribution rnd(c), later rnd(G + c))
+  per layer     allreduce [grads] -> [grads]; sgd [W, g, m] -> [W, m]
+"""
+import numpy as np
+
+from synth import nets
+
+from .graphs import BF16, F32, I32, U8, Builder, _pvars, _update
+
+
+def build_convnet(spec, params="pinned", inputs="host"):
+    assert spec["mode"] == "bf16", "conv nets run in bf16 mode"
+    b = Builder()
+    Nb = spec["batch"]
+    shapes, pshapes = nets.tensor_shapes(spec)
+    pin_in = inputs == "pinned"
+    x = b.var("x", Nb * int(np.prod(spec["input"])) * BF16, persistent=not pin_in, pinned=pin_in,
+              shape=[Nb] + spec["input"], dtype="bf16")
+    y = b.var("labels", Nb * I32, persistent=not pin_in, pinned=pin_in, shape=[Nb], dtype="i32")
+    P, Mo, G = _pvars(b, spec, pshapes, params)
+    layers = spec["layers"]
+
+    def nbytes(t, dt=BF16):
+        return Nb * int(np.prod(shapes[t])) * dt
+
+    # fuse a bn(relu) immediately consumed only by a maxpool (the stem)
+    consumers = {}
+    for lay in layers:
+        for t in [lay["in"]] + ([lay["residual"]] if lay.get("residual") else []):
+            consumers.setdefault(t, []).append(lay["name"])
+    fused_pool = {}
+    for i, lay in enumerate(layers[:-1]):
+        nxt = layers[i + 1]
+        if lay["type"] == "bn" and lay["relu"] and not lay.get("residual") and nxt["type"] == "maxpool" \
+                and nxt["in"] == lay["out"] and consumers[lay["out"]] == [nxt["name"]]:
+            fused_pool[lay["name"]] = nxt
+    skip = {p["name"] for p in fused_pool.values()}
+
+    t = {"x": x}       # tensor -> variable holding it
+    stat, idx, saved_out = {}, {}, {}
+    for lay in layers:
+        nm, ty = lay["name"], lay["type"]
+        if nm in skip:
+            continue
+        if ty == "conv":
+            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype="bf16")
+            H, W, C = shapes[lay["in"]]
+            Pq, Qq, K = shapes[lay["out"]]
+            attrs = {"N": Nb, "H": H, "W": W, "C": C, "K": K, "R": lay["r"], "S": lay["s"], "stride": lay["stride"],
+                     "pad": lay["pad"], "P": Pq, "Q": Qq}
+            lay["_attrs"] = attrs
+            b.fn(f"fwd.{nm}", "conv_fwd", {"x": t[lay["in"]], "w": P[nm + ".W"], "y": t[lay["out"]]}, attrs,
+                 [t[lay["in"]], P[nm + ".W"]], [t[lay["out"]]])
+        elif ty == "bn":
+            C = shapes[lay["in"]][-1]
+            stat[nm] = b.var(f"stat.{nm}", 2 * C * F32, shape=[2, C], dtype="f32")
+            if nm in fused_pool:
+                pool = fused_pool[nm]
+                H, W, _ = shapes[lay["in"]]
+                Pq, Qq, _ = shapes[pool["out"]]
+                t[pool["out"]] = b.var(pool["out"], nbytes(pool["out"]), shape=[Nb] + shapes[pool["out"]],
+                                       dtype="bf16")
+                idx[nm] = b.var(f"idx.{nm}", nbytes(pool["out"], U8), shape=[Nb] + shapes[pool["out"]], dtype="u8")
+                attrs = {"N": Nb, "H": H, "W": W, "C": C, "r": pool["r"], "stride": pool["stride"], "pad": pool["pad"],
+                         "P": Pq, "Q": Qq}
+                lay["_attrs"] = attrs
+                ins = [t[lay["in"]], P[nm + ".gamma"], P[nm + ".beta"]]
+                b.fn(f"fwd.{nm}+{pool['name']}", "bn_relu_pool_fwd",
+                     {"y": t[lay["in"]], "stat": stat[nm], "gamma": P[nm + ".gamma"], "beta": P[nm + ".beta"],
+                      "out": t[pool["out"]], "idx": idx[nm]}, attrs, ins, [stat[nm], t[pool["out"]], idx[nm]])
+            else:
+                t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype="bf16")
+                rows = Nb * int(np.prod(shapes[lay["in"]][:-1]))
+                res = t[lay["residual"]] if lay.get("residual") else None
+                attrs = {"rows": rows, "C": C, "relu": lay["relu"], "has_res": res is not None}
+                lay["_attrs"] = attrs
+                b.fn(f"fwd.{nm}", "bn_fwd",
+                     {"y": t[lay["in"]], "stat": stat[nm], "gamma": P[nm + ".gamma"], "beta": P[nm + ".beta"],
+                      "res": res, "out": t[lay["out"]]}, attrs,
+                     [t[lay["in"]], P[nm + ".gamma"], P[nm + ".beta"], res], [stat[nm], t[lay["out"]]])
+        elif ty == "gap":
+            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype="bf16")
+            H, W, C = shapes[lay["in"]]
+            lay["_attrs"] = {"N": Nb, "HW": H * W, "C": C}
+            b.fn(f"fwd.{nm}", "gap_fwd", {"x": t[lay["in"]], "out": t[lay["out"]]}, lay["_attrs"], [t[lay["in"]]],
+                 [t[lay["out"]]])
+        elif ty == "linear":
+            t[lay["out"]] = b.var(lay["out"], Nb * lay["features"] * F32, shape=[Nb, lay["features"]], dtype="f32")
+            K = int(np.prod(shapes[lay["in"]]))
+            lay["_attrs"] = {"M": Nb, "N": lay["features"], "K": K, "relu": False, "dtype": "bf16", "out_f32": True}
+            b.fn(f"fwd.{nm}", "linear_fwd", {"x": t[lay["in"]], "w": P[nm + ".W"], "b": P[nm + ".b"],
+                                             "y": t[lay["out"]]}, lay["_attrs"],
+                 [t[lay["in"]], P[nm + ".W"], P[nm + ".b"]], [t[lay["out"]]])
+        else:
+            raise ValueError(f"unsupported layer {ty}")
+    loss = b.var("loss", F32, persistent=True, shape=[], dtype="f32")
+    logits = t[spec["loss"]["in"]]
+    g = {}   # tensor -> variable holding its gradient
+    g[spec["loss"]["in"]] = b.var("grad.logits", Nb * spec["classes"] * F32, shape=[Nb, spec["classes"]],
+                                  dtype="f32")
+    b.fn("loss", "softmax_ce", {"logits": logits, "labels": y, "loss": loss, "dlogits": g[spec["loss"]["in"]]},
+         {"M": Nb, "N": spec["classes"]}, [logits, y], [loss, g[spec["loss"]["in"]]])
+
+    for lay in reversed(layers):
+        nm, ty = lay["name"], lay["type"]
+        if nm in skip:
+            continue
+        out_t = fused_pool[nm]["out"] if nm in fused_pool else lay["out"]
+        if out_t not in g:
+            continue
+        gv = g[out_t]
+        if ty == "linear":
+            dx = b.var(f"grad.{lay['in']}", nbytes(lay["in"]), shape=[Nb] + shapes[lay["in"]], dtype="bf16")
+            at = dict(lay["_attrs"], dy_f32=True)
+            b.fn(f"bwd.{nm}", "linear_bwd", {"dy": gv, "x": t[lay["in"]], "w": P[nm + ".W"], "dw": G[nm + ".W"],
+                                             "db": G[nm + ".b"], "dx": dx}, at,
+                 [gv, t[lay["in"]], P[nm + ".W"]], [G[nm + ".W"], G[nm + ".b"], dx])
+            g[lay["in"]] = dx
+            _update(b, spec, nm, P, Mo, G, [nm + ".W", nm + ".b"])
+        elif ty == "gap":
+            assert lay["in"] not in g
+            dx = b.var(f"grad.{lay['in']}", nbytes(lay["in"]), shape=[Nb] + shapes[lay["in"]], dtype="bf16")
+            b.fn(f"bwd.{nm}", "gap_bwd", {"g": gv, "dx": dx}, lay["_attrs"], [gv], [dx])
+            g[lay["in"]] = dx
+        elif ty == "bn" and nm in fused_pool:
+            yv = t[lay["in"]]
+            args = {"g": gv, "idx": idx[nm], "y": yv, "stat": stat[nm], "gamma": P[nm + ".gamma"],
+                    "beta": P[nm + ".beta"], "dgamma": G[nm + ".gamma"], "dbeta": G[nm + ".beta"]}
+            b.fn(f"bwd.{nm}.reduce", "pool_bn_bwd_reduce", args, lay["_attrs"],
+                 [gv, idx[nm], yv, stat[nm], P[nm + ".gamma"], P[nm + ".beta"]], [G[nm + ".gamma"], G[nm + ".beta"]])
+            b.fn(f"bwd.{nm}.apply", "pool_bn_bwd_apply", args, lay["_attrs"],
+                 [gv, idx[nm], yv, stat[nm], P[nm + ".gamma"], P[nm + ".beta"], G[nm + ".gamma"], G[nm + ".beta"]],
+                 [yv])
+            g[lay["in"]] = yv                    # y now holds dy
+            _update(b, spec, nm, P, Mo, G, [nm + ".gamma", nm + ".beta"])
+        elif ty == "bn":
+            yv, ov = t[lay["in"]], t[lay["out"]]
+            res = lay.get("residual")
+            args = {"g": gv, "out": ov if lay["relu"] else None, "y": yv, "stat": stat[nm], "gamma": P[nm + ".gamma"],
+                    "dgamma": G[nm + ".gamma"], "dbeta": G[nm + ".beta"]}
+            ins = [gv, ov if lay["relu"] else None, yv, stat[nm], P[nm + ".gamma"]]
+            b.fn(f"bwd.{nm}.reduce", "bn_bwd_reduce", args, lay["_attrs"], ins, [G[nm + ".gamma"], G[nm + ".beta"]])
+            b.fn(f"bwd.{nm}.apply", "bn_bwd_apply", args, lay["_attrs"], ins + [G[nm + ".gamma"], G[nm + ".beta"]],
+                 [yv] + ([gv] if res else []))
+            g[lay["in"]] = yv
+            if res:
+                assert res not in g, "residual must receive its first gradient here"
+                g[res] = gv                      # gv now holds dz
+            _update(b, spec, nm, P, Mo, G, [nm + ".gamma", nm + ".beta"])
+        elif ty == "conv":
+            dy = gv
+            b.fn(f"bwd.{nm}.wgrad", "conv_wgrad", {"dy": dy, "x": t[lay["in"]], "dw": G[nm + ".W"]}, lay["_attrs"],
+                 [dy, t[lay["in"]]], [G[nm + ".W"]])
+            if lay["in"] != "x":
+                acc = lay["in"] in g
+                if acc:
+                    dx = g[lay["in"]]
+                    ins = [dy, P[nm + ".W"], dx]
+                else:
+                    dx = b.var(f"grad.{lay['in']}", nbytes(lay["in"]), shape=[Nb] + shapes[lay["in"]], dtype="bf16")
+                    ins = [dy, P[nm + ".W"]]
+                    g[lay["in"]] = dx
+                b.fn(f"bwd.{nm}.dgrad", "conv_dgrad", {"dy": dy, "w": P[nm + ".W"], "dx": dx},
+                     dict(lay["_attrs"], accumulate=acc), ins, [dx])
+            _update(b, spec, nm, P, Mo, G, [nm + ".W"])
+        else:
+            raise ValueError(ty)
+    info = {"params": P, "momentum": Mo, "grads": G, "x": x, "labels": y, "loss": loss, "meta": b.meta}
+    return b.doc(), info

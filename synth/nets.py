@@ -35,9 +35,10 @@ def mlp6(batch=8, width=256, classes=256, mode="fp32"):
             "loss": {"type": "softmax_ce", "in": "logits"}}
 
 
-def resnet(depth=18, batch=8, image=224, classes=1000, mode="bf16", width=64, in_ch=8):
-    """ResNet-18/34 (basic blocks) or ResNet-50 (bottleneck) in NHWC with the
-    C=3 stem input zero-padded to `in_ch` = 8 channels."""
+def resnet(depth=18, batch=8, image=224, classes=1000, mode="bf16", width=64, in_ch=3):
+    """ResNet-18/34 (basic blocks) or ResNet-50 (bottleneck) in NHWC.  The
+    image keeps its 3 channels in memory (the stem's working set bounds the
+    feasible budget); kernels pad channels internally."""
     cfg = {18: ("basic", [2, 2, 2, 2]), 34: ("basic", [3, 4, 6, 3]),
            50: ("bottleneck", [3, 4, 6, 3])}[depth]
     kind, blocks = cfg

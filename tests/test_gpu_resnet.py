@@ -1,0 +1,77 @@
+"""Conv-net training step (bf16) through the C-ABI: parity with the CPU
+oracle (1e-3 relative L2 on every parameter gradient) on a tiny ResNet with
+every ResNet-18 layer kind, swap transparency (out-of-core == in-core,
+bitwise), and the ResNet-18 config's feasibility at 25% of its footprint."""
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import numerics as nm
+from paper_2010_14109_b200 import binding as B
+from paper_2010_14109_b200 import graphs
+from synth import nets
+
+MiB = 1 << 20
+
+
+def to_bf16_bits(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16).view(torch.int16).numpy()
+
+
+def test_resnet18_config_feasible_at_quarter_footprint():
+    """configs[1]: budget fixed at 25% of the in-core footprint F_peak (Z21)."""
+    spec = nets.resnet(18, batch=256)
+    doc, info = graphs.build(spec, params="persistent")
+    G = B.Graph(doc)
+    peak = G.in_core_peak()
+    budget = peak // 4
+    assert G.min_feasible_budget(0) <= budget
+    W = G.max_feasible_window(budget)
+    s = G.plan(budget, W, B.OC_ALLOC_VA, chunk_bytes=2 * MiB, phys_bytes=budget + 256 * MiB, allow_oom=True)
+    st = s.stats()
+    assert st["peak_sched"] <= budget and st["bytes_d2h"] > 0
+
+
+def run_step(spec, doc, info, budget, window, mode, phys, chunk=2 * MiB, steps=1, timeline=False):
+    from paper_2010_14109_b200.runtime import OutOfCoreStep
+    st = OutOfCoreStep(doc, budget, window, mode=mode, chunk_bytes=chunk, phys_bytes=phys, timeline=timeline)
+    x, y = nets.make_inputs(spec)
+    p = nets.make_params(spec)
+    st.write(info["x"], to_bf16_bits(x))
+    st.write(info["labels"], y)
+    for k, v in p.items():
+        st.write(info["params"][k], v)
+        st.write(info["momentum"][k], np.zeros_like(v))
+    for _ in range(steps):
+        met = st.step()
+    out = {"loss": float(st.read(info["loss"])[0]), "metrics": met, "stats": st.stats}
+    for k in p:
+        out["p." + k] = st.read(info["params"][k]).reshape(p[k].shape)
+        out["m." + k] = st.read(info["momentum"][k]).reshape(p[k].shape)
+    st.close()
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["va", "best"])
+def test_tiny_resnet_parity_and_transparency(mode):
+    spec = nets.tiny_resnet(batch=4, image=16, classes=10)
+    doc, info = graphs.build(spec, params="persistent")
+    G = B.Graph(doc)
+    peak = G.in_core_peak()
+    budget = max(G.min_feasible_budget(0), int(peak * 0.5))
+    x, y = nets.make_inputs(spec)
+    p = nets.make_params(spec)
+    ref = nm.train_step(spec, p, x, y)
+    phys = 256 * MiB if mode == "va" else budget * 2
+    ooc = run_step(spec, doc, info, budget, B.OC_WINDOW_MAX_FEASIBLE, mode, phys)
+    assert ooc["metrics"]["bytes_d2h"] > 0
+    assert abs(ooc["loss"] - ref["loss"]) <= 1e-3 * abs(ref["loss"])
+    for k in p:
+        e = nm.rel_l2(ooc["m." + k], ref["grads"][k])
+        assert e <= 1e-3, (k, e)
+    inc = run_step(spec, doc, info, peak, 0, "best", peak * 2)
+    for k in p:
+        assert np.array_equal(inc["m." + k], ooc["m." + k]), k
