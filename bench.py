@@ -1,0 +1,391 @@
+"""Benchmark of the out-of-core training step (BASELINE.json metric:
+"samples/sec at k× in-budget batch vs in-core; host-link GB/s; overlap %").
+
+Default workload (N=1): configs[1] — ResNet-18, 224×224 synthetic images,
+batch 256, budget fixed at 25% of the in-core footprint F_peak (reading Z21),
+schedule-window = the largest feasible (Z12), VA allocator with 2 MiB chunks.
+One step = forward + backward + update of the whole network through the
+C-ABI (oc_run_step), inputs swapped in from pinned host memory as part of the
+schedule.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config r18|r50|mlp] [--mode va|best|first]
+
+Multi-GPU: one process per GPU (torchrun), each replica with its own budget,
+pool and host link (weak scaling); gradients averaged with NCCL inside the
+step.  Rank 0 prints ONE JSON line.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MiB = 1 << 20
+PCIE5_X16_GBS = 63.0          # 32 GT/s × 16 × 128/130 / 8, per direction
+FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # derived peak for FFMA kernels
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="r18", choices=["r18", "r50", "mlp"])
+    ap.add_argument("--mode", default="va", choices=["va", "best", "first"])
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--budget-frac", type=float, default=0.25)
+    ap.add_argument("--chunk-mib", type=int, default=2)
+    ap.add_argument("--no-incore", action="store_true")
+    return ap.parse_args()
+
+
+def config(args):
+    from synth import nets
+    if args.config == "mlp":
+        spec = nets.mlp6()
+        return spec, {"workload": "configs[0] 6-layer MLP fp32 b=8, 4 MiB budget", "budget": 4 * MiB}
+    if args.config == "r50":
+        b = args.batch or 256
+        spec = nets.resnet(50, batch=b)
+        return spec, {"workload": f"ResNet-50 224x224 b={b} at {args.budget_frac:.2f} of F_peak"}
+    b = args.batch or 256
+    spec = nets.resnet(18, batch=b)
+    return spec, {"workload": f"configs[1] ResNet-18 224x224 b={b}, budget {args.budget_frac:.2f} x in-core footprint"}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.samples = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=5)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def trainable_batch(spec_fn, budget, lo=1, hi=4096, params="persistent"):
+    """Largest batch whose IN-CORE footprint fits `budget` (bisection on the
+    planner's F_peak) — the denominator of the trainable-batch multiple."""
+    from paper_2010_14109_b200 import binding as B
+    from paper_2010_14109_b200 import graphs
+
+    def fits(b):
+        doc, _ = graphs.build(spec_fn(b), params=params)
+        return B.Graph(doc).in_core_peak() <= budget
+    if not fits(lo):
+        return 0
+    while lo < hi:
+        mid = (lo + hi + 1) // 2
+        if fits(mid):
+            lo = mid
+        else:
+            hi = mid - 1
+    return lo
+
+
+def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None):
+    import torch
+    from paper_2010_14109_b200 import binding as B
+    from paper_2010_14109_b200.runtime import OutOfCoreStep
+    from synth import nets
+    G = B.Graph(doc)
+    W = window if window is not None else G.max_feasible_window(budget)
+    # VA physical pool: scheduler budget + chunk rounding headroom (Eq.2: IF < N_max·m_c)
+    probe = G.plan(budget, W, B.OC_ALLOC_VA if mode == "va" else B.OC_ALLOC_ARENA_BEST, chunk_bytes=chunk,
+                   phys_bytes=budget * 4, allow_oom=True)
+    ps = probe.stats()
+    phys = ps["peak_phys"] + chunk if mode == "va" else max(ps["peak_phys"], 1)
+    st = OutOfCoreStep(doc, budget, W, mode=mode, chunk_bytes=chunk, phys_bytes=phys, timeline=timeline)
+    x, y = nets.make_inputs(spec)
+    p = nets.make_params(spec)
+    if spec["mode"] == "bf16":
+        xb = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy()
+    else:
+        xb = x
+    st.write(info["x"], xb)
+    st.write(info["labels"], y)
+    for k, v in p.items():
+        st.write(info["params"][k], v)
+        st.write(info["momentum"][k], np.zeros_like(v))
+    return st, W, phys
+
+
+def conv_flops(doc):
+    """Algorithmic FLOPs per function (2·MACs) for the tensor-contraction ops."""
+    d = json.loads(doc)
+    fl = {}
+    for f in d["functions"]:
+        op = f.get("op") or {}
+        a = op.get("attrs", {})
+        k = op.get("kind")
+        if k in ("conv_fwd", "conv_dgrad", "conv_wgrad"):
+            fl[f["id"]] = (k, 2.0 * a["N"] * a["P"] * a["Q"] * a["K"] * a["R"] * a["S"] * a["C"])
+        elif k in ("linear_fwd", "linear_bwd"):
+            fl[f["id"]] = (k, 2.0 * a["M"] * a["N"] * a["K"] * (1 if k == "linear_fwd" else 2))
+    return fl
+
+
+def run_ours(args, rank, world):
+    import torch
+    import torch.distributed as dist
+    from paper_2010_14109_b200 import binding as B
+    from paper_2010_14109_b200 import graphs
+    from paper_2010_14109_b200.runtime import nccl_unique_id
+    from synth import nets
+
+    spec, cfg = config(args)
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    chunk = args.chunk_mib * MiB
+    params = "persistent"
+    doc, info = graphs.build(spec, params=params, inputs="host")
+    G = B.Graph(doc)
+    F_peak = G.in_core_peak()
+    budget = cfg.get("budget") or int(F_peak * args.budget_frac)
+    st, W, phys = setup_step(spec, info, doc, budget, args.mode, chunk)
+    if world > 1:
+        uid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        st.attach_nccl(uid[0], rank, world)
+    for _ in range(args.warmup):
+        st.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    mets = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(dev) as clk:
+        torch.cuda.synchronize()
+        t_wall0 = time.perf_counter()
+        e0.record(st.streams[0])
+        for _ in range(args.steps):
+            mets.append(st.step())
+        e1.record(st.streams[0])
+        torch.cuda.synchronize()
+        t_wall1 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    dev_ms = e0.elapsed_time(e1)
+    tl = st.timeline()
+    loss = float(st.read(info["loss"])[0])
+    ms = torch.tensor([dev_ms, (t_wall1 - t_wall0) * 1e3], dtype=torch.float64)
+    if world > 1:
+        ms = ms.cuda()
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        ms = ms.cpu()
+    dev_ms, wall_ms = float(ms[0]), float(ms[1])
+    B_glob = spec["batch"] * world
+    value = B_glob * args.steps / (dev_ms / 1e3)
+    e2e = B_glob * args.steps / (wall_ms / 1e3)
+    ss = st.stats
+    mstat = st.mem_stats()
+    step_ms = dev_ms / args.steps
+    h2d = float(np.mean([m["bytes_h2d"] for m in mets]))
+    d2h = float(np.mean([m["bytes_d2h"] for m in mets]))
+    overlap = float(np.mean([m["overlap_frac"] for m in mets]))
+    h2d_busy = float(np.mean([m["h2d_busy_ms"] for m in mets]))
+    d2h_busy = float(np.mean([m["d2h_busy_ms"] for m in mets]))
+    comp_busy = float(np.mean([m["compute_busy_ms"] for m in mets]))
+    n_k = int(sum(m["n_kernels"] for m in mets))
+    # dominant contraction kernel from the live per-function events of the timed steps
+    fl = conv_flops(doc)
+    per_kind = {}
+    for ev in tl:
+        if ev["stream"] != "compute" or ev["id"] not in fl:
+            continue
+        kind, f = fl[ev["id"]]
+        a = per_kind.setdefault(kind, [0.0, 0.0, 0])
+        a[0] += f
+        a[1] += (ev["t1"] - ev["t0"]) / 1e3
+        a[2] += 1
+    fn_time = {}
+    for ev in tl:
+        if ev["stream"] == "compute":
+            kind = ev["id"].split(".")[0] if ev["id"] not in fl else fl[ev["id"]][0]
+            fn_time[ev["id"]] = ev["t1"] - ev["t0"]
+    st.close()
+    st = None
+    # in-core reference at the same batch (no budget pressure: W=0, budget = F_peak)
+    incore = None
+    if not args.no_incore and spec["mode"] == "bf16":
+        torch.cuda.empty_cache()
+        st2, _, _ = setup_step(spec, info, doc, F_peak, "best", chunk, timeline=False, window=0)
+        for _ in range(max(1, args.warmup)):
+            st2.step()
+        torch.cuda.synchronize()
+        e0.record(st2.streams[0])
+        for _ in range(max(3, args.steps // 2)):
+            st2.step()
+        e1.record(st2.streams[0])
+        torch.cuda.synchronize()
+        incore = spec["batch"] * max(3, args.steps // 2) / (e0.elapsed_time(e1) / 1e3) * world
+        st2.close()
+    if rank != 0:
+        return None
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
+    roof = None
+    if per_kind:
+        kind, (flops, secs, cnt) = max(per_kind.items(), key=lambda kv: kv[1][1])
+        ach = flops / secs / 1e12
+        impl = os.environ.get("OC_CONV_IMPL", "simt")
+        if impl == "simt":
+            roof = {"bound": "alu", "achieved": ach, "peak": FP32_SIMT_TFLOPS, "unit": "TFLOP/s",
+                    "frac": ach / FP32_SIMT_TFLOPS, "traffic": None, "kernel": kind, "launches": cnt,
+                    "peak_source": "derived: 148 SM x 128 FFMA lanes x 2 x 1.965 GHz"}
+        else:
+            pk = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+            roof = {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
+                    "traffic": None, "kernel": kind, "launches": cnt,
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"}
+    # step-level roofline: slower of compute at tensor peak and swap bytes over the link (NS)
+    total_flops = sum(f for (_, f) in fl.values())
+    t_link = max(h2d / (55.6e9), d2h / (57.3e9))
+    t_tc = total_flops / (peaks.get("bf16_tflops_sustained", 1395.5) * 1e12)
+    t_roof = max(t_link, t_tc)
+    train_mult = None
+    if args.config == "r18":
+        b0 = trainable_batch(lambda b: nets.resnet(18, batch=b), budget)
+        train_mult = spec["batch"] / b0 if b0 else None
+    line = {
+        "metric": "samples/sec at k x in-budget batch vs in-core; host-link GB/s; overlap %",
+        "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16" if spec["mode"] == "bf16" else "f32", "data": "synthetic (seeded N(0,1) images, U labels)",
+        "config": dict(cfg, global_batch=B_glob, per_gpu_batch=spec["batch"], budget_bytes=budget,
+                       in_core_footprint_bytes=F_peak, window_bytes=W, allocator=args.mode, chunk_bytes=chunk,
+                       phys_pool_bytes=phys, parallelism=f"dp{world}",
+                       l2_flush="inputs larger than L2 (activations GBs per step)"),
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "note": "wall clock around oc_run_step with host inputs/params swapped in and loss read back"},
+        "gpu_launches": n_k,
+        "roofline": roof,
+        "step_roofline": {"t_link_ms": t_link * 1e3, "t_tensor_ms": t_tc * 1e3, "bound": "host-link" if t_link > t_tc
+                          else "tensor", "frac": t_roof / (step_ms / 1e3)},
+        "host_link": {"h2d_gbs_step": h2d / (step_ms / 1e3) / 1e9, "d2h_gbs_step": d2h / (step_ms / 1e3) / 1e9,
+                      "h2d_gbs_busy": (h2d / (h2d_busy / 1e3) / 1e9) if h2d_busy else None,
+                      "d2h_gbs_busy": (d2h / (d2h_busy / 1e3) / 1e9) if d2h_busy else None,
+                      "pcie5_x16_gbs_per_dir": PCIE5_X16_GBS, "measured_pinned_gbs": {"h2d": 55.6, "d2h": 57.3}},
+        "overlap_pct": 100 * overlap,
+        "compute_busy_ms": comp_busy,
+        "in_core_samples_per_s": incore,
+        "fraction_of_in_core": (value / incore) if incore else None,
+        "trainable_batch_multiple": train_mult,
+        "schedule": {k: ss[k] for k in ("bytes_h2d", "bytes_alloc", "bytes_d2h", "bytes_d2h_dirty", "peak_sched",
+                                        "peak_phys", "if_peak", "n_max")},
+        "vmm": {k: mstat[k] for k in ("n_driver_map", "n_map_calls", "n_map_memo_hits", "map_us")},
+        "loss": loss,
+        "paper_context": "V100 ResNet-50 b=1440 (7.5x physical memory) at 55% of in-core speed (PAPER.md P:10)",
+    }
+    if rank == 0 and args.config != "mlp":
+        line["cpu_baseline"] = cpu_baseline(args)
+    return line
+
+
+def cpu_baseline(args, steps=1):
+    """The oracle (oracle/numerics.train_step, numpy float64) on a bounded
+    sample of the same workload: ResNet-18 224x224 at batch 2."""
+    from oracle import numerics as nm
+    from synth import nets
+    cores = len(os.sched_getaffinity(0))
+    spec = nets.resnet(18, batch=2) if args.config != "r50" else nets.resnet(50, batch=1)
+    x, y = nets.make_inputs(spec)
+    p = nets.make_params(spec)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        nm.train_step(spec, p, x, y)
+    dt = time.perf_counter() - t0
+    return {"value": spec["batch"] * steps / dt, "unit": "samples/s", "cores": cores, "kind": "oracle",
+            "sample": f"{spec['name']} batch {spec['batch']}, {steps} step(s), numpy float64 with bf16 rounding"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, bounded sample per step."""
+    from oracle import numerics as nm
+    from synth import nets
+    cores = len(os.sched_getaffinity(0))
+    spec = nets.resnet(18, batch=1) if args.config != "mlp" else nets.mlp6()
+    x, y = nets.make_inputs(spec)
+    p = nets.make_params(spec)
+    for _ in range(args.warmup):
+        nm.train_step(spec, p, x, y)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        nm.train_step(spec, p, x, y)
+    dt = time.perf_counter() - t0
+    v = spec["batch"] * args.steps / dt
+    _, cfg = config(args)
+    sample = f"{spec['name']} batch {spec['batch']} per step (numpy float64 oracle)"
+    return {"impl": "reference", "metric": "samples/sec at k x in-budget batch vs in-core; host-link GB/s; overlap %",
+            "value": v, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    line = run_ours(args, rank, world)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
