@@ -269,7 +269,7 @@ def run_ours(args, rank, world):
     if per_kind:
         kind, (flops, secs, cnt) = max(per_kind.items(), key=lambda kv: kv[1][1])
         ach = flops / secs / 1e12
-        impl = os.environ.get("OC_CONV_IMPL", "simt")
+        impl = os.environ.get("OC_CONV_IMPL", "tc")
         if impl == "simt":
             roof = {"bound": "alu", "achieved": ach, "peak": FP32_SIMT_TFLOPS, "unit": "TFLOP/s",
                     "frac": ach / FP32_SIMT_TFLOPS, "traffic": None, "kernel": kind, "launches": cnt,

@@ -1,0 +1,518 @@
+// Convolution on the 5th-generation tensor cores: implicit GEMM with
+// tcgen05.mma (kind::f16, bf16 × bf16 -> fp32 in TMEM), operands gathered
+// from NHWC activations by cp.async straight into the UMMA canonical
+// SWIZZLE_128B shared-memory layouts, an mbarrier-paced multi-stage pipeline,
+// a single elected MMA-issuing thread, and a TMEM -> register epilogue.
+//
+//   fprop  D[m=(n,p,q)][k]        = Σ_{(r,s,c)} X[n,p·st−pad+r,q·st−pad+s,c] · W[k,r,s,c]
+//          A = im2col(X) (K-major rows), B = W_bf16 [K][RSC] (K-major)
+//   dgrad  D[m=(n,h,w)][c]        = Σ_{(r,s,k)} dY[n,(h+pad−r)/st,(w+pad−s)/st,k] · W[k,r,s,c]
+//          one launch per output phase (h mod st, w mod st) over that phase's
+//          valid taps only, so a stride-2 dgrad does no wasted MMA work;
+//          A = gathered dY (K-major), B = Wt_bf16 [C][R][S][K] (K-major)
+//   wgrad  D[(r,s,c)][k]          = Σ_{m=(n,p,q)} X[n,p·st−pad+r,q·st−pad+s,c] · dY[m,k]
+//          both operands MN-major (contiguous along channels), deterministic
+//          split-K over m (fixed slices, fixed-order sum), then dW[k][(r,s,c)]
+//
+// Tile: UMMA M = 128, N = BN (64 or 128), K-block 64 (one 128-byte swizzle
+// row of bf16).  CTA: warps 0-3 gather (cp.async, zero-fill for padding) and
+// run the epilogue, warp 4 lane 0 issues the MMAs.  3 stages of
+// 16 KB + BN·128 B, so two CTAs share an SM and one's epilogue overlaps the
+// other's main loop.
+#include "conv.cuh"
+
+namespace oc {
+
+namespace tc {
+
+constexpr int BM = 128, BKE = 64, STAGES = 3, NPROD = 128, NTHREADS = 160;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// shared-memory matrix descriptor, SWIZZLE_128B (PTX ISA tcgen05 "matrix descriptor")
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: kind::f16, A/B = bf16, D = f32, M = 128
+__host__ __device__ constexpr uint32_t idesc(int n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+
+#define TMEM_LD32(taddr, r)                                                                                          \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"      \
+               "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                            \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),     \
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),            \
+                 "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),          \
+                 "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),          \
+                 "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                               \
+               : "r"(taddr))
+
+enum Mode { FPROP = 0, DGRAD = 1, WGRAD = 2 };
+
+struct Params {
+  ConvGeom g;
+  const __nv_bfloat16* act;    // fprop: X; dgrad: dY; wgrad: X
+  const __nv_bfloat16* wgt;    // fprop: W_bf16 [K][RSC]; dgrad: Wt_bf16 [C][RS][K]; wgrad: dY
+  void* out;                   // fprop/dgrad: bf16 NHWC; wgrad: fp32 partials [z][RSC][K]
+  int accumulate;              // dgrad: out = rnd(acc + out)
+  int64_t M, N;                // GEMM sizes
+  int64_t nkb;                 // K-blocks (per split for wgrad)
+  int64_t kb_per_split;        // wgrad
+  int64_t gemm_k;              // wgrad: N·P·Q
+  // dgrad phase
+  int ph, pw, Hp, Wp;          // output sub-grid of this phase: h = h'·st + ph
+  int r0, s0, nr, ns;          // valid taps: r = r0 + st·i (i < nr), s = s0 + st·j (j < ns)
+};
+
+template <int MODE, int BN>
+__global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  constexpr int A_BYTES = BM * BKE * 2;    // 16 KB
+  constexpr int B_BYTES = BN * BKE * 2;
+  constexpr int STAGE = A_BYTES + B_BYTES;
+  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const ConvGeom& g = P.g;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t n0 = (int64_t)blockIdx.y * BN;
+  const int z = blockIdx.z;
+  int64_t kb_begin = 0, nkb = P.nkb;
+  if (MODE == WGRAD) {
+    kb_begin = (int64_t)z * P.kb_per_split;
+    const int64_t total = (P.gemm_k + BKE - 1) / BKE;
+    nkb = total - kb_begin < P.kb_per_split ? total - kb_begin : P.kb_per_split;
+    if (nkb < 0) nkb = 0;
+  }
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], NPROD); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (tid < NPROD) {
+    // ------------------------------------------------------------ producers
+    for (int64_t it = 0; it < nkb; ++it) {
+      const int s = (int)(it % STAGES);
+      if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)((it / STAGES - 1) & 1));
+      const uint32_t a_base = smem_u32(smem + s * STAGE);
+      const uint32_t b_base = a_base + A_BYTES;
+      const int64_t kb = kb_begin + it;
+      if (MODE == FPROP || MODE == DGRAD) {
+        // K-block kb covers one tap (r,s) and 64 channels (Kch % 64 == 0)
+        const int Kch = MODE == FPROP ? g.C : g.K;       // reduced channels
+        const int64_t kk0 = kb * BKE;
+        const int tap = (int)(kk0 / Kch), c0 = (int)(kk0 % Kch);
+        int r, sx;
+        if (MODE == FPROP) { r = tap / g.S; sx = tap % g.S; }
+        else { r = P.r0 + g.st * (tap / P.ns); sx = P.s0 + g.st * (tap % P.ns); }
+        // A: 128 rows × 8 chunks; thread handles chunk (tid & 7) of rows (tid >> 3) + 16·i
+        const int ch = tid & 7;
+#pragma unroll
+        for (int i = 0; i < BM / 16; ++i) {
+          const int row = (tid >> 3) + 16 * i;
+          const int64_t m = m0 + row;
+          const __nv_bfloat16* src = P.act;
+          bool ok = m < P.M;
+          if (ok) {
+            if (MODE == FPROP) {
+              const int q = (int)(m % g.Q);
+              const int64_t t = m / g.Q;
+              const int p = (int)(t % g.P), n = (int)(t / g.P);
+              const int h = p * g.st - g.pad + r, w = q * g.st - g.pad + sx;
+              ok = h >= 0 && h < g.H && w >= 0 && w < g.W;
+              src = P.act + (((int64_t)n * g.H + h) * g.W + w) * g.C + c0 + ch * 8;
+            } else {
+              const int wq = (int)(m % P.Wp);
+              const int64_t t = m / P.Wp;
+              const int hq = (int)(t % P.Hp), n = (int)(t / P.Hp);
+              const int h = hq * g.st + P.ph, w = wq * g.st + P.pw;
+              const int pn = h + g.pad - r, qn = w + g.pad - sx;   // divisible by st by construction
+              const int p = pn / g.st, q = qn / g.st;
+              ok = pn >= 0 && qn >= 0 && p < g.P && q < g.Q;
+              src = P.act + (((int64_t)n * g.P + p) * g.Q + q) * g.K + c0 + ch * 8;
+            }
+          }
+          cp_async16(a_base + row * 128 + ((ch ^ (row & 7)) << 4), ok ? src : P.act, ok);
+        }
+        // B: BN rows of the bf16 weight copy, K-major
+#pragma unroll
+        for (int i = 0; i < BN / 16; ++i) {
+          const int row = (tid >> 3) + 16 * i;
+          const int64_t nn = n0 + row;
+          const bool ok = nn < P.N;
+          const __nv_bfloat16* src;
+          if (MODE == FPROP) src = P.wgt + nn * ((int64_t)g.R * g.S * g.C) + kk0 + ch * 8;
+          else src = P.wgt + (nn * g.R * g.S + (int64_t)r * g.S + sx) * g.K + c0 + ch * 8;
+          cp_async16(b_base + row * 128 + ((ch ^ (row & 7)) << 4), ok ? src : P.wgt, ok);
+        }
+      } else {
+        // WGRAD, MN-major tiles: K-row kk (an output pixel m) holds 128 (r,s,c) of X for A
+        // and BN output channels of dY for B.  Atom (8 K-rows × 64 MN) = 1 KB;
+        // A: [atom_k 8][atom_mn 2][8][128 B]  (LBO 1 KB, SBO 2 KB)
+        // B: [atom_k 8][atom_mn BN/64][8][128 B] (LBO 1 KB, SBO BN/64 KB)
+        const int64_t mbase = kb * BKE;
+        // A: 64 K-rows × 16 chunks = 1024 chunks, 8 per thread
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int e = tid + NPROD * i;
+          const int kr = e >> 4, j = e & 15;          // K-row, 16B chunk along MN
+          const int64_t mm = mbase + kr;
+          const int64_t rsc = m0 + j * 8;
+          bool ok = mm < P.gemm_k && rsc < P.M;
+          const __nv_bfloat16* src = P.act;
+          if (ok) {
+            const int c = (int)(rsc % g.C);
+            const int64_t rs = rsc / g.C;
+            const int sx = (int)(rs % g.S), r = (int)(rs / g.S);
+            const int q = (int)(mm % g.Q);
+            const int64_t t = mm / g.Q;
+            const int p = (int)(t % g.P), n = (int)(t / g.P);
+            const int h = p * g.st - g.pad + r, w = q * g.st - g.pad + sx;
+            ok = h >= 0 && h < g.H && w >= 0 && w < g.W;
+            src = P.act + (((int64_t)n * g.H + h) * g.W + w) * g.C + c;
+          }
+          const int row = kr & 7;
+          const uint32_t dst = a_base + (kr >> 3) * 2048 + (j >> 3) * 1024 + row * 128 + (((j & 7) ^ row) << 4);
+          cp_async16(dst, ok ? src : P.act, ok);
+        }
+        // B: 64 K-rows × BN/8 chunks
+        constexpr int BCH = BN / 8;
+#pragma unroll
+        for (int i = 0; i < (64 * BCH) / NPROD; ++i) {
+          const int e = tid + NPROD * i;
+          const int kr = e / BCH, j = e % BCH;
+          const int64_t mm = mbase + kr;
+          const int64_t kk = n0 + j * 8;
+          const bool ok = mm < P.gemm_k && kk < P.N;
+          const __nv_bfloat16* src = P.wgt + mm * g.K + kk;
+          const int row = kr & 7;
+          const uint32_t dst = b_base + (kr >> 3) * (BN / 64) * 1024 + (j >> 3) * 1024 + row * 128 +
+                               (((j & 7) ^ row) << 4);
+          cp_async16(dst, ok ? src : P.wgt, ok);
+        }
+      }
+      cp_commit();
+      if (it >= 1) {
+        cp_wait<1>();
+        fence_async_smem();
+        mbar_arrive(&full[(it - 1) % STAGES]);
+      }
+    }
+    if (nkb > 0) {
+      cp_wait<0>();
+      fence_async_smem();
+      mbar_arrive(&full[(nkb - 1) % STAGES]);
+    }
+  } else if (warp == 4) {
+    // ------------------------------------------------------------ MMA issuer (one elected lane)
+    constexpr uint32_t ID = idesc(BN, MODE == WGRAD, MODE == WGRAD);
+    for (int64_t it = 0; it < nkb; ++it) {
+      const int s = (int)(it % STAGES);
+      mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (lane == 0) {
+        const uint32_t a_base = smem_u32(smem + s * STAGE);
+        const uint32_t b_base = a_base + A_BYTES;
+#pragma unroll
+        for (int k = 0; k < BKE / 16; ++k) {
+          uint64_t da, db;
+          if (MODE == WGRAD) {
+            da = sdesc(a_base + k * 2 * 2048, 1024, 2048);
+            db = sdesc(b_base + k * 2 * (BN / 64) * 1024, 1024, (BN / 64) * 1024);
+          } else {
+            da = sdesc(a_base + k * 32, 16, 1024);
+            db = sdesc(b_base + k * 32, 16, 1024);
+          }
+          mma_bf16(tmem, da, db, ID, (it > 0 || k > 0) ? 1u : 0u);
+        }
+        mma_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+    if (nkb > 0 && lane == 0) mma_commit(tfull);
+    __syncwarp();
+  }
+
+  // ------------------------------------------------------------ epilogue (warps 0-3)
+  if (tid < NPROD) {
+    const int row = warp * 32 + lane;
+    const int64_t m = m0 + row;
+    if (nkb > 0) {
+      mbar_wait(tfull, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+#pragma unroll
+    for (int j0 = 0; j0 < BN; j0 += 32) {
+      uint32_t v[32];
+      if (nkb > 0) {
+        TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + j0, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0u;
+      }
+      if (m >= P.M) continue;
+      if (MODE == WGRAD) {
+        float* o = (float*)P.out + ((int64_t)z * P.M + m) * P.N + n0 + j0;
+        if (n0 + j0 + 32 <= P.N) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(o + i) = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                                            __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+        } else {
+          for (int i = 0; i < 32 && n0 + j0 + i < P.N; ++i) o[i] = __uint_as_float(v[i]);
+        }
+      } else {
+        int64_t orow;
+        if (MODE == FPROP) {
+          orow = m;
+        } else {
+          const int wq = (int)(m % P.Wp);
+          const int64_t t = m / P.Wp;
+          const int hq = (int)(t % P.Hp), n = (int)(t / P.Hp);
+          orow = ((int64_t)n * g.H + hq * g.st + P.ph) * g.W + wq * g.st + P.pw;
+        }
+        __nv_bfloat16* o = (__nv_bfloat16*)P.out + orow * P.N + n0 + j0;
+        if (n0 + j0 + 32 <= P.N) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            float f[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) f[u] = __uint_as_float(v[i + u]);
+            if (P.accumulate) {
+              uint4 old = *reinterpret_cast<const uint4*>(o + i);
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&old);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                float2 ff = __bfloat1622float2(h2[u]);
+                f[2 * u] += ff.x;
+                f[2 * u + 1] += ff.y;
+              }
+            }
+            uint4 pk;
+            __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) p2[u] = __floats2bfloat162_rn(f[2 * u], f[2 * u + 1]);
+            *reinterpret_cast<uint4*>(o + i) = pk;
+          }
+        } else {
+          for (int i = 0; i < 32 && n0 + j0 + i < P.N; ++i) {
+            float f = __uint_as_float(v[i]);
+            if (P.accumulate) f += __bfloat162float(o[i]);
+            o[i] = __float2bfloat16_rn(f);
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)BN));
+  }
+}
+
+// fp32 KRSC master -> bf16 [K][RSC] (fprop) or [C][R][S][K] (dgrad)
+__global__ void weight_bf16(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int K, int RS, int C,
+                            int transpose) {
+  const int64_t n = (int64_t)K * RS * C;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    const int64_t t = i / C;
+    const int rs = (int)(t % RS), k = (int)(t / RS);
+    const int64_t o = transpose ? ((int64_t)c * RS + rs) * K + k : i;
+    out[o] = __float2bfloat16_rn(w[i]);
+  }
+}
+
+__global__ void wgrad_reduce(int splits, int64_t RSC, int K, const float* __restrict__ part, float* __restrict__ dw) {
+  const int64_t n = RSC * K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % K);
+    const int64_t rsc = i / K;
+    float s = 0.f;
+    for (int zz = 0; zz < splits; ++zz) s += part[(int64_t)zz * n + i];
+    dw[(int64_t)k * RSC + rsc] = s;
+  }
+}
+
+template <int MODE, int BN>
+Status launch(OpArgs& a, const Params& P, dim3 grid) {
+  constexpr int smem = STAGES * (BM * BKE * 2 + BN * BKE * 2) + 1024 + 256;
+  auto kern = conv_tc_kernel<MODE, BN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  kern<<<grid, NTHREADS, smem, a.stream>>>(P);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+
+int wgrad_splits(const ConvGeom& g, int BN) {
+  const int64_t tiles = ((int64_t)g.R * g.S * g.C + BM - 1) / BM * ((g.K + BN - 1) / BN);
+  const int64_t kbs = ((int64_t)g.N * g.P * g.Q + BKE - 1) / BKE;
+  int64_t s = (2 * 148 + tiles - 1) / tiles;
+  if (s > kbs) s = kbs;
+  if (s > 128) s = 128;
+  return (int)(s < 1 ? 1 : s);
+}
+
+}  // namespace tc
+
+using namespace tc;
+
+bool conv_tc_ok(const ConvGeom& g, int mode) {
+  if (mode == FPROP) return g.C % 64 == 0 && g.K % 64 == 0;
+  if (mode == DGRAD) return g.K % 64 == 0 && g.C % 64 == 0 && (g.st == 1 || g.st == 2);
+  return g.C % 8 == 0 && g.K % 64 == 0;
+}
+
+size_t conv_tc_ws(const ConvGeom& g, int mode) {
+  size_t wbytes = (size_t)g.K * g.R * g.S * g.C * 2;
+  if (mode == WGRAD) {
+    const int BN = g.K % 128 == 0 ? 128 : 64;
+    return (size_t)wgrad_splits(g, BN) * g.R * g.S * g.C * g.K * 4;
+  }
+  return (wbytes + 255) / 256 * 256;
+}
+
+Status conv_fprop_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y) {
+  __nv_bfloat16* wb = (__nv_bfloat16*)a.ws;
+  const int64_t nw = (int64_t)g.K * g.R * g.S * g.C;
+  weight_bf16<<<grid_for(nw, 256, 4), 256, 0, a.stream>>>(w, wb, g.K, g.R * g.S, g.C, 0);
+  OC_LAUNCH_CHECK(a);
+  Params P{};
+  P.g = g;
+  P.act = x;
+  P.wgt = wb;
+  P.out = y;
+  P.M = (int64_t)g.N * g.P * g.Q;
+  P.N = g.K;
+  P.nkb = (int64_t)g.R * g.S * g.C / BKE;
+  if (g.K % 128 == 0) return launch<FPROP, 128>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.K / 128, 1));
+  return launch<FPROP, 64>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.K / 64, 1));
+}
+
+Status conv_dgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const float* w, __nv_bfloat16* dx,
+                     bool accumulate) {
+  __nv_bfloat16* wt = (__nv_bfloat16*)a.ws;
+  const int64_t nw = (int64_t)g.K * g.R * g.S * g.C;
+  weight_bf16<<<grid_for(nw, 256, 4), 256, 0, a.stream>>>(w, wt, g.K, g.R * g.S, g.C, 1);
+  OC_LAUNCH_CHECK(a);
+  for (int ph = 0; ph < g.st; ++ph)
+    for (int pw = 0; pw < g.st; ++pw) {
+      Params P{};
+      P.g = g;
+      P.act = dy;
+      P.wgt = wt;
+      P.out = dx;
+      P.accumulate = accumulate ? 1 : 0;
+      P.ph = ph;
+      P.pw = pw;
+      P.Hp = (g.H - ph + g.st - 1) / g.st;
+      P.Wp = (g.W - pw + g.st - 1) / g.st;
+      // taps with (h + pad − r) divisible by st for h ≡ ph (mod st)
+      P.r0 = ((ph + g.pad) % g.st + g.st) % g.st;
+      P.s0 = ((pw + g.pad) % g.st + g.st) % g.st;
+      P.nr = P.r0 < g.R ? (g.R - P.r0 + g.st - 1) / g.st : 0;
+      P.ns = P.s0 < g.S ? (g.S - P.s0 + g.st - 1) / g.st : 0;
+      P.M = (int64_t)g.N * P.Hp * P.Wp;
+      P.N = g.C;
+      P.nkb = (int64_t)P.nr * P.ns * g.K / BKE;
+      if (P.M == 0) continue;
+      if (P.nkb == 0 && accumulate) continue;  // no taps reach this phase: G stays as is
+      Status st = g.C % 128 == 0 ? launch<DGRAD, 128>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.C / 128, 1))
+                                 : launch<DGRAD, 64>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.C / 64, 1));
+      if (!st.good()) return st;
+    }
+  return Status::ok();
+}
+
+Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* x, float* dw) {
+  const int BN = g.K % 128 == 0 ? 128 : 64;
+  const int splits = wgrad_splits(g, BN);
+  Params P{};
+  P.g = g;
+  P.act = x;
+  P.wgt = dy;
+  P.out = a.ws;
+  P.M = (int64_t)g.R * g.S * g.C;
+  P.N = g.K;
+  P.gemm_k = (int64_t)g.N * g.P * g.Q;
+  const int64_t kbs = (P.gemm_k + BKE - 1) / BKE;
+  P.kb_per_split = (kbs + splits - 1) / splits;
+  P.nkb = P.kb_per_split;
+  dim3 grid((unsigned)((P.M + BM - 1) / BM), g.K / BN, splits);
+  Status st = BN == 128 ? launch<WGRAD, 128>(a, P, grid) : launch<WGRAD, 64>(a, P, grid);
+  if (!st.good()) return st;
+  wgrad_reduce<<<grid_for(P.M * g.K, 256, 4), 256, 0, a.stream>>>(splits, P.M, g.K, (const float*)a.ws, dw);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+
+}  // namespace oc

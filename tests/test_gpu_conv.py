@@ -1,0 +1,117 @@
+"""Kernel-level parity of the convolution ops (tcgen05 implicit GEMM and the
+CUDA-core fallback) with the oracle's direct-definition convolution, through
+the C-ABI executor on one-function graphs: several tiles, ragged M tails,
+stride 1 and 2, 1×1 and 3×3 filters, 64- and 128-wide N tiles, dgrad
+accumulation and the deterministic split-K wgrad."""
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import numerics as nm
+
+SHAPES = [  # N, H, W, C, K, R, stride, pad
+    (2, 9, 7, 64, 64, 3, 1, 1),
+    (3, 11, 10, 64, 128, 3, 2, 1),
+    (2, 12, 9, 64, 128, 1, 2, 0),
+    (1, 8, 8, 128, 128, 3, 1, 1),
+    (2, 7, 7, 128, 64, 3, 1, 1),
+    (2, 15, 13, 3, 64, 7, 2, 3),      # stem: CUDA-core path
+]
+
+
+def bf(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16)
+
+
+def _graph(kind, g, accumulate=False):
+    N, H, W, C, K, R, st, pad = g
+    P = (H + 2 * pad - R) // st + 1
+    Q = (W + 2 * pad - R) // st + 1
+    attrs = {"N": N, "H": H, "W": W, "C": C, "K": K, "R": R, "S": R, "stride": st, "pad": pad, "P": P, "Q": Q,
+             "accumulate": accumulate}
+    v = lambda n, b: {"id": n, "bytes": int(b), "pinned": True}
+    xs, ys, ws = N * H * W * C * 2, N * P * Q * K * 2, K * R * R * C * 4
+    if kind == "conv_fwd":
+        vars_ = [v("x", xs), v("w", ws), v("y", ys)]
+        fn = {"id": "f", "in": ["x", "w"], "out": ["y"], "op": {"kind": kind, "args": {"x": "x", "w": "w", "y": "y"},
+                                                             "attrs": attrs}}
+    elif kind == "conv_dgrad":
+        vars_ = [v("dy", ys), v("w", ws), v("dx", xs)]
+        fn = {"id": "f", "in": ["dy", "w"] + (["dx"] if accumulate else []), "out": ["dx"],
+              "op": {"kind": kind, "args": {"dy": "dy", "w": "w", "dx": "dx"}, "attrs": attrs}}
+    else:
+        vars_ = [v("dy", ys), v("x", xs), v("dw", ws)]
+        fn = {"id": "f", "in": ["dy", "x"], "out": ["dw"], "op": {"kind": kind, "args": {"dy": "dy", "x": "x", "dw": "dw"},
+                                                               "attrs": attrs}}
+    doc = json.dumps({"variables": vars_, "functions": [fn]})
+    return doc, (P, Q), sum(x["bytes"] for x in vars_)
+
+
+def _run(doc, total, inputs, out_name, out_dtype):
+    from paper_2010_14109_b200.runtime import OutOfCoreStep
+    st = OutOfCoreStep(doc, total, 0, mode="best", phys_bytes=4096)
+    for k, a in inputs.items():
+        st.write(k, a)
+    st.step()
+    r = st.read(out_name, out_dtype)
+    st.close()
+    return r
+
+
+def _bits(t):
+    return t.view(torch.int16).numpy()
+
+
+def _from_bits(a, shape):
+    return torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).float().numpy().reshape(shape).astype(np.float64)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("g", SHAPES)
+def test_conv_fwd(g):
+    N, H, W, C, K, R, st, pad = g
+    rng = np.random.default_rng(1)
+    x = bf(rng.standard_normal((N, H, W, C)))
+    w = rng.standard_normal((K, R, R, C)).astype(np.float32) * 0.1
+    doc, (P, Q), total = _graph("conv_fwd", g)
+    y = _run(doc, total, {"x": _bits(x), "w": w}, "y", np.uint16)
+    y = _from_bits(y, (N, P, Q, K))
+    ref = nm.round_bf16(nm.conv2d(x.float().numpy().astype(np.float64), nm.round_bf16(w.astype(np.float64)), st, pad))
+    assert nm.rel_l2(y, ref) < 2e-3
+    assert np.max(np.abs(y - ref)) <= 2 ** -7 * np.max(np.abs(ref)) + 1e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("g", SHAPES[:5])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_conv_dgrad(g, accumulate):
+    N, H, W, C, K, R, st, pad = g
+    rng = np.random.default_rng(2)
+    doc, (P, Q), total = _graph("conv_dgrad", g, accumulate)
+    dy = bf(rng.standard_normal((N, P, Q, K)))
+    w = rng.standard_normal((K, R, R, C)).astype(np.float32) * 0.1
+    old = bf(rng.standard_normal((N, H, W, C))) if accumulate else bf(np.zeros((N, H, W, C)))
+    dx = _run(doc, total, {"dy": _bits(dy), "w": w, "dx": _bits(old)}, "dx", np.uint16)
+    dx = _from_bits(dx, (N, H, W, C))
+    x0 = np.zeros((N, H, W, C))
+    ref, _ = nm.conv2d_backward(x0, nm.round_bf16(w.astype(np.float64)), dy.float().numpy().astype(np.float64), st, pad)
+    if accumulate:
+        ref = ref + old.float().numpy()
+    ref = nm.round_bf16(ref)
+    assert nm.rel_l2(dx, ref) < 2e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("g", SHAPES)
+def test_conv_wgrad(g):
+    N, H, W, C, K, R, st, pad = g
+    rng = np.random.default_rng(3)
+    doc, (P, Q), total = _graph("conv_wgrad", g)
+    dy = bf(rng.standard_normal((N, P, Q, K)))
+    x = bf(rng.standard_normal((N, H, W, C)))
+    dw = _run(doc, total, {"dy": _bits(dy), "x": _bits(x)}, "dw", np.float32).reshape(K, R, R, C)
+    _, ref = nm.conv2d_backward(x.float().numpy().astype(np.float64), np.zeros((K, R, R, C)),
+                                dy.float().numpy().astype(np.float64), st, pad)
+    assert nm.rel_l2(dw, ref) < 1e-5
