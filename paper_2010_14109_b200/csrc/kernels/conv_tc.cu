@@ -109,9 +109,10 @@ struct Params {
   // dgrad phase
   int ph, pw, Hp, Wp;          // output sub-grid of this phase: h = h'·st + ph
   int r0, s0, nr, ns;          // valid taps: r = r0 + st·i (i < nr), s = s0 + st·j (j < ns)
+  int64_t kpad;                // fprop with register gather: padded RSC (row pitch of W_bf16)
 };
 
-template <int MODE, int BN>
+template <int MODE, int BN, bool REG>
 __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -159,7 +160,108 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
       const uint32_t a_base = smem_u32(smem + s * STAGE);
       const uint32_t b_base = a_base + A_BYTES;
       const int64_t kb = kb_begin + it;
-      if (MODE == FPROP || MODE == DGRAD) {
+      if (REG && MODE == FPROP) {
+        // narrow-channel stem: K = (r,s,c) padded to kpad, gathered element by
+        // element into registers and stored as 16-byte swizzled chunks
+        const int ch = tid & 7;
+        const int RSC = g.R * g.S * g.C;
+        int er[8], es[8], ec[8];
+        bool ev[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int kk = (int)(kb * BKE) + ch * 8 + e;
+          ev[e] = kk < RSC;
+          ec[e] = kk % g.C;
+          const int rs = kk / g.C;
+          es[e] = rs % g.S;
+          er[e] = rs / g.S;
+        }
+#pragma unroll 2
+        for (int i = 0; i < BM / 16; ++i) {
+          const int row = (tid >> 3) + 16 * i;
+          const int64_t m = m0 + row;
+          uint32_t packed[4] = {0u, 0u, 0u, 0u};
+          if (m < P.M) {
+            const int q = (int)(m % g.Q);
+            const int64_t t = m / g.Q;
+            const int p = (int)(t % g.P), n = (int)(t / g.P);
+            const int h0 = p * g.st - g.pad, w0 = q * g.st - g.pad;
+            const unsigned short* xs = reinterpret_cast<const unsigned short*>(P.act) + (int64_t)n * g.H * g.W * g.C;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int h = h0 + er[e], w = w0 + es[e];
+              unsigned short v = 0;
+              if (ev[e] && h >= 0 && h < g.H && w >= 0 && w < g.W) v = __ldg(xs + ((int64_t)h * g.W + w) * g.C + ec[e]);
+              packed[e >> 1] |= (uint32_t)v << (16 * (e & 1));
+            }
+          }
+          const uint32_t dst = a_base + row * 128 + ((ch ^ (row & 7)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(packed[0]), "r"(packed[1]),
+                       "r"(packed[2]), "r"(packed[3])
+                       : "memory");
+        }
+#pragma unroll
+        for (int i = 0; i < BN / 16; ++i) {
+          const int row = (tid >> 3) + 16 * i;
+          const int64_t nn = n0 + row;
+          const bool ok = nn < P.N;
+          const __nv_bfloat16* src = P.wgt + nn * P.kpad + kb * BKE + ch * 8;
+          cp_async16(b_base + row * 128 + ((ch ^ (row & 7)) << 4), ok ? src : P.wgt, ok);
+        }
+      } else if (REG && MODE == WGRAD) {
+        const int64_t mbase = kb * BKE;
+        const int j = tid & 15;                     // fixed MN chunk: rows rsc = m0 + 8j .. +7
+        int er[8], es[8], ec[8];
+        bool ev[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int64_t rsc = m0 + j * 8 + e;
+          ev[e] = rsc < P.M;
+          ec[e] = (int)(rsc % g.C);
+          const int rs = (int)(rsc / g.C);
+          es[e] = rs % g.S;
+          er[e] = rs / g.S;
+        }
+#pragma unroll 2
+        for (int i = 0; i < 8; ++i) {
+          const int kr = (tid >> 4) + 8 * i;
+          const int64_t mm = mbase + kr;
+          uint32_t packed[4] = {0u, 0u, 0u, 0u};
+          if (mm < P.gemm_k) {
+            const int q = (int)(mm % g.Q);
+            const int64_t t = mm / g.Q;
+            const int p = (int)(t % g.P), n = (int)(t / g.P);
+            const int h0 = p * g.st - g.pad, w0 = q * g.st - g.pad;
+            const unsigned short* xs = reinterpret_cast<const unsigned short*>(P.act) + (int64_t)n * g.H * g.W * g.C;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int h = h0 + er[e], w = w0 + es[e];
+              unsigned short v = 0;
+              if (ev[e] && h >= 0 && h < g.H && w >= 0 && w < g.W) v = __ldg(xs + ((int64_t)h * g.W + w) * g.C + ec[e]);
+              packed[e >> 1] |= (uint32_t)v << (16 * (e & 1));
+            }
+          }
+          const int row = kr & 7;
+          const uint32_t dst = a_base + (kr >> 3) * 2048 + (j >> 3) * 1024 + row * 128 + (((j & 7) ^ row) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(packed[0]), "r"(packed[1]),
+                       "r"(packed[2]), "r"(packed[3])
+                       : "memory");
+        }
+        constexpr int BCH = BN / 8;
+#pragma unroll
+        for (int i = 0; i < (64 * BCH) / NPROD; ++i) {
+          const int e = tid + NPROD * i;
+          const int kr = e / BCH, jj = e % BCH;
+          const int64_t mm = mbase + kr;
+          const int64_t kk = n0 + jj * 8;
+          const bool ok = mm < P.gemm_k && kk < P.N;
+          const __nv_bfloat16* src = P.wgt + mm * g.K + kk;
+          const int row = kr & 7;
+          const uint32_t dst = b_base + (kr >> 3) * (BN / 64) * 1024 + (jj >> 3) * 1024 + row * 128 +
+                               (((jj & 7) ^ row) << 4);
+          cp_async16(dst, ok ? src : P.wgt, ok);
+        }
+      } else if (MODE == FPROP || MODE == DGRAD) {
         // K-block kb covers one tap (r,s) and 64 channels (Kch % 64 == 0)
         const int Kch = MODE == FPROP ? g.C : g.K;       // reduced channels
         const int64_t kk0 = kb * BKE;
@@ -375,16 +477,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
   }
 }
 
-// fp32 KRSC master -> bf16 [K][RSC] (fprop) or [C][R][S][K] (dgrad)
+// fp32 KRSC master -> bf16 [K][kpad] (fprop; zero padding past RSC) or [C][R][S][K] (dgrad)
 __global__ void weight_bf16(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int K, int RS, int C,
-                            int transpose) {
-  const int64_t n = (int64_t)K * RS * C;
+                            int transpose, int64_t kpad) {
+  const int64_t n = transpose ? (int64_t)K * RS * C : (int64_t)K * kpad;
+  const int64_t rsc = (int64_t)RS * C;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % C);
-    const int64_t t = i / C;
-    const int rs = (int)(t % RS), k = (int)(t / RS);
-    const int64_t o = transpose ? ((int64_t)c * RS + rs) * K + k : i;
-    out[o] = __float2bfloat16_rn(w[i]);
+    if (transpose) {
+      const int c = (int)(i % C);
+      const int64_t t = i / C;
+      const int rs = (int)(t % RS), k = (int)(t / RS);
+      out[((int64_t)c * RS + rs) * K + k] = __float2bfloat16_rn(w[i]);
+    } else {
+      const int64_t k = i / kpad, j = i % kpad;
+      out[i] = j < rsc ? __float2bfloat16_rn(w[k * rsc + j]) : __float2bfloat16_rn(0.f);
+    }
   }
 }
 
@@ -399,10 +506,10 @@ __global__ void wgrad_reduce(int splits, int64_t RSC, int K, const float* __rest
   }
 }
 
-template <int MODE, int BN>
+template <int MODE, int BN, bool REG = false>
 Status launch(OpArgs& a, const Params& P, dim3 grid) {
   constexpr int smem = STAGES * (BM * BKE * 2 + BN * BKE * 2) + 1024 + 256;
-  auto kern = conv_tc_kernel<MODE, BN>;
+  auto kern = conv_tc_kernel<MODE, BN, REG>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -427,13 +534,15 @@ int wgrad_splits(const ConvGeom& g, int BN) {
 using namespace tc;
 
 bool conv_tc_ok(const ConvGeom& g, int mode) {
-  if (mode == FPROP) return g.C % 64 == 0 && g.K % 64 == 0;
+  if (mode == FPROP) return g.K % 64 == 0 && (g.C % 64 == 0 || g.C < 64);
   if (mode == DGRAD) return g.K % 64 == 0 && g.C % 64 == 0 && (g.st == 1 || g.st == 2);
-  return g.C % 8 == 0 && g.K % 64 == 0;
+  return g.K % 64 == 0;
 }
 
+static int64_t kpad_of(const ConvGeom& g) { return ((int64_t)g.R * g.S * g.C + BKE - 1) / BKE * BKE; }
+
 size_t conv_tc_ws(const ConvGeom& g, int mode) {
-  size_t wbytes = (size_t)g.K * g.R * g.S * g.C * 2;
+  size_t wbytes = (size_t)g.K * kpad_of(g) * 2;
   if (mode == WGRAD) {
     const int BN = g.K % 128 == 0 ? 128 : 64;
     return (size_t)wgrad_splits(g, BN) * g.R * g.S * g.C * g.K * 4;
@@ -443,8 +552,9 @@ size_t conv_tc_ws(const ConvGeom& g, int mode) {
 
 Status conv_fprop_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y) {
   __nv_bfloat16* wb = (__nv_bfloat16*)a.ws;
-  const int64_t nw = (int64_t)g.K * g.R * g.S * g.C;
-  weight_bf16<<<grid_for(nw, 256, 4), 256, 0, a.stream>>>(w, wb, g.K, g.R * g.S, g.C, 0);
+  const bool reg = g.C % 64 != 0;
+  const int64_t kpad = kpad_of(g);
+  weight_bf16<<<grid_for(g.K * kpad, 256, 4), 256, 0, a.stream>>>(w, wb, g.K, g.R * g.S, g.C, 0, kpad);
   OC_LAUNCH_CHECK(a);
   Params P{};
   P.g = g;
@@ -453,7 +563,12 @@ Status conv_fprop_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const
   P.out = y;
   P.M = (int64_t)g.N * g.P * g.Q;
   P.N = g.K;
-  P.nkb = (int64_t)g.R * g.S * g.C / BKE;
+  P.kpad = kpad;
+  P.nkb = kpad / BKE;
+  if (reg) {
+    if (g.K % 128 == 0) return launch<FPROP, 128, true>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.K / 128, 1));
+    return launch<FPROP, 64, true>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.K / 64, 1));
+  }
   if (g.K % 128 == 0) return launch<FPROP, 128>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.K / 128, 1));
   return launch<FPROP, 64>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.K / 64, 1));
 }
@@ -462,7 +577,7 @@ Status conv_dgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, cons
                      bool accumulate) {
   __nv_bfloat16* wt = (__nv_bfloat16*)a.ws;
   const int64_t nw = (int64_t)g.K * g.R * g.S * g.C;
-  weight_bf16<<<grid_for(nw, 256, 4), 256, 0, a.stream>>>(w, wt, g.K, g.R * g.S, g.C, 1);
+  weight_bf16<<<grid_for(nw, 256, 4), 256, 0, a.stream>>>(w, wt, g.K, g.R * g.S, g.C, 1, 0);
   OC_LAUNCH_CHECK(a);
   for (int ph = 0; ph < g.st; ++ph)
     for (int pw = 0; pw < g.st; ++pw) {
@@ -508,7 +623,9 @@ Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, cons
   P.kb_per_split = (kbs + splits - 1) / splits;
   P.nkb = P.kb_per_split;
   dim3 grid((unsigned)((P.M + BM - 1) / BM), g.K / BN, splits);
-  Status st = BN == 128 ? launch<WGRAD, 128>(a, P, grid) : launch<WGRAD, 64>(a, P, grid);
+  Status st;
+  if (g.C % 8 != 0) st = BN == 128 ? launch<WGRAD, 128, true>(a, P, grid) : launch<WGRAD, 64, true>(a, P, grid);
+  else st = BN == 128 ? launch<WGRAD, 128>(a, P, grid) : launch<WGRAD, 64>(a, P, grid);
   if (!st.good()) return st;
   wgrad_reduce<<<grid_for(P.M * g.K, 256, 4), 256, 0, a.stream>>>(splits, P.M, g.K, (const float*)a.ws, dw);
   OC_LAUNCH_CHECK(a);

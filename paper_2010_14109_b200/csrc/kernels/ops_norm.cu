@@ -80,14 +80,26 @@ __global__ void __launch_bounds__(256) stats_partial(int64_t rows, int C, const 
 }
 
 // stat[0][c] = μ, stat[1][c] = rstd  (fixed-order double sum over chunks)
-__global__ void stats_finalize(int nblk, int64_t rows, int C, const float* __restrict__ part, float* __restrict__ stat) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  double s = 0, q = 0;
-  for (int b = 0; b < nblk; ++b) {
+// one warp per channel: lane-strided partial sums, then a fixed xor tree
+__device__ __forceinline__ void chunk_sums(int nblk, int C, int c, const float* __restrict__ part, double& s,
+                                           double& q) {
+  const int lane = threadIdx.x & 31;
+  s = 0;
+  q = 0;
+  for (int b = lane; b < nblk; b += 32) {
     s += part[(int64_t)b * 2 * C + c];
     q += part[(int64_t)b * 2 * C + C + c];
   }
+  s = warp_sum(s);
+  q = warp_sum(q);
+}
+
+__global__ void stats_finalize(int nblk, int64_t rows, int C, const float* __restrict__ part, float* __restrict__ stat) {
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= C) return;
+  double s, q;
+  chunk_sums(nblk, C, c, part, s, q);
+  if ((threadIdx.x & 31) != 0) return;
   double mu = s / rows;
   double var = q / rows - mu * mu;
   if (var < 0) var = 0;
@@ -101,7 +113,7 @@ Status batch_stats(OpArgs& a, int64_t rows, int C, const __nv_bfloat16* y, float
   if (a.ws_bytes < (size_t)nblk * 2 * C * 4) return Status::make(OC_E_INVARIANT, "bn: workspace too small");
   stats_partial<<<nblk, 256, 256 * 16 * 4, a.stream>>>(rows, C, y, (float*)a.ws);
   OC_LAUNCH_CHECK(a);
-  stats_finalize<<<(C + 127) / 128, 128, 0, a.stream>>>(nblk, rows, C, (const float*)a.ws, stat);
+  stats_finalize<<<(C + 7) / 8, 256, 0, a.stream>>>(nblk, rows, C, (const float*)a.ws, stat);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
@@ -193,13 +205,11 @@ __global__ void __launch_bounds__(256) bnb_partial(int64_t rows, int C, const __
 // dβ = Σdz, dγ = Σdz·x̂
 __global__ void bnb_finalize(int nblk, int C, const float* __restrict__ part, float* __restrict__ dgamma,
                              float* __restrict__ dbeta) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= C) return;
-  double s = 0, q = 0;
-  for (int b = 0; b < nblk; ++b) {
-    s += part[(int64_t)b * 2 * C + c];
-    q += part[(int64_t)b * 2 * C + C + c];
-  }
+  double s, q;
+  chunk_sums(nblk, C, c, part, s, q);
+  if ((threadIdx.x & 31) != 0) return;
   dbeta[c] = (float)s;
   dgamma[c] = (float)q;
 }
@@ -215,7 +225,7 @@ Status bn_bwd_reduce(OpArgs& a) {
                                                      (const __nv_bfloat16*)a.p(BB_Y), (const float*)a.p(BB_STAT),
                                                      Ab(a, "relu") ? 1 : 0, (float*)a.ws);
   OC_LAUNCH_CHECK(a);
-  bnb_finalize<<<(C + 127) / 128, 128, 0, a.stream>>>(nblk, C, (const float*)a.ws, (float*)a.p(BB_DGAMMA),
+  bnb_finalize<<<(C + 7) / 8, 256, 0, a.stream>>>(nblk, C, (const float*)a.ws, (float*)a.p(BB_DGAMMA),
                                                       (float*)a.p(BB_DBETA));
   OC_LAUNCH_CHECK(a);
   return Status::ok();
@@ -444,7 +454,7 @@ Status pool_bn_bwd_reduce(OpArgs& a) {
                                                      (const float*)a.p(PB_GAMMA), (const float*)a.p(PB_BETA),
                                                      (float*)a.ws);
   OC_LAUNCH_CHECK(a);
-  bnb_finalize<<<(g.C + 127) / 128, 128, 0, a.stream>>>(nblk, g.C, (const float*)a.ws, (float*)a.p(PB_DGAMMA),
+  bnb_finalize<<<(g.C + 7) / 8, 256, 0, a.stream>>>(nblk, g.C, (const float*)a.ws, (float*)a.p(PB_DGAMMA),
                                                         (float*)a.p(PB_DBETA));
   OC_LAUNCH_CHECK(a);
   return Status::ok();
