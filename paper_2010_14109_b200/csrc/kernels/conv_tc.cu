@@ -13,12 +13,15 @@
 //   wgrad  D[(r,s,c)][k]          = Σ_{m=(n,p,q)} X[n,p·st−pad+r,q·st−pad+s,c] · dY[m,k]
 //          both operands MN-major (contiguous along channels), deterministic
 //          split-K over m (fixed slices, fixed-order sum), then dW[k][(r,s,c)]
+//   narrow-channel stem (C=3): A is gathered element by element into
+//          registers and stored as swizzled 16-byte chunks (REG variants).
 //
 // Tile: UMMA M = 128, N = BN (64 or 128), K-block 64 (one 128-byte swizzle
-// row of bf16).  CTA: warps 0-3 gather (cp.async, zero-fill for padding) and
-// run the epilogue, warp 4 lane 0 issues the MMAs.  3 stages of
-// 16 KB + BN·128 B, so two CTAs share an SM and one's epilogue overlaps the
-// other's main loop.
+// row of bf16).  CTA: warps 0-3 gather and run the epilogue, warp 4 issues
+// the MMAs from one lane.  3 stages of 16 KB + BN·128 B, so two CTAs share an
+// SM and one's epilogue overlaps the other's main loop.  Address arithmetic
+// in the producers is hoisted out of the K loop (rows fixed per thread) and
+// what remains uses 32-bit multiply-shift division (FastDiv).
 #include "conv.cuh"
 
 namespace oc {
@@ -26,6 +29,21 @@ namespace oc {
 namespace tc {
 
 constexpr int BM = 128, BKE = 64, STAGES = 3, NPROD = 128, NTHREADS = 160;
+
+// n / d for 0 <= n < 2^31 by multiply-high and shift (Granlund–Montgomery)
+struct FastDiv {
+  uint32_t d, m, s;
+  void init(uint32_t div) {
+    d = div;
+    if (div <= 1) { m = 0; s = 0; return; }
+    s = 0;
+    while ((1ull << s) < div) ++s;
+    m = (uint32_t)(((1ull << 32) * ((1ull << s) - div)) / div + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return (uint32_t)(((uint64_t)__umulhi(n, m) + n) >> s);
+  }
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -56,6 +74,10 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void st_shared16(uint32_t dst, const uint32_t (&v)[4]) {
+  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+               : "memory");
+}
 
 // shared-memory matrix descriptor, SWIZZLE_128B (PTX ISA tcgen05 "matrix descriptor")
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -99,17 +121,18 @@ enum Mode { FPROP = 0, DGRAD = 1, WGRAD = 2 };
 struct Params {
   ConvGeom g;
   const __nv_bfloat16* act;    // fprop: X; dgrad: dY; wgrad: X
-  const __nv_bfloat16* wgt;    // fprop: W_bf16 [K][RSC]; dgrad: Wt_bf16 [C][RS][K]; wgrad: dY
+  const __nv_bfloat16* wgt;    // fprop: W_bf16 [K][kpad]; dgrad: Wt_bf16 [C][RS][K]; wgrad: dY
   void* out;                   // fprop/dgrad: bf16 NHWC; wgrad: fp32 partials [z][RSC][K]
   int accumulate;              // dgrad: out = rnd(acc + out)
-  int64_t M, N;                // GEMM sizes
-  int64_t nkb;                 // K-blocks (per split for wgrad)
-  int64_t kb_per_split;        // wgrad
-  int64_t gemm_k;              // wgrad: N·P·Q
-  // dgrad phase
-  int ph, pw, Hp, Wp;          // output sub-grid of this phase: h = h'·st + ph
-  int r0, s0, nr, ns;          // valid taps: r = r0 + st·i (i < nr), s = s0 + st·j (j < ns)
-  int64_t kpad;                // fprop with register gather: padded RSC (row pitch of W_bf16)
+  int M, N;                    // GEMM sizes (M < 2^31)
+  int nkb;                     // K-blocks (per split for wgrad)
+  int kb_per_split;            // wgrad
+  int gemm_k;                  // wgrad: N·P·Q
+  int ph, pw, Hp, Wp;          // dgrad phase: output sub-grid h = h'·st + ph
+  int r0, s0, nr, ns;          // dgrad taps: r = r0 + st·i (i < nr), s = s0 + st·j (j < ns)
+  int kpad;                    // fprop: padded RSC (row pitch of W_bf16)
+  int kch;                     // fprop: C; dgrad: K (channels reduced per tap)
+  FastDiv fQ, fP, fWp, fHp, fC, fS, fKch, fns;
 };
 
 template <int MODE, int BN, bool REG>
@@ -126,13 +149,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const ConvGeom& g = P.g;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int64_t n0 = (int64_t)blockIdx.y * BN;
+  const int m0 = blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
   const int z = blockIdx.z;
-  int64_t kb_begin = 0, nkb = P.nkb;
+  int kb_begin = 0, nkb = P.nkb;
   if (MODE == WGRAD) {
-    kb_begin = (int64_t)z * P.kb_per_split;
-    const int64_t total = (P.gemm_k + BKE - 1) / BKE;
+    kb_begin = z * P.kb_per_split;
+    const int total = (P.gemm_k + BKE - 1) / BKE;
     nkb = total - kb_begin < P.kb_per_split ? total - kb_begin : P.kb_per_split;
     if (nkb < 0) nkb = 0;
   }
@@ -154,204 +177,195 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
 
   if (tid < NPROD) {
     // ------------------------------------------------------------ producers
-    for (int64_t it = 0; it < nkb; ++it) {
-      const int s = (int)(it % STAGES);
+    const int ch = tid & 7;
+    // per-thread row state, fixed for the whole tile
+    int rh[8], rw[8];            // fprop: h0, w0 of the output pixel; dgrad: pbase, qbase
+    int64_t rbase[8];            // element offset of the row's (n, h0, w0) / (n, pbase, qbase)
+    bool rok[8];
+    int er[8], es[8], ec[8];     // REG / WGRAD: fixed (r,s,c) of this thread's MN elements
+    bool ev[8];
+    int w_r = 0, w_s = 0, w_c = 0;
+    bool w_ok = false;
+    if (MODE == FPROP || MODE == DGRAD) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int m = m0 + (tid >> 3) + 16 * i;
+        rok[i] = m < P.M;
+        const int mm = rok[i] ? m : 0;
+        if (MODE == FPROP) {
+          const uint32_t t = P.fQ.div(mm);
+          const int q = mm - (int)t * g.Q;
+          const uint32_t n = P.fP.div(t);
+          const int p = (int)t - (int)n * g.P;
+          rh[i] = p * g.st - g.pad;
+          rw[i] = q * g.st - g.pad;
+          rbase[i] = (int64_t)n * g.H * g.W * g.C;
+        } else {
+          const uint32_t t = P.fWp.div(mm);
+          const int wq = mm - (int)t * P.Wp;
+          const uint32_t n = P.fHp.div(t);
+          const int hq = (int)t - (int)n * P.Hp;
+          const int h = hq * g.st + P.ph, w = wq * g.st + P.pw;
+          rh[i] = (h + g.pad - P.r0) / g.st;     // p for the first valid tap row; exact division
+          rw[i] = (w + g.pad - P.s0) / g.st;
+          rbase[i] = (int64_t)n * g.P * g.Q * g.K;
+        }
+      }
+    }
+    if (MODE == WGRAD) {
+      if (REG) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int rsc = m0 + (tid & 15) * 8 + e;
+          ev[e] = rsc < P.M;
+          const int rs = (int)P.fC.div(ev[e] ? rsc : 0);
+          ec[e] = (ev[e] ? rsc : 0) - rs * g.C;
+          er[e] = (int)P.fS.div(rs);
+          es[e] = rs - er[e] * g.S;
+        }
+      } else {
+        const int rsc = m0 + (tid & 15) * 8;
+        w_ok = rsc < P.M;
+        const int rs = (int)P.fC.div(w_ok ? rsc : 0);
+        w_c = (w_ok ? rsc : 0) - rs * g.C;
+        w_r = (int)P.fS.div(rs);
+        w_s = rs - w_r * g.S;
+      }
+    }
+    if (REG && MODE == FPROP) {
+      // rows need n, h0, w0 (computed above); per K-block the 8 (r,s,c) of chunk ch
+    }
+
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
       if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)((it / STAGES - 1) & 1));
       const uint32_t a_base = smem_u32(smem + s * STAGE);
       const uint32_t b_base = a_base + A_BYTES;
-      const int64_t kb = kb_begin + it;
+      const int kb = kb_begin + it;
       if (REG && MODE == FPROP) {
-        // narrow-channel stem: K = (r,s,c) padded to kpad, gathered element by
-        // element into registers and stored as 16-byte swizzled chunks
-        const int ch = tid & 7;
         const int RSC = g.R * g.S * g.C;
-        int er[8], es[8], ec[8];
-        bool ev[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const int kk = (int)(kb * BKE) + ch * 8 + e;
+          const int kk = kb * BKE + ch * 8 + e;
           ev[e] = kk < RSC;
-          ec[e] = kk % g.C;
-          const int rs = kk / g.C;
-          es[e] = rs % g.S;
-          er[e] = rs / g.S;
+          const int rs = (int)P.fC.div(ev[e] ? kk : 0);
+          ec[e] = (ev[e] ? kk : 0) - rs * g.C;
+          er[e] = (int)P.fS.div(rs);
+          es[e] = rs - er[e] * g.S;
         }
+        const unsigned short* xs = reinterpret_cast<const unsigned short*>(P.act);
 #pragma unroll 2
-        for (int i = 0; i < BM / 16; ++i) {
+        for (int i = 0; i < 8; ++i) {
           const int row = (tid >> 3) + 16 * i;
-          const int64_t m = m0 + row;
           uint32_t packed[4] = {0u, 0u, 0u, 0u};
-          if (m < P.M) {
-            const int q = (int)(m % g.Q);
-            const int64_t t = m / g.Q;
-            const int p = (int)(t % g.P), n = (int)(t / g.P);
-            const int h0 = p * g.st - g.pad, w0 = q * g.st - g.pad;
-            const unsigned short* xs = reinterpret_cast<const unsigned short*>(P.act) + (int64_t)n * g.H * g.W * g.C;
+          if (rok[i]) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-              const int h = h0 + er[e], w = w0 + es[e];
+              const int h = rh[i] + er[e], w = rw[i] + es[e];
               unsigned short v = 0;
-              if (ev[e] && h >= 0 && h < g.H && w >= 0 && w < g.W) v = __ldg(xs + ((int64_t)h * g.W + w) * g.C + ec[e]);
+              if (ev[e] && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W)
+                v = __ldg(xs + rbase[i] + ((int64_t)h * g.W + w) * g.C + ec[e]);
               packed[e >> 1] |= (uint32_t)v << (16 * (e & 1));
             }
           }
-          const uint32_t dst = a_base + row * 128 + ((ch ^ (row & 7)) << 4);
-          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(packed[0]), "r"(packed[1]),
-                       "r"(packed[2]), "r"(packed[3])
-                       : "memory");
+          st_shared16(a_base + row * 128 + ((ch ^ (row & 7)) << 4), packed);
         }
 #pragma unroll
         for (int i = 0; i < BN / 16; ++i) {
           const int row = (tid >> 3) + 16 * i;
-          const int64_t nn = n0 + row;
+          const int nn = n0 + row;
           const bool ok = nn < P.N;
-          const __nv_bfloat16* src = P.wgt + nn * P.kpad + kb * BKE + ch * 8;
+          cp_async16(b_base + row * 128 + ((ch ^ (row & 7)) << 4),
+                     ok ? P.wgt + (int64_t)nn * P.kpad + kb * BKE + ch * 8 : P.wgt, ok);
+        }
+      } else if (MODE == FPROP || MODE == DGRAD) {
+        // K-block kb covers one tap and 64 consecutive reduced channels (kch % 64 == 0)
+        const int kk0 = kb * BKE;
+        const int tap = (int)P.fKch.div(kk0), c0 = kk0 - tap * P.kch;
+        int dr, ds;   // fprop: r, s; dgrad: tap indices i, j
+        if (MODE == FPROP) { dr = (int)P.fS.div(tap); ds = tap - dr * g.S; }
+        else { dr = (int)P.fns.div(tap); ds = tap - dr * P.ns; }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row = (tid >> 3) + 16 * i;
+          bool ok;
+          const __nv_bfloat16* src;
+          if (MODE == FPROP) {
+            const int h = rh[i] + dr, w = rw[i] + ds;
+            ok = rok[i] && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W;
+            src = P.act + rbase[i] + ((int64_t)h * g.W + w) * g.C + c0 + ch * 8;
+          } else {
+            const int p = rh[i] - dr, q = rw[i] - ds;
+            ok = rok[i] && (unsigned)p < (unsigned)g.P && (unsigned)q < (unsigned)g.Q;
+            src = P.act + rbase[i] + ((int64_t)p * g.Q + q) * g.K + c0 + ch * 8;
+          }
+          cp_async16(a_base + row * 128 + ((ch ^ (row & 7)) << 4), ok ? src : P.act, ok);
+        }
+        int r, sx;
+        if (MODE == FPROP) { r = dr; sx = ds; }
+        else { r = P.r0 + g.st * dr; sx = P.s0 + g.st * ds; }
+#pragma unroll
+        for (int i = 0; i < BN / 16; ++i) {
+          const int row = (tid >> 3) + 16 * i;
+          const int nn = n0 + row;
+          const bool ok = nn < P.N;
+          const __nv_bfloat16* src;
+          if (MODE == FPROP) src = P.wgt + (int64_t)nn * P.kpad + kk0 + ch * 8;
+          else src = P.wgt + ((int64_t)nn * g.R * g.S + r * g.S + sx) * g.K + c0 + ch * 8;
           cp_async16(b_base + row * 128 + ((ch ^ (row & 7)) << 4), ok ? src : P.wgt, ok);
         }
-      } else if (REG && MODE == WGRAD) {
-        const int64_t mbase = kb * BKE;
-        const int j = tid & 15;                     // fixed MN chunk: rows rsc = m0 + 8j .. +7
-        int er[8], es[8], ec[8];
-        bool ev[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int64_t rsc = m0 + j * 8 + e;
-          ev[e] = rsc < P.M;
-          ec[e] = (int)(rsc % g.C);
-          const int rs = (int)(rsc / g.C);
-          es[e] = rs % g.S;
-          er[e] = rs / g.S;
-        }
-#pragma unroll 2
+      } else {
+        // WGRAD, MN-major tiles: K-row kr (an output pixel m) holds 128 (r,s,c) of X for A
+        // and BN output channels of dY for B.  Atom (8 K-rows × 64 MN) = 1 KB;
+        // A: [atom_k 8][atom_mn 2][8][128 B]  (LBO 1 KB, SBO 2 KB)
+        // B: [atom_k 8][atom_mn BN/64][8][128 B] (LBO 1 KB, SBO BN/64 KB)
+        const int mbase = kb * BKE;
+        const int j = tid & 15;
+#pragma unroll 4
         for (int i = 0; i < 8; ++i) {
           const int kr = (tid >> 4) + 8 * i;
-          const int64_t mm = mbase + kr;
-          uint32_t packed[4] = {0u, 0u, 0u, 0u};
-          if (mm < P.gemm_k) {
-            const int q = (int)(mm % g.Q);
-            const int64_t t = mm / g.Q;
-            const int p = (int)(t % g.P), n = (int)(t / g.P);
-            const int h0 = p * g.st - g.pad, w0 = q * g.st - g.pad;
-            const unsigned short* xs = reinterpret_cast<const unsigned short*>(P.act) + (int64_t)n * g.H * g.W * g.C;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int h = h0 + er[e], w = w0 + es[e];
-              unsigned short v = 0;
-              if (ev[e] && h >= 0 && h < g.H && w >= 0 && w < g.W) v = __ldg(xs + ((int64_t)h * g.W + w) * g.C + ec[e]);
-              packed[e >> 1] |= (uint32_t)v << (16 * (e & 1));
-            }
-          }
+          const int mm = mbase + kr;
+          const bool mok = mm < P.gemm_k;
+          const uint32_t t = P.fQ.div(mok ? mm : 0);
+          const int q = (mok ? mm : 0) - (int)t * g.Q;
+          const uint32_t n = P.fP.div(t);
+          const int p = (int)t - (int)n * g.P;
+          const int h0 = p * g.st - g.pad, w0 = q * g.st - g.pad;
           const int row = kr & 7;
           const uint32_t dst = a_base + (kr >> 3) * 2048 + (j >> 3) * 1024 + row * 128 + (((j & 7) ^ row) << 4);
-          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(packed[0]), "r"(packed[1]),
-                       "r"(packed[2]), "r"(packed[3])
-                       : "memory");
+          if (REG) {
+            uint32_t packed[4] = {0u, 0u, 0u, 0u};
+            if (mok) {
+              const unsigned short* xs = reinterpret_cast<const unsigned short*>(P.act) + (int64_t)n * g.H * g.W * g.C;
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int h = h0 + er[e], w = w0 + es[e];
+                unsigned short v = 0;
+                if (ev[e] && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W)
+                  v = __ldg(xs + ((int64_t)h * g.W + w) * g.C + ec[e]);
+                packed[e >> 1] |= (uint32_t)v << (16 * (e & 1));
+              }
+            }
+            st_shared16(dst, packed);
+          } else {
+            const int h = h0 + w_r, w = w0 + w_s;
+            const bool ok = mok && w_ok && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W;
+            const __nv_bfloat16* src = P.act + (((int64_t)n * g.H + h) * g.W + w) * g.C + w_c;
+            cp_async16(dst, ok ? src : P.act, ok);
+          }
         }
         constexpr int BCH = BN / 8;
 #pragma unroll
         for (int i = 0; i < (64 * BCH) / NPROD; ++i) {
           const int e = tid + NPROD * i;
           const int kr = e / BCH, jj = e % BCH;
-          const int64_t mm = mbase + kr;
-          const int64_t kk = n0 + jj * 8;
+          const int mm = mbase + kr;
+          const int kk = n0 + jj * 8;
           const bool ok = mm < P.gemm_k && kk < P.N;
-          const __nv_bfloat16* src = P.wgt + mm * g.K + kk;
+          const __nv_bfloat16* src = P.wgt + (int64_t)mm * g.K + kk;
           const int row = kr & 7;
           const uint32_t dst = b_base + (kr >> 3) * (BN / 64) * 1024 + (jj >> 3) * 1024 + row * 128 +
                                (((jj & 7) ^ row) << 4);
-          cp_async16(dst, ok ? src : P.wgt, ok);
-        }
-      } else if (MODE == FPROP || MODE == DGRAD) {
-        // K-block kb covers one tap (r,s) and 64 channels (Kch % 64 == 0)
-        const int Kch = MODE == FPROP ? g.C : g.K;       // reduced channels
-        const int64_t kk0 = kb * BKE;
-        const int tap = (int)(kk0 / Kch), c0 = (int)(kk0 % Kch);
-        int r, sx;
-        if (MODE == FPROP) { r = tap / g.S; sx = tap % g.S; }
-        else { r = P.r0 + g.st * (tap / P.ns); sx = P.s0 + g.st * (tap % P.ns); }
-        // A: 128 rows × 8 chunks; thread handles chunk (tid & 7) of rows (tid >> 3) + 16·i
-        const int ch = tid & 7;
-#pragma unroll
-        for (int i = 0; i < BM / 16; ++i) {
-          const int row = (tid >> 3) + 16 * i;
-          const int64_t m = m0 + row;
-          const __nv_bfloat16* src = P.act;
-          bool ok = m < P.M;
-          if (ok) {
-            if (MODE == FPROP) {
-              const int q = (int)(m % g.Q);
-              const int64_t t = m / g.Q;
-              const int p = (int)(t % g.P), n = (int)(t / g.P);
-              const int h = p * g.st - g.pad + r, w = q * g.st - g.pad + sx;
-              ok = h >= 0 && h < g.H && w >= 0 && w < g.W;
-              src = P.act + (((int64_t)n * g.H + h) * g.W + w) * g.C + c0 + ch * 8;
-            } else {
-              const int wq = (int)(m % P.Wp);
-              const int64_t t = m / P.Wp;
-              const int hq = (int)(t % P.Hp), n = (int)(t / P.Hp);
-              const int h = hq * g.st + P.ph, w = wq * g.st + P.pw;
-              const int pn = h + g.pad - r, qn = w + g.pad - sx;   // divisible by st by construction
-              const int p = pn / g.st, q = qn / g.st;
-              ok = pn >= 0 && qn >= 0 && p < g.P && q < g.Q;
-              src = P.act + (((int64_t)n * g.P + p) * g.Q + q) * g.K + c0 + ch * 8;
-            }
-          }
-          cp_async16(a_base + row * 128 + ((ch ^ (row & 7)) << 4), ok ? src : P.act, ok);
-        }
-        // B: BN rows of the bf16 weight copy, K-major
-#pragma unroll
-        for (int i = 0; i < BN / 16; ++i) {
-          const int row = (tid >> 3) + 16 * i;
-          const int64_t nn = n0 + row;
-          const bool ok = nn < P.N;
-          const __nv_bfloat16* src;
-          if (MODE == FPROP) src = P.wgt + nn * ((int64_t)g.R * g.S * g.C) + kk0 + ch * 8;
-          else src = P.wgt + (nn * g.R * g.S + (int64_t)r * g.S + sx) * g.K + c0 + ch * 8;
-          cp_async16(b_base + row * 128 + ((ch ^ (row & 7)) << 4), ok ? src : P.wgt, ok);
-        }
-      } else {
-        // WGRAD, MN-major tiles: K-row kk (an output pixel m) holds 128 (r,s,c) of X for A
-        // and BN output channels of dY for B.  Atom (8 K-rows × 64 MN) = 1 KB;
-        // A: [atom_k 8][atom_mn 2][8][128 B]  (LBO 1 KB, SBO 2 KB)
-        // B: [atom_k 8][atom_mn BN/64][8][128 B] (LBO 1 KB, SBO BN/64 KB)
-        const int64_t mbase = kb * BKE;
-        // A: 64 K-rows × 16 chunks = 1024 chunks, 8 per thread
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = tid + NPROD * i;
-          const int kr = e >> 4, j = e & 15;          // K-row, 16B chunk along MN
-          const int64_t mm = mbase + kr;
-          const int64_t rsc = m0 + j * 8;
-          bool ok = mm < P.gemm_k && rsc < P.M;
-          const __nv_bfloat16* src = P.act;
-          if (ok) {
-            const int c = (int)(rsc % g.C);
-            const int64_t rs = rsc / g.C;
-            const int sx = (int)(rs % g.S), r = (int)(rs / g.S);
-            const int q = (int)(mm % g.Q);
-            const int64_t t = mm / g.Q;
-            const int p = (int)(t % g.P), n = (int)(t / g.P);
-            const int h = p * g.st - g.pad + r, w = q * g.st - g.pad + sx;
-            ok = h >= 0 && h < g.H && w >= 0 && w < g.W;
-            src = P.act + (((int64_t)n * g.H + h) * g.W + w) * g.C + c;
-          }
-          const int row = kr & 7;
-          const uint32_t dst = a_base + (kr >> 3) * 2048 + (j >> 3) * 1024 + row * 128 + (((j & 7) ^ row) << 4);
-          cp_async16(dst, ok ? src : P.act, ok);
-        }
-        // B: 64 K-rows × BN/8 chunks
-        constexpr int BCH = BN / 8;
-#pragma unroll
-        for (int i = 0; i < (64 * BCH) / NPROD; ++i) {
-          const int e = tid + NPROD * i;
-          const int kr = e / BCH, j = e % BCH;
-          const int64_t mm = mbase + kr;
-          const int64_t kk = n0 + j * 8;
-          const bool ok = mm < P.gemm_k && kk < P.N;
-          const __nv_bfloat16* src = P.wgt + mm * g.K + kk;
-          const int row = kr & 7;
-          const uint32_t dst = b_base + (kr >> 3) * (BN / 64) * 1024 + (j >> 3) * 1024 + row * 128 +
-                               (((j & 7) ^ row) << 4);
           cp_async16(dst, ok ? src : P.wgt, ok);
         }
       }
@@ -370,8 +384,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
   } else if (warp == 4) {
     // ------------------------------------------------------------ MMA issuer (one elected lane)
     constexpr uint32_t ID = idesc(BN, MODE == WGRAD, MODE == WGRAD);
-    for (int64_t it = 0; it < nkb; ++it) {
-      const int s = (int)(it % STAGES);
+    for (int it = 0; it < nkb; ++it) {
+      const int s = it % STAGES;
       mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (lane == 0) {
@@ -400,10 +414,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
   // ------------------------------------------------------------ epilogue (warps 0-3)
   if (tid < NPROD) {
     const int row = warp * 32 + lane;
-    const int64_t m = m0 + row;
+    const int m = m0 + row;
     if (nkb > 0) {
       mbar_wait(tfull, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    int64_t orow = m;
+    if (MODE == DGRAD && m < P.M) {
+      const uint32_t t = P.fWp.div(m);
+      const int wq = m - (int)t * P.Wp;
+      const uint32_t n = P.fHp.div(t);
+      const int hq = (int)t - (int)n * P.Hp;
+      orow = ((int64_t)n * g.H + hq * g.st + P.ph) * g.W + wq * g.st + P.pw;
     }
 #pragma unroll
     for (int j0 = 0; j0 < BN; j0 += 32) {
@@ -427,15 +449,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
           for (int i = 0; i < 32 && n0 + j0 + i < P.N; ++i) o[i] = __uint_as_float(v[i]);
         }
       } else {
-        int64_t orow;
-        if (MODE == FPROP) {
-          orow = m;
-        } else {
-          const int wq = (int)(m % P.Wp);
-          const int64_t t = m / P.Wp;
-          const int hq = (int)(t % P.Hp), n = (int)(t / P.Hp);
-          orow = ((int64_t)n * g.H + hq * g.st + P.ph) * g.W + wq * g.st + P.pw;
-        }
         __nv_bfloat16* o = (__nv_bfloat16*)P.out + orow * P.N + n0 + j0;
         if (n0 + j0 + 32 <= P.N) {
 #pragma unroll
@@ -479,9 +492,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
 
 // fp32 KRSC master -> bf16 [K][kpad] (fprop; zero padding past RSC) or [C][R][S][K] (dgrad)
 __global__ void weight_bf16(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int K, int RS, int C,
-                            int transpose, int64_t kpad) {
+                            int transpose, int kpad) {
   const int64_t n = transpose ? (int64_t)K * RS * C : (int64_t)K * kpad;
-  const int64_t rsc = (int64_t)RS * C;
+  const int rsc = RS * C;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     if (transpose) {
       const int c = (int)(i % C);
@@ -495,8 +508,8 @@ __global__ void weight_bf16(const float* __restrict__ w, __nv_bfloat16* __restri
   }
 }
 
-__global__ void wgrad_reduce(int splits, int64_t RSC, int K, const float* __restrict__ part, float* __restrict__ dw) {
-  const int64_t n = RSC * K;
+__global__ void wgrad_reduce(int splits, int RSC, int K, const float* __restrict__ part, float* __restrict__ dw) {
+  const int64_t n = (int64_t)RSC * K;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int k = (int)(i % K);
     const int64_t rsc = i / K;
@@ -529,17 +542,31 @@ int wgrad_splits(const ConvGeom& g, int BN) {
   return (int)(s < 1 ? 1 : s);
 }
 
+void fill_divs(Params& P) {
+  const ConvGeom& g = P.g;
+  P.fQ.init(g.Q);
+  P.fP.init(g.P);
+  P.fWp.init(P.Wp > 0 ? P.Wp : 1);
+  P.fHp.init(P.Hp > 0 ? P.Hp : 1);
+  P.fC.init(g.C);
+  P.fS.init(g.S);
+  P.fKch.init(P.kch > 0 ? P.kch : 1);
+  P.fns.init(P.ns > 0 ? P.ns : 1);
+}
+
 }  // namespace tc
 
 using namespace tc;
 
 bool conv_tc_ok(const ConvGeom& g, int mode) {
+  const int64_t big = (int64_t)g.N * g.H * g.W * std::max(g.C, g.K);
+  if (big >= (1ll << 31)) return false;  // 32-bit index arithmetic
   if (mode == FPROP) return g.K % 64 == 0 && (g.C % 64 == 0 || g.C < 64);
   if (mode == DGRAD) return g.K % 64 == 0 && g.C % 64 == 0 && (g.st == 1 || g.st == 2);
   return g.K % 64 == 0;
 }
 
-static int64_t kpad_of(const ConvGeom& g) { return ((int64_t)g.R * g.S * g.C + BKE - 1) / BKE * BKE; }
+static int kpad_of(const ConvGeom& g) { return (g.R * g.S * g.C + BKE - 1) / BKE * BKE; }
 
 size_t conv_tc_ws(const ConvGeom& g, int mode) {
   size_t wbytes = (size_t)g.K * kpad_of(g) * 2;
@@ -553,24 +580,23 @@ size_t conv_tc_ws(const ConvGeom& g, int mode) {
 Status conv_fprop_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y) {
   __nv_bfloat16* wb = (__nv_bfloat16*)a.ws;
   const bool reg = g.C % 64 != 0;
-  const int64_t kpad = kpad_of(g);
-  weight_bf16<<<grid_for(g.K * kpad, 256, 4), 256, 0, a.stream>>>(w, wb, g.K, g.R * g.S, g.C, 0, kpad);
+  const int kpad = kpad_of(g);
+  weight_bf16<<<grid_for((int64_t)g.K * kpad, 256, 4), 256, 0, a.stream>>>(w, wb, g.K, g.R * g.S, g.C, 0, kpad);
   OC_LAUNCH_CHECK(a);
   Params P{};
   P.g = g;
   P.act = x;
   P.wgt = wb;
   P.out = y;
-  P.M = (int64_t)g.N * g.P * g.Q;
+  P.M = g.N * g.P * g.Q;
   P.N = g.K;
   P.kpad = kpad;
+  P.kch = g.C;
   P.nkb = kpad / BKE;
-  if (reg) {
-    if (g.K % 128 == 0) return launch<FPROP, 128, true>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.K / 128, 1));
-    return launch<FPROP, 64, true>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.K / 64, 1));
-  }
-  if (g.K % 128 == 0) return launch<FPROP, 128>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.K / 128, 1));
-  return launch<FPROP, 64>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.K / 64, 1));
+  fill_divs(P);
+  const dim3 grid((P.M + BM - 1) / BM, g.K / (g.K % 128 == 0 ? 128 : 64), 1);
+  if (reg) return g.K % 128 == 0 ? launch<FPROP, 128, true>(a, P, grid) : launch<FPROP, 64, true>(a, P, grid);
+  return g.K % 128 == 0 ? launch<FPROP, 128>(a, P, grid) : launch<FPROP, 64>(a, P, grid);
 }
 
 Status conv_dgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const float* w, __nv_bfloat16* dx,
@@ -592,17 +618,19 @@ Status conv_dgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, cons
       P.Hp = (g.H - ph + g.st - 1) / g.st;
       P.Wp = (g.W - pw + g.st - 1) / g.st;
       // taps with (h + pad − r) divisible by st for h ≡ ph (mod st)
-      P.r0 = ((ph + g.pad) % g.st + g.st) % g.st;
-      P.s0 = ((pw + g.pad) % g.st + g.st) % g.st;
+      P.r0 = (ph + g.pad) % g.st;
+      P.s0 = (pw + g.pad) % g.st;
       P.nr = P.r0 < g.R ? (g.R - P.r0 + g.st - 1) / g.st : 0;
       P.ns = P.s0 < g.S ? (g.S - P.s0 + g.st - 1) / g.st : 0;
-      P.M = (int64_t)g.N * P.Hp * P.Wp;
+      P.M = g.N * P.Hp * P.Wp;
       P.N = g.C;
-      P.nkb = (int64_t)P.nr * P.ns * g.K / BKE;
+      P.kch = g.K;
+      P.nkb = P.nr * P.ns * g.K / BKE;
       if (P.M == 0) continue;
       if (P.nkb == 0 && accumulate) continue;  // no taps reach this phase: G stays as is
-      Status st = g.C % 128 == 0 ? launch<DGRAD, 128>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.C / 128, 1))
-                                 : launch<DGRAD, 64>(a, P, dim3((unsigned)((P.M + BM - 1) / BM), g.C / 64, 1));
+      fill_divs(P);
+      const dim3 grid((P.M + BM - 1) / BM, g.C / (g.C % 128 == 0 ? 128 : 64), 1);
+      Status st = g.C % 128 == 0 ? launch<DGRAD, 128>(a, P, grid) : launch<DGRAD, 64>(a, P, grid);
       if (!st.good()) return st;
     }
   return Status::ok();
@@ -616,18 +644,19 @@ Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, cons
   P.act = x;
   P.wgt = dy;
   P.out = a.ws;
-  P.M = (int64_t)g.R * g.S * g.C;
+  P.M = g.R * g.S * g.C;
   P.N = g.K;
-  P.gemm_k = (int64_t)g.N * g.P * g.Q;
-  const int64_t kbs = (P.gemm_k + BKE - 1) / BKE;
+  P.gemm_k = g.N * g.P * g.Q;
+  const int kbs = (P.gemm_k + BKE - 1) / BKE;
   P.kb_per_split = (kbs + splits - 1) / splits;
   P.nkb = P.kb_per_split;
-  dim3 grid((unsigned)((P.M + BM - 1) / BM), g.K / BN, splits);
+  fill_divs(P);
+  dim3 grid((P.M + BM - 1) / BM, g.K / BN, splits);
   Status st;
   if (g.C % 8 != 0) st = BN == 128 ? launch<WGRAD, 128, true>(a, P, grid) : launch<WGRAD, 64, true>(a, P, grid);
   else st = BN == 128 ? launch<WGRAD, 128>(a, P, grid) : launch<WGRAD, 64>(a, P, grid);
   if (!st.good()) return st;
-  wgrad_reduce<<<grid_for(P.M * g.K, 256, 4), 256, 0, a.stream>>>(splits, P.M, g.K, (const float*)a.ws, dw);
+  wgrad_reduce<<<grid_for((int64_t)P.M * g.K, 256, 4), 256, 0, a.stream>>>(splits, P.M, g.K, (const float*)a.ws, dw);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
