@@ -55,6 +55,45 @@ def run_step(spec, doc, info, budget, window, mode, phys, chunk=2 * MiB, steps=1
 
 
 @pytest.mark.gpu
+def test_resnet18_full_resolution_parity():
+    """The full ResNet-18 graph at 224x224 (batch 2 so the oracle finishes in
+    seconds; every conv spans many tiles with ragged tails) under a 25%
+    budget, VA allocator: every parameter gradient within 1e-3 of the oracle."""
+    spec = nets.resnet(18, batch=2)
+    doc, info = graphs.build(spec, params="persistent")
+    G = B.Graph(doc)
+    peak = G.in_core_peak()
+    budget = max(G.min_feasible_budget(0), peak // 4)
+    x, y = nets.make_inputs(spec)
+    p = nets.make_params(spec)
+    ref = nm.train_step(spec, p, x, y)
+    out = run_step(spec, doc, info, budget, B.OC_WINDOW_MAX_FEASIBLE, "va", 512 * MiB)
+    assert out["metrics"]["bytes_d2h"] > 0
+    assert abs(out["loss"] - ref["loss"]) <= 1e-3 * abs(ref["loss"])
+    errs = {k: nm.rel_l2(out["m." + k], ref["grads"][k]) for k in p}
+    worst = max(errs, key=errs.get)
+    assert errs[worst] <= 1e-3, (worst, errs[worst])
+
+
+@pytest.mark.gpu
+def test_resnet18_bench_size_swap_transparency():
+    """At the bench configuration (ResNet-18, batch 256, 25% budget, VA 2 MiB
+    chunks) the out-of-core step equals the in-core step bitwise — a property
+    that holds at any size."""
+    spec = nets.resnet(18, batch=256)
+    doc, info = graphs.build(spec, params="persistent")
+    G = B.Graph(doc)
+    peak = G.in_core_peak()
+    ooc = run_step(spec, doc, info, peak // 4, B.OC_WINDOW_MAX_FEASIBLE, "va", peak // 4 + 512 * MiB)
+    inc = run_step(spec, doc, info, peak, 0, "best", peak + 64 * MiB)
+    assert ooc["metrics"]["bytes_d2h"] > 10 ** 9
+    assert ooc["loss"] == inc["loss"]
+    for k in nets.make_params(spec):
+        assert np.array_equal(ooc["p." + k], inc["p." + k]), k
+        assert np.array_equal(ooc["m." + k], inc["m." + k]), k
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["va", "best"])
 def test_tiny_resnet_parity_and_transparency(mode):
     spec = nets.tiny_resnet(batch=4, image=16, classes=10)
