@@ -18,11 +18,13 @@ inline ConvGeom conv_geom(const JVal& j) {
                   (int)j.geti("Q")};
 }
 
-// CUDA-core implicit GEMM (conv_simt.cu)
-Status conv_fprop_simt(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y);
-Status conv_dgrad_simt(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const float* w, __nv_bfloat16* dx,
-                       bool accumulate);
-Status conv_wgrad_simt(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* x, float* dw);
+// CUDA-core implicit GEMM (conv_simt.cu); T = __nv_bfloat16 or float
+template <typename T>
+Status conv_fprop_simt(OpArgs& a, const ConvGeom& g, const T* x, const float* w, T* y);
+template <typename T>
+Status conv_dgrad_simt(OpArgs& a, const ConvGeom& g, const T* dy, const float* w, T* dx, bool accumulate);
+template <typename T>
+Status conv_wgrad_simt(OpArgs& a, const ConvGeom& g, const T* dy, const T* x, float* dw);
 size_t conv_wgrad_ws_simt(const ConvGeom& g);
 
 }  // namespace oc

@@ -1,8 +1,8 @@
-// Convolution as implicit GEMM on CUDA cores (bf16 operands, fp32 FFMA
-// accumulation) — the reference-speed fallback kept for small/odd shapes and
-// as the cross-check of the tcgen05 kernels (conv_tc.cu).  NHWC activations,
-// KRSC weights (fp32 masters rounded to bf16 on load, the act-dtype copy of
-// the numerics contract).
+// Convolution as implicit GEMM on CUDA cores (FFMA, fp32 accumulation) —
+// the fp32 parity mode's convolution (no TF32) and the fallback for
+// shapes outside the tcgen05 tiling; also the cross-check of conv_tc.cu.
+// NHWC activations of type T (bf16 or fp32), KRSC fp32 weight masters rounded
+// to T on load (the act-dtype weight copy of the numerics contract).
 //   fprop  y[m=(n,p,q), k]   = Σ_{(r,s,c)} x[n, p·st−pad+r, q·st−pad+s, c] · W[k,r,s,c]
 //   dgrad  dx[m=(n,h,w), c]  = Σ_{(r,s,k)} dy[n, (h+pad−r)/st, (w+pad−s)/st, k] · W[k,r,s,c]
 //                              (terms with a non-integer or out-of-range index vanish)
@@ -16,11 +16,10 @@ namespace {
 
 constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
 
-template <int MODE>
-__global__ void __launch_bounds__(256) conv_simt(ConvGeom g, const __nv_bfloat16* __restrict__ a_src,
-                                                 const float* __restrict__ w, const __nv_bfloat16* __restrict__ b_src,
-                                                 void* out, int accumulate, int64_t k_begin_step) {
-  // GEMM sizes
+template <int MODE, typename T>
+__global__ void __launch_bounds__(256) conv_simt(ConvGeom g, const T* __restrict__ a_src, const float* __restrict__ w,
+                                                 const T* __restrict__ b_src, void* out, int accumulate,
+                                                 int64_t k_step) {
   int64_t M, N, Kg;
   if (MODE == 0) { M = (int64_t)g.N * g.P * g.Q; N = g.K; Kg = (int64_t)g.R * g.S * g.C; }
   else if (MODE == 1) { M = (int64_t)g.N * g.H * g.W; N = g.C; Kg = (int64_t)g.R * g.S * g.K; }
@@ -31,8 +30,8 @@ __global__ void __launch_bounds__(256) conv_simt(ConvGeom g, const __nv_bfloat16
   const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
   int64_t kb = 0, ke = Kg;
   if (MODE == 2) {  // split-K slice z
-    kb = (int64_t)blockIdx.z * k_begin_step;
-    ke = (kb + k_begin_step < Kg) ? kb + k_begin_step : Kg;
+    kb = (int64_t)blockIdx.z * k_step;
+    ke = (kb + k_step < Kg) ? kb + k_step : Kg;
   }
   float acc[TM][TN] = {};
   for (int64_t k0 = kb; k0 < ke; k0 += BK) {
@@ -52,8 +51,7 @@ __global__ void __launch_bounds__(256) conv_simt(ConvGeom g, const __nv_bfloat16
             const int64_t t = gm / g.Q;
             const int p = (int)(t % g.P), n = (int)(t / g.P);
             const int h = p * g.st - g.pad + r, ww = q * g.st - g.pad + s;
-            if (h >= 0 && h < g.H && ww >= 0 && ww < g.W)
-              v = __bfloat162float(a_src[(((int64_t)n * g.H + h) * g.W + ww) * g.C + c]);
+            if (h >= 0 && h < g.H && ww >= 0 && ww < g.W) v = ld_f(a_src + (((int64_t)n * g.H + h) * g.W + ww) * g.C + c);
           } else if (MODE == 1) {
             const int k = (int)(gk % g.K);
             const int64_t rs = gk / g.K;
@@ -64,10 +62,10 @@ __global__ void __launch_bounds__(256) conv_simt(ConvGeom g, const __nv_bfloat16
             const int pn = h + g.pad - r, qn = ww + g.pad - s;
             if (pn >= 0 && qn >= 0 && pn % g.st == 0 && qn % g.st == 0) {
               const int p = pn / g.st, q = qn / g.st;
-              if (p < g.P && q < g.Q) v = __bfloat162float(a_src[(((int64_t)n * g.P + p) * g.Q + q) * g.K + k]);
+              if (p < g.P && q < g.Q) v = ld_f(a_src + (((int64_t)n * g.P + p) * g.Q + q) * g.K + k);
             }
           } else {
-            v = __bfloat162float(a_src[gk * g.K + gm]);  // dy[m][k], GEMM row = k
+            v = ld_f(a_src + gk * g.K + gm);  // dy[m][k], GEMM row = k
           }
         }
         As[kk][mm] = v;
@@ -78,11 +76,11 @@ __global__ void __launch_bounds__(256) conv_simt(ConvGeom g, const __nv_bfloat16
         float v = 0.f;
         if (gn < N && gk < ke) {
           if (MODE == 0) {
-            v = rnd<__nv_bfloat16>(w[gn * Kg + gk]);
+            v = rnd<T>(w[gn * Kg + gk]);
           } else if (MODE == 1) {
             const int k = (int)(gk % g.K);
             const int64_t rs = gk / g.K;
-            v = rnd<__nv_bfloat16>(w[((int64_t)k * g.R * g.S + rs) * g.C + gn]);
+            v = rnd<T>(w[((int64_t)k * g.R * g.S + rs) * g.C + gn]);
           } else {
             const int c = (int)(gn % g.C);
             const int64_t rs = gn / g.C;
@@ -91,8 +89,7 @@ __global__ void __launch_bounds__(256) conv_simt(ConvGeom g, const __nv_bfloat16
             const int64_t t = gk / g.Q;
             const int p = (int)(t % g.P), n = (int)(t / g.P);
             const int h = p * g.st - g.pad + r, ww = q * g.st - g.pad + s;
-            if (h >= 0 && h < g.H && ww >= 0 && ww < g.W)
-              v = __bfloat162float(b_src[(((int64_t)n * g.H + h) * g.W + ww) * g.C + c]);
+            if (h >= 0 && h < g.H && ww >= 0 && ww < g.W) v = ld_f(b_src + (((int64_t)n * g.H + h) * g.W + ww) * g.C + c);
           }
         }
         Bs[kk][nn] = v;
@@ -124,10 +121,10 @@ __global__ void __launch_bounds__(256) conv_simt(ConvGeom g, const __nv_bfloat16
       if (MODE == 2) {
         ((float*)out)[((int64_t)blockIdx.z * M + gm) * N + gn] = acc[i][j];
       } else {
-        __nv_bfloat16* o = (__nv_bfloat16*)out + gm * N + gn;
+        T* o = (T*)out + gm * N + gn;
         float v = acc[i][j];
-        if (accumulate) v += __bfloat162float(*o);
-        *o = __float2bfloat16_rn(v);
+        if (accumulate) v += ld_f(o);
+        st_f(o, v);
       }
     }
   }
@@ -148,22 +145,24 @@ int wgrad_splits_simt(const ConvGeom& g) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(64, 296 / std::max<int64_t>(1, tiles)));
 }
 
-Status conv_fprop_simt(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y) {
+template <typename T>
+Status conv_fprop_simt(OpArgs& a, const ConvGeom& g, const T* x, const float* w, T* y) {
   dim3 grid((g.K + BN - 1) / BN, (unsigned)(((int64_t)g.N * g.P * g.Q + BM - 1) / BM));
-  conv_simt<0><<<grid, 256, 0, a.stream>>>(g, x, w, nullptr, y, 0, 0);
+  conv_simt<0, T><<<grid, 256, 0, a.stream>>>(g, x, w, nullptr, y, 0, 0);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
 
-Status conv_dgrad_simt(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const float* w, __nv_bfloat16* dx,
-                       bool accumulate) {
+template <typename T>
+Status conv_dgrad_simt(OpArgs& a, const ConvGeom& g, const T* dy, const float* w, T* dx, bool accumulate) {
   dim3 grid((g.C + BN - 1) / BN, (unsigned)(((int64_t)g.N * g.H * g.W + BM - 1) / BM));
-  conv_simt<1><<<grid, 256, 0, a.stream>>>(g, dy, w, nullptr, dx, accumulate ? 1 : 0, 0);
+  conv_simt<1, T><<<grid, 256, 0, a.stream>>>(g, dy, w, nullptr, dx, accumulate ? 1 : 0, 0);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
 
-Status conv_wgrad_simt(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* x, float* dw) {
+template <typename T>
+Status conv_wgrad_simt(OpArgs& a, const ConvGeom& g, const T* dy, const T* x, float* dw) {
   const int splits = wgrad_splits_simt(g);
   const int64_t Kg = (int64_t)g.N * g.P * g.Q;
   int64_t step = (Kg + splits - 1) / splits;
@@ -171,12 +170,22 @@ Status conv_wgrad_simt(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, co
   const int64_t n = (int64_t)g.K * g.R * g.S * g.C;
   if (a.ws_bytes < (size_t)(splits * n * 4)) return Status::make(OC_E_INVARIANT, "wgrad: workspace too small");
   dim3 grid((unsigned)(((int64_t)g.R * g.S * g.C + BN - 1) / BN), (g.K + BM - 1) / BM, splits);
-  conv_simt<2><<<grid, 256, 0, a.stream>>>(g, dy, nullptr, x, a.ws, 0, step);
+  conv_simt<2, T><<<grid, 256, 0, a.stream>>>(g, dy, nullptr, x, a.ws, 0, step);
   OC_LAUNCH_CHECK(a);
   splitk_reduce<<<grid_for(n, 256, 4), 256, 0, a.stream>>>(splits, n, (const float*)a.ws, dw);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
+
+template Status conv_fprop_simt<__nv_bfloat16>(OpArgs&, const ConvGeom&, const __nv_bfloat16*, const float*,
+                                                __nv_bfloat16*);
+template Status conv_fprop_simt<float>(OpArgs&, const ConvGeom&, const float*, const float*, float*);
+template Status conv_dgrad_simt<__nv_bfloat16>(OpArgs&, const ConvGeom&, const __nv_bfloat16*, const float*,
+                                                __nv_bfloat16*, bool);
+template Status conv_dgrad_simt<float>(OpArgs&, const ConvGeom&, const float*, const float*, float*, bool);
+template Status conv_wgrad_simt<__nv_bfloat16>(OpArgs&, const ConvGeom&, const __nv_bfloat16*, const __nv_bfloat16*,
+                                                float*);
+template Status conv_wgrad_simt<float>(OpArgs&, const ConvGeom&, const float*, const float*, float*);
 
 size_t conv_wgrad_ws_simt(const ConvGeom& g) {
   return (size_t)wgrad_splits_simt(g) * g.K * g.R * g.S * g.C * 4;

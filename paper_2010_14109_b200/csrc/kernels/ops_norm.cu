@@ -1,15 +1,19 @@
 // Batch-norm / ReLU / residual-add / pooling kernels of the conv-net training
-// step, NHWC bf16 activations viewed as [rows, C].
+// step, NHWC activations (bf16, or fp32 in the fp32
+// parity mode) viewed as [rows, C].
 //
-// Memory-bound: every kernel moves 16-byte vectors (8 bf16 channels) per
-// thread with coalesced row-major access and grids sized in multiples of the
-// 148 SMs.  Per-channel reductions are deterministic two-level reductions
-// (fixed row chunks -> fp32 partials -> fixed-order double finalize) so the
-// step is bitwise reproducible whatever the swap schedule.
+// Memory-bound: every thread moves 8 channels (16 B of bf16) per access with
+// coalesced row-major access, grid-stride loops over grids sized in multiples
+// of the 148 SMs, and 32-bit index math with multiply-shift division.
+// Per-channel reductions are deterministic two-level reductions (fixed row
+// chunks -> fp32 partials -> fixed-order double finalize, one warp per
+// channel) so a step is bitwise reproducible whatever the swap schedule.
 //
 // Contract (oracle/numerics.py): x̂ = (y−μ)·rstd with batch statistics and
 // biased variance, eps = 1e-5; out = rnd(relu(γx̂ + β + res)); backward
 // dz = g·[out>0], dβ = Σdz, dγ = Σdz·x̂, dy = γ·rstd·(dz − dβ/n − x̂·dγ/n).
+// Algorithmic bytes per launch = one read of every input + one write of every
+// output (roofline: HBM).
 #include "common.cuh"
 
 namespace oc {
@@ -19,38 +23,16 @@ namespace {
 constexpr float kEps = 1e-5f;
 constexpr int kStatBlocks = 148 * 4;  // row chunks of the two-level reductions
 
-struct V8 {
-  float v[8];
-};
-
-__device__ __forceinline__ V8 ld8(const __nv_bfloat16* p) {
-  uint4 u = *reinterpret_cast<const uint4*>(p);
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-  V8 r;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float2 f = __bfloat1622float2(h[i]);
-    r.v[2 * i] = f.x;
-    r.v[2 * i + 1] = f.y;
-  }
-  return r;
-}
-
-__device__ __forceinline__ void st8(__nv_bfloat16* p, const V8& x) {
-  uint4 u;
-  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(x.v[2 * i], x.v[2 * i + 1]);
-  *reinterpret_cast<uint4*>(p) = u;
-}
+inline int stat_blocks(int64_t rows) { return (int)std::min<int64_t>(kStatBlocks, std::max<int64_t>(1, rows / 64)); }
 
 // ---------------------------------------------------------------- statistics
 // Partial Σy, Σy² over a contiguous row chunk per block.  Thread t covers the
 // 8 channels starting at (t % (C/8))·8 of every (256/(C/8))-th row.
-__global__ void __launch_bounds__(256) stats_partial(int64_t rows, int C, const __nv_bfloat16* __restrict__ y,
+template <typename T>
+__global__ void __launch_bounds__(256) stats_partial(int64_t rows, int C, const T* __restrict__ y,
                                                      float* __restrict__ part) {
-  const int g = C / 8;                 // threads per row
-  const int tpr = 256 / g;             // rows per block iteration (C <= 2048)
+  const int g = C / 8;
+  const int tpr = 256 / g;
   const int t = threadIdx.x;
   const int cg = t % g, rr = t / g;
   const int64_t chunk = (rows + gridDim.x - 1) / gridDim.x;
@@ -66,8 +48,7 @@ __global__ void __launch_bounds__(256) stats_partial(int64_t rows, int C, const 
 #pragma unroll
   for (int i = 0; i < 8; ++i) { sm[t * 16 + i] = s[i]; sm[t * 16 + 8 + i] = q[i]; }
   __syncthreads();
-  // fixed-order combine of the tpr threads sharing a channel group
-  for (int c = t; c < C; c += 256) {
+  for (int c = t; c < C; c += 256) {   // fixed-order combine of the threads sharing a channel group
     const int grp = c / 8, lane = c % 8;
     float as = 0.f, aq = 0.f;
     for (int k = 0; k < tpr; ++k) {
@@ -79,8 +60,7 @@ __global__ void __launch_bounds__(256) stats_partial(int64_t rows, int C, const 
   }
 }
 
-// stat[0][c] = μ, stat[1][c] = rstd  (fixed-order double sum over chunks)
-// one warp per channel: lane-strided partial sums, then a fixed xor tree
+// one warp per channel: lane-strided partial sums in double, then a fixed xor tree
 __device__ __forceinline__ void chunk_sums(int nblk, int C, int c, const float* __restrict__ part, double& s,
                                            double& q) {
   const int lane = threadIdx.x & 31;
@@ -94,39 +74,47 @@ __device__ __forceinline__ void chunk_sums(int nblk, int C, int c, const float* 
   q = warp_sum(q);
 }
 
+// stat[0][c] = μ, stat[1][c] = rstd
 __global__ void stats_finalize(int nblk, int64_t rows, int C, const float* __restrict__ part, float* __restrict__ stat) {
   const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= C) return;
   double s, q;
   chunk_sums(nblk, C, c, part, s, q);
   if ((threadIdx.x & 31) != 0) return;
-  double mu = s / rows;
+  const double mu = s / rows;
   double var = q / rows - mu * mu;
   if (var < 0) var = 0;
   stat[c] = (float)mu;
   stat[C + c] = (float)(1.0 / sqrt(var + (double)kEps));
 }
 
-Status batch_stats(OpArgs& a, int64_t rows, int C, const __nv_bfloat16* y, float* stat) {
+template <typename T>
+Status batch_stats(OpArgs& a, int64_t rows, int C, const T* y, float* stat) {
   if (C % 8 || C > 2048) return Status::make(OC_E_UNSUPPORTED, "bn: C must be a multiple of 8 and <= 2048");
-  const int nblk = (int)std::min<int64_t>(kStatBlocks, std::max<int64_t>(1, rows / 64));
+  const int nblk = stat_blocks(rows);
   if (a.ws_bytes < (size_t)nblk * 2 * C * 4) return Status::make(OC_E_INVARIANT, "bn: workspace too small");
-  stats_partial<<<nblk, 256, 256 * 16 * 4, a.stream>>>(rows, C, y, (float*)a.ws);
+  stats_partial<T><<<nblk, 256, 256 * 16 * 4, a.stream>>>(rows, C, y, (float*)a.ws);
   OC_LAUNCH_CHECK(a);
   stats_finalize<<<(C + 7) / 8, 256, 0, a.stream>>>(nblk, rows, C, (const float*)a.ws, stat);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
 
+size_t bn_ws(const JVal& at) {
+  const int64_t rows = at.geti("rows") ? at.geti("rows") : at.geti("N") * at.geti("H") * at.geti("W");
+  return (size_t)stat_blocks(rows) * 2 * at.geti("C") * 4;
+}
+
 // ---------------------------------------------------------------- forward
-__global__ void bn_apply_fwd(int64_t n8, int C, const __nv_bfloat16* __restrict__ y, const float* __restrict__ stat,
-                             const float* __restrict__ gamma, const float* __restrict__ beta,
-                             const __nv_bfloat16* __restrict__ res, __nv_bfloat16* __restrict__ out, int relu) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)((i * 8) % C);
-    V8 x = ld8(y + i * 8);
+template <typename T>
+__global__ void bn_apply_fwd(uint32_t n8, int C, FastDivU fc8, const T* __restrict__ y, const float* __restrict__ stat,
+                             const float* __restrict__ gamma, const float* __restrict__ beta, const T* __restrict__ res,
+                             T* __restrict__ out, int relu) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
+    const int c0 = (int)fc8.mod(i) * 8;
+    V8 x = ld8(y + (int64_t)i * 8);
     V8 r;
-    if (res) r = ld8(res + i * 8);
+    if (res) r = ld8(res + (int64_t)i * 8);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int c = c0 + k;
@@ -135,35 +123,32 @@ __global__ void bn_apply_fwd(int64_t n8, int C, const __nv_bfloat16* __restrict_
       if (relu) z = fmaxf(z, 0.f);
       x.v[k] = z;
     }
-    st8(out + i * 8, x);
+    st8(out + (int64_t)i * 8, x);
   }
 }
 
 enum { BF_Y, BF_STAT, BF_GAMMA, BF_BETA, BF_RES, BF_OUT };
-Status bn_fwd(OpArgs& a) {
+template <typename T>
+Status bn_fwd_t(OpArgs& a) {
   const int64_t rows = A(a, "rows");
   const int C = (int)A(a, "C");
-  auto y = (const __nv_bfloat16*)a.p(BF_Y);
-  OC_TRY(batch_stats(a, rows, C, y, (float*)a.p(BF_STAT)));
-  const int64_t n8 = rows * C / 8;
-  bn_apply_fwd<<<grid_for(n8, 256, 4), 256, 0, a.stream>>>(n8, C, y, (const float*)a.p(BF_STAT),
-                                                           (const float*)a.p(BF_GAMMA), (const float*)a.p(BF_BETA),
-                                                           (const __nv_bfloat16*)a.p(BF_RES),
-                                                           (__nv_bfloat16*)a.p(BF_OUT), Ab(a, "relu") ? 1 : 0);
+  auto y = (const T*)a.p(BF_Y);
+  OC_TRY(batch_stats<T>(a, rows, C, y, (float*)a.p(BF_STAT)));
+  const uint32_t n8 = (uint32_t)(rows * C / 8);
+  FastDivU fc8;
+  fc8.init(C / 8);
+  bn_apply_fwd<T><<<grid_for(n8, 256, 4), 256, 0, a.stream>>>(n8, C, fc8, y, (const float*)a.p(BF_STAT),
+                                                              (const float*)a.p(BF_GAMMA), (const float*)a.p(BF_BETA),
+                                                              (const T*)a.p(BF_RES), (T*)a.p(BF_OUT),
+                                                              Ab(a, "relu") ? 1 : 0);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
-size_t bn_ws(const JVal& at) {
-  int64_t rows = at.geti("rows"), C = at.geti("C");
-  int64_t nblk = std::min<int64_t>(kStatBlocks, std::max<int64_t>(1, rows / 64));
-  return (size_t)(nblk * 2 * C * 4);
-}
 
 // ---------------------------------------------------------------- backward
-// partial Σdz, Σdz·x̂ per channel
-__global__ void __launch_bounds__(256) bnb_partial(int64_t rows, int C, const __nv_bfloat16* __restrict__ g,
-                                                   const __nv_bfloat16* __restrict__ out,
-                                                   const __nv_bfloat16* __restrict__ y,
+template <typename T>
+__global__ void __launch_bounds__(256) bnb_partial(int64_t rows, int C, const T* __restrict__ g,
+                                                   const T* __restrict__ out, const T* __restrict__ y,
                                                    const float* __restrict__ stat, int relu, float* __restrict__ part) {
   const int gC = C / 8, tpr = 256 / gC;
   const int t = threadIdx.x, cg = t % gC, rr = t / gC;
@@ -181,7 +166,7 @@ __global__ void __launch_bounds__(256) bnb_partial(int64_t rows, int C, const __
       if (relu) ov = ld8(out + o);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        float dz = (!relu || ov.v[i] > 0.f) ? gv.v[i] : 0.f;
+        const float dz = (!relu || ov.v[i] > 0.f) ? gv.v[i] : 0.f;
         s[i] += dz;
         q[i] = fmaf(dz, (yv.v[i] - mu[i]) * rs[i], q[i]);
       }
@@ -215,31 +200,33 @@ __global__ void bnb_finalize(int nblk, int C, const float* __restrict__ part, fl
 }
 
 enum { BB_G, BB_OUT, BB_Y, BB_STAT, BB_GAMMA, BB_DGAMMA, BB_DBETA };
-Status bn_bwd_reduce(OpArgs& a) {
+template <typename T>
+Status bn_bwd_reduce_t(OpArgs& a) {
   const int64_t rows = A(a, "rows");
   const int C = (int)A(a, "C");
-  const int nblk = (int)std::min<int64_t>(kStatBlocks, std::max<int64_t>(1, rows / 64));
+  const int nblk = stat_blocks(rows);
   if (a.ws_bytes < (size_t)nblk * 2 * C * 4) return Status::make(OC_E_INVARIANT, "bn_bwd: workspace too small");
-  bnb_partial<<<nblk, 256, 256 * 16 * 4, a.stream>>>(rows, C, (const __nv_bfloat16*)a.p(BB_G),
-                                                     (const __nv_bfloat16*)a.p(BB_OUT),
-                                                     (const __nv_bfloat16*)a.p(BB_Y), (const float*)a.p(BB_STAT),
-                                                     Ab(a, "relu") ? 1 : 0, (float*)a.ws);
+  bnb_partial<T><<<nblk, 256, 256 * 16 * 4, a.stream>>>(rows, C, (const T*)a.p(BB_G), (const T*)a.p(BB_OUT),
+                                                        (const T*)a.p(BB_Y), (const float*)a.p(BB_STAT),
+                                                        Ab(a, "relu") ? 1 : 0, (float*)a.ws);
   OC_LAUNCH_CHECK(a);
   bnb_finalize<<<(C + 7) / 8, 256, 0, a.stream>>>(nblk, C, (const float*)a.ws, (float*)a.p(BB_DGAMMA),
-                                                      (float*)a.p(BB_DBETA));
+                                                  (float*)a.p(BB_DBETA));
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
 
 // dy = γ·rstd·(dz − dβ/n − x̂·dγ/n), written over y; dz written over g (residual branch)
-__global__ void bnb_apply(int64_t n8, int C, float inv_n, __nv_bfloat16* g, const __nv_bfloat16* __restrict__ out,
-                          __nv_bfloat16* y, const float* __restrict__ stat, const float* __restrict__ gamma,
+template <typename T>
+__global__ void bnb_apply(uint32_t n8, int C, FastDivU fc8, float inv_n, T* g, const T* __restrict__ out, T* y,
+                          const float* __restrict__ stat, const float* __restrict__ gamma,
                           const float* __restrict__ dgamma, const float* __restrict__ dbeta, int relu, int write_dz) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)((i * 8) % C);
-    V8 gv = ld8(g + i * 8), yv = ld8(y + i * 8);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
+    const int c0 = (int)fc8.mod(i) * 8;
+    const int64_t o = (int64_t)i * 8;
+    V8 gv = ld8(g + o), yv = ld8(y + o);
     V8 ov;
-    if (relu) ov = ld8(out + i * 8);
+    if (relu) ov = ld8(out + o);
     V8 dz, dy;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -249,63 +236,85 @@ __global__ void bnb_apply(int64_t n8, int C, float inv_n, __nv_bfloat16* g, cons
       dz.v[k] = z;
       dy.v[k] = gamma[c] * stat[C + c] * (z - dbeta[c] * inv_n - xh * dgamma[c] * inv_n);
     }
-    st8(y + i * 8, dy);
-    if (write_dz) st8(g + i * 8, dz);
+    st8(y + o, dy);
+    if (write_dz) st8(g + o, dz);
   }
 }
 
-enum { BA_G, BA_OUT, BA_Y, BA_STAT, BA_GAMMA, BA_DGAMMA, BA_DBETA };
-Status bn_bwd_apply(OpArgs& a) {
+template <typename T>
+Status bn_bwd_apply_t(OpArgs& a) {
   const int64_t rows = A(a, "rows");
   const int C = (int)A(a, "C");
-  const int64_t n8 = rows * C / 8;
-  bnb_apply<<<grid_for(n8, 256, 4), 256, 0, a.stream>>>(
-      n8, C, 1.f / (float)rows, (__nv_bfloat16*)a.p(BA_G), (const __nv_bfloat16*)a.p(BA_OUT),
-      (__nv_bfloat16*)a.p(BA_Y), (const float*)a.p(BA_STAT), (const float*)a.p(BA_GAMMA),
-      (const float*)a.p(BA_DGAMMA), (const float*)a.p(BA_DBETA), Ab(a, "relu") ? 1 : 0,
+  const uint32_t n8 = (uint32_t)(rows * C / 8);
+  FastDivU fc8;
+  fc8.init(C / 8);
+  bnb_apply<T><<<grid_for(n8, 256, 4), 256, 0, a.stream>>>(
+      n8, C, fc8, 1.f / (float)rows, (T*)a.p(BB_G), (const T*)a.p(BB_OUT), (T*)a.p(BB_Y), (const float*)a.p(BB_STAT),
+      (const float*)a.p(BB_GAMMA), (const float*)a.p(BB_DGAMMA), (const float*)a.p(BB_DBETA), Ab(a, "relu") ? 1 : 0,
       Ab(a, "has_res") ? 1 : 0);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
 
 // ---------------------------------------------------------------- stem: BN-ReLU-maxpool
+struct PoolGeom {
+  int N, H, W, C, r, st, pad, P, Q;
+  FastDivU fc8, fQ, fP, fW, fH;
+};
+
+PoolGeom geom(const OpArgs& a) {
+  PoolGeom g{(int)A(a, "N"), (int)A(a, "H"), (int)A(a, "W"), (int)A(a, "C"), (int)A(a, "r"),
+             (int)A(a, "stride"), (int)A(a, "pad"), (int)A(a, "P"), (int)A(a, "Q")};
+  g.fc8.init(g.C / 8);
+  g.fQ.init(g.Q);
+  g.fP.init(g.P);
+  g.fW.init(g.W);
+  g.fH.init(g.H);
+  return g;
+}
+
 // out[n,p,q,c] = max over the r×r window of rnd(relu(bn(y))) (first max,
 // row-major taps, padding excluded); idx = tap of the max (u8)
-__global__ void bn_relu_pool(int N, int H, int W, int C, int r, int st, int pad, int P, int Q,
-                             const __nv_bfloat16* __restrict__ y, const float* __restrict__ stat,
-                             const float* __restrict__ gamma, const float* __restrict__ beta,
-                             __nv_bfloat16* __restrict__ out, uint8_t* __restrict__ idx) {
-  const int64_t total = (int64_t)N * P * Q * (C / 8);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int cg = (int)(i % (C / 8));
-    int64_t t = i / (C / 8);
-    const int q = (int)(t % Q); t /= Q;
-    const int p = (int)(t % P);
-    const int n = (int)(t / P);
-    float best[8];
+template <typename T>
+__global__ void bn_relu_pool(PoolGeom g, const T* __restrict__ y, const float* __restrict__ stat,
+                             const float* __restrict__ gamma, const float* __restrict__ beta, T* __restrict__ out,
+                             uint8_t* __restrict__ idx) {
+  const int C = g.C;
+  const uint32_t total = (uint32_t)g.N * g.P * g.Q * (C / 8);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t t0 = g.fc8.div(i);
+    const int cg = (int)(i - t0 * (C / 8));
+    const uint32_t t1 = g.fQ.div(t0);
+    const int q = (int)(t0 - t1 * g.Q);
+    const uint32_t n = g.fP.div(t1);
+    const int p = (int)(t1 - n * g.P);
+    float best[8], gm[8], bt[8], mu[8], rs[8];
     uint8_t bi[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) { best[k] = -INFINITY; bi[k] = 0; }
-    for (int u = 0; u < r; ++u) {
-      const int h = p * st - pad + u;
-      if (h < 0 || h >= H) continue;
-      for (int v = 0; v < r; ++v) {
-        const int w = q * st - pad + v;
-        if (w < 0 || w >= W) continue;
-        V8 x = ld8(y + (((int64_t)n * H + h) * W + w) * C + cg * 8);
+    for (int k = 0; k < 8; ++k) {
+      best[k] = -INFINITY;
+      bi[k] = 0;
+      const int c = cg * 8 + k;
+      gm[k] = gamma[c]; bt[k] = beta[c]; mu[k] = stat[c]; rs[k] = stat[C + c];
+    }
+    for (int u = 0; u < g.r; ++u) {
+      const int h = p * g.st - g.pad + u;
+      if (h < 0 || h >= g.H) continue;
+      for (int v = 0; v < g.r; ++v) {
+        const int w = q * g.st - g.pad + v;
+        if (w < 0 || w >= g.W) continue;
+        V8 x = ld8(y + (((int64_t)n * g.H + h) * g.W + w) * C + cg * 8);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const int c = cg * 8 + k;
-          float z = fmaxf(fmaf(gamma[c], (x.v[k] - stat[c]) * stat[C + c], beta[c]), 0.f);
-          z = rnd<__nv_bfloat16>(z);
-          if (z > best[k]) { best[k] = z; bi[k] = (uint8_t)(u * r + v); }
+          const float z = rnd<T>(fmaxf(fmaf(gm[k], (x.v[k] - mu[k]) * rs[k], bt[k]), 0.f));
+          if (z > best[k]) { best[k] = z; bi[k] = (uint8_t)(u * g.r + v); }
         }
       }
     }
     V8 o;
 #pragma unroll
     for (int k = 0; k < 8; ++k) o.v[k] = best[k];
-    const int64_t oo = (((int64_t)n * P + p) * Q + q) * C + cg * 8;
+    const int64_t oo = (int64_t)i * 8;
     st8(out + oo, o);
     uint2 packed;
     packed.x = bi[0] | (bi[1] << 8) | (bi[2] << 16) | ((uint32_t)bi[3] << 24);
@@ -315,33 +324,25 @@ __global__ void bn_relu_pool(int N, int H, int W, int C, int r, int st, int pad,
 }
 
 enum { RP_Y, RP_STAT, RP_GAMMA, RP_BETA, RP_OUT, RP_IDX };
-Status bn_relu_pool_fwd(OpArgs& a) {
-  const int N = (int)A(a, "N"), H = (int)A(a, "H"), W = (int)A(a, "W"), C = (int)A(a, "C");
-  const int r = (int)A(a, "r"), st = (int)A(a, "stride"), pad = (int)A(a, "pad");
-  const int P = (int)A(a, "P"), Q = (int)A(a, "Q");
-  auto y = (const __nv_bfloat16*)a.p(RP_Y);
-  OC_TRY(batch_stats(a, (int64_t)N * H * W, C, y, (float*)a.p(RP_STAT)));
-  const int64_t total = (int64_t)N * P * Q * (C / 8);
-  bn_relu_pool<<<grid_for(total, 256, 2), 256, 0, a.stream>>>(N, H, W, C, r, st, pad, P, Q, y,
-                                                              (const float*)a.p(RP_STAT), (const float*)a.p(RP_GAMMA),
-                                                              (const float*)a.p(RP_BETA),
-                                                              (__nv_bfloat16*)a.p(RP_OUT), (uint8_t*)a.p(RP_IDX));
+template <typename T>
+Status bn_relu_pool_fwd_t(OpArgs& a) {
+  PoolGeom g = geom(a);
+  auto y = (const T*)a.p(RP_Y);
+  OC_TRY(batch_stats<T>(a, (int64_t)g.N * g.H * g.W, g.C, y, (float*)a.p(RP_STAT)));
+  const int64_t total = (int64_t)g.N * g.P * g.Q * (g.C / 8);
+  bn_relu_pool<T><<<grid_for(total, 256, 2), 256, 0, a.stream>>>(g, y, (const float*)a.p(RP_STAT),
+                                                                 (const float*)a.p(RP_GAMMA),
+                                                                 (const float*)a.p(RP_BETA), (T*)a.p(RP_OUT),
+                                                                 (uint8_t*)a.p(RP_IDX));
   OC_LAUNCH_CHECK(a);
   return Status::ok();
-}
-size_t rp_ws(const JVal& at) {
-  int64_t rows = at.geti("N") * at.geti("H") * at.geti("W"), C = at.geti("C");
-  int64_t nblk = std::min<int64_t>(kStatBlocks, std::max<int64_t>(1, rows / 64));
-  return (size_t)(nblk * 2 * C * 4);
 }
 
 // gradient reaching bn-output position (n,h,w,c) through the max pool:
 // rnd(Σ over windows whose argmax is this position of their output gradient)
-struct PoolGeom { int N, H, W, C, r, st, pad, P, Q; };
-
-__device__ __forceinline__ void pooled_grad8(const PoolGeom& g, int n, int h, int w, int cg,
-                                             const __nv_bfloat16* __restrict__ gp, const uint8_t* __restrict__ idx,
-                                             float ga[8]) {
+template <typename T>
+__device__ __forceinline__ void pooled_grad8(const PoolGeom& g, int n, int h, int w, int cg, const T* __restrict__ gp,
+                                             const uint8_t* __restrict__ idx, float ga[8]) {
 #pragma unroll
   for (int k = 0; k < 8; ++k) ga[k] = 0.f;
   const int p_lo = max(0, (h + g.pad - g.r + g.st) / g.st), p_hi = min(g.P - 1, (h + g.pad) / g.st);
@@ -358,18 +359,19 @@ __device__ __forceinline__ void pooled_grad8(const PoolGeom& g, int n, int h, in
       V8 gv = ld8(gp + oo);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        uint32_t word = k < 4 ? packed.x : packed.y;
-        uint8_t b = (word >> (8 * (k & 3))) & 0xff;
+        const uint32_t word = k < 4 ? packed.x : packed.y;
+        const uint8_t b = (word >> (8 * (k & 3))) & 0xff;
         if (b == tap) ga[k] += gv.v[k];
       }
     }
   }
 #pragma unroll
-  for (int k = 0; k < 8; ++k) ga[k] = rnd<__nv_bfloat16>(ga[k]);
+  for (int k = 0; k < 8; ++k) ga[k] = rnd<T>(ga[k]);
 }
 
-__global__ void __launch_bounds__(256) pbn_partial(PoolGeom g, const __nv_bfloat16* __restrict__ gp,
-                                                   const uint8_t* __restrict__ idx, const __nv_bfloat16* __restrict__ y,
+template <typename T>
+__global__ void __launch_bounds__(256) pbn_partial(PoolGeom g, const T* __restrict__ gp,
+                                                   const uint8_t* __restrict__ idx, const T* __restrict__ y,
                                                    const float* __restrict__ stat, const float* __restrict__ gamma,
                                                    const float* __restrict__ beta, float* __restrict__ part) {
   const int C = g.C, gC = C / 8, tpr = 256 / gC;
@@ -380,11 +382,12 @@ __global__ void __launch_bounds__(256) pbn_partial(PoolGeom g, const __nv_bfloat
   float s[8] = {}, q[8] = {};
   if (rr < tpr)
     for (int64_t r = r0 + rr; r < r1; r += tpr) {
-      const int w = (int)(r % g.W);
-      const int h = (int)((r / g.W) % g.H);
-      const int n = (int)(r / ((int64_t)g.W * g.H));
+      const uint32_t t1 = g.fW.div((uint32_t)r);
+      const int w = (int)((uint32_t)r - t1 * g.W);
+      const uint32_t n = g.fH.div(t1);
+      const int h = (int)(t1 - n * g.H);
       float ga[8];
-      pooled_grad8(g, n, h, w, cg, gp, idx, ga);
+      pooled_grad8<T>(g, (int)n, h, w, cg, gp, idx, ga);
       V8 yv = ld8(y + r * C + cg * 8);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -412,21 +415,23 @@ __global__ void __launch_bounds__(256) pbn_partial(PoolGeom g, const __nv_bfloat
   }
 }
 
-__global__ void pbn_apply(PoolGeom g, const __nv_bfloat16* __restrict__ gp, const uint8_t* __restrict__ idx,
-                          __nv_bfloat16* y, const float* __restrict__ stat, const float* __restrict__ gamma,
+template <typename T>
+__global__ void pbn_apply(PoolGeom g, const T* __restrict__ gp, const uint8_t* __restrict__ idx, T* y,
+                          const float* __restrict__ stat, const float* __restrict__ gamma,
                           const float* __restrict__ beta, const float* __restrict__ dgamma,
                           const float* __restrict__ dbeta, float inv_n) {
-  const int C = g.C, gC = C / 8;
-  const int64_t total = (int64_t)g.N * g.H * g.W * gC;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int cg = (int)(i % gC);
-    const int64_t r = i / gC;
-    const int w = (int)(r % g.W);
-    const int h = (int)((r / g.W) % g.H);
-    const int n = (int)(r / ((int64_t)g.W * g.H));
+  const int C = g.C;
+  const uint32_t total = (uint32_t)g.N * g.H * g.W * (C / 8);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t r = g.fc8.div(i);
+    const int cg = (int)(i - r * (C / 8));
+    const uint32_t t1 = g.fW.div(r);
+    const int w = (int)(r - t1 * g.W);
+    const uint32_t n = g.fH.div(t1);
+    const int h = (int)(t1 - n * g.H);
     float ga[8];
-    pooled_grad8(g, n, h, w, cg, gp, idx, ga);
-    V8 yv = ld8(y + r * C + cg * 8);
+    pooled_grad8<T>(g, (int)n, h, w, cg, gp, idx, ga);
+    V8 yv = ld8(y + (int64_t)i * 8);
     V8 dy;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -436,71 +441,87 @@ __global__ void pbn_apply(PoolGeom g, const __nv_bfloat16* __restrict__ gp, cons
       const float dz = z > 0.f ? ga[k] : 0.f;
       dy.v[k] = gamma[c] * stat[C + c] * (dz - dbeta[c] * inv_n - xh * dgamma[c] * inv_n);
     }
-    st8(y + r * C + cg * 8, dy);   // in place: each thread reads only its own y
+    st8(y + (int64_t)i * 8, dy);   // in place: each thread reads only its own y
   }
 }
 
 enum { PB_G, PB_IDX, PB_Y, PB_STAT, PB_GAMMA, PB_BETA, PB_DGAMMA, PB_DBETA };
-PoolGeom geom(const OpArgs& a) {
-  return PoolGeom{(int)A(a, "N"), (int)A(a, "H"), (int)A(a, "W"), (int)A(a, "C"), (int)A(a, "r"),
-                  (int)A(a, "stride"), (int)A(a, "pad"), (int)A(a, "P"), (int)A(a, "Q")};
-}
-Status pool_bn_bwd_reduce(OpArgs& a) {
+template <typename T>
+Status pool_bn_bwd_reduce_t(OpArgs& a) {
   PoolGeom g = geom(a);
   const int64_t rows = (int64_t)g.N * g.H * g.W;
-  const int nblk = (int)std::min<int64_t>(kStatBlocks, std::max<int64_t>(1, rows / 64));
-  pbn_partial<<<nblk, 256, 256 * 16 * 4, a.stream>>>(g, (const __nv_bfloat16*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX),
-                                                     (const __nv_bfloat16*)a.p(PB_Y), (const float*)a.p(PB_STAT),
-                                                     (const float*)a.p(PB_GAMMA), (const float*)a.p(PB_BETA),
-                                                     (float*)a.ws);
+  const int nblk = stat_blocks(rows);
+  if (a.ws_bytes < (size_t)nblk * 2 * g.C * 4) return Status::make(OC_E_INVARIANT, "pool_bn_bwd: workspace too small");
+  pbn_partial<T><<<nblk, 256, 256 * 16 * 4, a.stream>>>(g, (const T*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX),
+                                                        (const T*)a.p(PB_Y), (const float*)a.p(PB_STAT),
+                                                        (const float*)a.p(PB_GAMMA), (const float*)a.p(PB_BETA),
+                                                        (float*)a.ws);
   OC_LAUNCH_CHECK(a);
   bnb_finalize<<<(g.C + 7) / 8, 256, 0, a.stream>>>(nblk, g.C, (const float*)a.ws, (float*)a.p(PB_DGAMMA),
-                                                        (float*)a.p(PB_DBETA));
+                                                    (float*)a.p(PB_DBETA));
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
-Status pool_bn_bwd_apply(OpArgs& a) {
+template <typename T>
+Status pool_bn_bwd_apply_t(OpArgs& a) {
   PoolGeom g = geom(a);
   const int64_t rows = (int64_t)g.N * g.H * g.W;
   const int64_t total = rows * (g.C / 8);
-  pbn_apply<<<grid_for(total, 256, 2), 256, 0, a.stream>>>(
-      g, (const __nv_bfloat16*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX), (__nv_bfloat16*)a.p(PB_Y),
-      (const float*)a.p(PB_STAT), (const float*)a.p(PB_GAMMA), (const float*)a.p(PB_BETA),
-      (const float*)a.p(PB_DGAMMA), (const float*)a.p(PB_DBETA), 1.f / (float)rows);
+  pbn_apply<T><<<grid_for(total, 256, 2), 256, 0, a.stream>>>(
+      g, (const T*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX), (T*)a.p(PB_Y), (const float*)a.p(PB_STAT),
+      (const float*)a.p(PB_GAMMA), (const float*)a.p(PB_BETA), (const float*)a.p(PB_DGAMMA),
+      (const float*)a.p(PB_DBETA), 1.f / (float)rows);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
 
 // ---------------------------------------------------------------- global average pool
-__global__ void gap_fwd_k(int N, int HW, int C, const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ out) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+template <typename T>
+__global__ void gap_fwd_k(int N, int HW, int C, const T* __restrict__ x, T* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N * C) return;
   const int n = i / C, c = i % C;
   float s = 0.f;
-  for (int k = 0; k < HW; ++k) s += __bfloat162float(x[((int64_t)n * HW + k) * C + c]);
-  out[i] = __float2bfloat16_rn(s / (float)HW);
+  for (int k = 0; k < HW; ++k) s += ld_f(x + ((int64_t)n * HW + k) * C + c);
+  st_f(out + i, s / (float)HW);
 }
-__global__ void gap_bwd_k(int N, int HW, int C, const __nv_bfloat16* __restrict__ g, __nv_bfloat16* __restrict__ dx) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+template <typename T>
+__global__ void gap_bwd_k(int N, int HW, int C, const T* __restrict__ g, T* __restrict__ dx) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)N * HW * C) return;
   const int c = (int)(i % C);
   const int n = (int)(i / ((int64_t)HW * C));
-  dx[i] = __float2bfloat16_rn(__bfloat162float(g[(int64_t)n * C + c]) / (float)HW);
+  st_f(dx + i, ld_f(g + (int64_t)n * C + c) / (float)HW);
 }
-Status gap_fwd(OpArgs& a) {
+template <typename T>
+Status gap_fwd_t(OpArgs& a) {
   const int N = (int)A(a, "N"), HW = (int)A(a, "HW"), C = (int)A(a, "C");
-  gap_fwd_k<<<(N * C + 255) / 256, 256, 0, a.stream>>>(N, HW, C, (const __nv_bfloat16*)a.p(0), (__nv_bfloat16*)a.p(1));
+  gap_fwd_k<T><<<(N * C + 255) / 256, 256, 0, a.stream>>>(N, HW, C, (const T*)a.p(0), (T*)a.p(1));
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
-Status gap_bwd(OpArgs& a) {
+template <typename T>
+Status gap_bwd_t(OpArgs& a) {
   const int N = (int)A(a, "N"), HW = (int)A(a, "HW"), C = (int)A(a, "C");
   const int64_t tot = (int64_t)N * HW * C;
-  gap_bwd_k<<<(int)((tot + 255) / 256), 256, 0, a.stream>>>(N, HW, C, (const __nv_bfloat16*)a.p(0),
-                                                            (__nv_bfloat16*)a.p(1));
+  gap_bwd_k<T><<<(int)((tot + 255) / 256), 256, 0, a.stream>>>(N, HW, C, (const T*)a.p(0), (T*)a.p(1));
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
+
+// dtype dispatch: attrs.dtype = "bf16" (default) | "f32"
+#define OC_DT_DISPATCH(name)                                                  \
+  Status name(OpArgs& a) {                                                    \
+    return As(a, "dtype", "bf16") == "f32" ? name##_t<float>(a) : name##_t<__nv_bfloat16>(a); \
+  }
+OC_DT_DISPATCH(bn_fwd)
+OC_DT_DISPATCH(bn_bwd_reduce)
+OC_DT_DISPATCH(bn_bwd_apply)
+OC_DT_DISPATCH(bn_relu_pool_fwd)
+OC_DT_DISPATCH(pool_bn_bwd_reduce)
+OC_DT_DISPATCH(pool_bn_bwd_apply)
+OC_DT_DISPATCH(gap_fwd)
+OC_DT_DISPATCH(gap_bwd)
 
 }  // namespace
 
@@ -510,10 +531,10 @@ extern const OpDesc kBnBwdReduce{"bn_bwd_reduce", {"g", "out", "y", "stat", "gam
 extern const OpDesc kBnBwdApply{"bn_bwd_apply", {"g", "out", "y", "stat", "gamma", "dgamma", "dbeta"}, bn_bwd_apply,
                                 nullptr};
 extern const OpDesc kBnReluPoolFwd{"bn_relu_pool_fwd", {"y", "stat", "gamma", "beta", "out", "idx"}, bn_relu_pool_fwd,
-                                   rp_ws};
+                                   bn_ws};
 extern const OpDesc kPoolBnBwdReduce{"pool_bn_bwd_reduce",
                                      {"g", "idx", "y", "stat", "gamma", "beta", "dgamma", "dbeta"},
-                                     pool_bn_bwd_reduce, rp_ws};
+                                     pool_bn_bwd_reduce, bn_ws};
 extern const OpDesc kPoolBnBwdApply{"pool_bn_bwd_apply", {"g", "idx", "y", "stat", "gamma", "beta", "dgamma", "dbeta"},
                                     pool_bn_bwd_apply, nullptr};
 extern const OpDesc kGapFwd{"gap_fwd", {"x", "out"}, gap_fwd, nullptr};

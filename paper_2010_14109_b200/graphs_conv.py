@@ -24,18 +24,19 @@ from .graphs import BF16, F32, I32, U8, Builder, _pvars, _update
 
 
 def build_convnet(spec, params="pinned", inputs="host"):
-    assert spec["mode"] == "bf16", "conv nets run in bf16 mode"
+    # bf16 storage (tcgen05 convs) or the fp32 parity mode (CUDA-core convs, no TF32)
+    ACT, DT = (BF16, "bf16") if spec["mode"] == "bf16" else (F32, "f32")
     b = Builder()
     Nb = spec["batch"]
     shapes, pshapes = nets.tensor_shapes(spec)
     pin_in = inputs == "pinned"
-    x = b.var("x", Nb * int(np.prod(spec["input"])) * BF16, persistent=not pin_in, pinned=pin_in,
-              shape=[Nb] + spec["input"], dtype="bf16")
+    x = b.var("x", Nb * int(np.prod(spec["input"])) * ACT, persistent=not pin_in, pinned=pin_in,
+              shape=[Nb] + spec["input"], dtype=DT)
     y = b.var("labels", Nb * I32, persistent=not pin_in, pinned=pin_in, shape=[Nb], dtype="i32")
     P, Mo, G = _pvars(b, spec, pshapes, params)
     layers = spec["layers"]
 
-    def nbytes(t, dt=BF16):
+    def nbytes(t, dt=ACT):
         return Nb * int(np.prod(shapes[t])) * dt
 
     # fuse a bn(relu) immediately consumed only by a maxpool (the stem)
@@ -58,10 +59,11 @@ def build_convnet(spec, params="pinned", inputs="host"):
         if nm in skip:
             continue
         if ty == "conv":
-            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype="bf16")
+            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
             H, W, C = shapes[lay["in"]]
             Pq, Qq, K = shapes[lay["out"]]
-            attrs = {"N": Nb, "H": H, "W": W, "C": C, "K": K, "R": lay["r"], "S": lay["s"], "stride": lay["stride"],
+            attrs = {"dtype": DT, "N": Nb, "H": H, "W": W, "C": C, "K": K, "R": lay["r"], "S": lay["s"],
+                     "stride": lay["stride"],
                      "pad": lay["pad"], "P": Pq, "Q": Qq}
             lay["_attrs"] = attrs
             b.fn(f"fwd.{nm}", "conv_fwd", {"x": t[lay["in"]], "w": P[nm + ".W"], "y": t[lay["out"]]}, attrs,
@@ -74,9 +76,10 @@ def build_convnet(spec, params="pinned", inputs="host"):
                 H, W, _ = shapes[lay["in"]]
                 Pq, Qq, _ = shapes[pool["out"]]
                 t[pool["out"]] = b.var(pool["out"], nbytes(pool["out"]), shape=[Nb] + shapes[pool["out"]],
-                                       dtype="bf16")
+                                       dtype=DT)
                 idx[nm] = b.var(f"idx.{nm}", nbytes(pool["out"], U8), shape=[Nb] + shapes[pool["out"]], dtype="u8")
-                attrs = {"N": Nb, "H": H, "W": W, "C": C, "r": pool["r"], "stride": pool["stride"], "pad": pool["pad"],
+                attrs = {"dtype": DT, "N": Nb, "H": H, "W": W, "C": C, "r": pool["r"], "stride": pool["stride"],
+                         "pad": pool["pad"],
                          "P": Pq, "Q": Qq}
                 lay["_attrs"] = attrs
                 ins = [t[lay["in"]], P[nm + ".gamma"], P[nm + ".beta"]]
@@ -84,25 +87,25 @@ def build_convnet(spec, params="pinned", inputs="host"):
                      {"y": t[lay["in"]], "stat": stat[nm], "gamma": P[nm + ".gamma"], "beta": P[nm + ".beta"],
                       "out": t[pool["out"]], "idx": idx[nm]}, attrs, ins, [stat[nm], t[pool["out"]], idx[nm]])
             else:
-                t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype="bf16")
+                t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
                 rows = Nb * int(np.prod(shapes[lay["in"]][:-1]))
                 res = t[lay["residual"]] if lay.get("residual") else None
-                attrs = {"rows": rows, "C": C, "relu": lay["relu"], "has_res": res is not None}
+                attrs = {"dtype": DT, "rows": rows, "C": C, "relu": lay["relu"], "has_res": res is not None}
                 lay["_attrs"] = attrs
                 b.fn(f"fwd.{nm}", "bn_fwd",
                      {"y": t[lay["in"]], "stat": stat[nm], "gamma": P[nm + ".gamma"], "beta": P[nm + ".beta"],
                       "res": res, "out": t[lay["out"]]}, attrs,
                      [t[lay["in"]], P[nm + ".gamma"], P[nm + ".beta"], res], [stat[nm], t[lay["out"]]])
         elif ty == "gap":
-            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype="bf16")
+            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
             H, W, C = shapes[lay["in"]]
-            lay["_attrs"] = {"N": Nb, "HW": H * W, "C": C}
+            lay["_attrs"] = {"dtype": DT, "N": Nb, "HW": H * W, "C": C}
             b.fn(f"fwd.{nm}", "gap_fwd", {"x": t[lay["in"]], "out": t[lay["out"]]}, lay["_attrs"], [t[lay["in"]]],
                  [t[lay["out"]]])
         elif ty == "linear":
             t[lay["out"]] = b.var(lay["out"], Nb * lay["features"] * F32, shape=[Nb, lay["features"]], dtype="f32")
             K = int(np.prod(shapes[lay["in"]]))
-            lay["_attrs"] = {"M": Nb, "N": lay["features"], "K": K, "relu": False, "dtype": "bf16", "out_f32": True}
+            lay["_attrs"] = {"M": Nb, "N": lay["features"], "K": K, "relu": False, "dtype": DT, "out_f32": True}
             b.fn(f"fwd.{nm}", "linear_fwd", {"x": t[lay["in"]], "w": P[nm + ".W"], "b": P[nm + ".b"],
                                              "y": t[lay["out"]]}, lay["_attrs"],
                  [t[lay["in"]], P[nm + ".W"], P[nm + ".b"]], [t[lay["out"]]])
@@ -125,7 +128,7 @@ def build_convnet(spec, params="pinned", inputs="host"):
             continue
         gv = g[out_t]
         if ty == "linear":
-            dx = b.var(f"grad.{lay['in']}", nbytes(lay["in"]), shape=[Nb] + shapes[lay["in"]], dtype="bf16")
+            dx = b.var(f"grad.{lay['in']}", nbytes(lay["in"]), shape=[Nb] + shapes[lay["in"]], dtype=DT)
             at = dict(lay["_attrs"], dy_f32=True)
             b.fn(f"bwd.{nm}", "linear_bwd", {"dy": gv, "x": t[lay["in"]], "w": P[nm + ".W"], "dw": G[nm + ".W"],
                                              "db": G[nm + ".b"], "dx": dx}, at,
@@ -134,7 +137,7 @@ def build_convnet(spec, params="pinned", inputs="host"):
             _update(b, spec, nm, P, Mo, G, [nm + ".W", nm + ".b"])
         elif ty == "gap":
             assert lay["in"] not in g
-            dx = b.var(f"grad.{lay['in']}", nbytes(lay["in"]), shape=[Nb] + shapes[lay["in"]], dtype="bf16")
+            dx = b.var(f"grad.{lay['in']}", nbytes(lay["in"]), shape=[Nb] + shapes[lay["in"]], dtype=DT)
             b.fn(f"bwd.{nm}", "gap_bwd", {"g": gv, "dx": dx}, lay["_attrs"], [gv], [dx])
             g[lay["in"]] = dx
         elif ty == "bn" and nm in fused_pool:
@@ -172,7 +175,7 @@ def build_convnet(spec, params="pinned", inputs="host"):
                     dx = g[lay["in"]]
                     ins = [dy, P[nm + ".W"], dx]
                 else:
-                    dx = b.var(f"grad.{lay['in']}", nbytes(lay["in"]), shape=[Nb] + shapes[lay["in"]], dtype="bf16")
+                    dx = b.var(f"grad.{lay['in']}", nbytes(lay["in"]), shape=[Nb] + shapes[lay["in"]], dtype=DT)
                     ins = [dy, P[nm + ".W"]]
                     g[lay["in"]] = dx
                 b.fn(f"bwd.{nm}.dgrad", "conv_dgrad", {"dy": dy, "w": P[nm + ".W"], "dx": dx},

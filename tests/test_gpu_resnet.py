@@ -34,12 +34,12 @@ def test_resnet18_config_feasible_at_quarter_footprint():
     assert st["peak_sched"] <= budget and st["bytes_d2h"] > 0
 
 
-def run_step(spec, doc, info, budget, window, mode, phys, chunk=2 * MiB, steps=1, timeline=False):
+def run_step(spec, doc, info, budget, window, mode, phys, chunk=2 * MiB, steps=1, timeline=False, fp32_input=False):
     from paper_2010_14109_b200.runtime import OutOfCoreStep
     st = OutOfCoreStep(doc, budget, window, mode=mode, chunk_bytes=chunk, phys_bytes=phys, timeline=timeline)
     x, y = nets.make_inputs(spec)
     p = nets.make_params(spec)
-    st.write(info["x"], to_bf16_bits(x))
+    st.write(info["x"], x.astype(np.float32) if fp32_input else to_bf16_bits(x))
     st.write(info["labels"], y)
     for k, v in p.items():
         st.write(info["params"][k], v)
@@ -55,11 +55,13 @@ def run_step(spec, doc, info, budget, window, mode, phys, chunk=2 * MiB, steps=1
 
 
 @pytest.mark.gpu
-def test_resnet18_full_resolution_parity():
-    """The full ResNet-18 graph at 224x224 (batch 2 so the oracle finishes in
-    seconds; every conv spans many tiles with ragged tails) under a 25%
-    budget, VA allocator: every parameter gradient within 1e-3 of the oracle."""
-    spec = nets.resnet(18, batch=2)
+@pytest.mark.parametrize("mode", ["va", "best"])
+def test_resnet18_full_resolution_parity_fp32(mode):
+    """The full ResNet-18 graph at 224x224 in the fp32 parity mode (batch 2 so
+    the oracle finishes in seconds; every conv spans many tiles with ragged
+    tails) under a 25% budget: loss and every parameter gradient within 1e-5
+    relative L2 of the oracle (north_star fp32 tolerance)."""
+    spec = nets.resnet(18, batch=2, mode="fp32")
     doc, info = graphs.build(spec, params="persistent")
     G = B.Graph(doc)
     peak = G.in_core_peak()
@@ -67,12 +69,32 @@ def test_resnet18_full_resolution_parity():
     x, y = nets.make_inputs(spec)
     p = nets.make_params(spec)
     ref = nm.train_step(spec, p, x, y)
-    out = run_step(spec, doc, info, budget, B.OC_WINDOW_MAX_FEASIBLE, "va", 512 * MiB)
+    out = run_step(spec, doc, info, budget, B.OC_WINDOW_MAX_FEASIBLE, mode, 1024 * MiB, fp32_input=True)
     assert out["metrics"]["bytes_d2h"] > 0
-    assert abs(out["loss"] - ref["loss"]) <= 1e-3 * abs(ref["loss"])
+    assert abs(out["loss"] - ref["loss"]) <= 1e-5 * abs(ref["loss"])
     errs = {k: nm.rel_l2(out["m." + k], ref["grads"][k]) for k in p}
     worst = max(errs, key=errs.get)
-    assert errs[worst] <= 1e-3, (worst, errs[worst])
+    assert errs[worst] <= 1e-5, (worst, errs[worst])
+
+
+@pytest.mark.gpu
+def test_resnet18_full_resolution_bf16_loss():
+    """bf16 mode at full depth: the loss agrees with the oracle to 1e-3.
+    Per-gradient 1e-3 parity is ill-posed at this depth in bf16 — the
+    oracle's own gradients move by >10% under 1e-6 perturbations of one conv
+    output (test_bf16_deep_net_gradients_are_chaotic); it is checked on the
+    shallow net (test_tiny_resnet_parity_and_transparency), per kernel
+    (test_gpu_conv.py, test_gpu_ops.py) and at full depth in fp32."""
+    spec = nets.resnet(18, batch=2)
+    doc, info = graphs.build(spec, params="persistent")
+    G = B.Graph(doc)
+    peak = G.in_core_peak()
+    x, y = nets.make_inputs(spec)
+    p = nets.make_params(spec)
+    ref = nm.train_step(spec, p, x, y)
+    out = run_step(spec, doc, info, max(G.min_feasible_budget(0), peak // 4), B.OC_WINDOW_MAX_FEASIBLE, "va",
+                   512 * MiB)
+    assert abs(out["loss"] - ref["loss"]) <= 1e-3 * abs(ref["loss"])
 
 
 @pytest.mark.gpu
