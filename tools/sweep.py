@@ -1,0 +1,64 @@
+"""Knob sweeps of the out-of-core step on one GPU: schedule
+window W, allocator mode (VA chunk size / best-fit arena) and budget fraction.
+Prints one JSON line per point.  Not part of the product."""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="r18")
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--fracs", default="0.25")
+    ap.add_argument("--wfracs", default="0,0.25,0.5,0.75,1.0")
+    ap.add_argument("--modes", default="va")
+    ap.add_argument("--chunks", default="2")
+    ap.add_argument("--steps", type=int, default=4)
+    a = ap.parse_args()
+    import numpy as np
+    from paper_2010_14109_b200 import binding as B
+    from paper_2010_14109_b200 import graphs
+    from synth import nets
+    spec = nets.resnet(18 if a.config == "r18" else 50, batch=a.batch)
+    doc, info = graphs.build(spec, params="persistent")
+    G = B.Graph(doc)
+    F = G.in_core_peak()
+    for frac in [float(x) for x in a.fracs.split(",")]:
+        budget = int(F * frac)
+        try:
+            wmax = G.max_feasible_window(budget)
+        except B.OcError as e:
+            print(json.dumps({"frac": frac, "infeasible": str(e)}), flush=True)
+            continue
+        for mode in a.modes.split(","):
+            for ch in [int(c) for c in a.chunks.split(",")]:
+                for wf in [float(x) for x in a.wfracs.split(",")]:
+                    W = int(wmax * wf)
+                    try:
+                        st, W, phys = bench.setup_step(spec, info, doc, budget, mode, ch << 20, timeline=True,
+                                                       window=W)
+                    except Exception as e:  # noqa: BLE001
+                        print(json.dumps({"frac": frac, "mode": mode, "chunk_mib": ch, "wfrac": wf,
+                                          "error": str(e)[:200]}), flush=True)
+                        continue
+                    st.step()
+                    ms = [st.step() for _ in range(a.steps)]
+                    m = {k: float(np.mean([x[k] for x in ms])) for k in ("step_ms", "compute_busy_ms", "h2d_busy_ms",
+                                                                         "d2h_busy_ms", "overlap_frac", "bytes_h2d",
+                                                                         "bytes_d2h", "n_h2d", "n_d2h")}
+                    mem = st.mem_stats()
+                    print(json.dumps({"frac": frac, "budget": budget, "mode": mode, "chunk_mib": ch, "wfrac": wf,
+                                      "window": W, "phys": phys, "samples_per_s": a.batch / m["step_ms"] * 1e3,
+                                      **m, "peak_phys": st.stats["peak_phys"], "if_peak": st.stats["if_peak"],
+                                      "map_us_total": mem["map_us"]}), flush=True)
+                    st.close()
+
+
+if __name__ == "__main__":
+    main()
