@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--budget-frac", type=float, default=0.25)
     ap.add_argument("--chunk-mib", type=int, default=2)
     ap.add_argument("--no-incore", action="store_true")
+    ap.add_argument("--window", default="auto", help="auto | max | <bytes>")
     return ap.parse_args()
 
 
@@ -124,7 +125,7 @@ def trainable_batch(spec_fn, budget, lo=1, hi=4096, params="persistent"):
     return lo
 
 
-def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None):
+def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None, pack=64 << 10):
     import torch
     from paper_2010_14109_b200 import binding as B
     from paper_2010_14109_b200.runtime import OutOfCoreStep
@@ -136,7 +137,8 @@ def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None)
                    phys_bytes=budget * 4, allow_oom=True)
     ps = probe.stats()
     phys = ps["peak_phys"] + chunk if mode == "va" else max(ps["peak_phys"], 1)
-    st = OutOfCoreStep(doc, budget, W, mode=mode, chunk_bytes=chunk, phys_bytes=phys, timeline=timeline)
+    st = OutOfCoreStep(doc, budget, W, mode=mode, chunk_bytes=chunk, phys_bytes=phys, timeline=timeline,
+                       pack_threshold=pack)
     x, y = nets.make_inputs(spec)
     p = nets.make_params(spec)
     if spec["mode"] == "bf16":
@@ -183,7 +185,31 @@ def run_ours(args, rank, world):
     G = B.Graph(doc)
     F_peak = G.in_core_peak()
     budget = cfg.get("budget") or int(F_peak * args.budget_frac)
-    st, W, phys = setup_step(spec, info, doc, budget, args.mode, chunk)
+    # schedule-window: the paper's single hyperparameter, "decided experimentally"
+    # (P:120-style); auto = best of a few fractions of the largest feasible W
+    wmax = G.max_feasible_window(budget)
+    window_probe = []
+    if args.window == "auto":
+        best = None
+        for wf in (0.0, 0.25, 0.5, 1.0):
+            Wc = int(wmax * wf)
+            stc, _, _ = setup_step(spec, info, doc, budget, args.mode, chunk, timeline=False, window=Wc)
+            stc.step()
+            ms = float(np.mean([stc.step()["step_ms"] for _ in range(2)]))
+            stc.close()
+            window_probe.append({"window": Wc, "ms": ms})
+            if best is None or ms < best[1]:
+                best = (Wc, ms)
+        W_sel = best[0]
+    elif args.window == "max":
+        W_sel = wmax
+    else:
+        W_sel = int(args.window)
+    if world > 1:   # every replica runs the identical schedule
+        sel = [W_sel]
+        dist.broadcast_object_list(sel, src=0)
+        W_sel = sel[0]
+    st, W, phys = setup_step(spec, info, doc, budget, args.mode, chunk, window=W_sel)
     if world > 1:
         uid = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -294,7 +320,8 @@ def run_ours(args, rank, world):
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16" if spec["mode"] == "bf16" else "f32", "data": "synthetic (seeded N(0,1) images, U labels)",
         "config": dict(cfg, global_batch=B_glob, per_gpu_batch=spec["batch"], budget_bytes=budget,
-                       in_core_footprint_bytes=F_peak, window_bytes=W, allocator=args.mode, chunk_bytes=chunk,
+                       in_core_footprint_bytes=F_peak, window_bytes=W, window_max_feasible=wmax,
+                       window_selection=window_probe or args.window, allocator=args.mode, chunk_bytes=chunk,
                        phys_pool_bytes=phys, parallelism=f"dp{world}",
                        l2_flush="inputs larger than L2 (activations GBs per step)"),
         "clocks": clk.summary(),

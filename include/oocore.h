@@ -272,7 +272,10 @@ typedef struct oc_exec_options {
   uint32_t timeline;       /* 1: record CUDA events around every function and transfer */
   uint32_t elide_clean;    /* 1: skip D2H of variables whose host copy is valid (Z19) */
   uint32_t check;          /* 1: verify residency on the host while issuing (debug) */
-  uint32_t reserved;
+  uint32_t pack_threshold; /* bytes; swaps of variables up to this size are grouped per
+                              function into one SM-driven pack/unpack kernel that
+                              copies 16-byte vectors between device memory and the
+                              mapped pinned host copies; 0 = off */
 } oc_exec_options;
 
 typedef struct oc_step_metrics {

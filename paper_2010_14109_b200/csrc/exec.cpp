@@ -25,6 +25,7 @@
 
 #include "mem.hpp"
 #include "ops.hpp"
+#include "pack.hpp"
 
 namespace oc {
 
@@ -49,12 +50,15 @@ struct Slot {
   std::vector<uint32_t> chunks;    // VA mode: chunks from the replay
   std::vector<Ref> waits;          // release points of reused memory
   int32_t host_dep = -1;           // departure whose D2H must land before this H2D
+  bool packed = false;             // moved by the function's unpack kernel (A7)
 };
 
 struct Dep {
   uint32_t fn, var;
   uint8_t dirty;
   int32_t wait_fn;
+  int32_t slot = -1;               // arrival slot holding the variable when it leaves
+  bool packed = false;             // moved by the function's pack kernel (A7)
 };
 
 struct XVar {
@@ -71,6 +75,8 @@ struct XFn {
   std::vector<std::vector<uint32_t>> role_vars;  // per role, variables
   std::vector<int32_t> dep_of_wait;              // parallel to wait_out: departure ids
   std::vector<uint32_t> dep_reserve;             // departure ids reserved after f_i
+  uint32_t pin_off = 0, pin_n = 0;               // unpack entries (small arrivals) in pack_tab
+  uint32_t pout_off = 0, pout_n = 0;             // pack entries (small departures)
 };
 
 struct Interval { double a, b; };
@@ -129,6 +135,7 @@ struct Exec {
   uint64_t host_bytes = 0;
   void* ws = nullptr;
   size_t ws_bytes = 0;
+  PackEntry* pack_tab = nullptr;   // device copy of all pack/unpack entries (static addresses)
   // timeline (opt.timeline)
   std::vector<cudaEvent_t> tl_fn0, tl_fn1, tl_in0, tl_in1, tl_out0, tl_out1;
   std::vector<uint8_t> tl_in_used, tl_out_used;
@@ -191,7 +198,8 @@ Status Exec::create(int dev, const Graph* graph, const Schedule* sch, MemPool* m
       host_bytes += (g->var_bytes[v] + 255) / 256 * 256;
     }
   if (host_bytes) {
-    OC_CUDA(cudaHostAlloc((void**)&host, host_bytes, cudaHostAllocPortable));
+    // mapped: the pack/unpack kernel addresses it directly (UVA: same pointer on the device)
+    OC_CUDA(cudaHostAlloc((void**)&host, host_bytes, cudaHostAllocPortable | cudaHostAllocMapped));
     std::memset(host, 0, host_bytes);
   }
 
@@ -278,8 +286,42 @@ Status Exec::create(int dev, const Graph* graph, const Schedule* sch, MemPool* m
       if (a.kind == ARRIVE_H2D && var_last_dep[a.var] >= 0) sl.host_dep = var_last_dep[a.var];
       var_slot[a.var] = (int32_t)a.slot;
     }
-    for (uint32_t d : fns[i].dep_reserve) var_last_dep[deps[d].var] = (int32_t)d;
+    for (uint32_t d : fns[i].dep_reserve) {
+      var_last_dep[deps[d].var] = (int32_t)d;
+      deps[d].slot = var_slot[deps[d].var];
+    }
     for (uint32_t v : F.free) release(v, Ref{Ref::DONE, i});
+  }
+
+  // pack/unpack tables (A7): static entries per function, addresses fixed per slot
+  if (opt.pack_threshold) {
+    std::vector<PackEntry> tab;
+    for (uint32_t i = 0; i < n; ++i) {
+      XFn& X = fns[i];
+      X.pin_off = (uint32_t)tab.size();
+      for (const Arrival& a : s->fn[i].in) {
+        Slot& sl = slots[a.slot];
+        const XVar& xv = vars[sl.var];
+        if (sl.kind != ARRIVE_H2D || xv.bytes > opt.pack_threshold) continue;
+        sl.packed = true;
+        tab.push_back(PackEntry{(const unsigned char*)(host + xv.host_off), (unsigned char*)sl.addr, xv.bytes});
+      }
+      X.pin_n = (uint32_t)tab.size() - X.pin_off;
+      X.pout_off = (uint32_t)tab.size();
+      for (uint32_t d : X.dep_reserve) {
+        Dep& D = deps[d];
+        const XVar& xv = vars[D.var];
+        if (xv.bytes > opt.pack_threshold || !(D.dirty || !opt.elide_clean)) continue;
+        D.packed = true;
+        tab.push_back(PackEntry{(const unsigned char*)slots[D.slot].addr, (unsigned char*)(host + xv.host_off),
+                                xv.bytes});
+      }
+      X.pout_n = (uint32_t)tab.size() - X.pout_off;
+    }
+    if (!tab.empty()) {
+      OC_CUDA(cudaMalloc((void**)&pack_tab, tab.size() * sizeof(PackEntry)));
+      OC_CUDA(cudaMemcpy(pack_tab, tab.data(), tab.size() * sizeof(PackEntry), cudaMemcpyHostToDevice));
+    }
   }
 
   // ops
@@ -383,10 +425,11 @@ Status Exec::run(oc_step_metrics* out) {
       OC_CUDA(cudaStreamWaitEvent(cs, ev_out[X.dep_of_wait[k]], 0));
       vars[F.wait_out[k]].cur_slot = -1;  // swapped out: no longer resident
     }
-    // (a) arrivals
+    // (a) arrivals; small H2D arrivals go through one unpack kernel (A7)
     for (const Arrival& a : F.in) {
       Slot& sl = slots[a.slot];
       if (s->alloc.mode == OC_ALLOC_VA) OC_TRY(mem->bind(sl.span, sl.chunks));
+      if (sl.packed) continue;
       for (const Ref& r : sl.waits) OC_CUDA(cudaStreamWaitEvent(hs, ev_of(r), 0));
       if (sl.kind == ARRIVE_H2D) {
         if (sl.host_dep >= 0) OC_CUDA(cudaStreamWaitEvent(hs, ev_out[sl.host_dep], 0));
@@ -400,6 +443,29 @@ Status Exec::run(oc_step_metrics* out) {
       OC_CUDA(cudaEventRecord(ev_in[a.slot], hs));
       vars[sl.var].cur_slot = (int32_t)a.slot;
       vars[sl.var].need_wait = true;
+    }
+    if (X.pin_n) {
+      int32_t first = -1;
+      for (const Arrival& a : F.in) {
+        Slot& sl = slots[a.slot];
+        if (!sl.packed) continue;
+        if (first < 0) first = (int32_t)a.slot;
+        for (const Ref& r : sl.waits) OC_CUDA(cudaStreamWaitEvent(hs, ev_of(r), 0));
+        if (sl.host_dep >= 0) OC_CUDA(cudaStreamWaitEvent(hs, ev_out[sl.host_dep], 0));
+        bytes_h2d += vars[sl.var].bytes;
+      }
+      if (opt.timeline) { OC_CUDA(cudaEventRecord(tl_in0[first], hs)); tl_in_used[first] = 1; }
+      OC_TRY(pack_launch(pack_tab + X.pin_off, (int)X.pin_n, hs));
+      if (opt.timeline) OC_CUDA(cudaEventRecord(tl_in1[first], hs));
+      ++n_h2d;
+      ++n_kernels;
+      for (const Arrival& a : F.in) {
+        Slot& sl = slots[a.slot];
+        if (!sl.packed) continue;
+        OC_CUDA(cudaEventRecord(ev_in[a.slot], hs));
+        vars[sl.var].cur_slot = (int32_t)a.slot;
+        vars[sl.var].need_wait = true;
+      }
     }
     // f_i on the compute stream
     const Function& f = g->fns[i];
@@ -444,11 +510,25 @@ Status Exec::run(oc_step_metrics* out) {
     }
     if (opt.timeline) OC_CUDA(cudaEventRecord(tl_fn1[i], cs));
     OC_CUDA(cudaEventRecord(ev_done[i], cs));
-    // (c) reserved swap-outs after f_i
+    // (c) reserved swap-outs after f_i; small ones through one pack kernel (A7)
+    if (!X.dep_reserve.empty()) OC_CUDA(cudaStreamWaitEvent(ds, ev_done[i], 0));
+    if (X.pout_n) {
+      const uint32_t first = X.dep_reserve[0];
+      if (opt.timeline) { OC_CUDA(cudaEventRecord(tl_out0[first], ds)); tl_out_used[first] = 1; }
+      OC_TRY(pack_launch(pack_tab + X.pout_off, (int)X.pout_n, ds));
+      if (opt.timeline) OC_CUDA(cudaEventRecord(tl_out1[first], ds));
+      ++n_d2h;
+      ++n_kernels;
+      for (uint32_t d : X.dep_reserve)
+        if (deps[d].packed) bytes_d2h += vars[deps[d].var].bytes;
+    }
     for (uint32_t d : X.dep_reserve) {
       const Dep& D = deps[d];
       XVar& xv = vars[D.var];
-      OC_CUDA(cudaStreamWaitEvent(ds, ev_done[i], 0));
+      if (D.packed) {
+        OC_CUDA(cudaEventRecord(ev_out[d], ds));
+        continue;
+      }
       if (D.dirty || !opt.elide_clean) {
         if (opt.timeline) { OC_CUDA(cudaEventRecord(tl_out0[d], ds)); tl_out_used[d] = 1; }
         OC_CUDA(cudaMemcpyAsync(host + xv.host_off, addr_of(D.var), xv.bytes, cudaMemcpyDeviceToHost, ds));
@@ -522,6 +602,7 @@ void Exec::destroy() {
   if (ev_end) cudaEventDestroy(ev_end);
   if (host) cudaFreeHost(host);
   if (ws) cudaFree(ws);
+  if (pack_tab) cudaFree(pack_tab);
   if (nccl_comm && nccl_destroy) ((int (*)(void*))nccl_destroy)(nccl_comm);
 }
 

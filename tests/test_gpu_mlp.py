@@ -40,9 +40,9 @@ def test_mlp_graph_forces_swaps_at_4mib():
     assert s.json() == osch.canonical_json(sch)
 
 
-def _run(spec, doc, info, budget, window, mode, phys, chunk=2 * MiB):
+def _run(spec, doc, info, budget, window, mode, phys, chunk=2 * MiB, pack=64 << 10):
     from paper_2010_14109_b200.runtime import OutOfCoreStep
-    st = OutOfCoreStep(doc, budget, window, mode=mode, chunk_bytes=chunk, phys_bytes=phys)
+    st = OutOfCoreStep(doc, budget, window, mode=mode, chunk_bytes=chunk, phys_bytes=phys, pack_threshold=pack)
     x, y = nets.make_inputs(spec)
     p = nets.make_params(spec)
     st.write(info["x"], x)
@@ -77,3 +77,10 @@ def test_mlp_parity_and_swap_transparency(mode, phys):
     for k in p:
         assert np.array_equal(inc["m." + k], ooc["m." + k]), k          # bitwise swap transparency
         assert np.array_equal(inc["p." + k], ooc["p." + k]), k
+    # every swap through the SM pack/unpack kernel (A7) vs none through it
+    allpack = _run(spec, doc, info, 4 * MiB, B.OC_WINDOW_MAX_FEASIBLE, mode, phys, pack=1 << 30)
+    nopack = _run(spec, doc, info, 4 * MiB, B.OC_WINDOW_MAX_FEASIBLE, mode, phys, pack=0)
+    assert allpack["metrics"]["n_h2d"] < nopack["metrics"]["n_h2d"]
+    assert allpack["metrics"]["bytes_d2h"] == nopack["metrics"]["bytes_d2h"]
+    for k in p:
+        assert np.array_equal(allpack["p." + k], ooc["p." + k]) and np.array_equal(nopack["p." + k], ooc["p." + k])

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--modes", default="va")
     ap.add_argument("--chunks", default="2")
     ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--packs", default="65536", help="pack/unpack thresholds in bytes (0 = copy engines only)")
     a = ap.parse_args()
     import numpy as np
     from paper_2010_14109_b200 import binding as B
@@ -38,11 +39,11 @@ def main():
             continue
         for mode in a.modes.split(","):
             for ch in [int(c) for c in a.chunks.split(",")]:
-                for wf in [float(x) for x in a.wfracs.split(",")]:
+                for wf, pk in [(float(x), int(p)) for x in a.wfracs.split(",") for p in a.packs.split(",")]:
                     W = int(wmax * wf)
                     try:
                         st, W, phys = bench.setup_step(spec, info, doc, budget, mode, ch << 20, timeline=True,
-                                                       window=W)
+                                                       window=W, pack=pk)
                     except Exception as e:  # noqa: BLE001
                         print(json.dumps({"frac": frac, "mode": mode, "chunk_mib": ch, "wfrac": wf,
                                           "error": str(e)[:200]}), flush=True)
@@ -54,6 +55,7 @@ def main():
                                                                          "bytes_d2h", "n_h2d", "n_d2h")}
                     mem = st.mem_stats()
                     print(json.dumps({"frac": frac, "budget": budget, "mode": mode, "chunk_mib": ch, "wfrac": wf,
+                                      "pack": pk,
                                       "window": W, "phys": phys, "samples_per_s": a.batch / m["step_ms"] * 1e3,
                                       **m, "peak_phys": st.stats["peak_phys"], "if_peak": st.stats["if_peak"],
                                       "map_us_total": mem["map_us"]}), flush=True)
