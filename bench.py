@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="r18", choices=["r18", "r50", "mlp"])
+    ap.add_argument("--config", default="r18", choices=["r18", "r50", "r1001", "mlp"])
     ap.add_argument("--mode", default="va", choices=["va", "best", "first"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--budget-frac", type=float, default=0.25)
@@ -58,6 +58,11 @@ def config(args):
         b = args.batch or 256
         spec = nets.resnet(50, batch=b)
         return spec, {"workload": f"ResNet-50 224x224 b={b} at {args.budget_frac:.2f} of F_peak"}
+    if args.config == "r1001":
+        b = args.batch or 64
+        spec = nets.preact_resnet(1001, batch=b)
+        return spec, {"workload": f"configs[4] pre-activation ResNet-1001 32x32 b={b} at {args.budget_frac:.2f} "
+                                  "of F_peak"}
     b = args.batch or 256
     spec = nets.resnet(18, batch=b)
     return spec, {"workload": f"configs[1] ResNet-18 224x224 b={b}, budget {args.budget_frac:.2f} x in-core footprint"}
@@ -368,7 +373,8 @@ def cpu_baseline(args, steps=1):
     from oracle import numerics as nm
     from synth import nets
     cores = len(os.sched_getaffinity(0))
-    spec = nets.resnet(18, batch=2) if args.config != "r50" else nets.resnet(50, batch=1)
+    spec = {"r50": lambda: nets.resnet(50, batch=1), "r1001": lambda: nets.preact_resnet(1001, batch=2)}.get(
+        args.config, lambda: nets.resnet(18, batch=2))()
     x, y = nets.make_inputs(spec)
     p = nets.make_params(spec)
     t0 = time.perf_counter()

@@ -183,6 +183,8 @@ def train_step(spec, params, x, labels, momentum=None):
             saved[nm] = arg
         elif t == "gap":
             out = rnd(xin.mean(axis=(1, 2)))
+        elif t == "add":                      # residual sum of a pre-activation block
+            out = rnd(xin + acts[lay["in2"]])
         else:
             raise ValueError(t)
         acts[lay["out"]] = out
@@ -230,6 +232,9 @@ def train_step(spec, params, x, labels, momentum=None):
         elif t == "gap":
             H, W = xin.shape[1], xin.shape[2]
             acc(lay["in"], np.broadcast_to(g[:, None, None, :] / (H * W), xin.shape))
+        elif t == "add":
+            acc(lay["in"], g)
+            acc(lay["in2"], g)
     # ---------------- SGD with momentum (fp32 state)
     lr, mu = spec["sgd"]["lr"], spec["sgd"]["momentum"]
     new_p, new_m = {}, {}

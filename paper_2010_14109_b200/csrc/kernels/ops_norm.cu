@@ -199,7 +199,7 @@ __global__ void bnb_finalize(int nblk, int C, const float* __restrict__ part, fl
   dgamma[c] = (float)q;
 }
 
-enum { BB_G, BB_OUT, BB_Y, BB_STAT, BB_GAMMA, BB_DGAMMA, BB_DBETA };
+enum { BB_G, BB_OUT, BB_Y, BB_STAT, BB_GAMMA, BB_DGAMMA, BB_DBETA, BB_ACC };
 template <typename T>
 Status bn_bwd_reduce_t(OpArgs& a) {
   const int64_t rows = A(a, "rows");
@@ -216,11 +216,14 @@ Status bn_bwd_reduce_t(OpArgs& a) {
   return Status::ok();
 }
 
-// dy = γ·rstd·(dz − dβ/n − x̂·dγ/n), written over y; dz written over g (residual branch)
+// dy = γ·rstd·(dz − dβ/n − x̂·dγ/n), written over y — or, when the BN input
+// already holds a gradient contribution (acc), accumulated into it as
+// rnd(G + dy); dz written over g (residual branch)
 template <typename T>
 __global__ void bnb_apply(uint32_t n8, int C, FastDivU fc8, float inv_n, T* g, const T* __restrict__ out, T* y,
                           const float* __restrict__ stat, const float* __restrict__ gamma,
-                          const float* __restrict__ dgamma, const float* __restrict__ dbeta, int relu, int write_dz) {
+                          const float* __restrict__ dgamma, const float* __restrict__ dbeta, int relu, int write_dz,
+                          T* acc) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
     const int c0 = (int)fc8.mod(i) * 8;
     const int64_t o = (int64_t)i * 8;
@@ -236,7 +239,14 @@ __global__ void bnb_apply(uint32_t n8, int C, FastDivU fc8, float inv_n, T* g, c
       dz.v[k] = z;
       dy.v[k] = gamma[c] * stat[C + c] * (z - dbeta[c] * inv_n - xh * dgamma[c] * inv_n);
     }
-    st8(y + o, dy);
+    if (acc) {
+      V8 old = ld8(acc + o);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) dy.v[k] += old.v[k];
+      st8(acc + o, dy);
+    } else {
+      st8(y + o, dy);
+    }
     if (write_dz) st8(g + o, dz);
   }
 }
@@ -251,7 +261,7 @@ Status bn_bwd_apply_t(OpArgs& a) {
   bnb_apply<T><<<grid_for(n8, 256, 4), 256, 0, a.stream>>>(
       n8, C, fc8, 1.f / (float)rows, (T*)a.p(BB_G), (const T*)a.p(BB_OUT), (T*)a.p(BB_Y), (const float*)a.p(BB_STAT),
       (const float*)a.p(BB_GAMMA), (const float*)a.p(BB_DGAMMA), (const float*)a.p(BB_DBETA), Ab(a, "relu") ? 1 : 0,
-      Ab(a, "has_res") ? 1 : 0);
+      Ab(a, "has_res") ? 1 : 0, Ab(a, "accumulate") ? (T*)a.p(BB_ACC) : nullptr);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
@@ -509,6 +519,27 @@ Status gap_bwd_t(OpArgs& a) {
   return Status::ok();
 }
 
+// ---------------------------------------------------------------- residual add
+// out = rnd(a + b) (pre-activation blocks); 16-byte vectors
+template <typename T>
+__global__ void add_k(uint32_t n8, const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
+    V8 x = ld8(a + (int64_t)i * 8), y = ld8(b + (int64_t)i * 8);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x.v[k] += y.v[k];
+    st8(out + (int64_t)i * 8, x);
+  }
+}
+template <typename T>
+Status add_fwd_t(OpArgs& a) {
+  const int64_t n = A(a, "n");
+  if (n % 8) return Status::make(OC_E_UNSUPPORTED, "add: element count must be a multiple of 8");
+  const uint32_t n8 = (uint32_t)(n / 8);
+  add_k<T><<<grid_for(n8, 256, 4), 256, 0, a.stream>>>(n8, (const T*)a.p(0), (const T*)a.p(1), (T*)a.p(2));
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+
 // dtype dispatch: attrs.dtype = "bf16" (default) | "f32"
 #define OC_DT_DISPATCH(name)                                                  \
   Status name(OpArgs& a) {                                                    \
@@ -522,14 +553,17 @@ OC_DT_DISPATCH(pool_bn_bwd_reduce)
 OC_DT_DISPATCH(pool_bn_bwd_apply)
 OC_DT_DISPATCH(gap_fwd)
 OC_DT_DISPATCH(gap_bwd)
+OC_DT_DISPATCH(add_fwd)
 
 }  // namespace
+
+extern const OpDesc kAddFwd{"add_fwd", {"a", "b", "out"}, add_fwd, nullptr};
 
 extern const OpDesc kBnFwd{"bn_fwd", {"y", "stat", "gamma", "beta", "res", "out"}, bn_fwd, bn_ws};
 extern const OpDesc kBnBwdReduce{"bn_bwd_reduce", {"g", "out", "y", "stat", "gamma", "dgamma", "dbeta"},
                                  bn_bwd_reduce, bn_ws};
-extern const OpDesc kBnBwdApply{"bn_bwd_apply", {"g", "out", "y", "stat", "gamma", "dgamma", "dbeta"}, bn_bwd_apply,
-                                nullptr};
+extern const OpDesc kBnBwdApply{"bn_bwd_apply", {"g", "out", "y", "stat", "gamma", "dgamma", "dbeta", "acc"},
+                                bn_bwd_apply, nullptr};
 extern const OpDesc kBnReluPoolFwd{"bn_relu_pool_fwd", {"y", "stat", "gamma", "beta", "out", "idx"}, bn_relu_pool_fwd,
                                    bn_ws};
 extern const OpDesc kPoolBnBwdReduce{"pool_bn_bwd_reduce",

@@ -102,6 +102,11 @@ def build_convnet(spec, params="pinned", inputs="host"):
             lay["_attrs"] = {"dtype": DT, "N": Nb, "HW": H * W, "C": C}
             b.fn(f"fwd.{nm}", "gap_fwd", {"x": t[lay["in"]], "out": t[lay["out"]]}, lay["_attrs"], [t[lay["in"]]],
                  [t[lay["out"]]])
+        elif ty == "add":
+            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
+            lay["_attrs"] = {"dtype": DT, "n": Nb * int(np.prod(shapes[lay["out"]]))}
+            b.fn(f"fwd.{nm}", "add_fwd", {"a": t[lay["in"]], "b": t[lay["in2"]], "out": t[lay["out"]]},
+                 lay["_attrs"], [t[lay["in"]], t[lay["in2"]]], [t[lay["out"]]])
         elif ty == "linear":
             t[lay["out"]] = b.var(lay["out"], Nb * lay["features"] * F32, shape=[Nb, lay["features"]], dtype="f32")
             K = int(np.prod(shapes[lay["in"]]))
@@ -158,13 +163,28 @@ def build_convnet(spec, params="pinned", inputs="host"):
                     "dgamma": G[nm + ".gamma"], "dbeta": G[nm + ".beta"]}
             ins = [gv, ov if lay["relu"] else None, yv, stat[nm], P[nm + ".gamma"]]
             b.fn(f"bwd.{nm}.reduce", "bn_bwd_reduce", args, lay["_attrs"], ins, [G[nm + ".gamma"], G[nm + ".beta"]])
-            b.fn(f"bwd.{nm}.apply", "bn_bwd_apply", args, lay["_attrs"], ins + [G[nm + ".gamma"], G[nm + ".beta"]],
-                 [yv] + ([gv] if res else []))
-            g[lay["in"]] = yv
+            if lay["in"] in g:
+                # the BN input has another consumer whose gradient arrived first (a
+                # pre-activation block's shortcut): accumulate dy into it, G = rnd(G + dy)
+                acc_v = g[lay["in"]]
+                b.fn(f"bwd.{nm}.apply", "bn_bwd_apply", dict(args, acc=acc_v), dict(lay["_attrs"], accumulate=True),
+                     ins + [G[nm + ".gamma"], G[nm + ".beta"], acc_v], [acc_v] + ([gv] if res else []))
+            else:
+                b.fn(f"bwd.{nm}.apply", "bn_bwd_apply", args, lay["_attrs"],
+                     ins + [G[nm + ".gamma"], G[nm + ".beta"]], [yv] + ([gv] if res else []))
+                g[lay["in"]] = yv
             if res:
                 assert res not in g, "residual must receive its first gradient here"
                 g[res] = gv                      # gv now holds dz
             _update(b, spec, nm, P, Mo, G, [nm + ".gamma", nm + ".beta"])
+        elif ty == "add":
+            # out = a + b: both inputs receive g.  No kernel: the gradient variable
+            # is shared; in a pre-activation block every reader of g[a] (the last
+            # conv's backward) runs before any accumulation into g[b] (the shortcut's
+            # other consumer), so the aliasing is safe in the reverse layer order.
+            for src in (lay["in"], lay["in2"]):
+                assert src not in g, "add: input already has a gradient contribution"
+                g[src] = gv
         elif ty == "conv":
             dy = gv
             b.fn(f"bwd.{nm}.wgrad", "conv_wgrad", {"dy": dy, "x": t[lay["in"]], "dw": G[nm + ".W"]}, lay["_attrs"],

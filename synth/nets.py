@@ -87,6 +87,50 @@ def resnet(depth=18, batch=8, image=224, classes=1000, mode="bf16", width=64, in
             "loss": {"type": "softmax_ce", "in": "logits"}}
 
 
+def preact_resnet(depth=1001, batch=8, image=32, classes=10, mode="bf16", widths=(16, 32, 64)):
+    """Pre-activation bottleneck ResNet for CIFAR-shaped inputs (He et al.
+    2016, "identity mappings"; the paper cites ResNet-1001 as a model that
+    needs out-of-core training): depth = 9n + 2, three stages of n
+    bottleneck blocks  a = relu(bn(x)); h = conv1x1 -> bn-relu -> conv3x3(stride)
+    -> bn-relu -> conv1x1(4w); out = h + shortcut, shortcut = x or conv1x1(a)."""
+    assert (depth - 2) % 9 == 0
+    n = (depth - 2) // 9
+    L = []
+    L.append({"type": "conv", "name": "conv1", "in": "x", "out": "s0", "k": widths[0], "r": 3, "s": 3,
+              "stride": 1, "pad": 1})
+    prev, ch = "s0", widths[0]
+    for si, w in enumerate(widths):
+        for bi in range(n):
+            st = 2 if (bi == 0 and si > 0) else 1
+            pre = f"s{si + 1}b{bi}"
+            L.append({"type": "bn", "name": pre + "_bn1", "in": prev, "out": pre + "_a", "relu": True,
+                      "residual": None})
+            if st != 1 or ch != 4 * w:
+                L.append({"type": "conv", "name": pre + "_proj", "in": pre + "_a", "out": pre + "_sc",
+                          "k": 4 * w, "r": 1, "s": 1, "stride": st, "pad": 0})
+                sc = pre + "_sc"
+            else:
+                sc = prev
+            L.append({"type": "conv", "name": pre + "_c1", "in": pre + "_a", "out": pre + "_h1", "k": w, "r": 1,
+                      "s": 1, "stride": 1, "pad": 0})
+            L.append({"type": "bn", "name": pre + "_bn2", "in": pre + "_h1", "out": pre + "_a1", "relu": True,
+                      "residual": None})
+            L.append({"type": "conv", "name": pre + "_c2", "in": pre + "_a1", "out": pre + "_h2", "k": w, "r": 3,
+                      "s": 3, "stride": st, "pad": 1})
+            L.append({"type": "bn", "name": pre + "_bn3", "in": pre + "_h2", "out": pre + "_a2", "relu": True,
+                      "residual": None})
+            L.append({"type": "conv", "name": pre + "_c3", "in": pre + "_a2", "out": pre + "_h3", "k": 4 * w,
+                      "r": 1, "s": 1, "stride": 1, "pad": 0})
+            L.append({"type": "add", "name": pre + "_add", "in": pre + "_h3", "in2": sc, "out": pre + "_out"})
+            prev, ch = pre + "_out", 4 * w
+    L.append({"type": "bn", "name": "bn_final", "in": prev, "out": "a_final", "relu": True, "residual": None})
+    L.append({"type": "gap", "name": "gap", "in": "a_final", "out": "feat"})
+    L.append({"type": "linear", "name": "fc", "in": "feat", "out": "logits", "features": classes, "relu": False})
+    return {"name": f"preact_resnet{depth}", "mode": mode, "batch": batch, "input": [image, image, 3],
+            "classes": classes, "sgd": {"lr": 0.1, "momentum": 0.9}, "layers": L,
+            "loss": {"type": "softmax_ce", "in": "logits"}}
+
+
 def tiny_resnet(batch=4, image=16, classes=10, mode="bf16"):
     """A two-stage basic-block ResNet small enough for the fp64 oracle in
     seconds, with every layer kind of ResNet-18 (stem 7×7/2, maxpool,
@@ -139,6 +183,9 @@ def tensor_shapes(spec):
             shapes[lay["out"]] = [P, Q, C]
         elif t == "gap":
             shapes[lay["out"]] = [ish[-1]]
+        elif t == "add":
+            assert shapes[lay["in2"]] == ish, (lay["name"], shapes[lay["in2"]], ish)
+            shapes[lay["out"]] = list(ish)
         else:
             raise ValueError(t)
     return shapes, params

@@ -87,6 +87,43 @@ def test_resnet18_full_depth_parity_fp32(mode):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["va", "best"])
+def test_preact_resnet_parity_fp32(mode):
+    """Pre-activation bottleneck ResNet-29 (configs[4]'s ResNet-1001 family:
+    residual adds, BN inputs with two consumers accumulating their gradient,
+    projection shortcuts, narrow 16-64 channel convs on CUDA cores) in fp32
+    under a 1/3 budget: every gradient within 1e-5 of the oracle."""
+    spec = nets.preact_resnet(depth=29, batch=8, image=16, classes=10, mode="fp32")
+    doc, info = graphs.build(spec, params="persistent")
+    G = B.Graph(doc)
+    peak = G.in_core_peak()
+    budget = max(G.min_feasible_budget(0), peak // 3)
+    x, y = nets.make_inputs(spec)
+    p = nets.make_params(spec)
+    ref = nm.train_step(spec, p, x, y)
+    out = run_step(spec, doc, info, budget, B.OC_WINDOW_MAX_FEASIBLE, mode, None, fp32_input=True)
+    assert out["metrics"]["bytes_d2h"] > 0
+    assert abs(out["loss"] - ref["loss"]) <= 1e-5 * abs(ref["loss"])
+    errs = {k: nm.rel_l2(out["m." + k], ref["grads"][k]) for k in p}
+    worst = max(errs, key=errs.get)
+    assert errs[worst] <= 1e-5, (worst, errs[worst])
+
+
+@pytest.mark.gpu
+def test_preact_resnet_bf16_transparency():
+    """bf16 pre-activation ResNet-56: out-of-core (1/4 budget, VA) == in-core, bitwise."""
+    spec = nets.preact_resnet(depth=56, batch=32, image=32, classes=10)
+    doc, info = graphs.build(spec, params="persistent")
+    G = B.Graph(doc)
+    peak = G.in_core_peak()
+    ooc = run_step(spec, doc, info, max(G.min_feasible_budget(0), peak // 4), B.OC_WINDOW_MAX_FEASIBLE, "va", None)
+    inc = run_step(spec, doc, info, peak, 0, "best", None)
+    assert ooc["metrics"]["bytes_d2h"] > 0
+    for k in nets.make_params(spec):
+        assert np.array_equal(ooc["m." + k], inc["m." + k]), k
+
+
+@pytest.mark.gpu
 def test_resnet18_full_resolution_bf16_loss():
     """bf16 mode at full depth: the loss agrees with the oracle to 1e-3.
     Per-gradient 1e-3 parity is ill-posed at this depth in bf16 — the

@@ -125,6 +125,13 @@ def test_tiny_resnet_gradients_finite_differences():
     _fd_check_spec(spec, n_checks=16, tol=5e-5)
 
 
+def test_preact_resnet_gradients_finite_differences():
+    """Pre-activation bottleneck blocks (add layer, BN on a tensor with two
+    consumers, projection shortcuts): depth 11 = one block per stage."""
+    spec = nets.preact_resnet(depth=11, batch=4, image=8, classes=5)
+    _fd_check_spec(spec, n_checks=20, tol=5e-5)
+
+
 def test_bn_output_moments_and_sgd_closed_form():
     spec = nets.mlp6(batch=8, width=32, classes=10)
     spec["mode"] = "fp64"

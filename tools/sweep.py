@@ -26,7 +26,10 @@ def main():
     from paper_2010_14109_b200 import binding as B
     from paper_2010_14109_b200 import graphs
     from synth import nets
-    spec = nets.resnet(18 if a.config == "r18" else 50, batch=a.batch)
+    if a.config == "r1001":
+        spec = nets.preact_resnet(1001, batch=a.batch)
+    else:
+        spec = nets.resnet(18 if a.config == "r18" else 50, batch=a.batch)
     doc, info = graphs.build(spec, params="persistent")
     G = B.Graph(doc)
     F = G.in_core_peak()
