@@ -110,7 +110,7 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def trainable_batch(spec_fn, budget, lo=1, hi=4096, params="persistent"):
+def trainable_batch(spec_fn, budget, lo=1, hi=4096, params="pinned"):
     """Largest batch whose IN-CORE footprint fits `budget` (bisection on the
     planner's F_peak) — the denominator of the trainable-batch multiple."""
     from paper_2010_14109_b200 import binding as B
@@ -285,11 +285,14 @@ def run_ours(args, rank, world):
         a[0] += f
         a[1] += (ev["t1"] - ev["t0"]) / 1e3
         a[2] += 1
-    # in-core reference at the same batch (no budget pressure: W=0, budget = F_peak)
+    # in-core reference at the same batch: no swapping at all — parameters,
+    # gradients and momentum device-resident (pinned), budget = F_peak, W = 0
     incore = None
     if not args.no_incore and spec["mode"] == "bf16":
         torch.cuda.empty_cache()
-        st2, _, _ = setup_step(spec, info, doc, F_peak, "best", chunk, timeline=False, window=0)
+        doc_p, info_p = graphs.build(spec, params="pinned", inputs="host")
+        F_p = B.Graph(doc_p).in_core_peak()
+        st2, _, _ = setup_step(spec, info_p, doc_p, F_p, "best", chunk, timeline=False, window=0)
         for _ in range(max(1, args.warmup)):
             st2.step()
         torch.cuda.synchronize()

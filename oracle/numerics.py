@@ -94,6 +94,31 @@ def conv2d_backward(x, w, dy, stride, pad):
     return dxp[:, pad:pad + H, pad:pad + W, :], dw
 
 
+def conv_transpose2x2(x, w):
+    """2×2 stride-2 transposed convolution, x [N,H,W,C], w [C,2,2,K]:
+    y[n, 2p+i, 2q+j, k] = Σ_c x[n,p,q,c] · w[c,i,j,k]."""
+    N, H, W, C = x.shape
+    K = w.shape[3]
+    y = np.zeros((N, 2 * H, 2 * W, K))
+    for i in range(2):
+        for j in range(2):
+            y[:, i::2, j::2, :] = x @ w[:, i, j, :]
+    return y
+
+
+def conv_transpose2x2_backward(x, w, g):
+    """Returns (dx, dw) for conv_transpose2x2."""
+    N, H, W, C = x.shape
+    dx = np.zeros((N, H, W, C))
+    dw = np.zeros(w.shape)
+    for i in range(2):
+        for j in range(2):
+            gij = g[:, i::2, j::2, :]
+            dx += gij @ w[:, i, j, :].T
+            dw[:, i, j, :] = x.reshape(-1, C).T @ gij.reshape(-1, w.shape[3])
+    return dx, dw
+
+
 def maxpool(x, r, stride, pad):
     """Returns (out, argmax index into the r×r window, row-major, first max)."""
     N, H, W, C = x.shape
@@ -148,7 +173,7 @@ def train_step(spec, params, x, labels, momentum=None):
     f64 = {k: np.asarray(v, np.float64) for k, v in params.items()}
     wcopy = {}                                # act-dtype copies of weights
     for k, v in f64.items():
-        if k.endswith(".W"):
+        if k.endswith(".W") or k.endswith(".W2"):
             wcopy[k] = rnd(v)
     acts = {"x": rnd(np.asarray(x, np.float64))}
     saved = {}
@@ -165,6 +190,13 @@ def train_step(spec, params, x, labels, momentum=None):
             out = round_fp32(y) if lay["out"] == spec["loss"]["in"] else rnd(y)
         elif t == "conv":
             out = rnd(conv2d(xin, wcopy[nm + ".W"], lay["stride"], lay["pad"]))
+            if lay.get("in2"):
+                # conv over the concatenation [in, in2] = conv(in, W) + conv(in2, W2);
+                # contributions to one stored tensor accumulate in order with a
+                # rounding after each (Z23)
+                out = rnd(out + conv2d(acts[lay["in2"]], wcopy[nm + ".W2"], lay["stride"], lay["pad"]))
+        elif t == "convT":
+            out = rnd(conv_transpose2x2(xin, wcopy[nm + ".W"]))
         elif t == "bn":
             axes = tuple(range(xin.ndim - 1))
             mu = xin.mean(axis=axes)
@@ -188,10 +220,18 @@ def train_step(spec, params, x, labels, momentum=None):
         else:
             raise ValueError(t)
         acts[lay["out"]] = out
-    loss, dlogits = softmax_ce(acts[spec["loss"]["in"]], labels)
-    # ---------------- backward (reverse layer order)
     grads = {}
-    G = {spec["loss"]["in"]: round_fp32(dlogits)}   # dlogits stored fp32
+    if spec["loss"]["type"] == "softmax_ce_pix":
+        # per-pixel cross-entropy over the channel axis, mean over all pixels;
+        # the logits are a conv output (act dtype) and so is their gradient
+        z = acts[spec["loss"]["in"]]
+        K = z.shape[-1]
+        loss, dlogits = softmax_ce(z.reshape(-1, K), np.asarray(labels).reshape(-1))
+        G = {spec["loss"]["in"]: rnd(dlogits.reshape(z.shape))}
+    else:
+        loss, dlogits = softmax_ce(acts[spec["loss"]["in"]], labels)
+        G = {spec["loss"]["in"]: round_fp32(dlogits)}   # dlogits stored fp32
+    # ---------------- backward (reverse layer order)
 
     def acc(name, c):
         G[name] = rnd(c) if name not in G else rnd(G[name] + c)
@@ -216,6 +256,14 @@ def train_step(spec, params, x, labels, momentum=None):
             grads[nm + ".W"] = round_fp32(dw)
             if need_dx:
                 acc(lay["in"], dx)
+            if lay.get("in2"):
+                dx2, dw2 = conv2d_backward(acts[lay["in2"]], wcopy[nm + ".W2"], g, lay["stride"], lay["pad"])
+                grads[nm + ".W2"] = round_fp32(dw2)
+                acc(lay["in2"], dx2)
+        elif t == "convT":
+            dx, dw = conv_transpose2x2_backward(xin, wcopy[nm + ".W"], g)
+            grads[nm + ".W"] = round_fp32(dw)
+            acc(lay["in"], dx)
         elif t == "bn":
             xhat, rstd = saved[nm]
             out = acts[lay["out"]]

@@ -20,7 +20,7 @@ inline ConvGeom conv_geom(const JVal& j) {
 
 // CUDA-core implicit GEMM (conv_simt.cu); T = __nv_bfloat16 or float
 template <typename T>
-Status conv_fprop_simt(OpArgs& a, const ConvGeom& g, const T* x, const float* w, T* y);
+Status conv_fprop_simt(OpArgs& a, const ConvGeom& g, const T* x, const float* w, T* y, bool accumulate = false);
 template <typename T>
 Status conv_dgrad_simt(OpArgs& a, const ConvGeom& g, const T* dy, const float* w, T* dx, bool accumulate);
 template <typename T>

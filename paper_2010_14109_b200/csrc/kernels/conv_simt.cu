@@ -27,7 +27,8 @@ __global__ void __launch_bounds__(256) conv_simt(ConvGeom g, const T* __restrict
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  // M tiles on grid.x (up to 2^31 - 1), N tiles on grid.y
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
   int64_t kb = 0, ke = Kg;
   if (MODE == 2) {  // split-K slice z
     kb = (int64_t)blockIdx.z * k_step;
@@ -146,16 +147,16 @@ int wgrad_splits_simt(const ConvGeom& g) {
 }
 
 template <typename T>
-Status conv_fprop_simt(OpArgs& a, const ConvGeom& g, const T* x, const float* w, T* y) {
-  dim3 grid((g.K + BN - 1) / BN, (unsigned)(((int64_t)g.N * g.P * g.Q + BM - 1) / BM));
-  conv_simt<0, T><<<grid, 256, 0, a.stream>>>(g, x, w, nullptr, y, 0, 0);
+Status conv_fprop_simt(OpArgs& a, const ConvGeom& g, const T* x, const float* w, T* y, bool accumulate) {
+  dim3 grid((unsigned)(((int64_t)g.N * g.P * g.Q + BM - 1) / BM), (g.K + BN - 1) / BN);
+  conv_simt<0, T><<<grid, 256, 0, a.stream>>>(g, x, w, nullptr, y, accumulate ? 1 : 0, 0);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
 
 template <typename T>
 Status conv_dgrad_simt(OpArgs& a, const ConvGeom& g, const T* dy, const float* w, T* dx, bool accumulate) {
-  dim3 grid((g.C + BN - 1) / BN, (unsigned)(((int64_t)g.N * g.H * g.W + BM - 1) / BM));
+  dim3 grid((unsigned)(((int64_t)g.N * g.H * g.W + BM - 1) / BM), (g.C + BN - 1) / BN);
   conv_simt<1, T><<<grid, 256, 0, a.stream>>>(g, dy, w, nullptr, dx, accumulate ? 1 : 0, 0);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
@@ -169,7 +170,7 @@ Status conv_wgrad_simt(OpArgs& a, const ConvGeom& g, const T* dy, const T* x, fl
   step = (step + BK - 1) / BK * BK;
   const int64_t n = (int64_t)g.K * g.R * g.S * g.C;
   if (a.ws_bytes < (size_t)(splits * n * 4)) return Status::make(OC_E_INVARIANT, "wgrad: workspace too small");
-  dim3 grid((unsigned)(((int64_t)g.R * g.S * g.C + BN - 1) / BN), (g.K + BM - 1) / BM, splits);
+  dim3 grid((g.K + BM - 1) / BM, (unsigned)(((int64_t)g.R * g.S * g.C + BN - 1) / BN), splits);
   conv_simt<2, T><<<grid, 256, 0, a.stream>>>(g, dy, nullptr, x, a.ws, 0, step);
   OC_LAUNCH_CHECK(a);
   splitk_reduce<<<grid_for(n, 256, 4), 256, 0, a.stream>>>(splits, n, (const float*)a.ws, dw);
@@ -178,8 +179,8 @@ Status conv_wgrad_simt(OpArgs& a, const ConvGeom& g, const T* dy, const T* x, fl
 }
 
 template Status conv_fprop_simt<__nv_bfloat16>(OpArgs&, const ConvGeom&, const __nv_bfloat16*, const float*,
-                                                __nv_bfloat16*);
-template Status conv_fprop_simt<float>(OpArgs&, const ConvGeom&, const float*, const float*, float*);
+                                                __nv_bfloat16*, bool);
+template Status conv_fprop_simt<float>(OpArgs&, const ConvGeom&, const float*, const float*, float*, bool);
 template Status conv_dgrad_simt<__nv_bfloat16>(OpArgs&, const ConvGeom&, const __nv_bfloat16*, const float*,
                                                 __nv_bfloat16*, bool);
 template Status conv_dgrad_simt<float>(OpArgs&, const ConvGeom&, const float*, const float*, float*, bool);

@@ -559,8 +559,8 @@ void fill_divs(Params& P) {
 using namespace tc;
 
 bool conv_tc_ok(const ConvGeom& g, int mode) {
-  const int64_t big = (int64_t)g.N * g.H * g.W * std::max(g.C, g.K);
-  if (big >= (1ll << 31)) return false;  // 32-bit index arithmetic
+  // 32-bit element indices of the activations (the 64-bit tensor offsets are formed per row)
+  if ((int64_t)g.N * g.H * g.W * g.C >= (1ll << 31) || (int64_t)g.N * g.P * g.Q * g.K >= (1ll << 31)) return false;
   if (mode == FPROP) return g.K % 64 == 0 && (g.C % 64 == 0 || g.C < 64);
   if (mode == DGRAD) return g.K % 64 == 0 && g.C % 64 == 0 && (g.st == 1 || g.st == 2);
   return g.K % 64 == 0;
@@ -577,7 +577,8 @@ size_t conv_tc_ws(const ConvGeom& g, int mode) {
   return (wbytes + 255) / 256 * 256;
 }
 
-Status conv_fprop_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y) {
+Status conv_fprop_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y,
+                     bool accumulate) {
   __nv_bfloat16* wb = (__nv_bfloat16*)a.ws;
   const bool reg = g.C % 64 != 0;
   const int kpad = kpad_of(g);
@@ -593,6 +594,7 @@ Status conv_fprop_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const
   P.kpad = kpad;
   P.kch = g.C;
   P.nkb = kpad / BKE;
+  P.accumulate = accumulate ? 1 : 0;
   fill_divs(P);
   const dim3 grid((P.M + BM - 1) / BM, g.K / (g.K % 128 == 0 ? 128 : 64), 1);
   if (reg) return g.K % 128 == 0 ? launch<FPROP, 128, true>(a, P, grid) : launch<FPROP, 64, true>(a, P, grid);

@@ -1,10 +1,13 @@
 // Convolution ops of the training step: forward, data gradient, weight
-// gradient.  bf16 activations dispatch to the tcgen05
-// tensor-core implicit GEMM (conv_tc.cu) when the shape fits its tiling
-// (channels in multiples of 64; the 3-channel stem gathers into registers),
-// else to the CUDA-core implicit GEMM (conv_simt.cu).  fp32 activations
-// (attrs.dtype = "f32", the 1e-5 parity mode) always run on CUDA cores — no
-// TF32.  attrs.impl = "simt" or OC_CONV_IMPL=simt force CUDA cores.
+// gradient, and the 2×2 stride-2 transposed convolution
+// of the U-Net decoder expressed through the same kernels (a transposed conv
+// is the data gradient of the strided conv it inverts).  bf16 activations
+// dispatch to the tcgen05 tensor-core implicit GEMM (conv_tc.cu) when the
+// shape fits its tiling (channels in multiples of 64; the 3-channel stem
+// gathers into registers), else to the CUDA-core implicit GEMM
+// (conv_simt.cu).  fp32 activations (attrs.dtype = "f32", the 1e-5 parity
+// mode) always run on CUDA cores — no TF32.  attrs.impl = "simt" or
+// OC_CONV_IMPL=simt force CUDA cores.
 #include <cstdlib>
 #include <cstring>
 
@@ -14,7 +17,8 @@ namespace oc {
 
 bool conv_tc_ok(const ConvGeom& g, int mode);
 size_t conv_tc_ws(const ConvGeom& g, int mode);
-Status conv_fprop_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y);
+Status conv_fprop_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y,
+                     bool accumulate);
 Status conv_dgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const float* w, __nv_bfloat16* dx,
                      bool accumulate);
 Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* x, float* dw);
@@ -31,39 +35,50 @@ bool force_simt(const OpArgs* a) {
 }
 bool f32(const OpArgs& a) { return As(a, "dtype", "bf16") == "f32"; }
 
+// y = conv(x, w) (+ y when accumulating)
+Status fprop(OpArgs& a, const ConvGeom& g, const void* x, const float* w, void* y, bool acc) {
+  if (f32(a)) return conv_fprop_simt<float>(a, g, (const float*)x, w, (float*)y, acc);
+  if (!force_simt(&a) && conv_tc_ok(g, 0))
+    return conv_fprop_tc(a, g, (const __nv_bfloat16*)x, w, (__nv_bfloat16*)y, acc);
+  return conv_fprop_simt<__nv_bfloat16>(a, g, (const __nv_bfloat16*)x, w, (__nv_bfloat16*)y, acc);
+}
+Status dgrad(OpArgs& a, const ConvGeom& g, const void* dy, const float* w, void* dx, bool acc) {
+  if (f32(a)) return conv_dgrad_simt<float>(a, g, (const float*)dy, w, (float*)dx, acc);
+  if (!force_simt(&a) && conv_tc_ok(g, 1))
+    return conv_dgrad_tc(a, g, (const __nv_bfloat16*)dy, w, (__nv_bfloat16*)dx, acc);
+  return conv_dgrad_simt<__nv_bfloat16>(a, g, (const __nv_bfloat16*)dy, w, (__nv_bfloat16*)dx, acc);
+}
+Status wgrad(OpArgs& a, const ConvGeom& g, const void* dy, const void* x, float* dw) {
+  if (f32(a)) return conv_wgrad_simt<float>(a, g, (const float*)dy, (const float*)x, dw);
+  if (!force_simt(&a) && conv_tc_ok(g, 2))
+    return conv_wgrad_tc(a, g, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, dw);
+  return conv_wgrad_simt<__nv_bfloat16>(a, g, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, dw);
+}
+
 enum { CF_X, CF_W, CF_Y };
 Status conv_fwd(OpArgs& a) {
-  ConvGeom g = conv_geom(a);
-  auto w = (const float*)a.p(CF_W);
-  if (f32(a)) return conv_fprop_simt<float>(a, g, (const float*)a.p(CF_X), w, (float*)a.p(CF_Y));
-  auto x = (const __nv_bfloat16*)a.p(CF_X);
-  auto y = (__nv_bfloat16*)a.p(CF_Y);
-  if (!force_simt(&a) && conv_tc_ok(g, 0)) return conv_fprop_tc(a, g, x, w, y);
-  return conv_fprop_simt<__nv_bfloat16>(a, g, x, w, y);
+  return fprop(a, conv_geom(a), a.p(CF_X), (const float*)a.p(CF_W), a.p(CF_Y), Ab(a, "accumulate"));
 }
-
 enum { CD_DY, CD_W, CD_DX };
 Status conv_dgrad(OpArgs& a) {
-  ConvGeom g = conv_geom(a);
-  auto w = (const float*)a.p(CD_W);
-  const bool acc = Ab(a, "accumulate");
-  if (f32(a)) return conv_dgrad_simt<float>(a, g, (const float*)a.p(CD_DY), w, (float*)a.p(CD_DX), acc);
-  auto dy = (const __nv_bfloat16*)a.p(CD_DY);
-  auto dx = (__nv_bfloat16*)a.p(CD_DX);
-  if (!force_simt(&a) && conv_tc_ok(g, 1)) return conv_dgrad_tc(a, g, dy, w, dx, acc);
-  return conv_dgrad_simt<__nv_bfloat16>(a, g, dy, w, dx, acc);
+  return dgrad(a, conv_geom(a), a.p(CD_DY), (const float*)a.p(CD_W), a.p(CD_DX), Ab(a, "accumulate"));
 }
-
 enum { CW_DY, CW_X, CW_DW };
-Status conv_wgrad(OpArgs& a) {
-  ConvGeom g = conv_geom(a);
-  auto dw = (float*)a.p(CW_DW);
-  if (f32(a)) return conv_wgrad_simt<float>(a, g, (const float*)a.p(CW_DY), (const float*)a.p(CW_X), dw);
-  auto dy = (const __nv_bfloat16*)a.p(CW_DY);
-  auto x = (const __nv_bfloat16*)a.p(CW_X);
-  if (!force_simt(&a) && conv_tc_ok(g, 2)) return conv_wgrad_tc(a, g, dy, x, dw);
-  return conv_wgrad_simt<__nv_bfloat16>(a, g, dy, x, dw);
+Status conv_wgrad(OpArgs& a) { return wgrad(a, conv_geom(a), a.p(CW_DY), a.p(CW_X), (float*)a.p(CW_DW)); }
+
+// Transposed conv (2×2, stride 2): attrs describe the strided conv g it
+// inverts — g's input is the big map (C = K_out), its output the small map
+// (K = C_in), its weight [C_in][2][2][K_out] is the transposed conv's weight.
+//   y_big   = dgrad_g(dy = x_small)                     (convT forward)
+//   dx_small = fprop_g(x = dy_big)                      (convT data gradient)
+//   dW      = wgrad_g(dy = x_small, x = dy_big)         (convT weight gradient)
+Status convT_fwd(OpArgs& a) {
+  return dgrad(a, conv_geom(a), a.p(CF_X), (const float*)a.p(CF_W), a.p(CF_Y), false);
 }
+Status convT_dgrad(OpArgs& a) {
+  return fprop(a, conv_geom(a), a.p(CD_DY), (const float*)a.p(CD_W), a.p(CD_DX), Ab(a, "accumulate"));
+}
+Status convT_wgrad(OpArgs& a) { return wgrad(a, conv_geom(a), a.p(CW_X), a.p(CW_DY), (float*)a.p(CW_DW)); }
 
 size_t ws_fwd(const JVal& at) { return conv_tc_ws(conv_geom(at), 0); }
 size_t ws_dgrad(const JVal& at) { return conv_tc_ws(conv_geom(at), 1); }
@@ -77,5 +92,8 @@ size_t ws_wgrad(const JVal& at) {
 extern const OpDesc kConvFwd{"conv_fwd", {"x", "w", "y"}, conv_fwd, ws_fwd};
 extern const OpDesc kConvDgrad{"conv_dgrad", {"dy", "w", "dx"}, conv_dgrad, ws_dgrad};
 extern const OpDesc kConvWgrad{"conv_wgrad", {"dy", "x", "dw"}, conv_wgrad, ws_wgrad};
+extern const OpDesc kConvTFwd{"convT_fwd", {"x", "w", "y"}, convT_fwd, ws_dgrad};
+extern const OpDesc kConvTDgrad{"convT_dgrad", {"dy", "w", "dx"}, convT_dgrad, ws_fwd};
+extern const OpDesc kConvTWgrad{"convT_wgrad", {"dy", "x", "dw"}, convT_wgrad, ws_wgrad};
 
 }  // namespace oc

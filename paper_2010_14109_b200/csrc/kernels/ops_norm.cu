@@ -146,29 +146,41 @@ Status bn_fwd_t(OpArgs& a) {
 }
 
 // ---------------------------------------------------------------- backward
+// ReLU mask of the BN output: from the stored output when there is one
+// (residual blocks), else recomputed from y: relu'(γx̂ + β) (the BN-ReLU output
+// is then not needed by the backward, shrinking its working set)
 template <typename T>
 __global__ void __launch_bounds__(256) bnb_partial(int64_t rows, int C, const T* __restrict__ g,
                                                    const T* __restrict__ out, const T* __restrict__ y,
-                                                   const float* __restrict__ stat, int relu, float* __restrict__ part) {
+                                                   const float* __restrict__ stat, const float* __restrict__ gamma,
+                                                   const float* __restrict__ beta, int relu,
+                                                   float* __restrict__ part) {
   const int gC = C / 8, tpr = 256 / gC;
   const int t = threadIdx.x, cg = t % gC, rr = t / gC;
   const int64_t chunk = (rows + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = blockIdx.x * chunk, r1 = min(rows, r0 + chunk);
   float s[8] = {}, q[8] = {};
-  float mu[8], rs[8];
+  float mu[8], rs[8], gm[8], bt[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) { mu[i] = stat[cg * 8 + i]; rs[i] = stat[C + cg * 8 + i]; }
+  for (int i = 0; i < 8; ++i) {
+    mu[i] = stat[cg * 8 + i];
+    rs[i] = stat[C + cg * 8 + i];
+    gm[i] = gamma[cg * 8 + i];
+    bt[i] = beta ? beta[cg * 8 + i] : 0.f;
+  }
   if (rr < tpr)
     for (int64_t r = r0 + rr; r < r1; r += tpr) {
       const int64_t o = r * C + cg * 8;
       V8 gv = ld8(g + o), yv = ld8(y + o);
       V8 ov;
-      if (relu) ov = ld8(out + o);
+      if (relu && out) ov = ld8(out + o);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float dz = (!relu || ov.v[i] > 0.f) ? gv.v[i] : 0.f;
+        const float xh = (yv.v[i] - mu[i]) * rs[i];
+        const bool on = !relu || (out ? ov.v[i] > 0.f : fmaf(gm[i], xh, bt[i]) > 0.f);
+        const float dz = on ? gv.v[i] : 0.f;
         s[i] += dz;
-        q[i] = fmaf(dz, (yv.v[i] - mu[i]) * rs[i], q[i]);
+        q[i] = fmaf(dz, xh, q[i]);
       }
     }
   extern __shared__ float sm[];
@@ -199,15 +211,18 @@ __global__ void bnb_finalize(int nblk, int C, const float* __restrict__ part, fl
   dgamma[c] = (float)q;
 }
 
-enum { BB_G, BB_OUT, BB_Y, BB_STAT, BB_GAMMA, BB_DGAMMA, BB_DBETA, BB_ACC };
+enum { BB_G, BB_OUT, BB_Y, BB_STAT, BB_GAMMA, BB_DGAMMA, BB_DBETA, BB_ACC, BB_BETA };
 template <typename T>
 Status bn_bwd_reduce_t(OpArgs& a) {
   const int64_t rows = A(a, "rows");
   const int C = (int)A(a, "C");
   const int nblk = stat_blocks(rows);
   if (a.ws_bytes < (size_t)nblk * 2 * C * 4) return Status::make(OC_E_INVARIANT, "bn_bwd: workspace too small");
+  if (Ab(a, "relu") && !a.p(BB_OUT) && !a.p(BB_BETA))
+    return Status::make(OC_E_INVALID, "bn_bwd: ReLU mask needs the output or beta");
   bnb_partial<T><<<nblk, 256, 256 * 16 * 4, a.stream>>>(rows, C, (const T*)a.p(BB_G), (const T*)a.p(BB_OUT),
                                                         (const T*)a.p(BB_Y), (const float*)a.p(BB_STAT),
+                                                        (const float*)a.p(BB_GAMMA), (const float*)a.p(BB_BETA),
                                                         Ab(a, "relu") ? 1 : 0, (float*)a.ws);
   OC_LAUNCH_CHECK(a);
   bnb_finalize<<<(C + 7) / 8, 256, 0, a.stream>>>(nblk, C, (const float*)a.ws, (float*)a.p(BB_DGAMMA),
@@ -222,20 +237,21 @@ Status bn_bwd_reduce_t(OpArgs& a) {
 template <typename T>
 __global__ void bnb_apply(uint32_t n8, int C, FastDivU fc8, float inv_n, T* g, const T* __restrict__ out, T* y,
                           const float* __restrict__ stat, const float* __restrict__ gamma,
-                          const float* __restrict__ dgamma, const float* __restrict__ dbeta, int relu, int write_dz,
-                          T* acc) {
+                          const float* __restrict__ beta, const float* __restrict__ dgamma,
+                          const float* __restrict__ dbeta, int relu, int write_dz, T* acc) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
     const int c0 = (int)fc8.mod(i) * 8;
     const int64_t o = (int64_t)i * 8;
     V8 gv = ld8(g + o), yv = ld8(y + o);
     V8 ov;
-    if (relu) ov = ld8(out + o);
+    if (relu && out) ov = ld8(out + o);
     V8 dz, dy;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int c = c0 + k;
-      const float z = (!relu || ov.v[k] > 0.f) ? gv.v[k] : 0.f;
       const float xh = (yv.v[k] - stat[c]) * stat[C + c];
+      const bool on = !relu || (out ? ov.v[k] > 0.f : fmaf(gamma[c], xh, beta[c]) > 0.f);
+      const float z = on ? gv.v[k] : 0.f;
       dz.v[k] = z;
       dy.v[k] = gamma[c] * stat[C + c] * (z - dbeta[c] * inv_n - xh * dgamma[c] * inv_n);
     }
@@ -260,8 +276,9 @@ Status bn_bwd_apply_t(OpArgs& a) {
   fc8.init(C / 8);
   bnb_apply<T><<<grid_for(n8, 256, 4), 256, 0, a.stream>>>(
       n8, C, fc8, 1.f / (float)rows, (T*)a.p(BB_G), (const T*)a.p(BB_OUT), (T*)a.p(BB_Y), (const float*)a.p(BB_STAT),
-      (const float*)a.p(BB_GAMMA), (const float*)a.p(BB_DGAMMA), (const float*)a.p(BB_DBETA), Ab(a, "relu") ? 1 : 0,
-      Ab(a, "has_res") ? 1 : 0, Ab(a, "accumulate") ? (T*)a.p(BB_ACC) : nullptr);
+      (const float*)a.p(BB_GAMMA), (const float*)a.p(BB_BETA), (const float*)a.p(BB_DGAMMA),
+      (const float*)a.p(BB_DBETA), Ab(a, "relu") ? 1 : 0, Ab(a, "has_res") ? 1 : 0,
+      Ab(a, "accumulate") ? (T*)a.p(BB_ACC) : nullptr);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
@@ -305,7 +322,7 @@ __global__ void bn_relu_pool(PoolGeom g, const T* __restrict__ y, const float* _
       best[k] = -INFINITY;
       bi[k] = 0;
       const int c = cg * 8 + k;
-      gm[k] = gamma[c]; bt[k] = beta[c]; mu[k] = stat[c]; rs[k] = stat[C + c];
+      if (gamma) { gm[k] = gamma[c]; bt[k] = beta[c]; mu[k] = stat[c]; rs[k] = stat[C + c]; }
     }
     for (int u = 0; u < g.r; ++u) {
       const int h = p * g.st - g.pad + u;
@@ -316,7 +333,8 @@ __global__ void bn_relu_pool(PoolGeom g, const T* __restrict__ y, const float* _
         V8 x = ld8(y + (((int64_t)n * g.H + h) * g.W + w) * C + cg * 8);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const float z = rnd<T>(fmaxf(fmaf(gm[k], (x.v[k] - mu[k]) * rs[k], bt[k]), 0.f));
+          // plain max-pool (gamma == nullptr) pools the stored values themselves
+          const float z = gamma ? rnd<T>(fmaxf(fmaf(gm[k], (x.v[k] - mu[k]) * rs[k], bt[k]), 0.f)) : x.v[k];
           if (z > best[k]) { best[k] = z; bi[k] = (uint8_t)(u * g.r + v); }
         }
       }
@@ -348,9 +366,10 @@ Status bn_relu_pool_fwd_t(OpArgs& a) {
   return Status::ok();
 }
 
-// gradient reaching bn-output position (n,h,w,c) through the max pool:
-// rnd(Σ over windows whose argmax is this position of their output gradient)
-template <typename T>
+// gradient reaching pool-input position (n,h,w,c) through the max pool:
+// Σ over windows whose argmax is this position of their output gradient,
+// rounded to T unless the caller accumulates it first
+template <typename T, bool ROUND = true>
 __device__ __forceinline__ void pooled_grad8(const PoolGeom& g, int n, int h, int w, int cg, const T* __restrict__ gp,
                                              const uint8_t* __restrict__ idx, float ga[8]) {
 #pragma unroll
@@ -375,9 +394,105 @@ __device__ __forceinline__ void pooled_grad8(const PoolGeom& g, int n, int h, in
       }
     }
   }
+  if (ROUND) {
 #pragma unroll
-  for (int k = 0; k < 8; ++k) ga[k] = rnd<T>(ga[k]);
+    for (int k = 0; k < 8; ++k) ga[k] = rnd<T>(ga[k]);
+  }
 }
+
+// plain max-pool backward: dx = rnd(Σ routed) or, accumulating, rnd(dx + Σ routed)
+template <typename T>
+__global__ void mp_bwd(PoolGeom g, const T* __restrict__ gp, const uint8_t* __restrict__ idx, T* dx, int accumulate) {
+  const int C = g.C;
+  const uint32_t total = (uint32_t)g.N * g.H * g.W * (C / 8);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t r = g.fc8.div(i);
+    const int cg = (int)(i - r * (C / 8));
+    const uint32_t t1 = g.fW.div(r);
+    const int w = (int)(r - t1 * g.W);
+    const uint32_t n = g.fH.div(t1);
+    const int h = (int)(t1 - n * g.H);
+    float ga[8];
+    pooled_grad8<T, false>(g, (int)n, h, w, cg, gp, idx, ga);
+    V8 o;
+    if (accumulate) o = ld8(dx + (int64_t)i * 8);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o.v[k] = accumulate ? o.v[k] + ga[k] : ga[k];
+    st8(dx + (int64_t)i * 8, o);
+  }
+}
+
+enum { MP_X, MP_OUT, MP_IDX };
+template <typename T>
+Status maxpool_fwd_t(OpArgs& a) {
+  PoolGeom g = geom(a);
+  const int64_t total = (int64_t)g.N * g.P * g.Q * (g.C / 8);
+  bn_relu_pool<T><<<grid_for(total, 256, 2), 256, 0, a.stream>>>(g, (const T*)a.p(MP_X), nullptr, nullptr, nullptr,
+                                                                 (T*)a.p(MP_OUT), (uint8_t*)a.p(MP_IDX));
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+enum { MB_G, MB_IDX, MB_DX };
+template <typename T>
+Status maxpool_bwd_t(OpArgs& a) {
+  PoolGeom g = geom(a);
+  const int64_t total = (int64_t)g.N * g.H * g.W * (g.C / 8);
+  mp_bwd<T><<<grid_for(total, 256, 2), 256, 0, a.stream>>>(g, (const T*)a.p(MB_G), (const uint8_t*)a.p(MB_IDX),
+                                                           (T*)a.p(MB_DX), Ab(a, "accumulate") ? 1 : 0);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+
+// ---------------------------------------------------------------- per-pixel softmax CE
+// rows = pixels, K classes (logits and dlogits in the act dtype); loss = mean
+// over rows, reduced in fixed order (per-block partials, then one warp)
+template <typename T>
+__global__ void ce_pix_rows(int64_t rows, int K, const T* __restrict__ z, const int* __restrict__ lab,
+                            T* __restrict__ dz, float inv_rows, float* __restrict__ part) {
+  float acc = 0.f;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const T* zr = z + r * K;
+    float mx = -INFINITY;
+    for (int k = 0; k < K; ++k) mx = fmaxf(mx, ld_f(zr + k));
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += expf(ld_f(zr + k) - mx);
+    const int y = lab[r];
+    acc += (logf(s) + mx) - ld_f(zr + y);
+    const float inv_s = 1.f / s;
+    for (int k = 0; k < K; ++k)
+      st_f(dz + r * K + k, (expf(ld_f(zr + k) - mx) * inv_s - (k == y ? 1.f : 0.f)) * inv_rows);
+  }
+  acc = warp_sum(acc);
+  __shared__ float red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+__global__ void ce_pix_final(int nblk, const float* __restrict__ part, float inv_rows, float* __restrict__ loss) {
+  double s = 0;
+  for (int b = threadIdx.x; b < nblk; b += 32) s += part[b];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) loss[0] = (float)(s * inv_rows);
+}
+enum { CP_Z, CP_LAB, CP_LOSS, CP_DZ };
+template <typename T>
+Status softmax_ce_pix_t(OpArgs& a) {
+  const int64_t rows = A(a, "rows");
+  const int K = (int)A(a, "K");
+  const int nblk = grid_for(rows, 256, 4);
+  if (a.ws_bytes < (size_t)nblk * 4) return Status::make(OC_E_INVARIANT, "ce_pix: workspace too small");
+  ce_pix_rows<T><<<nblk, 256, 0, a.stream>>>(rows, K, (const T*)a.p(CP_Z), (const int*)a.p(CP_LAB), (T*)a.p(CP_DZ),
+                                             1.f / (float)rows, (float*)a.ws);
+  OC_LAUNCH_CHECK(a);
+  ce_pix_final<<<1, 32, 0, a.stream>>>(nblk, (const float*)a.ws, 1.f / (float)rows, (float*)a.p(CP_LOSS));
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+size_t ce_pix_ws(const JVal& at) { return (size_t)grid_for(at.geti("rows"), 256, 4) * 4; }
 
 template <typename T>
 __global__ void __launch_bounds__(256) pbn_partial(PoolGeom g, const T* __restrict__ gp,
@@ -554,15 +669,23 @@ OC_DT_DISPATCH(pool_bn_bwd_apply)
 OC_DT_DISPATCH(gap_fwd)
 OC_DT_DISPATCH(gap_bwd)
 OC_DT_DISPATCH(add_fwd)
+OC_DT_DISPATCH(maxpool_fwd)
+OC_DT_DISPATCH(maxpool_bwd)
+OC_DT_DISPATCH(softmax_ce_pix)
 
 }  // namespace
 
 extern const OpDesc kAddFwd{"add_fwd", {"a", "b", "out"}, add_fwd, nullptr};
+extern const OpDesc kMaxpoolFwd{"maxpool_fwd", {"x", "out", "idx"}, maxpool_fwd, nullptr};
+extern const OpDesc kMaxpoolBwd{"maxpool_bwd", {"g", "idx", "dx"}, maxpool_bwd, nullptr};
+extern const OpDesc kSoftmaxCEPix{"softmax_ce_pix", {"logits", "labels", "loss", "dlogits"}, softmax_ce_pix,
+                                  ce_pix_ws};
 
 extern const OpDesc kBnFwd{"bn_fwd", {"y", "stat", "gamma", "beta", "res", "out"}, bn_fwd, bn_ws};
-extern const OpDesc kBnBwdReduce{"bn_bwd_reduce", {"g", "out", "y", "stat", "gamma", "dgamma", "dbeta"},
-                                 bn_bwd_reduce, bn_ws};
-extern const OpDesc kBnBwdApply{"bn_bwd_apply", {"g", "out", "y", "stat", "gamma", "dgamma", "dbeta", "acc"},
+extern const OpDesc kBnBwdReduce{"bn_bwd_reduce",
+                                 {"g", "out", "y", "stat", "gamma", "dgamma", "dbeta", "acc", "beta"}, bn_bwd_reduce,
+                                 bn_ws};
+extern const OpDesc kBnBwdApply{"bn_bwd_apply", {"g", "out", "y", "stat", "gamma", "dgamma", "dbeta", "acc", "beta"},
                                 bn_bwd_apply, nullptr};
 extern const OpDesc kBnReluPoolFwd{"bn_relu_pool_fwd", {"y", "stat", "gamma", "beta", "out", "idx"}, bn_relu_pool_fwd,
                                    bn_ws};

@@ -9,7 +9,8 @@ namespace oc {
 #define OC_OPS(X)                                                                                   \
   X(kLinearFwd) X(kLinearBwd) X(kSoftmaxCE) X(kSGD) X(kAllreduce) X(kNop) X(kConvFwd) X(kConvDgrad) \
   X(kConvWgrad) X(kBnFwd) X(kBnBwdReduce) X(kBnBwdApply) X(kBnReluPoolFwd) X(kPoolBnBwdReduce)      \
-  X(kPoolBnBwdApply) X(kGapFwd) X(kGapBwd) X(kAddFwd)
+  X(kPoolBnBwdApply) X(kGapFwd) X(kGapBwd) X(kAddFwd) X(kMaxpoolFwd) X(kMaxpoolBwd) X(kSoftmaxCEPix) X(kConvTFwd) \
+  X(kConvTDgrad) X(kConvTWgrad)
 
 #define OC_DECL(n) extern const OpDesc n;
 OC_OPS(OC_DECL)

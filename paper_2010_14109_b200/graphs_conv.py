@@ -32,7 +32,8 @@ def build_convnet(spec, params="pinned", inputs="host"):
     pin_in = inputs == "pinned"
     x = b.var("x", Nb * int(np.prod(spec["input"])) * ACT, persistent=not pin_in, pinned=pin_in,
               shape=[Nb] + spec["input"], dtype=DT)
-    y = b.var("labels", Nb * I32, persistent=not pin_in, pinned=pin_in, shape=[Nb], dtype="i32")
+    ylen = Nb * (int(np.prod(spec["input"][:2])) if spec["loss"]["type"] == "softmax_ce_pix" else 1)
+    y = b.var("labels", ylen * I32, persistent=not pin_in, pinned=pin_in, shape=[ylen], dtype="i32")
     P, Mo, G = _pvars(b, spec, pshapes, params)
     layers = spec["layers"]
 
@@ -42,7 +43,7 @@ def build_convnet(spec, params="pinned", inputs="host"):
     # fuse a bn(relu) immediately consumed only by a maxpool (the stem)
     consumers = {}
     for lay in layers:
-        for t in [lay["in"]] + ([lay["residual"]] if lay.get("residual") else []):
+        for t in [lay["in"]] + [lay[k] for k in ("residual", "in2") if lay.get(k)]:
             consumers.setdefault(t, []).append(lay["name"])
     fused_pool = {}
     for i, lay in enumerate(layers[:-1]):
@@ -68,6 +69,32 @@ def build_convnet(spec, params="pinned", inputs="host"):
             lay["_attrs"] = attrs
             b.fn(f"fwd.{nm}", "conv_fwd", {"x": t[lay["in"]], "w": P[nm + ".W"], "y": t[lay["out"]]}, attrs,
                  [t[lay["in"]], P[nm + ".W"]], [t[lay["out"]]])
+            if lay.get("in2"):
+                # conv over [in, in2] without materialising the concat: a second conv
+                # accumulates into y (y = rnd(y + conv(in2, W2)), Z23)
+                C2 = shapes[lay["in2"]][-1]
+                lay["_attrs2"] = dict(attrs, C=C2, accumulate=True)
+                b.fn(f"fwd.{nm}.2", "conv_fwd", {"x": t[lay["in2"]], "w": P[nm + ".W2"], "y": t[lay["out"]]},
+                     lay["_attrs2"], [t[lay["in2"]], P[nm + ".W2"], t[lay["out"]]], [t[lay["out"]]])
+        elif ty == "convT":
+            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
+            H, W, C = shapes[lay["in"]]
+            # the 2×2 stride-2 conv whose data gradient this is: input = the big map
+            # (C_g = K_out), output = the small map (K_g = C_in), weight [C_in][2][2][K_out]
+            attrs = {"dtype": DT, "N": Nb, "H": 2 * H, "W": 2 * W, "C": lay["k"], "K": C, "R": 2, "S": 2,
+                     "stride": 2, "pad": 0, "P": H, "Q": W}
+            lay["_attrs"] = attrs
+            b.fn(f"fwd.{nm}", "convT_fwd", {"x": t[lay["in"]], "w": P[nm + ".W"], "y": t[lay["out"]]}, attrs,
+                 [t[lay["in"]], P[nm + ".W"]], [t[lay["out"]]])
+        elif ty == "maxpool":
+            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
+            idx[nm] = b.var(f"idx.{nm}", nbytes(lay["out"], U8), shape=[Nb] + shapes[lay["out"]], dtype="u8")
+            H, W, C = shapes[lay["in"]]
+            Pq, Qq, _ = shapes[lay["out"]]
+            lay["_attrs"] = {"dtype": DT, "N": Nb, "H": H, "W": W, "C": C, "r": lay["r"], "stride": lay["stride"],
+                             "pad": lay["pad"], "P": Pq, "Q": Qq}
+            b.fn(f"fwd.{nm}", "maxpool_fwd", {"x": t[lay["in"]], "out": t[lay["out"]], "idx": idx[nm]},
+                 lay["_attrs"], [t[lay["in"]]], [t[lay["out"]], idx[nm]])
         elif ty == "bn":
             C = shapes[lay["in"]][-1]
             stat[nm] = b.var(f"stat.{nm}", 2 * C * F32, shape=[2, C], dtype="f32")
@@ -119,10 +146,18 @@ def build_convnet(spec, params="pinned", inputs="host"):
     loss = b.var("loss", F32, persistent=True, shape=[], dtype="f32")
     logits = t[spec["loss"]["in"]]
     g = {}   # tensor -> variable holding its gradient
-    g[spec["loss"]["in"]] = b.var("grad.logits", Nb * spec["classes"] * F32, shape=[Nb, spec["classes"]],
-                                  dtype="f32")
-    b.fn("loss", "softmax_ce", {"logits": logits, "labels": y, "loss": loss, "dlogits": g[spec["loss"]["in"]]},
-         {"M": Nb, "N": spec["classes"]}, [logits, y], [loss, g[spec["loss"]["in"]]])
+    if spec["loss"]["type"] == "softmax_ce_pix":
+        # per-pixel CE over the channel axis of a conv output (act dtype in and out)
+        lt = spec["loss"]["in"]
+        g[lt] = b.var("grad.logits", nbytes(lt), shape=[Nb] + shapes[lt], dtype=DT)
+        rows = Nb * int(np.prod(shapes[lt][:-1]))
+        b.fn("loss", "softmax_ce_pix", {"logits": logits, "labels": y, "loss": loss, "dlogits": g[lt]},
+             {"dtype": DT, "rows": rows, "K": spec["classes"]}, [logits, y], [loss, g[lt]])
+    else:
+        g[spec["loss"]["in"]] = b.var("grad.logits", Nb * spec["classes"] * F32, shape=[Nb, spec["classes"]],
+                                      dtype="f32")
+        b.fn("loss", "softmax_ce", {"logits": logits, "labels": y, "loss": loss, "dlogits": g[spec["loss"]["in"]]},
+             {"M": Nb, "N": spec["classes"]}, [logits, y], [loss, g[spec["loss"]["in"]]])
 
     for lay in reversed(layers):
         nm, ty = lay["name"], lay["type"]
@@ -159,9 +194,13 @@ def build_convnet(spec, params="pinned", inputs="host"):
         elif ty == "bn":
             yv, ov = t[lay["in"]], t[lay["out"]]
             res = lay.get("residual")
-            args = {"g": gv, "out": ov if lay["relu"] else None, "y": yv, "stat": stat[nm], "gamma": P[nm + ".gamma"],
+            # ReLU mask: from the stored output only when a residual entered the sum;
+            # otherwise recomputed from y, γ, β — the backward then touches g and y only
+            use_out = lay["relu"] and bool(res)
+            args = {"g": gv, "out": ov if use_out else None, "y": yv, "stat": stat[nm], "gamma": P[nm + ".gamma"],
+                    "beta": P[nm + ".beta"] if (lay["relu"] and not use_out) else None,
                     "dgamma": G[nm + ".gamma"], "dbeta": G[nm + ".beta"]}
-            ins = [gv, ov if lay["relu"] else None, yv, stat[nm], P[nm + ".gamma"]]
+            ins = [gv, ov if use_out else None, yv, stat[nm], P[nm + ".gamma"], args["beta"]]
             b.fn(f"bwd.{nm}.reduce", "bn_bwd_reduce", args, lay["_attrs"], ins, [G[nm + ".gamma"], G[nm + ".beta"]])
             if lay["in"] in g:
                 # the BN input has another consumer whose gradient arrived first (a
@@ -187,20 +226,53 @@ def build_convnet(spec, params="pinned", inputs="host"):
                 g[src] = gv
         elif ty == "conv":
             dy = gv
-            b.fn(f"bwd.{nm}.wgrad", "conv_wgrad", {"dy": dy, "x": t[lay["in"]], "dw": G[nm + ".W"]}, lay["_attrs"],
-                 [dy, t[lay["in"]]], [G[nm + ".W"]])
-            if lay["in"] != "x":
-                acc = lay["in"] in g
-                if acc:
-                    dx = g[lay["in"]]
-                    ins = [dy, P[nm + ".W"], dx]
-                else:
-                    dx = b.var(f"grad.{lay['in']}", nbytes(lay["in"]), shape=[Nb] + shapes[lay["in"]], dtype=DT)
-                    ins = [dy, P[nm + ".W"]]
-                    g[lay["in"]] = dx
-                b.fn(f"bwd.{nm}.dgrad", "conv_dgrad", {"dy": dy, "w": P[nm + ".W"], "dx": dx},
-                     dict(lay["_attrs"], accumulate=acc), ins, [dx])
+            parts = [(lay["in"], nm + ".W", lay["_attrs"], "")]
+            if lay.get("in2"):
+                parts.append((lay["in2"], nm + ".W2", lay["_attrs2"], "2"))
+            for src, wname, at, sfx in parts:
+                at = {k: v for k, v in at.items() if k != "accumulate"}
+                b.fn(f"bwd.{nm}.wgrad{sfx}", "conv_wgrad", {"dy": dy, "x": t[src], "dw": G[wname]}, at,
+                     [dy, t[src]], [G[wname]])
+                if src != "x":
+                    acc = src in g
+                    if acc:
+                        dx = g[src]
+                        ins = [dy, P[wname], dx]
+                    else:
+                        dx = b.var(f"grad.{src}", nbytes(src), shape=[Nb] + shapes[src], dtype=DT)
+                        ins = [dy, P[wname]]
+                        g[src] = dx
+                    b.fn(f"bwd.{nm}.dgrad{sfx}", "conv_dgrad", {"dy": dy, "w": P[wname], "dx": dx},
+                         dict(at, accumulate=acc), ins, [dx])
+            _update(b, spec, nm, P, Mo, G, [p[1] for p in parts])
+        elif ty == "convT":
+            # dW via the virtual conv's wgrad with the roles of its input/output-gradient swapped
+            src = lay["in"]
+            b.fn(f"bwd.{nm}.wgrad", "convT_wgrad", {"dy": gv, "x": t[src], "dw": G[nm + ".W"]}, lay["_attrs"],
+                 [gv, t[src]], [G[nm + ".W"]])
+            acc = src in g
+            if acc:
+                dx = g[src]
+                ins = [gv, P[nm + ".W"], dx]
+            else:
+                dx = b.var(f"grad.{src}", nbytes(src), shape=[Nb] + shapes[src], dtype=DT)
+                ins = [gv, P[nm + ".W"]]
+                g[src] = dx
+            b.fn(f"bwd.{nm}.dgrad", "convT_dgrad", {"dy": gv, "w": P[nm + ".W"], "dx": dx},
+                 dict(lay["_attrs"], accumulate=acc), ins, [dx])
             _update(b, spec, nm, P, Mo, G, [nm + ".W"])
+        elif ty == "maxpool":
+            src = lay["in"]
+            acc = src in g
+            if acc:
+                dx = g[src]
+                ins = [gv, idx[nm], dx]
+            else:
+                dx = b.var(f"grad.{src}", nbytes(src), shape=[Nb] + shapes[src], dtype=DT)
+                ins = [gv, idx[nm]]
+                g[src] = dx
+            b.fn(f"bwd.{nm}", "maxpool_bwd", {"g": gv, "idx": idx[nm], "dx": dx},
+                 dict(lay["_attrs"], accumulate=acc), ins, [dx])
         else:
             raise ValueError(ty)
     info = {"params": P, "momentum": Mo, "grads": G, "x": x, "labels": y, "loss": loss, "meta": b.meta}

@@ -131,6 +131,50 @@ def preact_resnet(depth=1001, batch=8, image=32, classes=10, mode="bf16", widths
             "loss": {"type": "softmax_ce", "in": "logits"}}
 
 
+def unet(batch=8, image=1024, base=64, depth=4, classes=19, mode="bf16"):
+    """U-Net for semantic segmentation (configs[3]): per level two
+    conv3×3-BN-ReLU, 2×2 max-pool down, 2×2 stride-2 transposed conv up, the
+    skip tensor concatenated with the upsampled one — expressed as a conv with
+    two inputs (`in2`, weights W and W2 over the two channel groups, no
+    materialised concat) — and a 1×1 head to `classes` logits with a
+    per-pixel softmax cross-entropy."""
+    L = []
+
+    def cbr(name, i, o, k, i2=None):
+        c = {"type": "conv", "name": name + "_c", "in": i, "out": name + "_y", "k": k, "r": 3, "s": 3,
+             "stride": 1, "pad": 1}
+        if i2:
+            c["in2"] = i2
+        L.append(c)
+        L.append({"type": "bn", "name": name + "_bn", "in": name + "_y", "out": o, "relu": True, "residual": None})
+
+    prev = "x"
+    skips = []
+    for lvl in range(depth):
+        w = base * 2 ** lvl
+        cbr(f"e{lvl}a", prev, f"e{lvl}a_o", w)
+        cbr(f"e{lvl}b", f"e{lvl}a_o", f"e{lvl}", w)
+        skips.append(f"e{lvl}")
+        L.append({"type": "maxpool", "name": f"pool{lvl}", "in": f"e{lvl}", "out": f"p{lvl}", "r": 2, "stride": 2,
+                  "pad": 0})
+        prev = f"p{lvl}"
+    w = base * 2 ** depth
+    cbr("mida", prev, "mida_o", w)
+    cbr("midb", "mida_o", "mid", w)
+    prev = "mid"
+    for lvl in range(depth - 1, -1, -1):
+        w = base * 2 ** lvl
+        L.append({"type": "convT", "name": f"up{lvl}", "in": prev, "out": f"u{lvl}", "k": w})
+        cbr(f"d{lvl}a", f"u{lvl}", f"d{lvl}a_o", w, i2=skips[lvl])
+        cbr(f"d{lvl}b", f"d{lvl}a_o", f"d{lvl}", w)
+        prev = f"d{lvl}"
+    L.append({"type": "conv", "name": "head", "in": prev, "out": "logits", "k": classes, "r": 1, "s": 1,
+              "stride": 1, "pad": 0})
+    return {"name": "unet", "mode": mode, "batch": batch, "input": [image, image, 3], "classes": classes,
+            "sgd": {"lr": 0.01, "momentum": 0.9}, "layers": L,
+            "loss": {"type": "softmax_ce_pix", "in": "logits"}}
+
+
 def tiny_resnet(batch=4, image=16, classes=10, mode="bf16"):
     """A two-stage basic-block ResNet small enough for the fp64 oracle in
     seconds, with every layer kind of ResNet-18 (stem 7×7/2, maxpool,
@@ -170,7 +214,15 @@ def tensor_shapes(spec):
             P = (H + 2 * lay["pad"] - lay["r"]) // lay["stride"] + 1
             Q = (W + 2 * lay["pad"] - lay["s"]) // lay["stride"] + 1
             params[lay["name"] + ".W"] = [lay["k"], lay["r"], lay["s"], C]
+            if lay.get("in2"):          # second input channel group (concat-conv)
+                H2, W2, C2 = shapes[lay["in2"]]
+                assert (H2, W2) == (H, W)
+                params[lay["name"] + ".W2"] = [lay["k"], lay["r"], lay["s"], C2]
             shapes[lay["out"]] = [P, Q, lay["k"]]
+        elif t == "convT":              # 2×2 stride-2 transposed conv, weight [C_in, 2, 2, K_out]
+            H, W, C = ish
+            params[lay["name"] + ".W"] = [C, 2, 2, lay["k"]]
+            shapes[lay["out"]] = [2 * H, 2 * W, lay["k"]]
         elif t == "bn":
             C = ish[-1]
             params[lay["name"] + ".gamma"] = [C]
@@ -198,7 +250,10 @@ def make_inputs(spec, seed_x=0, seed_y=1):
     x = rx.standard_normal([b] + list(spec["input"])).astype(np.float32)
     if len(spec["input"]) == 3 and spec["input"][2] == 8:
         x[..., 3:] = 0.0
-    y = np.random.default_rng(seed_y).integers(0, spec["classes"], size=b).astype(np.int32)
+    ysize = b
+    if spec.get("loss", {}).get("type") == "softmax_ce_pix":   # one label per pixel
+        ysize = [b] + list(spec["input"][:2])
+    y = np.random.default_rng(seed_y).integers(0, spec["classes"], size=ysize).astype(np.int32)
     return x, y
 
 

@@ -125,6 +125,34 @@ def test_tiny_resnet_gradients_finite_differences():
     _fd_check_spec(spec, n_checks=16, tol=5e-5)
 
 
+def test_conv_transpose_is_adjoint_of_strided_conv():
+    """<convT(x, W), y> = <x, conv(y, W')> with W'[c, i, j, k] -> KRSC [c][i][j][k]
+    as the 2×2 stride-2 conv from the K-channel map to the C-channel map: the
+    transposed conv is the adjoint (textbook definition)."""
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((2, 3, 4, 5))
+    w = rng.standard_normal((5, 2, 2, 6))          # [C_in, 2, 2, K_out]
+    y = rng.standard_normal((2, 6, 8, 6))
+    lhs = np.sum(nm.conv_transpose2x2(x, w) * y)
+    rhs = np.sum(x * nm.conv2d(y, w, 2, 0))        # w as KRSC with K=C_in, C=K_out
+    assert np.isclose(lhs, rhs)
+    G = rng.standard_normal((2, 6, 8, 6))
+    dx, dw = nm.conv_transpose2x2_backward(x, w, G)
+    f = lambda: float(np.sum(nm.conv_transpose2x2(x, w) * G))
+    for _ in range(5):
+        i = tuple(int(rng.integers(0, s)) for s in x.shape)
+        assert abs(_fd(f, x, i) - dx[i]) < 1e-6 * (1 + abs(dx[i]))
+        j = tuple(int(rng.integers(0, s)) for s in w.shape)
+        assert abs(_fd(f, w, j) - dw[j]) < 1e-6 * (1 + abs(dw[j]))
+
+
+def test_unet_gradients_finite_differences():
+    """U-Net pieces: concat-conv (two inputs), 2×2 max-pool with a skip consumer,
+    transposed conv, per-pixel softmax cross-entropy."""
+    spec = nets.unet(batch=2, image=8, base=4, depth=2, classes=3)
+    _fd_check_spec(spec, n_checks=24, tol=5e-5)
+
+
 def test_preact_resnet_gradients_finite_differences():
     """Pre-activation bottleneck blocks (add layer, BN on a tensor with two
     consumers, projection shortcuts): depth 11 = one block per stage."""

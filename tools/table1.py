@@ -74,11 +74,15 @@ def main():
         for row in a.rows.split(","):
             rec = {"batch": b, "ratio": round(r, 3), "row": row, "F_peak": F}
             if row == "incore":
-                if F > phys:
+                # no swapping: parameters/gradients/momentum device-resident
+                doc_i, info_i = graphs.build(spec, params="pinned")
+                Fi = B.Graph(doc_i).in_core_peak()
+                rec["F_peak"] = Fi
+                if Fi > phys:
                     rec["result"] = "x"
                     print(json.dumps(rec), flush=True)
                     continue
-                budget, W, mode, ph = F, 0, "best", F
+                budget, W, mode, ph = Fi, 0, "best", Fi
             else:
                 mode = row
                 budget, st = max_budget(G, phys, mode, chunk)
@@ -90,7 +94,8 @@ def main():
                 rec.update(budget_sched=budget, peak_phys_replay=st["peak_phys"], if_peak=st["if_peak"])
             try:
                 t0 = time.time()
-                stp, W, phys_used = bench.setup_step(spec, info, doc, budget, "va" if mode == "va" else "best", chunk,
+                d_, i_ = (doc_i, info_i) if row == "incore" else (doc, info)
+                stp, W, phys_used = bench.setup_step(spec, i_, d_, budget, "va" if mode == "va" else "best", chunk,
                                                      timeline=False, window=W)
                 stp.step()
                 ms = [stp.step()["step_ms"] for _ in range(a.steps)]
