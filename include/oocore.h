@@ -276,6 +276,10 @@ typedef struct oc_exec_options {
                               function into one SM-driven pack/unpack kernel that
                               copies 16-byte vectors between device memory and the
                               mapped pinned host copies; 0 = off */
+  uint32_t use_graph;      /* 1: after one eager step (all VA mappings memoised), capture
+                              the step's issue — copies, event waits, kernels, NCCL — into a
+                              CUDA graph once and replay it every later step; ignored with
+                              timeline */
 } oc_exec_options;
 
 typedef struct oc_step_metrics {

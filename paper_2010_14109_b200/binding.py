@@ -62,7 +62,7 @@ class oc_streams(C.Structure):
 
 class oc_exec_options(C.Structure):
     _fields_ = [("timeline", C.c_uint32), ("elide_clean", C.c_uint32), ("check", C.c_uint32),
-                ("pack_threshold", C.c_uint32)]
+                ("pack_threshold", C.c_uint32), ("use_graph", C.c_uint32)]
 
 
 class oc_step_metrics(C.Structure):

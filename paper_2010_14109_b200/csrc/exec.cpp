@@ -129,7 +129,10 @@ struct Exec {
   std::vector<Dep> deps;
   std::vector<int32_t> end_deps;
   std::vector<cudaEvent_t> ev_done, ev_in, ev_out;
-  cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_fork = nullptr;
+  cudaGraphExec_t gexec = nullptr;    // captured step (opt.use_graph)
+  uint64_t g_bytes_h2d = 0, g_bytes_d2h = 0;
+  uint32_t g_n_h2d = 0, g_n_d2h = 0, g_n_kernels = 0;
   bool have_prev = false;
   char* host = nullptr;
   uint64_t host_bytes = 0;
@@ -381,6 +384,7 @@ Status Exec::create(int dev, const Graph* graph, const Schedule* sch, MemPool* m
   OC_TRY(mk(ev_in, slots.size(), false));
   OC_TRY(mk(ev_out, deps.size(), false));
   OC_CUDA(cudaEventCreate(&ev_start));
+  OC_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
   OC_CUDA(cudaEventCreate(&ev_end));
   if (opt.timeline) {
     OC_TRY(mk(tl_fn0, n, true));
@@ -410,13 +414,17 @@ Status Exec::run(oc_step_metrics* out) {
   uint32_t n_h2d = 0, n_d2h = 0, n_kernels = 0;
   tl_in_used.assign(slots.size(), 0);
   tl_out_used.assign(deps.size(), 0);
-
-  OC_CUDA(cudaEventRecord(ev_start, cs));
-  // the previous step (incl. its end waits) is complete on the compute stream
-  OC_CUDA(cudaStreamWaitEvent(hs, ev_start, 0));
-  OC_CUDA(cudaStreamWaitEvent(ds, ev_start, 0));
   auto ev_of = [&](const Ref& r) { return r.type == Ref::DONE ? ev_done[r.idx] : ev_out[r.idx]; };
+
+  // The whole step is issued by `issue`: eagerly, or once into a CUDA graph
+  // (opt.use_graph, after one eager step has memoised every VA mapping) that
+  // later steps replay with a single launch.
   const uint32_t n = g->nf();
+  auto issue = [&]() -> Status {
+  // the previous step (incl. its end waits) is complete on the compute stream
+  OC_CUDA(cudaEventRecord(ev_fork, cs));
+  OC_CUDA(cudaStreamWaitEvent(hs, ev_fork, 0));
+  OC_CUDA(cudaStreamWaitEvent(ds, ev_fork, 0));
   for (uint32_t i = 0; i < n; ++i) {
     const FnSchedule& F = s->fn[i];
     XFn& X = fns[i];
@@ -542,6 +550,29 @@ Status Exec::run(oc_step_metrics* out) {
     for (uint32_t v : F.free) vars[v].cur_slot = -1;
   }
   for (int32_t d : end_deps) OC_CUDA(cudaStreamWaitEvent(cs, ev_out[d], 0));
+  return Status::ok();
+  };
+
+  if (opt.use_graph && !gexec && step_index >= 1 && !opt.timeline) {
+    const uint64_t maps_before = mem->n_driver_map;
+    OC_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    Status st = issue();
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+    if (!st.good()) return st;
+    if (ce != cudaSuccess) return cuda_status(ce, "cudaStreamEndCapture");
+    if (mem->n_driver_map != maps_before) return Status::make(OC_E_INVARIANT, "VA mapping changed during capture");
+    OC_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
+    cudaGraphDestroy(graph);
+    g_bytes_h2d = bytes_h2d; g_bytes_d2h = bytes_d2h; g_n_h2d = n_h2d; g_n_d2h = n_d2h; g_n_kernels = n_kernels;
+  }
+  OC_CUDA(cudaEventRecord(ev_start, cs));
+  if (gexec) {
+    OC_CUDA(cudaGraphLaunch(gexec, cs));
+    bytes_h2d = g_bytes_h2d; bytes_d2h = g_bytes_d2h; n_h2d = g_n_h2d; n_d2h = g_n_d2h; n_kernels = g_n_kernels;
+  } else {
+    OC_TRY(issue());
+  }
   OC_CUDA(cudaEventRecord(ev_end, cs));
   const double t_host1 = now_ms();
   OC_CUDA(cudaEventSynchronize(ev_end));
@@ -599,6 +630,8 @@ void Exec::destroy() {
   kill(ev_done); kill(ev_in); kill(ev_out);
   kill(tl_fn0); kill(tl_fn1); kill(tl_in0); kill(tl_in1); kill(tl_out0); kill(tl_out1);
   if (ev_start) cudaEventDestroy(ev_start);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (gexec) cudaGraphExecDestroy(gexec);
   if (ev_end) cudaEventDestroy(ev_end);
   if (host) cudaFreeHost(host);
   if (ws) cudaFree(ws);

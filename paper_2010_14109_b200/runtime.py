@@ -17,7 +17,7 @@ _NP = {"f32": np.float32, "i32": np.int32, "u8": np.uint8, "bf16": np.uint16}
 class OutOfCoreStep:
     def __init__(self, doc, budget, window=B.OC_WINDOW_MAX_FEASIBLE, mode="va", chunk_bytes=40 << 20,
                  phys_bytes=0, device=0, timeline=False, elide_clean=True, align=512, meta=None,
-                 pack_threshold=64 << 10):
+                 pack_threshold=64 << 10, use_graph=False):
         if not torch.cuda.is_available():
             raise RuntimeError("OutOfCoreStep needs a CUDA device (no CPU fallback)")
         self.device = device
@@ -45,7 +45,8 @@ class OutOfCoreStep:
                                       C.byref(self.mem), C.byref(err)), err)
         self.exec = B.P()
         ss = B.oc_streams(self.streams[0].cuda_stream, self.streams[1].cuda_stream, self.streams[2].cuda_stream)
-        opt = B.oc_exec_options(1 if timeline else 0, 1 if elide_clean else 0, 0, int(pack_threshold))
+        opt = B.oc_exec_options(1 if timeline else 0, 1 if elide_clean else 0, 0, int(pack_threshold),
+                                1 if use_graph else 0)
         B.check(B.lib().oc_exec_create(device, self.graph.h, self.sched.h, self.mem, C.byref(ss), C.byref(opt),
                                        C.byref(self.exec), C.byref(err)), err)
         # device-resident (pinned) variables live in torch tensors bound to the executor

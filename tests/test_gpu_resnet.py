@@ -161,6 +161,36 @@ def test_resnet18_bench_size_swap_transparency():
 
 
 @pytest.mark.gpu
+def test_cuda_graph_replay_equals_eager():
+    """opt.use_graph: after one eager step the step is captured into a CUDA
+    graph and replayed; three steps (eager + capture + replay) must equal
+    three eager steps bitwise, with swaps happening in every step."""
+    from paper_2010_14109_b200.runtime import OutOfCoreStep
+    spec = nets.tiny_resnet(batch=4, image=16, classes=10)
+    doc, info = graphs.build(spec, params="persistent")
+    G = B.Graph(doc)
+    peak = G.in_core_peak()
+    budget = max(G.min_feasible_budget(0), int(peak * 0.5))
+    x, y = nets.make_inputs(spec)
+    p = nets.make_params(spec)
+    res = []
+    for use_graph in (False, True):
+        st = OutOfCoreStep(doc, budget, B.OC_WINDOW_MAX_FEASIBLE, mode="va", chunk_bytes=2 * MiB,
+                           phys_bytes=256 * MiB, use_graph=use_graph)
+        st.write(info["x"], to_bf16_bits(x))
+        st.write(info["labels"], y)
+        for k, v in p.items():
+            st.write(info["params"][k], v)
+            st.write(info["momentum"][k], np.zeros_like(v))
+        mets = [st.step() for _ in range(3)]
+        assert all(m["bytes_d2h"] > 0 for m in mets)
+        res.append({k: st.read(info["params"][k]) for k in p})
+        st.close()
+    for k in p:
+        assert np.array_equal(res[0][k], res[1][k]), k
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["va", "best"])
 def test_tiny_resnet_parity_and_transparency(mode):
     spec = nets.tiny_resnet(batch=4, image=16, classes=10)
