@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--chunk-mib", type=int, default=2)
     ap.add_argument("--no-incore", action="store_true")
     ap.add_argument("--window", default="auto", help="auto | max | <bytes>")
+    ap.add_argument("--no-graph", action="store_true", help="issue every step eagerly (no CUDA graph replay)")
     return ap.parse_args()
 
 
@@ -130,7 +131,7 @@ def trainable_batch(spec_fn, budget, lo=1, hi=4096, params="pinned"):
     return lo
 
 
-def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None, pack=64 << 10):
+def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None, pack=64 << 10, use_graph=False):
     import torch
     from paper_2010_14109_b200 import binding as B
     from paper_2010_14109_b200.runtime import OutOfCoreStep
@@ -143,7 +144,7 @@ def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None,
     ps = probe.stats()
     phys = ps["peak_phys"] + chunk if mode == "va" else max(ps["peak_phys"], 1)
     st = OutOfCoreStep(doc, budget, W, mode=mode, chunk_bytes=chunk, phys_bytes=phys, timeline=timeline,
-                       pack_threshold=pack)
+                       pack_threshold=pack, use_graph=use_graph)
     x, y = nets.make_inputs(spec)
     p = nets.make_params(spec)
     if spec["mode"] == "bf16":
@@ -217,7 +218,10 @@ def run_ours(args, rank, world):
     # timed steps run without per-event instrumentation (timing events between
     # back-to-back copies cost ~6% of the step); a second, instrumented pass
     # below measures overlap, link busy time and the per-kernel durations
-    st, W, phys = setup_step(spec, info, doc, budget, args.mode, chunk, timeline=False, window=W_sel)
+    # the timed steps replay the step as one CUDA graph (captured after the first
+    # warm-up step memoised every VA mapping); --no-graph issues it eagerly
+    st, W, phys = setup_step(spec, info, doc, budget, args.mode, chunk, timeline=False, window=W_sel,
+                             use_graph=not args.no_graph)
     uid = None
     if world > 1:
         uid = [nccl_unique_id() if rank == 0 else None]
@@ -338,7 +342,7 @@ def run_ours(args, rank, world):
         "config": dict(cfg, global_batch=B_glob, per_gpu_batch=spec["batch"], budget_bytes=budget,
                        in_core_footprint_bytes=F_peak, window_bytes=W, window_max_feasible=wmax,
                        window_selection=window_probe or args.window, allocator=args.mode, chunk_bytes=chunk,
-                       phys_pool_bytes=phys, parallelism=f"dp{world}",
+                       phys_pool_bytes=phys, parallelism=f"dp{world}", cuda_graph_replay=not args.no_graph,
                        l2_flush="inputs larger than L2 (activations GBs per step)"),
         "clocks": clk.summary(),
         "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
