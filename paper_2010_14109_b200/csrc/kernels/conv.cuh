@@ -6,16 +6,22 @@ namespace oc {
 
 struct ConvGeom {
   int N, H, W, C, K, R, S, st, pad, P, Q;
+  int Cw;   // channels of the weight tensor W[K][R][S][Cw], Cw <= C: activation
+            // channels past Cw are zero padding (a narrow stem input stored in
+            // 16-byte pixels, attrs "Cw"); default Cw = C
+  int pad_slice;  // narrow inputs: images per zero-padding slice (attrs
+                  // "pad_slice"; 0 = as many as fit 32 MiB)
 };
 
 inline ConvGeom conv_geom(const OpArgs& a) {
   return ConvGeom{(int)A(a, "N"), (int)A(a, "H"), (int)A(a, "W"), (int)A(a, "C"), (int)A(a, "K"), (int)A(a, "R"),
-                  (int)A(a, "S"), (int)A(a, "stride"), (int)A(a, "pad"), (int)A(a, "P"), (int)A(a, "Q")};
+                  (int)A(a, "S"), (int)A(a, "stride"), (int)A(a, "pad"), (int)A(a, "P"), (int)A(a, "Q"),
+                  (int)A(a, "Cw", A(a, "C")), (int)A(a, "pad_slice", 0)};
 }
 inline ConvGeom conv_geom(const JVal& j) {
   return ConvGeom{(int)j.geti("N"), (int)j.geti("H"), (int)j.geti("W"), (int)j.geti("C"), (int)j.geti("K"),
                   (int)j.geti("R"), (int)j.geti("S"), (int)j.geti("stride"), (int)j.geti("pad"), (int)j.geti("P"),
-                  (int)j.geti("Q")};
+                  (int)j.geti("Q"), (int)j.geti("Cw", j.geti("C")), (int)j.geti("pad_slice", 0)};
 }
 
 // CUDA-core implicit GEMM (conv_simt.cu); T = __nv_bfloat16 or float

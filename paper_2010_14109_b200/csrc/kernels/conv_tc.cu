@@ -13,14 +13,16 @@
 //   wgrad  D[(r,s,c)][k]          = Σ_{m=(n,p,q)} X[n,p·st−pad+r,q·st−pad+s,c] · dY[m,k]
 //          both operands MN-major (contiguous along channels), deterministic
 //          split-K over m (fixed slices, fixed-order sum), then dW[k][(r,s,c)]
-//   narrow-channel stem (C=3): A is gathered element by element into
-//          registers and stored as swizzled 16-byte chunks (REG variants).
+//   narrow inputs (C % 64 != 0, C % 8 == 0): each 16-byte chunk of a K-block
+//          is its own (tap, 8 channels); a 3-channel input is first re-laid out
+//          slice by slice into 8-channel pixels (zero-padded, weight Cw = 3).
 //
 // Tile: UMMA M = 128, N = BN (64 or 128), K-block 64 (one 128-byte swizzle
 // row of bf16).  CTA: warps 0-3 gather and run the epilogue, warp 4 issues
-// the MMAs from one lane.  3 stages of 16 KB + BN·128 B, so two CTAs share an
-// SM and one's epilogue overlaps the other's main loop.  Address arithmetic
-// in the producers is hoisted out of the K loop (rows fixed per thread) and
+// the MMAs from one lane.  96 KB of stages (4 at BN=64, 3 at BN=128), each
+// filled by cp.async with completion tracked by the stage's mbarrier
+// (cp.async.mbarrier.arrive.noinc), so two CTAs share an SM and one's
+// epilogue overlaps the other's main loop.  Address arithmetic in the producers is hoisted out of the K loop (rows fixed per thread) and
 // what remains uses 32-bit multiply-shift division (FastDiv).
 #include "conv.cuh"
 
@@ -28,7 +30,9 @@ namespace oc {
 
 namespace tc {
 
-constexpr int BM = 128, BKE = 64, STAGES = 3, NPROD = 128, NTHREADS = 160;
+constexpr int BM = 128, BKE = 64, NPROD = 128, NTHREADS = 160;
+// pipeline depth: 96 KB of stages either way, so two CTAs share an SM
+__host__ __device__ constexpr int stages_for(int bn) { return bn == 64 ? 4 : 3; }
 
 // n / d for 0 <= n < 2^31 by multiply-high and shift (Granlund–Montgomery)
 struct FastDiv {
@@ -74,10 +78,6 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void st_shared16(uint32_t dst, const uint32_t (&v)[4]) {
-  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
-               : "memory");
-}
 
 // shared-memory matrix descriptor, SWIZZLE_128B (PTX ISA tcgen05 "matrix descriptor")
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -132,19 +132,22 @@ struct Params {
   int r0, s0, nr, ns;          // dgrad taps: r = r0 + st·i (i < nr), s = s0 + st·j (j < ns)
   int kpad;                    // fprop: padded RSC (row pitch of W_bf16)
   int kch;                     // fprop: C; dgrad: K (channels reduced per tap)
+  int narrow;                  // fprop, C % 64 != 0 (C % 8 == 0): each 16-byte chunk of a
+                               // K-block is its own (tap, c0); chunks past R·S·C are zero
   FastDiv fQ, fP, fWp, fHp, fC, fS, fKch, fns;
 };
 
-template <int MODE, int BN, bool REG>
+template <int MODE, int BN>
 __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
+  constexpr int NST = stages_for(BN);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   constexpr int A_BYTES = BM * BKE * 2;    // 16 KB
   constexpr int B_BYTES = BN * BKE * 2;
   constexpr int STAGE = A_BYTES + B_BYTES;
-  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* full = (uint64_t*)(smem + NST * STAGE);
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;
   uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], NPROD); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], NPROD); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -182,9 +185,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
     int rh[8], rw[8];            // fprop: h0, w0 of the output pixel; dgrad: pbase, qbase
     int64_t rbase[8];            // element offset of the row's (n, h0, w0) / (n, pbase, qbase)
     bool rok[8];
-    int er[8], es[8], ec[8];     // REG / WGRAD: fixed (r,s,c) of this thread's MN elements
-    bool ev[8];
-    int w_r = 0, w_s = 0, w_c = 0;
+    int w_r = 0, w_s = 0, w_c = 0;   // WGRAD: fixed (r,s,c) of this thread's 8 MN elements
     bool w_ok = false;
     if (MODE == FPROP || MODE == DGRAD) {
 #pragma unroll
@@ -213,75 +214,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
       }
     }
     if (MODE == WGRAD) {
-      if (REG) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int rsc = m0 + (tid & 15) * 8 + e;
-          ev[e] = rsc < P.M;
-          const int rs = (int)P.fC.div(ev[e] ? rsc : 0);
-          ec[e] = (ev[e] ? rsc : 0) - rs * g.C;
-          er[e] = (int)P.fS.div(rs);
-          es[e] = rs - er[e] * g.S;
-        }
-      } else {
-        const int rsc = m0 + (tid & 15) * 8;
-        w_ok = rsc < P.M;
-        const int rs = (int)P.fC.div(w_ok ? rsc : 0);
-        w_c = (w_ok ? rsc : 0) - rs * g.C;
-        w_r = (int)P.fS.div(rs);
-        w_s = rs - w_r * g.S;
-      }
-    }
-    if (REG && MODE == FPROP) {
-      // rows need n, h0, w0 (computed above); per K-block the 8 (r,s,c) of chunk ch
+      const int rsc = m0 + (tid & 15) * 8;
+      w_ok = rsc < P.M;
+      const int rs = (int)P.fC.div(w_ok ? rsc : 0);
+      w_c = (w_ok ? rsc : 0) - rs * g.C;
+      w_r = (int)P.fS.div(rs);
+      w_s = rs - w_r * g.S;
     }
 
     for (int it = 0; it < nkb; ++it) {
-      const int s = it % STAGES;
-      if (it >= STAGES) mbar_wait(&empty[s], (uint32_t)((it / STAGES - 1) & 1));
+      const int s = it % NST;
+      if (it >= NST) mbar_wait(&empty[s], (uint32_t)((it / NST - 1) & 1));
       const uint32_t a_base = smem_u32(smem + s * STAGE);
       const uint32_t b_base = a_base + A_BYTES;
       const int kb = kb_begin + it;
-      if (REG && MODE == FPROP) {
-        const int RSC = g.R * g.S * g.C;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int kk = kb * BKE + ch * 8 + e;
-          ev[e] = kk < RSC;
-          const int rs = (int)P.fC.div(ev[e] ? kk : 0);
-          ec[e] = (ev[e] ? kk : 0) - rs * g.C;
-          er[e] = (int)P.fS.div(rs);
-          es[e] = rs - er[e] * g.S;
-        }
-        const unsigned short* xs = reinterpret_cast<const unsigned short*>(P.act);
-#pragma unroll 2
-        for (int i = 0; i < 8; ++i) {
-          const int row = (tid >> 3) + 16 * i;
-          uint32_t packed[4] = {0u, 0u, 0u, 0u};
-          if (rok[i]) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int h = rh[i] + er[e], w = rw[i] + es[e];
-              unsigned short v = 0;
-              if (ev[e] && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W)
-                v = __ldg(xs + rbase[i] + ((int64_t)h * g.W + w) * g.C + ec[e]);
-              packed[e >> 1] |= (uint32_t)v << (16 * (e & 1));
-            }
-          }
-          st_shared16(a_base + row * 128 + ((ch ^ (row & 7)) << 4), packed);
-        }
-#pragma unroll
-        for (int i = 0; i < BN / 16; ++i) {
-          const int row = (tid >> 3) + 16 * i;
-          const int nn = n0 + row;
-          const bool ok = nn < P.N;
-          cp_async16(b_base + row * 128 + ((ch ^ (row & 7)) << 4),
-                     ok ? P.wgt + (int64_t)nn * P.kpad + kb * BKE + ch * 8 : P.wgt, ok);
-        }
-      } else if (MODE == FPROP || MODE == DGRAD) {
-        // K-block kb covers one tap and 64 consecutive reduced channels (kch % 64 == 0)
+      if (MODE == FPROP || MODE == DGRAD) {
+        // K-block kb covers one tap and 64 consecutive reduced channels (kch % 64 == 0),
+        // or, narrow, 8 chunks each of its own tap
         const int kk0 = kb * BKE;
-        const int tap = (int)P.fKch.div(kk0), c0 = kk0 - tap * P.kch;
+        const int kt = P.narrow ? kk0 + ch * 8 : kk0;
+        const bool kok = !P.narrow || kt < g.R * g.S * g.C;
+        const int tap = (int)P.fKch.div(kt), c0 = kt - tap * P.kch + (P.narrow ? 0 : ch * 8);
         int dr, ds;   // fprop: r, s; dgrad: tap indices i, j
         if (MODE == FPROP) { dr = (int)P.fS.div(tap); ds = tap - dr * g.S; }
         else { dr = (int)P.fns.div(tap); ds = tap - dr * P.ns; }
@@ -292,12 +245,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
           const __nv_bfloat16* src;
           if (MODE == FPROP) {
             const int h = rh[i] + dr, w = rw[i] + ds;
-            ok = rok[i] && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W;
-            src = P.act + rbase[i] + ((int64_t)h * g.W + w) * g.C + c0 + ch * 8;
+            ok = kok && rok[i] && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W;
+            src = P.act + rbase[i] + ((int64_t)h * g.W + w) * g.C + c0;
           } else {
             const int p = rh[i] - dr, q = rw[i] - ds;
             ok = rok[i] && (unsigned)p < (unsigned)g.P && (unsigned)q < (unsigned)g.Q;
-            src = P.act + rbase[i] + ((int64_t)p * g.Q + q) * g.K + c0 + ch * 8;
+            src = P.act + rbase[i] + ((int64_t)p * g.Q + q) * g.K + c0;
           }
           cp_async16(a_base + row * 128 + ((ch ^ (row & 7)) << 4), ok ? src : P.act, ok);
         }
@@ -311,7 +264,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
           const bool ok = nn < P.N;
           const __nv_bfloat16* src;
           if (MODE == FPROP) src = P.wgt + (int64_t)nn * P.kpad + kk0 + ch * 8;
-          else src = P.wgt + ((int64_t)nn * g.R * g.S + r * g.S + sx) * g.K + c0 + ch * 8;
+          else src = P.wgt + ((int64_t)nn * g.R * g.S + r * g.S + sx) * g.K + c0;
           cp_async16(b_base + row * 128 + ((ch ^ (row & 7)) << 4), ok ? src : P.wgt, ok);
         }
       } else {
@@ -333,26 +286,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
           const int h0 = p * g.st - g.pad, w0 = q * g.st - g.pad;
           const int row = kr & 7;
           const uint32_t dst = a_base + (kr >> 3) * 2048 + (j >> 3) * 1024 + row * 128 + (((j & 7) ^ row) << 4);
-          if (REG) {
-            uint32_t packed[4] = {0u, 0u, 0u, 0u};
-            if (mok) {
-              const unsigned short* xs = reinterpret_cast<const unsigned short*>(P.act) + (int64_t)n * g.H * g.W * g.C;
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int h = h0 + er[e], w = w0 + es[e];
-                unsigned short v = 0;
-                if (ev[e] && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W)
-                  v = __ldg(xs + ((int64_t)h * g.W + w) * g.C + ec[e]);
-                packed[e >> 1] |= (uint32_t)v << (16 * (e & 1));
-              }
-            }
-            st_shared16(dst, packed);
-          } else {
-            const int h = h0 + w_r, w = w0 + w_s;
-            const bool ok = mok && w_ok && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W;
-            const __nv_bfloat16* src = P.act + (((int64_t)n * g.H + h) * g.W + w) * g.C + w_c;
-            cp_async16(dst, ok ? src : P.act, ok);
-          }
+          const int h = h0 + w_r, w = w0 + w_s;
+          const bool ok = mok && w_ok && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W;
+          const __nv_bfloat16* src = P.act + (((int64_t)n * g.H + h) * g.W + w) * g.C + w_c;
+          cp_async16(dst, ok ? src : P.act, ok);
         }
         constexpr int BCH = BN / 8;
 #pragma unroll
@@ -369,24 +306,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
           cp_async16(dst, ok ? src : P.wgt, ok);
         }
       }
-      cp_commit();
-      if (it >= 1) {
-        cp_wait<1>();
-        fence_async_smem();
-        mbar_arrive(&full[(it - 1) % STAGES]);
-      }
-    }
-    if (nkb > 0) {
-      cp_wait<0>();
-      fence_async_smem();
-      mbar_arrive(&full[(nkb - 1) % STAGES]);
+      // the stage's full barrier receives this thread's arrival when its copies
+      // land (no wait here: the producer runs ahead by up to NST stages)
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s])) : "memory");
     }
   } else if (warp == 4) {
     // ------------------------------------------------------------ MMA issuer (one elected lane)
     constexpr uint32_t ID = idesc(BN, MODE == WGRAD, MODE == WGRAD);
     for (int it = 0; it < nkb; ++it) {
-      const int s = it % STAGES;
-      mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
+      const int s = it % NST;
+      mbar_wait(&full[s], (uint32_t)((it / NST) & 1));
+      fence_async_smem();   // cp.async (generic proxy) writes -> tcgen05 operand reads
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (lane == 0) {
         const uint32_t a_base = smem_u32(smem + s * STAGE);
@@ -490,9 +420,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
   }
 }
 
-// fp32 KRSC master -> bf16 [K][kpad] (fprop; zero padding past RSC) or [C][R][S][K] (dgrad)
+// fp32 KRSC master -> bf16 [K][kpad] (fprop; (r,s,c) over the activation's C
+// channels, zero past Cw and past RSC) or [C][R][S][K] (dgrad, Cw = C)
 __global__ void weight_bf16(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int K, int RS, int C,
-                            int transpose, int kpad) {
+                            int transpose, int kpad, int Cw) {
   const int64_t n = transpose ? (int64_t)K * RS * C : (int64_t)K * kpad;
   const int rsc = RS * C;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -503,26 +434,32 @@ __global__ void weight_bf16(const float* __restrict__ w, __nv_bfloat16* __restri
       out[((int64_t)c * RS + rs) * K + k] = __float2bfloat16_rn(w[i]);
     } else {
       const int64_t k = i / kpad, j = i % kpad;
-      out[i] = j < rsc ? __float2bfloat16_rn(w[k * rsc + j]) : __float2bfloat16_rn(0.f);
+      const int rs = (int)(j / C), c = (int)(j % C);
+      out[i] = (j < rsc && c < Cw) ? __float2bfloat16_rn(w[(k * RS + rs) * Cw + c]) : __float2bfloat16_rn(0.f);
     }
   }
 }
 
-__global__ void wgrad_reduce(int splits, int RSC, int K, const float* __restrict__ part, float* __restrict__ dw) {
+// dW[k][(r,s,c)] = Σ_z part[z][(r,s,c)][k] in split order; partial rows of the
+// padding channels c >= Cw are dropped
+__global__ void wgrad_reduce(int splits, int RSC, int K, int C, int Cw, const float* __restrict__ part,
+                             float* __restrict__ dw) {
   const int64_t n = (int64_t)RSC * K;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int k = (int)(i % K);
-    const int64_t rsc = i / K;
+    const int rsc = (int)(i / K);
+    const int rs = rsc / C, c = rsc - rs * C;
+    if (c >= Cw) continue;
     float s = 0.f;
     for (int zz = 0; zz < splits; ++zz) s += part[(int64_t)zz * n + i];
-    dw[(int64_t)k * RSC + rsc] = s;
+    dw[(int64_t)k * (RSC / C) * Cw + rs * Cw + c] = s;
   }
 }
 
-template <int MODE, int BN, bool REG = false>
+template <int MODE, int BN>
 Status launch(OpArgs& a, const Params& P, dim3 grid) {
-  constexpr int smem = STAGES * (BM * BKE * 2 + BN * BKE * 2) + 1024 + 256;
-  auto kern = conv_tc_kernel<MODE, BN, REG>;
+  constexpr int smem = stages_for(BN) * (BM * BKE * 2 + BN * BKE * 2) + 1024 + 256;
+  auto kern = conv_tc_kernel<MODE, BN>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -561,51 +498,122 @@ using namespace tc;
 bool conv_tc_ok(const ConvGeom& g, int mode) {
   // 32-bit element indices of the activations (the 64-bit tensor offsets are formed per row)
   if ((int64_t)g.N * g.H * g.W * g.C >= (1ll << 31) || (int64_t)g.N * g.P * g.Q * g.K >= (1ll << 31)) return false;
-  if (mode == FPROP) return g.K % 64 == 0 && (g.C % 64 == 0 || g.C < 64);
+  // zero-padded activation channels (Cw < C) only on the 16-byte-chunk paths
+  if (g.Cw != g.C && (g.C % 8 != 0 || g.Cw > g.C || mode == DGRAD)) return false;
   if (mode == DGRAD) return g.K % 64 == 0 && g.C % 64 == 0 && (g.st == 1 || g.st == 2);
   return g.K % 64 == 0;
 }
 
-static int kpad_of(const ConvGeom& g) { return (g.R * g.S * g.C + BKE - 1) / BKE * BKE; }
+namespace {
 
-size_t conv_tc_ws(const ConvGeom& g, int mode) {
-  size_t wbytes = (size_t)g.K * kpad_of(g) * 2;
-  if (mode == WGRAD) {
-    const int BN = g.K % 128 == 0 ? 128 : 64;
-    return (size_t)wgrad_splits(g, BN) * g.R * g.S * g.C * g.K * 4;
-  }
-  return (wbytes + 255) / 256 * 256;
+int kpad_of(const ConvGeom& g) { return (g.R * g.S * g.C + BKE - 1) / BKE * BKE; }
+size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+
+// Narrow input (C % 8 != 0, the 3-channel network input): the kernels see a
+// copy in 16-byte-aligned pixels of C8 channels (zero past C, weight channels
+// Cw = C), written into the workspace one slice of images at a time so the
+// copy stays small and is never part of the budgeted memory.
+struct Narrow {
+  bool on;
+  ConvGeom gk;        // the geometry the kernels run (C = C8, Cw = C)
+  int64_t slice;      // images per slice
+  size_t slice_bytes;
+};
+Narrow narrow_of(const ConvGeom& g) {
+  Narrow n{g.C % 8 != 0, g, g.N, 0};
+  if (!n.on) return n;
+  n.gk.C = (g.C + 7) / 8 * 8;
+  n.gk.Cw = g.C;
+  const int64_t per = (int64_t)g.H * g.W * n.gk.C * 2;
+  n.slice = g.pad_slice > 0 ? g.pad_slice : (32ll << 20) / per;
+  if (n.slice < 1) n.slice = 1;
+  if (n.slice > g.N) n.slice = g.N;
+  n.slice_bytes = align256((size_t)(n.slice * per));
+  return n;
 }
 
-Status conv_fprop_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y,
-                     bool accumulate) {
-  __nv_bfloat16* wb = (__nv_bfloat16*)a.ws;
-  const bool reg = g.C % 64 != 0;
-  const int kpad = kpad_of(g);
-  weight_bf16<<<grid_for((int64_t)g.K * kpad, 256, 4), 256, 0, a.stream>>>(w, wb, g.K, g.R * g.S, g.C, 0, kpad);
+__global__ void pad_pixels(int64_t rows, int C, int C8, const __nv_bfloat16* __restrict__ x,
+                           __nv_bfloat16* __restrict__ out) {
+  const unsigned short* xs = reinterpret_cast<const unsigned short*>(x);
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    for (int c0 = 0; c0 < C8; c0 += 8) {
+      uint32_t v[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (c0 + e < C) v[e >> 1] |= (uint32_t)xs[r * C + c0 + e] << (16 * (e & 1));
+      *reinterpret_cast<uint4*>(out + r * C8 + c0) = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+  }
+}
+
+Status pad_slice(OpArgs& a, const Narrow& nw, int64_t n0, int64_t nn, const __nv_bfloat16* x,
+                 __nv_bfloat16* buf) {
+  const ConvGeom& g = nw.gk;
+  const int64_t rows = nn * g.H * g.W;
+  pad_pixels<<<grid_for(rows, 256, 2), 256, 0, a.stream>>>(rows, g.Cw, g.C, x + n0 * g.H * g.W * g.Cw, buf);
   OC_LAUNCH_CHECK(a);
-  Params P{};
-  P.g = g;
-  P.act = x;
-  P.wgt = wb;
-  P.out = y;
-  P.M = g.N * g.P * g.Q;
-  P.N = g.K;
-  P.kpad = kpad;
-  P.kch = g.C;
-  P.nkb = kpad / BKE;
-  P.accumulate = accumulate ? 1 : 0;
-  fill_divs(P);
-  const dim3 grid((P.M + BM - 1) / BM, g.K / (g.K % 128 == 0 ? 128 : 64), 1);
-  if (reg) return g.K % 128 == 0 ? launch<FPROP, 128, true>(a, P, grid) : launch<FPROP, 64, true>(a, P, grid);
-  return g.K % 128 == 0 ? launch<FPROP, 128>(a, P, grid) : launch<FPROP, 64>(a, P, grid);
+  return Status::ok();
+}
+
+int wgrad_bn(const ConvGeom& g) { return g.K % 128 == 0 ? 128 : 64; }
+
+}  // namespace
+
+size_t conv_tc_ws(const ConvGeom& g0, int mode) {
+  const Narrow nw = narrow_of(g0);
+  const ConvGeom& g = nw.gk;
+  if (mode == WGRAD) {
+    ConvGeom gs = g;
+    gs.N = (int)nw.slice;
+    const int64_t nsl = (g.N + nw.slice - 1) / nw.slice;
+    return align256((size_t)nsl * wgrad_splits(gs, wgrad_bn(g)) * g.R * g.S * g.C * g.K * 4) + nw.slice_bytes;
+  }
+  return align256((size_t)g.K * kpad_of(g) * 2) + nw.slice_bytes;
+}
+
+Status conv_fprop_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y,
+                     bool accumulate) {
+  const Narrow nw = narrow_of(g0);
+  const ConvGeom& g = nw.gk;
+  __nv_bfloat16* wb = (__nv_bfloat16*)a.ws;
+  const int kpad = kpad_of(g);
+  __nv_bfloat16* xbuf = (__nv_bfloat16*)((char*)a.ws + align256((size_t)g.K * kpad * 2));
+  weight_bf16<<<grid_for((int64_t)g.K * kpad, 256, 4), 256, 0, a.stream>>>(w, wb, g.K, g.R * g.S, g.C, 0, kpad,
+                                                                            g.Cw);
+  OC_LAUNCH_CHECK(a);
+  for (int64_t n0 = 0; n0 < g.N; n0 += nw.slice) {
+    const int64_t nn = g.N - n0 < nw.slice ? g.N - n0 : nw.slice;
+    Params P{};
+    P.g = g;
+    P.g.N = (int)nn;
+    P.act = x;
+    if (nw.on) {
+      Status st = pad_slice(a, nw, n0, nn, x, xbuf);
+      if (!st.good()) return st;
+      P.act = xbuf;
+    }
+    P.wgt = wb;
+    P.out = y + n0 * g.P * g.Q * g.K;
+    P.M = (int)(nn * g.P * g.Q);
+    P.N = g.K;
+    P.kpad = kpad;
+    P.kch = g.C;
+    P.narrow = g.C % 64 != 0 ? 1 : 0;
+    P.nkb = kpad / BKE;
+    P.accumulate = accumulate ? 1 : 0;
+    fill_divs(P);
+    const dim3 grid((P.M + BM - 1) / BM, g.K / (g.K % 128 == 0 ? 128 : 64), 1);
+    Status st = g.K % 128 == 0 ? launch<FPROP, 128>(a, P, grid) : launch<FPROP, 64>(a, P, grid);
+    if (!st.good()) return st;
+  }
+  return Status::ok();
 }
 
 Status conv_dgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const float* w, __nv_bfloat16* dx,
                      bool accumulate) {
   __nv_bfloat16* wt = (__nv_bfloat16*)a.ws;
   const int64_t nw = (int64_t)g.K * g.R * g.S * g.C;
-  weight_bf16<<<grid_for(nw, 256, 4), 256, 0, a.stream>>>(w, wt, g.K, g.R * g.S, g.C, 1, 0);
+  weight_bf16<<<grid_for(nw, 256, 4), 256, 0, a.stream>>>(w, wt, g.K, g.R * g.S, g.C, 1, 0, g.C);
   OC_LAUNCH_CHECK(a);
   for (int ph = 0; ph < g.st; ++ph)
     for (int pw = 0; pw < g.st; ++pw) {
@@ -638,27 +646,44 @@ Status conv_dgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, cons
   return Status::ok();
 }
 
-Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* x, float* dw) {
-  const int BN = g.K % 128 == 0 ? 128 : 64;
-  const int splits = wgrad_splits(g, BN);
-  Params P{};
-  P.g = g;
-  P.act = x;
-  P.wgt = dy;
-  P.out = a.ws;
-  P.M = g.R * g.S * g.C;
-  P.N = g.K;
-  P.gemm_k = g.N * g.P * g.Q;
-  const int kbs = (P.gemm_k + BKE - 1) / BKE;
-  P.kb_per_split = (kbs + splits - 1) / splits;
-  P.nkb = P.kb_per_split;
-  fill_divs(P);
-  dim3 grid((P.M + BM - 1) / BM, g.K / BN, splits);
-  Status st;
-  if (g.C % 8 != 0) st = BN == 128 ? launch<WGRAD, 128, true>(a, P, grid) : launch<WGRAD, 64, true>(a, P, grid);
-  else st = BN == 128 ? launch<WGRAD, 128>(a, P, grid) : launch<WGRAD, 64>(a, P, grid);
-  if (!st.good()) return st;
-  wgrad_reduce<<<grid_for((int64_t)P.M * g.K, 256, 4), 256, 0, a.stream>>>(splits, P.M, g.K, (const float*)a.ws, dw);
+Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* dy, const __nv_bfloat16* x, float* dw) {
+  const Narrow nw = narrow_of(g0);
+  const ConvGeom& g = nw.gk;
+  const int BN = wgrad_bn(g);
+  ConvGeom gs = g;
+  gs.N = (int)nw.slice;
+  const int splits = wgrad_splits(gs, BN);
+  const int64_t nsl = (g.N + nw.slice - 1) / nw.slice;
+  const int RSC = g.R * g.S * g.C;
+  float* part = (float*)a.ws;
+  __nv_bfloat16* xbuf = (__nv_bfloat16*)((char*)a.ws + align256((size_t)nsl * splits * RSC * g.K * 4));
+  for (int64_t sl = 0; sl < nsl; ++sl) {
+    const int64_t n0 = sl * nw.slice;
+    const int64_t nn = g.N - n0 < nw.slice ? g.N - n0 : nw.slice;
+    Params P{};
+    P.g = g;
+    P.g.N = (int)nn;
+    P.act = x;
+    if (nw.on) {
+      Status st = pad_slice(a, nw, n0, nn, x, xbuf);
+      if (!st.good()) return st;
+      P.act = xbuf;
+    }
+    P.wgt = dy + n0 * g.P * g.Q * g.K;
+    P.out = part + sl * splits * (int64_t)RSC * g.K;
+    P.M = RSC;
+    P.N = g.K;
+    P.gemm_k = (int)(nn * g.P * g.Q);
+    const int kbs = (P.gemm_k + BKE - 1) / BKE;
+    P.kb_per_split = (kbs + splits - 1) / splits;
+    P.nkb = P.kb_per_split;
+    fill_divs(P);
+    dim3 grid((P.M + BM - 1) / BM, g.K / BN, splits);
+    Status st = BN == 128 ? launch<WGRAD, 128>(a, P, grid) : launch<WGRAD, 64>(a, P, grid);
+    if (!st.good()) return st;
+  }
+  wgrad_reduce<<<grid_for((int64_t)RSC * g.K, 256, 4), 256, 0, a.stream>>>((int)(nsl * splits), RSC, g.K, g.C, g.Cw,
+                                                                          part, dw);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }

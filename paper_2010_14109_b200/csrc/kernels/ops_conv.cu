@@ -3,8 +3,9 @@
 // of the U-Net decoder expressed through the same kernels (a transposed conv
 // is the data gradient of the strided conv it inverts).  bf16 activations
 // dispatch to the tcgen05 tensor-core implicit GEMM (conv_tc.cu) when the
-// shape fits its tiling (channels in multiples of 64; the 3-channel stem
-// gathers into registers), else to the CUDA-core implicit GEMM
+// shape fits its tiling (channels in multiples of 64, or of 8 with one tap
+// per 16-byte chunk — the stem input zero-padded to 8 channels, attrs Cw = 3;
+// other narrow inputs gather into registers), else to the CUDA-core implicit GEMM
 // (conv_simt.cu).  fp32 activations (attrs.dtype = "f32", the 1e-5 parity
 // mode) always run on CUDA cores — no TF32.  attrs.impl = "simt" or
 // OC_CONV_IMPL=simt force CUDA cores.
@@ -35,23 +36,33 @@ bool force_simt(const OpArgs* a) {
 }
 bool f32(const OpArgs& a) { return As(a, "dtype", "bf16") == "f32"; }
 
+Status padded_unsupported() {
+  return Status::make(OC_E_UNSUPPORTED, "conv: zero-padded input channels (Cw < C) need the tensor-core path");
+}
+
 // y = conv(x, w) (+ y when accumulating)
 Status fprop(OpArgs& a, const ConvGeom& g, const void* x, const float* w, void* y, bool acc) {
+  if (f32(a) && g.Cw != g.C) return padded_unsupported();
   if (f32(a)) return conv_fprop_simt<float>(a, g, (const float*)x, w, (float*)y, acc);
   if (!force_simt(&a) && conv_tc_ok(g, 0))
     return conv_fprop_tc(a, g, (const __nv_bfloat16*)x, w, (__nv_bfloat16*)y, acc);
+  if (g.Cw != g.C) return padded_unsupported();
   return conv_fprop_simt<__nv_bfloat16>(a, g, (const __nv_bfloat16*)x, w, (__nv_bfloat16*)y, acc);
 }
 Status dgrad(OpArgs& a, const ConvGeom& g, const void* dy, const float* w, void* dx, bool acc) {
+  if (f32(a) && g.Cw != g.C) return padded_unsupported();
   if (f32(a)) return conv_dgrad_simt<float>(a, g, (const float*)dy, w, (float*)dx, acc);
   if (!force_simt(&a) && conv_tc_ok(g, 1))
     return conv_dgrad_tc(a, g, (const __nv_bfloat16*)dy, w, (__nv_bfloat16*)dx, acc);
+  if (g.Cw != g.C) return padded_unsupported();
   return conv_dgrad_simt<__nv_bfloat16>(a, g, (const __nv_bfloat16*)dy, w, (__nv_bfloat16*)dx, acc);
 }
 Status wgrad(OpArgs& a, const ConvGeom& g, const void* dy, const void* x, float* dw) {
+  if (f32(a) && g.Cw != g.C) return padded_unsupported();
   if (f32(a)) return conv_wgrad_simt<float>(a, g, (const float*)dy, (const float*)x, dw);
   if (!force_simt(&a) && conv_tc_ok(g, 2))
     return conv_wgrad_tc(a, g, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, dw);
+  if (g.Cw != g.C) return padded_unsupported();
   return conv_wgrad_simt<__nv_bfloat16>(a, g, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, dw);
 }
 

@@ -17,7 +17,10 @@ SHAPES = [  # N, H, W, C, K, R, stride, pad
     (2, 12, 9, 64, 128, 1, 2, 0),
     (1, 8, 8, 128, 128, 3, 1, 1),
     (2, 7, 7, 128, 64, 3, 1, 1),
-    (2, 15, 13, 3, 64, 7, 2, 3),      # stem: CUDA-core path
+    (2, 15, 13, 3, 64, 7, 2, 3),      # stem: 3 channels zero-padded to 8, one tap per 16-byte chunk
+    (3, 17, 16, 3, 64, 7, 2, 3, 2),   # ... in slices of 2 images (ragged last slice)
+    (2, 9, 11, 16, 64, 3, 1, 1),      # 16 channels: 4 taps per K-block
+    (3, 10, 9, 5, 128, 3, 2, 1, 1),   # 5 channels, BN = 128, one image per slice
 ]
 
 
@@ -26,11 +29,13 @@ def bf(a):
 
 
 def _graph(kind, g, accumulate=False):
-    N, H, W, C, K, R, st, pad = g
+    N, H, W, C, K, R, st, pad = g[:8]
     P = (H + 2 * pad - R) // st + 1
     Q = (W + 2 * pad - R) // st + 1
     attrs = {"N": N, "H": H, "W": W, "C": C, "K": K, "R": R, "S": R, "stride": st, "pad": pad, "P": P, "Q": Q,
              "accumulate": accumulate}
+    if len(g) > 8:
+        attrs["pad_slice"] = g[8]
     v = lambda n, b: {"id": n, "bytes": int(b), "pinned": True}
     xs, ys, ws = N * H * W * C * 2, N * P * Q * K * 2, K * R * R * C * 4
     if kind == "conv_fwd":
@@ -71,7 +76,7 @@ def _from_bits(a, shape):
 @pytest.mark.gpu
 @pytest.mark.parametrize("g", SHAPES)
 def test_conv_fwd(g):
-    N, H, W, C, K, R, st, pad = g
+    N, H, W, C, K, R, st, pad = g[:8]
     rng = np.random.default_rng(1)
     x = bf(rng.standard_normal((N, H, W, C)))
     w = rng.standard_normal((K, R, R, C)).astype(np.float32) * 0.1
@@ -87,7 +92,7 @@ def test_conv_fwd(g):
 @pytest.mark.parametrize("g", SHAPES[:5])
 @pytest.mark.parametrize("accumulate", [False, True])
 def test_conv_dgrad(g, accumulate):
-    N, H, W, C, K, R, st, pad = g
+    N, H, W, C, K, R, st, pad = g[:8]
     rng = np.random.default_rng(2)
     doc, (P, Q), total = _graph("conv_dgrad", g, accumulate)
     dy = bf(rng.standard_normal((N, P, Q, K)))
@@ -106,7 +111,7 @@ def test_conv_dgrad(g, accumulate):
 @pytest.mark.gpu
 @pytest.mark.parametrize("g", SHAPES)
 def test_conv_wgrad(g):
-    N, H, W, C, K, R, st, pad = g
+    N, H, W, C, K, R, st, pad = g[:8]
     rng = np.random.default_rng(3)
     doc, (P, Q), total = _graph("conv_wgrad", g)
     dy = bf(rng.standard_normal((N, P, Q, K)))
