@@ -24,51 +24,18 @@
 // (cp.async.mbarrier.arrive.noinc), so two CTAs share an SM and one's
 // epilogue overlaps the other's main loop.  Address arithmetic in the producers is hoisted out of the K loop (rows fixed per thread) and
 // what remains uses 32-bit multiply-shift division (FastDiv).
-#include "conv.cuh"
+#include "tc_util.cuh"
 
 namespace oc {
 
 namespace tc {
 
+using namespace tcu;
+
 constexpr int BM = 128, BKE = 64, NPROD = 128, NTHREADS = 160;
 // pipeline depth: 96 KB of stages either way, so two CTAs share an SM
 __host__ __device__ constexpr int stages_for(int bn) { return bn == 64 ? 4 : 3; }
 
-// n / d for 0 <= n < 2^31 by multiply-high and shift (Granlund–Montgomery)
-struct FastDiv {
-  uint32_t d, m, s;
-  void init(uint32_t div) {
-    d = div;
-    if (div <= 1) { m = 0; s = 0; return; }
-    s = 0;
-    while ((1ull << s) < div) ++s;
-    m = (uint32_t)(((1ull << 32) * ((1ull << s) - div)) / div + 1);
-  }
-  __device__ __forceinline__ uint32_t div(uint32_t n) const {
-    return (uint32_t)(((uint64_t)__umulhi(n, m) + n) >> s);
-  }
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
 }
@@ -77,46 +44,8 @@ template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// shared-memory matrix descriptor, SWIZZLE_128B (PTX ISA tcgen05 "matrix descriptor")
-__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((addr & 0x3FFFF) >> 4);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
-  return d;
-}
-// instruction descriptor: kind::f16, A/B = bf16, D = f32, M = 128
-__host__ __device__ constexpr uint32_t idesc(int n, bool a_mn, bool b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
-         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-}
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(id), "r"(acc));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
-               : "memory");
-}
-
-#define TMEM_LD32(taddr, r)                                                                                          \
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"      \
-               "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                            \
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),     \
-                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),            \
-                 "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),          \
-                 "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),          \
-                 "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                               \
-               : "r"(taddr))
-
-enum Mode { FPROP = 0, DGRAD = 1, WGRAD = 2 };
 
 struct Params {
   ConvGeom g;
@@ -495,6 +424,14 @@ void fill_divs(Params& P) {
 
 using namespace tc;
 
+bool conv_tma_ok(const ConvGeom& g, int mode);
+Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* wb, int kpad,
+                      __nv_bfloat16* y, bool accumulate);
+Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* wt,
+                      __nv_bfloat16* dx, bool accumulate);
+Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
+                      int splits, int kb_per_split);
+
 bool conv_tc_ok(const ConvGeom& g, int mode) {
   // 32-bit element indices of the activations (the 64-bit tensor offsets are formed per row)
   if ((int64_t)g.N * g.H * g.W * g.C >= (1ll << 31) || (int64_t)g.N * g.P * g.Q * g.K >= (1ll << 31)) return false;
@@ -601,6 +538,11 @@ Status conv_fprop_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* x, cons
     P.narrow = g.C % 64 != 0 ? 1 : 0;
     P.nkb = kpad / BKE;
     P.accumulate = accumulate ? 1 : 0;
+    if (conv_tma_ok(P.g, FPROP)) {
+      Status st = conv_fprop_tma(a, P.g, P.act, wb, kpad, (__nv_bfloat16*)P.out, accumulate);
+      if (!st.good()) return st;
+      continue;
+    }
     fill_divs(P);
     const dim3 grid((P.M + BM - 1) / BM, g.K / (g.K % 128 == 0 ? 128 : 64), 1);
     Status st = g.K % 128 == 0 ? launch<FPROP, 128>(a, P, grid) : launch<FPROP, 64>(a, P, grid);
@@ -615,6 +557,7 @@ Status conv_dgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, cons
   const int64_t nw = (int64_t)g.K * g.R * g.S * g.C;
   weight_bf16<<<grid_for(nw, 256, 4), 256, 0, a.stream>>>(w, wt, g.K, g.R * g.S, g.C, 1, 0, g.C);
   OC_LAUNCH_CHECK(a);
+  if (conv_tma_ok(g, DGRAD)) return conv_dgrad_tma(a, g, dy, wt, dx, accumulate);
   for (int ph = 0; ph < g.st; ++ph)
     for (int pw = 0; pw < g.st; ++pw) {
       Params P{};
@@ -652,7 +595,15 @@ Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* dy, con
   const int BN = wgrad_bn(g);
   ConvGeom gs = g;
   gs.N = (int)nw.slice;
-  const int splits = wgrad_splits(gs, BN);
+  int splits = wgrad_splits(gs, BN);
+  if (conv_tma_ok(g, WGRAD)) {
+    // persistent kernel: at most two units per SM, balanced (floor, not ceil)
+    const int64_t tiles = ((int64_t)g.R * g.S * g.C + BM - 1) / BM * (g.K / BN);
+    const int64_t kbs = ((int64_t)gs.N * g.P * g.Q + BKE - 1) / BKE;
+    int64_t s2 = (2 * 148) / tiles;
+    s2 = s2 < 1 ? 1 : (s2 > kbs ? kbs : s2);
+    splits = (int)(s2 < splits ? s2 : splits);
+  }
   const int64_t nsl = (g.N + nw.slice - 1) / nw.slice;
   const int RSC = g.R * g.S * g.C;
   float* part = (float*)a.ws;
@@ -677,6 +628,11 @@ Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* dy, con
     const int kbs = (P.gemm_k + BKE - 1) / BKE;
     P.kb_per_split = (kbs + splits - 1) / splits;
     P.nkb = P.kb_per_split;
+    if (conv_tma_ok(P.g, WGRAD)) {
+      Status st = conv_wgrad_tma(a, P.g, P.act, P.wgt, (float*)P.out, splits, P.kb_per_split);
+      if (!st.good()) return st;
+      continue;
+    }
     fill_divs(P);
     dim3 grid((P.M + BM - 1) / BM, g.K / BN, splits);
     Status st = BN == 128 ? launch<WGRAD, 128>(a, P, grid) : launch<WGRAD, 64>(a, P, grid);

@@ -1,0 +1,492 @@
+// Convolution on the 5th-generation tensor cores with TMA-fed operands: a
+// persistent, warp-specialised implicit GEMM.
+//
+//   warp 0      one elected thread issues the TMA loads of a K-block into a
+//               ring of shared-memory stages (mbarrier full/empty pipeline);
+//               the activation operand is gathered by the TMA engine in
+//               im2col mode (a box of output pixels × 64 channels at one
+//               filter tap, zero fill outside the image), the weight / dY
+//               operand with tiled 2-D loads, both in the UMMA SWIZZLE_128B
+//               canonical layouts
+//   warp 1      one elected thread issues tcgen05.mma (bf16 × bf16 -> fp32)
+//               into one of two TMEM accumulators, so the epilogue of tile t
+//               overlaps the main loop of tile t+1
+//   warps 2-5   epilogue: tcgen05.ld TMEM -> registers -> bf16 / fp32 rows
+//
+// One CTA per SM loops over tiles (tile u, u + gridDim.x, ...).
+//   fprop   D[(n,p,q)][k] = Σ_{r,s,c} X[n, p·st−pad+r, q·st−pad+s, c] · W[k,r,s,c]
+//   dgrad   per output phase (h mod st, w mod st), a stride-1 gather over dY
+//           at the phase's taps only, W's taps reversed so the im2col offsets
+//           run forward: stride 1 gives D[(n,h,w)][c] = Σ_{r',s',k}
+//           dY[n, h−pad'+r', w−pad'+s', k] · W[k, R−1−r', S−1−s', c], pad' = R−1−pad
+//   wgrad   D[(r,s,c)][k] = Σ_{(n,p,q)} X[n, p·st−pad+r, q·st−pad+s, c] · dY[(n,p,q), k]:
+//           A = two im2col boxes of 64 pixels × 64 channels (MN-major),
+//           B = dY rows (MN-major), deterministic split-K over pixel blocks
+//   narrow  fprop over 8-channel (16-byte) pixels: eight im2col boxes of
+//           128 pixels × 8 channels per K-block, one filter tap each, in the
+//           no-swizzle core-matrix layout (LBO = 2 KB between taps)
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
+#include "tc_util.cuh"
+
+namespace oc {
+namespace tma {
+
+using namespace tcu;
+
+constexpr int BM = 128, BK = 64, NTHREADS = 192;
+__host__ __device__ constexpr int tma_stages(int bn) { return bn == 64 ? 8 : 6; }
+__host__ __device__ constexpr int tma_smem(int bn) { return tma_stages(bn) * (BM * BK * 2 + bn * BK * 2) + 1024 + 256; }
+
+struct Params {
+  CUtensorMap ta;          // im2col map of the gathered activation (X or dY)
+  CUtensorMap tb;          // tiled map of the other operand (W_bf16, Wt_bf16 or dY)
+  void* out;               // bf16 [M][N] rows, or fp32 wgrad partials [z][M][N]
+  int accumulate;          // out = rnd(acc + out)
+  int M, N;                // GEMM rows / columns
+  int num_m, num_n, splits;
+  int nkb;                 // fprop/dgrad: K-blocks per tile; wgrad: pixel blocks in all
+  int kb_per_split;        // wgrad
+  int Pd, Qd, st, padh, padw;  // im2col base of output pixel (n,p,q): (w, h) = (q·st − padw, p·st − padh)
+  int R, S, Cr;            // im2col tap grid (dgrad: the phase's nr × ns); channels reduced per tap
+  // dgrad phase (ph, pw) of stride dst: im2col tap (i', j') is filter tap
+  // (r0 + dst·(R−1−i'), s0 + dst·(S−1−j')) of W (width Sw), and GEMM row
+  // (n, h', w') is dx pixel (n, h'·dst + ph, w'·dst + pw) of an Ho × Wo map
+  int Sw, r0, s0, dst, ph, pw, Ho, Wo;
+  FastDiv fQ, fP, fCb, fS;
+};
+
+__device__ __forceinline__ void base_of(const Params& P, int pix, int& w, int& h, int& n) {
+  const uint32_t t = P.fQ.div((uint32_t)pix);
+  const int q = pix - (int)t * P.Qd;
+  const uint32_t nn = P.fP.div(t);
+  const int p = (int)t - (int)nn * P.Pd;
+  w = q * P.st - P.padw;
+  h = p * P.st - P.padh;
+  n = (int)nn;
+}
+
+template <int MODE, int BN, bool NARROW>
+__global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_constant__ Params P) {
+  constexpr int NST = tma_stages(BN);
+  constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
+  constexpr uint32_t TCOLS = 2 * BN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + NST * STAGE);
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (NARROW) {
+    // taps past R·S are never loaded; their (weight-zero) A columns must hold
+    // finite values, so the stages start zeroed
+    for (int i = threadIdx.x; i < NST * STAGE / 16; i += NTHREADS)
+      asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(smem_u32(smem) + i * 16), "r"(0) : "memory");
+    fence_async_smem();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&P.ta);
+    tma_prefetch(&P.tb);
+    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  const int units = P.num_m * P.num_n * (MODE == WGRAD ? P.splits : 1);
+  auto unit_of = [&](int u, int& mt, int& nt, int& z, int& kb0, int& nk) {
+    nt = u % P.num_n;
+    const int t = u / P.num_n;
+    mt = t % P.num_m;
+    z = t / P.num_m;
+    if (MODE == WGRAD) {
+      kb0 = z * P.kb_per_split;
+      nk = P.nkb - kb0 < P.kb_per_split ? P.nkb - kb0 : P.kb_per_split;
+      if (nk < 0) nk = 0;
+    } else {
+      kb0 = 0;
+      nk = P.nkb;
+    }
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int mt, nt, z, kb0, nk;
+        unit_of(u, mt, nt, z, kb0, nk);
+        int bw = 0, bh = 0, bn = 0;
+        if (MODE != WGRAD) base_of(P, mt * BM, bw, bh, bn);
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int sg = (int)(it % NST);
+          if (it >= (uint32_t)NST) mbar_wait(&empty[sg], ((it / NST) - 1) & 1);
+          const uint32_t a = smem_u32(smem + sg * STAGE), b = a + A_BYTES;
+          const int kb = kb0 + i;
+          if (MODE == WGRAD) {
+            int pw, ph, pn;
+            base_of(P, kb * BK, pw, ph, pn);
+            uint32_t bytes = B_BYTES;
+            const int rb0 = mt * 2;   // 64-row blocks of (r,s,c)
+            const int nrb = (P.M - mt * BM) >= BM ? 2 : ((P.M - mt * BM) + 63) / 64;
+            bytes += nrb * 8192;
+            mbar_expect_tx(&full[sg], bytes);
+            for (int j = 0; j < nrb; ++j) {
+              const int blk = rb0 + j;                     // (tap, 64-channel block)
+              const int tap = (int)P.fCb.div((uint32_t)blk), cb = blk - tap * (P.Cr / 64);
+              const int r = (int)P.fS.div((uint32_t)tap), s = tap - r * P.S;
+              tma_load_im2col(a + j * 8192, &P.ta, &full[sg], cb * 64, pw, ph, pn, (uint16_t)s, (uint16_t)r);
+            }
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * 8192, &P.tb, &full[sg], nt * BN + j * 64, kb * BK);
+          } else if (NARROW) {
+            const int t0 = kb * 8;
+            int nt8 = P.R * P.S - t0;
+            nt8 = nt8 < 8 ? nt8 : 8;
+            mbar_expect_tx(&full[sg], B_BYTES + nt8 * 2048);
+            for (int j = 0; j < nt8; ++j) {
+              const int r = (int)P.fS.div((uint32_t)(t0 + j)), s = t0 + j - r * P.S;
+              tma_load_im2col(a + j * 2048, &P.ta, &full[sg], 0, bw, bh, bn, (uint16_t)s, (uint16_t)r);
+            }
+            tma_load_2d(b, &P.tb, &full[sg], kb * BK, nt * BN);
+          } else {
+            mbar_expect_tx(&full[sg], STAGE);
+            const int tap = (int)P.fCb.div((uint32_t)kb), cb = kb - tap * (P.Cr / 64);
+            const int r = (int)P.fS.div((uint32_t)tap), s = tap - r * P.S;
+            tma_load_im2col(a, &P.ta, &full[sg], cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
+            const int btap = MODE == DGRAD ? (P.r0 + P.dst * (P.R - 1 - r)) * P.Sw + P.s0 + P.dst * (P.S - 1 - s) : tap;
+            tma_load_2d(b, &P.tb, &full[sg], btap * P.Cr + cb * 64, nt * BN);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t ID = idesc(BN, MODE == WGRAD, MODE == WGRAD);
+    uint32_t it = 0, lt = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+      int mt, nt, z, kb0, nk;
+      unit_of(u, mt, nt, z, kb0, nk);
+      const uint32_t buf = lt & 1;
+      if (lt >= 2) mbar_wait(&tempty[buf], ((lt >> 1) - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t d = tmem + buf * BN;
+      for (int i = 0; i < nk; ++i, ++it) {
+        const int sg = (int)(it % NST);
+        mbar_wait(&full[sg], (it / NST) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint32_t a = smem_u32(smem + sg * STAGE), b = a + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t da, db;
+            if (MODE == WGRAD) {          // MN-major: 64-wide MN atoms 8 KB apart, 8-row K groups 1 KB apart
+              da = sdesc(a + k * 2048, 8192, 1024);
+              db = sdesc(b + k * 2048, 8192, 1024);
+            } else if (NARROW) {          // K-major, no swizzle: taps 2 KB apart, 8-row groups 128 B apart
+              da = sdesc(a + k * 2 * 2048, 2048, 128, 0);
+              db = sdesc(b + k * 32, 16, 1024);
+            } else {                      // K-major SWIZZLE_128B
+              da = sdesc(a + k * 32, 16, 1024);
+              db = sdesc(b + k * 32, 16, 1024);
+            }
+            mma_bf16(d, da, db, ID, (i > 0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[sg]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) mma_commit(&tfull[buf]);
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 2-5)
+    const int q = warp & 3;            // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    uint32_t lt = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+      int mt, nt, z, kb0, nk;
+      unit_of(u, mt, nt, z, kb0, nk);
+      const uint32_t buf = lt & 1;
+      mbar_wait(&tfull[buf], (lt >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int m = mt * BM + row;
+      int64_t orow = m;
+      if (MODE == DGRAD && m < P.M) {
+        int w, h, n;
+        base_of(P, m, w, h, n);     // (w, h) = (w' − pad', h' − pad')
+        orow = ((int64_t)n * P.Ho + (h + P.padh) * P.dst + P.ph) * P.Wo + (w + P.padw) * P.dst + P.pw;
+      }
+#pragma unroll
+      for (int j0 = 0; j0 < BN; j0 += 32) {
+        uint32_t v[32];
+        TMEM_LD32(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + j0, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (nk == 0) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0u;
+        }
+        if (m >= P.M) continue;
+        const int col = nt * BN + j0;
+        if (MODE == WGRAD) {
+          float* o = (float*)P.out + ((int64_t)z * P.M + m) * P.N + col;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(o + i) = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                                            __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+        } else {
+          __nv_bfloat16* o = (__nv_bfloat16*)P.out + orow * P.N + col;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            float f[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[i + e]);
+            if (P.accumulate) {
+              uint4 old = *reinterpret_cast<const uint4*>(o + i);
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&old);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 ff = __bfloat1622float2(h2[e]);
+                f[2 * e] += ff.x;
+                f[2 * e + 1] += ff.y;
+              }
+            }
+            uint4 pk;
+            __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) p2[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+            *reinterpret_cast<uint4*>(o + i) = pk;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+  }
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+Status encode_fail(CUresult r, const char* what) { return cu_status(r, what); }
+
+// NHWC bf16 activation [N][H][W][C] gathered for an output grid Pd × Qd
+Status make_im2col(CUtensorMap* m, const void* base, int N, int H, int W, int C, int ch, int pix, int Pd, int Qd,
+                   int st, int padh, int padw, bool swizzle) {
+  Driver* d;
+  std::string msg;
+  if (!driver(d, msg)) return Status::make(OC_E_CUDA, msg);
+  const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  // bounding box of the base pixels, {W, H}: first at −pad, last at (Q−1)·st − pad
+  const int lower[2] = {-padw, -padh};
+  const int upper[2] = {(Qd - 1) * st - padw - (W - 1), (Pd - 1) * st - padh - (H - 1)};
+  const cuuint32_t es[4] = {1, (cuuint32_t)st, (cuuint32_t)st, 1};
+  CUresult r = d->TensorMapEncodeIm2col(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                                        lower, upper, (cuuint32_t)ch, (cuuint32_t)pix, es,
+                                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                        swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? Status::ok() : encode_fail(r, "cuTensorMapEncodeIm2col");
+}
+
+// row-major bf16 [rows][cols], boxes of 64 columns × box_rows rows, SWIZZLE_128B
+Status make_tiled(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  Driver* d;
+  std::string msg;
+  if (!driver(d, msg)) return Status::make(OC_E_CUDA, msg);
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r = d->TensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                                       box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? Status::ok() : encode_fail(r, "cuTensorMapEncodeTiled");
+}
+
+void fill(Params& P) {
+  P.fQ.init(P.Qd);
+  P.fP.init(P.Pd);
+  P.fCb.init(P.Cr / 64 > 0 ? P.Cr / 64 : 1);
+  P.fS.init(P.S);
+}
+
+template <int MODE, int BN, bool NARROW>
+Status launch(OpArgs& a, const Params& P) {
+  constexpr int smem = tma_smem(BN);
+  auto kern = conv_tma_kernel<MODE, BN, NARROW>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const int units = P.num_m * P.num_n * (MODE == WGRAD ? P.splits : 1);
+  if (units == 0) return Status::ok();
+  kern<<<std::min(units, sm_count()), NTHREADS, smem, a.stream>>>(P);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+
+}  // namespace tma
+
+using namespace tma;
+
+bool conv_tma_enabled() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = std::getenv("OC_CONV_TMA");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env == 1;
+}
+
+// which kernel geometries the TMA kernels take (after the narrow-input re-layout)
+bool conv_tma_ok(const ConvGeom& g, int mode) {
+  if (!conv_tma_enabled()) return false;
+  if (g.pad > 127 || g.R > 64 || g.S > 64 || g.st > 8) return false;
+  if (mode == FPROP) return g.K % 64 == 0 && (g.C % 64 == 0 || g.C == 8);
+  if (mode == DGRAD) return g.C % 64 == 0 && g.K % 64 == 0;
+  return g.C % 64 == 0 && g.K % 64 == 0;
+}
+
+// y[M = N·P·Q][K] = im2col(x) · W_bf16[K][kpad]ᵀ
+Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* wb, int kpad,
+                      __nv_bfloat16* y, bool accumulate) {
+  const bool narrow = g.C == 8;
+  Params P{};
+  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, narrow ? 8 : 64, BM, g.P, g.Q, g.st, g.pad, g.pad, !narrow);
+  if (!st.good()) return st;
+  const int BN = g.K % 128 == 0 ? 128 : 64;
+  st = make_tiled(&P.tb, wb, (uint64_t)kpad, (uint64_t)g.K, (uint32_t)BN);
+  if (!st.good()) return st;
+  P.out = y;
+  P.accumulate = accumulate ? 1 : 0;
+  P.M = g.N * g.P * g.Q;
+  P.N = g.K;
+  P.num_m = (P.M + BM - 1) / BM;
+  P.num_n = g.K / BN;
+  P.splits = 1;
+  P.nkb = kpad / BK;
+  P.Pd = g.P;
+  P.Qd = g.Q;
+  P.st = g.st;
+  P.padh = P.padw = g.pad;
+  P.R = g.R;
+  P.S = g.S;
+  P.Cr = g.C;
+  fill(P);
+  if (narrow) return BN == 128 ? launch<FPROP, 128, true>(a, P) : launch<FPROP, 64, true>(a, P);
+  return BN == 128 ? launch<FPROP, 128, false>(a, P) : launch<FPROP, 64, false>(a, P);
+}
+
+// dgrad, one launch per output phase (h mod st, w mod st) over that phase's
+// valid taps: dx[(n,h',w')][C] = im2col_{pad''}(dy) · Wt_bf16[C][(r,s,K)]ᵀ at the
+// phase's filter taps; a phase no tap reaches gets zeros (or keeps dx when accumulating)
+Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* wt,
+                      __nv_bfloat16* dx, bool accumulate) {
+  const int BN = g.C % 128 == 0 ? 128 : 64;
+  for (int ph = 0; ph < g.st; ++ph)
+    for (int pw = 0; pw < g.st; ++pw) {
+      Params P{};
+      const int Hp = (g.H - ph + g.st - 1) / g.st, Wp = (g.W - pw + g.st - 1) / g.st;
+      const int r0 = (ph + g.pad) % g.st, s0 = (pw + g.pad) % g.st;
+      const int nr = r0 < g.R ? (g.R - r0 + g.st - 1) / g.st : 0;
+      const int ns = s0 < g.S ? (g.S - s0 + g.st - 1) / g.st : 0;
+      if (Hp <= 0 || Wp <= 0) continue;
+      if ((nr == 0 || ns == 0) && accumulate) continue;
+      // dy row of (h', tap i') is h' − pad'' + i' with pad'' = nr − 1 − (ph + pad − r0)/st
+      const int dh = (ph + g.pad - r0) / g.st, dw = (pw + g.pad - s0) / g.st;
+      const int padh = nr > 0 ? nr - 1 - dh : 0, padw = ns > 0 ? ns - 1 - dw : 0;
+      Status st = make_im2col(&P.ta, dy, g.N, g.P, g.Q, g.K, 64, BM, Hp, Wp, 1, padh, padw, true);
+      if (!st.good()) return st;
+      st = make_tiled(&P.tb, wt, (uint64_t)g.R * g.S * g.K, (uint64_t)g.C, (uint32_t)BN);
+      if (!st.good()) return st;
+      P.out = dx;
+      P.accumulate = accumulate ? 1 : 0;
+      P.M = g.N * Hp * Wp;
+      P.N = g.C;
+      P.num_m = (P.M + BM - 1) / BM;
+      P.num_n = g.C / BN;
+      P.splits = 1;
+      P.nkb = nr * ns * g.K / BK;
+      P.Pd = Hp;
+      P.Qd = Wp;
+      P.st = 1;
+      P.padh = padh;
+      P.padw = padw;
+      P.R = nr > 0 ? nr : 1;
+      P.S = ns > 0 ? ns : 1;
+      P.Cr = g.K;
+      P.Sw = g.S;
+      P.r0 = r0;
+      P.s0 = s0;
+      P.dst = g.st;
+      P.ph = ph;
+      P.pw = pw;
+      P.Ho = g.H;
+      P.Wo = g.W;
+      fill(P);
+      st = BN == 128 ? launch<DGRAD, 128, false>(a, P) : launch<DGRAD, 64, false>(a, P);
+      if (!st.good()) return st;
+    }
+  return Status::ok();
+}
+
+// wgrad partials part[z][R·S·C][K] over pixel blocks [z·kbps, (z+1)·kbps)
+Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
+                      int splits, int kb_per_split) {
+  Params P{};
+  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, 64, BK, g.P, g.Q, g.st, g.pad, g.pad, true);
+  if (!st.good()) return st;
+  const int BN = g.K % 128 == 0 ? 128 : 64;
+  st = make_tiled(&P.tb, dy, (uint64_t)g.K, (uint64_t)g.N * g.P * g.Q, 64);
+  if (!st.good()) return st;
+  P.out = part;
+  P.M = g.R * g.S * g.C;
+  P.N = g.K;
+  P.num_m = (P.M + BM - 1) / BM;
+  P.num_n = g.K / BN;
+  P.splits = splits;
+  P.nkb = (g.N * g.P * g.Q + BK - 1) / BK;
+  P.kb_per_split = kb_per_split;
+  P.Pd = g.P;
+  P.Qd = g.Q;
+  P.st = g.st;
+  P.padh = P.padw = g.pad;
+  P.R = g.R;
+  P.S = g.S;
+  P.Cr = g.C;
+  fill(P);
+  return BN == 128 ? launch<WGRAD, 128, false>(a, P) : launch<WGRAD, 64, false>(a, P);
+}
+
+}  // namespace oc

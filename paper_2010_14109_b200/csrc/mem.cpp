@@ -48,6 +48,8 @@ bool driver(Driver*& d, std::string& msg) {
     ok &= get("cuMemSetAccess", (void**)&g_drv.MemSetAccess);
     ok &= get("cuMemGetAllocationGranularity", (void**)&g_drv.MemGetAllocationGranularity);
     ok &= get("cuGetErrorString", (void**)&g_drv.GetErrorString);
+    ok &= get("cuTensorMapEncodeTiled", (void**)&g_drv.TensorMapEncodeTiled);
+    ok &= get("cuTensorMapEncodeIm2col", (void**)&g_drv.TensorMapEncodeIm2col);
     g_drv.loaded = ok;
   });
   d = &g_drv;
