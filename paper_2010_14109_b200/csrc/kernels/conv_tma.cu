@@ -22,9 +22,10 @@
 //   wgrad   D[(r,s,c)][k] = Σ_{(n,p,q)} X[n, p·st−pad+r, q·st−pad+s, c] · dY[(n,p,q), k]:
 //           A = two im2col boxes of 64 pixels × 64 channels (MN-major),
 //           B = dY rows (MN-major), deterministic split-K over pixel blocks
-//   narrow  fprop over 8-channel (16-byte) pixels: eight im2col boxes of
-//           128 pixels × 8 channels per K-block, one filter tap each, in the
-//           no-swizzle core-matrix layout (LBO = 2 KB between taps)
+//   narrow  fprop over 8- or 16-channel (16 / 32-byte) pixels: 8 or 4 im2col
+//           boxes of 128 pixels per K-block, one filter tap each, in the
+//           no-swizzle core-matrix layout (LBO = 2 KB between taps) or the
+//           SWIZZLE_32B layout (one tap per K-step)
 #include <algorithm>
 #include <cstdlib>
 #include <string>
@@ -68,7 +69,7 @@ __device__ __forceinline__ void base_of(const Params& P, int pix, int& w, int& h
   n = (int)nn;
 }
 
-template <int MODE, int BN, bool NARROW>
+template <int MODE, int BN, int NCH>
 __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_constant__ Params P) {
   constexpr int NST = tma_stages(BN);
   constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  if (NARROW) {
+  if (NCH) {
     // taps past R·S are never loaded; their (weight-zero) A columns must hold
     // finite values, so the stages start zeroed
     for (int i = threadIdx.x; i < NST * STAGE / 16; i += NTHREADS)
@@ -152,14 +153,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
             }
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * 8192, &P.tb, &full[sg], nt * BN + j * 64, kb * BK);
-          } else if (NARROW) {
-            const int t0 = kb * 8;
-            int nt8 = P.R * P.S - t0;
-            nt8 = nt8 < 8 ? nt8 : 8;
-            mbar_expect_tx(&full[sg], B_BYTES + nt8 * 2048);
-            for (int j = 0; j < nt8; ++j) {
+          } else if (NCH) {
+            // 64 / NCH taps per K-block, one box of 128 pixels × NCH channels each
+            constexpr int TPB = 64 / (NCH ? NCH : 64), BOX = BM * NCH * 2;
+            const int t0 = kb * TPB;
+            int ntap = P.R * P.S - t0;
+            ntap = ntap < TPB ? ntap : TPB;
+            mbar_expect_tx(&full[sg], B_BYTES + ntap * BOX);
+            for (int j = 0; j < ntap; ++j) {
               const int r = (int)P.fS.div((uint32_t)(t0 + j)), s = t0 + j - r * P.S;
-              tma_load_im2col(a + j * 2048, &P.ta, &full[sg], 0, bw, bh, bn, (uint16_t)s, (uint16_t)r);
+              tma_load_im2col(a + j * BOX, &P.ta, &full[sg], 0, bw, bh, bn, (uint16_t)s, (uint16_t)r);
             }
             tma_load_2d(b, &P.tb, &full[sg], kb * BK, nt * BN);
           } else {
@@ -196,8 +199,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
             if (MODE == WGRAD) {          // MN-major: 64-wide MN atoms 8 KB apart, 8-row K groups 1 KB apart
               da = sdesc(a + k * 2048, 8192, 1024);
               db = sdesc(b + k * 2048, 8192, 1024);
-            } else if (NARROW) {          // K-major, no swizzle: taps 2 KB apart, 8-row groups 128 B apart
+            } else if (NCH == 8) {        // K-major, no swizzle: taps 2 KB apart, 8-row groups 128 B apart
               da = sdesc(a + k * 2 * 2048, 2048, 128, 0);
+              db = sdesc(b + k * 32, 16, 1024);
+            } else if (NCH == 16) {       // K-major SWIZZLE_32B: one tap (16 ch) per K-step, 8-row atoms 256 B apart
+              da = sdesc(a + k * 4096, 16, 256, 6);
               db = sdesc(b + k * 32, 16, 1024);
             } else {                      // K-major SWIZZLE_128B
               da = sdesc(a + k * 32, 16, 1024);
@@ -300,7 +306,7 @@ Status encode_fail(CUresult r, const char* what) { return cu_status(r, what); }
 
 // NHWC bf16 activation [N][H][W][C] gathered for an output grid Pd × Qd
 Status make_im2col(CUtensorMap* m, const void* base, int N, int H, int W, int C, int ch, int pix, int Pd, int Qd,
-                   int st, int padh, int padw, bool swizzle) {
+                   int st, int padh, int padw, CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   Driver* d;
   std::string msg;
   if (!driver(d, msg)) return Status::make(OC_E_CUDA, msg);
@@ -312,8 +318,7 @@ Status make_im2col(CUtensorMap* m, const void* base, int N, int H, int W, int C,
   const cuuint32_t es[4] = {1, (cuuint32_t)st, (cuuint32_t)st, 1};
   CUresult r = d->TensorMapEncodeIm2col(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
                                         lower, upper, (cuuint32_t)ch, (cuuint32_t)pix, es,
-                                        CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                        swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                        CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? Status::ok() : encode_fail(r, "cuTensorMapEncodeIm2col");
 }
@@ -340,10 +345,10 @@ void fill(Params& P) {
   P.fS.init(P.S);
 }
 
-template <int MODE, int BN, bool NARROW>
+template <int MODE, int BN, int NCH>
 Status launch(OpArgs& a, const Params& P) {
   constexpr int smem = tma_smem(BN);
-  auto kern = conv_tma_kernel<MODE, BN, NARROW>;
+  auto kern = conv_tma_kernel<MODE, BN, NCH>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -373,7 +378,7 @@ bool conv_tma_enabled() {
 bool conv_tma_ok(const ConvGeom& g, int mode) {
   if (!conv_tma_enabled()) return false;
   if (g.pad > 127 || g.R > 64 || g.S > 64 || g.st > 8) return false;
-  if (mode == FPROP) return g.K % 64 == 0 && (g.C % 64 == 0 || g.C == 8);
+  if (mode == FPROP) return g.K % 64 == 0 && (g.C % 64 == 0 || g.C == 8 || g.C == 16);
   if (mode == DGRAD) return g.C % 64 == 0 && g.K % 64 == 0;
   return g.C % 64 == 0 && g.K % 64 == 0;
 }
@@ -381,9 +386,11 @@ bool conv_tma_ok(const ConvGeom& g, int mode) {
 // y[M = N·P·Q][K] = im2col(x) · W_bf16[K][kpad]ᵀ
 Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* wb, int kpad,
                       __nv_bfloat16* y, bool accumulate) {
-  const bool narrow = g.C == 8;
+  const int nch = g.C % 64 == 0 ? 0 : g.C;     // 8 or 16: narrow pixels, one tap per box
   Params P{};
-  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, narrow ? 8 : 64, BM, g.P, g.Q, g.st, g.pad, g.pad, !narrow);
+  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, nch ? nch : 64, BM, g.P, g.Q, g.st, g.pad, g.pad,
+                          nch == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                   : (nch == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B));
   if (!st.good()) return st;
   const int BN = g.K % 128 == 0 ? 128 : 64;
   st = make_tiled(&P.tb, wb, (uint64_t)kpad, (uint64_t)g.K, (uint32_t)BN);
@@ -404,8 +411,9 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   P.S = g.S;
   P.Cr = g.C;
   fill(P);
-  if (narrow) return BN == 128 ? launch<FPROP, 128, true>(a, P) : launch<FPROP, 64, true>(a, P);
-  return BN == 128 ? launch<FPROP, 128, false>(a, P) : launch<FPROP, 64, false>(a, P);
+  if (nch == 8) return BN == 128 ? launch<FPROP, 128, 8>(a, P) : launch<FPROP, 64, 8>(a, P);
+  if (nch == 16) return BN == 128 ? launch<FPROP, 128, 16>(a, P) : launch<FPROP, 64, 16>(a, P);
+  return BN == 128 ? launch<FPROP, 128, 0>(a, P) : launch<FPROP, 64, 0>(a, P);
 }
 
 // dgrad, one launch per output phase (h mod st, w mod st) over that phase's
@@ -426,7 +434,7 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
       // dy row of (h', tap i') is h' − pad'' + i' with pad'' = nr − 1 − (ph + pad − r0)/st
       const int dh = (ph + g.pad - r0) / g.st, dw = (pw + g.pad - s0) / g.st;
       const int padh = nr > 0 ? nr - 1 - dh : 0, padw = ns > 0 ? ns - 1 - dw : 0;
-      Status st = make_im2col(&P.ta, dy, g.N, g.P, g.Q, g.K, 64, BM, Hp, Wp, 1, padh, padw, true);
+      Status st = make_im2col(&P.ta, dy, g.N, g.P, g.Q, g.K, 64, BM, Hp, Wp, 1, padh, padw);
       if (!st.good()) return st;
       st = make_tiled(&P.tb, wt, (uint64_t)g.R * g.S * g.K, (uint64_t)g.C, (uint32_t)BN);
       if (!st.good()) return st;
@@ -455,7 +463,7 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
       P.Ho = g.H;
       P.Wo = g.W;
       fill(P);
-      st = BN == 128 ? launch<DGRAD, 128, false>(a, P) : launch<DGRAD, 64, false>(a, P);
+      st = BN == 128 ? launch<DGRAD, 128, 0>(a, P) : launch<DGRAD, 64, 0>(a, P);
       if (!st.good()) return st;
     }
   return Status::ok();
@@ -465,7 +473,7 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
 Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
                       int splits, int kb_per_split) {
   Params P{};
-  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, 64, BK, g.P, g.Q, g.st, g.pad, g.pad, true);
+  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, 64, BK, g.P, g.Q, g.st, g.pad, g.pad);
   if (!st.good()) return st;
   const int BN = g.K % 128 == 0 ? 128 : 64;
   st = make_tiled(&P.tb, dy, (uint64_t)g.K, (uint64_t)g.N * g.P * g.Q, 64);
@@ -486,7 +494,7 @@ Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   P.S = g.S;
   P.Cr = g.C;
   fill(P);
-  return BN == 128 ? launch<WGRAD, 128, false>(a, P) : launch<WGRAD, 64, false>(a, P);
+  return BN == 128 ? launch<WGRAD, 128, 0>(a, P) : launch<WGRAD, 64, 0>(a, P);
 }
 
 }  // namespace oc

@@ -21,6 +21,9 @@ SHAPES = [  # N, H, W, C, K, R, stride, pad
     (3, 17, 16, 3, 64, 7, 2, 3, 2),   # ... in slices of 2 images (ragged last slice)
     (2, 9, 11, 16, 64, 3, 1, 1),      # 16 channels: 4 taps per K-block
     (3, 10, 9, 5, 128, 3, 2, 1, 1),   # 5 channels, BN = 128, one image per slice
+    (2, 16, 14, 3, 64, 7, 2, 3),      # stride-2 stem, even H, W: space-to-depth 4x4 conv over 16 channels
+    (3, 18, 12, 3, 128, 7, 2, 3, 2),  # ... BN = 128, slices of 2 images
+    (2, 10, 12, 3, 64, 3, 2, 1),      # 3x3 stride 2 -> 2x2 space-to-depth taps
 ]
 
 
