@@ -47,6 +47,10 @@ def parse():
     ap.add_argument("--no-incore", action="store_true")
     ap.add_argument("--window", default="auto", help="auto | max | <bytes>")
     ap.add_argument("--no-graph", action="store_true", help="issue every step eagerly (no CUDA graph replay)")
+    ap.add_argument("--policy", default="paper", choices=["paper", "vdnn", "lms"],
+                    help="swap-timing window: the paper's byte window, or the prior-art function-distance "
+                         "window (vdnn = 1 function ahead, lms = --distance functions ahead; SURVEY F1)")
+    ap.add_argument("--distance", type=int, default=3, help="lms policy: functions of look-ahead")
     return ap.parse_args()
 
 
@@ -60,10 +64,12 @@ def config(args):
         spec = nets.resnet(50, batch=b)
         return spec, {"workload": f"ResNet-50 224x224 b={b} at {args.budget_frac:.2f} of F_peak"}
     if args.config == "r1001":
-        b = args.batch or 64
+        # b=256: every activation is >= 2 MiB (one VA chunk); tensors below one
+        # chunk (parameters, optimizer state, BN statistics) stay resident (Z26)
+        b = args.batch or 256
         spec = nets.preact_resnet(1001, batch=b)
         return spec, {"workload": f"configs[4] pre-activation ResNet-1001 32x32 b={b} at {args.budget_frac:.2f} "
-                                  "of F_peak"}
+                                  "of F_peak, tensors < 1 VA chunk pinned", "pin_below": args.chunk_mib * MiB}
     b = args.batch or 256
     spec = nets.resnet(18, batch=b)
     return spec, {"workload": f"configs[1] ResNet-18 224x224 b={b}, budget {args.budget_frac:.2f} x in-core footprint"}
@@ -131,7 +137,8 @@ def trainable_batch(spec_fn, budget, lo=1, hi=4096, params="pinned"):
     return lo
 
 
-def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None, pack=64 << 10, use_graph=False):
+def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None, pack=64 << 10, use_graph=False,
+               distance=0):
     import torch
     from paper_2010_14109_b200 import binding as B
     from paper_2010_14109_b200.runtime import OutOfCoreStep
@@ -140,11 +147,11 @@ def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None,
     W = window if window is not None else G.max_feasible_window(budget)
     # VA physical pool: scheduler budget + chunk rounding headroom (Eq.2: IF < N_max·m_c)
     probe = G.plan(budget, W, B.OC_ALLOC_VA if mode == "va" else B.OC_ALLOC_ARENA_BEST, chunk_bytes=chunk,
-                   phys_bytes=budget * 4, allow_oom=True)
+                   phys_bytes=budget * 4, allow_oom=True, distance=distance)
     ps = probe.stats()
     phys = ps["peak_phys"] + chunk if mode == "va" else max(ps["peak_phys"], 1)
     st = OutOfCoreStep(doc, budget, W, mode=mode, chunk_bytes=chunk, phys_bytes=phys, timeline=timeline,
-                       pack_threshold=pack, use_graph=use_graph)
+                       pack_threshold=pack, use_graph=use_graph, distance=distance)
     x, y = nets.make_inputs(spec)
     p = nets.make_params(spec)
     if spec["mode"] == "bf16":
@@ -187,7 +194,7 @@ def run_ours(args, rank, world):
     torch.cuda.set_device(dev)
     chunk = args.chunk_mib * MiB
     params = "persistent"
-    doc, info = graphs.build(spec, params=params, inputs="host")
+    doc, info = graphs.build(spec, params=params, inputs="host", pin_below=cfg.get("pin_below", 0))
     G = B.Graph(doc)
     F_peak = G.in_core_peak()
     budget = cfg.get("budget") or int(F_peak * args.budget_frac)
@@ -195,7 +202,10 @@ def run_ours(args, rank, world):
     # (P:120-style); auto = best of a few fractions of the largest feasible W
     wmax = G.max_feasible_window(budget)
     window_probe = []
-    if args.window == "auto":
+    dist_ = {"paper": 0, "vdnn": 1, "lms": args.distance}[args.policy]
+    if dist_:
+        W_sel = 0
+    elif args.window == "auto":
         best = None
         for wf in (0.0, 0.25, 0.5, 1.0):
             Wc = int(wmax * wf)
@@ -221,7 +231,7 @@ def run_ours(args, rank, world):
     # the timed steps replay the step as one CUDA graph (captured after the first
     # warm-up step memoised every VA mapping); --no-graph issues it eagerly
     st, W, phys = setup_step(spec, info, doc, budget, args.mode, chunk, timeline=False, window=W_sel,
-                             use_graph=not args.no_graph)
+                             use_graph=not args.no_graph, distance=dist_)
     uid = None
     if world > 1:
         uid = [nccl_unique_id() if rank == 0 else None]
@@ -254,7 +264,7 @@ def run_ours(args, rank, world):
     d2h = float(np.mean([m["bytes_d2h"] for m in mets]))
     st.close()
     # instrumented pass: identical schedule, CUDA events around every function and transfer
-    sti, _, _ = setup_step(spec, info, doc, budget, args.mode, chunk, timeline=True, window=W_sel)
+    sti, _, _ = setup_step(spec, info, doc, budget, args.mode, chunk, timeline=True, window=W_sel, distance=dist_)
     if world > 1:
         uid2 = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid2, src=0)
@@ -342,6 +352,7 @@ def run_ours(args, rank, world):
         "config": dict(cfg, global_batch=B_glob, per_gpu_batch=spec["batch"], budget_bytes=budget,
                        in_core_footprint_bytes=F_peak, window_bytes=W, window_max_feasible=wmax,
                        window_selection=window_probe or args.window, allocator=args.mode, chunk_bytes=chunk,
+                       swap_policy=args.policy if not dist_ else f"{args.policy} (function distance {dist_})",
                        phys_pool_bytes=phys, parallelism=f"dp{world}", cuda_graph_replay=not args.no_graph,
                        l2_flush="inputs larger than L2 (activations GBs per step)"),
         "clocks": clk.summary(),

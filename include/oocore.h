@@ -159,6 +159,12 @@ typedef struct oc_plan_params {
   uint64_t budget_bytes; /* B: physical budget incl. pinned variables */
   uint64_t window_bytes; /* schedule-window W, or OC_WINDOW_MAX_FEASIBLE (Z12) */
   oc_alloc_model alloc;
+  /* 0: the paper's byte window.  d >= 1: the prior-art window by
+   * function count, r_i = e_{min(i+d, n-1)}: d = 1 is
+   * vDNN's prefetch-one-layer-ahead, a fixed d the LMS graph distance
+   * (P:48-50); window_bytes is then ignored.  Steps (a)-(c) are unchanged. */
+  uint32_t distance;
+  uint32_t reserved; /* must be 0 */
 } oc_plan_params;
 
 typedef struct oc_schedule oc_schedule;
@@ -172,6 +178,9 @@ void oc_schedule_destroy(oc_schedule* s);
 /* max_i B_i(W) + pinned bytes: the smallest feasible budget at window W
  * (DESIGN.md §4 closed form). */
 uint64_t oc_min_feasible_budget(const oc_graph* g, uint64_t window);
+/* The same for the function-distance window d >= 1 (F1): max_i bytes of the
+ * distinct variables of f_i .. f_{i+d}, plus pinned bytes. */
+uint64_t oc_min_feasible_budget_distance(const oc_graph* g, uint32_t distance);
 /* Largest W with oc_min_feasible_budget(W) ≤ budget; OC_E_INFEASIBLE_BUDGET
  * when even W = 0 does not fit. */
 int oc_max_feasible_window(const oc_graph* g, uint64_t budget, uint64_t* window, oc_err* err);

@@ -49,6 +49,16 @@ def window_ends(seq, window):
     return r
 
 
+def window_ends_distance(seq, distance):
+    """Prior-art window of SURVEY §8(f) F1, by function count instead of bytes:
+    r_i = e_{min(i+d, n-1)}.  d = 1 is vDNN's "prefetch one layer ahead"
+    (P:46); a fixed d is LMS's fixed graph distance.  The rest of
+    the sweep — (a) arrivals, (b) oldest-first waits, (c) reservations — is
+    unchanged, so only the window rule differs from the paper's method."""
+    n = len(seq.l)
+    return [seq.e[min(i + distance, n - 1)] for i in range(n)]
+
+
 def window_bytes(g, seq, window):
     """B_i(W): bytes of the distinct variables in v[l_i : r_i]."""
     r = window_ends(seq, window)
@@ -81,15 +91,21 @@ class Schedule:
         self.r = []
 
 
-def build_schedule(g, seq, budget, window):
+def build_schedule(g, seq, budget, window, distance=0):
     """Sweep f_1..f_n performing (a) -> (b) -> (c) at each function.
 
     `budget` is the physical budget B; pinned variables are resident all step,
-    so the scheduler works against B_s = B - Σ pinned (reading Z10)."""
+    so the scheduler works against B_s = B - Σ pinned (reading Z10).
+    distance > 0 replaces the byte window by the prior-art function-distance
+    window (window_ends_distance; `window` is then ignored and reported 0)."""
     attach_bytes(g, seq)
     n = len(seq.l)
     b = g.var_bytes
-    r = window_ends(seq, window)
+    if distance:
+        window = 0
+        r = window_ends_distance(seq, distance)
+    else:
+        r = window_ends(seq, window)
     budget_s = budget - pinned_bytes(g)
 
     sigma = [HOST] * g.n_vars          # Z4: every variable starts on the host
@@ -102,6 +118,7 @@ def build_schedule(g, seq, budget, window):
     peak = 0
     sch = Schedule(n)
     sch.budget, sch.window, sch.r = budget, window, r
+    sch.distance = distance
     bytes_h2d = bytes_alloc = 0
     waited = {}                        # reservation id -> dirty_at_reserve (survivors)
 
@@ -193,14 +210,15 @@ def canonical_json(sch):
                    '"reserve_out":[' + ",".join(str(v) for v in sch.reserve_out[i]) + '],'
                    '"free":[' + ",".join(str(v) for v in sch.free[i]) + ']}')
     s = sch.stats
-    return ('{"v":1,"budget":%d,"window":%d,"fn":[%s],"end_wait":[%s],"stats":{"bytes_h2d":%d,'
+    dist = ',"distance":%d' % sch.distance if getattr(sch, "distance", 0) else ""
+    return ('{"v":1,"budget":%d,"window":%d%s,"fn":[%s],"end_wait":[%s],"stats":{"bytes_h2d":%d,'
             '"bytes_alloc":%d,"bytes_d2h":%d,"bytes_d2h_clean_elided":%d,"peak_sched":%d}}'
-            % (sch.budget, sch.window, ",".join(fns), ",".join(str(v) for v in sch.end_wait),
+            % (sch.budget, sch.window, dist, ",".join(fns), ",".join(str(v) for v in sch.end_wait),
                s["bytes_h2d"], s["bytes_alloc"], s["bytes_d2h"], s["bytes_d2h_clean_elided"],
                s["peak_sched"]))
 
 
-def min_feasible_budget(g, seq, window):
+def min_feasible_budget(g, seq, window, distance=0):
     """Smallest budget B for which build_schedule succeeds at this window,
     found by binary search over B (budget monotonicity S:157)."""
     attach_bytes(g, seq)
@@ -209,7 +227,7 @@ def min_feasible_budget(g, seq, window):
 
     def ok(B):
         try:
-            build_schedule(g, seq, B, window)
+            build_schedule(g, seq, B, window, distance)
             return True
         except InfeasibleBudget:
             return False

@@ -29,7 +29,8 @@ class oc_alloc_model(C.Structure):
 
 
 class oc_plan_params(C.Structure):
-    _fields_ = [("budget_bytes", C.c_uint64), ("window_bytes", C.c_uint64), ("alloc", oc_alloc_model)]
+    _fields_ = [("budget_bytes", C.c_uint64), ("window_bytes", C.c_uint64), ("alloc", oc_alloc_model),
+                ("distance", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class oc_sched_stats(C.Structure):
@@ -94,6 +95,7 @@ _SIGS = {
     "oc_plan_schedule": (C.c_int, [P, C.POINTER(oc_plan_params), C.POINTER(P), E]),
     "oc_schedule_destroy": (None, [P]),
     "oc_min_feasible_budget": (C.c_uint64, [P, C.c_uint64]),
+    "oc_min_feasible_budget_distance": (C.c_uint64, [P, C.c_uint32]),
     "oc_max_feasible_window": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_uint64), E]),
     "oc_schedule_json": (C.c_int, [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "oc_schedule_stats": (C.c_int, [P, C.POINTER(oc_sched_stats)]),
@@ -188,7 +190,9 @@ class Graph:
         lib().oc_graph_footprint(self.h, C.byref(t), C.byref(m))
         return {"total_bytes": t.value, "max_function_bytes": m.value}
 
-    def min_feasible_budget(self, window):
+    def min_feasible_budget(self, window, distance=0):
+        if distance:
+            return lib().oc_min_feasible_budget_distance(self.h, distance)
         return lib().oc_min_feasible_budget(self.h, window)
 
     def max_feasible_window(self, budget):
@@ -198,8 +202,9 @@ class Graph:
         return w.value
 
     def plan(self, budget, window=OC_WINDOW_MAX_FEASIBLE, mode=OC_ALLOC_VA, chunk_bytes=40 << 20,
-             phys_bytes=0, align=512, allow_oom=False):
-        p = oc_plan_params(budget, window, oc_alloc_model(mode, align, chunk_bytes, phys_bytes))
+             phys_bytes=0, align=512, allow_oom=False, distance=0):
+        """distance = 0: the paper's byte window; d >= 1: prior-art function-distance window (F1)."""
+        p = oc_plan_params(budget, window, oc_alloc_model(mode, align, chunk_bytes, phys_bytes), distance, 0)
         h = P()
         err = oc_err()
         rc = lib().oc_plan_schedule(self.h, C.byref(p), C.byref(h), C.byref(err))

@@ -132,7 +132,8 @@ int oc_plan_schedule(const oc_graph* h, const oc_plan_params* p, oc_schedule** o
   if (!h || !p || !out || !h->g.finalized) { Status::make(OC_E_ARG, "null or unfinalized").fill(err); return OC_E_ARG; }
   *out = nullptr;
   uint64_t W = p->window_bytes;
-  if (W == OC_WINDOW_MAX_FEASIBLE) {
+  if (p->distance) W = 0;
+  else if (W == OC_WINDOW_MAX_FEASIBLE) {
     Status st = max_feasible_window(h->g, p->budget_bytes, W);
     if (!st.good()) { st.fill(err); return st.code; }
   }
@@ -140,7 +141,7 @@ int oc_plan_schedule(const oc_graph* h, const oc_plan_params* p, oc_schedule** o
   if (!s) return OC_E_ARG;
   s->owner = h;
   s->s.alloc = p->alloc;
-  Status st = build_schedule(h->g, p->budget_bytes, W, s->s);
+  Status st = build_schedule(h->g, p->budget_bytes, W, s->s, p->distance);
   if (!st.good()) {
     st.fill(err);
     delete s;
@@ -156,6 +157,10 @@ void oc_schedule_destroy(oc_schedule* s) { delete s; }
 
 uint64_t oc_min_feasible_budget(const oc_graph* h, uint64_t window) {
   return h ? min_feasible_budget(h->g, window) : 0;
+}
+
+uint64_t oc_min_feasible_budget_distance(const oc_graph* h, uint32_t distance) {
+  return (h && distance) ? min_feasible_budget(h->g, 0, distance) : 0;
 }
 
 int oc_max_feasible_window(const oc_graph* h, uint64_t budget, uint64_t* window, oc_err* err) {

@@ -108,6 +108,7 @@ struct ReplayStats {
 struct Schedule {
   const Graph* g = nullptr;
   uint64_t budget = 0, window = 0;
+  uint32_t distance = 0;      // > 0: prior-art function-distance window (F1)
   oc_alloc_model alloc{};
   std::vector<int64_t> r;
   std::vector<FnSchedule> fn;
@@ -134,9 +135,10 @@ struct ArenaPlacer {
 };
 
 std::vector<int64_t> window_ends(const Graph& g, uint64_t W);
-uint64_t min_feasible_budget(const Graph& g, uint64_t W);
+std::vector<int64_t> window_ends_distance(const Graph& g, uint32_t d);
+uint64_t min_feasible_budget(const Graph& g, uint64_t W, uint32_t distance = 0);
 Status max_feasible_window(const Graph& g, uint64_t budget, uint64_t& W);
-Status build_schedule(const Graph& g, uint64_t budget, uint64_t W, Schedule& s);
+Status build_schedule(const Graph& g, uint64_t budget, uint64_t W, Schedule& s, uint32_t distance = 0);
 Status replay_allocator(const Graph& g, Schedule& s);
 std::string schedule_json(const Schedule& s);
 

@@ -33,6 +33,16 @@ std::vector<int64_t> window_ends(const Graph& g, uint64_t W) {
   return r;
 }
 
+// Prior-art window by function count: r_i = e_{min(i+d, n−1)};
+// d = 1 is vDNN's prefetch-one-layer-ahead, a fixed d LMS's graph
+// distance.  Steps (a)-(c) are unchanged.
+std::vector<int64_t> window_ends_distance(const Graph& g, uint32_t d) {
+  const uint32_t n = g.nf();
+  std::vector<int64_t> r(n);
+  for (uint32_t i = 0; i < n; ++i) r[i] = g.e[std::min<uint64_t>((uint64_t)i + d, n - 1)];
+  return r;
+}
+
 // B_i(W): bytes of the distinct variables in v[l_i : r_i]; both ends move forward
 static std::vector<uint64_t> window_bytes(const Graph& g, const std::vector<int64_t>& r) {
   std::vector<uint32_t> cnt(g.nv(), 0);
@@ -54,8 +64,8 @@ static std::vector<uint64_t> window_bytes(const Graph& g, const std::vector<int6
   return out;
 }
 
-uint64_t min_feasible_budget(const Graph& g, uint64_t W) {
-  auto r = window_ends(g, W);
+uint64_t min_feasible_budget(const Graph& g, uint64_t W, uint32_t distance) {
+  auto r = distance ? window_ends_distance(g, distance) : window_ends(g, W);
   auto B = window_bytes(g, r);
   uint64_t m = 0;
   for (uint64_t x : B) m = std::max(m, x);
@@ -79,12 +89,13 @@ Status max_feasible_window(const Graph& g, uint64_t budget, uint64_t& W) {
   return Status::ok();
 }
 
-Status build_schedule(const Graph& g, uint64_t budget, uint64_t W, Schedule& s) {
+Status build_schedule(const Graph& g, uint64_t budget, uint64_t W, Schedule& s, uint32_t distance) {
   const uint32_t n = g.nf(), nv = g.nv();
   s.g = &g;
   s.budget = budget;
-  s.window = W;
-  s.r = window_ends(g, W);
+  s.window = distance ? 0 : W;
+  s.distance = distance;
+  s.r = distance ? window_ends_distance(g, distance) : window_ends(g, W);
   s.fn.assign(n, FnSchedule());
   s.end_wait.clear();
   // B_s = B − pinned (Z10); may be negative, then the first function fails in (b)
@@ -344,7 +355,9 @@ Status replay_allocator(const Graph& g, Schedule& s) {
 
 std::string schedule_json(const Schedule& s) {
   std::ostringstream o;
-  o << "{\"v\":1,\"budget\":" << s.budget << ",\"window\":" << s.window << ",\"fn\":[";
+  o << "{\"v\":1,\"budget\":" << s.budget << ",\"window\":" << s.window;
+  if (s.distance) o << ",\"distance\":" << s.distance;
+  o << ",\"fn\":[";
   for (size_t i = 0; i < s.fn.size(); ++i) {
     const FnSchedule& F = s.fn[i];
     if (i) o << ',';

@@ -51,12 +51,27 @@ class Builder:
         return json.dumps({"variables": self.vars, "functions": self.fns}, separators=(",", ":"))
 
 
-def build(spec, params="persistent", inputs="host"):
+def build(spec, params="persistent", inputs="host", pin_below=0):
     """Returns (graph document JSON, info dict).  info maps roles to variable
-    names: params (name -> var), momentum, grads, x, labels, loss, shapes."""
+    names: params (name -> var), momentum, grads, x, labels, loss, shapes.
+
+    pin_below: variables smaller than this many bytes (other than the step's
+    inputs and loss) are pinned — resident for the whole step, charged to the
+    budget, never swapped (Z26: the LMS-style size threshold; with VA
+    chunks of m_c bytes a tensor far below m_c would otherwise map a whole
+    chunk, Eq.1)."""
     if any(l["type"] != "linear" for l in spec["layers"]):
-        return _build_convnet(spec, params, inputs)
-    return _build_mlp(spec, params, inputs)
+        doc, info = _build_convnet(spec, params, inputs)
+    else:
+        doc, info = _build_mlp(spec, params, inputs)
+    if pin_below:
+        d = json.loads(doc)
+        keep = {info["x"], info["labels"], info["loss"]}
+        for v in d["variables"]:
+            if v["bytes"] < pin_below and v["id"] not in keep:
+                v["pinned"], v["persistent"] = True, False
+        doc = json.dumps(d, separators=(",", ":"))
+    return doc, info
 
 
 def _pvars(b, spec, pshapes, params):

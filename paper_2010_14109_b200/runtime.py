@@ -17,7 +17,7 @@ _NP = {"f32": np.float32, "i32": np.int32, "u8": np.uint8, "bf16": np.uint16}
 class OutOfCoreStep:
     def __init__(self, doc, budget, window=B.OC_WINDOW_MAX_FEASIBLE, mode="va", chunk_bytes=40 << 20,
                  phys_bytes=0, device=0, timeline=False, elide_clean=True, align=512, meta=None,
-                 pack_threshold=64 << 10, use_graph=False):
+                 pack_threshold=64 << 10, use_graph=False, distance=0):
         if not torch.cuda.is_available():
             raise RuntimeError("OutOfCoreStep needs a CUDA device (no CPU fallback)")
         self.device = device
@@ -31,7 +31,8 @@ class OutOfCoreStep:
         self.graph = B.Graph(doc)
         m = {"va": B.OC_ALLOC_VA, "best": B.OC_ALLOC_ARENA_BEST, "first": B.OC_ALLOC_ARENA_FIRST}[mode]
         self.mode = mode
-        self.sched = self.graph.plan(budget, window, m, chunk_bytes=chunk_bytes, phys_bytes=phys_bytes, align=align)
+        self.sched = self.graph.plan(budget, window, m, chunk_bytes=chunk_bytes, phys_bytes=phys_bytes, align=align,
+                                     distance=distance)
         st = self.sched.stats()
         self.stats = st
         pool = phys_bytes or (budget - st["pinned_bytes"])

@@ -104,6 +104,39 @@ def test_closed_form_feasibility_scan():
             assert scheduler.min_feasible_budget(g, seq, W) == need
 
 
+def test_distance_window_closed_form_and_special_cases():
+    """F1 prior-art policies (vDNN d = 1, LMS fixed distance d):
+    the window of f_i is V̂_i ∪ ... ∪ V̂_{i+d}, so greedy feasibility is
+    B >= max_i bytes(∪_{j=i..i+d} V̂_j) + pinned — computed here from the
+    functions' variable lists, not from the oracle's window ends; d >= n
+    gives the same events as an infinite byte window; every schedule passes
+    the replay validator."""
+    for seed in range(30):
+        g, seq = _load(sg.random_graph(seed, n_fns=9, n_vars=11, max_bytes=9, p_pinned=0.1))
+        scheduler.attach_bytes(g, seq)
+        pinned = scheduler.pinned_bytes(g)
+        total = sum(g.var_bytes)
+        n = g.n_fns
+        fvars = [set(seq.occ[seq.l[i]:seq.e[i] + 1]) for i in range(n)]
+        for d in (1, 2, 4):
+            need = max(sum(g.var_bytes[v] for v in set().union(*fvars[i:min(i + d, n - 1) + 1]))
+                       for i in range(n)) + pinned
+            for B in range(pinned, total + 2):
+                try:
+                    sch = scheduler.build_schedule(g, seq, B, 0, distance=d)
+                    ok = True
+                except scheduler.InfeasibleBudget:
+                    ok = False
+                assert ok == (need <= B), (seed, d, B, need)
+                if ok:
+                    validate.validate(g, seq, sch, B)
+            assert scheduler.min_feasible_budget(g, seq, 0, distance=d) == need
+        a = scheduler.build_schedule(g, seq, total, 0, distance=n)
+        b = scheduler.build_schedule(g, seq, total, 10 ** 12)
+        assert (a.ins, a.wait_out, a.reserve_out, a.free) == (b.ins, b.wait_out, b.reserve_out, b.free)
+        assert '"distance":%d' % n in scheduler.canonical_json(a)
+
+
 def test_window_infinite_special_case():
     """window and budget >= footprint -> only initial swap-ins and
     terminal frees (plus write-backs of modified persistent variables)."""

@@ -29,21 +29,22 @@ def test_library_loads_and_exports_header_symbols():
     assert set(B.exported_symbols()) == declared
 
 
-def _both(doc, budget, window, mode="va", chunk=4, phys=None, align=1):
+def _both(doc, budget, window, mode="va", chunk=4, phys=None, align=1, distance=0):
     g = graph.load_graph(doc)
     seq = graph.build_sequence(g)
     G = B.Graph(doc)
     try:
-        o = scheduler.build_schedule(g, seq, budget, window)
+        o = scheduler.build_schedule(g, seq, budget, window, distance=distance)
     except scheduler.InfeasibleBudget as e:
         with pytest.raises(B.OcError) as ei:
-            G.plan(budget, window, B.OC_ALLOC_VA, chunk_bytes=1, phys_bytes=max(1, budget))
+            G.plan(budget, window, B.OC_ALLOC_VA, chunk_bytes=1, phys_bytes=max(1, budget), distance=distance)
         assert ei.value.code == B.OC_E_INFEASIBLE_BUDGET
         assert ei.value.fn == e.fn and ei.value.needed == e.needed
         return None
     modes = {"va": B.OC_ALLOC_VA, "best": B.OC_ALLOC_ARENA_BEST, "first": B.OC_ALLOC_ARENA_FIRST}
     phys = phys if phys is not None else max(1, budget)
-    s = G.plan(budget, window, modes[mode], chunk_bytes=chunk, phys_bytes=phys, align=align, allow_oom=True)
+    s = G.plan(budget, window, modes[mode], chunk_bytes=chunk, phys_bytes=phys, align=align, allow_oom=True,
+               distance=distance)
     assert s.json() == scheduler.canonical_json(o)
     assert s.window_ends() == o.r
     st, _ = allocators.replay(g, o, mode, chunk_bytes=chunk, phys_bytes=phys, align=align)
@@ -89,6 +90,26 @@ def test_random_graphs_bit_exact():
         if s is not None:
             hashes.append(hashlib.sha256(s.json().encode()).hexdigest())
     assert len(hashes) > 300
+
+
+def test_prior_art_distance_windows_bit_exact():
+    """F1 policies (vDNN d = 1, LMS-style fixed distance): canonical schedule
+    bytes, window ends, replay integers and infeasibility identical to the
+    oracle on 300 random graphs; min-feasible budgets identical."""
+    n_ok = 0
+    for seed in range(300):
+        doc = sg.random_graph(seed, p_pinned=0.05)
+        g = graph.load_graph(doc)
+        total = sum(g.var_bytes)
+        budget = max(1, total // (1 + seed % 4))
+        d = 1 + seed % 4
+        mode = ("va", "best", "first")[seed % 3]
+        s = _both(doc, budget, 0, mode=mode, chunk=1 + seed % 16, phys=budget + (seed % 7) * 8, distance=d)
+        n_ok += s is not None
+        seq = graph.build_sequence(g)
+        assert B.Graph(doc).min_feasible_budget(0, distance=d) == scheduler.min_feasible_budget(g, seq, 0,
+                                                                                               distance=d)
+    assert n_ok > 100
 
 
 def test_feasibility_helpers_match_oracle():

@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--chunks", default="2")
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--packs", default="65536", help="pack/unpack thresholds in bytes (0 = copy engines only)")
+    ap.add_argument("--pin-below", type=int, default=0, help="pin variables smaller than this (bytes, Z26)")
+    ap.add_argument("--distances", default="", help="also run the prior-art function-distance windows (F1), e.g. 1,2,4")
     a = ap.parse_args()
     import numpy as np
     from paper_2010_14109_b200 import binding as B
@@ -30,7 +32,7 @@ def main():
         spec = nets.preact_resnet(1001, batch=a.batch)
     else:
         spec = nets.resnet(18 if a.config == "r18" else 50, batch=a.batch)
-    doc, info = graphs.build(spec, params="persistent")
+    doc, info = graphs.build(spec, params="persistent", pin_below=a.pin_below)
     G = B.Graph(doc)
     F = G.in_core_peak()
     for frac in [float(x) for x in a.fracs.split(",")]:
@@ -42,13 +44,15 @@ def main():
             continue
         for mode in a.modes.split(","):
             for ch in [int(c) for c in a.chunks.split(",")]:
-                for wf, pk in [(float(x), int(p)) for x in a.wfracs.split(",") for p in a.packs.split(",")]:
+                runs = [(float(x), int(p), 0) for x in a.wfracs.split(",") for p in a.packs.split(",")]
+                runs += [(0.0, int(a.packs.split(",")[0]), int(d)) for d in a.distances.split(",") if d]
+                for wf, pk, dd in runs:
                     W = int(wmax * wf)
                     try:
                         st, W, phys = bench.setup_step(spec, info, doc, budget, mode, ch << 20, timeline=True,
-                                                       window=W, pack=pk)
+                                                       window=W, pack=pk, distance=dd)
                     except Exception as e:  # noqa: BLE001
-                        print(json.dumps({"frac": frac, "mode": mode, "chunk_mib": ch, "wfrac": wf,
+                        print(json.dumps({"frac": frac, "mode": mode, "chunk_mib": ch, "wfrac": wf, "distance": dd,
                                           "error": str(e)[:200]}), flush=True)
                         continue
                     st.step()
@@ -58,7 +62,7 @@ def main():
                                                                          "bytes_d2h", "n_h2d", "n_d2h")}
                     mem = st.mem_stats()
                     print(json.dumps({"frac": frac, "budget": budget, "mode": mode, "chunk_mib": ch, "wfrac": wf,
-                                      "pack": pk,
+                                      "pack": pk, "policy": "paper" if not dd else f"distance {dd}",
                                       "window": W, "phys": phys, "samples_per_s": a.batch / m["step_ms"] * 1e3,
                                       **m, "peak_phys": st.stats["peak_phys"], "if_peak": st.stats["if_peak"],
                                       "map_us_total": mem["map_us"]}), flush=True)
