@@ -301,11 +301,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
         float* o = (float*)P.out + ((int64_t)z * P.M + m) * P.N + n0 + j0;
         if (n0 + j0 + 32 <= P.N) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(o + i) = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
-                                                            __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+          for (int i = 0; i < 32; i += 4) {
+            float4 f = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
+                                   __uint_as_float(v[i + 3]));
+            if (P.accumulate) {   // later image slice: partial += (fixed slice order)
+              const float4 old = *reinterpret_cast<const float4*>(o + i);
+              f.x += old.x; f.y += old.y; f.z += old.z; f.w += old.w;
+            }
+            *reinterpret_cast<float4*>(o + i) = f;
+          }
         } else {
-          for (int i = 0; i < 32 && n0 + j0 + i < P.N; ++i) o[i] = __uint_as_float(v[i]);
+          for (int i = 0; i < 32 && n0 + j0 + i < P.N; ++i)
+            o[i] = P.accumulate ? o[i] + __uint_as_float(v[i]) : __uint_as_float(v[i]);
         }
       } else {
         __nv_bfloat16* o = (__nv_bfloat16*)P.out + orow * P.N + n0 + j0;
@@ -370,19 +377,30 @@ __global__ void weight_bf16(const float* __restrict__ w, __nv_bfloat16* __restri
 }
 
 // dW[k][(r,s,c)] = Σ_z part[z][(r,s,c)][k] in split order; partial rows of the
-// padding channels c >= Cw are dropped
-__global__ void wgrad_reduce(int splits, int RSC, int K, int C, int Cw, const float* __restrict__ part,
-                             float* __restrict__ dw) {
+// padding channels c >= Cw are dropped.  32×32 tiles through shared memory so
+// both the partial reads (along k) and the dW writes (along rsc) coalesce.
+__global__ void __launch_bounds__(1024) wgrad_reduce(int splits, int RSC, int K, int C, int Cw,
+                                                     const float* __restrict__ part, float* __restrict__ dw) {
+  __shared__ float tile[32][33];
   const int64_t n = (int64_t)RSC * K;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(i % K);
-    const int rsc = (int)(i / K);
-    const int rs = rsc / C, c = rsc - rs * C;
-    if (c >= Cw) continue;
+  const int k0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 × 32, one output each
+  {
+    const int rsc = r0 + ty, k = k0 + tx;
     float s = 0.f;
-    for (int zz = 0; zz < splits; ++zz) s += part[(int64_t)zz * n + i];
-    dw[(int64_t)k * (RSC / C) * Cw + rs * Cw + c] = s;
+    if (rsc < RSC && k < K) {
+      const int64_t i = (int64_t)rsc * K + k;
+#pragma unroll 8
+      for (int zz = 0; zz < splits; ++zz) s += part[(int64_t)zz * n + i];   // loads independent, sum in order
+    }
+    tile[ty][tx] = s;
   }
+  __syncthreads();
+  const int k = k0 + ty, rsc = r0 + tx;
+  if (rsc >= RSC || k >= K) return;
+  const int rs = rsc / C, c = rsc - rs * C;
+  if (c >= Cw) return;
+  dw[(int64_t)k * (RSC / C) * Cw + rs * Cw + c] = tile[tx][ty];
 }
 
 template <int MODE, int BN>
@@ -430,7 +448,7 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
 Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* wt,
                       __nv_bfloat16* dx, bool accumulate);
 Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
-                      int splits, int kb_per_split);
+                      int splits, int kb_per_split, bool accumulate);
 
 bool conv_tc_ok(const ConvGeom& g, int mode) {
   // 32-bit element indices of the activations (the 64-bit tensor offsets are formed per row)
@@ -580,6 +598,7 @@ __global__ void wgrad_reduce_s2d(int splits, int RSC2, int K, const float* __res
     const int tr = r + 2 * c2 - pad, ts = s + 2 * c2 - pad;
     const int row = ((tr >> 1) * S2 + (ts >> 1)) * 16 + ((tr & 1) * 2 + (ts & 1)) * C + c;
     float acc = 0.f;
+#pragma unroll 8
     for (int z = 0; z < splits; ++z) acc += part[((int64_t)z * RSC2 + row) * K + k];
     dw[e] = acc;
   }
@@ -596,7 +615,7 @@ size_t conv_tc_ws(const ConvGeom& g0, int mode) {
     ConvGeom gs = g;
     gs.N = (int)nw.slice;
     const int64_t nsl = (g.N + nw.slice - 1) / nw.slice;
-    return align256((size_t)nsl * wgrad_splits(gs, wgrad_bn(g)) * g.R * g.S * g.C * g.K * 4) + nw.slice_bytes;
+    return align256((size_t)wgrad_splits(gs, wgrad_bn(g)) * g.R * g.S * g.C * g.K * 4) + nw.slice_bytes;
   }
   return align256((size_t)g.K * kpad_of(g) * 2) + nw.slice_bytes;
 }
@@ -703,8 +722,9 @@ Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* dy, con
   }
   const int64_t nsl = (g.N + nw.slice - 1) / nw.slice;
   const int RSC = g.R * g.S * g.C;
+  // one set of split partials; image slices after the first accumulate into it
   float* part = (float*)a.ws;
-  __nv_bfloat16* xbuf = (__nv_bfloat16*)((char*)a.ws + align256((size_t)nsl * splits * RSC * g.K * 4));
+  __nv_bfloat16* xbuf = (__nv_bfloat16*)((char*)a.ws + align256((size_t)splits * RSC * g.K * 4));
   for (int64_t sl = 0; sl < nsl; ++sl) {
     const int64_t n0 = sl * nw.slice;
     const int64_t nn = g.N - n0 < nw.slice ? g.N - n0 : nw.slice;
@@ -718,7 +738,8 @@ Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* dy, con
       P.act = xbuf;
     }
     P.wgt = dy + n0 * g.P * g.Q * g.K;
-    P.out = part + sl * splits * (int64_t)RSC * g.K;
+    P.out = part;
+    P.accumulate = sl > 0 ? 1 : 0;
     P.M = RSC;
     P.N = g.K;
     P.gemm_k = (int)(nn * g.P * g.Q);
@@ -726,7 +747,7 @@ Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* dy, con
     P.kb_per_split = (kbs + splits - 1) / splits;
     P.nkb = P.kb_per_split;
     if (conv_tma_ok(P.g, WGRAD)) {
-      Status st = conv_wgrad_tma(a, P.g, P.act, P.wgt, (float*)P.out, splits, P.kb_per_split);
+      Status st = conv_wgrad_tma(a, P.g, P.act, P.wgt, (float*)P.out, splits, P.kb_per_split, sl > 0);
       if (!st.good()) return st;
       continue;
     }
@@ -737,10 +758,10 @@ Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* dy, con
   }
   if (nw.s2d)
     wgrad_reduce_s2d<<<grid_for((int64_t)g0.K * g0.R * g0.S * g0.C, 256, 4), 256, 0, a.stream>>>(
-        (int)(nsl * splits), RSC, g.K, part, dw, g0.R, g0.S, g0.C, g.S, g.pad, g0.pad);
+        splits, RSC, g.K, part, dw, g0.R, g0.S, g0.C, g.S, g.pad, g0.pad);
   else
-    wgrad_reduce<<<grid_for((int64_t)RSC * g.K, 256, 4), 256, 0, a.stream>>>((int)(nsl * splits), RSC, g.K, g.C,
-                                                                            g.Cw, part, dw);
+    wgrad_reduce<<<dim3((g.K + 31) / 32, (RSC + 31) / 32), 1024, 0, a.stream>>>(splits, RSC, g.K, g.C, g.Cw, part,
+                                                                               dw);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }

@@ -38,8 +38,14 @@ namespace tma {
 using namespace tcu;
 
 constexpr int BM = 128, BK = 64, NTHREADS = 192;
-__host__ __device__ constexpr int tma_stages(int bn) { return bn == 64 ? 8 : 6; }
-__host__ __device__ constexpr int tma_smem(int bn) { return tma_stages(bn) * (BM * BK * 2 + bn * BK * 2) + 1024 + 256; }
+// stages: as many as fit ~196 KB (at most 8)
+__host__ __device__ constexpr int tma_stage_bytes(int bn, int mt) { return mt * BM * BK * 2 + bn * BK * 2; }
+__host__ __device__ constexpr int tma_stages(int bn, int mt) {
+  return (196 * 1024) / tma_stage_bytes(bn, mt) < 8 ? (196 * 1024) / tma_stage_bytes(bn, mt) : 8;
+}
+__host__ __device__ constexpr int tma_smem(int bn, int mt) {
+  return tma_stages(bn, mt) * tma_stage_bytes(bn, mt) + 1024 + 256;
+}
 
 struct Params {
   CUtensorMap ta;          // im2col map of the gathered activation (X or dY)
@@ -69,11 +75,11 @@ __device__ __forceinline__ void base_of(const Params& P, int pix, int& w, int& h
   n = (int)nn;
 }
 
-template <int MODE, int BN, int NCH>
+template <int MODE, int BN, int NCH, int MT>
 __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_constant__ Params P) {
-  constexpr int NST = tma_stages(BN);
-  constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
-  constexpr uint32_t TCOLS = 2 * BN;
+  constexpr int NST = tma_stages(BN, MT);
+  constexpr int A_TILE = BM * BK * 2, A_BYTES = MT * A_TILE, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
+  constexpr uint32_t TCOLS = 2 * MT * BN;   // two accumulator sets of MT tiles × BN columns
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + NST * STAGE);
@@ -107,6 +113,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  // a unit = MT consecutive 128-row tiles (super-tile mt) × one BN column block (× one split)
   const int units = P.num_m * P.num_n * (MODE == WGRAD ? P.splits : 1);
   auto unit_of = [&](int u, int& mt, int& nt, int& z, int& kb0, int& nk) {
     nt = u % P.num_n;
@@ -130,8 +137,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         int mt, nt, z, kb0, nk;
         unit_of(u, mt, nt, z, kb0, nk);
-        int bw = 0, bh = 0, bn = 0;
-        if (MODE != WGRAD) base_of(P, mt * BM, bw, bh, bn);
+        int bw[MT], bh[MT], bn[MT];
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          bw[t] = bh[t] = bn[t] = 0;
+          if (MODE != WGRAD) base_of(P, (mt * MT + t) * BM, bw[t], bh[t], bn[t]);
+        }
         for (int i = 0; i < nk; ++i, ++it) {
           const int sg = (int)(it % NST);
           if (it >= (uint32_t)NST) mbar_wait(&empty[sg], ((it / NST) - 1) & 1);
@@ -140,13 +151,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
           if (MODE == WGRAD) {
             int pw, ph, pn;
             base_of(P, kb * BK, pw, ph, pn);
-            uint32_t bytes = B_BYTES;
-            const int rb0 = mt * 2;   // 64-row blocks of (r,s,c)
-            const int nrb = (P.M - mt * BM) >= BM ? 2 : ((P.M - mt * BM) + 63) / 64;
-            bytes += nrb * 8192;
-            mbar_expect_tx(&full[sg], bytes);
+            // 64-row (tap, 64-channel) blocks of (r,s,c) inside the M range
+            const int rb0 = mt * MT * 2;
+            int nrb = (P.M + 63) / 64 - rb0;
+            nrb = nrb < 2 * MT ? nrb : 2 * MT;
+            mbar_expect_tx(&full[sg], B_BYTES + nrb * 8192);
             for (int j = 0; j < nrb; ++j) {
-              const int blk = rb0 + j;                     // (tap, 64-channel block)
+              const int blk = rb0 + j;
               const int tap = (int)P.fCb.div((uint32_t)blk), cb = blk - tap * (P.Cr / 64);
               const int r = (int)P.fS.div((uint32_t)tap), s = tap - r * P.S;
               tma_load_im2col(a + j * 8192, &P.ta, &full[sg], cb * 64, pw, ph, pn, (uint16_t)s, (uint16_t)r);
@@ -159,17 +170,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
             const int t0 = kb * TPB;
             int ntap = P.R * P.S - t0;
             ntap = ntap < TPB ? ntap : TPB;
-            mbar_expect_tx(&full[sg], B_BYTES + ntap * BOX);
-            for (int j = 0; j < ntap; ++j) {
-              const int r = (int)P.fS.div((uint32_t)(t0 + j)), s = t0 + j - r * P.S;
-              tma_load_im2col(a + j * BOX, &P.ta, &full[sg], 0, bw, bh, bn, (uint16_t)s, (uint16_t)r);
-            }
+            mbar_expect_tx(&full[sg], B_BYTES + MT * ntap * BOX);
+#pragma unroll
+            for (int t = 0; t < MT; ++t)
+              for (int j = 0; j < ntap; ++j) {
+                const int r = (int)P.fS.div((uint32_t)(t0 + j)), s = t0 + j - r * P.S;
+                tma_load_im2col(a + t * A_TILE + j * BOX, &P.ta, &full[sg], 0, bw[t], bh[t], bn[t], (uint16_t)s,
+                                (uint16_t)r);
+              }
             tma_load_2d(b, &P.tb, &full[sg], kb * BK, nt * BN);
           } else {
             mbar_expect_tx(&full[sg], STAGE);
             const int tap = (int)P.fCb.div((uint32_t)kb), cb = kb - tap * (P.Cr / 64);
             const int r = (int)P.fS.div((uint32_t)tap), s = tap - r * P.S;
-            tma_load_im2col(a, &P.ta, &full[sg], cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
+#pragma unroll
+            for (int t = 0; t < MT; ++t)
+              tma_load_im2col(a + t * A_TILE, &P.ta, &full[sg], cb * 64, bw[t], bh[t], bn[t], (uint16_t)s,
+                              (uint16_t)r);
             const int btap = MODE == DGRAD ? (P.r0 + P.dst * (P.R - 1 - r)) * P.Sw + P.s0 + P.dst * (P.S - 1 - s) : tap;
             tma_load_2d(b, &P.tb, &full[sg], btap * P.Cr + cb * 64, nt * BN);
           }
@@ -186,30 +203,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
       const uint32_t buf = lt & 1;
       if (lt >= 2) mbar_wait(&tempty[buf], ((lt >> 1) - 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t d = tmem + buf * BN;
+      const uint32_t d = tmem + buf * MT * BN;
       for (int i = 0; i < nk; ++i, ++it) {
         const int sg = (int)(it % NST);
         mbar_wait(&full[sg], (it / NST) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
-          const uint32_t a = smem_u32(smem + sg * STAGE), b = a + A_BYTES;
+          const uint32_t a0 = smem_u32(smem + sg * STAGE), b = a0 + A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            uint64_t da, db;
-            if (MODE == WGRAD) {          // MN-major: 64-wide MN atoms 8 KB apart, 8-row K groups 1 KB apart
-              da = sdesc(a + k * 2048, 8192, 1024);
-              db = sdesc(b + k * 2048, 8192, 1024);
-            } else if (NCH == 8) {        // K-major, no swizzle: taps 2 KB apart, 8-row groups 128 B apart
-              da = sdesc(a + k * 2 * 2048, 2048, 128, 0);
-              db = sdesc(b + k * 32, 16, 1024);
-            } else if (NCH == 16) {       // K-major SWIZZLE_32B: one tap (16 ch) per K-step, 8-row atoms 256 B apart
-              da = sdesc(a + k * 4096, 16, 256, 6);
-              db = sdesc(b + k * 32, 16, 1024);
-            } else {                      // K-major SWIZZLE_128B
-              da = sdesc(a + k * 32, 16, 1024);
-              db = sdesc(b + k * 32, 16, 1024);
+            uint64_t db;
+            if (MODE == WGRAD) db = sdesc(b + k * 2048, 8192, 1024);   // MN-major: atoms 8 KB, K groups 1 KB
+            else db = sdesc(b + k * 32, 16, 1024);                      // K-major SWIZZLE_128B
+#pragma unroll
+            for (int t = 0; t < MT; ++t) {
+              const uint32_t a = a0 + t * A_TILE;
+              uint64_t da;
+              if (MODE == WGRAD) da = sdesc(a + k * 2048, 8192, 1024);
+              else if (NCH == 8) da = sdesc(a + k * 2 * 2048, 2048, 128, 0);   // no swizzle: taps 2 KB apart
+              else if (NCH == 16) da = sdesc(a + k * 4096, 16, 256, 6);        // SWIZZLE_32B: one tap per K-step
+              else da = sdesc(a + k * 32, 16, 1024);
+              mma_bf16(d + t * BN, da, db, ID, (i > 0 || k > 0) ? 1u : 0u);
             }
-            mma_bf16(d, da, db, ID, (i > 0 || k > 0) ? 1u : 0u);
           }
           mma_commit(&empty[sg]);
         }
@@ -229,52 +244,61 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
       const uint32_t buf = lt & 1;
       mbar_wait(&tfull[buf], (lt >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int m = mt * BM + row;
-      int64_t orow = m;
-      if (MODE == DGRAD && m < P.M) {
-        int w, h, n;
-        base_of(P, m, w, h, n);     // (w, h) = (w' − pad', h' − pad')
-        orow = ((int64_t)n * P.Ho + (h + P.padh) * P.dst + P.ph) * P.Wo + (w + P.padw) * P.dst + P.pw;
-      }
 #pragma unroll
-      for (int j0 = 0; j0 < BN; j0 += 32) {
-        uint32_t v[32];
-        TMEM_LD32(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + j0, v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (nk == 0) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 0u;
+      for (int t = 0; t < MT; ++t) {
+        const int m = (mt * MT + t) * BM + row;
+        int64_t orow = m;
+        if (MODE == DGRAD && m < P.M) {
+          int w, h, n;
+          base_of(P, m, w, h, n);     // (w, h) = (w' − pad', h' − pad')
+          orow = ((int64_t)n * P.Ho + (h + P.padh) * P.dst + P.ph) * P.Wo + (w + P.padw) * P.dst + P.pw;
         }
-        if (m >= P.M) continue;
-        const int col = nt * BN + j0;
-        if (MODE == WGRAD) {
-          float* o = (float*)P.out + ((int64_t)z * P.M + m) * P.N + col;
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(o + i) = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
-                                                            __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
-        } else {
-          __nv_bfloat16* o = (__nv_bfloat16*)P.out + orow * P.N + col;
+        for (int j0 = 0; j0 < BN; j0 += 32) {
+          uint32_t v[32];
+          TMEM_LD32(tmem + ((uint32_t)(q * 32) << 16) + (buf * MT + t) * BN + j0, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (nk == 0) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            float f[8];
+            for (int e = 0; e < 32; ++e) v[e] = 0u;
+          }
+          if (m >= P.M) continue;
+          const int col = nt * BN + j0;
+          if (MODE == WGRAD) {
+            float* o = (float*)P.out + ((int64_t)z * P.M + m) * P.N + col;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[i + e]);
-            if (P.accumulate) {
-              uint4 old = *reinterpret_cast<const uint4*>(o + i);
-              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&old);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 ff = __bfloat1622float2(h2[e]);
-                f[2 * e] += ff.x;
-                f[2 * e + 1] += ff.y;
+            for (int i = 0; i < 32; i += 4) {
+              float4 f = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
+                                     __uint_as_float(v[i + 3]));
+              if (P.accumulate) {   // later image slice: partial += (fixed slice order)
+                const float4 old = *reinterpret_cast<const float4*>(o + i);
+                f.x += old.x; f.y += old.y; f.z += old.z; f.w += old.w;
               }
+              *reinterpret_cast<float4*>(o + i) = f;
             }
-            uint4 pk;
-            __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+          } else {
+            __nv_bfloat16* o = (__nv_bfloat16*)P.out + orow * P.N + col;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) p2[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
-            *reinterpret_cast<uint4*>(o + i) = pk;
+            for (int i = 0; i < 32; i += 8) {
+              float f[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[i + e]);
+              if (P.accumulate) {
+                uint4 old = *reinterpret_cast<const uint4*>(o + i);
+                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&old);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 ff = __bfloat1622float2(h2[e]);
+                  f[2 * e] += ff.x;
+                  f[2 * e + 1] += ff.y;
+                }
+              }
+              uint4 pk;
+              __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) p2[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+              *reinterpret_cast<uint4*>(o + i) = pk;
+            }
           }
         }
       }
@@ -345,20 +369,39 @@ void fill(Params& P) {
   P.fS.init(P.S);
 }
 
-template <int MODE, int BN, int NCH>
-Status launch(OpArgs& a, const Params& P) {
-  constexpr int smem = tma_smem(BN);
-  auto kern = conv_tma_kernel<MODE, BN, NCH>;
+int conv_mt() {
+  static int mt = 0;
+  if (!mt) {
+    const char* e = std::getenv("OC_CONV_MT");
+    mt = (e && e[0] == '1') ? 1 : 2;
+  }
+  return mt;
+}
+
+template <int MODE, int BN, int NCH, int MT>
+Status launch_mt(OpArgs& a, Params P) {
+  constexpr int smem = tma_smem(BN, MT);
+  auto kern = conv_tma_kernel<MODE, BN, NCH, MT>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
+  P.num_m = (P.M + BM * MT - 1) / (BM * MT);   // super-tiles of MT × 128 rows
   const int units = P.num_m * P.num_n * (MODE == WGRAD ? P.splits : 1);
   if (units == 0) return Status::ok();
   kern<<<std::min(units, sm_count()), NTHREADS, smem, a.stream>>>(P);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
+}
+
+// fprop / dgrad: MT = 2, each unit is two 128-row tiles sharing every B stage
+// (half the B traffic per FLOP; measured 7-16% faster).  wgrad keeps single
+// tiles: its M = R·S·C is short (e.g. 576) and pairs would pad it further.
+// OC_CONV_MT=1 selects single tiles everywhere.
+template <int MODE, int BN, int NCH>
+Status launch(OpArgs& a, const Params& P) {
+  return (MODE != WGRAD && conv_mt() == 2) ? launch_mt<MODE, BN, NCH, 2>(a, P) : launch_mt<MODE, BN, NCH, 1>(a, P);
 }
 
 }  // namespace tma
@@ -471,7 +514,7 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
 
 // wgrad partials part[z][R·S·C][K] over pixel blocks [z·kbps, (z+1)·kbps)
 Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
-                      int splits, int kb_per_split) {
+                      int splits, int kb_per_split, bool accumulate) {
   Params P{};
   Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, 64, BK, g.P, g.Q, g.st, g.pad, g.pad);
   if (!st.good()) return st;
@@ -479,6 +522,7 @@ Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   st = make_tiled(&P.tb, dy, (uint64_t)g.K, (uint64_t)g.N * g.P * g.Q, 64);
   if (!st.good()) return st;
   P.out = part;
+  P.accumulate = accumulate ? 1 : 0;
   P.M = g.R * g.S * g.C;
   P.N = g.K;
   P.num_m = (P.M + BM - 1) / BM;

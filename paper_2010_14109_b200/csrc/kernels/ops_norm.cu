@@ -106,24 +106,47 @@ size_t bn_ws(const JVal& at) {
 }
 
 // ---------------------------------------------------------------- forward
+// Elementwise kernels map thread t of a block to channel group t % (C/8) of
+// row t / (C/8), blocks to consecutive row groups: a block touches one
+// contiguous span, and each thread's 8 channels — hence its per-channel
+// parameters, held in registers — never change.
+inline int rowgroup_blocks(int64_t rows, int C) {
+  const int tpr = 256 / (C / 8);
+  return (int)std::max<int64_t>(1, std::min<int64_t>((rows + tpr - 1) / tpr, 148 * 16));
+}
+
 template <typename T>
-__global__ void bn_apply_fwd(uint32_t n8, int C, FastDivU fc8, const T* __restrict__ y, const float* __restrict__ stat,
-                             const float* __restrict__ gamma, const float* __restrict__ beta, const T* __restrict__ res,
-                             T* __restrict__ out, int relu) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
-    const int c0 = (int)fc8.mod(i) * 8;
-    V8 x = ld8(y + (int64_t)i * 8);
-    V8 r;
-    if (res) r = ld8(res + (int64_t)i * 8);
+__global__ void __launch_bounds__(256) bn_apply_fwd(int64_t rows, int C, const T* __restrict__ y,
+                                                    const float* __restrict__ stat, const float* __restrict__ gamma,
+                                                    const float* __restrict__ beta, const T* __restrict__ res,
+                                                    T* __restrict__ out, int relu) {
+  const int gC = C / 8, tpr = 256 / gC;
+  const int cg = threadIdx.x % gC, rr = threadIdx.x / gC;
+  if (rr >= tpr) return;
+  float mu[8], rs[8], gm[8], bt[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = cg * 8 + k;
+    mu[k] = stat[c];
+    rs[k] = stat[C + c];
+    gm[k] = gamma[c];
+    bt[k] = beta[c];
+  }
+  const int64_t stride = (int64_t)gridDim.x * tpr;
+#pragma unroll 2
+  for (int64_t r = (int64_t)blockIdx.x * tpr + rr; r < rows; r += stride) {
+    const int64_t o = r * C + cg * 8;
+    V8 x = ld8(y + o);
+    V8 rv;
+    if (res) rv = ld8(res + o);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int c = c0 + k;
-      float z = fmaf(gamma[c], (x.v[k] - stat[c]) * stat[C + c], beta[c]);
-      if (res) z += r.v[k];
+      float z = fmaf(gm[k], (x.v[k] - mu[k]) * rs[k], bt[k]);
+      if (res) z += rv.v[k];
       if (relu) z = fmaxf(z, 0.f);
       x.v[k] = z;
     }
-    st8(out + (int64_t)i * 8, x);
+    st8(out + o, x);
   }
 }
 
@@ -134,13 +157,10 @@ Status bn_fwd_t(OpArgs& a) {
   const int C = (int)A(a, "C");
   auto y = (const T*)a.p(BF_Y);
   OC_TRY(batch_stats<T>(a, rows, C, y, (float*)a.p(BF_STAT)));
-  const uint32_t n8 = (uint32_t)(rows * C / 8);
-  FastDivU fc8;
-  fc8.init(C / 8);
-  bn_apply_fwd<T><<<grid_for(n8, 256, 4), 256, 0, a.stream>>>(n8, C, fc8, y, (const float*)a.p(BF_STAT),
-                                                              (const float*)a.p(BF_GAMMA), (const float*)a.p(BF_BETA),
-                                                              (const T*)a.p(BF_RES), (T*)a.p(BF_OUT),
-                                                              Ab(a, "relu") ? 1 : 0);
+  bn_apply_fwd<T><<<rowgroup_blocks(rows, C), 256, 0, a.stream>>>(rows, C, y, (const float*)a.p(BF_STAT),
+                                                                  (const float*)a.p(BF_GAMMA),
+                                                                  (const float*)a.p(BF_BETA), (const T*)a.p(BF_RES),
+                                                                  (T*)a.p(BF_OUT), Ab(a, "relu") ? 1 : 0);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
@@ -235,25 +255,39 @@ Status bn_bwd_reduce_t(OpArgs& a) {
 // already holds a gradient contribution (acc), accumulated into it as
 // rnd(G + dy); dz written over g (residual branch)
 template <typename T>
-__global__ void bnb_apply(uint32_t n8, int C, FastDivU fc8, float inv_n, T* g, const T* __restrict__ out, T* y,
-                          const float* __restrict__ stat, const float* __restrict__ gamma,
-                          const float* __restrict__ beta, const float* __restrict__ dgamma,
-                          const float* __restrict__ dbeta, int relu, int write_dz, T* acc) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
-    const int c0 = (int)fc8.mod(i) * 8;
-    const int64_t o = (int64_t)i * 8;
+__global__ void __launch_bounds__(256) bnb_apply(int64_t rows, int C, float inv_n, T* g, const T* __restrict__ out,
+                                                 T* y, const float* __restrict__ stat, const float* __restrict__ gamma,
+                                                 const float* __restrict__ beta, const float* __restrict__ dgamma,
+                                                 const float* __restrict__ dbeta, int relu, int write_dz, T* acc) {
+  const int gC = C / 8, tpr = 256 / gC;
+  const int cg = threadIdx.x % gC, rr = threadIdx.x / gC;
+  if (rr >= tpr) return;
+  float mu[8], rs[8], gm[8], bt[8], dg[8], db[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = cg * 8 + k;
+    mu[k] = stat[c];
+    rs[k] = stat[C + c];
+    gm[k] = gamma[c];
+    bt[k] = beta ? beta[c] : 0.f;
+    dg[k] = dgamma[c];
+    db[k] = dbeta[c];
+  }
+  const int64_t stride = (int64_t)gridDim.x * tpr;
+#pragma unroll 2
+  for (int64_t r = (int64_t)blockIdx.x * tpr + rr; r < rows; r += stride) {
+    const int64_t o = r * C + cg * 8;
     V8 gv = ld8(g + o), yv = ld8(y + o);
     V8 ov;
     if (relu && out) ov = ld8(out + o);
     V8 dz, dy;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int c = c0 + k;
-      const float xh = (yv.v[k] - stat[c]) * stat[C + c];
-      const bool on = !relu || (out ? ov.v[k] > 0.f : fmaf(gamma[c], xh, beta[c]) > 0.f);
+      const float xh = (yv.v[k] - mu[k]) * rs[k];
+      const bool on = !relu || (out ? ov.v[k] > 0.f : fmaf(gm[k], xh, bt[k]) > 0.f);
       const float z = on ? gv.v[k] : 0.f;
       dz.v[k] = z;
-      dy.v[k] = gamma[c] * stat[C + c] * (z - dbeta[c] * inv_n - xh * dgamma[c] * inv_n);
+      dy.v[k] = gm[k] * rs[k] * (z - db[k] * inv_n - xh * dg[k] * inv_n);
     }
     if (acc) {
       V8 old = ld8(acc + o);
@@ -271,11 +305,9 @@ template <typename T>
 Status bn_bwd_apply_t(OpArgs& a) {
   const int64_t rows = A(a, "rows");
   const int C = (int)A(a, "C");
-  const uint32_t n8 = (uint32_t)(rows * C / 8);
-  FastDivU fc8;
-  fc8.init(C / 8);
-  bnb_apply<T><<<grid_for(n8, 256, 4), 256, 0, a.stream>>>(
-      n8, C, fc8, 1.f / (float)rows, (T*)a.p(BB_G), (const T*)a.p(BB_OUT), (T*)a.p(BB_Y), (const float*)a.p(BB_STAT),
+  if (C % 8 || C > 2048) return Status::make(OC_E_UNSUPPORTED, "bn: C must be a multiple of 8 and <= 2048");
+  bnb_apply<T><<<rowgroup_blocks(rows, C), 256, 0, a.stream>>>(
+      rows, C, 1.f / (float)rows, (T*)a.p(BB_G), (const T*)a.p(BB_OUT), (T*)a.p(BB_Y), (const float*)a.p(BB_STAT),
       (const float*)a.p(BB_GAMMA), (const float*)a.p(BB_BETA), (const float*)a.p(BB_DGAMMA),
       (const float*)a.p(BB_DBETA), Ab(a, "relu") ? 1 : 0, Ab(a, "has_res") ? 1 : 0,
       Ab(a, "accumulate") ? (T*)a.p(BB_ACC) : nullptr);
@@ -372,17 +404,19 @@ Status bn_relu_pool_fwd_t(OpArgs& a) {
 template <typename T, bool ROUND = true>
 __device__ __forceinline__ void pooled_grad8(const PoolGeom& g, int n, int h, int w, int cg, const T* __restrict__ gp,
                                              const uint8_t* __restrict__ idx, float ga[8]) {
+  const int r = g.r, st = g.st;
 #pragma unroll
   for (int k = 0; k < 8; ++k) ga[k] = 0.f;
-  const int p_lo = max(0, (h + g.pad - g.r + g.st) / g.st), p_hi = min(g.P - 1, (h + g.pad) / g.st);
-  const int q_lo = max(0, (w + g.pad - g.r + g.st) / g.st), q_hi = min(g.Q - 1, (w + g.pad) / g.st);
+  // windows p with p·st − pad <= h <= p·st − pad + r − 1
+  const int p_lo = max(0, (h + g.pad - r + st) / st), p_hi = min(g.P - 1, (h + g.pad) / st);
+  const int q_lo = max(0, (w + g.pad - r + st) / st), q_hi = min(g.Q - 1, (w + g.pad) / st);
   for (int p = p_lo; p <= p_hi; ++p) {
-    const int u = h - (p * g.st - g.pad);
-    if (u < 0 || u >= g.r) continue;
+    const int u = h - (p * st - g.pad);
+    if (u < 0 || u >= r) continue;
     for (int q = q_lo; q <= q_hi; ++q) {
-      const int v = w - (q * g.st - g.pad);
-      if (v < 0 || v >= g.r) continue;
-      const uint8_t tap = (uint8_t)(u * g.r + v);
+      const int v = w - (q * st - g.pad);
+      if (v < 0 || v >= r) continue;
+      const uint8_t tap = (uint8_t)(u * r + v);
       const int64_t oo = (((int64_t)n * g.P + p) * g.Q + q) * g.C + cg * 8;
       uint2 packed = *reinterpret_cast<const uint2*>(idx + oo);
       V8 gv = ld8(gp + oo);
@@ -505,6 +539,15 @@ __global__ void __launch_bounds__(256) pbn_partial(PoolGeom g, const T* __restri
   const int64_t chunk = (rows + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = blockIdx.x * chunk, r1 = min(rows, r0 + chunk);
   float s[8] = {}, q[8] = {};
+  float mu[8], rs[8], gm[8], bt[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = (cg * 8 + k) % C;
+    mu[k] = stat[c];
+    rs[k] = stat[C + c];
+    gm[k] = gamma[c];
+    bt[k] = beta[c];
+  }
   if (rr < tpr)
     for (int64_t r = r0 + rr; r < r1; r += tpr) {
       const uint32_t t1 = g.fW.div((uint32_t)r);
@@ -516,9 +559,8 @@ __global__ void __launch_bounds__(256) pbn_partial(PoolGeom g, const T* __restri
       V8 yv = ld8(y + r * C + cg * 8);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const int c = cg * 8 + k;
-        const float xh = (yv.v[k] - stat[c]) * stat[C + c];
-        const float z = fmaf(gamma[c], xh, beta[c]);
+        const float xh = (yv.v[k] - mu[k]) * rs[k];
+        const float z = fmaf(gm[k], xh, bt[k]);
         const float dz = z > 0.f ? ga[k] : 0.f;
         s[k] += dz;
         q[k] = fmaf(dz, xh, q[k]);
@@ -541,32 +583,193 @@ __global__ void __launch_bounds__(256) pbn_partial(PoolGeom g, const T* __restri
 }
 
 template <typename T>
-__global__ void pbn_apply(PoolGeom g, const T* __restrict__ gp, const uint8_t* __restrict__ idx, T* y,
-                          const float* __restrict__ stat, const float* __restrict__ gamma,
-                          const float* __restrict__ beta, const float* __restrict__ dgamma,
-                          const float* __restrict__ dbeta, float inv_n) {
-  const int C = g.C;
-  const uint32_t total = (uint32_t)g.N * g.H * g.W * (C / 8);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const uint32_t r = g.fc8.div(i);
-    const int cg = (int)(i - r * (C / 8));
-    const uint32_t t1 = g.fW.div(r);
-    const int w = (int)(r - t1 * g.W);
+__global__ void __launch_bounds__(256) pbn_apply(PoolGeom g, const T* __restrict__ gp, const uint8_t* __restrict__ idx,
+                                                 T* y, const float* __restrict__ stat, const float* __restrict__ gamma,
+                                                 const float* __restrict__ beta, const float* __restrict__ dgamma,
+                                                 const float* __restrict__ dbeta, float inv_n) {
+  const int C = g.C, gC = C / 8, tpr = 256 / gC;
+  const int cg = threadIdx.x % gC, rr = threadIdx.x / gC;
+  if (rr >= tpr) return;
+  float mu[8], rs[8], gm[8], bt[8], dg[8], db[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = cg * 8 + k;
+    mu[k] = stat[c];
+    rs[k] = stat[C + c];
+    gm[k] = gamma[c];
+    bt[k] = beta[c];
+    dg[k] = dgamma[c];
+    db[k] = dbeta[c];
+  }
+  const int64_t rows = (int64_t)g.N * g.H * g.W;
+  const int64_t stride = (int64_t)gridDim.x * tpr;
+  for (int64_t r = (int64_t)blockIdx.x * tpr + rr; r < rows; r += stride) {
+    const uint32_t t1 = g.fW.div((uint32_t)r);
+    const int w = (int)((uint32_t)r - t1 * g.W);
     const uint32_t n = g.fH.div(t1);
     const int h = (int)(t1 - n * g.H);
     float ga[8];
     pooled_grad8<T>(g, (int)n, h, w, cg, gp, idx, ga);
-    V8 yv = ld8(y + (int64_t)i * 8);
+    const int64_t o = r * C + cg * 8;
+    V8 yv = ld8(y + o);
     V8 dy;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int c = cg * 8 + k;
-      const float xh = (yv.v[k] - stat[c]) * stat[C + c];
-      const float z = fmaf(gamma[c], xh, beta[c]);
+      const float xh = (yv.v[k] - mu[k]) * rs[k];
+      const float z = fmaf(gm[k], xh, bt[k]);
       const float dz = z > 0.f ? ga[k] : 0.f;
-      dy.v[k] = gamma[c] * stat[C + c] * (dz - dbeta[c] * inv_n - xh * dgamma[c] * inv_n);
+      dy.v[k] = gm[k] * rs[k] * (dz - db[k] * inv_n - xh * dg[k] * inv_n);
     }
-    st8(y + (int64_t)i * 8, dy);   // in place: each thread reads only its own y
+    st8(y + o, dy);   // in place: each thread reads only its own y
+  }
+}
+
+// 3×3 / stride-2 / pad-1 pool over an even H × W map (the stem): a thread
+// owns the 2×2 input block (2i..2i+1, 2j..2j+1) × 8 channels, which only the
+// windows (i|i+1, j|j+1) reach; each window's argmax tap lands in at most one
+// of the four pixels.  Windows are visited in (p, q) ascending order, the order
+// pooled_grad8 sums them in, so the routed gradients are bitwise the same.
+template <typename T>
+__device__ __forceinline__ void pool_block_grad(const PoolGeom& g, int n, int i, int j, int cg, const T* __restrict__ gp,
+                                                const uint8_t* __restrict__ idx, float ga[4][8]) {
+#pragma unroll
+  for (int px = 0; px < 4; ++px)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ga[px][k] = 0.f;
+#pragma unroll
+  for (int wi = 0; wi < 2; ++wi) {
+    const int p = i + wi;
+    if (p >= g.P) continue;
+#pragma unroll
+    for (int wj = 0; wj < 2; ++wj) {
+      const int q = j + wj;
+      if (q >= g.Q) continue;
+      const int64_t oo = (((int64_t)n * g.P + p) * g.Q + q) * g.C + cg * 8;
+      const uint2 packed = *reinterpret_cast<const uint2*>(idx + oo);
+      const V8 gv = ld8(gp + oo);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t tap = ((k < 4 ? packed.x : packed.y) >> (8 * (k & 3))) & 0xff;
+        const int u = (int)((tap * 11) >> 5), v = (int)tap - 3 * u;   // tap / 3, tap % 3 for tap < 9
+        const int dr = 2 * wi - 1 + u, dc = 2 * wj - 1 + v;           // row / col inside the 2×2 block
+#pragma unroll
+        for (int px = 0; px < 4; ++px)
+          if (dr == (px >> 1) && dc == (px & 1)) ga[px][k] += gv.v[k];
+      }
+    }
+  }
+#pragma unroll
+  for (int px = 0; px < 4; ++px)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ga[px][k] = rnd<T>(ga[px][k]);
+}
+
+inline bool stem_pool(const PoolGeom& g) {
+  return g.r == 3 && g.st == 2 && g.pad == 1 && g.H % 2 == 0 && g.W % 2 == 0 && g.P == g.H / 2 && g.Q == g.W / 2;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) pbn_partial_blk(PoolGeom g, const T* __restrict__ gp,
+                                                       const uint8_t* __restrict__ idx, const T* __restrict__ y,
+                                                       const float* __restrict__ stat,
+                                                       const float* __restrict__ gamma,
+                                                       const float* __restrict__ beta, float* __restrict__ part) {
+  const int C = g.C, gC = C / 8, tpr = 256 / gC;
+  const int t = threadIdx.x, cg = t % gC, rr = t / gC;
+  const int64_t units = (int64_t)g.N * g.P * g.Q;           // 2×2 input blocks
+  const int64_t chunk = (units + gridDim.x - 1) / gridDim.x;
+  const int64_t u0 = blockIdx.x * chunk, u1 = min(units, u0 + chunk);
+  float s[8] = {}, q[8] = {};
+  float mu[8], rs[8], gm[8], bt[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = (cg * 8 + k) % C;
+    mu[k] = stat[c];
+    rs[k] = stat[C + c];
+    gm[k] = gamma[c];
+    bt[k] = beta[c];
+  }
+  if (rr < tpr)
+    for (int64_t u = u0 + rr; u < u1; u += tpr) {
+      const uint32_t t1 = g.fQ.div((uint32_t)u);
+      const int j = (int)((uint32_t)u - t1 * g.Q);
+      const uint32_t n = g.fP.div(t1);
+      const int i = (int)(t1 - n * g.P);
+      float ga[4][8];
+      pool_block_grad<T>(g, (int)n, i, j, cg, gp, idx, ga);
+#pragma unroll
+      for (int px = 0; px < 4; ++px) {
+        const int64_t o = (((int64_t)n * g.H + 2 * i + (px >> 1)) * g.W + 2 * j + (px & 1)) * C + cg * 8;
+        const V8 yv = ld8(y + o);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float xh = (yv.v[k] - mu[k]) * rs[k];
+          const float z = fmaf(gm[k], xh, bt[k]);
+          const float dz = z > 0.f ? ga[px][k] : 0.f;
+          s[k] += dz;
+          q[k] = fmaf(dz, xh, q[k]);
+        }
+      }
+    }
+  extern __shared__ float sm[];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) { sm[t * 16 + k] = s[k]; sm[t * 16 + 8 + k] = q[k]; }
+  __syncthreads();
+  for (int c = t; c < C; c += 256) {
+    const int grp = c / 8, lane = c % 8;
+    float as = 0.f, aq = 0.f;
+    for (int k = 0; k < tpr; ++k) {
+      as += sm[(k * gC + grp) * 16 + lane];
+      aq += sm[(k * gC + grp) * 16 + 8 + lane];
+    }
+    part[(int64_t)blockIdx.x * 2 * C + c] = as;
+    part[(int64_t)blockIdx.x * 2 * C + C + c] = aq;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) pbn_apply_blk(PoolGeom g, const T* __restrict__ gp,
+                                                     const uint8_t* __restrict__ idx, T* y,
+                                                     const float* __restrict__ stat, const float* __restrict__ gamma,
+                                                     const float* __restrict__ beta, const float* __restrict__ dgamma,
+                                                     const float* __restrict__ dbeta, float inv_n) {
+  const int C = g.C, gC = C / 8, tpr = 256 / gC;
+  const int cg = threadIdx.x % gC, rr = threadIdx.x / gC;
+  if (rr >= tpr) return;
+  float mu[8], rs[8], gm[8], bt[8], dg[8], db[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = cg * 8 + k;
+    mu[k] = stat[c];
+    rs[k] = stat[C + c];
+    gm[k] = gamma[c];
+    bt[k] = beta[c];
+    dg[k] = dgamma[c];
+    db[k] = dbeta[c];
+  }
+  const int64_t units = (int64_t)g.N * g.P * g.Q;
+  const int64_t stride = (int64_t)gridDim.x * tpr;
+  for (int64_t u = (int64_t)blockIdx.x * tpr + rr; u < units; u += stride) {
+    const uint32_t t1 = g.fQ.div((uint32_t)u);
+    const int j = (int)((uint32_t)u - t1 * g.Q);
+    const uint32_t n = g.fP.div(t1);
+    const int i = (int)(t1 - n * g.P);
+    float ga[4][8];
+    pool_block_grad<T>(g, (int)n, i, j, cg, gp, idx, ga);
+#pragma unroll
+    for (int px = 0; px < 4; ++px) {
+      const int64_t o = (((int64_t)n * g.H + 2 * i + (px >> 1)) * g.W + 2 * j + (px & 1)) * C + cg * 8;
+      const V8 yv = ld8(y + o);
+      V8 dy;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float xh = (yv.v[k] - mu[k]) * rs[k];
+        const float z = fmaf(gm[k], xh, bt[k]);
+        const float dz = z > 0.f ? ga[px][k] : 0.f;
+        dy.v[k] = gm[k] * rs[k] * (dz - db[k] * inv_n - xh * dg[k] * inv_n);
+      }
+      st8(y + o, dy);   // in place: each thread reads only its own four pixels of y
+    }
   }
 }
 
@@ -577,10 +780,14 @@ Status pool_bn_bwd_reduce_t(OpArgs& a) {
   const int64_t rows = (int64_t)g.N * g.H * g.W;
   const int nblk = stat_blocks(rows);
   if (a.ws_bytes < (size_t)nblk * 2 * g.C * 4) return Status::make(OC_E_INVARIANT, "pool_bn_bwd: workspace too small");
-  pbn_partial<T><<<nblk, 256, 256 * 16 * 4, a.stream>>>(g, (const T*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX),
-                                                        (const T*)a.p(PB_Y), (const float*)a.p(PB_STAT),
-                                                        (const float*)a.p(PB_GAMMA), (const float*)a.p(PB_BETA),
-                                                        (float*)a.ws);
+  if (stem_pool(g))
+    pbn_partial_blk<T><<<nblk, 256, 256 * 16 * 4, a.stream>>>(
+        g, (const T*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX), (const T*)a.p(PB_Y), (const float*)a.p(PB_STAT),
+        (const float*)a.p(PB_GAMMA), (const float*)a.p(PB_BETA), (float*)a.ws);
+  else
+    pbn_partial<T><<<nblk, 256, 256 * 16 * 4, a.stream>>>(
+        g, (const T*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX), (const T*)a.p(PB_Y), (const float*)a.p(PB_STAT),
+        (const float*)a.p(PB_GAMMA), (const float*)a.p(PB_BETA), (float*)a.ws);
   OC_LAUNCH_CHECK(a);
   bnb_finalize<<<(g.C + 7) / 8, 256, 0, a.stream>>>(nblk, g.C, (const float*)a.ws, (float*)a.p(PB_DGAMMA),
                                                     (float*)a.p(PB_DBETA));
@@ -591,11 +798,17 @@ template <typename T>
 Status pool_bn_bwd_apply_t(OpArgs& a) {
   PoolGeom g = geom(a);
   const int64_t rows = (int64_t)g.N * g.H * g.W;
-  const int64_t total = rows * (g.C / 8);
-  pbn_apply<T><<<grid_for(total, 256, 2), 256, 0, a.stream>>>(
-      g, (const T*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX), (T*)a.p(PB_Y), (const float*)a.p(PB_STAT),
-      (const float*)a.p(PB_GAMMA), (const float*)a.p(PB_BETA), (const float*)a.p(PB_DGAMMA),
-      (const float*)a.p(PB_DBETA), 1.f / (float)rows);
+  if (g.C % 8 || g.C > 2048) return Status::make(OC_E_UNSUPPORTED, "pool_bn: C must be a multiple of 8 and <= 2048");
+  if (stem_pool(g))
+    pbn_apply_blk<T><<<rowgroup_blocks(rows / 4, g.C), 256, 0, a.stream>>>(
+        g, (const T*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX), (T*)a.p(PB_Y), (const float*)a.p(PB_STAT),
+        (const float*)a.p(PB_GAMMA), (const float*)a.p(PB_BETA), (const float*)a.p(PB_DGAMMA),
+        (const float*)a.p(PB_DBETA), 1.f / (float)rows);
+  else
+    pbn_apply<T><<<rowgroup_blocks(rows, g.C), 256, 0, a.stream>>>(
+        g, (const T*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX), (T*)a.p(PB_Y), (const float*)a.p(PB_STAT),
+        (const float*)a.p(PB_GAMMA), (const float*)a.p(PB_BETA), (const float*)a.p(PB_DGAMMA),
+        (const float*)a.p(PB_DBETA), 1.f / (float)rows);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
