@@ -24,6 +24,15 @@ Definitions used (standard):
               dy = γ/√(σ²+eps) · (dz − mean(dz) − x̂ · mean(dz · x̂))
   softmax-CE  L = mean_n(−log softmax(z_n)[y_n]);  dz = (softmax(z) − onehot)/N
   SGD-mom.    v ← μ v + g;  w ← w − lr · v
+  GAN layers (configs[4] BigGAN-style step):
+  upsample2   y[n,2i+a,2j+b,c] = x[n,i,j,c]          (nearest, ×2)
+  avgpool2    y[n,i,j,c] = ¼ Σ_{a,b} x[n,2i+a,2j+b,c]
+  tanh, relu  elementwise; tanh' = 1 − y², relu'(0) = 0
+  attention   SAGAN self-attention over the H·W positions of one sample:
+              q = x Wqᵀ, k = x Wkᵀ, v = x Wvᵀ (1×1 convs), P = softmax_rows(q kᵀ),
+              o = P v, out = o Woᵀ, y = x + γ·out  (γ a learned scalar, ".gain")
+  hinge       D: L = mean(relu(1 − D(x_real))) + mean(relu(1 + D(G(z))));
+              G: L = −mean(D(G(z)))
 """
 import numpy as np
 
@@ -160,68 +169,250 @@ def softmax_ce(z, labels):
     return loss, dz / N
 
 
+def upsample2(x):
+    return np.repeat(np.repeat(x, 2, axis=1), 2, axis=2)
+
+
+def upsample2_backward(g):
+    """Σ over each 2×2 block, summed in the order (0,0), (0,1), (1,0), (1,1)."""
+    return ((g[:, 0::2, 0::2] + g[:, 0::2, 1::2]) + g[:, 1::2, 0::2]) + g[:, 1::2, 1::2]
+
+
+def avgpool2(x):
+    return 0.25 * (((x[:, 0::2, 0::2] + x[:, 0::2, 1::2]) + x[:, 1::2, 0::2]) + x[:, 1::2, 1::2])
+
+
+def avgpool2_backward(g):
+    return upsample2(0.25 * g)
+
+
+def attention(q, k, v, rnd):
+    """Per sample n: P = softmax over keys of q kᵀ (rows = query positions),
+    stored in the act dtype; o = P v.  q, k [N, L, dq], v [N, L, dv]."""
+    S = np.einsum("nid,njd->nij", q, k)
+    S = S - S.max(axis=2, keepdims=True)
+    e = np.exp(S)
+    P = rnd(e / e.sum(axis=2, keepdims=True))
+    return P, rnd(np.einsum("nij,njd->nid", P, v))
+
+
+def attention_backward(q, k, v, P, o, do):
+    """Gradients of o = softmax(q kᵀ) v wrt q, k, v (P the stored softmax):
+    dv = Pᵀ do; dP = do vᵀ; dS = P ⊙ (dP − rowsum(dP ⊙ P)), rowsum(dP ⊙ P)_i
+    = do_i · o_i; dq = dS k; dk = dSᵀ q."""
+    dv = np.einsum("nij,nid->njd", P, do)
+    dP = np.einsum("nid,njd->nij", do, v)
+    rs = np.einsum("nid,nid->ni", do, o)[:, :, None]
+    dS = P * (dP - rs)
+    return np.einsum("nij,njd->nid", dS, k), np.einsum("nij,nid->njd", dS, q), dv
+
+
 # --------------------------------------------------------------- training step
+
+
+class _Net:
+    """Forward / backward interpreter of a layer list (the definitions above,
+    with the storage roundings of the numerics contract)."""
+
+    def __init__(self, layers, params, mode):
+        self.layers = layers
+        self.mode = mode
+        self.rnd = rounder(mode)
+        self.r32 = _identity if mode == "fp64" else round_fp32
+        self.f64 = {k: np.asarray(v, np.float64) for k, v in params.items()}
+        self.wcopy = {k: self.rnd(v) for k, v in self.f64.items()
+                      if k.endswith((".W", ".W2", ".Wq", ".Wk", ".Wv", ".Wo"))}
+
+    def forward(self, acts, fp32_out=()):
+        rnd, f64, wcopy = self.rnd, self.f64, self.wcopy
+        saved = {}
+        for lay in self.layers:
+            t, nm = lay["type"], lay["name"]
+            xin = acts[lay["in"]]
+            if t == "linear":
+                xi = xin.reshape(xin.shape[0], -1)
+                y = xi @ wcopy[nm + ".W"].T + f64[nm + ".b"]
+                if lay["relu"]:
+                    y = np.maximum(y, 0.0)
+                # logits / scores (a linear feeding a loss) are fp32
+                out = self.r32(y) if lay["out"] in fp32_out else rnd(y)
+                if lay.get("reshape"):
+                    out = out.reshape([xin.shape[0]] + list(lay["reshape"]))
+            elif t == "conv":
+                out = rnd(conv2d(xin, wcopy[nm + ".W"], lay["stride"], lay["pad"]))
+                if lay.get("in2"):
+                    # conv over the concatenation [in, in2] = conv(in, W) + conv(in2, W2);
+                    # contributions to one stored tensor accumulate in order with a
+                    # rounding after each (DESIGN.md Z23)
+                    out = rnd(out + conv2d(acts[lay["in2"]], wcopy[nm + ".W2"], lay["stride"], lay["pad"]))
+            elif t == "convT":
+                out = rnd(conv_transpose2x2(xin, wcopy[nm + ".W"]))
+            elif t == "bn":
+                axes = tuple(range(xin.ndim - 1))
+                mu = xin.mean(axis=axes)
+                var = ((xin - mu) ** 2).mean(axis=axes)
+                rstd = 1.0 / np.sqrt(var + BN_EPS)
+                xhat = (xin - mu) * rstd
+                z = f64[nm + ".gamma"] * xhat + f64[nm + ".beta"]
+                if lay.get("residual"):
+                    z = z + acts[lay["residual"]]
+                if lay["relu"]:
+                    z = np.maximum(z, 0.0)
+                out = rnd(z)
+                saved[nm] = (xhat, rstd)
+            elif t == "maxpool":
+                out, arg = maxpool(xin, lay["r"], lay["stride"], lay["pad"])
+                saved[nm] = arg
+            elif t == "gap":
+                out = rnd(xin.mean(axis=(1, 2)))
+            elif t == "add":                      # residual sum
+                out = rnd(xin + acts[lay["in2"]])
+            elif t == "relu":
+                out = np.maximum(xin, 0.0)
+            elif t == "tanh":
+                out = rnd(np.tanh(xin))
+            elif t == "upsample2":
+                out = upsample2(xin)
+            elif t == "avgpool2":
+                out = rnd(avgpool2(xin))
+            elif t == "attn":
+                N, H, W, C = xin.shape
+                x2 = xin.reshape(N, H * W, C)
+                q = rnd(x2 @ wcopy[nm + ".Wq"].reshape(-1, C).T)
+                k = rnd(x2 @ wcopy[nm + ".Wk"].reshape(-1, C).T)
+                v = rnd(x2 @ wcopy[nm + ".Wv"].reshape(-1, C).T)
+                P, o = attention(q, k, v, rnd)
+                ao = rnd(o @ wcopy[nm + ".Wo"].reshape(C, -1).T)
+                out = rnd(x2 + f64[nm + ".gain"][0] * ao).reshape(xin.shape)
+                saved[nm] = (q, k, v, P, o, ao)
+            else:
+                raise ValueError(t)
+            acts[lay["out"]] = out
+        return saved
+
+    def backward(self, acts, saved, G, grads=None, input_names=()):
+        """Reverse-order backward from the gradients in G (tensor -> grad).
+        grads: dict to fill with parameter gradients, or None (data gradients
+        only).  input_names: graph inputs whose gradient is wanted."""
+        rnd, f64, wcopy, r32 = self.rnd, self.f64, self.wcopy, self.r32
+
+        def acc(name, c):
+            G[name] = rnd(c) if name not in G else rnd(G[name] + c)
+
+        def pg(key, val):
+            if grads is not None:
+                grads[key] = r32(val)
+
+        produced = {lay["out"] for lay in self.layers}
+        for lay in reversed(self.layers):
+            t, nm = lay["type"], lay["name"]
+            if lay["out"] not in G:
+                continue
+            g = G[lay["out"]]
+            xin = acts[lay["in"]]
+            need_dx = lay["in"] in produced or lay["in"] in input_names
+            if t == "linear":
+                out = acts[lay["out"]]
+                g2 = g.reshape(g.shape[0], -1)
+                out2 = out.reshape(out.shape[0], -1)
+                dz = g2 * (out2 > 0) if lay["relu"] else g2
+                xi = xin.reshape(xin.shape[0], -1)
+                pg(nm + ".W", dz.T @ xi)
+                pg(nm + ".b", dz.sum(axis=0))
+                if need_dx:
+                    acc(lay["in"], (dz @ wcopy[nm + ".W"]).reshape(xin.shape))
+            elif t == "conv":
+                dx, dw = conv2d_backward(xin, wcopy[nm + ".W"], g, lay["stride"], lay["pad"])
+                pg(nm + ".W", dw)
+                if need_dx:
+                    acc(lay["in"], dx)
+                if lay.get("in2"):
+                    dx2, dw2 = conv2d_backward(acts[lay["in2"]], wcopy[nm + ".W2"], g, lay["stride"], lay["pad"])
+                    pg(nm + ".W2", dw2)
+                    acc(lay["in2"], dx2)
+            elif t == "convT":
+                dx, dw = conv_transpose2x2_backward(xin, wcopy[nm + ".W"], g)
+                pg(nm + ".W", dw)
+                acc(lay["in"], dx)
+            elif t == "bn":
+                xhat, rstd = saved[nm]
+                out = acts[lay["out"]]
+                dz = g * (out > 0) if lay["relu"] else g
+                axes = tuple(range(xin.ndim - 1))
+                pg(nm + ".gamma", (dz * xhat).sum(axis=axes))
+                pg(nm + ".beta", dz.sum(axis=axes))
+                if lay.get("residual"):
+                    acc(lay["residual"], dz)
+                dy = f64[nm + ".gamma"] * rstd * (dz - dz.mean(axis=axes) - xhat * (dz * xhat).mean(axis=axes))
+                acc(lay["in"], dy)
+            elif t == "maxpool":
+                acc(lay["in"], maxpool_backward(g, saved[nm], xin.shape, lay["r"], lay["stride"], lay["pad"]))
+            elif t == "gap":
+                H, W = xin.shape[1], xin.shape[2]
+                acc(lay["in"], np.broadcast_to(g[:, None, None, :] / (H * W), xin.shape))
+            elif t == "add":
+                acc(lay["in"], g)
+                acc(lay["in2"], g)
+            elif t == "relu":
+                if need_dx:
+                    acc(lay["in"], g * (xin > 0))
+            elif t == "tanh":
+                y = acts[lay["out"]]
+                if need_dx:
+                    acc(lay["in"], g * (1.0 - y * y))
+            elif t == "upsample2":
+                if need_dx:
+                    acc(lay["in"], upsample2_backward(g))
+            elif t == "avgpool2":
+                if need_dx:
+                    acc(lay["in"], avgpool2_backward(g))
+            elif t == "attn":
+                q, k, v, P, o, ao = saved[nm]
+                N, H, W, C = xin.shape
+                x2 = xin.reshape(N, H * W, C)
+                g2 = g.reshape(N, H * W, C)
+                gam = f64[nm + ".gain"][0]
+                pg(nm + ".gain", np.array([(g2 * ao).sum()]))
+                dao = rnd(gam * g2)
+                Wo = wcopy[nm + ".Wo"].reshape(C, -1)
+                pg(nm + ".Wo", (dao.reshape(-1, C).T @ o.reshape(-1, o.shape[-1])).reshape(C, 1, 1, -1))
+                do = rnd(dao @ Wo)
+                dq, dk, dv = attention_backward(q, k, v, P, o, do)
+                dq, dk, dv = rnd(dq), rnd(dk), rnd(dv)
+                # x feeds the residual, then q, k, v (contributions in that order)
+                parts = [g2]
+                for d, wn in ((dq, ".Wq"), (dk, ".Wk"), (dv, ".Wv")):
+                    Wm = wcopy[nm + wn].reshape(-1, C)
+                    pg(nm + wn, (d.reshape(-1, d.shape[-1]).T @ x2.reshape(-1, C)).reshape(-1, 1, 1, C))
+                    parts.append(d @ Wm)
+                if need_dx:
+                    for c in parts:
+                        acc(lay["in"], c.reshape(xin.shape))
+        return G
+
+
+def _sgd(spec, params, grads, momentum, r32):
+    lr, mu = spec["sgd"]["lr"], spec["sgd"]["momentum"]
+    new_p, new_m = {}, {}
+    for k in params:
+        m0 = np.zeros_like(np.asarray(params[k], np.float64)) if momentum is None else np.asarray(momentum[k],
+                                                                                                  np.float64)
+        v = r32(mu * m0 + grads[k])
+        new_m[k] = v
+        new_p[k] = r32(np.asarray(params[k], np.float64) - lr * v)
+    return new_p, new_m
 
 
 def train_step(spec, params, x, labels, momentum=None):
     """One step.  `params`: dict name -> fp32 array (masters); `momentum`:
     dict or None (zeros).  Returns dict with loss, grads, new params, new
     momentum and the stored activations (for inspection)."""
-    mode = spec["mode"]
-    rnd = rounder(mode)
-    round_fp32 = _identity if mode == "fp64" else globals()["round_fp32"]
-    f64 = {k: np.asarray(v, np.float64) for k, v in params.items()}
-    wcopy = {}                                # act-dtype copies of weights
-    for k, v in f64.items():
-        if k.endswith(".W") or k.endswith(".W2"):
-            wcopy[k] = rnd(v)
+    net = _Net(spec["layers"], params, spec["mode"])
+    rnd, r32 = net.rnd, net.r32
     acts = {"x": rnd(np.asarray(x, np.float64))}
-    saved = {}
-    # ---------------- forward
-    for lay in spec["layers"]:
-        t, nm = lay["type"], lay["name"]
-        xin = acts[lay["in"]]
-        if t == "linear":
-            xi = xin.reshape(xin.shape[0], -1)
-            y = xi @ wcopy[nm + ".W"].T + f64[nm + ".b"]
-            if lay["relu"]:
-                y = np.maximum(y, 0.0)
-            # logits (a linear without ReLU feeding the loss) are fp32
-            out = round_fp32(y) if lay["out"] == spec["loss"]["in"] else rnd(y)
-        elif t == "conv":
-            out = rnd(conv2d(xin, wcopy[nm + ".W"], lay["stride"], lay["pad"]))
-            if lay.get("in2"):
-                # conv over the concatenation [in, in2] = conv(in, W) + conv(in2, W2);
-                # contributions to one stored tensor accumulate in order with a
-                # rounding after each (DESIGN.md Z23)
-                out = rnd(out + conv2d(acts[lay["in2"]], wcopy[nm + ".W2"], lay["stride"], lay["pad"]))
-        elif t == "convT":
-            out = rnd(conv_transpose2x2(xin, wcopy[nm + ".W"]))
-        elif t == "bn":
-            axes = tuple(range(xin.ndim - 1))
-            mu = xin.mean(axis=axes)
-            var = ((xin - mu) ** 2).mean(axis=axes)
-            rstd = 1.0 / np.sqrt(var + BN_EPS)
-            xhat = (xin - mu) * rstd
-            z = f64[nm + ".gamma"] * xhat + f64[nm + ".beta"]
-            if lay.get("residual"):
-                z = z + acts[lay["residual"]]
-            if lay["relu"]:
-                z = np.maximum(z, 0.0)
-            out = rnd(z)
-            saved[nm] = (xhat, rstd)
-        elif t == "maxpool":
-            out, arg = maxpool(xin, lay["r"], lay["stride"], lay["pad"])
-            saved[nm] = arg
-        elif t == "gap":
-            out = rnd(xin.mean(axis=(1, 2)))
-        elif t == "add":                      # residual sum of a pre-activation block
-            out = rnd(xin + acts[lay["in2"]])
-        else:
-            raise ValueError(t)
-        acts[lay["out"]] = out
-    grads = {}
-    if spec["loss"]["type"] == "softmax_ce_pix":
+    pix = spec["loss"]["type"] == "softmax_ce_pix"
+    saved = net.forward(acts, fp32_out=() if pix else (spec["loss"]["in"],))
+    if pix:
         # per-pixel cross-entropy over the channel axis, mean over all pixels;
         # the logits are a conv output (act dtype) and so is their gradient
         z = acts[spec["loss"]["in"]]
@@ -230,68 +421,57 @@ def train_step(spec, params, x, labels, momentum=None):
         G = {spec["loss"]["in"]: rnd(dlogits.reshape(z.shape))}
     else:
         loss, dlogits = softmax_ce(acts[spec["loss"]["in"]], labels)
-        G = {spec["loss"]["in"]: round_fp32(dlogits)}   # dlogits stored fp32
-    # ---------------- backward (reverse layer order)
-
-    def acc(name, c):
-        G[name] = rnd(c) if name not in G else rnd(G[name] + c)
-
-    for lay in reversed(spec["layers"]):
-        t, nm = lay["type"], lay["name"]
-        if lay["out"] not in G:
-            continue
-        g = G[lay["out"]]
-        xin = acts[lay["in"]]
-        need_dx = lay["in"] != "x"
-        if t == "linear":
-            out = acts[lay["out"]]
-            dz = g * (out > 0) if lay["relu"] else g
-            xi = xin.reshape(xin.shape[0], -1)
-            grads[nm + ".W"] = round_fp32(dz.T @ xi)
-            grads[nm + ".b"] = round_fp32(dz.sum(axis=0))
-            if need_dx:
-                acc(lay["in"], (dz @ wcopy[nm + ".W"]).reshape(xin.shape))
-        elif t == "conv":
-            dx, dw = conv2d_backward(xin, wcopy[nm + ".W"], g, lay["stride"], lay["pad"])
-            grads[nm + ".W"] = round_fp32(dw)
-            if need_dx:
-                acc(lay["in"], dx)
-            if lay.get("in2"):
-                dx2, dw2 = conv2d_backward(acts[lay["in2"]], wcopy[nm + ".W2"], g, lay["stride"], lay["pad"])
-                grads[nm + ".W2"] = round_fp32(dw2)
-                acc(lay["in2"], dx2)
-        elif t == "convT":
-            dx, dw = conv_transpose2x2_backward(xin, wcopy[nm + ".W"], g)
-            grads[nm + ".W"] = round_fp32(dw)
-            acc(lay["in"], dx)
-        elif t == "bn":
-            xhat, rstd = saved[nm]
-            out = acts[lay["out"]]
-            dz = g * (out > 0) if lay["relu"] else g
-            axes = tuple(range(xin.ndim - 1))
-            grads[nm + ".gamma"] = round_fp32((dz * xhat).sum(axis=axes))
-            grads[nm + ".beta"] = round_fp32(dz.sum(axis=axes))
-            if lay.get("residual"):
-                acc(lay["residual"], dz)
-            dy = f64[nm + ".gamma"] * rstd * (dz - dz.mean(axis=axes) - xhat * (dz * xhat).mean(axis=axes))
-            acc(lay["in"], dy)
-        elif t == "maxpool":
-            acc(lay["in"], maxpool_backward(g, saved[nm], xin.shape, lay["r"], lay["stride"], lay["pad"]))
-        elif t == "gap":
-            H, W = xin.shape[1], xin.shape[2]
-            acc(lay["in"], np.broadcast_to(g[:, None, None, :] / (H * W), xin.shape))
-        elif t == "add":
-            acc(lay["in"], g)
-            acc(lay["in2"], g)
-    # ---------------- SGD with momentum (fp32 state)
-    lr, mu = spec["sgd"]["lr"], spec["sgd"]["momentum"]
-    new_p, new_m = {}, {}
-    for k in params:
-        m0 = np.zeros_like(f64[k]) if momentum is None else np.asarray(momentum[k], np.float64)
-        v = round_fp32(mu * m0 + grads[k])
-        new_m[k] = v
-        new_p[k] = round_fp32(f64[k] - lr * v)
+        G = {spec["loss"]["in"]: r32(dlogits)}   # dlogits stored fp32
+    grads = {}
+    net.backward(acts, saved, G, grads)
+    new_p, new_m = _sgd(spec, params, grads, momentum, r32)
     return {"loss": float(loss), "grads": grads, "params": new_p, "momentum": new_m, "acts": acts}
+
+
+def hinge_d(s, n_real):
+    """D hinge loss over scores s [2N] (real first) and its gradient."""
+    real, fake = s[:n_real], s[n_real:]
+    loss = np.maximum(0.0, 1.0 - real).mean() + np.maximum(0.0, 1.0 + fake).mean()
+    ds = np.concatenate([-(real < 1.0).astype(np.float64) / len(real), (fake > -1.0).astype(np.float64) / len(fake)])
+    return float(loss), ds
+
+
+def gan_step(spec, pG, pD, z1, z2, x_real, momG=None, momD=None):
+    """One BigGAN-style step: a D-step on [x_real; G(z1)]
+    with the hinge loss and an SGD-momentum update of D, then a G-step on
+    G(z2) through the updated D (D's parameters fixed) with L = −mean D(G(z2))
+    and an SGD-momentum update of G."""
+    mode = spec["mode"]
+    N = z1.shape[0]
+    G_, D_ = spec["G"], spec["D"]
+    g_net = _Net(G_["layers"], pG, mode)
+    rnd, r32 = g_net.rnd, g_net.r32
+    # ---- D-step
+    a1 = {"z": r32(np.asarray(z1, np.float64))}
+    g_net.forward(a1)
+    xd = np.concatenate([rnd(np.asarray(x_real, np.float64)), a1[G_["out"]]])
+    d_net = _Net(D_["layers"], pD, mode)
+    ad = {"x": xd}
+    sd = d_net.forward(ad, fp32_out=(D_["out"],))
+    score = ad[D_["out"]].reshape(-1)
+    loss_d, ds = hinge_d(score, N)
+    gradsD = {}
+    d_net.backward(ad, sd, {D_["out"]: r32(ds.reshape(-1, 1))}, gradsD)
+    pD_new, momD_new = _sgd(spec, pD, gradsD, momD, r32)
+    # ---- G-step through the updated D
+    a2 = {"z": r32(np.asarray(z2, np.float64))}
+    sg = g_net.forward(a2)
+    d2 = _Net(D_["layers"], pD_new, mode)
+    ad2 = {"x": a2[G_["out"]]}
+    sd2 = d2.forward(ad2, fp32_out=(D_["out"],))
+    score2 = ad2[D_["out"]].reshape(-1)
+    loss_g = float(-score2.mean())
+    Gd = d2.backward(ad2, sd2, {D_["out"]: r32(np.full((N, 1), -1.0 / N))}, None, input_names=("x",))
+    gradsG = {}
+    g_net.backward(a2, sg, {G_["out"]: Gd["x"]}, gradsG)
+    pG_new, momG_new = _sgd(spec, pG, gradsG, momG, r32)
+    return {"loss_d": loss_d, "loss_g": loss_g, "gradsD": gradsD, "gradsG": gradsG, "pD": pD_new, "pG": pG_new,
+            "momD": momD_new, "momG": momG_new, "score_d": score, "score_g": score2}
 
 
 def rel_l2(a, b):

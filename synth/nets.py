@@ -199,16 +199,20 @@ def tiny_resnet(batch=4, image=16, classes=10, mode="bf16"):
 
 def tensor_shapes(spec):
     """Shape of every activation tensor (without batch) and every parameter."""
-    shapes = {"x": list(spec["input"])}
+    return net_shapes(spec["layers"], "x", list(spec["input"]))
+
+
+def net_shapes(layers, in_name, in_shape):
+    shapes = {in_name: list(in_shape)}
     params = {}
-    for lay in spec["layers"]:
+    for lay in layers:
         t = lay["type"]
         ish = shapes[lay["in"]]
         if t == "linear":
             fin = int(np.prod(ish))
             params[lay["name"] + ".W"] = [lay["features"], fin]
             params[lay["name"] + ".b"] = [lay["features"]]
-            shapes[lay["out"]] = [lay["features"]]
+            shapes[lay["out"]] = list(lay["reshape"]) if lay.get("reshape") else [lay["features"]]
         elif t == "conv":
             H, W, C = ish
             P = (H + 2 * lay["pad"] - lay["r"]) // lay["stride"] + 1
@@ -238,6 +242,21 @@ def tensor_shapes(spec):
         elif t == "add":
             assert shapes[lay["in2"]] == ish, (lay["name"], shapes[lay["in2"]], ish)
             shapes[lay["out"]] = list(ish)
+        elif t in ("relu", "tanh"):
+            shapes[lay["out"]] = list(ish)
+        elif t == "upsample2":
+            shapes[lay["out"]] = [2 * ish[0], 2 * ish[1], ish[2]]
+        elif t == "avgpool2":
+            shapes[lay["out"]] = [ish[0] // 2, ish[1] // 2, ish[2]]
+        elif t == "attn":
+            C = ish[-1]
+            dq, dv = lay["dq"], lay["dv"]
+            params[lay["name"] + ".Wq"] = [dq, 1, 1, C]
+            params[lay["name"] + ".Wk"] = [dq, 1, 1, C]
+            params[lay["name"] + ".Wv"] = [dv, 1, 1, C]
+            params[lay["name"] + ".Wo"] = [C, 1, 1, dv]
+            params[lay["name"] + ".gain"] = [1]
+            shapes[lay["out"]] = list(ish)
         else:
             raise ValueError(t)
     return shapes, params
@@ -257,14 +276,19 @@ def make_inputs(spec, seed_x=0, seed_y=1):
     return x, y
 
 
-def make_params(spec, seed=2):
+def make_params(spec, seed=2, pshapes=None):
     """Linear: W, b ~ U(±1/sqrt(fan_in)); conv: W ~ N(0, 2/fan_in) (He);
-    BN: gamma = 1, beta = 0.  All fp32."""
+    BN: gamma = 1, beta = 0; attention gain γ = 0.5 (BigGAN starts at 0,
+    which would leave the attention weights without gradient in a one-step
+    check).  All fp32."""
     rng = np.random.default_rng(seed)
-    _, pshapes = tensor_shapes(spec)
+    if pshapes is None:
+        _, pshapes = tensor_shapes(spec)
     out = {}
     for name, shp in pshapes.items():
-        if name.endswith(".gamma"):
+        if name.endswith(".gain"):
+            out[name] = np.full(shp, 0.5, np.float32)
+        elif name.endswith(".gamma"):
             out[name] = np.ones(shp, np.float32)
         elif name.endswith(".beta"):
             out[name] = np.zeros(shp, np.float32)
@@ -279,3 +303,103 @@ def make_params(spec, seed=2):
             bound = 1.0 / np.sqrt(fan_in)
             out[name] = rng.uniform(-bound, bound, shp).astype(np.float32)
     return out
+
+
+def biggan(batch=32, image=128, ch=96, z_dim=120, mode="bf16", n_blocks=5, attn_res=64,
+           g_mult=(16, 16, 8, 4, 2, 1), d_mult=(1, 2, 4, 8, 16)):
+    """configs[4] first half: a BigGAN-style 128² GAN step.
+    G: z -> linear -> 4×4×16ch, 5 up-ResBlocks (BN-ReLU-up-conv3×3-BN-ReLU-
+    conv3×3 + up-conv1×1 shortcut), self-attention at 64², BN-ReLU-conv3×3-tanh.
+    D: 5 down-ResBlocks (ReLU-conv3×3-ReLU-conv3×3-avgpool + conv1×1-avgpool
+    shortcut; no pre-ReLU in the first), self-attention at 64², ReLU, global
+    average pool, linear -> score.  Hinge loss, a D-step then a G-step.
+    Simplified against BigGAN: unconditional (no class
+    embedding / conditional BN / projection), no spectral normalisation,
+    SGD-momentum instead of Adam."""
+    base = image >> n_blocks
+    G, D = [], []
+    c0 = g_mult[0] * ch
+    G.append({"type": "linear", "name": "g.fc", "in": "z", "out": "g.h0", "features": base * base * c0,
+              "relu": False, "reshape": [base, base, c0]})
+    prev, res, cin = "g.h0", base, c0
+    for b in range(n_blocks):
+        cout = g_mult[b + 1] * ch
+        p = f"g.b{b}"
+        G += [{"type": "bn", "name": p + ".bn1", "in": prev, "out": p + ".a1", "relu": True, "residual": None},
+              {"type": "upsample2", "name": p + ".up1", "in": p + ".a1", "out": p + ".u1"},
+              {"type": "conv", "name": p + ".c1", "in": p + ".u1", "out": p + ".y1", "k": cout, "r": 3, "s": 3,
+               "stride": 1, "pad": 1},
+              {"type": "bn", "name": p + ".bn2", "in": p + ".y1", "out": p + ".a2", "relu": True, "residual": None},
+              {"type": "conv", "name": p + ".c2", "in": p + ".a2", "out": p + ".y2", "k": cout, "r": 3, "s": 3,
+               "stride": 1, "pad": 1},
+              {"type": "upsample2", "name": p + ".up0", "in": prev, "out": p + ".u0"},
+              {"type": "conv", "name": p + ".sc", "in": p + ".u0", "out": p + ".s0", "k": cout, "r": 1, "s": 1,
+               "stride": 1, "pad": 0},
+              {"type": "add", "name": p + ".add", "in": p + ".y2", "in2": p + ".s0", "out": p + ".o"}]
+        prev, res, cin = p + ".o", res * 2, cout
+        if res == attn_res:
+            G.append({"type": "attn", "name": p + ".attn", "in": prev, "out": p + ".att", "dq": max(1, cin // 8),
+                      "dv": max(1, cin // 2)})
+            prev = p + ".att"
+    G += [{"type": "bn", "name": "g.bnf", "in": prev, "out": "g.af", "relu": True, "residual": None},
+          {"type": "conv", "name": "g.cf", "in": "g.af", "out": "g.yf", "k": 3, "r": 3, "s": 3, "stride": 1,
+           "pad": 1},
+          {"type": "tanh", "name": "g.tanh", "in": "g.yf", "out": "g.img"}]
+    prev, res, cin = "x", image, 3
+    for b in range(n_blocks):
+        cout = d_mult[b] * ch
+        p = f"d.b{b}"
+        if b == 0:
+            first = prev
+        else:
+            D.append({"type": "relu", "name": p + ".r0", "in": prev, "out": p + ".r0"})
+            first = p + ".r0"
+        D += [{"type": "conv", "name": p + ".c1", "in": first, "out": p + ".y1", "k": cout, "r": 3, "s": 3,
+               "stride": 1, "pad": 1},
+              {"type": "relu", "name": p + ".r1", "in": p + ".y1", "out": p + ".a1"},
+              {"type": "conv", "name": p + ".c2", "in": p + ".a1", "out": p + ".y2", "k": cout, "r": 3, "s": 3,
+               "stride": 1, "pad": 1},
+              {"type": "avgpool2", "name": p + ".pool", "in": p + ".y2", "out": p + ".h"},
+              {"type": "conv", "name": p + ".sc", "in": prev, "out": p + ".s0", "k": cout, "r": 1, "s": 1,
+               "stride": 1, "pad": 0},
+              {"type": "avgpool2", "name": p + ".pool0", "in": p + ".s0", "out": p + ".s1"},
+              {"type": "add", "name": p + ".add", "in": p + ".h", "in2": p + ".s1", "out": p + ".o"}]
+        prev, res, cin = p + ".o", res // 2, cout
+        if res == attn_res:
+            D.append({"type": "attn", "name": p + ".attn", "in": prev, "out": p + ".att", "dq": max(1, cin // 8),
+                      "dv": max(1, cin // 2)})
+            prev = p + ".att"
+    D += [{"type": "relu", "name": "d.rf", "in": prev, "out": "d.rf"},
+          {"type": "gap", "name": "d.gap", "in": "d.rf", "out": "d.feat"},
+          {"type": "linear", "name": "d.fc", "in": "d.feat", "out": "d.score", "features": 1, "relu": False}]
+    return {"name": "biggan", "mode": mode, "batch": batch, "z_dim": z_dim, "image": image,
+            "sgd": {"lr": 0.01, "momentum": 0.9},
+            "G": {"layers": G, "in": "z", "out": "g.img"}, "D": {"layers": D, "in": "x", "out": "d.score"}}
+
+
+def tiny_biggan(batch=4, mode="fp32"):
+    """A 16² GAN with every BigGAN layer kind: 2 up / 2 down blocks, attention at 8²."""
+    return biggan(batch=batch, image=16, ch=4, z_dim=8, mode=mode, n_blocks=2, attn_res=8, g_mult=(4, 2, 1),
+                  d_mult=(1, 2))
+
+
+def gan_shapes(spec):
+    gs, gp = net_shapes(spec["G"]["layers"], "z", [spec["z_dim"]])
+    I = spec["image"]
+    ds, dp = net_shapes(spec["D"]["layers"], "x", [I, I, 3])
+    return gs, gp, ds, dp
+
+
+def make_gan_inputs(spec, seed=0):
+    """z1, z2 ~ N(0,1) [b, z_dim]; x_real ~ U(−1, 1) NHWC (the tanh range)."""
+    b, I = spec["batch"], spec["image"]
+    r = np.random.default_rng(seed)
+    z1 = r.standard_normal((b, spec["z_dim"])).astype(np.float32)
+    z2 = r.standard_normal((b, spec["z_dim"])).astype(np.float32)
+    x = r.uniform(-1.0, 1.0, (b, I, I, 3)).astype(np.float32)
+    return z1, z2, x
+
+
+def make_gan_params(spec, seed=2):
+    _, gp, _, dp = gan_shapes(spec)
+    return make_params(spec, seed, gp), make_params(spec, seed + 1, dp)

@@ -235,3 +235,100 @@ def test_bf16_deep_net_gradients_are_chaotic():
             nm.conv2d = orig
         out[mode] = np.median([nm.rel_l2(r1["grads"][k], r0["grads"][k]) for k in p])
     assert out["bf16"] > 1e-1 and out["fp32"] < 1e-4, out
+
+
+# ---------------------------------------------------------------- GAN step (configs[4])
+
+
+def test_upsample_avgpool_loops_and_adjoints():
+    """upsample2 / avgpool2 against explicit loops, and each backward is the
+    adjoint of its forward (<f(x), y> = <x, f*(y)>)."""
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((2, 3, 4, 5))
+    up = nm.upsample2(x)
+    for i in range(6):
+        for j in range(8):
+            assert np.array_equal(up[:, i, j], x[:, i // 2, j // 2])
+    y = rng.standard_normal(up.shape)
+    assert np.isclose((up * y).sum(), (x * nm.upsample2_backward(y)).sum())
+    x2 = rng.standard_normal((2, 6, 4, 3))
+    ap = nm.avgpool2(x2)
+    for i in range(3):
+        for j in range(2):
+            assert np.allclose(ap[:, i, j], x2[:, 2 * i:2 * i + 2, 2 * j:2 * j + 2].mean(axis=(1, 2)))
+    y2 = rng.standard_normal(ap.shape)
+    assert np.isclose((ap * y2).sum(), (x2 * nm.avgpool2_backward(y2)).sum())
+
+
+def test_attention_definition_and_finite_differences():
+    """SAGAN attention: per-position loops of the definition, rows of P sum to
+    one, and the backward against central differences (fp64)."""
+    rng = np.random.default_rng(1)
+    N, L, dq, dv = 2, 5, 3, 4
+    q, k = rng.standard_normal((N, L, dq)), rng.standard_normal((N, L, dq))
+    v = rng.standard_normal((N, L, dv))
+    ident = nm.rounder("fp64")
+    P, o = nm.attention(q, k, v, ident)
+    for n in range(N):
+        for i in range(L):
+            s = np.array([q[n, i] @ k[n, j] for j in range(L)])
+            p = np.exp(s - s.max()) / np.exp(s - s.max()).sum()
+            assert np.allclose(P[n, i], p) and np.allclose(o[n, i], p @ v[n])
+    assert np.allclose(P.sum(axis=2), 1.0)
+    R = rng.standard_normal(o.shape)
+    dq_, dk_, dv_ = nm.attention_backward(q, k, v, P, o, R)
+    f = lambda: (nm.attention(q, k, v, ident)[1] * R).sum()
+    for arr, grad in ((q, dq_), (k, dk_), (v, dv_)):
+        for idx in [(0, 1, 2), (1, 4, 0), (1, 0, 1)]:
+            assert abs(_fd(f, arr, idx) - grad[idx]) < 1e-7 * (1 + abs(grad[idx]))
+
+
+def test_hinge_loss_closed_form():
+    s = np.array([2.0, 0.5, -0.5, -2.0])     # two real, two fake
+    loss, ds = nm.hinge_d(s, 2)
+    assert np.isclose(loss, (0 + 0.5) / 2 + (0.5 + 0) / 2)
+    assert np.allclose(ds, [0.0, -0.5, 0.5, 0.0])
+
+
+def test_gan_step_gradients_finite_differences():
+    """tiny BigGAN (every layer kind: linear->reshape, BN-ReLU, nearest
+    upsampling, convs, residual adds, attention, tanh, ReLU, average pooling,
+    GAP, linear score) in fp64: the D-step gradients against central
+    differences of the hinge loss; the G-step gradients against central
+    differences of −mean D'(G(z2)) with D' the updated discriminator held fixed."""
+    spec = nets.tiny_biggan(batch=3, mode="fp64")
+    pG, pD = nets.make_gan_params(spec)
+    pG = {k: v.astype(np.float64) for k, v in pG.items()}
+    pD = {k: v.astype(np.float64) for k, v in pD.items()}
+    z1, z2, x = nets.make_gan_inputs(spec)
+    res = nm.gan_step(spec, pG, pD, z1, z2, x)
+    G_, D_ = spec["G"], spec["D"]
+
+    def d_loss():
+        a = {"z": z1.astype(np.float64)}
+        nm._Net(G_["layers"], pG, "fp64").forward(a)
+        ad = {"x": np.concatenate([x.astype(np.float64), a[G_["out"]]])}
+        nm._Net(D_["layers"], pD, "fp64").forward(ad, fp32_out=(D_["out"],))
+        return nm.hinge_d(ad[D_["out"]].reshape(-1), 3)[0]
+
+    pD_new = res["pD"]
+
+    def g_loss():
+        a = {"z": z2.astype(np.float64)}
+        nm._Net(G_["layers"], pG, "fp64").forward(a)
+        ad = {"x": a[G_["out"]]}
+        nm._Net(D_["layers"], pD_new, "fp64").forward(ad, fp32_out=(D_["out"],))
+        return float(-ad[D_["out"]].mean())
+
+    assert np.isclose(d_loss(), res["loss_d"]) and np.isclose(g_loss(), res["loss_g"])
+    rng = np.random.default_rng(7)
+    for params, grads, f in ((pD, res["gradsD"], d_loss), (pG, res["gradsG"], g_loss)):
+        names = sorted(params)
+        for _ in range(16):
+            k = names[int(rng.integers(0, len(names)))]
+            idx = tuple(int(rng.integers(0, s)) for s in params[k].shape)
+            num = _fd(f, params[k], idx, eps=1e-6)
+            ana = grads[k][idx]
+            assert abs(num - ana) <= 2e-5 * (abs(ana) + 1e-3), (k, idx, num, ana)
+    for k in pG:     # every G parameter, attention included, receives a gradient
+        assert np.abs(res["gradsG"][k]).max() > 0, k
