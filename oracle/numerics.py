@@ -447,7 +447,7 @@ def gan_step(spec, pG, pD, z1, z2, x_real, momG=None, momD=None):
     g_net = _Net(G_["layers"], pG, mode)
     rnd, r32 = g_net.rnd, g_net.r32
     # ---- D-step
-    a1 = {"z": r32(np.asarray(z1, np.float64))}
+    a1 = {"z": rnd(np.asarray(z1, np.float64))}      # z stored in the act dtype
     g_net.forward(a1)
     xd = np.concatenate([rnd(np.asarray(x_real, np.float64)), a1[G_["out"]]])
     d_net = _Net(D_["layers"], pD, mode)
@@ -459,7 +459,7 @@ def gan_step(spec, pG, pD, z1, z2, x_real, momG=None, momD=None):
     d_net.backward(ad, sd, {D_["out"]: r32(ds.reshape(-1, 1))}, gradsD)
     pD_new, momD_new = _sgd(spec, pD, gradsD, momD, r32)
     # ---- G-step through the updated D
-    a2 = {"z": r32(np.asarray(z2, np.float64))}
+    a2 = {"z": rnd(np.asarray(z2, np.float64))}
     sg = g_net.forward(a2)
     d2 = _Net(D_["layers"], pD_new, mode)
     ad2 = {"x": a2[G_["out"]]}

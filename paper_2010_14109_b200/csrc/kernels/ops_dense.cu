@@ -9,92 +9,13 @@
 // (MLP 8×256×256, ResNet FC b×512×1000).  Convolutions — the dominant
 // contractions — run on tcgen05 (kernels/conv_tc.cu).
 #include "common.cuh"
+#include "gemm_simt.cuh"
 
 namespace oc {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
-
-// C[m,n] (+)= Σ_k A(m,k)·B(k,n), generic strides.
-//   maskA: A(m,k) is used only where mask(m,k) > 0 (ReLU'(·), same strides as A)
-//   RB:    round B to bf16 on load (bf16 copy of an fp32 master weight)
-//   bias:  per-n bias; relu: max(·,0); accumulate: C = rnd(C + acc)
-template <typename TA, typename TB, typename TC, bool RB>
-__global__ void __launch_bounds__(256) gemm_simt(int M, int N, int K, const TA* __restrict__ A, int64_t sam,
-                                                 int64_t sak, const TA* __restrict__ maskA, const TB* __restrict__ B,
-                                                 int64_t sbk, int64_t sbn, TC* C, int64_t scm, int64_t scn,
-                                                 const float* __restrict__ bias, int relu, int accumulate) {
-  __shared__ float As[BK][BM + 4];
-  __shared__ float Bs[BK][BN + 4];
-  const int tid = threadIdx.x;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int tx = tid % 16, ty = tid / 16;
-  float acc[TM][TN] = {};
-  for (int k0 = 0; k0 < K; k0 += BK) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      int e = tid + r * 256;  // 0..1023
-      int mm = e % BM, kk = e / BM;
-      int gm = m0 + mm, gk = k0 + kk;
-      float va = 0.f;
-      if (gm < M && gk < K) {
-        int64_t off = gm * sam + gk * sak;
-        va = ld_f(A + off);
-        if (maskA && !(ld_f(maskA + off) > 0.f)) va = 0.f;
-      }
-      As[kk][mm] = va;
-      int nn = e % BN, kb = e / BN;
-      int gn = n0 + nn, gk2 = k0 + kb;
-      float vb = 0.f;
-      if (gn < N && gk2 < K) {
-        vb = ld_f(B + gk2 * sbk + gn * sbn);
-        if (RB) vb = rnd<__nv_bfloat16>(vb);
-      }
-      Bs[kb][nn] = vb;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      float a[TM], b[TN];
-#pragma unroll
-      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
-#pragma unroll
-      for (int j = 0; j < TN; ++j) b[j] = Bs[kk][tx * TN + j];
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < TM; ++i) {
-    int gm = m0 + ty * TM + i;
-    if (gm >= M) continue;
-#pragma unroll
-    for (int j = 0; j < TN; ++j) {
-      int gn = n0 + tx * TN + j;
-      if (gn >= N) continue;
-      float v = acc[i][j];
-      if (bias) v += bias[gn];
-      if (relu) v = fmaxf(v, 0.f);
-      TC* p = C + gm * scm + gn * scn;
-      if (accumulate) v = v + ld_f(p);
-      st_f(p, v);
-    }
-  }
-}
-
-template <typename TA, typename TB, typename TC, bool RB>
-Status gemm(OpArgs& a, int M, int N, int K, const TA* A, int64_t sam, int64_t sak, const TA* mask, const TB* B,
-            int64_t sbk, int64_t sbn, TC* C, int64_t scm, int64_t scn, const float* bias, bool relu, bool acc) {
-  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
-  gemm_simt<TA, TB, TC, RB><<<grid, 256, 0, a.stream>>>(M, N, K, A, sam, sak, mask, B, sbk, sbn, C, scm, scn, bias,
-                                                        relu ? 1 : 0, acc ? 1 : 0);
-  OC_LAUNCH_CHECK(a);
-  return Status::ok();
-}
+using simt::gemm;
 
 // db[n] = Σ_m dz[m,n] (masked), sequential over m per column: deterministic
 template <typename T>
@@ -142,18 +63,20 @@ Status linear_bwd(OpArgs& a) {
     // dy fp32 [M,N]; mask (if any) has dy's layout and type
     const float* dy = (const float*)a.p(LB_DY);
     const float* mask = relu ? (const float*)a.p(LB_Y) : nullptr;
-    // dW[n,k] = Σ_m dz[m,n] x[m,k]
-    if (dt == "f32") {
+    // dW[n,k] = Σ_m dz[m,n] x[m,k]  (dw / db null: data gradient only)
+    if (dw && dt == "f32") {
       OC_TRY((gemm<float, float, float, false>(a, N, K, M, dy, 1, N, mask, (const float*)a.p(LB_X), K, 1, dw, K, 1,
                                                nullptr, false, false)));
-    } else {
-      // x is bf16: run with A = x^T? keep A = dz (fp32), B = x (bf16 exact)
+    } else if (dw) {
+      // x is bf16: A = dz (fp32), B = x (bf16 exact)
       OC_TRY((gemm<float, __nv_bfloat16, float, false>(a, N, K, M, dy, 1, N, mask,
                                                        (const __nv_bfloat16*)a.p(LB_X), K, 1, dw, K, 1, nullptr,
                                                        false, false)));
     }
-    colsum<float><<<(N + 255) / 256, 256, 0, a.stream>>>(M, N, dy, mask, db);
-    OC_LAUNCH_CHECK(a);
+    if (db) {
+      colsum<float><<<(N + 255) / 256, 256, 0, a.stream>>>(M, N, dy, mask, db);
+      OC_LAUNCH_CHECK(a);
+    }
     if (a.p(LB_DX)) {
       if (dt == "f32")
         return gemm<float, float, float, false>(a, M, K, N, dy, N, 1, mask, (const float*)a.p(LB_W), K, 1,
@@ -166,11 +89,14 @@ Status linear_bwd(OpArgs& a) {
   // bf16 dy (hidden bf16 linear layers)
   const __nv_bfloat16* dy = (const __nv_bfloat16*)a.p(LB_DY);
   const __nv_bfloat16* mask = relu ? (const __nv_bfloat16*)a.p(LB_Y) : nullptr;
-  OC_TRY((gemm<__nv_bfloat16, __nv_bfloat16, float, false>(a, N, K, M, dy, 1, N, mask,
-                                                           (const __nv_bfloat16*)a.p(LB_X), K, 1, dw, K, 1, nullptr,
-                                                           false, false)));
-  colsum<__nv_bfloat16><<<(N + 255) / 256, 256, 0, a.stream>>>(M, N, dy, mask, db);
-  OC_LAUNCH_CHECK(a);
+  if (dw)
+    OC_TRY((gemm<__nv_bfloat16, __nv_bfloat16, float, false>(a, N, K, M, dy, 1, N, mask,
+                                                             (const __nv_bfloat16*)a.p(LB_X), K, 1, dw, K, 1,
+                                                             nullptr, false, false)));
+  if (db) {
+    colsum<__nv_bfloat16><<<(N + 255) / 256, 256, 0, a.stream>>>(M, N, dy, mask, db);
+    OC_LAUNCH_CHECK(a);
+  }
   if (a.p(LB_DX))
     return gemm<__nv_bfloat16, float, __nv_bfloat16, true>(a, M, K, N, dy, N, 1, mask, (const float*)a.p(LB_W), K,
                                                            1, (__nv_bfloat16*)a.p(LB_DX), K, 1, nullptr, false,

@@ -10,7 +10,9 @@ namespace oc {
   X(kLinearFwd) X(kLinearBwd) X(kSoftmaxCE) X(kSGD) X(kAllreduce) X(kNop) X(kConvFwd) X(kConvDgrad) \
   X(kConvWgrad) X(kBnFwd) X(kBnBwdReduce) X(kBnBwdApply) X(kBnReluPoolFwd) X(kPoolBnBwdReduce)      \
   X(kPoolBnBwdApply) X(kGapFwd) X(kGapBwd) X(kAddFwd) X(kMaxpoolFwd) X(kMaxpoolBwd) X(kSoftmaxCEPix) X(kConvTFwd) \
-  X(kConvTDgrad) X(kConvTWgrad)
+  X(kConvTDgrad) X(kConvTWgrad) X(kUpsample2Fwd) X(kUpsample2Bwd) X(kAvgpool2Fwd) X(kAvgpool2Bwd) \
+  X(kReluFwd) X(kReluBwd) X(kTanhFwd) X(kTanhBwd) X(kConcatBatch) X(kScaleAddFwd) X(kScaleAddBwd) X(kAttnFwd) \
+  X(kAttnBwd) X(kHingeD) X(kHingeG)
 
 #define OC_DECL(n) extern const OpDesc n;
 OC_OPS(OC_DECL)

@@ -60,6 +60,9 @@ def build(spec, params="persistent", inputs="host", pin_below=0):
     budget, never swapped (Z26: the LMS-style size threshold; with VA
     chunks of m_c bytes a tensor far below m_c would otherwise map a whole
     chunk, Eq.1)."""
+    if "G" in spec:                       # GAN step (configs[4], graphs_gan.py)
+        from .graphs_gan import build_gan
+        return build_gan(spec, params, inputs)
     if any(l["type"] != "linear" for l in spec["layers"]):
         doc, info = _build_convnet(spec, params, inputs)
     else:

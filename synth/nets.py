@@ -379,7 +379,7 @@ def biggan(batch=32, image=128, ch=96, z_dim=120, mode="bf16", n_blocks=5, attn_
 
 def tiny_biggan(batch=4, mode="fp32"):
     """A 16² GAN with every BigGAN layer kind: 2 up / 2 down blocks, attention at 8²."""
-    return biggan(batch=batch, image=16, ch=4, z_dim=8, mode=mode, n_blocks=2, attn_res=8, g_mult=(4, 2, 1),
+    return biggan(batch=batch, image=16, ch=8, z_dim=8, mode=mode, n_blocks=2, attn_res=8, g_mult=(4, 2, 1),
                   d_mult=(1, 2))
 
 

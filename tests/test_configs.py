@@ -40,3 +40,24 @@ def test_r1001_40mib_chunks_blow_up_internal_fragmentation(r1001):
         r1001.plan(budget, 0, B.OC_ALLOC_VA, chunk_bytes=40 * MiB, phys_bytes=budget + 64 * MiB)
     s = r1001.plan(budget, 0, B.OC_ALLOC_VA, chunk_bytes=40 * MiB, phys_bytes=budget * 8, allow_oom=True)
     assert s.stats()["if_peak"] > budget // 2
+
+
+def test_biggan_config_feasible_and_tiny_gan_schedule_matches_oracle():
+    """configs[4] BigGAN-style step: the per-chunk attention maps keep every
+    function's working set small enough for a quarter of F_peak; the tiny
+    GAN's canonical schedule bytes equal the oracle's."""
+    import json
+    from oracle import graph as og, scheduler as osch
+    spec = nets.biggan(batch=32)
+    doc, _ = graphs.build(spec, params="persistent")
+    G = B.Graph(doc)
+    assert G.min_feasible_budget(0) <= G.in_core_peak() // 4
+    tdoc, _ = graphs.build(nets.tiny_biggan(batch=4), params="persistent")
+    g = og.load_graph(tdoc)
+    seq = og.build_sequence(g)
+    Gt = B.Graph(tdoc)
+    budget = max(Gt.min_feasible_budget(0), Gt.in_core_peak() // 3)
+    o = osch.build_schedule(g, seq, budget, 0)
+    s = Gt.plan(budget, 0, B.OC_ALLOC_ARENA_BEST, chunk_bytes=1, phys_bytes=budget * 4, allow_oom=True)
+    assert s.json() == osch.canonical_json(o)
+    assert json.loads(s.json())["stats"]["bytes_d2h"] > 0
