@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="r18", choices=["r18", "r50", "r1001", "mlp"])
+    ap.add_argument("--config", default="r18", choices=["r18", "r50", "r1001", "mlp", "biggan"])
     ap.add_argument("--mode", default="va", choices=["va", "best", "first"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--budget-frac", type=float, default=0.25)
@@ -63,6 +63,11 @@ def config(args):
         b = args.batch or 256
         spec = nets.resnet(50, batch=b)
         return spec, {"workload": f"ResNet-50 224x224 b={b} at {args.budget_frac:.2f} of F_peak"}
+    if args.config == "biggan":
+        b = args.batch or 32
+        spec = nets.biggan(batch=b)
+        return spec, {"workload": f"configs[4] BigGAN-style 128x128 ch=96 GAN step (D-step + G-step) b={b} at "
+                                  f"{args.budget_frac:.2f} of F_peak"}
     if args.config == "r1001":
         # b=256: every activation is >= 2 MiB (one VA chunk); tensors below one
         # chunk (parameters, optimizer state, BN statistics) stay resident (Z26)
@@ -152,6 +157,17 @@ def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None,
     phys = ps["peak_phys"] + chunk if mode == "va" else max(ps["peak_phys"], 1)
     st = OutOfCoreStep(doc, budget, W, mode=mode, chunk_bytes=chunk, phys_bytes=phys, timeline=timeline,
                        pack_threshold=pack, use_graph=use_graph, distance=distance)
+    if "G" in spec:          # GAN step: noise, real images, G and D parameters
+        pG, pD = nets.make_gan_params(spec)
+        z1, z2, xr = nets.make_gan_inputs(spec)
+        for name, arr in (("z1", z1), ("z2", z2), ("x_real", xr)):
+            st.write(info[name], torch.from_numpy(arr).to(torch.bfloat16).view(torch.int16).numpy()
+                     if spec["mode"] == "bf16" else arr)
+        for net, pp in (("G", pG), ("D", pD)):
+            for k, v in pp.items():
+                st.write(info[net]["params"][k], v)
+                st.write(info[net]["momentum"][k], np.zeros_like(v))
+        return st, W, phys
     x, y = nets.make_inputs(spec)
     p = nets.make_params(spec)
     if spec["mode"] == "bf16":
@@ -178,6 +194,10 @@ def conv_flops(doc):
             fl[f["id"]] = (k, 2.0 * a["N"] * a["P"] * a["Q"] * a["K"] * a["R"] * a["S"] * a["C"])
         elif k in ("linear_fwd", "linear_bwd"):
             fl[f["id"]] = (k, 2.0 * a["M"] * a["N"] * a["K"] * (1 if k == "linear_fwd" else 2))
+        elif k in ("attn_fwd", "attn_bwd"):
+            nb, L = a.get("nb", a["N"]), a["L"]
+            per = (a["dq"] + a["dv"]) if k == "attn_fwd" else (2 * a["dv"] + 2 * a["dq"])
+            fl[f["id"]] = (k, 2.0 * nb * L * L * per)
     return fl
 
 
@@ -256,7 +276,7 @@ def run_ours(args, rank, world):
     if world > 1:
         dist.barrier()
     dev_ms = e0.elapsed_time(e1)
-    loss = float(st.read(info["loss"])[0])
+    loss = float(st.read(info["loss_g" if "G" in spec else "loss"])[0])
     ss = st.stats
     mstat = st.mem_stats()
     n_k = int(sum(m["n_kernels"] for m in mets))
@@ -332,8 +352,14 @@ def run_ours(args, rank, world):
                     "peak_source": "derived: 148 SM x 128 FFMA lanes x 2 x 1.965 GHz"}
         else:
             pk = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+            # DRAM bytes per launch of this kernel kind from the committed ncu capture of the step
+            tpath = os.path.join(ROOT, "profiles", "r01_conv_traffic.json")
+            traffic = None
+            if os.path.exists(tpath) and args.config == "r18":
+                traffic = json.load(open(tpath)).get(kind, {}).get("bytes_per_launch")
             roof = {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
-                    "traffic": None, "kernel": kind, "launches": cnt,
+                    "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, profiles/r01_conv_traffic.json)",
+                    "kernel": kind, "launches": cnt,
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"}
     # step-level roofline: slower of compute at tensor peak and swap bytes over the link (NS)
     total_flops = sum(f for (_, f) in fl.values())
@@ -391,6 +417,16 @@ def cpu_baseline(args, steps=1):
     from oracle import numerics as nm
     from synth import nets
     cores = len(os.sched_getaffinity(0))
+    if args.config == "biggan":
+        spec = nets.biggan(batch=1)
+        pG, pD = nets.make_gan_params(spec)
+        z1, z2, xr = nets.make_gan_inputs(spec)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            nm.gan_step(spec, pG, pD, z1, z2, xr)
+        dt = time.perf_counter() - t0
+        return {"value": spec["batch"] * steps / dt, "unit": "samples/s", "cores": cores, "kind": "oracle",
+                "sample": f"biggan batch 1, {steps} step(s), numpy float64 with bf16 rounding"}
     spec = {"r50": lambda: nets.resnet(50, batch=1), "r1001": lambda: nets.preact_resnet(1001, batch=2)}.get(
         args.config, lambda: nets.resnet(18, batch=2))()
     x, y = nets.make_inputs(spec)

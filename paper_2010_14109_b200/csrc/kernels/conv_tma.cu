@@ -38,13 +38,15 @@ namespace tma {
 using namespace tcu;
 
 constexpr int BM = 128, BK = 64, NTHREADS = 192;
+constexpr int WKB = 128;   // wgrad K-block: 128 pixels (one 16 KB MN-major atom column per 64 channels)
+__host__ __device__ constexpr int kblock(int mode) { return mode == 2 ? WKB : BK; }
 // stages: as many as fit ~196 KB (at most 8)
-__host__ __device__ constexpr int tma_stage_bytes(int bn, int mt) { return mt * BM * BK * 2 + bn * BK * 2; }
-__host__ __device__ constexpr int tma_stages(int bn, int mt) {
-  return (196 * 1024) / tma_stage_bytes(bn, mt) < 8 ? (196 * 1024) / tma_stage_bytes(bn, mt) : 8;
+__host__ __device__ constexpr int tma_stage_bytes(int bn, int mt, int kb) { return mt * BM * kb * 2 + bn * kb * 2; }
+__host__ __device__ constexpr int tma_stages(int bn, int mt, int kb) {
+  return (196 * 1024) / tma_stage_bytes(bn, mt, kb) < 8 ? (196 * 1024) / tma_stage_bytes(bn, mt, kb) : 8;
 }
-__host__ __device__ constexpr int tma_smem(int bn, int mt) {
-  return tma_stages(bn, mt) * tma_stage_bytes(bn, mt) + 1024 + 256;
+__host__ __device__ constexpr int tma_smem(int bn, int mt, int kb) {
+  return tma_stages(bn, mt, kb) * tma_stage_bytes(bn, mt, kb) + 1024 + 256;
 }
 
 struct Params {
@@ -77,8 +79,10 @@ __device__ __forceinline__ void base_of(const Params& P, int pix, int& w, int& h
 
 template <int MODE, int BN, int NCH, int MT>
 __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_constant__ Params P) {
-  constexpr int NST = tma_stages(BN, MT);
-  constexpr int A_TILE = BM * BK * 2, A_BYTES = MT * A_TILE, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
+  constexpr int KB = kblock(MODE);              // K extent of a stage (elements, or wgrad pixels)
+  constexpr int ATOM = KB * 128;                 // wgrad: one 64-wide MN-major atom column
+  constexpr int NST = tma_stages(BN, MT, KB);
+  constexpr int A_TILE = BM * KB * 2, A_BYTES = MT * A_TILE, B_BYTES = BN * KB * 2, STAGE = A_BYTES + B_BYTES;
   constexpr uint32_t TCOLS = 2 * MT * BN;   // two accumulator sets of MT tiles × BN columns
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -150,20 +154,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
           const int kb = kb0 + i;
           if (MODE == WGRAD) {
             int pw, ph, pn;
-            base_of(P, kb * BK, pw, ph, pn);
+            base_of(P, kb * KB, pw, ph, pn);
             // 64-row (tap, 64-channel) blocks of (r,s,c) inside the M range
             const int rb0 = mt * MT * 2;
             int nrb = (P.M + 63) / 64 - rb0;
             nrb = nrb < 2 * MT ? nrb : 2 * MT;
-            mbar_expect_tx(&full[sg], B_BYTES + nrb * 8192);
+            mbar_expect_tx(&full[sg], B_BYTES + nrb * ATOM);
             for (int j = 0; j < nrb; ++j) {
               const int blk = rb0 + j;
               const int tap = (int)P.fCb.div((uint32_t)blk), cb = blk - tap * (P.Cr / 64);
               const int r = (int)P.fS.div((uint32_t)tap), s = tap - r * P.S;
-              tma_load_im2col(a + j * 8192, &P.ta, &full[sg], cb * 64, pw, ph, pn, (uint16_t)s, (uint16_t)r);
+              tma_load_im2col(a + j * ATOM, &P.ta, &full[sg], cb * 64, pw, ph, pn, (uint16_t)s, (uint16_t)r);
             }
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * 8192, &P.tb, &full[sg], nt * BN + j * 64, kb * BK);
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * ATOM, &P.tb, &full[sg], nt * BN + j * 64, kb * KB);
           } else if (NCH) {
             // 64 / NCH taps per K-block, one box of 128 pixels × NCH channels each
             constexpr int TPB = 64 / (NCH ? NCH : 64), BOX = BM * NCH * 2;
@@ -211,15 +215,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
         if (lane == 0) {
           const uint32_t a0 = smem_u32(smem + sg * STAGE), b = a0 + A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
+          for (int k = 0; k < KB / 16; ++k) {
             uint64_t db;
-            if (MODE == WGRAD) db = sdesc(b + k * 2048, 8192, 1024);   // MN-major: atoms 8 KB, K groups 1 KB
+            if (MODE == WGRAD) db = sdesc(b + k * 2048, ATOM, 1024);   // MN-major: atom columns ATOM apart, K groups 1 KB
             else db = sdesc(b + k * 32, 16, 1024);                      // K-major SWIZZLE_128B
 #pragma unroll
             for (int t = 0; t < MT; ++t) {
               const uint32_t a = a0 + t * A_TILE;
               uint64_t da;
-              if (MODE == WGRAD) da = sdesc(a + k * 2048, 8192, 1024);
+              if (MODE == WGRAD) da = sdesc(a + k * 2048, ATOM, 1024);
               else if (NCH == 8) da = sdesc(a + k * 2 * 2048, 2048, 128, 0);   // no swizzle: taps 2 KB apart
               else if (NCH == 16) da = sdesc(a + k * 4096, 16, 256, 6);        // SWIZZLE_32B: one tap per K-step
               else da = sdesc(a + k * 32, 16, 1024);
@@ -380,7 +384,7 @@ int conv_mt() {
 
 template <int MODE, int BN, int NCH, int MT>
 Status launch_mt(OpArgs& a, Params P) {
-  constexpr int smem = tma_smem(BN, MT);
+  constexpr int smem = tma_smem(BN, MT, kblock(MODE));
   auto kern = conv_tma_kernel<MODE, BN, NCH, MT>;
   static bool attr = false;
   if (!attr) {
@@ -516,10 +520,10 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
 Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
                       int splits, int kb_per_split, bool accumulate) {
   Params P{};
-  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, 64, BK, g.P, g.Q, g.st, g.pad, g.pad);
+  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, 64, WKB, g.P, g.Q, g.st, g.pad, g.pad);
   if (!st.good()) return st;
   const int BN = g.K % 128 == 0 ? 128 : 64;
-  st = make_tiled(&P.tb, dy, (uint64_t)g.K, (uint64_t)g.N * g.P * g.Q, 64);
+  st = make_tiled(&P.tb, dy, (uint64_t)g.K, (uint64_t)g.N * g.P * g.Q, WKB);
   if (!st.good()) return st;
   P.out = part;
   P.accumulate = accumulate ? 1 : 0;
@@ -528,8 +532,9 @@ Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   P.num_m = (P.M + BM - 1) / BM;
   P.num_n = g.K / BN;
   P.splits = splits;
-  P.nkb = (g.N * g.P * g.Q + BK - 1) / BK;
-  P.kb_per_split = kb_per_split;
+  P.nkb = (g.N * g.P * g.Q + WKB - 1) / WKB;
+  P.kb_per_split = (P.nkb + splits - 1) / splits;
+  (void)kb_per_split;
   P.Pd = g.P;
   P.Qd = g.Q;
   P.st = g.st;
