@@ -213,6 +213,30 @@ int oc_schedule_stats(const oc_schedule* s, oc_sched_stats* out);
 /* r_i of every function (n = number of functions). */
 int oc_schedule_window_ends(const oc_schedule* s, int64_t* r, size_t n);
 
+/* Makespan model of one step (the paper's execution
+ * semantics P:86): one compute stream running f_1..f_n in order and two
+ * FIFO copy channels.  Before f_i the swap-outs promoted in (b) must have
+ * completed; the arrivals of (a) enter the H2D channel once f_{i-1} has
+ * ended and those waits are done; f_i starts when f_{i-1} ended, its waits
+ * completed and every variable of V̂_i has arrived; the reservations of (c)
+ * enter the D2H channel when f_i ends (clean ones move nothing when
+ * elide_clean, Z19).  Transfer time = fixed latency + bytes / bandwidth.
+ * fn_ms: the n compute times in ms (measured per-function durations, or any
+ * cost model); stall_ms (nullable, n entries): f_i's wait after f_{i-1}.
+ * Deterministic float64 arithmetic in a fixed order (the oracle,
+ * oracle/simulator.py, reproduces it bit for bit).  OC_E_ARG on n mismatch. */
+typedef struct oc_link_model {
+  double h2d_gbs, d2h_gbs;           /* bandwidth per direction, GB/s (1e9 B/s), > 0 */
+  double h2d_fixed_us, d2h_fixed_us; /* per-transfer latency */
+  uint32_t elide_clean;
+  uint32_t reserved;                 /* must be 0 */
+} oc_link_model;
+typedef struct oc_sim_result {
+  double makespan_ms, compute_ms, h2d_busy_ms, d2h_busy_ms, stall_ms;
+} oc_sim_result;
+int oc_simulate(const oc_schedule* s, const double* fn_ms, size_t n, const oc_link_model* link, oc_sim_result* out,
+                double* stall_ms);
+
 /* ------------------------------------------------------------------ memory
  * Virtual-addressing allocator on the CUDA driver VMM API:
  * a pool of ⌊phys_bytes / m_c⌋ physical chunks (cuMemCreate, created lazily);

@@ -189,9 +189,11 @@ def build_schedule(g, seq, budget, window, distance=0):
         sch.end_wait.append(v)
         waited[rid] = dirty
     # compaction: only reservations that are eventually waited survive
+    sch.reserve_dirty = [[] for _ in range(n)]   # host copy stale at reservation (Z19), per entry
     for (i, v, rid) in reservations:
         if rid in waited:
             sch.reserve_out[i].append(v)
+            sch.reserve_dirty[i].append(bool(waited[rid]))
     bytes_d2h = sum(b[v] for (i, v, rid) in reservations if rid in waited)
     bytes_d2h_dirty = sum(b[v] for (i, v, rid) in reservations if rid in waited and waited[rid])
     sch.stats = {"bytes_h2d": bytes_h2d, "bytes_alloc": bytes_alloc, "bytes_d2h": bytes_d2h,

@@ -33,6 +33,16 @@ class oc_plan_params(C.Structure):
                 ("distance", C.c_uint32), ("reserved", C.c_uint32)]
 
 
+class oc_link_model(C.Structure):
+    _fields_ = [("h2d_gbs", C.c_double), ("d2h_gbs", C.c_double), ("h2d_fixed_us", C.c_double),
+                ("d2h_fixed_us", C.c_double), ("elide_clean", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+class oc_sim_result(C.Structure):
+    _fields_ = [("makespan_ms", C.c_double), ("compute_ms", C.c_double), ("h2d_busy_ms", C.c_double),
+                ("d2h_busy_ms", C.c_double), ("stall_ms", C.c_double)]
+
+
 class oc_sched_stats(C.Structure):
     _fields_ = [("budget", C.c_uint64), ("window", C.c_uint64), ("bytes_h2d", C.c_uint64),
                 ("bytes_alloc", C.c_uint64), ("bytes_d2h", C.c_uint64), ("bytes_d2h_dirty", C.c_uint64),
@@ -100,6 +110,8 @@ _SIGS = {
     "oc_schedule_json": (C.c_int, [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "oc_schedule_stats": (C.c_int, [P, C.POINTER(oc_sched_stats)]),
     "oc_schedule_window_ends": (C.c_int, [P, C.POINTER(C.c_int64), C.c_size_t]),
+    "oc_simulate": (C.c_int, [P, C.POINTER(C.c_double), C.c_size_t, C.POINTER(oc_link_model), C.POINTER(oc_sim_result),
+                              C.POINTER(C.c_double)]),
     "oc_mem_create": (C.c_int, [C.c_int, C.POINTER(oc_alloc_model), C.c_uint32, C.POINTER(P), E]),
     "oc_alloc": (C.c_int, [P, C.c_uint64, C.POINTER(oc_span), E]),
     "oc_map": (C.c_int, [P, C.c_uint64, P, C.POINTER(oc_span), E]),
@@ -244,3 +256,17 @@ class Schedule:
         arr = (C.c_int64 * max(n, 1))()
         lib().oc_schedule_window_ends(self.h, arr, n)
         return list(arr[:n])
+
+    def simulate(self, fn_ms, h2d_gbs, d2h_gbs, h2d_us=0.0, d2h_us=0.0, elide_clean=True):
+        """Makespan model of the step (oc_simulate)."""
+        n = self.graph.n_fns
+        fn = (C.c_double * max(n, 1))(*[float(x) for x in fn_ms])
+        stall = (C.c_double * max(n, 1))()
+        res = oc_sim_result()
+        link = oc_link_model(h2d_gbs, d2h_gbs, h2d_us, d2h_us, 1 if elide_clean else 0, 0)
+        rc = lib().oc_simulate(self.h, fn, n, C.byref(link), C.byref(res), stall)
+        if rc != OC_OK:
+            raise OcError(rc, oc_err())
+        out = {k: getattr(res, k) for k, _ in oc_sim_result._fields_}
+        out["stall_per_fn_ms"] = list(stall[:n])
+        return out

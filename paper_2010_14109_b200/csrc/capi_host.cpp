@@ -212,4 +212,61 @@ int oc_schedule_window_ends(const oc_schedule* s, int64_t* r, size_t n) {
   return OC_OK;
 }
 
+// oracle/simulator.py, operation for operation (float64, same order)
+int oc_simulate(const oc_schedule* sh, const double* fn_ms, size_t n, const oc_link_model* link, oc_sim_result* out,
+                double* stall_ms) {
+  if (!sh || !fn_ms || !link || !out || link->h2d_gbs <= 0 || link->d2h_gbs <= 0) return OC_E_ARG;
+  const Schedule& s = sh->s;
+  const Graph& g = *s.g;
+  if (n != s.fn.size()) return OC_E_ARG;
+  std::vector<double> ready(g.nv(), 0.0), out_done(g.nv(), 0.0);
+  double h2d_free = 0.0, d2h_free = 0.0, end_prev = 0.0;
+  oc_sim_result r{};
+  std::vector<uint8_t> mark(g.nv(), 0);
+  for (size_t i = 0; i < n; ++i) {
+    const FnSchedule& F = s.fn[i];
+    double t_wait = 0.0;
+    for (uint32_t v : F.wait_out) t_wait = std::max(t_wait, out_done[v]);
+    const double t_trig = std::max(end_prev, t_wait);
+    for (const Arrival& a : F.in) {
+      if (a.kind == ARRIVE_H2D) {
+        const double start = std::max(h2d_free, t_trig);
+        const double dur = link->h2d_fixed_us * 1e-3 + (double)g.var_bytes[a.var] / (link->h2d_gbs * 1e6);
+        h2d_free = start + dur;
+        r.h2d_busy_ms += dur;
+        ready[a.var] = h2d_free;
+      } else {
+        ready[a.var] = t_trig;
+      }
+    }
+    double need = 0.0;
+    for (int64_t k = g.l[i]; k <= g.e[i]; ++k) {
+      const uint32_t v = g.occ[k];
+      if (!g.pinned[v]) need = std::max(need, ready[v]);
+    }
+    const double start = std::max(std::max(end_prev, t_wait), need);
+    if (stall_ms) stall_ms[i] = start - end_prev;
+    r.stall_ms += start - end_prev;
+    const double end = start + fn_ms[i];
+    r.compute_ms += fn_ms[i];
+    for (const Departure& d : F.reserve_out) {
+      if (link->elide_clean && !d.dirty) {
+        out_done[d.var] = end;
+        continue;
+      }
+      const double s0 = std::max(d2h_free, end);
+      const double dur = link->d2h_fixed_us * 1e-3 + (double)g.var_bytes[d.var] / (link->d2h_gbs * 1e6);
+      d2h_free = s0 + dur;
+      r.d2h_busy_ms += dur;
+      out_done[d.var] = d2h_free;
+    }
+    end_prev = end;
+  }
+  double makespan = end_prev;
+  for (uint32_t v : s.end_wait) makespan = std::max(makespan, out_done[v]);
+  r.makespan_ms = makespan;
+  *out = r;
+  return OC_OK;
+}
+
 }  // extern "C"

@@ -469,6 +469,16 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
 Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* wt,
                       __nv_bfloat16* dx, bool accumulate) {
   const int BN = g.C % 128 == 0 ? 128 : 64;
+  // phases no filter tap reaches (e.g. 3 of the 4 phases of a 1×1 stride-2 conv):
+  // without accumulation their dx is zero — cleared once for the whole tensor
+  bool tapless = false;
+  for (int ph = 0; ph < g.st; ++ph)
+    for (int pw = 0; pw < g.st; ++pw)
+      tapless |= ((ph + g.pad) % g.st >= g.R) || ((pw + g.pad) % g.st >= g.S);
+  if (tapless && !accumulate) {
+    cudaError_t e = cudaMemsetAsync(dx, 0, (size_t)g.N * g.H * g.W * g.C * 2, a.stream);
+    if (e != cudaSuccess) return cuda_status(e, "dgrad zero fill");
+  }
   for (int ph = 0; ph < g.st; ++ph)
     for (int pw = 0; pw < g.st; ++pw) {
       Params P{};
@@ -477,7 +487,7 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
       const int nr = r0 < g.R ? (g.R - r0 + g.st - 1) / g.st : 0;
       const int ns = s0 < g.S ? (g.S - s0 + g.st - 1) / g.st : 0;
       if (Hp <= 0 || Wp <= 0) continue;
-      if ((nr == 0 || ns == 0) && accumulate) continue;
+      if (nr == 0 || ns == 0) continue;   // zero (cleared above) or unchanged (accumulating)
       // dy row of (h', tap i') is h' − pad'' + i' with pad'' = nr − 1 − (ph + pad − r0)/st
       const int dh = (ph + g.pad - r0) / g.st, dw = (pw + g.pad - s0) / g.st;
       const int padh = nr > 0 ? nr - 1 - dh : 0, padw = ns > 0 ? ns - 1 - dw : 0;

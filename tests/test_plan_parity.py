@@ -140,3 +140,36 @@ def test_error_classification_matches_oracle():
         with pytest.raises(B.OcError) as ec:
             B.Graph(d)
         assert ec.value.code == {"parse": B.OC_E_PARSE, "invalid": B.OC_E_INVALID}[eo.value.kind], d
+
+
+def test_makespan_model_bit_exact():
+    """oc_simulate reproduces oracle/simulator.py exactly: makespan
+    and per-function stalls on 300 random graphs with random compute times and
+    link parameters, copies of clean variables elided or not."""
+    import numpy as np
+    from oracle import simulator
+    rng = np.random.default_rng(3)
+    n_ok = 0
+    for seed in range(300):
+        doc = sg.random_graph(seed, p_pinned=0.05)
+        g = graph.load_graph(doc)
+        seq = graph.build_sequence(g)
+        total = sum(g.var_bytes)
+        budget = max(1, total // (1 + seed % 3))
+        window = (seed * 31) % (total + 1)
+        try:
+            o = scheduler.build_schedule(g, seq, budget, window)
+        except scheduler.InfeasibleBudget:
+            continue
+        s = B.Graph(doc).plan(budget, window, B.OC_ALLOC_ARENA_BEST, chunk_bytes=1, phys_bytes=budget * 8,
+                              allow_oom=True)
+        fn_ms = [float(x) for x in rng.uniform(0.0, 3.0, g.n_fns)]
+        h2d, d2h = float(rng.uniform(1e-7, 1e-5)), float(rng.uniform(1e-7, 1e-5))
+        hu, du = float(rng.uniform(0, 5)), float(rng.uniform(0, 5))
+        elide = bool(seed % 2)
+        ref = simulator.simulate(g, seq, o, fn_ms, h2d, d2h, hu, du, elide)
+        got = s.simulate(fn_ms, h2d, d2h, hu, du, elide)
+        assert got["makespan_ms"] == ref["makespan_ms"], seed
+        assert got["stall_per_fn_ms"] == ref["stall_ms"], seed
+        n_ok += 1
+    assert n_ok > 100
