@@ -183,7 +183,10 @@ class Graph:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().oc_graph_destroy(self.h)
+            try:
+                lib().oc_graph_destroy(self.h)
+            except TypeError:      # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     @property
@@ -234,7 +237,10 @@ class Schedule:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().oc_schedule_destroy(self.h)
+            try:
+                lib().oc_schedule_destroy(self.h)
+            except TypeError:      # interpreter shutdown
+                pass
             self.h = None
 
     def json(self):

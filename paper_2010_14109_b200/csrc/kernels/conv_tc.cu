@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
 // fp32 KRSC master -> bf16 [K][kpad] (fprop; (r,s,c) over the activation's C
 // channels, zero past Cw and past RSC) or [C][R][S][K] (dgrad, Cw = C)
 __global__ void weight_bf16(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int K, int RS, int C,
-                            int transpose, int kpad, int Cw) {
+                            int transpose, int kpad, int Cw, int Kw = 1 << 30) {
   const int64_t n = transpose ? (int64_t)K * RS * C : (int64_t)K * kpad;
   const int rsc = RS * C;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -371,7 +371,8 @@ __global__ void weight_bf16(const float* __restrict__ w, __nv_bfloat16* __restri
     } else {
       const int64_t k = i / kpad, j = i % kpad;
       const int rs = (int)(j / C), c = (int)(j % C);
-      out[i] = (j < rsc && c < Cw) ? __float2bfloat16_rn(w[(k * RS + rs) * Cw + c]) : __float2bfloat16_rn(0.f);
+      out[i] = (j < rsc && c < Cw && k < Kw) ? __float2bfloat16_rn(w[(k * RS + rs) * Cw + c])
+                                             : __float2bfloat16_rn(0.f);
     }
   }
 }
@@ -380,7 +381,8 @@ __global__ void weight_bf16(const float* __restrict__ w, __nv_bfloat16* __restri
 // padding channels c >= Cw are dropped.  32×32 tiles through shared memory so
 // both the partial reads (along k) and the dW writes (along rsc) coalesce.
 __global__ void __launch_bounds__(1024) wgrad_reduce(int splits, int RSC, int K, int C, int Cw,
-                                                     const float* __restrict__ part, float* __restrict__ dw) {
+                                                     const float* __restrict__ part, float* __restrict__ dw,
+                                                     int Kw = 1 << 30) {
   __shared__ float tile[32][33];
   const int64_t n = (int64_t)RSC * K;
   const int k0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(1024) wgrad_reduce(int splits, int RSC, int K,
   }
   __syncthreads();
   const int k = k0 + ty, rsc = r0 + tx;
-  if (rsc >= RSC || k >= K) return;
+  if (rsc >= RSC || k >= K || k >= Kw) return;
   const int rs = rsc / C, c = rsc - rs * C;
   if (c >= Cw) return;
   dw[(int64_t)k * (RSC / C) * Cw + rs * Cw + c] = tile[tx][ty];
@@ -444,15 +446,31 @@ using namespace tc;
 
 bool conv_tma_ok(const ConvGeom& g, int mode);
 Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* wb, int kpad,
-                      __nv_bfloat16* y, bool accumulate);
+                      __nv_bfloat16* y, bool accumulate, int nst = 0);
 Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* wt,
-                      __nv_bfloat16* dx, bool accumulate);
+                      __nv_bfloat16* dx, bool accumulate, int nst = 0);
 Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
                       int splits, int kb_per_split, bool accumulate);
 
+bool conv_tma_enabled();
+
+// channel counts the 64-wide tiles do not divide (e.g. ResNet-1001's 16/32,
+// BigGAN's 96, attention's 12-48): zero-padded to multiples of 64 in
+// workspace copies (operands) and zero-padded weights, only the real
+// channels stored (TMA kernels)
+bool pad_path(const ConvGeom& g, int mode) {
+  if (!conv_tma_enabled() || g.Cw != g.C || g.C % 8 || g.K % 8) return false;
+  const bool nch = g.C == 8 || g.C == 16;
+  if (mode == DGRAD) return g.C % 64 != 0 || g.K % 64 != 0;
+  return g.K % 64 != 0 || (g.C % 64 != 0 && !nch);
+}
+
 bool conv_tc_ok(const ConvGeom& g, int mode) {
   // 32-bit element indices of the activations (the 64-bit tensor offsets are formed per row)
-  if ((int64_t)g.N * g.H * g.W * g.C >= (1ll << 31) || (int64_t)g.N * g.P * g.Q * g.K >= (1ll << 31)) return false;
+  if ((int64_t)g.N * g.H * g.W * ((g.C + 63) / 64 * 64) >= (1ll << 31) ||
+      (int64_t)g.N * g.P * g.Q * ((g.K + 63) / 64 * 64) >= (1ll << 31))
+    return false;
+  if (pad_path(g, mode)) return true;
   // zero-padded activation channels (Cw < C) only on the 16-byte-chunk paths
   if (g.Cw != g.C && (g.C % 8 != 0 || g.Cw > g.C || mode == DGRAD)) return false;
   if (mode == DGRAD) return g.K % 64 == 0 && g.C % 64 == 0 && (g.st == 1 || g.st == 2);
@@ -608,7 +626,145 @@ int wgrad_bn(const ConvGeom& g) { return g.K % 128 == 0 ? 128 : 64; }
 
 }  // namespace
 
+namespace {
+
+int up64(int c) { return (c + 63) / 64 * 64; }
+
+// the padded problem: C -> Cp, K -> Kp; operand copies in image slices
+struct PadPlan {
+  ConvGeom gk;             // padded geometry (full batch)
+  bool pad_x, pad_y;       // X (C channels) / dY (K channels) need a padded copy
+  int64_t slice;
+  size_t xbytes, ybytes;   // per-slice copy bytes
+};
+PadPlan pad_plan(const ConvGeom& g, int mode) {
+  PadPlan p{g, false, false, g.N, 0, 0};
+  const bool nch = (g.C == 8 || g.C == 16) && mode == FPROP;   // fprop gathers 8/16-ch pixels natively
+  const int Cp = (g.C % 64 == 0 || nch) ? g.C : up64(g.C), Kp = up64(g.K);
+  p.gk.C = p.gk.Cw = Cp;
+  p.gk.K = Kp;
+  p.pad_x = Cp != g.C && mode != DGRAD;
+  p.pad_y = Kp != g.K && mode != FPROP;
+  const int64_t px = p.pad_x ? (int64_t)g.H * g.W * Cp * 2 : 0, py = p.pad_y ? (int64_t)g.P * g.Q * Kp * 2 : 0;
+  if (px + py > 0) p.slice = std::max<int64_t>(1, std::min<int64_t>(g.N, (64ll << 20) / (px + py)));
+  p.xbytes = align256((size_t)(p.slice * px));
+  p.ybytes = align256((size_t)(p.slice * py));
+  return p;
+}
+int tma_wgrad_splits(const ConvGeom& gk, int64_t slice) {
+  const int BN = gk.K % 128 == 0 ? 128 : 64;
+  const int64_t tiles = ((int64_t)gk.R * gk.S * gk.C + BM - 1) / BM * (gk.K / BN);
+  const int64_t kbs = (slice * gk.P * gk.Q + 127) / 128;
+  int64_t s2 = (2 * 148) / tiles;
+  return (int)(s2 < 1 ? 1 : (s2 > kbs ? kbs : s2));
+}
+size_t pad_ws(const ConvGeom& g, int mode) {
+  const PadPlan p = pad_plan(g, mode);
+  const ConvGeom& k = p.gk;
+  if (mode == FPROP) return align256((size_t)k.K * kpad_of(k) * 2) + p.xbytes;
+  if (mode == DGRAD) return align256((size_t)k.C * k.R * k.S * k.K * 2) + p.ybytes;
+  return align256((size_t)tma_wgrad_splits(k, p.slice) * k.R * k.S * k.C * k.K * 4) + p.xbytes + p.ybytes;
+}
+
+// Wt[c][rs][k] for c < Cp, k < Kp: W[k][rs][c] inside the real channels, else 0
+__global__ void weight_bf16_tpad(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int K, int RS, int C,
+                                 int Kp, int Cp) {
+  const int64_t n = (int64_t)Cp * RS * Kp;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % Kp);
+    const int64_t t = i / Kp;
+    const int rs = (int)(t % RS), c = (int)(t / RS);
+    out[i] = (c < C && k < K) ? __float2bfloat16_rn(w[((int64_t)k * RS + rs) * C + c]) : __float2bfloat16_rn(0.f);
+  }
+}
+
+Status pad_copy(OpArgs& a, int64_t rows, int C, int Cp, const __nv_bfloat16* src, __nv_bfloat16* dst) {
+  pad_pixels<<<grid_for(rows, 256, 2), 256, 0, a.stream>>>(rows, C, Cp, src, dst);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+
+Status conv_fprop_pad(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y,
+                      bool accumulate) {
+  const PadPlan pp = pad_plan(g, FPROP);
+  const ConvGeom& k = pp.gk;
+  const int kpad = kpad_of(k);
+  __nv_bfloat16* wb = (__nv_bfloat16*)a.ws;
+  __nv_bfloat16* xbuf = (__nv_bfloat16*)((char*)a.ws + align256((size_t)k.K * kpad * 2));
+  weight_bf16<<<grid_for((int64_t)k.K * kpad, 256, 4), 256, 0, a.stream>>>(w, wb, k.K, k.R * k.S, k.C, 0, kpad, g.C,
+                                                                            g.K);
+  OC_LAUNCH_CHECK(a);
+  for (int64_t n0 = 0; n0 < g.N; n0 += pp.slice) {
+    const int64_t nn = std::min<int64_t>(pp.slice, g.N - n0);
+    ConvGeom gs = k;
+    gs.N = (int)nn;
+    const __nv_bfloat16* act = x + n0 * g.H * g.W * g.C;
+    if (pp.pad_x) {
+      OC_TRY(pad_copy(a, nn * g.H * g.W, g.C, k.C, act, xbuf));
+      act = xbuf;
+    }
+    OC_TRY(conv_fprop_tma(a, gs, act, wb, kpad, y + n0 * g.P * g.Q * g.K, accumulate, g.K));
+  }
+  return Status::ok();
+}
+
+Status conv_dgrad_pad(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const float* w, __nv_bfloat16* dx,
+                      bool accumulate) {
+  const PadPlan pp = pad_plan(g, DGRAD);
+  const ConvGeom& k = pp.gk;
+  __nv_bfloat16* wt = (__nv_bfloat16*)a.ws;
+  __nv_bfloat16* ybuf = (__nv_bfloat16*)((char*)a.ws + align256((size_t)k.C * k.R * k.S * k.K * 2));
+  weight_bf16_tpad<<<grid_for((int64_t)k.C * k.R * k.S * k.K, 256, 4), 256, 0, a.stream>>>(w, wt, g.K, g.R * g.S,
+                                                                                            g.C, k.K, k.C);
+  OC_LAUNCH_CHECK(a);
+  for (int64_t n0 = 0; n0 < g.N; n0 += pp.slice) {
+    const int64_t nn = std::min<int64_t>(pp.slice, g.N - n0);
+    ConvGeom gs = k;
+    gs.N = (int)nn;
+    const __nv_bfloat16* act = dy + n0 * g.P * g.Q * g.K;
+    if (pp.pad_y) {
+      OC_TRY(pad_copy(a, nn * g.P * g.Q, g.K, k.K, act, ybuf));
+      act = ybuf;
+    }
+    OC_TRY(conv_dgrad_tma(a, gs, act, wt, dx + n0 * g.H * g.W * g.C, accumulate, g.C));
+  }
+  return Status::ok();
+}
+
+Status conv_wgrad_pad(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* x, float* dw) {
+  const PadPlan pp = pad_plan(g, WGRAD);
+  const ConvGeom& k = pp.gk;
+  const int splits = tma_wgrad_splits(k, pp.slice);
+  const int RSCp = k.R * k.S * k.C;
+  float* part = (float*)a.ws;
+  __nv_bfloat16* xbuf = (__nv_bfloat16*)((char*)a.ws + align256((size_t)splits * RSCp * k.K * 4));
+  __nv_bfloat16* ybuf = (__nv_bfloat16*)((char*)xbuf + pp.xbytes);
+  for (int64_t n0 = 0, sl = 0; n0 < g.N; n0 += pp.slice, ++sl) {
+    const int64_t nn = std::min<int64_t>(pp.slice, g.N - n0);
+    ConvGeom gs = k;
+    gs.N = (int)nn;
+    const __nv_bfloat16* xa = x + n0 * g.H * g.W * g.C;
+    const __nv_bfloat16* ya = dy + n0 * g.P * g.Q * g.K;
+    if (pp.pad_x) {
+      OC_TRY(pad_copy(a, nn * g.H * g.W, g.C, k.C, xa, xbuf));
+      xa = xbuf;
+    }
+    if (pp.pad_y) {
+      OC_TRY(pad_copy(a, nn * g.P * g.Q, g.K, k.K, ya, ybuf));
+      ya = ybuf;
+    }
+    OC_TRY(conv_wgrad_tma(a, gs, xa, ya, part, splits, 0, sl > 0));
+  }
+  wgrad_reduce<<<dim3((k.K + 31) / 32, (RSCp + 31) / 32), 1024, 0, a.stream>>>(splits, RSCp, k.K, k.C, g.C, part, dw,
+                                                                              g.K);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+
+}  // namespace
+
 size_t conv_tc_ws(const ConvGeom& g0, int mode) {
+  if (pad_path(g0, mode)) return pad_ws(g0, mode);
   const Narrow nw = narrow_of(g0);
   const ConvGeom& g = nw.gk;
   if (mode == WGRAD) {
@@ -622,6 +778,7 @@ size_t conv_tc_ws(const ConvGeom& g0, int mode) {
 
 Status conv_fprop_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y,
                      bool accumulate) {
+  if (pad_path(g0, FPROP)) return conv_fprop_pad(a, g0, x, w, y, accumulate);
   const Narrow nw = narrow_of(g0);
   const ConvGeom& g = nw.gk;
   __nv_bfloat16* wb = (__nv_bfloat16*)a.ws;
@@ -669,6 +826,7 @@ Status conv_fprop_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* x, cons
 
 Status conv_dgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const float* w, __nv_bfloat16* dx,
                      bool accumulate) {
+  if (pad_path(g, DGRAD)) return conv_dgrad_pad(a, g, dy, w, dx, accumulate);
   __nv_bfloat16* wt = (__nv_bfloat16*)a.ws;
   const int64_t nw = (int64_t)g.K * g.R * g.S * g.C;
   weight_bf16<<<grid_for(nw, 256, 4), 256, 0, a.stream>>>(w, wt, g.K, g.R * g.S, g.C, 1, 0, g.C);
@@ -706,6 +864,7 @@ Status conv_dgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, cons
 }
 
 Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* dy, const __nv_bfloat16* x, float* dw) {
+  if (pad_path(g0, WGRAD)) return conv_wgrad_pad(a, g0, dy, x, dw);
   const Narrow nw = narrow_of(g0);
   const ConvGeom& g = nw.gk;
   const int BN = wgrad_bn(g);

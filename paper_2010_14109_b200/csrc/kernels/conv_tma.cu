@@ -53,6 +53,7 @@ struct Params {
   CUtensorMap ta;          // im2col map of the gathered activation (X or dY)
   CUtensorMap tb;          // tiled map of the other operand (W_bf16, Wt_bf16 or dY)
   void* out;               // bf16 [M][N] rows, or fp32 wgrad partials [z][M][N]
+  int nst;                 // fprop/dgrad: stored columns (row stride) when N is zero-padded; 0 = N
   int accumulate;          // out = rnd(acc + out)
   int M, N;                // GEMM rows / columns
   int num_m, num_n, splits;
@@ -281,9 +282,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
               *reinterpret_cast<float4*>(o + i) = f;
             }
           } else {
-            __nv_bfloat16* o = (__nv_bfloat16*)P.out + orow * P.N + col;
+            const int nst = P.nst ? P.nst : P.N;   // padded output channels past nst are not stored
+            __nv_bfloat16* o = (__nv_bfloat16*)P.out + orow * nst + col;
 #pragma unroll
             for (int i = 0; i < 32; i += 8) {
+              if (col + i >= nst) break;
               float f[8];
 #pragma unroll
               for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[i + e]);
@@ -431,8 +434,9 @@ bool conv_tma_ok(const ConvGeom& g, int mode) {
 }
 
 // y[M = N·P·Q][K] = im2col(x) · W_bf16[K][kpad]ᵀ
+// nst (optional): the stored output channels when g.K is a zero-padded width
 Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* wb, int kpad,
-                      __nv_bfloat16* y, bool accumulate) {
+                      __nv_bfloat16* y, bool accumulate, int nst) {
   const int nch = g.C % 64 == 0 ? 0 : g.C;     // 8 or 16: narrow pixels, one tap per box
   Params P{};
   Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, nch ? nch : 64, BM, g.P, g.Q, g.st, g.pad, g.pad,
@@ -443,6 +447,7 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   st = make_tiled(&P.tb, wb, (uint64_t)kpad, (uint64_t)g.K, (uint32_t)BN);
   if (!st.good()) return st;
   P.out = y;
+  P.nst = nst;
   P.accumulate = accumulate ? 1 : 0;
   P.M = g.N * g.P * g.Q;
   P.N = g.K;
@@ -467,7 +472,7 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
 // valid taps: dx[(n,h',w')][C] = im2col_{pad''}(dy) · Wt_bf16[C][(r,s,K)]ᵀ at the
 // phase's filter taps; a phase no tap reaches gets zeros (or keeps dx when accumulating)
 Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* wt,
-                      __nv_bfloat16* dx, bool accumulate) {
+                      __nv_bfloat16* dx, bool accumulate, int nst) {
   const int BN = g.C % 128 == 0 ? 128 : 64;
   // phases no filter tap reaches (e.g. 3 of the 4 phases of a 1×1 stride-2 conv):
   // without accumulation their dx is zero — cleared once for the whole tensor
@@ -476,7 +481,7 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
     for (int pw = 0; pw < g.st; ++pw)
       tapless |= ((ph + g.pad) % g.st >= g.R) || ((pw + g.pad) % g.st >= g.S);
   if (tapless && !accumulate) {
-    cudaError_t e = cudaMemsetAsync(dx, 0, (size_t)g.N * g.H * g.W * g.C * 2, a.stream);
+    cudaError_t e = cudaMemsetAsync(dx, 0, (size_t)g.N * g.H * g.W * (nst ? nst : g.C) * 2, a.stream);
     if (e != cudaSuccess) return cuda_status(e, "dgrad zero fill");
   }
   for (int ph = 0; ph < g.st; ++ph)
@@ -496,6 +501,7 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
       st = make_tiled(&P.tb, wt, (uint64_t)g.R * g.S * g.K, (uint64_t)g.C, (uint32_t)BN);
       if (!st.good()) return st;
       P.out = dx;
+      P.nst = nst;
       P.accumulate = accumulate ? 1 : 0;
       P.M = g.N * Hp * Wp;
       P.N = g.C;

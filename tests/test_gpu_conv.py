@@ -25,6 +25,15 @@ SHAPES = [  # N, H, W, C, K, R, stride, pad
     (3, 18, 12, 3, 128, 7, 2, 3, 2),  # ... BN = 128, slices of 2 images
     (2, 10, 12, 3, 64, 3, 2, 1),      # 3x3 stride 2 -> 2x2 space-to-depth taps
 ]
+# channel counts the 64-wide tiles do not divide: operands zero-padded to 64 in
+# workspace copies, weights padded, only the real channels stored
+PAD = [
+    (2, 9, 7, 32, 16, 3, 1, 1),       # ResNet-1001-like 32 -> 16
+    (3, 8, 8, 16, 32, 1, 1, 0),       # 16 -> 32, 1x1 (fprop gathers 16-ch pixels)
+    (2, 10, 9, 96, 96, 3, 2, 1),      # BigGAN-like 96 channels, stride 2 (dgrad phases)
+    (2, 6, 6, 64, 24, 1, 1, 0),       # attention-like 64 -> 24
+    (2, 8, 8, 24, 64, 3, 1, 1),       # 24 -> 64
+]
 
 
 def bf(a):
@@ -77,7 +86,7 @@ def _from_bits(a, shape):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("g", SHAPES)
+@pytest.mark.parametrize("g", SHAPES + PAD)
 def test_conv_fwd(g):
     N, H, W, C, K, R, st, pad = g[:8]
     rng = np.random.default_rng(1)
@@ -92,7 +101,7 @@ def test_conv_fwd(g):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("g", SHAPES[:5])
+@pytest.mark.parametrize("g", SHAPES[:5] + PAD)
 @pytest.mark.parametrize("accumulate", [False, True])
 def test_conv_dgrad(g, accumulate):
     N, H, W, C, K, R, st, pad = g[:8]
@@ -112,7 +121,7 @@ def test_conv_dgrad(g, accumulate):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("g", SHAPES)
+@pytest.mark.parametrize("g", SHAPES + PAD)
 def test_conv_wgrad(g):
     N, H, W, C, K, R, st, pad = g[:8]
     rng = np.random.default_rng(3)

@@ -190,11 +190,31 @@ def test_cuda_graph_replay_equals_eager():
         assert np.array_equal(res[0][k], res[1][k]), k
 
 
+def _force_simt(doc):
+    d = json.loads(doc)
+    for f in d["functions"]:
+        if f["op"]["kind"].startswith("conv"):
+            f["op"]["attrs"]["impl"] = "simt"
+    return json.dumps(d)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["va", "best"])
-def test_tiny_resnet_parity_and_transparency(mode):
+@pytest.mark.parametrize("impl,tol", [("simt", 1e-3), ("tc", 1e-2)])
+def test_tiny_resnet_parity_and_transparency(mode, impl, tol):
+    """Every gradient of a shallow bf16 ResNet against the oracle.  With the
+    CUDA-core convs (fp32 FFMA in order) the stored bf16 values match the
+    oracle's almost everywhere and every gradient is within 1e-3 (measured
+    ~1e-7).  The tensor-core convs (16/32-channel layers zero-padded to 64)
+    accumulate in a different order; each kernel matches the CUDA-core one to
+    within one bf16 ulp on 0.02 % of outputs (tools/cmp_pad_vs_simt.py), but
+    one flipped stored value can re-route a max-pool argmax and the
+    difference grows toward the stem (Z24): measured 6e-3 at conv1.W, 1e-2
+    bound."""
     spec = nets.tiny_resnet(batch=4, image=16, classes=10)
     doc, info = graphs.build(spec, params="persistent")
+    if impl == "simt":
+        doc = _force_simt(doc)
     G = B.Graph(doc)
     peak = G.in_core_peak()
     budget = max(G.min_feasible_budget(0), int(peak * 0.5))
@@ -207,7 +227,7 @@ def test_tiny_resnet_parity_and_transparency(mode):
     assert abs(ooc["loss"] - ref["loss"]) <= 1e-3 * abs(ref["loss"])
     for k in p:
         e = nm.rel_l2(ooc["m." + k], ref["grads"][k])
-        assert e <= 1e-3, (k, e)
+        assert e <= tol, (k, e)
     inc = run_step(spec, doc, info, peak, 0, "best", peak * 2)
     for k in p:
         assert np.array_equal(inc["m." + k], ooc["m." + k]), k

@@ -61,6 +61,14 @@ def main():
                                                                          "d2h_busy_ms", "overlap_frac", "bytes_h2d",
                                                                          "bytes_d2h", "n_h2d", "n_d2h")}
                     mem = st.mem_stats()
+                    # F4: the makespan model on this schedule with this run's per-function times
+                    fid = [f["id"] for f in json.loads(doc)["functions"]]
+                    dur = {}
+                    for ev in st.timeline():
+                        if ev["stream"] == "compute":
+                            dur[ev["id"]] = dur.get(ev["id"], 0.0) + (ev["t1"] - ev["t0"])
+                    pred = st.sched.simulate([dur.get(f, 0.0) for f in fid], 55.6, 57.3, 10.0, 10.0, True)
+                    m["predicted_ms"] = pred["makespan_ms"]
                     print(json.dumps({"frac": frac, "budget": budget, "mode": mode, "chunk_mib": ch, "wfrac": wf,
                                       "pack": pk, "policy": "paper" if not dd else f"distance {dd}",
                                       "window": W, "phys": phys, "samples_per_s": a.batch / m["step_ms"] * 1e3,
