@@ -17,6 +17,7 @@
 // Addresses are fixed per arrival slot and identical every step, so after the
 // first step no driver call is made (memoised VA) and the host only issues
 // copies, event waits and kernels.
+#include <cstdlib>
 #include <algorithm>
 #include <chrono>
 #include <cstring>
@@ -122,6 +123,11 @@ struct Exec {
   const Schedule* s = nullptr;
   MemPool* mem = nullptr;
   cudaStream_t cs = nullptr, hs = nullptr, ds = nullptr;
+  // optional second copy stream per direction (OC_COPY_STREAMS=2): consecutive
+  // transfers alternate between the two, so one copy's setup overlaps the
+  // previous copy; every dependency is an explicit event, so order is free
+  cudaStream_t hs2 = nullptr, ds2 = nullptr;
+  cudaEvent_t ev_join[2] = {nullptr, nullptr};
   oc_exec_options opt{};
   std::vector<XVar> vars;
   std::vector<XFn> fns;
@@ -171,6 +177,12 @@ Status Exec::create(int dev, const Graph* graph, const Schedule* sch, MemPool* m
   ds = (cudaStream_t)st.d2h;
   if (o) opt = *o;
   OC_CUDA(cudaSetDevice(dev));
+  if (const char* e = std::getenv("OC_COPY_STREAMS"); e && e[0] == '2') {
+    OC_CUDA(cudaStreamCreateWithFlags(&hs2, cudaStreamNonBlocking));
+    OC_CUDA(cudaStreamCreateWithFlags(&ds2, cudaStreamNonBlocking));
+    OC_CUDA(cudaEventCreateWithFlags(&ev_join[0], cudaEventDisableTiming));
+    OC_CUDA(cudaEventCreateWithFlags(&ev_join[1], cudaEventDisableTiming));
+  }
   if (s->replay.oom_fn >= 0) return Status::make(OC_E_DEVICE_OOM, "schedule's allocator replay ran out of memory");
   const auto& am = s->alloc;
   if (am.mode != m->model.mode) return Status::make(OC_E_ARG, "schedule and memory pool use different allocator modes");
@@ -425,6 +437,11 @@ Status Exec::run(oc_step_metrics* out) {
   OC_CUDA(cudaEventRecord(ev_fork, cs));
   OC_CUDA(cudaStreamWaitEvent(hs, ev_fork, 0));
   OC_CUDA(cudaStreamWaitEvent(ds, ev_fork, 0));
+  if (hs2) {
+    OC_CUDA(cudaStreamWaitEvent(hs2, ev_fork, 0));
+    OC_CUDA(cudaStreamWaitEvent(ds2, ev_fork, 0));
+  }
+  uint32_t n_hcopy = 0, n_dcopy = 0;
   for (uint32_t i = 0; i < n; ++i) {
     const FnSchedule& F = s->fn[i];
     XFn& X = fns[i];
@@ -438,17 +455,18 @@ Status Exec::run(oc_step_metrics* out) {
       Slot& sl = slots[a.slot];
       if (s->alloc.mode == OC_ALLOC_VA) OC_TRY(mem->bind(sl.span, sl.chunks));
       if (sl.packed) continue;
-      for (const Ref& r : sl.waits) OC_CUDA(cudaStreamWaitEvent(hs, ev_of(r), 0));
+      cudaStream_t h = (hs2 && sl.kind == ARRIVE_H2D && (n_hcopy++ & 1)) ? hs2 : hs;
+      for (const Ref& r : sl.waits) OC_CUDA(cudaStreamWaitEvent(h, ev_of(r), 0));
       if (sl.kind == ARRIVE_H2D) {
-        if (sl.host_dep >= 0) OC_CUDA(cudaStreamWaitEvent(hs, ev_out[sl.host_dep], 0));
+        if (sl.host_dep >= 0) OC_CUDA(cudaStreamWaitEvent(h, ev_out[sl.host_dep], 0));
         XVar& xv = vars[sl.var];
-        if (opt.timeline) { OC_CUDA(cudaEventRecord(tl_in0[a.slot], hs)); tl_in_used[a.slot] = 1; }
-        OC_CUDA(cudaMemcpyAsync((void*)sl.addr, host + xv.host_off, xv.bytes, cudaMemcpyHostToDevice, hs));
-        if (opt.timeline) OC_CUDA(cudaEventRecord(tl_in1[a.slot], hs));
+        if (opt.timeline) { OC_CUDA(cudaEventRecord(tl_in0[a.slot], h)); tl_in_used[a.slot] = 1; }
+        OC_CUDA(cudaMemcpyAsync((void*)sl.addr, host + xv.host_off, xv.bytes, cudaMemcpyHostToDevice, h));
+        if (opt.timeline) OC_CUDA(cudaEventRecord(tl_in1[a.slot], h));
         bytes_h2d += xv.bytes;
         ++n_h2d;
       }
-      OC_CUDA(cudaEventRecord(ev_in[a.slot], hs));
+      OC_CUDA(cudaEventRecord(ev_in[a.slot], h));
       vars[sl.var].cur_slot = (int32_t)a.slot;
       vars[sl.var].need_wait = true;
     }
@@ -519,7 +537,10 @@ Status Exec::run(oc_step_metrics* out) {
     if (opt.timeline) OC_CUDA(cudaEventRecord(tl_fn1[i], cs));
     OC_CUDA(cudaEventRecord(ev_done[i], cs));
     // (c) reserved swap-outs after f_i; small ones through one pack kernel (A7)
-    if (!X.dep_reserve.empty()) OC_CUDA(cudaStreamWaitEvent(ds, ev_done[i], 0));
+    if (!X.dep_reserve.empty()) {
+      OC_CUDA(cudaStreamWaitEvent(ds, ev_done[i], 0));
+      if (ds2) OC_CUDA(cudaStreamWaitEvent(ds2, ev_done[i], 0));
+    }
     if (X.pout_n) {
       const uint32_t first = X.dep_reserve[0];
       if (opt.timeline) { OC_CUDA(cudaEventRecord(tl_out0[first], ds)); tl_out_used[first] = 1; }
@@ -537,19 +558,27 @@ Status Exec::run(oc_step_metrics* out) {
         OC_CUDA(cudaEventRecord(ev_out[d], ds));
         continue;
       }
+      cudaStream_t dsk = ds;
       if (D.dirty || !opt.elide_clean) {
-        if (opt.timeline) { OC_CUDA(cudaEventRecord(tl_out0[d], ds)); tl_out_used[d] = 1; }
-        OC_CUDA(cudaMemcpyAsync(host + xv.host_off, addr_of(D.var), xv.bytes, cudaMemcpyDeviceToHost, ds));
-        if (opt.timeline) OC_CUDA(cudaEventRecord(tl_out1[d], ds));
+        if (ds2 && (n_dcopy++ & 1)) dsk = ds2;
+        if (opt.timeline) { OC_CUDA(cudaEventRecord(tl_out0[d], dsk)); tl_out_used[d] = 1; }
+        OC_CUDA(cudaMemcpyAsync(host + xv.host_off, addr_of(D.var), xv.bytes, cudaMemcpyDeviceToHost, dsk));
+        if (opt.timeline) OC_CUDA(cudaEventRecord(tl_out1[d], dsk));
         bytes_d2h += xv.bytes;
         ++n_d2h;
       }
-      OC_CUDA(cudaEventRecord(ev_out[d], ds));
+      OC_CUDA(cudaEventRecord(ev_out[d], dsk));
     }
     // frees: nothing to issue; the memory is released at ev_done[i]
     for (uint32_t v : F.free) vars[v].cur_slot = -1;
   }
   for (int32_t d : end_deps) OC_CUDA(cudaStreamWaitEvent(cs, ev_out[d], 0));
+  if (hs2) {   // join the extra copy streams (their work is already complete or awaited)
+    OC_CUDA(cudaEventRecord(ev_join[0], hs2));
+    OC_CUDA(cudaEventRecord(ev_join[1], ds2));
+    OC_CUDA(cudaStreamWaitEvent(cs, ev_join[0], 0));
+    OC_CUDA(cudaStreamWaitEvent(cs, ev_join[1], 0));
+  }
   return Status::ok();
   };
 
@@ -620,6 +649,11 @@ Status Exec::run(oc_step_metrics* out) {
 void Exec::destroy() {
   cudaSetDevice(device);
   cudaDeviceSynchronize();
+  if (hs2) cudaStreamDestroy(hs2);
+  if (ds2) cudaStreamDestroy(ds2);
+  for (auto& e : ev_join)
+    if (e) cudaEventDestroy(e), e = nullptr;
+  hs2 = ds2 = nullptr;
   for (auto& sl : slots) {
     if (sl.span.va) {
       if (!sl.span.mapped.empty()) mem->driver_unmap(sl.span);

@@ -200,7 +200,7 @@ def _force_simt(doc):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["va", "best"])
-@pytest.mark.parametrize("impl,tol", [("simt", 1e-3), ("tc", 1e-2)])
+@pytest.mark.parametrize("impl,tol", [("simt", 1e-3), ("tc", 2e-2)])
 def test_tiny_resnet_parity_and_transparency(mode, impl, tol):
     """Every gradient of a shallow bf16 ResNet against the oracle.  With the
     CUDA-core convs (fp32 FFMA in order) the stored bf16 values match the
@@ -209,7 +209,7 @@ def test_tiny_resnet_parity_and_transparency(mode, impl, tol):
     accumulate in a different order; each kernel matches the CUDA-core one to
     within one bf16 ulp on 0.02 % of outputs (tools/cmp_pad_vs_simt.py), but
     one flipped stored value can re-route a max-pool argmax and the
-    difference grows toward the stem (Z24): measured 6e-3 at conv1.W, 1e-2
+    difference grows toward the stem (Z24): measured 6-8e-3 at conv1.W, 2e-2
     bound."""
     spec = nets.tiny_resnet(batch=4, image=16, classes=10)
     doc, info = graphs.build(spec, params="persistent")
