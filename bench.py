@@ -262,7 +262,7 @@ def run_ours(args, rank, world):
             Wc = int(wmax * k / 15)
             sc = G.plan(budget, Wc, B.OC_ALLOC_VA if args.mode == "va" else B.OC_ALLOC_ARENA_BEST,
                         chunk_bytes=chunk, phys_bytes=budget * 4, allow_oom=True)
-            pred = sc.simulate(fn_ms, 55.6, 57.3, 10.0, 10.0, True)["makespan_ms"]
+            pred = sc.simulate(fn_ms, 55.6, 57.3, 10.0, 10.0, True, model=1)["makespan_ms"]
             window_probe.append({"window": Wc, "predicted_ms": pred})
             if best is None or pred < best[1]:
                 best = (Wc, pred)
@@ -330,7 +330,8 @@ def run_ours(args, rank, world):
         if ev["stream"] == "compute":
             dur[ev["id"]] = dur.get(ev["id"], 0.0) + (ev["t1"] - ev["t0"])   # last instrumented step
     fn_ms = [dur.get(f, 0.0) for f in fid]
-    sim = sti.sched.simulate(fn_ms, 55.6, 57.3, 10.0, 10.0, True)
+    sim = sti.sched.simulate(fn_ms, 55.6, 57.3, 10.0, 10.0, True, model=1)
+    sim0 = sti.sched.simulate(fn_ms, 55.6, 57.3, 10.0, 10.0, True, model=0)
     sti.close()
     ms = torch.tensor([dev_ms, (t_wall1 - t_wall0) * 1e3], dtype=torch.float64)
     if world > 1:
@@ -432,10 +433,12 @@ def run_ours(args, rank, world):
                       "d2h_gbs_busy": (d2h / (d2h_busy / 1e3) / 1e9) if d2h_busy else None,
                       "pcie5_x16_gbs_per_dir": PCIE5_X16_GBS, "measured_pinned_gbs": {"h2d": 55.6, "d2h": 57.3}},
         "overlap_pct": 100 * overlap,
-        "makespan_model": {"predicted_ms": sim["makespan_ms"], "compute_ms": sim["compute_ms"],
+        "makespan_model": {"predicted_ms": sim["makespan_ms"], "predicted_boundary_ms": sim0["makespan_ms"],
+                           "compute_ms": sim["compute_ms"],
                            "stall_ms": sim["stall_ms"], "link": "55.6 / 57.3 GB/s, 10 us per copy",
                            "note": "oc_simulate on this schedule with the instrumented pass's per-function times; "
-                                   "compare instrumented_pass.ms_per_step"},
+                                   "compare instrumented_pass.ms_per_step; model 1 = executor ordering, "
+                                   "boundary = the paper's function-boundary semantics"},
         "instrumented_pass": {"steps": 3, "ms_per_step": instr_step_ms,
                               "note": "overlap, busy times and kernel durations come from this pass (CUDA events "
                                       "around every function and transfer); the timed steps run without them"},

@@ -229,7 +229,14 @@ typedef struct oc_link_model {
   double h2d_gbs, d2h_gbs;           /* bandwidth per direction, GB/s (1e9 B/s), > 0 */
   double h2d_fixed_us, d2h_fixed_us; /* per-transfer latency */
   uint32_t elide_clean;
-  uint32_t reserved;                 /* must be 0 */
+  /* 0: the paper's boundary semantics above.  1: the executor's ordering —
+   * an arrival waits only for the memory the allocator replay gave it (VA
+   * chunks / arena byte range) to be released (end of the freeing function,
+   * or completion of the previous occupant's swap-out) and, for a variable
+   * written back, for that copy; each channel is one in-order stream on
+   * which alloc-only arrivals and elided swap-outs pass without transfer
+   * time (oracle/simulator.simulate_exec). */
+  uint32_t model;
 } oc_link_model;
 typedef struct oc_sim_result {
   double makespan_ms, compute_ms, h2d_busy_ms, d2h_busy_ms, stall_ms;

@@ -74,3 +74,86 @@ def lower_bounds(g, sch, fn_ms, h2d_gbs, d2h_gbs):
     """Σ compute, H2D bytes / bandwidth, D2H bytes / bandwidth."""
     return {"compute": sum(fn_ms), "h2d": sch.stats["bytes_h2d"] / (h2d_gbs * 1e6),
             "d2h": sch.stats["bytes_d2h_clean_elided"] / (d2h_gbs * 1e6)}
+
+
+def simulate_exec(g, seq, sch, placements, mode, fn_ms, h2d_gbs, d2h_gbs, h2d_us=0.0, d2h_us=0.0,
+                  elide_clean=True, align=512):
+    """Placement-aware variant: the executor's ordering instead of the paper's
+    boundary semantics.  An arrival is not held until f_{i−1} ends; it waits
+    only for the memory it reuses — the chunks (VA) or byte range (arena) the
+    allocator replay gave it (`placements`, from allocators.replay), released
+    at the end of the function that freed the previous occupant or at the
+    completion of its swap-out — and, for a variable written back, for that
+    copy.  Each copy channel is one in-order stream: an alloc-only arrival or a
+    clean (elided) swap-out occupies no transfer time but still passes the
+    stream in order.  Compute as in simulate()."""
+    b = g.var_bytes
+    n = len(sch.ins)
+    place = iter(placements)
+    rel_chunk, rel_iv, held = {}, [], {}
+    ready, out_done, host_ready = {}, {}, {}
+    h2d_free = d2h_free = end_prev = 0.0
+
+    def units_of(v, p):
+        if mode == "va":
+            return ("c", list(p))
+        size = -(-b[v] // align) * align
+        return ("r", (p, p + size))
+
+    def mem_ready(u):
+        t = 0.0
+        if u[0] == "c":
+            for c in u[1]:
+                t = max(t, rel_chunk.get(c, 0.0))
+        else:
+            lo, hi = u[1]
+            for (a, z, tr) in rel_iv:
+                if a < hi and lo < z:
+                    t = max(t, tr)
+        return t
+
+    def release(u, t):
+        if u[0] == "c":
+            for c in u[1]:
+                rel_chunk[c] = t
+        else:
+            rel_iv.append((u[1][0], u[1][1], t))
+
+    stall = []
+    for i in range(n):
+        t_wait = 0.0
+        for v in sch.wait_out[i]:
+            t_wait = max(t_wait, out_done[v])
+            release(held.pop(v), out_done[v])
+        for v, kind in sch.ins[i]:
+            i2, v2, p = next(place)
+            assert (i2, v2) == (i, v)
+            u = units_of(v, p)
+            t = max(h2d_free, mem_ready(u))
+            if kind == "h2d":
+                t = max(t, host_ready.get(v, 0.0))
+                t = t + (h2d_us * 1e-3 + b[v] / (h2d_gbs * 1e6))
+            h2d_free = t
+            ready[v] = t
+            held[v] = u
+        need = 0.0
+        for v in set(seq.occ[seq.l[i]:seq.e[i] + 1]):
+            if not g.pinned[v]:
+                need = max(need, ready[v])
+        start = max(end_prev, t_wait, need)
+        stall.append(start - end_prev)
+        end = start + fn_ms[i]
+        for v, dirty in zip(sch.reserve_out[i], sch.reserve_dirty[i]):
+            t = max(d2h_free, end)
+            if dirty or not elide_clean:
+                t = t + (d2h_us * 1e-3 + b[v] / (d2h_gbs * 1e6))
+                host_ready[v] = t
+            d2h_free = t
+            out_done[v] = t
+        for v in sch.free[i]:
+            release(held.pop(v), end)
+        end_prev = end
+    makespan = end_prev
+    for v in sch.end_wait:
+        makespan = max(makespan, out_done[v])
+    return {"makespan_ms": makespan, "stall_ms": stall}

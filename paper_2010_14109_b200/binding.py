@@ -35,7 +35,7 @@ class oc_plan_params(C.Structure):
 
 class oc_link_model(C.Structure):
     _fields_ = [("h2d_gbs", C.c_double), ("d2h_gbs", C.c_double), ("h2d_fixed_us", C.c_double),
-                ("d2h_fixed_us", C.c_double), ("elide_clean", C.c_uint32), ("reserved", C.c_uint32)]
+                ("d2h_fixed_us", C.c_double), ("elide_clean", C.c_uint32), ("model", C.c_uint32)]
 
 
 class oc_sim_result(C.Structure):
@@ -263,13 +263,14 @@ class Schedule:
         lib().oc_schedule_window_ends(self.h, arr, n)
         return list(arr[:n])
 
-    def simulate(self, fn_ms, h2d_gbs, d2h_gbs, h2d_us=0.0, d2h_us=0.0, elide_clean=True):
-        """Makespan model of the step (oc_simulate)."""
+    def simulate(self, fn_ms, h2d_gbs, d2h_gbs, h2d_us=0.0, d2h_us=0.0, elide_clean=True, model=0):
+        """Makespan model of the step (oc_simulate); model 0 = the
+        paper's boundary semantics, 1 = the executor's placement-aware ordering."""
         n = self.graph.n_fns
         fn = (C.c_double * max(n, 1))(*[float(x) for x in fn_ms])
         stall = (C.c_double * max(n, 1))()
         res = oc_sim_result()
-        link = oc_link_model(h2d_gbs, d2h_gbs, h2d_us, d2h_us, 1 if elide_clean else 0, 0)
+        link = oc_link_model(h2d_gbs, d2h_gbs, h2d_us, d2h_us, 1 if elide_clean else 0, model)
         rc = lib().oc_simulate(self.h, fn, n, C.byref(link), C.byref(res), stall)
         if rc != OC_OK:
             raise OcError(rc, oc_err())

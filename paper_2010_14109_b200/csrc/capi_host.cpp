@@ -222,7 +222,96 @@ int oc_simulate(const oc_schedule* sh, const double* fn_ms, size_t n, const oc_l
   std::vector<double> ready(g.nv(), 0.0), out_done(g.nv(), 0.0);
   double h2d_free = 0.0, d2h_free = 0.0, end_prev = 0.0;
   oc_sim_result r{};
-  std::vector<uint8_t> mark(g.nv(), 0);
+  if (link->model == 1) {
+    // executor ordering (oracle/simulator.simulate_exec)
+    const bool va = s.alloc.mode == OC_ALLOC_VA;
+    const uint64_t al = s.alloc.align ? s.alloc.align : 1;
+    std::vector<double> rel_chunk;
+    struct Iv { uint64_t lo, hi; double t; };
+    std::vector<Iv> rel_iv;
+    std::vector<const Arrival*> held(g.nv(), nullptr);
+    std::vector<double> host_ready(g.nv(), 0.0);
+    auto range_of = [&](const Arrival& a) {
+      const uint64_t size = (g.var_bytes[a.var] + al - 1) / al * al;
+      return std::make_pair(a.offset, a.offset + size);
+    };
+    auto mem_ready = [&](const Arrival& a) {
+      double t = 0.0;
+      if (va) {
+        for (uint32_t c : a.chunks)
+          if (c < rel_chunk.size()) t = std::max(t, rel_chunk[c]);
+      } else {
+        const auto rg = range_of(a);
+        for (const Iv& iv : rel_iv)
+          if (iv.lo < rg.second && rg.first < iv.hi) t = std::max(t, iv.t);
+      }
+      return t;
+    };
+    auto release = [&](const Arrival* a, double t) {
+      if (!a) return;
+      if (va) {
+        for (uint32_t c : a->chunks) {
+          if (c >= rel_chunk.size()) rel_chunk.resize(c + 1, 0.0);
+          rel_chunk[c] = t;
+        }
+      } else {
+        const auto rg = range_of(*a);
+        rel_iv.push_back(Iv{rg.first, rg.second, t});
+      }
+    };
+    for (size_t i = 0; i < n; ++i) {
+      const FnSchedule& F = s.fn[i];
+      double t_wait = 0.0;
+      for (uint32_t v : F.wait_out) {
+        t_wait = std::max(t_wait, out_done[v]);
+        release(held[v], out_done[v]);
+        held[v] = nullptr;
+      }
+      for (const Arrival& a : F.in) {
+        double t = std::max(h2d_free, mem_ready(a));
+        if (a.kind == ARRIVE_H2D) {
+          t = std::max(t, host_ready[a.var]);
+          const double dur = link->h2d_fixed_us * 1e-3 + (double)g.var_bytes[a.var] / (link->h2d_gbs * 1e6);
+          t = t + dur;
+          r.h2d_busy_ms += dur;
+        }
+        h2d_free = t;
+        ready[a.var] = t;
+        held[a.var] = &a;
+      }
+      double need = 0.0;
+      for (int64_t k = g.l[i]; k <= g.e[i]; ++k) {
+        const uint32_t v = g.occ[k];
+        if (!g.pinned[v]) need = std::max(need, ready[v]);
+      }
+      const double start = std::max(std::max(end_prev, t_wait), need);
+      if (stall_ms) stall_ms[i] = start - end_prev;
+      r.stall_ms += start - end_prev;
+      const double end = start + fn_ms[i];
+      r.compute_ms += fn_ms[i];
+      for (const Departure& d : F.reserve_out) {
+        double t = std::max(d2h_free, end);
+        if (d.dirty || !link->elide_clean) {
+          const double dur = link->d2h_fixed_us * 1e-3 + (double)g.var_bytes[d.var] / (link->d2h_gbs * 1e6);
+          t = t + dur;
+          r.d2h_busy_ms += dur;
+          host_ready[d.var] = t;
+        }
+        d2h_free = t;
+        out_done[d.var] = t;
+      }
+      for (uint32_t v : F.free) {
+        release(held[v], end);
+        held[v] = nullptr;
+      }
+      end_prev = end;
+    }
+    double makespan = end_prev;
+    for (uint32_t v : s.end_wait) makespan = std::max(makespan, out_done[v]);
+    r.makespan_ms = makespan;
+    *out = r;
+    return OC_OK;
+  }
   for (size_t i = 0; i < n; ++i) {
     const FnSchedule& F = s.fn[i];
     double t_wait = 0.0;

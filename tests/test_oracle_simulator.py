@@ -82,3 +82,35 @@ def test_everything_resident_no_transfer_stalls():
         fn_ms = [1.0] * g.n_fns
         r = simulator.simulate(g, seq, sch, fn_ms, h2d_gbs=1e12, d2h_gbs=1e12)
         assert abs(r["makespan_ms"] - g.n_fns) < 1e-6
+
+
+def test_executor_model_bounded_by_boundary_model_and_lower_bounds():
+    """The placement-aware (executor) model only removes the function-boundary
+    gate of the arrivals — the memory it waits for was released no later
+    than that boundary — so its makespan is never above the paper-semantics
+    model's, and never below the lower bounds (300 random graphs, VA and
+    best-fit placements)."""
+    from oracle import allocators
+    rng = np.random.default_rng(1)
+    n_ok = 0
+    for seed in range(300):
+        g, seq = _load(sg.random_graph(seed, p_pinned=0.05))
+        total = sum(g.var_bytes)
+        budget = max(1, total // (1 + seed % 3))
+        try:
+            sch = scheduler.build_schedule(g, seq, budget, (seed * 7) % (total + 1))
+        except scheduler.InfeasibleBudget:
+            continue
+        mode = ("va", "best")[seed % 2]
+        st, pl = allocators.replay(g, sch, mode, chunk_bytes=2, phys_bytes=total * 4, align=1)
+        if st["oom"] is not None:
+            continue
+        fn_ms = list(rng.uniform(0.0, 2.0, g.n_fns))
+        args = (fn_ms, 1e-6, 2e-6, 0.1, 0.2, bool(seed % 3))
+        a = simulator.simulate(g, seq, sch, *args)
+        e = simulator.simulate_exec(g, seq, sch, pl, mode, *args, align=1)
+        lb = simulator.lower_bounds(g, sch, fn_ms, 1e-6, 2e-6)
+        assert e["makespan_ms"] <= a["makespan_ms"] + 1e-9, seed
+        assert e["makespan_ms"] >= max(lb["compute"], lb["h2d"]) - 1e-9, seed
+        n_ok += 1
+    assert n_ok > 100

@@ -173,3 +173,40 @@ def test_makespan_model_bit_exact():
         assert got["stall_per_fn_ms"] == ref["stall_ms"], seed
         n_ok += 1
     assert n_ok > 100
+
+
+def test_executor_makespan_model_bit_exact():
+    """oc_simulate model 1 (placement-aware executor ordering) reproduces
+    oracle/simulator.simulate_exec exactly, with the allocator placements of
+    the VA and best-fit replays."""
+    import numpy as np
+    from oracle import simulator
+    rng = np.random.default_rng(4)
+    n_ok = 0
+    for seed in range(300):
+        doc = sg.random_graph(seed, p_pinned=0.05)
+        g = graph.load_graph(doc)
+        seq = graph.build_sequence(g)
+        total = sum(g.var_bytes)
+        budget = max(1, total // (1 + seed % 3))
+        window = (seed * 17) % (total + 1)
+        try:
+            o = scheduler.build_schedule(g, seq, budget, window)
+        except scheduler.InfeasibleBudget:
+            continue
+        mode = ("va", "best")[seed % 2]
+        chunk, phys = 1 + seed % 5, total * 4
+        st, pl = allocators.replay(g, o, mode, chunk_bytes=chunk, phys_bytes=phys, align=1)
+        if st["oom"] is not None:
+            continue
+        s = B.Graph(doc).plan(budget, window, B.OC_ALLOC_VA if mode == "va" else B.OC_ALLOC_ARENA_BEST,
+                              chunk_bytes=chunk, phys_bytes=phys, align=1)
+        fn_ms = [float(x) for x in rng.uniform(0.0, 3.0, g.n_fns)]
+        h2d, d2h = float(rng.uniform(1e-7, 1e-5)), float(rng.uniform(1e-7, 1e-5))
+        elide = bool(seed % 3)
+        ref = simulator.simulate_exec(g, seq, o, pl, mode, fn_ms, h2d, d2h, 1.0, 2.0, elide, align=1)
+        got = s.simulate(fn_ms, h2d, d2h, 1.0, 2.0, elide, model=1)
+        assert got["makespan_ms"] == ref["makespan_ms"], seed
+        assert got["stall_per_fn_ms"] == ref["stall_ms"], seed
+        n_ok += 1
+    assert n_ok > 100

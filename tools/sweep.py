@@ -67,8 +67,9 @@ def main():
                     for ev in st.timeline():
                         if ev["stream"] == "compute":
                             dur[ev["id"]] = dur.get(ev["id"], 0.0) + (ev["t1"] - ev["t0"])
-                    pred = st.sched.simulate([dur.get(f, 0.0) for f in fid], 55.6, 57.3, 10.0, 10.0, True)
-                    m["predicted_ms"] = pred["makespan_ms"]
+                    fm = [dur.get(f, 0.0) for f in fid]
+                    m["predicted_ms"] = st.sched.simulate(fm, 55.6, 57.3, 10.0, 10.0, True, model=1)["makespan_ms"]
+                    m["predicted_boundary_ms"] = st.sched.simulate(fm, 55.6, 57.3, 10.0, 10.0, True)["makespan_ms"]
                     print(json.dumps({"frac": frac, "budget": budget, "mode": mode, "chunk_mib": ch, "wfrac": wf,
                                       "pack": pk, "policy": "paper" if not dd else f"distance {dd}",
                                       "window": W, "phys": phys, "samples_per_s": a.batch / m["step_ms"] * 1e3,
