@@ -330,8 +330,13 @@ def run_ours(args, rank, world):
         if ev["stream"] == "compute":
             dur[ev["id"]] = dur.get(ev["id"], 0.0) + (ev["t1"] - ev["t0"])   # last instrumented step
     fn_ms = [dur.get(f, 0.0) for f in fid]
-    sim = sti.sched.simulate(fn_ms, 55.6, 57.3, 10.0, 10.0, True, model=1)
-    sim0 = sti.sched.simulate(fn_ms, 55.6, 57.3, 10.0, 10.0, True, model=0)
+    # link rates calibrated on this pass: bytes over busy copy time per direction
+    bw_h = float(np.mean([m["bytes_h2d"] / max(m["h2d_busy_ms"], 1e-9) for m in mets_i])) / 1e6
+    bw_d = float(np.mean([m["bytes_d2h"] / max(m["d2h_busy_ms"], 1e-9) for m in mets_i])) / 1e6
+    bw_h = bw_h if bw_h > 1 else 55.6
+    bw_d = bw_d if bw_d > 1 else 57.3
+    sim = sti.sched.simulate(fn_ms, bw_h, bw_d, 0.0, 0.0, True, model=1)
+    sim0 = sti.sched.simulate(fn_ms, bw_h, bw_d, 0.0, 0.0, True, model=0)
     sti.close()
     ms = torch.tensor([dev_ms, (t_wall1 - t_wall0) * 1e3], dtype=torch.float64)
     if world > 1:
@@ -435,7 +440,9 @@ def run_ours(args, rank, world):
         "overlap_pct": 100 * overlap,
         "makespan_model": {"predicted_ms": sim["makespan_ms"], "predicted_boundary_ms": sim0["makespan_ms"],
                            "compute_ms": sim["compute_ms"],
-                           "stall_ms": sim["stall_ms"], "link": "55.6 / 57.3 GB/s, 10 us per copy",
+                           "stall_ms": sim["stall_ms"],
+                           "link_gbs": {"h2d": bw_h, "d2h": bw_d, "source": "bytes / busy copy time of the "
+                                                                           "instrumented pass"},
                            "note": "oc_simulate on this schedule with the instrumented pass's per-function times; "
                                    "compare instrumented_pass.ms_per_step; model 1 = executor ordering, "
                                    "boundary = the paper's function-boundary semantics"},

@@ -68,8 +68,10 @@ def main():
                         if ev["stream"] == "compute":
                             dur[ev["id"]] = dur.get(ev["id"], 0.0) + (ev["t1"] - ev["t0"])
                     fm = [dur.get(f, 0.0) for f in fid]
-                    m["predicted_ms"] = st.sched.simulate(fm, 55.6, 57.3, 10.0, 10.0, True, model=1)["makespan_ms"]
-                    m["predicted_boundary_ms"] = st.sched.simulate(fm, 55.6, 57.3, 10.0, 10.0, True)["makespan_ms"]
+                    bh = m["bytes_h2d"] / max(m["h2d_busy_ms"], 1e-9) / 1e6 or 55.6
+                    bd = m["bytes_d2h"] / max(m["d2h_busy_ms"], 1e-9) / 1e6 or 57.3
+                    m["predicted_ms"] = st.sched.simulate(fm, bh, bd, 0.0, 0.0, True, model=1)["makespan_ms"]
+                    m["predicted_boundary_ms"] = st.sched.simulate(fm, bh, bd, 0.0, 0.0, True)["makespan_ms"]
                     print(json.dumps({"frac": frac, "budget": budget, "mode": mode, "chunk_mib": ch, "wfrac": wf,
                                       "pack": pk, "policy": "paper" if not dd else f"distance {dd}",
                                       "window": W, "phys": phys, "samples_per_s": a.batch / m["step_ms"] * 1e3,
