@@ -249,7 +249,9 @@ def run_ours(args, rank, world):
         # of the schedule), oc_simulate ranks 16 candidate windows
         stc, _, _ = setup_step(spec, info, doc, budget, args.mode, chunk, timeline=True, window=0)
         stc.step()
-        stc.step()
+        mc = stc.step()
+        bh = mc["bytes_h2d"] / max(mc["h2d_busy_ms"], 1e-9) / 1e6 or 55.6
+        bd = mc["bytes_d2h"] / max(mc["d2h_busy_ms"], 1e-9) / 1e6 or 57.3
         fid = [f["id"] for f in json.loads(doc)["functions"]]
         dur = {}
         for ev in stc.timeline():
@@ -262,7 +264,7 @@ def run_ours(args, rank, world):
             Wc = int(wmax * k / 15)
             sc = G.plan(budget, Wc, B.OC_ALLOC_VA if args.mode == "va" else B.OC_ALLOC_ARENA_BEST,
                         chunk_bytes=chunk, phys_bytes=budget * 4, allow_oom=True)
-            pred = sc.simulate(fn_ms, 55.6, 57.3, 10.0, 10.0, True, model=1)["makespan_ms"]
+            pred = sc.simulate(fn_ms, bh, bd, 0.0, 0.0, True, model=1)["makespan_ms"]
             window_probe.append({"window": Wc, "predicted_ms": pred})
             if best is None or pred < best[1]:
                 best = (Wc, pred)
