@@ -466,67 +466,61 @@ def run_ours(args, rank, world):
     return line
 
 
-def cpu_baseline(args, steps=1):
-    """The oracle (oracle/numerics.train_step, numpy float64) on a bounded
-    sample of the same workload: ResNet-18 224x224 at batch 2."""
+def oracle_sample(args):
+    """The oracle's bounded sample of the configured workload: (one-step
+    callable, samples per step, time scale to the real sample, description)."""
     from oracle import numerics as nm
     from synth import nets
-    cores = len(os.sched_getaffinity(0))
-    if args.config == "unet":
-        # SURVEY §8(d): b = 1 on a 256² crop, scaled by pixel count (labelled extrapolated)
-        spec = nets.unet(batch=1, image=256)
-        x, y = nets.make_inputs(spec)
-        p = nets.make_params(spec)
-        t0 = time.perf_counter()
-        for _ in range(steps):
-            nm.train_step(spec, p, x, y)
-        dt = time.perf_counter() - t0
-        return {"value": steps / dt / 16.0, "unit": "samples/s", "cores": cores, "kind": "oracle",
-                "sample": "unet batch 1 on a 256x256 crop, time scaled by the 16x pixel count (extrapolated)"}
     if args.config == "biggan":
         spec = nets.biggan(batch=1)
         pG, pD = nets.make_gan_params(spec)
         z1, z2, xr = nets.make_gan_inputs(spec)
-        t0 = time.perf_counter()
-        for _ in range(steps):
-            nm.gan_step(spec, pG, pD, z1, z2, xr)
-        dt = time.perf_counter() - t0
-        return {"value": spec["batch"] * steps / dt, "unit": "samples/s", "cores": cores, "kind": "oracle",
-                "sample": f"biggan batch 1, {steps} step(s), numpy float64 with bf16 rounding"}
-    spec = {"r50": lambda: nets.resnet(50, batch=1), "r1001": lambda: nets.preact_resnet(1001, batch=2)}.get(
-        args.config, lambda: nets.resnet(18, batch=2))()
+        return (lambda: nm.gan_step(spec, pG, pD, z1, z2, xr)), 1, 1.0, \
+            "biggan batch 1 per step (numpy float64 oracle with bf16 rounding)"
+    if args.config == "unet":
+        # SURVEY §8(d): b = 1 on a 256² crop, scaled by pixel count (labelled extrapolated)
+        spec = nets.unet(batch=1, image=256)
+        scale, note = 16.0, "unet batch 1 on a 256x256 crop, time scaled by the 16x pixel count (extrapolated)"
+    elif args.config == "mlp":
+        spec, scale, note = nets.mlp6(), 1.0, "mlp6 batch 8 per step"
+    else:
+        spec = {"r50": lambda: nets.resnet(50, batch=1), "r1001": lambda: nets.preact_resnet(1001, batch=2)}.get(
+            args.config, lambda: nets.resnet(18, batch=2))()
+        scale, note = 1.0, f"{spec['name']} batch {spec['batch']} per step"
     x, y = nets.make_inputs(spec)
     p = nets.make_params(spec)
+    return (lambda: nm.train_step(spec, p, x, y)), spec["batch"], scale, note + " (numpy float64 oracle)"
+
+
+def cpu_baseline(args, steps=1):
+    """The oracle on a bounded sample of the same workload, on all host cores."""
+    cores = len(os.sched_getaffinity(0))
+    fn, batch, scale, note = oracle_sample(args)
     t0 = time.perf_counter()
     for _ in range(steps):
-        nm.train_step(spec, p, x, y)
-    dt = time.perf_counter() - t0
-    return {"value": spec["batch"] * steps / dt, "unit": "samples/s", "cores": cores, "kind": "oracle",
-            "sample": f"{spec['name']} batch {spec['batch']}, {steps} step(s), numpy float64 with bf16 rounding"}
+        fn()
+    dt = (time.perf_counter() - t0) * scale
+    return {"value": batch * steps / dt, "unit": "samples/s", "cores": cores, "kind": "oracle",
+            "sample": f"{note}, {steps} step(s)"}
 
 
 def run_reference(args):
     """--impl reference: the CPU oracle as it stands, bounded sample per step."""
-    from oracle import numerics as nm
-    from synth import nets
     cores = len(os.sched_getaffinity(0))
-    spec = nets.resnet(18, batch=1) if args.config != "mlp" else nets.mlp6()
-    x, y = nets.make_inputs(spec)
-    p = nets.make_params(spec)
+    fn, batch, scale, note = oracle_sample(args)
     for _ in range(args.warmup):
-        nm.train_step(spec, p, x, y)
+        fn()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        nm.train_step(spec, p, x, y)
-    dt = time.perf_counter() - t0
-    v = spec["batch"] * args.steps / dt
+        fn()
+    dt = (time.perf_counter() - t0) * scale
+    v = batch * args.steps / dt
     _, cfg = config(args)
-    sample = f"{spec['name']} batch {spec['batch']} per step (numpy float64 oracle)"
     return {"impl": "reference", "metric": "samples/sec at k x in-budget batch vs in-core; host-link GB/s; overlap %",
             "value": v, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": cfg,
-            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "oracle", "sample": note},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
