@@ -91,3 +91,100 @@ def min_budget_all_schedules(g):
         if optimal_cost(g, B) is not None:
             return B
     return None
+
+
+class _Sch:
+    """Minimal schedule record in the scheduler's format (for the simulator)."""
+
+    def __init__(self, n):
+        self.ins = [[] for _ in range(n)]
+        self.wait_out = [[] for _ in range(n)]
+        self.reserve_out = [[] for _ in range(n)]
+        self.reserve_dirty = [[] for _ in range(n)]
+        self.free = [[] for _ in range(n)]
+        self.end_wait = []
+
+
+def _schedule_of(g, seq, sets):
+    """The swap schedule realising resident sets S_0..S_{n-1} (S_i held while
+    f_i runs): arrivals S_i − S_{i−1} before f_i, ordered by next use;
+    departures S_{i−1} − S_i that are still needed (used later, or
+    persistent) reserved after their last use (copied if dirty, else
+    elidable) and waited before f_i, others dropped; dirty persistent
+    variables written back at the end — the same event vocabulary as the
+    greedy (P:86)."""
+    n = g.n_fns
+    sch = _Sch(n)
+    uses = [set(seq.occ[seq.l[i]:seq.e[i] + 1]) for i in range(n)]
+    first_occ = {}
+    for k, v in enumerate(seq.occ):
+        first_occ.setdefault((v, k), k)
+    written = set()
+    dirty, last_use = {}, {}
+    later = [set() for _ in range(n + 1)]           # used by f_j, j >= i
+    for i in range(n - 1, -1, -1):
+        later[i] = later[i + 1] | uses[i]
+    prev = frozenset()
+    for i in range(n):
+        S = sets[i]
+        for v in sorted(prev - S):
+            if v in last_use and (v in later[i] or g.persistent[v]):   # still needed: swap out
+                sch.reserve_out[last_use[v]].append(v)
+                sch.reserve_dirty[last_use[v]].append(bool(dirty.get(v)))
+                sch.wait_out[i].append(v)
+            dirty.pop(v, None)
+            last_use.pop(v, None)
+
+        def next_use(v):
+            for j in range(i, n):
+                if v in uses[j]:
+                    return j
+            return n
+        for v in sorted(S - prev, key=lambda v: (next_use(v), v)):
+            sch.ins[i].append((v, "h2d" if (g.persistent[v] or v in written) else "alloc"))
+        for v in uses[i]:
+            if not g.pinned[v]:
+                last_use[v] = i
+        for v in g.fn_out[i]:
+            if not g.pinned[v]:
+                dirty[v] = True
+                written.add(v)
+        prev = S
+    for v in sorted(prev):
+        if g.persistent[v] and dirty.get(v):
+            sch.reserve_out[last_use[v]].append(v)
+            sch.reserve_dirty[last_use[v]].append(True)
+            sch.end_wait.append(v)
+    return sch
+
+
+def optimal_makespan(g, seq, budget, fn_ms, h2d_gbs, d2h_gbs, elide_clean=True):
+    """Minimum simulated makespan (oracle/simulator.simulate, the paper's
+    boundary semantics) over every sequence of resident sets S_i ⊇ V̂_i with
+    bytes(S_i) + pinned <= B (the P:62 search space), or None.  Limits: <= 4
+    functions, <= 5 non-pinned variables."""
+    from . import simulator
+    vars_ = [v for v in range(g.n_vars) if not g.pinned[v]]
+    if len(vars_) > 5 or g.n_fns > 4:
+        raise ValueError("instance exceeds brute-force limits")
+    b = g.var_bytes
+    cap = budget - sum(x for v, x in enumerate(b) if g.pinned[v])
+    n = g.n_fns
+    uses = [set(v for v in seq.occ[seq.l[i]:seq.e[i] + 1] if not g.pinned[v]) for i in range(n)]
+    choices = [[S for S in _subsets_containing(uses[i], vars_) if sum(b[v] for v in S) <= cap] for i in range(n)]
+    if any(not c for c in choices):
+        return None
+    best = [INF, None]
+
+    def rec(i, sets):
+        if i == n:
+            sch = _schedule_of(g, seq, sets)
+            m = simulator.simulate(g, seq, sch, fn_ms, h2d_gbs, d2h_gbs, 0.0, 0.0, elide_clean)["makespan_ms"]
+            if m < best[0]:
+                best[0], best[1] = m, list(sets)
+            return
+        for S in choices[i]:
+            rec(i + 1, sets + [S])
+
+    rec(0, [])
+    return best[0]

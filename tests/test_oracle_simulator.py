@@ -114,3 +114,39 @@ def test_executor_model_bounded_by_boundary_model_and_lower_bounds():
         assert e["makespan_ms"] >= max(lb["compute"], lb["h2d"]) - 1e-9, seed
         n_ok += 1
     assert n_ok > 100
+
+
+def test_greedy_makespan_never_beats_the_exhaustive_optimum():
+    """on tiny graphs (<= 4 functions, <= 5 variables)
+    the greedy's simulated makespan at every window is >= the minimum over
+    all resident-set sequences (P:62), which itself is >= the lower bounds;
+    the brute force finds a schedule exactly when the greedy does (Z11 at
+    W = 0).  The gap is measured, not bounded (the paper claims no
+    optimality, P:212)."""
+    from oracle import bruteforce
+    rng = np.random.default_rng(2)
+    gaps = []
+    for seed in range(60):
+        g, seq = _load(sg.random_graph(seed, n_fns=4, n_vars=5, max_bytes=6, p_pinned=0.0))
+        if sum(1 for v in range(g.n_vars) if not g.pinned[v]) > 5 or g.n_fns > 4:
+            continue
+        total = sum(g.var_bytes)
+        fn_ms = list(rng.uniform(0.5, 2.0, g.n_fns))
+        for B in (total // 2, total):
+            opt = bruteforce.optimal_makespan(g, seq, B, fn_ms, 1e-6, 1e-6)
+            try:
+                g0 = scheduler.build_schedule(g, seq, B, 0)
+            except scheduler.InfeasibleBudget:
+                assert opt is None, (seed, B)
+                continue
+            assert opt is not None
+            for W in (0, 3, 10 ** 9):
+                try:
+                    sch = scheduler.build_schedule(g, seq, B, W)
+                except scheduler.InfeasibleBudget:
+                    continue
+                m = simulator.simulate(g, seq, sch, fn_ms, 1e-6, 1e-6)["makespan_ms"]
+                assert m >= opt - 1e-9, (seed, B, W, m, opt)
+                gaps.append(m / opt - 1.0)
+            del g0
+    assert gaps and min(gaps) >= -1e-9
