@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="r18", choices=["r18", "r50", "r1001", "mlp", "biggan", "unet"])
+    ap.add_argument("--config", default="r18", choices=["r18", "r50", "r1001", "mlp", "biggan", "unet", "densenet"])
     ap.add_argument("--mode", default="va", choices=["va", "best", "first"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--budget-frac", type=float, default=0.25)
@@ -63,6 +63,11 @@ def config(args):
         b = args.batch or 256
         spec = nets.resnet(50, batch=b)
         return spec, {"workload": f"ResNet-50 224x224 b={b} at {args.budget_frac:.2f} of F_peak"}
+    if args.config == "densenet":
+        # the paper's second family (Fig.4/5), DenseNet-121 224²
+        b = args.batch or 128
+        spec = nets.densenet(batch=b)
+        return spec, {"workload": f"F3 DenseNet-121 224x224 b={b} at {args.budget_frac:.2f} of F_peak"}
     if args.config == "unet":
         # configs[3]: U-Net 1024² b=8 at 1/8 of F_peak (pass --budget-frac 0.125)
         b = args.batch or 8
@@ -483,6 +488,9 @@ def oracle_sample(args):
         scale, note = 16.0, "unet batch 1 on a 256x256 crop, time scaled by the 16x pixel count (extrapolated)"
     elif args.config == "mlp":
         spec, scale, note = nets.mlp6(), 1.0, "mlp6 batch 8 per step"
+    elif args.config == "densenet":
+        spec = nets.densenet(batch=1)
+        scale, note = 1.0, "densenet121 batch 1 per step"
     else:
         spec = {"r50": lambda: nets.resnet(50, batch=1), "r1001": lambda: nets.preact_resnet(1001, batch=2)}.get(
             args.config, lambda: nets.resnet(18, batch=2))()

@@ -31,6 +31,7 @@ Definitions used (standard):
   attention   SAGAN self-attention over the H·W positions of one sample:
               q = x Wqᵀ, k = x Wkᵀ, v = x Wvᵀ (1×1 convs), P = softmax_rows(q kᵀ),
               o = P v, out = o Woᵀ, y = x + γ·out  (γ a learned scalar, ".gain")
+  concat      y = [a, b] along channels (DenseNet); gradient split
   hinge       D: L = mean(relu(1 − D(x_real))) + mean(relu(1 + D(G(z))));
               G: L = −mean(D(G(z)))
 """
@@ -271,6 +272,8 @@ class _Net:
                 out = np.maximum(xin, 0.0)
             elif t == "tanh":
                 out = rnd(np.tanh(xin))
+            elif t == "concat":                    # channels [in, in2] (a copy: no rounding)
+                out = np.concatenate([xin, acts[lay["in2"]]], axis=-1)
             elif t == "upsample2":
                 out = upsample2(xin)
             elif t == "avgpool2":
@@ -360,6 +363,11 @@ class _Net:
                 y = acts[lay["out"]]
                 if need_dx:
                     acc(lay["in"], g * (1.0 - y * y))
+            elif t == "concat":
+                ca = xin.shape[-1]
+                if need_dx:
+                    acc(lay["in"], g[..., :ca])
+                acc(lay["in2"], g[..., ca:])
             elif t == "upsample2":
                 if need_dx:
                     acc(lay["in"], upsample2_backward(g))

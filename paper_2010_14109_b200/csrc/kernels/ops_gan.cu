@@ -162,6 +162,39 @@ __global__ void concat_k(int64_t na8, int64_t nb8, const T* __restrict__ a, cons
     st8(out + i * 8, i < na8 ? ld8(a + i * 8) : ld8(b + (i - na8) * 8));
 }
 
+// ---------------------------------------------------------------- channel concatenation (DenseNet)
+template <typename T>
+__global__ void concat_ch_k(int64_t rows, int Ca8, int Cb8, const T* __restrict__ a, const T* __restrict__ b,
+                            T* __restrict__ out) {
+  const int C8 = Ca8 + Cb8;
+  const int64_t n = rows * C8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / C8;
+    const int c8 = (int)(i - r * C8);
+    st8(out + i * 8, c8 < Ca8 ? ld8(a + (r * Ca8 + c8) * 8) : ld8(b + (r * Cb8 + c8 - Ca8) * 8));
+  }
+}
+// da, db = the channel slices of g (each stored, or accumulated rnd(d + slice); null = not wanted)
+template <typename T>
+__global__ void concat_ch_bwd_k(int64_t rows, int Ca8, int Cb8, const T* __restrict__ g, T* da, T* db, int acc_a,
+                                int acc_b) {
+  const int C8 = Ca8 + Cb8;
+  const int64_t n = rows * C8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / C8;
+    const int c8 = (int)(i - r * C8);
+    T* d = c8 < Ca8 ? (da ? da + (r * Ca8 + c8) * 8 : nullptr) : (db ? db + (r * Cb8 + c8 - Ca8) * 8 : nullptr);
+    if (!d) continue;
+    V8 v = ld8(g + i * 8);
+    if (c8 < Ca8 ? acc_a : acc_b) {
+      const V8 o = ld8(d);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v.v[k] += o.v[k];
+    }
+    st8(d, v);
+  }
+}
+
 // ---------------------------------------------------------------- y = x + γ·a
 template <typename T>
 __global__ void scale_add_k(int64_t n8, const T* __restrict__ x, const T* __restrict__ a,
@@ -336,6 +369,26 @@ Status concat_batch_t(OpArgs& a) {
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
+template <typename T>
+Status concat_ch_fwd_t(OpArgs& a) {
+  const int64_t rows = A(a, "rows");
+  const int Ca = (int)A(a, "Ca"), Cb = (int)A(a, "Cb");
+  if (Ca % 8 || Cb % 8) return Status::make(OC_E_UNSUPPORTED, "concat: channels % 8");
+  concat_ch_k<T><<<grid_for(rows * (Ca + Cb) / 8, 256, 4), 256, 0, a.stream>>>(rows, Ca / 8, Cb / 8, (const T*)a.p(0),
+                                                                               (const T*)a.p(1), (T*)a.p(2));
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+template <typename T>
+Status concat_ch_bwd_t(OpArgs& a) {
+  const int64_t rows = A(a, "rows");
+  const int Ca = (int)A(a, "Ca"), Cb = (int)A(a, "Cb");
+  if (Ca % 8 || Cb % 8) return Status::make(OC_E_UNSUPPORTED, "concat: channels % 8");
+  concat_ch_bwd_k<T><<<grid_for(rows * (Ca + Cb) / 8, 256, 4), 256, 0, a.stream>>>(
+      rows, Ca / 8, Cb / 8, (const T*)a.p(0), (T*)a.p(1), (T*)a.p(2), Ab(a, "acc_a") ? 1 : 0, Ab(a, "acc_b") ? 1 : 0);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
 enum { SA_X, SA_A, SA_GAIN, SA_Y };
 template <typename T>
 Status scale_add_fwd_t(OpArgs& a) {
@@ -434,6 +487,8 @@ OC_GAN_DISPATCH(relu_bwd)
 OC_GAN_DISPATCH(tanh_fwd)
 OC_GAN_DISPATCH(tanh_bwd)
 OC_GAN_DISPATCH(concat_batch)
+OC_GAN_DISPATCH(concat_ch_fwd)
+OC_GAN_DISPATCH(concat_ch_bwd)
 OC_GAN_DISPATCH(scale_add_fwd)
 OC_GAN_DISPATCH(scale_add_bwd)
 OC_GAN_DISPATCH(attn_fwd)
@@ -488,6 +543,8 @@ extern const OpDesc kReluBwd{"relu_bwd", {"g", "x", "dx"}, relu_bwd, nullptr};
 extern const OpDesc kTanhFwd{"tanh_fwd", {"x", "y"}, tanh_fwd, nullptr};
 extern const OpDesc kTanhBwd{"tanh_bwd", {"g", "y", "dx"}, tanh_bwd, nullptr};
 extern const OpDesc kConcatBatch{"concat_batch", {"a", "b", "out"}, concat_batch, nullptr};
+extern const OpDesc kConcatChFwd{"concat_ch_fwd", {"a", "b", "out"}, concat_ch_fwd, nullptr};
+extern const OpDesc kConcatChBwd{"concat_ch_bwd", {"g", "da", "db"}, concat_ch_bwd, nullptr};
 extern const OpDesc kScaleAddFwd{"scale_add_fwd", {"x", "a", "gain", "y"}, scale_add_fwd, nullptr};
 extern const OpDesc kScaleAddBwd{"scale_add_bwd", {"g", "a", "gain", "dgain", "da"}, scale_add_bwd, scale_add_ws};
 extern const OpDesc kAttnFwd{"attn_fwd", {"q", "k", "v", "p", "o"}, attn_fwd, attn_ws};

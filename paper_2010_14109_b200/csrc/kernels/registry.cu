@@ -12,7 +12,7 @@ namespace oc {
   X(kPoolBnBwdApply) X(kGapFwd) X(kGapBwd) X(kAddFwd) X(kMaxpoolFwd) X(kMaxpoolBwd) X(kSoftmaxCEPix) X(kConvTFwd) \
   X(kConvTDgrad) X(kConvTWgrad) X(kUpsample2Fwd) X(kUpsample2Bwd) X(kAvgpool2Fwd) X(kAvgpool2Bwd) \
   X(kReluFwd) X(kReluBwd) X(kTanhFwd) X(kTanhBwd) X(kConcatBatch) X(kScaleAddFwd) X(kScaleAddBwd) X(kAttnFwd) \
-  X(kAttnBwd) X(kHingeD) X(kHingeG)
+  X(kAttnBwd) X(kHingeD) X(kHingeG) X(kConcatChFwd) X(kConcatChBwd)
 
 #define OC_DECL(n) extern const OpDesc n;
 OC_OPS(OC_DECL)

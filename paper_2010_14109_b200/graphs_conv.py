@@ -15,6 +15,8 @@ Function granularity is chosen so every function's working set stays small
   conv          conv_wgrad [dy, x] -> [dW];  conv_dgrad [dy, W, (G)] -> [G]
                 (G accumulates: first contribution rnd(c), later rnd(G + c))
   per layer     allreduce [grads] -> [grads]; sgd [W, g, m] -> [W, m]
+  DenseNet      concat_ch_fwd [a, b] -> [out]; concat_ch_bwd [g] -> [da, db]
+                (each slice stored or accumulated); avgpool2 transitions
 """
 import numpy as np
 
@@ -123,6 +125,19 @@ def build_convnet(spec, params="pinned", inputs="host"):
                      {"y": t[lay["in"]], "stat": stat[nm], "gamma": P[nm + ".gamma"], "beta": P[nm + ".beta"],
                       "res": res, "out": t[lay["out"]]}, attrs,
                      [t[lay["in"]], P[nm + ".gamma"], P[nm + ".beta"], res], [stat[nm], t[lay["out"]]])
+        elif ty == "avgpool2":
+            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
+            H, W, C = shapes[lay["in"]]
+            lay["_attrs"] = {"dtype": DT, "N": Nb, "H": H, "W": W, "C": C}
+            b.fn(f"fwd.{nm}", "avgpool2_fwd", {"x": t[lay["in"]], "y": t[lay["out"]]}, lay["_attrs"],
+                 [t[lay["in"]]], [t[lay["out"]]])
+        elif ty == "concat":
+            # DenseNet: the layer's features appended to the running map (a copy)
+            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
+            H, W, Ca = shapes[lay["in"]]
+            lay["_attrs"] = {"dtype": DT, "rows": Nb * H * W, "Ca": Ca, "Cb": shapes[lay["in2"]][-1]}
+            b.fn(f"fwd.{nm}", "concat_ch_fwd", {"a": t[lay["in"]], "b": t[lay["in2"]], "out": t[lay["out"]]},
+                 lay["_attrs"], [t[lay["in"]], t[lay["in2"]]], [t[lay["out"]]])
         elif ty == "gap":
             t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
             H, W, C = shapes[lay["in"]]
@@ -261,6 +276,29 @@ def build_convnet(spec, params="pinned", inputs="host"):
             b.fn(f"bwd.{nm}.dgrad", "convT_dgrad", {"dy": gv, "w": P[nm + ".W"], "dx": dx},
                  dict(lay["_attrs"], accumulate=acc), ins, [dx])
             _update(b, spec, nm, P, Mo, G, [nm + ".W"])
+        elif ty == "avgpool2":
+            src = lay["in"]
+            acc = src in g
+            if acc:
+                dx = g[src]
+                ins = [gv, dx]
+            else:
+                dx = b.var(f"grad.{src}", nbytes(src), shape=[Nb] + shapes[src], dtype=DT)
+                ins = [gv]
+                g[src] = dx
+            b.fn(f"bwd.{nm}", "avgpool2_bwd", {"g": gv, "dx": dx}, dict(lay["_attrs"], accumulate=acc), ins, [dx])
+        elif ty == "concat":
+            outs, ins, accs = [], [gv], []
+            for src in (lay["in"], lay["in2"]):
+                acc = src in g
+                if acc:
+                    ins.append(g[src])
+                else:
+                    g[src] = b.var(f"grad.{src}", nbytes(src), shape=[Nb] + shapes[src], dtype=DT)
+                outs.append(g[src])
+                accs.append(acc)
+            b.fn(f"bwd.{nm}", "concat_ch_bwd", {"g": gv, "da": outs[0], "db": outs[1]},
+                 dict(lay["_attrs"], acc_a=accs[0], acc_b=accs[1]), ins, outs)
         elif ty == "maxpool":
             src = lay["in"]
             acc = src in g

@@ -244,6 +244,10 @@ def net_shapes(layers, in_name, in_shape):
             shapes[lay["out"]] = list(ish)
         elif t in ("relu", "tanh"):
             shapes[lay["out"]] = list(ish)
+        elif t == "concat":             # channel concatenation [in, in2]
+            H2, W2, C2 = shapes[lay["in2"]]
+            assert (H2, W2) == tuple(ish[:2])
+            shapes[lay["out"]] = [ish[0], ish[1], ish[2] + C2]
         elif t == "upsample2":
             shapes[lay["out"]] = [2 * ish[0], 2 * ish[1], ish[2]]
         elif t == "avgpool2":
@@ -303,6 +307,56 @@ def make_params(spec, seed=2, pshapes=None):
             bound = 1.0 / np.sqrt(fan_in)
             out[name] = rng.uniform(-bound, bound, shp).astype(np.float32)
     return out
+
+
+def densenet(batch=64, image=224, classes=1000, mode="bf16", growth=32, blocks=(6, 12, 24, 16), bn_size=4,
+             init=64, compression=0.5):
+    """DenseNet-BC (Huang et al.; DenseNet-121 by default), the second workload
+    family of the paper's Fig.4/5: stem conv7×7/2-BN-ReLU-
+    maxpool3/2; dense layers BN-ReLU-conv1×1(4k)-BN-ReLU-conv3×3(k) whose
+    output is concatenated to the running feature map (materialised, one
+    2-input concatenation per layer — the quadratic memory the family is known
+    for); transitions BN-ReLU-conv1×1(θC)-avgpool2; BN-ReLU-GAP-FC."""
+    L = []
+
+    def conv(name, i, o, k, r, st, pad):
+        L.append({"type": "conv", "name": name, "in": i, "out": o, "k": k, "r": r, "s": r, "stride": st, "pad": pad})
+
+    def bn(name, i, o):
+        L.append({"type": "bn", "name": name, "in": i, "out": o, "relu": True, "residual": None})
+
+    conv("conv0", "x", "c0", init, 7, 2, 3)
+    bn("bn0", "c0", "a0")
+    L.append({"type": "maxpool", "name": "pool0", "in": "a0", "out": "p0", "r": 3, "stride": 2, "pad": 1})
+    prev, C = "p0", init
+    for bi, nl in enumerate(blocks):
+        for li in range(nl):
+            p = f"b{bi}l{li}"
+            bn(p + ".bn1", prev, p + ".a1")
+            conv(p + ".c1", p + ".a1", p + ".y1", bn_size * growth, 1, 1, 0)
+            bn(p + ".bn2", p + ".y1", p + ".a2")
+            conv(p + ".c2", p + ".a2", p + ".y2", growth, 3, 1, 1)
+            L.append({"type": "concat", "name": p + ".cat", "in": prev, "in2": p + ".y2", "out": p + ".cat"})
+            prev, C = p + ".cat", C + growth
+        if bi < len(blocks) - 1:
+            p = f"t{bi}"
+            Ct = int(C * compression)
+            bn(p + ".bn", prev, p + ".a")
+            conv(p + ".c", p + ".a", p + ".y", Ct, 1, 1, 0)
+            L.append({"type": "avgpool2", "name": p + ".pool", "in": p + ".y", "out": p + ".o"})
+            prev, C = p + ".o", Ct
+    bn("bnf", prev, "af")
+    L.append({"type": "gap", "name": "gap", "in": "af", "out": "feat"})
+    L.append({"type": "linear", "name": "fc", "in": "feat", "out": "logits", "features": classes, "relu": False})
+    return {"name": f"densenet{sum(blocks) * 2 + 5}", "mode": mode, "batch": batch, "input": [image, image, 3],
+            "classes": classes, "sgd": {"lr": 0.1, "momentum": 0.9}, "layers": L,
+            "loss": {"type": "softmax_ce", "in": "logits"}}
+
+
+def tiny_densenet(batch=4, image=16, classes=10, mode="bf16"):
+    """Two dense blocks of two layers, growth 8, every DenseNet layer kind."""
+    return densenet(batch=batch, image=image, classes=classes, mode=mode, growth=8, blocks=(2, 2), bn_size=2,
+                    init=16)
 
 
 def biggan(batch=32, image=128, ch=96, z_dim=120, mode="bf16", n_blocks=5, attn_res=64,

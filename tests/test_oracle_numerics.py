@@ -332,3 +332,10 @@ def test_gan_step_gradients_finite_differences():
             assert abs(num - ana) <= 2e-5 * (abs(ana) + 1e-3), (k, idx, num, ana)
     for k in pG:     # every G parameter, attention included, receives a gradient
         assert np.abs(res["gradsG"][k]).max() > 0, k
+
+
+def test_densenet_gradients_finite_differences():
+    """tiny DenseNet-BC: concatenation, average-pool transitions,
+    BN inputs with two consumers — every parameter kind against central
+    differences (fp64)."""
+    _fd_check_spec(nets.tiny_densenet(batch=3, image=16, classes=5), n_checks=20)
