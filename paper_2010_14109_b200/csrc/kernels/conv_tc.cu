@@ -1,8 +1,8 @@
-// Convolution on the 5th-generation tensor cores: implicit GEMM with
-// tcgen05.mma (kind::f16, bf16 × bf16 -> fp32 in TMEM), operands gathered
-// from NHWC activations by cp.async straight into the UMMA canonical
-// SWIZZLE_128B shared-memory layouts, an mbarrier-paced multi-stage pipeline,
-// a single elected MMA-issuing thread, and a TMEM -> register epilogue.
+// Convolution on the 5th-generation tensor cores — the host side of every
+// bf16 tensor-core conv (weight transforms, narrow-input re-layouts,
+// channel padding, split-K reduction, dispatch) and the cp.async-gathered
+// implicit-GEMM kernel used where the TMA kernel (conv_tma.cu) does not
+// apply (narrow-channel weight gradients such as the space-to-depth stem).
 //
 //   fprop  D[m=(n,p,q)][k]        = Σ_{(r,s,c)} X[n,p·st−pad+r,q·st−pad+s,c] · W[k,r,s,c]
 //          A = im2col(X) (K-major rows), B = W_bf16 [K][RSC] (K-major)
@@ -13,17 +13,19 @@
 //   wgrad  D[(r,s,c)][k]          = Σ_{m=(n,p,q)} X[n,p·st−pad+r,q·st−pad+s,c] · dY[m,k]
 //          both operands MN-major (contiguous along channels), deterministic
 //          split-K over m (fixed slices, fixed-order sum), then dW[k][(r,s,c)]
-//   narrow inputs (C % 64 != 0, C % 8 == 0): each 16-byte chunk of a K-block
-//          is its own (tap, 8 channels); a 3-channel input is first re-laid out
-//          slice by slice into 8-channel pixels (zero-padded, weight Cw = 3).
+//   narrow inputs (C % 8 != 0, the 3-channel image): re-laid out slice by
+//          slice in the workspace — space-to-depth for a stride-2 stem, else
+//          8-channel 16-byte pixels (weight channels Cw = 3)
+//   channel counts the 64-wide tiles do not divide: operands zero-padded to
+//          multiples of 64 in workspace copies, real channels stored
 //
-// Tile: UMMA M = 128, N = BN (64 or 128), K-block 64 (one 128-byte swizzle
-// row of bf16).  CTA: warps 0-3 gather and run the epilogue, warp 4 issues
-// the MMAs from one lane.  96 KB of stages (4 at BN=64, 3 at BN=128), each
-// filled by cp.async with completion tracked by the stage's mbarrier
-// (cp.async.mbarrier.arrive.noinc), so two CTAs share an SM and one's
-// epilogue overlaps the other's main loop.  Address arithmetic in the producers is hoisted out of the K loop (rows fixed per thread) and
-// what remains uses 32-bit multiply-shift division (FastDiv).
+// cp.async kernel: UMMA M = 128, N = BN (64 or 128), K-block 64 (one
+// 128-byte swizzle row of bf16).  CTA: warps 0-3 gather and run the epilogue,
+// warp 4 issues the MMAs from one lane.  96 KB of stages (4 at BN=64, 3 at
+// BN=128), each filled by cp.async with completion tracked by the stage's
+// mbarrier (cp.async.mbarrier.arrive.noinc), so two CTAs share an SM and one's
+// epilogue overlaps the other's main loop.  Producer address arithmetic is
+// hoisted out of the K loop and uses 32-bit multiply-shift division.
 #include "tc_util.cuh"
 
 namespace oc {
@@ -38,11 +40,6 @@ __host__ __device__ constexpr int stages_for(int bn) { return bn == 64 ? 4 : 3; 
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 
