@@ -457,7 +457,8 @@ bool conv_tma_enabled();
 // channels stored (TMA kernels)
 bool pad_path(const ConvGeom& g, int mode) {
   if (!conv_tma_enabled() || g.Cw != g.C || g.C % 8 || g.K % 8) return false;
-  const bool nch = g.C == 8 || g.C == 16;
+  // 8/16-channel pixels are gathered natively by the fprop kernel, 16-channel ones by wgrad
+  const bool nch = (mode == FPROP && (g.C == 8 || g.C == 16)) || (mode == WGRAD && g.C == 16);
   if (mode == DGRAD) return g.C % 64 != 0 || g.K % 64 != 0;
   return g.K % 64 != 0 || (g.C % 64 != 0 && !nch);
 }
@@ -636,7 +637,7 @@ struct PadPlan {
 };
 PadPlan pad_plan(const ConvGeom& g, int mode) {
   PadPlan p{g, false, false, g.N, 0, 0};
-  const bool nch = (g.C == 8 || g.C == 16) && mode == FPROP;   // fprop gathers 8/16-ch pixels natively
+  const bool nch = (mode == FPROP && (g.C == 8 || g.C == 16)) || (mode == WGRAD && g.C == 16);
   const int Cp = (g.C % 64 == 0 || nch) ? g.C : up64(g.C), Kp = up64(g.K);
   p.gk.C = p.gk.Cw = Cp;
   p.gk.K = Kp;

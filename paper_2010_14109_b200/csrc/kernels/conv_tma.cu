@@ -153,7 +153,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
           if (it >= (uint32_t)NST) mbar_wait(&empty[sg], ((it / NST) - 1) & 1);
           const uint32_t a = smem_u32(smem + sg * STAGE), b = a + A_BYTES;
           const int kb = kb0 + i;
-          if (MODE == WGRAD) {
+          if (MODE == WGRAD && NCH == 16) {
+            // 16-channel input (the space-to-depth stem): 8 taps per 128-row tile,
+            // one box of KB pixels × 16 channels (SWIZZLE_32B) each
+            int pw, ph, pn;
+            base_of(P, kb * KB, pw, ph, pn);
+            constexpr int BOX = KB * 32;
+            const int t0 = mt * 8;
+            int ntap = P.R * P.S - t0;
+            ntap = ntap < 8 ? ntap : 8;
+            mbar_expect_tx(&full[sg], B_BYTES + ntap * BOX);
+            for (int j = 0; j < ntap; ++j) {
+              const int r = (int)P.fS.div((uint32_t)(t0 + j)), s = t0 + j - r * P.S;
+              tma_load_im2col(a + j * BOX, &P.ta, &full[sg], 0, pw, ph, pn, (uint16_t)s, (uint16_t)r);
+            }
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * ATOM, &P.tb, &full[sg], nt * BN + j * 64, kb * KB);
+          } else if (MODE == WGRAD) {
             int pw, ph, pn;
             base_of(P, kb * KB, pw, ph, pn);
             // 64-row (tap, 64-channel) blocks of (r,s,c) inside the M range
@@ -224,7 +240,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
             for (int t = 0; t < MT; ++t) {
               const uint32_t a = a0 + t * A_TILE;
               uint64_t da;
-              if (MODE == WGRAD) da = sdesc(a + k * 2048, ATOM, 1024);
+              if (MODE == WGRAD && NCH == 16) da = sdesc(a + k * 512, KB * 32, 256, 6);   // MN-major SW32: taps KB·32 B apart
+              else if (MODE == WGRAD) da = sdesc(a + k * 2048, ATOM, 1024);
               else if (NCH == 8) da = sdesc(a + k * 2 * 2048, 2048, 128, 0);   // no swizzle: taps 2 KB apart
               else if (NCH == 16) da = sdesc(a + k * 4096, 16, 256, 6);        // SWIZZLE_32B: one tap per K-step
               else da = sdesc(a + k * 32, 16, 1024);
@@ -430,7 +447,7 @@ bool conv_tma_ok(const ConvGeom& g, int mode) {
   if (g.pad > 127 || g.R > 64 || g.S > 64 || g.st > 8) return false;
   if (mode == FPROP) return g.K % 64 == 0 && (g.C % 64 == 0 || g.C == 8 || g.C == 16);
   if (mode == DGRAD) return g.C % 64 == 0 && g.K % 64 == 0;
-  return g.C % 64 == 0 && g.K % 64 == 0;
+  return (g.C % 64 == 0 || g.C == 16) && g.K % 64 == 0;
 }
 
 // y[M = N·P·Q][K] = im2col(x) · W_bf16[K][kpad]ᵀ
@@ -536,7 +553,9 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
 Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
                       int splits, int kb_per_split, bool accumulate) {
   Params P{};
-  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, 64, WKB, g.P, g.Q, g.st, g.pad, g.pad);
+  const int nch = g.C == 16 ? 16 : 0;
+  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, nch ? 16 : 64, WKB, g.P, g.Q, g.st, g.pad, g.pad,
+                          nch ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B);
   if (!st.good()) return st;
   const int BN = g.K % 128 == 0 ? 128 : 64;
   st = make_tiled(&P.tb, dy, (uint64_t)g.K, (uint64_t)g.N * g.P * g.Q, WKB);
@@ -559,6 +578,7 @@ Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   P.S = g.S;
   P.Cr = g.C;
   fill(P);
+  if (nch) return BN == 128 ? launch<WGRAD, 128, 16>(a, P) : launch<WGRAD, 64, 16>(a, P);
   return BN == 128 ? launch<WGRAD, 128, 0>(a, P) : launch<WGRAD, 64, 0>(a, P);
 }
 
