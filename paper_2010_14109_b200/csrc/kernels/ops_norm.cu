@@ -254,24 +254,28 @@ Status bn_bwd_reduce_t(OpArgs& a) {
 // dy = γ·rstd·(dz − dβ/n − x̂·dγ/n), written over y — or, when the BN input
 // already holds a gradient contribution (acc), accumulated into it as
 // rnd(G + dy); dz written over g (residual branch)
-template <typename T>
+// Variants by (mask source, residual dz output, accumulation) so each keeps
+// only the per-channel parameters it reads live in registers.
+// MASK: 0 none, 1 from the stored output, 2 recomputed from y (γx̂ + β > 0)
+template <typename T, int MASK, bool DZ, bool ACC>
 __global__ void __launch_bounds__(256) bnb_apply(int64_t rows, int C, float inv_n, T* g, const T* __restrict__ out,
                                                  T* y, const float* __restrict__ stat, const float* __restrict__ gamma,
                                                  const float* __restrict__ beta, const float* __restrict__ dgamma,
-                                                 const float* __restrict__ dbeta, int relu, int write_dz, T* acc) {
+                                                 const float* __restrict__ dbeta, T* acc) {
   const int gC = C / 8, tpr = 256 / gC;
   const int cg = threadIdx.x % gC, rr = threadIdx.x / gC;
   if (rr >= tpr) return;
-  float mu[8], rs[8], gm[8], bt[8], dg[8], db[8];
+  float mu[8], rs[8], gm[8], bt[8], a1[8], c1[8], c2[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int c = cg * 8 + k;
     mu[k] = stat[c];
     rs[k] = stat[C + c];
     gm[k] = gamma[c];
-    bt[k] = beta ? beta[c] : 0.f;
-    dg[k] = dgamma[c];
-    db[k] = dbeta[c];
+    bt[k] = MASK == 2 ? beta[c] : 0.f;
+    a1[k] = gm[k] * rs[k];
+    c1[k] = dbeta[c] * inv_n;
+    c2[k] = dgamma[c] * inv_n;
   }
   const int64_t stride = (int64_t)gridDim.x * tpr;
 #pragma unroll 2
@@ -279,17 +283,17 @@ __global__ void __launch_bounds__(256) bnb_apply(int64_t rows, int C, float inv_
     const int64_t o = r * C + cg * 8;
     V8 gv = ld8(g + o), yv = ld8(y + o);
     V8 ov;
-    if (relu && out) ov = ld8(out + o);
+    if (MASK == 1) ov = ld8(out + o);
     V8 dz, dy;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const float xh = (yv.v[k] - mu[k]) * rs[k];
-      const bool on = !relu || (out ? ov.v[k] > 0.f : fmaf(gm[k], xh, bt[k]) > 0.f);
+      const bool on = MASK == 0 || (MASK == 1 ? ov.v[k] > 0.f : fmaf(gm[k], xh, bt[k]) > 0.f);
       const float z = on ? gv.v[k] : 0.f;
       dz.v[k] = z;
-      dy.v[k] = gm[k] * rs[k] * (z - db[k] * inv_n - xh * dg[k] * inv_n);
+      dy.v[k] = a1[k] * (z - c1[k] - xh * c2[k]);
     }
-    if (acc) {
+    if (ACC) {
       V8 old = ld8(acc + o);
 #pragma unroll
       for (int k = 0; k < 8; ++k) dy.v[k] += old.v[k];
@@ -297,8 +301,20 @@ __global__ void __launch_bounds__(256) bnb_apply(int64_t rows, int C, float inv_
     } else {
       st8(y + o, dy);
     }
-    if (write_dz) st8(g + o, dz);
+    if (DZ) st8(g + o, dz);
   }
+}
+
+template <typename T, int MASK>
+Status bnb_apply_launch(OpArgs& a, int64_t rows, int C, bool dz, bool acc, T* accp) {
+  auto k = dz ? (acc ? bnb_apply<T, MASK, true, true> : bnb_apply<T, MASK, true, false>)
+              : (acc ? bnb_apply<T, MASK, false, true> : bnb_apply<T, MASK, false, false>);
+  k<<<rowgroup_blocks(rows, C), 256, 0, a.stream>>>(
+      rows, C, 1.f / (float)rows, (T*)a.p(BB_G), (const T*)a.p(BB_OUT), (T*)a.p(BB_Y), (const float*)a.p(BB_STAT),
+      (const float*)a.p(BB_GAMMA), (const float*)a.p(BB_BETA), (const float*)a.p(BB_DGAMMA),
+      (const float*)a.p(BB_DBETA), accp);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
 }
 
 template <typename T>
@@ -306,13 +322,11 @@ Status bn_bwd_apply_t(OpArgs& a) {
   const int64_t rows = A(a, "rows");
   const int C = (int)A(a, "C");
   if (C % 8 || C > 2048) return Status::make(OC_E_UNSUPPORTED, "bn: C must be a multiple of 8 and <= 2048");
-  bnb_apply<T><<<rowgroup_blocks(rows, C), 256, 0, a.stream>>>(
-      rows, C, 1.f / (float)rows, (T*)a.p(BB_G), (const T*)a.p(BB_OUT), (T*)a.p(BB_Y), (const float*)a.p(BB_STAT),
-      (const float*)a.p(BB_GAMMA), (const float*)a.p(BB_BETA), (const float*)a.p(BB_DGAMMA),
-      (const float*)a.p(BB_DBETA), Ab(a, "relu") ? 1 : 0, Ab(a, "has_res") ? 1 : 0,
-      Ab(a, "accumulate") ? (T*)a.p(BB_ACC) : nullptr);
-  OC_LAUNCH_CHECK(a);
-  return Status::ok();
+  const bool relu = Ab(a, "relu"), dz = Ab(a, "has_res"), acc = Ab(a, "accumulate");
+  T* accp = acc ? (T*)a.p(BB_ACC) : nullptr;
+  if (!relu) return bnb_apply_launch<T, 0>(a, rows, C, dz, acc, accp);
+  if (a.p(BB_OUT)) return bnb_apply_launch<T, 1>(a, rows, C, dz, acc, accp);
+  return bnb_apply_launch<T, 2>(a, rows, C, dz, acc, accp);
 }
 
 // ---------------------------------------------------------------- stem: BN-ReLU-maxpool
