@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256) stats_partial(int64_t rows, int C, const 
   const int64_t r0 = blockIdx.x * chunk, r1 = min(rows, r0 + chunk);
   float s[8] = {}, q[8] = {};
   if (rr < tpr)
+#pragma unroll 2
     for (int64_t r = r0 + rr; r < r1; r += tpr) {
       V8 x = ld8(y + r * C + cg * 8);
 #pragma unroll
@@ -169,12 +170,12 @@ Status bn_fwd_t(OpArgs& a) {
 // ReLU mask of the BN output: from the stored output when there is one
 // (residual blocks), else recomputed from y: relu'(γx̂ + β) (the BN-ReLU output
 // is then not needed by the backward, shrinking its working set)
-template <typename T>
+// MASK: 0 none, 1 from the stored output, 2 recomputed from y (as bnb_apply)
+template <typename T, int MASK>
 __global__ void __launch_bounds__(256) bnb_partial(int64_t rows, int C, const T* __restrict__ g,
                                                    const T* __restrict__ out, const T* __restrict__ y,
                                                    const float* __restrict__ stat, const float* __restrict__ gamma,
-                                                   const float* __restrict__ beta, int relu,
-                                                   float* __restrict__ part) {
+                                                   const float* __restrict__ beta, float* __restrict__ part) {
   const int gC = C / 8, tpr = 256 / gC;
   const int t = threadIdx.x, cg = t % gC, rr = t / gC;
   const int64_t chunk = (rows + gridDim.x - 1) / gridDim.x;
@@ -186,18 +187,19 @@ __global__ void __launch_bounds__(256) bnb_partial(int64_t rows, int C, const T*
     mu[i] = stat[cg * 8 + i];
     rs[i] = stat[C + cg * 8 + i];
     gm[i] = gamma[cg * 8 + i];
-    bt[i] = beta ? beta[cg * 8 + i] : 0.f;
+    bt[i] = MASK == 2 ? beta[cg * 8 + i] : 0.f;
   }
   if (rr < tpr)
+#pragma unroll 2
     for (int64_t r = r0 + rr; r < r1; r += tpr) {
       const int64_t o = r * C + cg * 8;
       V8 gv = ld8(g + o), yv = ld8(y + o);
       V8 ov;
-      if (relu && out) ov = ld8(out + o);
+      if (MASK == 1) ov = ld8(out + o);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const float xh = (yv.v[i] - mu[i]) * rs[i];
-        const bool on = !relu || (out ? ov.v[i] > 0.f : fmaf(gm[i], xh, bt[i]) > 0.f);
+        const bool on = MASK == 0 || (MASK == 1 ? ov.v[i] > 0.f : fmaf(gm[i], xh, bt[i]) > 0.f);
         const float dz = on ? gv.v[i] : 0.f;
         s[i] += dz;
         q[i] = fmaf(dz, xh, q[i]);
@@ -240,10 +242,11 @@ Status bn_bwd_reduce_t(OpArgs& a) {
   if (a.ws_bytes < (size_t)nblk * 2 * C * 4) return Status::make(OC_E_INVARIANT, "bn_bwd: workspace too small");
   if (Ab(a, "relu") && !a.p(BB_OUT) && !a.p(BB_BETA))
     return Status::make(OC_E_INVALID, "bn_bwd: ReLU mask needs the output or beta");
-  bnb_partial<T><<<nblk, 256, 256 * 16 * 4, a.stream>>>(rows, C, (const T*)a.p(BB_G), (const T*)a.p(BB_OUT),
-                                                        (const T*)a.p(BB_Y), (const float*)a.p(BB_STAT),
-                                                        (const float*)a.p(BB_GAMMA), (const float*)a.p(BB_BETA),
-                                                        Ab(a, "relu") ? 1 : 0, (float*)a.ws);
+  const int mask = !Ab(a, "relu") ? 0 : (a.p(BB_OUT) ? 1 : 2);
+  auto kp = mask == 0 ? bnb_partial<T, 0> : (mask == 1 ? bnb_partial<T, 1> : bnb_partial<T, 2>);
+  kp<<<nblk, 256, 256 * 16 * 4, a.stream>>>(rows, C, (const T*)a.p(BB_G), (const T*)a.p(BB_OUT), (const T*)a.p(BB_Y),
+                                            (const float*)a.p(BB_STAT), (const float*)a.p(BB_GAMMA),
+                                            (const float*)a.p(BB_BETA), (float*)a.ws);
   OC_LAUNCH_CHECK(a);
   bnb_finalize<<<(C + 7) / 8, 256, 0, a.stream>>>(nblk, C, (const float*)a.ws, (float*)a.p(BB_DGAMMA),
                                                   (float*)a.p(BB_DBETA));
