@@ -148,6 +148,7 @@ struct Exec {
   // timeline (opt.timeline)
   std::vector<cudaEvent_t> tl_fn0, tl_fn1, tl_in0, tl_in1, tl_out0, tl_out1;
   std::vector<uint8_t> tl_in_used, tl_out_used;
+  std::vector<KernelTimer> tl_k;   // per function: the contraction kernel launches
   // NCCL
   void* nccl_lib = nullptr;
   void* nccl_comm = nullptr;
@@ -405,6 +406,7 @@ Status Exec::create(int dev, const Graph* graph, const Schedule* sch, MemPool* m
     OC_TRY(mk(tl_in1, slots.size(), true));
     OC_TRY(mk(tl_out0, deps.size(), true));
     OC_TRY(mk(tl_out1, deps.size(), true));
+    tl_k.resize(n);
   }
   return Status::ok();
 }
@@ -526,6 +528,10 @@ Status Exec::run(oc_step_metrics* out) {
       oa.stream = cs;
       oa.nccl_comm = nccl_comm;
       oa.nccl_allreduce = nccl_allreduce;
+      if (opt.timeline) {
+        tl_k[i].used = 0;
+        oa.ktimer = &tl_k[i];
+      }
       Status st = X.op->launch(oa);
       if (!st.good()) {
         st.fn = i;
@@ -654,6 +660,7 @@ void Exec::destroy() {
   for (auto& e : ev_join)
     if (e) cudaEventDestroy(e), e = nullptr;
   hs2 = ds2 = nullptr;
+  for (auto& k : tl_k) k.destroy();
   for (auto& sl : slots) {
     if (sl.span.va) {
       if (!sl.span.mapped.empty()) mem->driver_unmap(sl.span);
@@ -733,7 +740,8 @@ int oc_exec_timeline(oc_exec* xh, char* buf, size_t cap, size_t* need) {
     for (uint32_t i = 0; i < X.fns.size(); ++i)
       if (X.fns[i].op)
         o << "{\"t0\":" << t(X.tl_fn0[i]) << ",\"t1\":" << t(X.tl_fn1[i]) << ",\"stream\":\"compute\",\"id\":\""
-          << X.g->fns[i].name << "\"}\n";
+          << X.g->fns[i].name << "\",\"k_ms\":" << (i < X.tl_k.size() ? X.tl_k[i].ms() : 0.0f)
+          << ",\"k_n\":" << (i < X.tl_k.size() ? X.tl_k[i].used / 2 : 0) << "}\n";
     for (size_t k = 0; k < X.slots.size(); ++k)
       if (k < X.tl_in_used.size() && X.tl_in_used[k])
         o << "{\"t0\":" << t(X.tl_in0[k]) << ",\"t1\":" << t(X.tl_in1[k]) << ",\"stream\":\"h2d\",\"id\":\""

@@ -149,7 +149,9 @@ int wgrad_splits_simt(const ConvGeom& g) {
 template <typename T>
 Status conv_fprop_simt(OpArgs& a, const ConvGeom& g, const T* x, const float* w, T* y, bool accumulate) {
   dim3 grid((unsigned)(((int64_t)g.N * g.P * g.Q + BM - 1) / BM), (g.K + BN - 1) / BN);
+  if (a.ktimer) a.ktimer->begin(a.stream);
   conv_simt<0, T><<<grid, 256, 0, a.stream>>>(g, x, w, nullptr, y, accumulate ? 1 : 0, 0);
+  if (a.ktimer) a.ktimer->end(a.stream);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
@@ -157,7 +159,9 @@ Status conv_fprop_simt(OpArgs& a, const ConvGeom& g, const T* x, const float* w,
 template <typename T>
 Status conv_dgrad_simt(OpArgs& a, const ConvGeom& g, const T* dy, const float* w, T* dx, bool accumulate) {
   dim3 grid((unsigned)(((int64_t)g.N * g.H * g.W + BM - 1) / BM), (g.C + BN - 1) / BN);
+  if (a.ktimer) a.ktimer->begin(a.stream);
   conv_simt<1, T><<<grid, 256, 0, a.stream>>>(g, dy, w, nullptr, dx, accumulate ? 1 : 0, 0);
+  if (a.ktimer) a.ktimer->end(a.stream);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
@@ -171,7 +175,9 @@ Status conv_wgrad_simt(OpArgs& a, const ConvGeom& g, const T* dy, const T* x, fl
   const int64_t n = (int64_t)g.K * g.R * g.S * g.C;
   if (a.ws_bytes < (size_t)(splits * n * 4)) return Status::make(OC_E_INVARIANT, "wgrad: workspace too small");
   dim3 grid((g.K + BM - 1) / BM, (unsigned)(((int64_t)g.R * g.S * g.C + BN - 1) / BN), splits);
+  if (a.ktimer) a.ktimer->begin(a.stream);
   conv_simt<2, T><<<grid, 256, 0, a.stream>>>(g, dy, nullptr, x, a.ws, 0, step);
+  if (a.ktimer) a.ktimer->end(a.stream);
   OC_LAUNCH_CHECK(a);
   splitk_reduce<<<grid_for(n, 256, 4), 256, 0, a.stream>>>(splits, n, (const float*)a.ws, dw);
   OC_LAUNCH_CHECK(a);

@@ -411,7 +411,9 @@ Status launch(OpArgs& a, const Params& P, dim3 grid) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
+  if (a.ktimer) a.ktimer->begin(a.stream);
   kern<<<grid, NTHREADS, smem, a.stream>>>(P);
+  if (a.ktimer) a.ktimer->end(a.stream);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }

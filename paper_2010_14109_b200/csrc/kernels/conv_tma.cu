@@ -27,6 +27,7 @@
 //           no-swizzle core-matrix layout (LBO = 2 KB between taps) or the
 //           SWIZZLE_32B layout (one tap per K-step)
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -78,12 +79,16 @@ __device__ __forceinline__ void base_of(const Params& P, int pix, int& w, int& h
   n = (int)nn;
 }
 
-template <int MODE, int BN, int NCH, int MT>
+// CG = 2: CTA pairs (cta_group::2).  A unit is MT tiles of 256 rows (CTA rank
+// r holds rows 128·r .. 128·r + 127 of each) × BN columns; each CTA stages its
+// own A rows and B columns [BN/2·r, BN/2·(r+1)), rank 0 issues 256 × BN MMAs.
+template <int MODE, int BN, int NCH, int MT, int CG = 1>
 __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_constant__ Params P) {
+  static_assert(CG == 1 || (MODE != WGRAD && NCH == 0), "CTA pairs: fprop / dgrad over 64-channel pixels");
   constexpr int KB = kblock(MODE);              // K extent of a stage (elements, or wgrad pixels)
   constexpr int ATOM = KB * 128;                 // wgrad: one 64-wide MN-major atom column
-  constexpr int NST = tma_stages(BN, MT, KB);
-  constexpr int A_TILE = BM * KB * 2, A_BYTES = MT * A_TILE, B_BYTES = BN * KB * 2, STAGE = A_BYTES + B_BYTES;
+  constexpr int NST = tma_stages(BN / CG, MT, KB);
+  constexpr int A_TILE = BM * KB * 2, A_BYTES = MT * A_TILE, B_BYTES = (BN / CG) * KB * 2, STAGE = A_BYTES + B_BYTES;
   constexpr uint32_t TCOLS = 2 * MT * BN;   // two accumulator sets of MT tiles × BN columns
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -105,18 +110,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
     tma_prefetch(&P.ta);
     tma_prefetch(&P.tb);
     for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4 * CG); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TCOLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TCOLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TCOLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (CG == 2) cluster_sync();   // peer barriers initialised before any remote arrive
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const int u0 = blockIdx.x / CG, ustep = gridDim.x / CG;
 
   // a unit = MT consecutive 128-row tiles (super-tile mt) × one BN column block (× one split)
   const int units = P.num_m * P.num_n * (MODE == WGRAD ? P.splits : 1);
@@ -139,14 +153,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t it = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int u = u0; u < units; u += ustep) {
         int mt, nt, z, kb0, nk;
         unit_of(u, mt, nt, z, kb0, nk);
         int bw[MT], bh[MT], bn[MT];
 #pragma unroll
         for (int t = 0; t < MT; ++t) {
           bw[t] = bh[t] = bn[t] = 0;
-          if (MODE != WGRAD) base_of(P, (mt * MT + t) * BM, bw[t], bh[t], bn[t]);
+          if (MODE != WGRAD) base_of(P, ((mt * MT + t) * CG + (int)rank) * BM, bw[t], bh[t], bn[t]);
         }
         for (int i = 0; i < nk; ++i, ++it) {
           const int sg = (int)(it % NST);
@@ -201,24 +215,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
               }
             tma_load_2d(b, &P.tb, &full[sg], kb * BK, nt * BN);
           } else {
-            mbar_expect_tx(&full[sg], STAGE);
             const int tap = (int)P.fCb.div((uint32_t)kb), cb = kb - tap * (P.Cr / 64);
             const int r = (int)P.fS.div((uint32_t)tap), s = tap - r * P.S;
-#pragma unroll
-            for (int t = 0; t < MT; ++t)
-              tma_load_im2col(a + t * A_TILE, &P.ta, &full[sg], cb * 64, bw[t], bh[t], bn[t], (uint16_t)s,
-                              (uint16_t)r);
             const int btap = MODE == DGRAD ? (P.r0 + P.dst * (P.R - 1 - r)) * P.Sw + P.s0 + P.dst * (P.S - 1 - s) : tap;
-            tma_load_2d(b, &P.tb, &full[sg], btap * P.Cr + cb * 64, nt * BN);
+            if (CG == 2) {
+              // both CTAs' bytes land on the leader's barrier
+              const uint32_t fb = mapa(smem_u32(&full[sg]), 0);
+              if (rank == 0) mbar_expect_tx(&full[sg], CG * STAGE);
+#pragma unroll
+              for (int t = 0; t < MT; ++t)
+                tma_load_im2col_pair(a + t * A_TILE, &P.ta, fb, cb * 64, bw[t], bh[t], bn[t], (uint16_t)s,
+                                     (uint16_t)r);
+              tma_load_2d_pair(b, &P.tb, fb, btap * P.Cr + cb * 64, nt * BN + (int)rank * (BN / CG));
+            } else {
+              mbar_expect_tx(&full[sg], STAGE);
+#pragma unroll
+              for (int t = 0; t < MT; ++t)
+                tma_load_im2col(a + t * A_TILE, &P.ta, &full[sg], cb * 64, bw[t], bh[t], bn[t], (uint16_t)s,
+                                (uint16_t)r);
+              tma_load_2d(b, &P.tb, &full[sg], btap * P.Cr + cb * 64, nt * BN);
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t ID = idesc(BN, MODE == WGRAD, MODE == WGRAD);
+    // ------------------------------------------------------------ MMA issuer (pair: the leader only)
+    constexpr uint32_t ID = idesc_m(BM * CG, BN, MODE == WGRAD, MODE == WGRAD);
     uint32_t it = 0, lt = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+    for (int u = (CG == 2 && rank != 0) ? units : u0; u < units; u += ustep, ++lt) {
       int mt, nt, z, kb0, nk;
       unit_of(u, mt, nt, z, kb0, nk);
       const uint32_t buf = lt & 1;
@@ -245,14 +270,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
               else if (NCH == 8) da = sdesc(a + k * 2 * 2048, 2048, 128, 0);   // no swizzle: taps 2 KB apart
               else if (NCH == 16) da = sdesc(a + k * 4096, 16, 256, 6);        // SWIZZLE_32B: one tap per K-step
               else da = sdesc(a + k * 32, 16, 1024);
-              mma_bf16(d + t * BN, da, db, ID, (i > 0 || k > 0) ? 1u : 0u);
+              if (CG == 2) mma_bf16_pair(d + t * BN, da, db, ID, (i > 0 || k > 0) ? 1u : 0u);
+              else mma_bf16(d + t * BN, da, db, ID, (i > 0 || k > 0) ? 1u : 0u);
             }
           }
-          mma_commit(&empty[sg]);
+          if (CG == 2) mma_commit_pair(&empty[sg]);
+          else mma_commit(&empty[sg]);
         }
         __syncwarp();
       }
-      if (lane == 0) mma_commit(&tfull[buf]);
+      if (lane == 0) {
+        if (CG == 2) mma_commit_pair(&tfull[buf]);
+        else mma_commit(&tfull[buf]);
+      }
       __syncwarp();
     }
   } else {
@@ -260,7 +290,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
     const int q = warp & 3;            // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
     uint32_t lt = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+    for (int u = u0; u < units; u += ustep, ++lt) {
       int mt, nt, z, kb0, nk;
       unit_of(u, mt, nt, z, kb0, nk);
       const uint32_t buf = lt & 1;
@@ -268,7 +298,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
       for (int t = 0; t < MT; ++t) {
-        const int m = (mt * MT + t) * BM + row;
+        const int m = ((mt * MT + t) * CG + (int)rank) * BM + row;
         int64_t orow = m;
         if (MODE == DGRAD && m < P.M) {
           int w, h, n;
@@ -328,14 +358,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(mapa(smem_u32(&tempty[buf]), 0));
+        else mbar_arrive(&tempty[buf]);
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (CG == 2) cluster_sync();   // the leader's MMAs read this CTA's stages and write its TMEM
+  else __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+    if (CG == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
   }
 }
 
@@ -346,6 +381,18 @@ int sm_count() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// CTA pairs the device can hold at once (one 2-CTA cluster per TPC at our
+// shared-memory footprint); 74 on a 148-SM B200
+int max_pairs() {
+  static int n = 0;
+  if (!n) {
+    n = sm_count() / 2;
+    const char* e = std::getenv("OC_CONV_PAIRS");
+    if (e && std::atoi(e) > 0) n = std::atoi(e);
   }
   return n;
 }
@@ -402,30 +449,101 @@ int conv_mt() {
   return mt;
 }
 
-template <int MODE, int BN, int NCH, int MT>
+template <int MODE, int BN, int NCH, int MT, int CG = 1>
 Status launch_mt(OpArgs& a, Params P) {
-  constexpr int smem = tma_smem(BN, MT, kblock(MODE));
-  auto kern = conv_tma_kernel<MODE, BN, NCH, MT>;
+  constexpr int smem = tma_smem(BN / CG, MT, kblock(MODE));
+  auto kern = conv_tma_kernel<MODE, BN, NCH, MT, CG>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (CG == 2) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     attr = true;
   }
-  P.num_m = (P.M + BM * MT - 1) / (BM * MT);   // super-tiles of MT × 128 rows
+  P.num_m = (P.M + BM * MT * CG - 1) / (BM * MT * CG);   // super-tiles of MT × (128·CG) rows
   const int units = P.num_m * P.num_n * (MODE == WGRAD ? P.splits : 1);
   if (units == 0) return Status::ok();
-  kern<<<std::min(units, sm_count()), NTHREADS, smem, a.stream>>>(P);
+  if (a.ktimer) a.ktimer->begin(a.stream);
+  if (CG == 1) {
+    kern<<<std::min(units, sm_count()), NTHREADS, smem, a.stream>>>(P);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = a.stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const int pairs = std::min(units, max_pairs());
+    cfg.gridDim = dim3(2 * pairs);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, P);
+    if (e != cudaSuccess) return cuda_status(e, "conv_tma pair launch");
+  }
+  if (a.ktimer) a.ktimer->end(a.stream);
   OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
 
-// fprop / dgrad: MT = 2, each unit is two 128-row tiles sharing every B stage
-// (half the B traffic per FLOP; measured 7-16% faster).  wgrad keeps single
-// tiles: its M = R·S·C is short (e.g. 576) and pairs would pad it further.
-// OC_CONV_MT=1 selects single tiles everywhere.
+// wgrad keeps single 128-row tiles: its M = R·S·C is short (e.g. 576) and
+// pairs would pad it further.
 template <int MODE, int BN, int NCH>
 Status launch(OpArgs& a, const Params& P) {
   return (MODE != WGRAD && conv_mt() == 2) ? launch_mt<MODE, BN, NCH, 2>(a, P) : launch_mt<MODE, BN, NCH, 1>(a, P);
+}
+
+// Tile shape of the 64-channel fprop / dgrad GEMM (M rows, N columns).
+// Shared memory feeds both the TMA writes and the UMMA operand reads
+// (128 B/clk per SM); per 128 × N × 16 MMA step (N/2 cycles) a single CTA
+// reads A (4 KB) + B (N·32 B) and the TMA writes the next K-block.  CTA pairs
+// (cta_group::2) stage half of B per CTA, which lowers that traffic:
+//   pair N=256: 128 B/clk at the MMA rate (fits), pair N=128 ×2 tiles: 176,
+//   single N=128 ×2 tiles: 224 (the MMA can run at most ~57 %), pair N=64: 304,
+//   single N=64: 352.  The choice weighs that against wave quantisation over
+//   the persistent grid (148 CTAs or max_pairs() pairs).  OC_CONV_CG=1 keeps
+//   single CTAs.
+struct Tile { int bn, mt, cg; };
+Tile choose_tile(int M, int N) {
+  const char* e = std::getenv("OC_CONV_CG");
+  const int env = (e && e[0] == '1') ? 1 : 2;
+  // OC_CONV_TILE="bn,mt,cg" forces one of the shapes below (tests)
+  if (const char* f = std::getenv("OC_CONV_TILE")) {
+    Tile t{0, 0, 0};
+    if (std::sscanf(f, "%d,%d,%d", &t.bn, &t.mt, &t.cg) == 3 && t.bn > 0 && N % t.bn == 0 &&
+        ((t.bn == 256 && t.mt == 1 && t.cg == 2) || ((t.bn == 128 || t.bn == 64) && t.mt == 2) ||
+         ((t.bn == 128 || t.bn == 64) && t.mt == 1 && t.cg == 1)))
+      return t;
+  }
+  const Tile cand[5] = {{256, 1, 2}, {128, 2, 2}, {128, 2, 1}, {64, 2, 2}, {64, 2, 1}};
+  const double eff[5] = {0.85, 128.0 / 176, 128.0 / 224, 128.0 / 304, 128.0 / 352};
+  Tile best{N % 128 == 0 ? 128 : 64, conv_mt(), 1};
+  double bt = 1e300;
+  for (int i = 0; i < 5; ++i) {
+    const Tile& t = cand[i];
+    if (N % t.bn) continue;
+    if (t.cg == 2 && env == 1) continue;
+    if (t.mt != conv_mt() && t.cg == 1) continue;
+    const int rows = BM * t.mt * t.cg;
+    const long units = (long)((M + rows - 1) / rows) * (N / t.bn);
+    const int slots = t.cg == 2 ? max_pairs() : sm_count();
+    const double waves = (double)((units + slots - 1) / slots);
+    const double time = waves * rows * t.bn / t.cg / eff[i];   // per SM
+    if (time < bt * 0.999) { bt = time; best = t; }
+  }
+  return best;
+}
+
+template <int MODE>
+Status launch_tile(OpArgs& a, const Params& P, Tile t) {
+  if (t.cg == 2) {
+    if (t.bn == 256) return launch_mt<MODE, 256, 0, 1, 2>(a, P);
+    if (t.bn == 128) return launch_mt<MODE, 128, 0, 2, 2>(a, P);
+    return launch_mt<MODE, 64, 0, 2, 2>(a, P);
+  }
+  if (t.mt == 1) return t.bn == 128 ? launch_mt<MODE, 128, 0, 1>(a, P) : launch_mt<MODE, 64, 0, 1>(a, P);
+  return t.bn == 128 ? launch_mt<MODE, 128, 0, 2>(a, P) : launch_mt<MODE, 64, 0, 2>(a, P);
 }
 
 }  // namespace tma
@@ -460,8 +578,9 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
                           nch == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE
                                    : (nch == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B));
   if (!st.good()) return st;
-  const int BN = g.K % 128 == 0 ? 128 : 64;
-  st = make_tiled(&P.tb, wb, (uint64_t)kpad, (uint64_t)g.K, (uint32_t)BN);
+  const Tile tile = nch ? Tile{g.K % 128 == 0 ? 128 : 64, conv_mt(), 1} : choose_tile(g.N * g.P * g.Q, g.K);
+  const int BN = tile.bn;
+  st = make_tiled(&P.tb, wb, (uint64_t)kpad, (uint64_t)g.K, (uint32_t)(BN / tile.cg));
   if (!st.good()) return st;
   P.out = y;
   P.nst = nst;
@@ -482,7 +601,7 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   fill(P);
   if (nch == 8) return BN == 128 ? launch<FPROP, 128, 8>(a, P) : launch<FPROP, 64, 8>(a, P);
   if (nch == 16) return BN == 128 ? launch<FPROP, 128, 16>(a, P) : launch<FPROP, 64, 16>(a, P);
-  return BN == 128 ? launch<FPROP, 128, 0>(a, P) : launch<FPROP, 64, 0>(a, P);
+  return launch_tile<FPROP>(a, P, tile);
 }
 
 // dgrad, one launch per output phase (h mod st, w mod st) over that phase's
@@ -490,7 +609,6 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
 // phase's filter taps; a phase no tap reaches gets zeros (or keeps dx when accumulating)
 Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* wt,
                       __nv_bfloat16* dx, bool accumulate, int nst) {
-  const int BN = g.C % 128 == 0 ? 128 : 64;
   // phases no filter tap reaches (e.g. 3 of the 4 phases of a 1×1 stride-2 conv):
   // without accumulation their dx is zero — cleared once for the whole tensor
   bool tapless = false;
@@ -515,7 +633,9 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
       const int padh = nr > 0 ? nr - 1 - dh : 0, padw = ns > 0 ? ns - 1 - dw : 0;
       Status st = make_im2col(&P.ta, dy, g.N, g.P, g.Q, g.K, 64, BM, Hp, Wp, 1, padh, padw);
       if (!st.good()) return st;
-      st = make_tiled(&P.tb, wt, (uint64_t)g.R * g.S * g.K, (uint64_t)g.C, (uint32_t)BN);
+      const Tile tile = choose_tile(g.N * Hp * Wp, g.C);
+      const int BN = tile.bn;
+      st = make_tiled(&P.tb, wt, (uint64_t)g.R * g.S * g.K, (uint64_t)g.C, (uint32_t)(BN / tile.cg));
       if (!st.good()) return st;
       P.out = dx;
       P.nst = nst;
@@ -543,7 +663,7 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
       P.Ho = g.H;
       P.Wo = g.W;
       fill(P);
-      st = BN == 128 ? launch<DGRAD, 128, 0>(a, P) : launch<DGRAD, 64, 0>(a, P);
+      st = launch_tile<DGRAD>(a, P, tile);
       if (!st.good()) return st;
     }
   return Status::ok();

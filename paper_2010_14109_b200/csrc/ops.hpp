@@ -16,7 +16,43 @@
 
 namespace oc {
 
+// Event pairs around the main contraction kernel launches of one function
+// (timeline mode only): the bench's roofline divides algorithmic FLOPs by the
+// kernel's own launch durations, without the operand re-layout kernels.
+struct KernelTimer {
+  std::vector<cudaEvent_t> ev;   // 2 per launch, created on demand, reused every step
+  size_t used = 0;
+  void begin(cudaStream_t s) {
+    if (used + 2 > ev.size())
+      for (int k = 0; k < 2; ++k) {
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        ev.push_back(e);
+      }
+    cudaEventRecord(ev[used], s);
+  }
+  void end(cudaStream_t s) {
+    cudaEventRecord(ev[used + 1], s);
+    used += 2;
+  }
+  float ms() const {
+    float t = 0;
+    for (size_t k = 0; k + 1 < used; k += 2) {
+      float v = 0;
+      cudaEventElapsedTime(&v, ev[k], ev[k + 1]);
+      t += v;
+    }
+    return t;
+  }
+  void destroy() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    ev.clear();
+    used = 0;
+  }
+};
+
 struct OpArgs {
+  KernelTimer* ktimer = nullptr;   // non-null in timeline mode
   // one entry per role in OpDesc::roles order; list roles hold several
   std::vector<std::vector<void*>> ptr;
   std::vector<std::vector<uint64_t>> bytes;

@@ -132,3 +132,36 @@ def test_conv_wgrad(g):
     _, ref = nm.conv2d_backward(x.float().numpy().astype(np.float64), np.zeros((K, R, R, C)),
                                 dy.float().numpy().astype(np.float64), st, pad)
     assert nm.rel_l2(dw, ref) < 1e-5
+
+
+# CTA-pair (cta_group::2) tiles and the single-CTA ones, forced per launch
+# (OC_CONV_TILE = "N-tile,tiles per unit,CTAs"): ragged M tails that leave the
+# second CTA of a pair, or the second tile of a unit, past the last row
+TILES = ["256,1,2", "128,2,2", "64,2,2", "128,2,1", "64,1,1"]
+TILE_SHAPES = [  # N, H, W, C, K, R, stride, pad
+    (2, 9, 7, 64, 256, 3, 1, 1),      # M = 126: one pair, the second CTA's rows all past M
+    (3, 11, 10, 256, 256, 3, 2, 1),   # stride 2 (dgrad: 4 phases)
+    (2, 12, 9, 128, 256, 1, 2, 0),    # 1x1 stride 2 (dgrad: tap-less phases)
+    (5, 13, 13, 128, 128, 3, 1, 1),   # M = 845: several pairs and a ragged tail
+    (4, 9, 9, 256, 64, 3, 1, 1),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tile", TILES)
+@pytest.mark.parametrize("g", TILE_SHAPES)
+def test_conv_tiles_fwd(g, tile, monkeypatch):
+    if g[4] % int(tile.split(",")[0]):
+        pytest.skip("N tile does not divide K")
+    monkeypatch.setenv("OC_CONV_TILE", tile)
+    test_conv_fwd(g)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tile", TILES)
+@pytest.mark.parametrize("g", TILE_SHAPES)
+def test_conv_tiles_dgrad(g, tile, monkeypatch):
+    if g[3] % int(tile.split(",")[0]):
+        pytest.skip("N tile does not divide C")
+    monkeypatch.setenv("OC_CONV_TILE", tile)
+    test_conv_dgrad(g, True)
