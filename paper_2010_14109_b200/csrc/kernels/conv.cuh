@@ -11,6 +11,8 @@ struct ConvGeom {
             // 16-byte pixels, attrs "Cw"); default Cw = C
   int pad_slice;  // narrow inputs: images per zero-padding slice (attrs
                   // "pad_slice"; 0 = as many as fit 32 MiB)
+  int nopadh;     // kernel geometry of the folded stem: no vertical padding
+                  // (the vertical taps live in the channels), pad is horizontal only
 };
 
 inline ConvGeom conv_geom(const OpArgs& a) {

@@ -41,18 +41,22 @@ using namespace tcu;
 constexpr int BM = 128, BK = 64, NTHREADS = 192;
 constexpr int WKB = 128;   // wgrad K-block: 128 pixels (one 16 KB MN-major atom column per 64 channels)
 __host__ __device__ constexpr int kblock(int mode) { return mode == 2 ? WKB : BK; }
-// stages: as many as fit ~196 KB (at most 8)
+// stages: as many as fit 192 KB (at most 8); fprop / dgrad add 32 KB of
+// epilogue staging (two 32-row × 64-column bf16 boxes per epilogue warp)
+constexpr int STG_BYTES = 8 * 4096;
 __host__ __device__ constexpr int tma_stage_bytes(int bn, int mt, int kb) { return mt * BM * kb * 2 + bn * kb * 2; }
 __host__ __device__ constexpr int tma_stages(int bn, int mt, int kb) {
-  return (196 * 1024) / tma_stage_bytes(bn, mt, kb) < 8 ? (196 * 1024) / tma_stage_bytes(bn, mt, kb) : 8;
+  return (192 * 1024) / tma_stage_bytes(bn, mt, kb) < 8 ? (192 * 1024) / tma_stage_bytes(bn, mt, kb) : 8;
 }
 __host__ __device__ constexpr int tma_smem(int bn, int mt, int kb) {
-  return tma_stages(bn, mt, kb) * tma_stage_bytes(bn, mt, kb) + 1024 + 256;
+  return tma_stages(bn, mt, kb) * tma_stage_bytes(bn, mt, kb) + (kb == WKB ? 0 : STG_BYTES) + 1024 + 256;
 }
 
 struct Params {
   CUtensorMap ta;          // im2col map of the gathered activation (X or dY)
   CUtensorMap tb;          // tiled map of the other operand (W_bf16, Wt_bf16 or dY)
+  CUtensorMap tc;          // tstore: tiled map of the bf16 output rows (boxes of 32 rows × 64 columns, SWIZZLE_128B)
+  int tstore;              // 1: the epilogue stores through shared memory with TMA (row-contiguous output)
   void* out;               // bf16 [M][N] rows, or fp32 wgrad partials [z][M][N]
   int nst;                 // fprop/dgrad: stored columns (row stride) when N is zero-padded; 0 = N
   int accumulate;          // out = rnd(acc + out)
@@ -92,7 +96,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
   constexpr uint32_t TCOLS = 2 * MT * BN;   // two accumulator sets of MT tiles × BN columns
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + NST * STAGE);
+  uint8_t* stg = smem + NST * STAGE;   // epilogue staging (fprop / dgrad)
+  uint64_t* full = (uint64_t*)(stg + (MODE == WGRAD ? 0 : STG_BYTES));
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
@@ -289,7 +294,67 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
     // ------------------------------------------------------------ epilogue (warps 2-5)
     const int q = warp & 3;            // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
-    uint32_t lt = 0;
+    uint32_t lt = 0, sc = 0;
+    // TMA-store epilogue: the warp's 32 rows × 64 columns go to a SWIZZLE_128B
+    // staging box (row r's 16-byte chunk c at r·128 + (c ^ r % 8)·16: the
+    // rows' stores spread over all banks) and one lane stores the box with
+    // TMA — whole 128-byte row segments instead of 32 rows × 16 bytes per
+    // instruction
+    if (MODE != WGRAD && P.tstore) {
+      for (int u = u0; u < units; u += ustep, ++lt) {
+        int mt, nt, z, kb0, nk;
+        unit_of(u, mt, nt, z, kb0, nk);
+        const uint32_t buf = lt & 1;
+        mbar_wait(&tfull[buf], (lt >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          const int row0 = ((mt * MT + t) * CG + (int)rank) * BM + q * 32;
+#pragma unroll
+          for (int j0 = 0; j0 < BN; j0 += 64, ++sc) {
+            uint32_t v0[32], v1[32];
+            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (buf * MT + t) * BN + j0;
+            TMEM_LD32(ta, v0);
+            TMEM_LD32(ta + 32, v1);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");   // this buffer's last store read
+            __syncwarp();
+            const uint32_t sb = smem_u32(stg) + (uint32_t)(q * 2 + (sc & 1)) * 4096u;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              uint32_t w[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const uint32_t lo = c < 4 ? v0[c * 8 + 2 * e] : v1[(c - 4) * 8 + 2 * e];
+                const uint32_t hi = c < 4 ? v0[c * 8 + 2 * e + 1] : v1[(c - 4) * 8 + 2 * e + 1];
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(nk ? __uint_as_float(lo) : 0.f, nk ? __uint_as_float(hi) : 0.f);
+                w[e] = *reinterpret_cast<uint32_t*>(&h2);
+              }
+              asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sb + lane * 128 + ((c ^ (lane & 7)) << 4)),
+                           "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                           : "memory");
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if (row0 < P.M && nt * BN + j0 < (P.nst ? P.nst : P.N))
+                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&P.tc),
+                             "r"(sb), "r"(nt * BN + j0), "r"(row0)
+                             : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2) mbar_arrive_cluster(mapa(smem_u32(&tempty[buf]), 0));
+          else mbar_arrive(&tempty[buf]);
+        }
+      }
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      __syncwarp();
+    } else
     for (int u = u0; u < units; u += ustep, ++lt) {
       int mt, nt, z, kb0, nk;
       unit_of(u, mt, nt, z, kb0, nk);
@@ -433,6 +498,20 @@ Status make_tiled(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows
   return r == CUDA_SUCCESS ? Status::ok() : encode_fail(r, "cuTensorMapEncodeTiled");
 }
 
+bool tstore_enabled() {
+  const char* e = std::getenv("OC_CONV_TSTORE");
+  return !(e && e[0] == '0');
+}
+// the TMA-store epilogue for row-contiguous bf16 outputs that are not accumulated
+Status set_tstore(Params& P, void* out, int rows, int cols_stored, bool ok) {
+  P.tstore = 0;
+  if (!ok || !tstore_enabled() || cols_stored % 8) return Status::ok();
+  Status st = make_tiled(&P.tc, out, (uint64_t)cols_stored, (uint64_t)rows, 32);
+  if (!st.good()) return st;
+  P.tstore = 1;
+  return Status::ok();
+}
+
 void fill(Params& P) {
   P.fQ.init(P.Qd);
   P.fP.init(P.Pd);
@@ -563,6 +642,7 @@ bool conv_tma_enabled() {
 bool conv_tma_ok(const ConvGeom& g, int mode) {
   if (!conv_tma_enabled()) return false;
   if (g.pad > 127 || g.R > 64 || g.S > 64 || g.st > 8) return false;
+  if (g.nopadh && mode == DGRAD) return false;
   if (mode == FPROP) return g.K % 64 == 0 && (g.C % 64 == 0 || g.C == 8 || g.C == 16);
   if (mode == DGRAD) return g.C % 64 == 0 && g.K % 64 == 0;
   return (g.C % 64 == 0 || g.C == 16) && g.K % 64 == 0;
@@ -574,7 +654,8 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
                       __nv_bfloat16* y, bool accumulate, int nst) {
   const int nch = g.C % 64 == 0 ? 0 : g.C;     // 8 or 16: narrow pixels, one tap per box
   Params P{};
-  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, nch ? nch : 64, BM, g.P, g.Q, g.st, g.pad, g.pad,
+  const int padh = g.nopadh ? 0 : g.pad;
+  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, nch ? nch : 64, BM, g.P, g.Q, g.st, padh, g.pad,
                           nch == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE
                                    : (nch == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B));
   if (!st.good()) return st;
@@ -585,6 +666,8 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   P.out = y;
   P.nst = nst;
   P.accumulate = accumulate ? 1 : 0;
+  st = set_tstore(P, y, g.N * g.P * g.Q, nst ? nst : g.K, !accumulate);
+  if (!st.good()) return st;
   P.M = g.N * g.P * g.Q;
   P.N = g.K;
   P.num_m = (P.M + BM - 1) / BM;
@@ -594,7 +677,8 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   P.Pd = g.P;
   P.Qd = g.Q;
   P.st = g.st;
-  P.padh = P.padw = g.pad;
+  P.padh = padh;
+  P.padw = g.pad;
   P.R = g.R;
   P.S = g.S;
   P.Cr = g.C;
@@ -640,6 +724,8 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
       P.out = dx;
       P.nst = nst;
       P.accumulate = accumulate ? 1 : 0;
+      st = set_tstore(P, dx, g.N * Hp * Wp, nst ? nst : g.C, !accumulate && g.st == 1);
+      if (!st.good()) return st;
       P.M = g.N * Hp * Wp;
       P.N = g.C;
       P.num_m = (P.M + BM - 1) / BM;
@@ -674,7 +760,8 @@ Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
                       int splits, int kb_per_split, bool accumulate) {
   Params P{};
   const int nch = g.C == 16 ? 16 : 0;
-  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, nch ? 16 : 64, WKB, g.P, g.Q, g.st, g.pad, g.pad,
+  const int padh = g.nopadh ? 0 : g.pad;
+  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, nch ? 16 : 64, WKB, g.P, g.Q, g.st, padh, g.pad,
                           nch ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B);
   if (!st.good()) return st;
   const int BN = g.K % 128 == 0 ? 128 : 64;
@@ -693,7 +780,8 @@ Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   P.Pd = g.P;
   P.Qd = g.Q;
   P.st = g.st;
-  P.padh = P.padw = g.pad;
+  P.padh = padh;
+  P.padw = g.pad;
   P.R = g.R;
   P.S = g.S;
   P.Cr = g.C;

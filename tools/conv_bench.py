@@ -21,6 +21,15 @@ SHAPES = {  # name: N, H, W, C, K, R, stride, pad
     "l3_3x3": (256, 14, 14, 256, 256, 3, 1, 1),
     "l4_3x3": (256, 7, 7, 512, 512, 3, 1, 1),
 }
+# ResNet-50 bottleneck 1x1 shapes (b = 256): short reductions, wide outputs
+R50 = {
+    "r50_1x1_64_256": (256, 56, 56, 64, 256, 1, 1, 0),
+    "r50_1x1_256_64": (256, 56, 56, 256, 64, 1, 1, 0),
+    "r50_1x1_1024_256": (256, 14, 14, 1024, 256, 1, 1, 0),
+    "r50_1x1_512_2048": (256, 7, 7, 512, 2048, 1, 1, 0),
+    "r50_3x3_128": (256, 28, 28, 128, 128, 3, 1, 1),
+}
+SHAPES_ALL = {**SHAPES, **R50}
 
 
 def graph(kind, s):
@@ -60,7 +69,7 @@ def main():
         for kind in a.passes.split(","):
             if name.startswith("stem") and kind == "dgrad":
                 continue
-            doc, total, flops = graph(kind, SHAPES[name])
+            doc, total, flops = graph(kind, SHAPES_ALL[name])
             st = OutOfCoreStep(doc, total, 0, mode="best", phys_bytes=4096)
             rng = np.random.default_rng(0)
             for vname, t in st.dev.items():
