@@ -512,9 +512,13 @@ bool s2d_enabled() {
   }
   return env == 1;
 }
+// opt-in (OC_CONV_FOLD=1): measured on B200 at ResNet-18 b=256 the folded
+// stem runs at the speed of the 16-channel one (both gathers are L2→SM bound
+// at ~5.5 TB/s; the fold only moves the 16× re-read from 32-byte to 128-byte
+// rows) while writing 4× the workspace bytes
 bool fold_enabled() {
   const char* e = std::getenv("OC_CONV_FOLD");
-  return !(e && e[0] == '0') && conv_tma_enabled();
+  return e && e[0] == '1' && conv_tma_enabled();
 }
 Narrow narrow_of(const ConvGeom& g) {
   Narrow n{g.C % 8 != 0, false, false, g, g, g.N, 0};
@@ -565,14 +569,15 @@ __global__ void pad_pixels(int64_t rows, int C, int C8, const __nv_bfloat16* __r
 }
 
 // X [n][H][W][C] -> X' [n][H/2][W/2][16]
-__global__ void s2d_pixels(int64_t pix, int H2, int W2, int C, const __nv_bfloat16* __restrict__ x,
+// grid: x over v, y over (n, u) — no 64-bit index division
+__global__ void s2d_pixels(int rows, int H2, int W2, int C, const __nv_bfloat16* __restrict__ x,
                            __nv_bfloat16* __restrict__ out) {
   const unsigned short* xs = reinterpret_cast<const unsigned short*>(x);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pix; i += (int64_t)gridDim.x * blockDim.x) {
-    const int v = (int)(i % W2);
-    const int64_t t = i / W2;
-    const int u = (int)(t % H2);
-    const int64_t n = t / H2;
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int y = blockIdx.y; v < W2 && y < rows; y += gridDim.y) {
+    const int u = y % H2;
+    const int64_t n = y / H2;
+    const int64_t i = (int64_t)y * W2 + v;
     uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
     for (int ab = 0; ab < 4; ++ab) {
       const int64_t src = ((n * 2 * H2 + 2 * u + (ab >> 1)) * 2 * W2 + 2 * v + (ab & 1)) * C;
@@ -591,14 +596,15 @@ __global__ void s2d_pixels(int64_t pix, int H2, int W2, int C, const __nv_bfloat
 // (rows 2u, 2u+1, columns 2v, 2v+1: two contiguous 12-byte runs, 4-byte
 // aligned) once and stores it as chunk i of the four X'' pixels (n, u+c2−i, v);
 // the virtual rows u < 0 and u >= H/2 store the zero chunks of the padding
-__global__ void fold_pixels(int64_t threads, int P, int H2, int W2, int c2, const __nv_bfloat16* __restrict__ x,
+// grid: x over v (128 threads per block), y over (n, virtual row) — no 64-bit
+// index division in the hot loop
+__global__ void fold_pixels(int rows, int P, int H2, int W2, int c2, const __nv_bfloat16* __restrict__ x,
                             __nv_bfloat16* __restrict__ out) {
   const int U = H2 + 4 - 1;   // virtual rows −c2 .. H2 + 3 − c2 − 1
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < threads; q += (int64_t)gridDim.x * blockDim.x) {
-    const int v = (int)(q % W2);
-    int64_t t = q / W2;
-    const int u = (int)(t % U) - c2;
-    const int64_t n = t / U;
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int y = blockIdx.y; v < W2 && y < rows; y += gridDim.y) {
+    const int u = y % U - c2;
+    const int64_t n = y / U;
     uint4 lo = make_uint4(0u, 0u, 0u, 0u), hi = lo;
     if (u >= 0 && u < H2) {
       const uint32_t* r0 = reinterpret_cast<const uint32_t*>(x + ((n * 2 * H2 + 2 * u) * 2 * W2 + 2 * v) * 3);
@@ -622,12 +628,13 @@ Status pad_slice(OpArgs& a, const Narrow& nw, int64_t n0, int64_t nn, const __nv
   const ConvGeom& g0 = nw.g0;
   const __nv_bfloat16* xs = x + n0 * g0.H * g0.W * g0.C;
   if (nw.fold) {
-    const int64_t threads = nn * (g0.H / 2 + 3) * nw.gk.W;
-    fold_pixels<<<grid_for(threads, 256, 2), 256, 0, a.stream>>>(threads, nw.gk.H, g0.H / 2, nw.gk.W, nw.gk.pad, xs,
-                                                                 buf);
+    const int rows = (int)(nn * (g0.H / 2 + 3));
+    const dim3 grid((nw.gk.W + 127) / 128, (unsigned)std::min(rows, 65535));
+    fold_pixels<<<grid, 128, 0, a.stream>>>(rows, nw.gk.H, g0.H / 2, nw.gk.W, nw.gk.pad, xs, buf);
   } else if (nw.s2d) {
-    const int64_t pix = nn * nw.gk.H * nw.gk.W;
-    s2d_pixels<<<grid_for(pix, 256, 2), 256, 0, a.stream>>>(pix, nw.gk.H, nw.gk.W, g0.C, xs, buf);
+    const int rows = (int)(nn * nw.gk.H);
+    const dim3 grid((nw.gk.W + 127) / 128, (unsigned)std::min(rows, 65535));
+    s2d_pixels<<<grid, 128, 0, a.stream>>>(rows, nw.gk.H, nw.gk.W, g0.C, xs, buf);
   } else {
     const int64_t rows = nn * g0.H * g0.W;
     pad_pixels<<<grid_for(rows, 256, 2), 256, 0, a.stream>>>(rows, g0.C, nw.gk.C, xs, buf);
@@ -655,23 +662,24 @@ __global__ void weight_bf16_s2d(const float* __restrict__ w, __nv_bfloat16* __re
 }
 
 // dW[k][r][s][c] = Σ_z part[z][(i,j,(a,b,c))][k], the (i,j,a,b) holding filter tap (r,s)
+// (thread index k-fastest: the split partials [z][row][k] are read coalesced)
 __global__ void wgrad_reduce_s2d(int splits, int RSC2, int K, const float* __restrict__ part, float* __restrict__ dw,
                                  int R, int S, int C, int S2, int c2, int pad, int fold) {
-  const int64_t n = (int64_t)K * R * S * C;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e % C);
-    int64_t t = e / C;
-    const int s = (int)(t % S);
-    t /= S;
-    const int r = (int)(t % R);
-    const int k = (int)(t / R);
+  const int n = K * R * S * C;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int k = e % K;
+    int t = e / K;
+    const int c = t % C;
+    t /= C;
+    const int s = t % S;
+    const int r = t / S;
     const int tr = r + 2 * c2 - pad, ts = s + 2 * c2 - pad;
     const int row = (fold ? (ts >> 1) * 64 + (tr >> 1) * 16 : ((tr >> 1) * S2 + (ts >> 1)) * 16) +
                     ((tr & 1) * 2 + (ts & 1)) * C + c;
     float acc = 0.f;
 #pragma unroll 8
     for (int z = 0; z < splits; ++z) acc += part[((int64_t)z * RSC2 + row) * K + k];
-    dw[e] = acc;
+    dw[(((int64_t)k * R + r) * S + s) * C + c] = acc;
   }
 }
 

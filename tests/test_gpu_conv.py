@@ -165,3 +165,16 @@ def test_conv_tiles_dgrad(g, tile, monkeypatch):
         pytest.skip("N tile does not divide C")
     monkeypatch.setenv("OC_CONV_TILE", tile)
     test_conv_dgrad(g, True)
+
+
+# the folded stem (OC_CONV_FOLD=1): space-to-depth pixels with the four
+# vertical taps in the channels, a 1x4 conv over 64-channel pixels
+FOLD_SHAPES = [(2, 16, 14, 3, 64, 7, 2, 3), (3, 18, 12, 3, 128, 7, 2, 3, 2)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("g", FOLD_SHAPES)
+def test_conv_folded_stem(g, monkeypatch):
+    monkeypatch.setenv("OC_CONV_FOLD", "1")
+    test_conv_fwd(g)
+    test_conv_wgrad(g)
