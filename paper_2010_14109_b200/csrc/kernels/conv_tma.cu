@@ -88,7 +88,7 @@ __device__ __forceinline__ void base_of(const Params& P, int pix, int& w, int& h
 // own A rows and B columns [BN/2·r, BN/2·(r+1)), rank 0 issues 256 × BN MMAs.
 template <int MODE, int BN, int NCH, int MT, int CG = 1>
 __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_constant__ Params P) {
-  static_assert(CG == 1 || (MODE != WGRAD && NCH == 0), "CTA pairs: fprop / dgrad over 64-channel pixels");
+  static_assert(CG == 1 || (NCH == 0 && (MODE != WGRAD || BN / CG >= 64)), "CTA pairs: 64-channel pixels; wgrad: whole 64-column B atoms per CTA");
   constexpr int KB = kblock(MODE);              // K extent of a stage (elements, or wgrad pixels)
   constexpr int ATOM = KB * 128;                 // wgrad: one 64-wide MN-major atom column
   constexpr int NST = tma_stages(BN / CG, MT, KB);
@@ -192,18 +192,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
             int pw, ph, pn;
             base_of(P, kb * KB, pw, ph, pn);
             // 64-row (tap, 64-channel) blocks of (r,s,c) inside the M range
-            const int rb0 = mt * MT * 2;
-            int nrb = (P.M + 63) / 64 - rb0;
-            nrb = nrb < 2 * MT ? nrb : 2 * MT;
-            mbar_expect_tx(&full[sg], B_BYTES + nrb * ATOM);
-            for (int j = 0; j < nrb; ++j) {
-              const int blk = rb0 + j;
-              const int tap = (int)P.fCb.div((uint32_t)blk), cb = blk - tap * (P.Cr / 64);
-              const int r = (int)P.fS.div((uint32_t)tap), s = tap - r * P.S;
-              tma_load_im2col(a + j * ATOM, &P.ta, &full[sg], cb * 64, pw, ph, pn, (uint16_t)s, (uint16_t)r);
-            }
+            // (pair: this CTA's 128 rows, and half of the BN columns)
+            auto nrb_of = [&](int rk) {
+              const int n = (P.M + 63) / 64 - (mt * MT * CG + rk) * 2;
+              return n < 0 ? 0 : (n < 2 * MT ? n : 2 * MT);
+            };
+            const int rb0 = (mt * MT * CG + (int)rank) * 2;
+            const int nrb = nrb_of((int)rank);
+            if (CG == 2) {
+              const uint32_t fb = mapa(smem_u32(&full[sg]), 0);
+              if (rank == 0) mbar_expect_tx(&full[sg], 2 * B_BYTES + (nrb_of(0) + nrb_of(1)) * ATOM);
+              for (int j = 0; j < nrb; ++j) {
+                const int blk = rb0 + j;
+                const int tap = (int)P.fCb.div((uint32_t)blk), cb = blk - tap * (P.Cr / 64);
+                const int r = (int)P.fS.div((uint32_t)tap), s = tap - r * P.S;
+                tma_load_im2col_pair(a + j * ATOM, &P.ta, fb, cb * 64, pw, ph, pn, (uint16_t)s, (uint16_t)r);
+              }
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * ATOM, &P.tb, &full[sg], nt * BN + j * 64, kb * KB);
+              for (int j = 0; j < BN / CG / 64; ++j)
+                tma_load_2d_pair(b + j * ATOM, &P.tb, fb, nt * BN + (int)rank * (BN / CG) + j * 64, kb * KB);
+            } else {
+              mbar_expect_tx(&full[sg], B_BYTES + nrb * ATOM);
+              for (int j = 0; j < nrb; ++j) {
+                const int blk = rb0 + j;
+                const int tap = (int)P.fCb.div((uint32_t)blk), cb = blk - tap * (P.Cr / 64);
+                const int r = (int)P.fS.div((uint32_t)tap), s = tap - r * P.S;
+                tma_load_im2col(a + j * ATOM, &P.ta, &full[sg], cb * 64, pw, ph, pn, (uint16_t)s, (uint16_t)r);
+              }
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * ATOM, &P.tb, &full[sg], nt * BN + j * 64, kb * KB);
+            }
           } else if (NCH) {
             // 64 / NCH taps per K-block, one box of 128 pixels × NCH channels each
             constexpr int TPB = 64 / (NCH ? NCH : 64), BOX = BM * NCH * 2;
@@ -765,6 +783,13 @@ Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
                           nch ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B);
   if (!st.good()) return st;
   const int BN = g.K % 128 == 0 ? 128 : 64;
+  // CTA pairs over 256 (r,s,c) rows × 256 columns (half of B per CTA) when K
+  // allows: measured at ResNet-18 b=256 l3/l4 797 -> 937 / 732 -> 839 TF/s;
+  // 128-column pairs were slower than single CTAs (l2: 781 -> 644), so they
+  // are only forced (OC_WGRAD_CG=2, tests).  OC_WGRAD_CG=1 keeps single CTAs.
+  const char* ecg = std::getenv("OC_WGRAD_CG");
+  const bool force = ecg && ecg[0] == '2', off = ecg && ecg[0] == '1';
+  const int pbn = (nch || off) ? 0 : (g.K % 256 == 0 ? 256 : ((force && g.K % 128 == 0) ? 128 : 0));
   st = make_tiled(&P.tb, dy, (uint64_t)g.K, (uint64_t)g.N * g.P * g.Q, WKB);
   if (!st.good()) return st;
   P.out = part;
@@ -787,6 +812,11 @@ Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   P.Cr = g.C;
   fill(P);
   if (nch) return BN == 128 ? launch<WGRAD, 128, 16>(a, P) : launch<WGRAD, 64, 16>(a, P);
+  if (pbn == 256) {
+    P.num_n = g.K / 256;
+    return launch_mt<WGRAD, 256, 0, 1, 2>(a, P);
+  }
+  if (pbn == 128) return launch_mt<WGRAD, 128, 0, 1, 2>(a, P);
   return BN == 128 ? launch<WGRAD, 128, 0>(a, P) : launch<WGRAD, 64, 0>(a, P);
 }
 

@@ -178,3 +178,21 @@ def test_conv_folded_stem(g, monkeypatch):
     monkeypatch.setenv("OC_CONV_FOLD", "1")
     test_conv_fwd(g)
     test_conv_wgrad(g)
+
+
+# weight gradient on CTA pairs (K divisible by 128: 256 (r,s,c) rows × 128 / 256
+# columns per pair) against single CTAs (OC_WGRAD_CG=1)
+WGRAD_PAIR_SHAPES = [
+    (2, 9, 7, 64, 256, 3, 1, 1),      # M = 576: the second CTA of the last pair holds 64 rows
+    (3, 11, 10, 128, 128, 3, 2, 1),
+    (2, 12, 9, 256, 512, 1, 2, 0),    # M = 256: one pair
+    (2, 7, 7, 192, 256, 3, 1, 1),     # M = 1728
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cg", ["2", "1"])
+@pytest.mark.parametrize("g", WGRAD_PAIR_SHAPES)
+def test_conv_wgrad_pairs(g, cg, monkeypatch):
+    monkeypatch.setenv("OC_WGRAD_CG", cg)
+    test_conv_wgrad(g)
