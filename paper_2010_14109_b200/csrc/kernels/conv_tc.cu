@@ -445,7 +445,10 @@ using namespace tc;
 
 bool conv_tma_ok(const ConvGeom& g, int mode);
 Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* wb, int kpad,
-                      __nv_bfloat16* y, bool accumulate, int nst = 0);
+                      __nv_bfloat16* y, bool accumulate, int nst = 0, float* stat_part = nullptr,
+                      int* stat_slots = nullptr);
+constexpr int kStatSlotsMax = 148 * 4;   // epilogue statistics slots per launch (CTA × epilogue warp)
+Status bn_stats_from_parts(OpArgs& a, int nslots, int64_t rows, int C, const float* part, float* stat);
 Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* wt,
                       __nv_bfloat16* dx, bool accumulate, int nst = 0);
 Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
@@ -837,14 +840,26 @@ size_t conv_tc_ws(const ConvGeom& g0, int mode) {
   return align256((size_t)g.K * kpad_of(g) * 2) + nw.slice_bytes;
 }
 
+// partial-sum region of the fused BN statistics: one set of slots per image slice
+size_t conv_tc_stat_ws(const ConvGeom& g0) {
+  const Narrow nw = narrow_of(g0);
+  const int64_t nsl = (g0.N + nw.slice - 1) / nw.slice;
+  return align256((size_t)nsl * kStatSlotsMax * 2 * g0.K * 4);
+}
+
 Status conv_fprop_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y,
-                     bool accumulate) {
+                     bool accumulate, float* stat, bool* stat_done) {
+  if (stat_done) *stat_done = false;
   if (pad_path(g0, FPROP)) return conv_fprop_pad(a, g0, x, w, y, accumulate);
   const Narrow nw = narrow_of(g0);
   const ConvGeom& g = nw.gk;
   __nv_bfloat16* wb = (__nv_bfloat16*)a.ws;
   const int kpad = kpad_of(g);
   __nv_bfloat16* xbuf = (__nv_bfloat16*)((char*)a.ws + align256((size_t)g.K * kpad * 2));
+  // fused statistics: slices append their epilogue slots (part[slot][2][K]) after the conv workspace
+  float* part = stat ? (float*)((char*)a.ws + conv_tc_ws(g0, FPROP)) : nullptr;
+  int nslots = 0;
+  bool fused = stat != nullptr;
   if (nw.s2d)
     weight_bf16_s2d<<<grid_for((int64_t)g.K * kpad, 256, 4), 256, 0, a.stream>>>(
         w, wb, g.K, g0.R, g0.S, g0.C, nw.fold ? 4 : g.R, g.S, g.pad, g0.pad, kpad, nw.fold ? 1 : 0);
@@ -873,14 +888,23 @@ Status conv_fprop_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* x, cons
     P.nkb = kpad / BKE;
     P.accumulate = accumulate ? 1 : 0;
     if (conv_tma_ok(P.g, FPROP)) {
-      Status st = conv_fprop_tma(a, P.g, P.act, wb, kpad, (__nv_bfloat16*)P.out, accumulate);
+      int sl = 0;
+      Status st = conv_fprop_tma(a, P.g, P.act, wb, kpad, (__nv_bfloat16*)P.out, accumulate, 0,
+                                 fused ? part + (size_t)nslots * 2 * g.K : nullptr, fused ? &sl : nullptr);
       if (!st.good()) return st;
+      if (sl == 0) fused = false;
+      nslots += sl;
       continue;
     }
+    fused = false;
     fill_divs(P);
     const dim3 grid((P.M + BM - 1) / BM, g.K / (g.K % 128 == 0 ? 128 : 64), 1);
     Status st = g.K % 128 == 0 ? launch<FPROP, 128>(a, P, grid) : launch<FPROP, 64>(a, P, grid);
     if (!st.good()) return st;
+  }
+  if (fused) {
+    OC_TRY(bn_stats_from_parts(a, nslots, (int64_t)g.N * g.P * g.Q, g.K, part, stat));
+    if (stat_done) *stat_done = true;
   }
   return Status::ok();
 }

@@ -57,6 +57,7 @@ struct Params {
   CUtensorMap tb;          // tiled map of the other operand (W_bf16, Wt_bf16 or dY)
   CUtensorMap tc;          // tstore: tiled map of the bf16 output rows (boxes of 32 rows × 64 columns, SWIZZLE_128B)
   int tstore;              // 1: the epilogue stores through shared memory with TMA (row-contiguous output)
+  float* stat_part;        // tstore + fused BN statistics: part[slot][2][N] (Σy, Σy² of the stored bf16 values)
   void* out;               // bf16 [M][N] rows, or fp32 wgrad partials [z][M][N]
   int nst;                 // fprop/dgrad: stored columns (row stride) when N is zero-padded; 0 = N
   int accumulate;          // out = rnd(acc + out)
@@ -319,6 +320,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
     // TMA — whole 128-byte row segments instead of 32 rows × 16 bytes per
     // instruction
     if (MODE != WGRAD && P.tstore) {
+      // fused BN statistics: the grid is a multiple of num_n, so a CTA's N
+      // block (u mod num_n) is fixed and lane l owns columns 2l, 2l+1 of each
+      // 64-column box for the whole launch (fixed order: bitwise reproducible)
+      float ssum[BN / 64][2], ssq[BN / 64][2];
+#pragma unroll
+      for (int jb = 0; jb < BN / 64; ++jb) ssum[jb][0] = ssum[jb][1] = ssq[jb][0] = ssq[jb][1] = 0.f;
       for (int u = u0; u < units; u += ustep, ++lt) {
         int mt, nt, z, kb0, nk;
         unit_of(u, mt, nt, z, kb0, nk);
@@ -354,6 +361,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
             }
             fence_async_smem();
             __syncwarp();
+            if (P.stat_part) {
+              // column sums of the 32 staged rows (conflict-free: the swizzle
+              // spreads a row's eight 16-byte chunks over all banks); rows past M are zero
+              float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f;
+#pragma unroll 8
+              for (int r = 0; r < 32; ++r) {
+                uint32_t wv;
+                asm volatile("ld.shared.b32 %0, [%1];"
+                             : "=r"(wv)
+                             : "r"(sb + r * 128 + ((((uint32_t)lane >> 2) ^ (uint32_t)(r & 7)) << 4) + (lane & 3) * 4));
+                const float2 f = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wv));
+                s0 += f.x;
+                s1 += f.y;
+                q0 = fmaf(f.x, f.x, q0);
+                q1 = fmaf(f.y, f.y, q1);
+              }
+              ssum[j0 / 64][0] += s0;
+              ssum[j0 / 64][1] += s1;
+              ssq[j0 / 64][0] += q0;
+              ssq[j0 / 64][1] += q1;
+            }
             if (lane == 0) {
               if (row0 < P.M && nt * BN + j0 < (P.nst ? P.nst : P.N))
                 asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&P.tc),
@@ -372,6 +400,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
       }
       if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       __syncwarp();
+      if (P.stat_part && u0 < units) {
+        const int slot = (u0 / P.num_n) * (4 * CG) + (int)rank * 4 + q;
+        const int nt = u0 % P.num_n;
+        float* pp = P.stat_part + (int64_t)slot * 2 * P.N;
+#pragma unroll
+        for (int jb = 0; jb < BN / 64; ++jb) {
+          const int c = nt * BN + jb * 64 + 2 * lane;
+          *reinterpret_cast<float2*>(pp + c) = make_float2(ssum[jb][0], ssum[jb][1]);
+          *reinterpret_cast<float2*>(pp + P.N + c) = make_float2(ssq[jb][0], ssq[jb][1]);
+        }
+      }
     } else
     for (int u = u0; u < units; u += ustep, ++lt) {
       int mt, nt, z, kb0, nk;
@@ -547,7 +586,7 @@ int conv_mt() {
 }
 
 template <int MODE, int BN, int NCH, int MT, int CG = 1>
-Status launch_mt(OpArgs& a, Params P) {
+Status launch_mt(OpArgs& a, Params P, int* stat_slots = nullptr) {
   constexpr int smem = tma_smem(BN / CG, MT, kblock(MODE));
   auto kern = conv_tma_kernel<MODE, BN, NCH, MT, CG>;
   static bool attr = false;
@@ -559,9 +598,16 @@ Status launch_mt(OpArgs& a, Params P) {
   P.num_m = (P.M + BM * MT * CG - 1) / (BM * MT * CG);   // super-tiles of MT × (128·CG) rows
   const int units = P.num_m * P.num_n * (MODE == WGRAD ? P.splits : 1);
   if (units == 0) return Status::ok();
+  int ctas = std::min(units, CG == 1 ? sm_count() : max_pairs());   // CTAs, or pairs
+  if (P.stat_part) {
+    // fused statistics: whole groups of num_n CTAs (pairs), 4·CG slots per group member
+    ctas = ctas / P.num_n * P.num_n;
+    if (ctas == 0) return Status::make(OC_E_INVARIANT, "conv: statistics epilogue needs num_n CTAs");
+    if (stat_slots) *stat_slots = ctas / P.num_n * 4 * CG;
+  }
   if (a.ktimer) a.ktimer->begin(a.stream);
   if (CG == 1) {
-    kern<<<std::min(units, sm_count()), NTHREADS, smem, a.stream>>>(P);
+    kern<<<ctas, NTHREADS, smem, a.stream>>>(P);
   } else {
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[1];
@@ -574,8 +620,7 @@ Status launch_mt(OpArgs& a, Params P) {
     cfg.stream = a.stream;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    const int pairs = std::min(units, max_pairs());
-    cfg.gridDim = dim3(2 * pairs);
+    cfg.gridDim = dim3(2 * ctas);
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, P);
     if (e != cudaSuccess) return cuda_status(e, "conv_tma pair launch");
   }
@@ -587,8 +632,9 @@ Status launch_mt(OpArgs& a, Params P) {
 // wgrad keeps single 128-row tiles: its M = R·S·C is short (e.g. 576) and
 // pairs would pad it further.
 template <int MODE, int BN, int NCH>
-Status launch(OpArgs& a, const Params& P) {
-  return (MODE != WGRAD && conv_mt() == 2) ? launch_mt<MODE, BN, NCH, 2>(a, P) : launch_mt<MODE, BN, NCH, 1>(a, P);
+Status launch(OpArgs& a, const Params& P, int* stat_slots = nullptr) {
+  return (MODE != WGRAD && conv_mt() == 2) ? launch_mt<MODE, BN, NCH, 2>(a, P, stat_slots)
+                                           : launch_mt<MODE, BN, NCH, 1>(a, P, stat_slots);
 }
 
 // Tile shape of the 64-channel fprop / dgrad GEMM (M rows, N columns).
@@ -633,14 +679,14 @@ Tile choose_tile(int M, int N) {
 }
 
 template <int MODE>
-Status launch_tile(OpArgs& a, const Params& P, Tile t) {
+Status launch_tile(OpArgs& a, const Params& P, Tile t, int* ss = nullptr) {
   if (t.cg == 2) {
-    if (t.bn == 256) return launch_mt<MODE, 256, 0, 1, 2>(a, P);
-    if (t.bn == 128) return launch_mt<MODE, 128, 0, 2, 2>(a, P);
-    return launch_mt<MODE, 64, 0, 2, 2>(a, P);
+    if (t.bn == 256) return launch_mt<MODE, 256, 0, 1, 2>(a, P, ss);
+    if (t.bn == 128) return launch_mt<MODE, 128, 0, 2, 2>(a, P, ss);
+    return launch_mt<MODE, 64, 0, 2, 2>(a, P, ss);
   }
-  if (t.mt == 1) return t.bn == 128 ? launch_mt<MODE, 128, 0, 1>(a, P) : launch_mt<MODE, 64, 0, 1>(a, P);
-  return t.bn == 128 ? launch_mt<MODE, 128, 0, 2>(a, P) : launch_mt<MODE, 64, 0, 2>(a, P);
+  if (t.mt == 1) return t.bn == 128 ? launch_mt<MODE, 128, 0, 1>(a, P, ss) : launch_mt<MODE, 64, 0, 1>(a, P, ss);
+  return t.bn == 128 ? launch_mt<MODE, 128, 0, 2>(a, P, ss) : launch_mt<MODE, 64, 0, 2>(a, P, ss);
 }
 
 }  // namespace tma
@@ -668,8 +714,11 @@ bool conv_tma_ok(const ConvGeom& g, int mode) {
 
 // y[M = N·P·Q][K] = im2col(x) · W_bf16[K][kpad]ᵀ
 // nst (optional): the stored output channels when g.K is a zero-padded width
+// stat_part (optional): fused BN statistics of y (TMA-store epilogue only); on
+// return *stat_slots = the slots written (0: not fused, the caller reduces y)
 Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* wb, int kpad,
-                      __nv_bfloat16* y, bool accumulate, int nst) {
+                      __nv_bfloat16* y, bool accumulate, int nst, float* stat_part, int* stat_slots) {
+  if (stat_slots) *stat_slots = 0;
   const int nch = g.C % 64 == 0 ? 0 : g.C;     // 8 or 16: narrow pixels, one tap per box
   Params P{};
   const int padh = g.nopadh ? 0 : g.pad;
@@ -701,9 +750,14 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   P.S = g.S;
   P.Cr = g.C;
   fill(P);
-  if (nch == 8) return BN == 128 ? launch<FPROP, 128, 8>(a, P) : launch<FPROP, 64, 8>(a, P);
-  if (nch == 16) return BN == 128 ? launch<FPROP, 128, 16>(a, P) : launch<FPROP, 64, 16>(a, P);
-  return launch_tile<FPROP>(a, P, tile);
+  int* ss = nullptr;
+  if (stat_part && P.tstore && !nst && !accumulate) {
+    P.stat_part = stat_part;
+    ss = stat_slots;
+  }
+  if (nch == 8) return BN == 128 ? launch<FPROP, 128, 8>(a, P, ss) : launch<FPROP, 64, 8>(a, P, ss);
+  if (nch == 16) return BN == 128 ? launch<FPROP, 128, 16>(a, P, ss) : launch<FPROP, 64, 16>(a, P, ss);
+  return launch_tile<FPROP>(a, P, tile, ss);
 }
 
 // dgrad, one launch per output phase (h mod st, w mod st) over that phase's

@@ -19,7 +19,9 @@ namespace oc {
 bool conv_tc_ok(const ConvGeom& g, int mode);
 size_t conv_tc_ws(const ConvGeom& g, int mode);
 Status conv_fprop_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y,
-                     bool accumulate);
+                     bool accumulate, float* stat = nullptr, bool* stat_done = nullptr);
+size_t conv_tc_stat_ws(const ConvGeom& g);
+Status bn_stats_of(OpArgs& a, int64_t rows, int C, const void* y, bool f32, float* stat);
 Status conv_dgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const float* w, __nv_bfloat16* dx,
                      bool accumulate);
 Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* x, float* dw);
@@ -66,9 +68,25 @@ Status wgrad(OpArgs& a, const ConvGeom& g, const void* dy, const void* x, float*
   return conv_wgrad_simt<__nv_bfloat16>(a, g, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, dw);
 }
 
-enum { CF_X, CF_W, CF_Y };
+enum { CF_X, CF_W, CF_Y, CF_STAT };
+// attrs.bn_stat (role "stat"): also produce the batch statistics [μ; rstd] of y
+// for the BN that consumes it — from the tensor-core epilogue's per-channel
+// partial sums when that path ran (no extra pass over y), else by the BN
+// reduction over y
 Status conv_fwd(OpArgs& a) {
-  return fprop(a, conv_geom(a), a.p(CF_X), (const float*)a.p(CF_W), a.p(CF_Y), Ab(a, "accumulate"));
+  const ConvGeom g = conv_geom(a);
+  const bool acc = Ab(a, "accumulate");
+  float* stat = (float*)a.p(CF_STAT);
+  if (!stat) return fprop(a, g, a.p(CF_X), (const float*)a.p(CF_W), a.p(CF_Y), acc);
+  bool done = false;
+  if (!f32(a) && !force_simt(&a) && conv_tc_ok(g, 0) && !acc) {
+    OC_TRY(conv_fprop_tc(a, g, (const __nv_bfloat16*)a.p(CF_X), (const float*)a.p(CF_W), (__nv_bfloat16*)a.p(CF_Y),
+                         false, stat, &done));
+  } else {
+    OC_TRY(fprop(a, g, a.p(CF_X), (const float*)a.p(CF_W), a.p(CF_Y), acc));
+  }
+  if (!done) OC_TRY(bn_stats_of(a, (int64_t)g.N * g.P * g.Q, g.K, a.p(CF_Y), f32(a), stat));
+  return Status::ok();
 }
 enum { CD_DY, CD_W, CD_DX };
 Status conv_dgrad(OpArgs& a) {
@@ -91,7 +109,10 @@ Status convT_dgrad(OpArgs& a) {
 }
 Status convT_wgrad(OpArgs& a) { return wgrad(a, conv_geom(a), a.p(CW_X), a.p(CW_DY), (float*)a.p(CW_DW)); }
 
-size_t ws_fwd(const JVal& at) { return conv_tc_ws(conv_geom(at), 0); }
+size_t ws_fwd(const JVal& at) {
+  const ConvGeom g = conv_geom(at);
+  return conv_tc_ws(g, 0) + (at.getb("bn_stat") ? conv_tc_stat_ws(g) : 0);
+}
 size_t ws_dgrad(const JVal& at) { return conv_tc_ws(conv_geom(at), 1); }
 size_t ws_wgrad(const JVal& at) {
   ConvGeom g = conv_geom(at);
@@ -100,7 +121,7 @@ size_t ws_wgrad(const JVal& at) {
 
 }  // namespace
 
-extern const OpDesc kConvFwd{"conv_fwd", {"x", "w", "y"}, conv_fwd, ws_fwd};
+extern const OpDesc kConvFwd{"conv_fwd", {"x", "w", "y", "stat"}, conv_fwd, ws_fwd};
 extern const OpDesc kConvDgrad{"conv_dgrad", {"dy", "w", "dx"}, conv_dgrad, ws_dgrad};
 extern const OpDesc kConvWgrad{"conv_wgrad", {"dy", "x", "dw"}, conv_wgrad, ws_wgrad};
 extern const OpDesc kConvTFwd{"convT_fwd", {"x", "w", "y"}, convT_fwd, ws_dgrad};

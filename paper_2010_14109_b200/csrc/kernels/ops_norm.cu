@@ -157,7 +157,8 @@ Status bn_fwd_t(OpArgs& a) {
   const int64_t rows = A(a, "rows");
   const int C = (int)A(a, "C");
   auto y = (const T*)a.p(BF_Y);
-  OC_TRY(batch_stats<T>(a, rows, C, y, (float*)a.p(BF_STAT)));
+  // attrs.stat_in: the producing conv already wrote μ, rstd (fused statistics epilogue)
+  if (!Ab(a, "stat_in")) OC_TRY(batch_stats<T>(a, rows, C, y, (float*)a.p(BF_STAT)));
   bn_apply_fwd<T><<<rowgroup_blocks(rows, C), 256, 0, a.stream>>>(rows, C, y, (const float*)a.p(BF_STAT),
                                                                   (const float*)a.p(BF_GAMMA),
                                                                   (const float*)a.p(BF_BETA), (const T*)a.p(BF_RES),
@@ -405,7 +406,7 @@ template <typename T>
 Status bn_relu_pool_fwd_t(OpArgs& a) {
   PoolGeom g = geom(a);
   auto y = (const T*)a.p(RP_Y);
-  OC_TRY(batch_stats<T>(a, (int64_t)g.N * g.H * g.W, g.C, y, (float*)a.p(RP_STAT)));
+  if (!Ab(a, "stat_in")) OC_TRY(batch_stats<T>(a, (int64_t)g.N * g.H * g.W, g.C, y, (float*)a.p(RP_STAT)));
   const int64_t total = (int64_t)g.N * g.P * g.Q * (g.C / 8);
   bn_relu_pool<T><<<grid_for(total, 256, 2), 256, 0, a.stream>>>(g, y, (const float*)a.p(RP_STAT),
                                                                  (const float*)a.p(RP_GAMMA),
@@ -904,6 +905,20 @@ OC_DT_DISPATCH(maxpool_bwd)
 OC_DT_DISPATCH(softmax_ce_pix)
 
 }  // namespace
+
+// BN batch statistics for a producer op (conv_fwd with attrs.bn_stat): from the
+// partial sums its epilogue wrote (part[slot][2][C], Σy and Σy² of the stored
+// bf16 values), or — when the conv ran on a path without that epilogue — the
+// usual two-level reduction over y
+Status bn_stats_from_parts(OpArgs& a, int nslots, int64_t rows, int C, const float* part, float* stat) {
+  stats_finalize<<<(C + 7) / 8, 256, 0, a.stream>>>(nslots, rows, C, part, stat);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+Status bn_stats_of(OpArgs& a, int64_t rows, int C, const void* y, bool f32, float* stat) {
+  return f32 ? batch_stats<float>(a, rows, C, (const float*)y, stat)
+             : batch_stats<__nv_bfloat16>(a, rows, C, (const __nv_bfloat16*)y, stat);
+}
 
 extern const OpDesc kAddFwd{"add_fwd", {"a", "b", "out"}, add_fwd, nullptr};
 extern const OpDesc kMaxpoolFwd{"maxpool_fwd", {"x", "out", "idx"}, maxpool_fwd, nullptr};

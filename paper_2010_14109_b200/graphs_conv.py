@@ -54,6 +54,15 @@ def build_convnet(spec, params="pinned", inputs="host"):
                 and nxt["in"] == lay["out"] and consumers[lay["out"]] == [nxt["name"]]:
             fused_pool[lay["name"]] = nxt
     skip = {p["name"] for p in fused_pool.values()}
+    # a bn whose input is a plain conv's output gets its batch statistics from
+    # that conv (conv_fwd attrs.bn_stat: the tensor-core epilogue sums Σy, Σy²
+    # of the stored values per channel, so the bn skips its reduction pass)
+    conv_out = {lay["out"]: lay["name"] for lay in layers if lay["type"] == "conv" and not lay.get("in2")}
+    bn_of_conv = {}
+    if DT == "bf16" and spec.get("fused_bn_stats", True):
+        for lay in layers:
+            if lay["type"] == "bn" and lay["in"] in conv_out:
+                bn_of_conv[conv_out[lay["in"]]] = lay["name"]
 
     t = {"x": x}       # tensor -> variable holding it
     stat, idx, saved_out = {}, {}, {}
@@ -69,8 +78,15 @@ def build_convnet(spec, params="pinned", inputs="host"):
                      "stride": lay["stride"],
                      "pad": lay["pad"], "P": Pq, "Q": Qq}
             lay["_attrs"] = attrs
-            b.fn(f"fwd.{nm}", "conv_fwd", {"x": t[lay["in"]], "w": P[nm + ".W"], "y": t[lay["out"]]}, attrs,
-                 [t[lay["in"]], P[nm + ".W"]], [t[lay["out"]]])
+            if nm in bn_of_conv:
+                bnm = bn_of_conv[nm]
+                stat[bnm] = b.var(f"stat.{bnm}", 2 * K * F32, shape=[2, K], dtype="f32")
+                b.fn(f"fwd.{nm}", "conv_fwd",
+                     {"x": t[lay["in"]], "w": P[nm + ".W"], "y": t[lay["out"]], "stat": stat[bnm]},
+                     dict(attrs, bn_stat=True), [t[lay["in"]], P[nm + ".W"]], [t[lay["out"]], stat[bnm]])
+            else:
+                b.fn(f"fwd.{nm}", "conv_fwd", {"x": t[lay["in"]], "w": P[nm + ".W"], "y": t[lay["out"]]}, attrs,
+                     [t[lay["in"]], P[nm + ".W"]], [t[lay["out"]]])
             if lay.get("in2"):
                 # conv over [in, in2] without materialising the concat: a second conv
                 # accumulates into y (y = rnd(y + conv(in2, W2)), Z23)
@@ -99,7 +115,11 @@ def build_convnet(spec, params="pinned", inputs="host"):
                  lay["_attrs"], [t[lay["in"]]], [t[lay["out"]], idx[nm]])
         elif ty == "bn":
             C = shapes[lay["in"]][-1]
-            stat[nm] = b.var(f"stat.{nm}", 2 * C * F32, shape=[2, C], dtype="f32")
+            stat_in = nm in stat   # produced by the conv (bn_stat)
+            if not stat_in:
+                stat[nm] = b.var(f"stat.{nm}", 2 * C * F32, shape=[2, C], dtype="f32")
+            sin = [stat[nm]] if stat_in else []
+            sout = [] if stat_in else [stat[nm]]
             if nm in fused_pool:
                 pool = fused_pool[nm]
                 H, W, _ = shapes[lay["in"]]
@@ -111,10 +131,11 @@ def build_convnet(spec, params="pinned", inputs="host"):
                          "pad": pool["pad"],
                          "P": Pq, "Q": Qq}
                 lay["_attrs"] = attrs
-                ins = [t[lay["in"]], P[nm + ".gamma"], P[nm + ".beta"]]
+                ins = [t[lay["in"]], P[nm + ".gamma"], P[nm + ".beta"]] + sin
                 b.fn(f"fwd.{nm}+{pool['name']}", "bn_relu_pool_fwd",
                      {"y": t[lay["in"]], "stat": stat[nm], "gamma": P[nm + ".gamma"], "beta": P[nm + ".beta"],
-                      "out": t[pool["out"]], "idx": idx[nm]}, attrs, ins, [stat[nm], t[pool["out"]], idx[nm]])
+                      "out": t[pool["out"]], "idx": idx[nm]}, dict(attrs, stat_in=stat_in), ins,
+                     sout + [t[pool["out"]], idx[nm]])
             else:
                 t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
                 rows = Nb * int(np.prod(shapes[lay["in"]][:-1]))
@@ -123,8 +144,8 @@ def build_convnet(spec, params="pinned", inputs="host"):
                 lay["_attrs"] = attrs
                 b.fn(f"fwd.{nm}", "bn_fwd",
                      {"y": t[lay["in"]], "stat": stat[nm], "gamma": P[nm + ".gamma"], "beta": P[nm + ".beta"],
-                      "res": res, "out": t[lay["out"]]}, attrs,
-                     [t[lay["in"]], P[nm + ".gamma"], P[nm + ".beta"], res], [stat[nm], t[lay["out"]]])
+                      "res": res, "out": t[lay["out"]]}, dict(attrs, stat_in=stat_in),
+                     [t[lay["in"]], P[nm + ".gamma"], P[nm + ".beta"], res] + sin, sout + [t[lay["out"]]])
         elif ty == "avgpool2":
             t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
             H, W, C = shapes[lay["in"]]

@@ -196,3 +196,55 @@ WGRAD_PAIR_SHAPES = [
 def test_conv_wgrad_pairs(g, cg, monkeypatch):
     monkeypatch.setenv("OC_WGRAD_CG", cg)
     test_conv_wgrad(g)
+
+
+# conv_fwd with attrs.bn_stat: the batch statistics [μ; rstd] of the stored y
+# for the BN that consumes it — from the tensor-core epilogue's per-channel
+# partial sums (pairs, single CTAs, narrow stem slices) or, on the CUDA-core
+# path, the BN reduction over y — against the definition over the stored
+# bf16 values (biased variance, eps 1e-5; oracle/numerics.py)
+STAT_CASES = [
+    ((2, 9, 7, 64, 256, 3, 1, 1), "256,1,2"),
+    ((5, 13, 13, 128, 128, 3, 1, 1), "128,2,2"),
+    ((5, 13, 13, 128, 128, 3, 1, 1), "128,2,1"),
+    ((4, 9, 9, 256, 64, 3, 1, 1), "64,2,2"),
+    ((3, 11, 10, 64, 128, 3, 2, 1), ""),
+    ((3, 17, 16, 3, 64, 7, 2, 3, 2), ""),      # stem: space-to-depth slices of 2 images
+    ((2, 15, 13, 3, 64, 7, 2, 3), ""),         # 8-channel pixels
+    ((2, 9, 7, 64, 64, 3, 1, 1), "simt"),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("g,tile", STAT_CASES)
+def test_conv_fused_bn_stats(g, tile, monkeypatch):
+    from paper_2010_14109_b200.runtime import OutOfCoreStep
+    N, H, W, C, K, R, st, pad = g[:8]
+    if tile and tile != "simt":
+        monkeypatch.setenv("OC_CONV_TILE", tile)
+    doc, (P, Q), total = _graph("conv_fwd", g)
+    d = json.loads(doc)
+    d["variables"].append({"id": "stat", "bytes": 2 * K * 4, "pinned": True})
+    f = d["functions"][0]
+    f["out"].append("stat")
+    f["op"]["args"]["stat"] = "stat"
+    f["op"]["attrs"]["bn_stat"] = True
+    if tile == "simt":
+        f["op"]["attrs"]["impl"] = "simt"
+    doc = json.dumps(d)
+    rng = np.random.default_rng(5)
+    x = bf(rng.standard_normal((N, H, W, C)))
+    w = rng.standard_normal((K, R, R, C)).astype(np.float32) * 0.1 + 0.02
+    s = OutOfCoreStep(doc, total + 2 * K * 4, 0, mode="best", phys_bytes=4096)
+    s.write("x", _bits(x))
+    s.write("w", w)
+    s.step()
+    y = _from_bits(s.read("y", np.uint16), (N * P * Q, K))
+    stat = s.read("stat", np.float32).reshape(2, K)
+    s.close()
+    mu = y.mean(0)
+    var = np.maximum((y * y).mean(0) - mu * mu, 0)
+    rstd = 1 / np.sqrt(var + 1e-5)
+    sd = np.sqrt(var)
+    assert np.all(np.abs(stat[0] - mu) <= 2e-5 * (np.abs(mu) + sd) + 1e-7)
+    assert np.max(np.abs(stat[1] / rstd - 1)) < 2e-5
