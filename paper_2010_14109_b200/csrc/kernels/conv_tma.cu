@@ -364,14 +364,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
             if (P.stat_part) {
               // column sums of the 32 staged rows (conflict-free: the swizzle
               // spreads a row's eight 16-byte chunks over all banks); rows past M are zero
+              // (plain loads, all issued before the sums: the row order of the sums is fixed)
+              const uint8_t* sbp = stg + (q * 2 + (sc & 1)) * 4096 + (lane & 3) * 4;
+              uint32_t wv[32];
+#pragma unroll
+              for (int r = 0; r < 32; ++r)
+                wv[r] = *reinterpret_cast<const uint32_t*>(sbp + r * 128 + ((((uint32_t)lane >> 2) ^ (uint32_t)(r & 7)) << 4));
               float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f;
-#pragma unroll 8
+#pragma unroll
               for (int r = 0; r < 32; ++r) {
-                uint32_t wv;
-                asm volatile("ld.shared.b32 %0, [%1];"
-                             : "=r"(wv)
-                             : "r"(sb + r * 128 + ((((uint32_t)lane >> 2) ^ (uint32_t)(r & 7)) << 4) + (lane & 3) * 4));
-                const float2 f = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wv));
+                const float2 f = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wv[r]));
                 s0 += f.x;
                 s1 += f.y;
                 q0 = fmaf(f.x, f.x, q0);
