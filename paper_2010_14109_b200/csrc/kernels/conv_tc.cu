@@ -355,19 +355,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const Params P) {
 
 // fp32 KRSC master -> bf16 [K][kpad] (fprop; (r,s,c) over the activation's C
 // channels, zero past Cw and past RSC) or [C][R][S][K] (dgrad, Cw = C)
+// 32-bit indices (weights hold < 2^31 elements); the transposed copy walks
+// the output so its 2-byte stores coalesce (the fp32 reads go through L2)
 __global__ void weight_bf16(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int K, int RS, int C,
                             int transpose, int kpad, int Cw, int Kw = 1 << 30) {
-  const int64_t n = transpose ? (int64_t)K * RS * C : (int64_t)K * kpad;
+  const int n = transpose ? K * RS * C : K * kpad;
   const int rsc = RS * C;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     if (transpose) {
-      const int c = (int)(i % C);
-      const int64_t t = i / C;
-      const int rs = (int)(t % RS), k = (int)(t / RS);
-      out[((int64_t)c * RS + rs) * K + k] = __float2bfloat16_rn(w[i]);
+      const int k = i % K, t = i / K;   // out[(c·RS + rs)·K + k]
+      const int rs = t % RS, c = t / RS;
+      out[i] = __float2bfloat16_rn(w[(k * RS + rs) * C + c]);
     } else {
-      const int64_t k = i / kpad, j = i % kpad;
-      const int rs = (int)(j / C), c = (int)(j % C);
+      const int k = i / kpad, j = i - k * kpad;
+      const int rs = j / C, c = j - rs * C;
       out[i] = (j < rsc && c < Cw && k < Kw) ? __float2bfloat16_rn(w[(k * RS + rs) * Cw + c])
                                              : __float2bfloat16_rn(0.f);
     }
@@ -755,7 +756,7 @@ Status conv_fprop_pad(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   const int kpad = kpad_of(k);
   __nv_bfloat16* wb = (__nv_bfloat16*)a.ws;
   __nv_bfloat16* xbuf = (__nv_bfloat16*)((char*)a.ws + align256((size_t)k.K * kpad * 2));
-  weight_bf16<<<grid_for((int64_t)k.K * kpad, 256, 4), 256, 0, a.stream>>>(w, wb, k.K, k.R * k.S, k.C, 0, kpad, g.C,
+  weight_bf16<<<grid_for((int64_t)k.K * kpad, 256, 1), 256, 0, a.stream>>>(w, wb, k.K, k.R * k.S, k.C, 0, kpad, g.C,
                                                                             g.K);
   OC_LAUNCH_CHECK(a);
   for (int64_t n0 = 0; n0 < g.N; n0 += pp.slice) {
@@ -864,7 +865,7 @@ Status conv_fprop_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* x, cons
     weight_bf16_s2d<<<grid_for((int64_t)g.K * kpad, 256, 4), 256, 0, a.stream>>>(
         w, wb, g.K, g0.R, g0.S, g0.C, nw.fold ? 4 : g.R, g.S, g.pad, g0.pad, kpad, nw.fold ? 1 : 0);
   else
-    weight_bf16<<<grid_for((int64_t)g.K * kpad, 256, 4), 256, 0, a.stream>>>(w, wb, g.K, g.R * g.S, g.C, 0, kpad,
+    weight_bf16<<<grid_for((int64_t)g.K * kpad, 256, 1), 256, 0, a.stream>>>(w, wb, g.K, g.R * g.S, g.C, 0, kpad,
                                                                               g.Cw);
   OC_LAUNCH_CHECK(a);
   for (int64_t n0 = 0; n0 < g.N; n0 += nw.slice) {
@@ -914,7 +915,7 @@ Status conv_dgrad_tc(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, cons
   if (pad_path(g, DGRAD)) return conv_dgrad_pad(a, g, dy, w, dx, accumulate);
   __nv_bfloat16* wt = (__nv_bfloat16*)a.ws;
   const int64_t nw = (int64_t)g.K * g.R * g.S * g.C;
-  weight_bf16<<<grid_for(nw, 256, 4), 256, 0, a.stream>>>(w, wt, g.K, g.R * g.S, g.C, 1, 0, g.C);
+  weight_bf16<<<grid_for(nw, 256, 1), 256, 0, a.stream>>>(w, wt, g.K, g.R * g.S, g.C, 1, 0, g.C);
   OC_LAUNCH_CHECK(a);
   if (conv_tma_ok(g, DGRAD)) return conv_dgrad_tma(a, g, dy, wt, dx, accumulate);
   for (int ph = 0; ph < g.st; ++ph)
