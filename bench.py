@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--config", default="r18", choices=["r18", "r50", "r1001", "mlp", "biggan", "unet", "densenet"])
     ap.add_argument("--mode", default="va", choices=["va", "best", "first"])
     ap.add_argument("--batch", type=int, default=0)
-    ap.add_argument("--budget-frac", type=float, default=0.25)
+    ap.add_argument("--budget-frac", type=float, default=None,
+                    help="budget as a fraction of F_peak (default: 0.125 for configs[3] U-Net, else 0.25)")
     ap.add_argument("--chunk-mib", type=int, default=2)
     ap.add_argument("--no-incore", action="store_true")
     ap.add_argument("--window", default="auto", help="auto (timed probes) | model (makespan model, F4) | max | <bytes>")
@@ -51,7 +52,10 @@ def parse():
                     help="swap-timing window: the paper's byte window, or the prior-art function-distance "
                          "window (vdnn = 1 function ahead, lms = --distance functions ahead; SURVEY F1)")
     ap.add_argument("--distance", type=int, default=3, help="lms policy: functions of look-ahead")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.budget_frac is None:
+        a.budget_frac = 0.125 if a.config == "unet" else 0.25
+    return a
 
 
 def config(args):
