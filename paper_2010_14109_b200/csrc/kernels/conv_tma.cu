@@ -11,9 +11,15 @@
 //   warp 1      one elected thread issues tcgen05.mma (bf16 × bf16 -> fp32)
 //               into one of two TMEM accumulators, so the epilogue of tile t
 //               overlaps the main loop of tile t+1
-//   warps 2-5   epilogue: tcgen05.ld TMEM -> registers -> bf16 / fp32 rows
+//   warps 2-5   epilogue: tcgen05.ld TMEM -> registers -> bf16 / fp32 rows;
+//               fprop / stride-1 dgrad stage 32 × 64 bf16 boxes in shared
+//               memory (SWIZZLE_128B) and store them with TMA, optionally
+//               summing Σy, Σy² per channel for the BN that follows
 //
-// One CTA per SM loops over tiles (tile u, u + gridDim.x, ...).
+// One CTA per SM loops over tiles (tile u, u + gridDim.x, ...).  CG = 2 runs
+// CTA pairs (cta_group::2, a 2-CTA cluster on one TPC): 256-row MMAs issued by
+// the leader, each CTA staging its own A rows and half of the B columns (the
+// operand traffic per FLOP that bounds the single-CTA kernel).
 //   fprop   D[(n,p,q)][k] = Σ_{r,s,c} X[n, p·st−pad+r, q·st−pad+s, c] · W[k,r,s,c]
 //   dgrad   per output phase (h mod st, w mod st), a stride-1 gather over dY
 //           at the phase's taps only, W's taps reversed so the im2col offsets
