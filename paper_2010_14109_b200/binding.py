@@ -174,6 +174,53 @@ def check(code, err):
 # ------------------------------------------------------------ thin wrappers
 
 
+class Mem:
+    """The allocator C-ABI (oc_mem_create / oc_alloc / oc_map / oc_unmap /
+    oc_free / oc_mem_get_stats, include/oocore.h): VA chunk pool
+    or caching best/first-fit arena (P:100).  Argument marshalling only;
+    streams are raw cudaStream_t values (e.g. torch.cuda.Stream.cuda_stream)."""
+
+    def __init__(self, device=0, mode=OC_ALLOC_VA, chunk_bytes=2 << 20, phys_bytes=64 << 20, align=512, flags=0):
+        self.h = P()
+        err = oc_err()
+        model = oc_alloc_model(mode=mode, align=align, chunk_bytes=chunk_bytes, phys_bytes=phys_bytes)
+        check(lib().oc_mem_create(device, C.byref(model), flags, C.byref(self.h), C.byref(err)), err)
+
+    def alloc(self, nbytes):
+        sp, err = oc_span(), oc_err()
+        check(lib().oc_alloc(self.h, nbytes, C.byref(sp), C.byref(err)), err)
+        return sp
+
+    def map(self, handle, stream=0):
+        sp, err = oc_span(), oc_err()
+        check(lib().oc_map(self.h, handle, P(stream), C.byref(sp), C.byref(err)), err)
+        return sp
+
+    def unmap(self, handle, stream=0):
+        err = oc_err()
+        check(lib().oc_unmap(self.h, handle, P(stream), C.byref(err)), err)
+
+    def free(self, handle):
+        err = oc_err()
+        check(lib().oc_free(self.h, handle, C.byref(err)), err)
+
+    def stats(self):
+        st = oc_mem_stats()
+        check(lib().oc_mem_get_stats(self.h, C.byref(st)), oc_err())
+        return {k: getattr(st, k) for k, _ in oc_mem_stats._fields_}
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().oc_mem_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except TypeError:
+            pass
+
+
 class Graph:
     def __init__(self, doc):
         self.h = P()
