@@ -299,6 +299,13 @@ def run_ours(args, rank, world):
                              use_graph=not args.no_graph, distance=dist_)
     uid = None
     if world > 1:
+        # every replica must run the identical schedule: compare
+        # the canonical schedule bytes across ranks before the first step
+        import hashlib
+        hs = [None] * world
+        dist.all_gather_object(hs, hashlib.sha256(st.sched.json().encode()).hexdigest())
+        if len(set(hs)) != 1:
+            raise RuntimeError(f"ranks planned different schedules: {hs}")
         uid = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         st.attach_nccl(uid[0], rank, world)
