@@ -697,6 +697,221 @@ Status launch_tile(OpArgs& a, const Params& P, Tile t, int* ss = nullptr) {
   return t.bn == 128 ? launch_mt<MODE, 128, 0, 2>(a, P, ss) : launch_mt<MODE, 64, 0, 2>(a, P, ss);
 }
 
+// ---------------------------------------------------------------- stem
+// The space-to-depth stem (a 4×4 stride-1 conv over 16-channel, 32-byte
+// pixels, K = 64 outputs) gathered as halo tiles instead of im2col boxes:
+// the im2col kernel fetches every 32-byte pixel once per tap (16×) and is
+// L2→SM bound.  Here a unit is a 16 × 8 block of output pixels of one image;
+// the producer loads, per horizontal tap j, one tiled box of 19 rows × 8
+// pixels (SWIZZLE_32B, zero fill outside the image) — 4 boxes, 19 KB, for
+// all 16 taps — and tap (i, j)'s A operand is box j from row i on (a
+// 256-byte, pattern-aligned offset).  The whole weight W' (64 × 256 bf16,
+// 32 KB) stays resident in shared memory.  Epilogue as the generic kernel's
+// TMA-store path (4-D boxes of 4 × 8 pixels × 64 channels) with the fused
+// BN statistics.
+namespace stem {
+
+constexpr int TH = 16, TW = 8, TAP = 4, HR = TH + TAP - 1;
+constexpr int COPY = HR * TW * 32;              // 4864 B = 19 SW32 pattern repeats
+constexpr int ASTAGE = TAP * COPY;              // 19456 B
+constexpr int NSTG = 8;
+constexpr int BBYTES = 4 * 8192;                // W': 4 SWIZZLE_128B boxes of 64 K × 64 rows
+constexpr int SMEM = BBYTES + NSTG * ASTAGE + STG_BYTES + 1024 + 256;
+
+struct Params {
+  CUtensorMap tx;   // X' [N][H'][W'][16] bf16, box {16, 8, 19, 1}, SWIZZLE_32B
+  CUtensorMap tw;   // W' [64][256] bf16, box {64, 64}, SWIZZLE_128B
+  CUtensorMap ty;   // y [N][P][Q][64] bf16, box {64, 8, 4, 1}, SWIZZLE_128B
+  int tq, tpq, units, pad;
+  float* stat_part;   // fused BN statistics: part[slot][2][64]
+};
+
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint64_t* b, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(dst),
+      "l"(map), "r"(smem_u32(b)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1) stem_kernel(const __grid_constant__ Params P) {
+  constexpr uint32_t TCOLS = 128;   // two 64-column accumulators
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* bsm = smem;
+  uint8_t* asm_ = smem + BBYTES;
+  uint8_t* stg = asm_ + NSTG * ASTAGE;
+  uint64_t* full = (uint64_t*)(stg + STG_BYTES);
+  uint64_t* empty = full + NSTG;
+  uint64_t* tfull = empty + NSTG;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bfull = tempty + 2;
+  uint32_t* tmem_slot = (uint32_t*)(bfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&P.tx);
+    tma_prefetch(&P.tw);
+    for (int s = 0; s < NSTG; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    mbar_init(bfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  auto tile_of = [&](int u, int& n, int& p0, int& q0) {
+    n = u / P.tpq;
+    const int r = u - n * P.tpq;
+    const int tp = r / P.tq;
+    p0 = tp * TH;
+    q0 = (r - tp * P.tq) * TW;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(bfull, BBYTES);
+      for (int k = 0; k < 4; ++k) tma_load_2d(smem_u32(bsm) + k * 8192, &P.tw, bfull, k * 64, 0);
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < P.units; u += gridDim.x, ++it) {
+        int n, p0, q0;
+        tile_of(u, n, p0, q0);
+        const int sg = (int)(it % NSTG);
+        if (it >= (uint32_t)NSTG) mbar_wait(&empty[sg], ((it / NSTG) - 1) & 1);
+        const uint32_t a = smem_u32(asm_) + sg * ASTAGE;
+        mbar_expect_tx(&full[sg], ASTAGE);
+#pragma unroll
+        for (int j = 0; j < TAP; ++j) tma_load_4d(a + j * COPY, &P.tx, &full[sg], 0, q0 + j - P.pad, p0 - P.pad, n);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t ID = idesc(64, false, false);
+    if (lane == 0) mbar_wait(bfull, 0);
+    __syncwarp();
+    uint32_t it = 0, lt = 0;
+    for (int u = blockIdx.x; u < P.units; u += gridDim.x, ++it, ++lt) {
+      const uint32_t buf = lt & 1;
+      if (lt >= 2) mbar_wait(&tempty[buf], ((lt >> 1) - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int sg = (int)(it % NSTG);
+      mbar_wait(&full[sg], (it / NSTG) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (lane == 0) {
+        const uint32_t a = smem_u32(asm_) + sg * ASTAGE, b = smem_u32(bsm);
+#pragma unroll
+        for (int i = 0; i < TAP; ++i)
+#pragma unroll
+          for (int j = 0; j < TAP; ++j) {
+            const int t = i * TAP + j;   // W' column block t·16 (tap (i, j), 16 channels)
+            const uint64_t da = sdesc(a + j * COPY + i * 256, 16, 256, 6);
+            const uint64_t db = sdesc(b + (t >> 2) * 8192 + (t & 3) * 32, 16, 1024);
+            mma_bf16(tmem + buf * 64, da, db, ID, t > 0 ? 1u : 0u);
+          }
+        mma_commit(&empty[sg]);
+        mma_commit(&tfull[buf]);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int q = warp & 3;
+    float s0a = 0.f, s1a = 0.f, q0a = 0.f, q1a = 0.f;
+    uint32_t lt = 0, sc = 0;
+    for (int u = blockIdx.x; u < P.units; u += gridDim.x, ++lt, ++sc) {
+      int n, p0, q0;
+      tile_of(u, n, p0, q0);
+      const uint32_t buf = lt & 1;
+      mbar_wait(&tfull[buf], (lt >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t v0[32], v1[32];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + buf * 64;
+      TMEM_LD32(ta, v0);
+      TMEM_LD32(ta + 32, v1);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);   // accumulator drained into registers
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncwarp();
+      const uint32_t sb = smem_u32(stg) + (uint32_t)(q * 2 + (sc & 1)) * 4096u;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t lo = c < 4 ? v0[c * 8 + 2 * e] : v1[(c - 4) * 8 + 2 * e];
+          const uint32_t hi = c < 4 ? v0[c * 8 + 2 * e + 1] : v1[(c - 4) * 8 + 2 * e + 1];
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
+          w[e] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sb + lane * 128 + ((c ^ (lane & 7)) << 4)),
+                     "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                     : "memory");
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (P.stat_part) {
+        const uint8_t* sbp = stg + (q * 2 + (sc & 1)) * 4096 + (lane & 3) * 4;
+        uint32_t wv[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r)
+          wv[r] = *reinterpret_cast<const uint32_t*>(sbp + r * 128 + ((((uint32_t)lane >> 2) ^ (uint32_t)(r & 7)) << 4));
+        float s0 = 0.f, s1 = 0.f, q0s = 0.f, q1s = 0.f;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wv[r]));
+          s0 += f.x;
+          s1 += f.y;
+          q0s = fmaf(f.x, f.x, q0s);
+          q1s = fmaf(f.y, f.y, q1s);
+        }
+        s0a += s0;
+        s1a += s1;
+        q0a += q0s;
+        q1a += q1s;
+      }
+      if (lane == 0) {
+        asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(&P.ty),
+                     "r"(sb), "r"(0), "r"(q0), "r"(p0 + q * 4), "r"(n)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+    if (P.stat_part) {
+      float* pp = P.stat_part + (int64_t)(blockIdx.x * 4 + q) * 2 * 64;
+      *reinterpret_cast<float2*>(pp + 2 * lane) = make_float2(s0a, s1a);
+      *reinterpret_cast<float2*>(pp + 64 + 2 * lane) = make_float2(q0a, q1a);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+  }
+}
+
+Status encode_tiled(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                    const cuuint32_t* box, CUtensorMapSwizzle sw) {
+  Driver* d;
+  std::string msg;
+  if (!driver(d, msg)) return Status::make(OC_E_CUDA, msg);
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = d->TensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides,
+                                       box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? Status::ok() : encode_fail(r, "cuTensorMapEncodeTiled (stem)");
+}
+
+}  // namespace stem
+
 }  // namespace tma
 
 using namespace tma;
@@ -722,11 +937,58 @@ bool conv_tma_ok(const ConvGeom& g, int mode) {
 
 // y[M = N·P·Q][K] = im2col(x) · W_bf16[K][kpad]ᵀ
 // nst (optional): the stored output channels when g.K is a zero-padded width
+bool stem_enabled() {
+  const char* e = std::getenv("OC_CONV_STEM");
+  return !(e && e[0] == '0');
+}
+
+// the halo-tile stem kernel (namespace stem): 4×4 stride-1 conv over 16-channel
+// pixels with 64 outputs, output map tiled exactly by 16 × 8 blocks
+Status conv_stem_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* wb, int kpad,
+                     __nv_bfloat16* y, float* stat_part, int* stat_slots) {
+  using namespace stem;
+  stem::Params P{};
+  {
+    const cuuint64_t dims[4] = {16, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
+    const cuuint64_t strides[3] = {32, (cuuint64_t)g.W * 32, (cuuint64_t)g.H * g.W * 32};
+    const cuuint32_t box[4] = {16, TW, HR, 1};
+    OC_TRY(encode_tiled(&P.tx, x, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_32B));
+  }
+  OC_TRY(make_tiled(&P.tw, wb, (uint64_t)kpad, 64, 64));
+  {
+    const cuuint64_t dims[4] = {64, (cuuint64_t)g.Q, (cuuint64_t)g.P, (cuuint64_t)g.N};
+    const cuuint64_t strides[3] = {128, (cuuint64_t)g.Q * 128, (cuuint64_t)g.P * g.Q * 128};
+    const cuuint32_t box[4] = {64, TW, 4, 1};
+    OC_TRY(encode_tiled(&P.ty, y, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B));
+  }
+  P.tq = g.Q / TW;
+  P.tpq = (g.P / TH) * P.tq;
+  P.units = g.N * P.tpq;
+  P.pad = g.pad;
+  P.stat_part = stat_part;
+  if (P.units == 0) return Status::ok();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(stem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  const int ctas = std::min(P.units, sm_count());
+  if (stat_part && stat_slots) *stat_slots = ctas * 4;
+  if (a.ktimer) a.ktimer->begin(a.stream);
+  stem_kernel<<<ctas, NTHREADS, SMEM, a.stream>>>(P);
+  if (a.ktimer) a.ktimer->end(a.stream);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+
 // stat_part (optional): fused BN statistics of y (TMA-store epilogue only); on
 // return *stat_slots = the slots written (0: not fused, the caller reduces y)
 Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* wb, int kpad,
                       __nv_bfloat16* y, bool accumulate, int nst, float* stat_part, int* stat_slots) {
   if (stat_slots) *stat_slots = 0;
+  if (g.C == 16 && g.R == 4 && g.S == 4 && g.st == 1 && !g.nopadh && g.K == 64 && kpad == 256 && g.P % 16 == 0 &&
+      g.Q % 8 == 0 && !accumulate && !nst && tstore_enabled() && stem_enabled())
+    return conv_stem_tma(a, g, x, wb, kpad, y, stat_part, stat_slots);
   const int nch = g.C % 64 == 0 ? 0 : g.C;     // 8 or 16: narrow pixels, one tap per box
   Params P{};
   const int padh = g.nopadh ? 0 : g.pad;

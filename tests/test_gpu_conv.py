@@ -248,3 +248,23 @@ def test_conv_fused_bn_stats(g, tile, monkeypatch):
     sd = np.sqrt(var)
     assert np.all(np.abs(stat[0] - mu) <= 2e-5 * (np.abs(mu) + sd) + 1e-7)
     assert np.max(np.abs(stat[1] / rstd - 1)) < 2e-5
+
+
+# the halo-tile stem kernel (space-to-depth 4x4 conv, 64 outputs, output map
+# tiled by 16 x 8 blocks): exact tilings, image slices, zero padding at every
+# border; and the same shapes on the im2col kernel (OC_CONV_STEM=0)
+STEM_SHAPES = [(2, 32, 32, 3, 64, 7, 2, 3), (3, 32, 48, 3, 64, 7, 2, 3, 2), (1, 64, 16, 3, 64, 7, 2, 3)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("stem", ["1", "0"])
+@pytest.mark.parametrize("g", STEM_SHAPES)
+def test_conv_stem_halo(g, stem, monkeypatch):
+    monkeypatch.setenv("OC_CONV_STEM", stem)
+    test_conv_fwd(g)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("g", STEM_SHAPES[:2])
+def test_conv_stem_halo_fused_bn_stats(g, monkeypatch):
+    test_conv_fused_bn_stats(g, "", monkeypatch)
