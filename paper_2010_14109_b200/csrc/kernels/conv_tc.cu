@@ -665,25 +665,39 @@ __global__ void weight_bf16_s2d(const float* __restrict__ w, __nv_bfloat16* __re
   }
 }
 
-// dW[k][r][s][c] = Σ_z part[z][(i,j,(a,b,c))][k], the (i,j,a,b) holding filter tap (r,s)
-// (thread index k-fastest: the split partials [z][row][k] are read coalesced)
-__global__ void wgrad_reduce_s2d(int splits, int RSC2, int K, const float* __restrict__ part, float* __restrict__ dw,
-                                 int R, int S, int C, int S2, int c2, int pad, int fold) {
+// dW[k][r][s][c] = Σ_z part[z][(i,j,(a,b,c))][k], the (i,j,a,b) holding filter tap (r,s).
+// A block = 32 consecutive elements (k fastest: the partials are read
+// coalesced) × 8 split groups; group g sums the splits z ≡ g (mod 8) in order,
+// then the 8 group sums are added in order (fixed: bitwise reproducible)
+__global__ void __launch_bounds__(256) wgrad_reduce_s2d(int splits, int RSC2, int K, const float* __restrict__ part,
+                                                        float* __restrict__ dw, int R, int S, int C, int S2, int c2,
+                                                        int pad, int fold) {
+  __shared__ float sm[8][33];
   const int n = K * R * S * C;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
-    const int k = e % K;
+  const int l = threadIdx.x & 31, gz = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + l;
+  int row = 0, k = 0, r = 0, s = 0, c = 0;
+  float acc = 0.f;
+  if (e < n) {
+    k = e % K;
     int t = e / K;
-    const int c = t % C;
+    c = t % C;
     t /= C;
-    const int s = t % S;
-    const int r = t / S;
+    s = t % S;
+    r = t / S;
     const int tr = r + 2 * c2 - pad, ts = s + 2 * c2 - pad;
-    const int row = (fold ? (ts >> 1) * 64 + (tr >> 1) * 16 : ((tr >> 1) * S2 + (ts >> 1)) * 16) +
-                    ((tr & 1) * 2 + (ts & 1)) * C + c;
-    float acc = 0.f;
-#pragma unroll 8
-    for (int z = 0; z < splits; ++z) acc += part[((int64_t)z * RSC2 + row) * K + k];
-    dw[(((int64_t)k * R + r) * S + s) * C + c] = acc;
+    row = (fold ? (ts >> 1) * 64 + (tr >> 1) * 16 : ((tr >> 1) * S2 + (ts >> 1)) * 16) + ((tr & 1) * 2 + (ts & 1)) * C +
+          c;
+#pragma unroll 4
+    for (int z = gz; z < splits; z += 8) acc += part[((int64_t)z * RSC2 + row) * K + k];
+  }
+  sm[gz][l] = acc;
+  __syncthreads();
+  if (gz == 0 && e < n) {
+    float tot = 0.f;
+#pragma unroll
+    for (int g2 = 0; g2 < 8; ++g2) tot += sm[g2][l];
+    dw[(((int64_t)k * R + r) * S + s) * C + c] = tot;
   }
 }
 
@@ -1002,7 +1016,7 @@ Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* dy, con
     if (!st.good()) return st;
   }
   if (nw.s2d)
-    wgrad_reduce_s2d<<<grid_for((int64_t)g0.K * g0.R * g0.S * g0.C, 256, 4), 256, 0, a.stream>>>(
+    wgrad_reduce_s2d<<<(unsigned)((g0.K * g0.R * g0.S * g0.C + 31) / 32), 256, 0, a.stream>>>(
         splits, RSC, g.K, part, dw, g0.R, g0.S, g0.C, g.S, g.pad, g0.pad, nw.fold ? 1 : 0);
   else
     wgrad_reduce<<<dim3((g.K + 31) / 32, (RSC + 31) / 32), 1024, 0, a.stream>>>(splits, RSC, g.K, g.C, g.Cw, part,

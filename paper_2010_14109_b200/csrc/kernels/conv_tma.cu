@@ -898,6 +898,135 @@ __global__ void __launch_bounds__(NTHREADS, 1) stem_kernel(const __grid_constant
   }
 }
 
+// Weight gradient of the same stem, halo-gathered: dW'[(t, c)][k] = Σ_pixels
+// X'(pixel shifted by tap t = (i, j))[c] · dY[pixel][k].  Per 16 × 8 tile of
+// output pixels (one 128-pixel K-block) the producer loads, per j, a box of
+// 23 rows × 8 pixels of X' (SWIZZLE_32B) and the tile's dY rows (SWIZZLE_128B).
+// The MN-major A operand of horizontal tap j stacks 8 vertical taps i = 0..7
+// (the four real ones and four that only fill the 128-row MMA) whose 16-channel
+// atoms are the same box one pixel row apart: LBO = SBO = 256 bytes.  Each CTA
+// accumulates its tiles in four TMEM accumulators (one per j) and writes its
+// split partial part[z = CTA][(t, c)][k] once (slices after the first add).
+constexpr int WHR = TH + 7;                    // 23 rows: vertical taps 0..7 over 16 rows
+constexpr int WCOPY = WHR * TW * 32;           // 5888 B
+constexpr int WSTAGE = TAP * WCOPY + TH * TW * 128;   // + dY tile 16 KB = 39936 B
+constexpr int WNSTG = 5;
+constexpr int WSMEM = WNSTG * WSTAGE + 1024 + 256;
+
+struct WParams {
+  CUtensorMap tx;   // X' box {16, 8, 23, 1}, SWIZZLE_32B
+  CUtensorMap tdy;  // dY [N][P][Q][64] box {64, 8, 16, 1}, SWIZZLE_128B
+  int tq, tpq, units, pad, accumulate;
+  float* part;      // [gridDim.x][256][64]
+};
+
+__global__ void __launch_bounds__(NTHREADS, 1) stem_wgrad_kernel(const __grid_constant__ WParams P) {
+  constexpr uint32_t TCOLS = 256;   // four 64-column accumulators (j = 0..3)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + WNSTG * WSTAGE);
+  uint64_t* empty = full + WNSTG;
+  uint64_t* tfull = empty + WNSTG;
+  uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&P.tx);
+    tma_prefetch(&P.tdy);
+    for (int s = 0; s < WNSTG; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  auto tile_of = [&](int u, int& n, int& p0, int& q0) {
+    n = u / P.tpq;
+    const int r = u - n * P.tpq;
+    const int tp = r / P.tq;
+    p0 = tp * TH;
+    q0 = (r - tp * P.tq) * TW;
+  };
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < P.units; u += gridDim.x, ++it) {
+        int n, p0, q0;
+        tile_of(u, n, p0, q0);
+        const int sg = (int)(it % WNSTG);
+        if (it >= (uint32_t)WNSTG) mbar_wait(&empty[sg], ((it / WNSTG) - 1) & 1);
+        const uint32_t a = smem_u32(smem) + sg * WSTAGE;
+        mbar_expect_tx(&full[sg], WSTAGE);
+#pragma unroll
+        for (int j = 0; j < TAP; ++j) tma_load_4d(a + j * WCOPY, &P.tx, &full[sg], 0, q0 + j - P.pad, p0 - P.pad, n);
+        tma_load_4d(a + TAP * WCOPY, &P.tdy, &full[sg], 0, q0, p0, n);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t ID = idesc(64, true, true);
+    uint32_t it = 0;
+    for (int u = blockIdx.x; u < P.units; u += gridDim.x, ++it) {
+      const int sg = (int)(it % WNSTG);
+      mbar_wait(&full[sg], (it / WNSTG) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (lane == 0) {
+        const uint32_t a = smem_u32(smem) + sg * WSTAGE, b = a + TAP * WCOPY;
+#pragma unroll
+        for (int k = 0; k < TH * TW / 16; ++k) {   // 16 pixels (two tile rows) per MMA
+          const uint64_t db = sdesc(b + k * 2048, 16384, 1024);
+#pragma unroll
+          for (int j = 0; j < TAP; ++j)
+            mma_bf16(tmem + j * 64, sdesc(a + j * WCOPY + k * 512, 256, 256, 6), db, ID, (it > 0 || k > 0) ? 1u : 0u);
+        }
+        mma_commit(&empty[sg]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) mma_commit(tfull);   // arrives once all issued MMAs completed (also with no units)
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    const int r = q * 32 + lane;        // D row = (vertical tap i, channel c)
+    const int i = r >> 4, c = r & 15;
+    mbar_wait(tfull, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const bool any = blockIdx.x < P.units;
+#pragma unroll
+    for (int j = 0; j < TAP; ++j) {
+      uint32_t v0[32], v1[32];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + j * 64;
+      TMEM_LD32(ta, v0);
+      TMEM_LD32(ta + 32, v1);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (i >= TAP) continue;
+      float* o = P.part + ((int64_t)blockIdx.x * 256 + (i * TAP + j) * 16 + c) * 64;
+#pragma unroll
+      for (int e = 0; e < 64; e += 4) {
+        const uint32_t* v = e < 32 ? &v0[e] : &v1[e - 32];
+        float4 f = any ? make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]),
+                                     __uint_as_float(v[3]))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (P.accumulate) {
+          const float4 old = *reinterpret_cast<const float4*>(o + e);
+          f.x += old.x; f.y += old.y; f.z += old.z; f.w += old.w;
+        }
+        *reinterpret_cast<float4*>(o + e) = f;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+  }
+}
+
 Status encode_tiled(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
                     const cuuint32_t* box, CUtensorMapSwizzle sw) {
   Driver* d;
@@ -1097,9 +1226,47 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
   return Status::ok();
 }
 
+// the halo-tile stem weight gradient (namespace stem): one split partial per CTA
+Status conv_stem_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy,
+                           float* part, int splits, bool accumulate) {
+  using namespace stem;
+  WParams P{};
+  {
+    const cuuint64_t dims[4] = {16, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
+    const cuuint64_t strides[3] = {32, (cuuint64_t)g.W * 32, (cuuint64_t)g.H * g.W * 32};
+    const cuuint32_t box[4] = {16, TW, WHR, 1};
+    OC_TRY(encode_tiled(&P.tx, x, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_32B));
+  }
+  {
+    const cuuint64_t dims[4] = {64, (cuuint64_t)g.Q, (cuuint64_t)g.P, (cuuint64_t)g.N};
+    const cuuint64_t strides[3] = {128, (cuuint64_t)g.Q * 128, (cuuint64_t)g.P * g.Q * 128};
+    const cuuint32_t box[4] = {64, TW, TH, 1};
+    OC_TRY(encode_tiled(&P.tdy, dy, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B));
+  }
+  P.tq = g.Q / TW;
+  P.tpq = (g.P / TH) * P.tq;
+  P.units = g.N * P.tpq;
+  P.pad = g.pad;
+  P.accumulate = accumulate ? 1 : 0;
+  P.part = part;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(stem_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WSMEM);
+    attr = true;
+  }
+  if (a.ktimer) a.ktimer->begin(a.stream);
+  stem_wgrad_kernel<<<splits, NTHREADS, WSMEM, a.stream>>>(P);   // every CTA writes its partial (zeros if idle)
+  if (a.ktimer) a.ktimer->end(a.stream);
+  OC_LAUNCH_CHECK(a);
+  return Status::ok();
+}
+
 // wgrad partials part[z][R·S·C][K] over pixel blocks [z·kbps, (z+1)·kbps)
 Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
                       int splits, int kb_per_split, bool accumulate) {
+  if (g.C == 16 && g.R == 4 && g.S == 4 && g.st == 1 && !g.nopadh && g.K == 64 && g.P % 16 == 0 && g.Q % 8 == 0 &&
+      splits >= 1 && splits <= 1024 && stem_enabled())
+    return conv_stem_wgrad_tma(a, g, x, dy, part, splits, accumulate);
   Params P{};
   const int nch = g.C == 16 ? 16 : 0;
   const int padh = g.nopadh ? 0 : g.pad;

@@ -262,6 +262,7 @@ STEM_SHAPES = [(2, 32, 32, 3, 64, 7, 2, 3), (3, 32, 48, 3, 64, 7, 2, 3, 2), (1, 
 def test_conv_stem_halo(g, stem, monkeypatch):
     monkeypatch.setenv("OC_CONV_STEM", stem)
     test_conv_fwd(g)
+    test_conv_wgrad(g)
 
 
 @pytest.mark.gpu
