@@ -290,4 +290,5 @@ def test_conv_halo3(g, halo, monkeypatch):
 @pytest.mark.gpu
 @pytest.mark.parametrize("g", HALO_SHAPES[:2])
 def test_conv_halo3_fused_bn_stats(g, monkeypatch):
+    monkeypatch.setenv("OC_CONV_HALO", "1")
     test_conv_fused_bn_stats(g, "", monkeypatch)
