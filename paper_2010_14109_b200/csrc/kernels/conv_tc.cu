@@ -582,6 +582,15 @@ __global__ void s2d_pixels(int rows, int H2, int W2, int C, const __nv_bfloat16*
     const int u = y % H2;
     const int64_t n = y / H2;
     const int64_t i = (int64_t)y * W2 + v;
+    uint4* o = reinterpret_cast<uint4*>(out + i * 16);
+    if (C == 3) {
+      // the 2 × 2 block is two contiguous, 4-byte aligned 12-byte runs ((a, b, c) order = memory order)
+      const uint32_t* r0 = reinterpret_cast<const uint32_t*>(x + ((n * 2 * H2 + 2 * u) * 2 * W2 + 2 * v) * 3);
+      const uint32_t* r1 = r0 + 3 * W2;
+      o[0] = make_uint4(__ldg(r0), __ldg(r0 + 1), __ldg(r0 + 2), __ldg(r1));
+      o[1] = make_uint4(__ldg(r1 + 1), __ldg(r1 + 2), 0u, 0u);
+      continue;
+    }
     uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
     for (int ab = 0; ab < 4; ++ab) {
       const int64_t src = ((n * 2 * H2 + 2 * u + (ab >> 1)) * 2 * W2 + 2 * v + (ab & 1)) * C;
@@ -590,7 +599,6 @@ __global__ void s2d_pixels(int rows, int H2, int W2, int C, const __nv_bfloat16*
         w[e >> 1] |= (uint32_t)xs[src + c] << (16 * (e & 1));
       }
     }
-    uint4* o = reinterpret_cast<uint4*>(out + i * 16);
     o[0] = make_uint4(w[0], w[1], w[2], w[3]);
     o[1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
