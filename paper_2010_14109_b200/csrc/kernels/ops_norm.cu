@@ -358,6 +358,11 @@ __global__ void bn_relu_pool(PoolGeom g, const T* __restrict__ y, const float* _
                              uint8_t* __restrict__ idx) {
   const int C = g.C;
   const uint32_t total = (uint32_t)g.N * g.P * g.Q * (C / 8);
+  // the grid stride is a multiple of C/8 when 256 is (C a power of two up to
+  // 2048): a thread's channel group never changes, its BN parameters stay in registers
+  const bool fixed_cg = 256 % (C / 8) == 0;
+  float gm[8], bt[8], mu[8], rs[8];
+  int cg_loaded = -1;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const uint32_t t0 = g.fc8.div(i);
     const int cg = (int)(i - t0 * (C / 8));
@@ -365,14 +370,20 @@ __global__ void bn_relu_pool(PoolGeom g, const T* __restrict__ y, const float* _
     const int q = (int)(t0 - t1 * g.Q);
     const uint32_t n = g.fP.div(t1);
     const int p = (int)(t1 - n * g.P);
-    float best[8], gm[8], bt[8], mu[8], rs[8];
+    float best[8];
     uint8_t bi[8];
+    if (gamma && (!fixed_cg || cg_loaded < 0)) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int c = cg * 8 + k;
+        gm[k] = gamma[c]; bt[k] = beta[c]; mu[k] = stat[c]; rs[k] = stat[C + c];
+      }
+      cg_loaded = cg;
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       best[k] = -INFINITY;
       bi[k] = 0;
-      const int c = cg * 8 + k;
-      if (gamma) { gm[k] = gamma[c]; bt[k] = beta[c]; mu[k] = stat[c]; rs[k] = stat[C + c]; }
     }
     for (int u = 0; u < g.r; ++u) {
       const int h = p * g.st - g.pad + u;
