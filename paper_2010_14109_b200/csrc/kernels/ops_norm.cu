@@ -412,6 +412,84 @@ __global__ void bn_relu_pool(PoolGeom g, const T* __restrict__ y, const float* _
   }
 }
 
+// The stem geometry (3×3, stride 2, pad 1, bf16, C = 64) tiled: a block takes
+// 4 × 16 output pixels, stages their 9 × 33 input pixels in shared memory with
+// BN-ReLU applied and rounded once per element (padding as −inf, which never
+// wins the first-max rule), then each thread pools from shared memory — y is
+// read about once instead of 9 BN evaluations per output.
+constexpr int PT_P = 4, PT_Q = 16, PT_R = 2 * PT_P + 1, PT_C = 2 * PT_Q + 1;
+__global__ void __launch_bounds__(256) bn_relu_pool_tiled(PoolGeom g, const __nv_bfloat16* __restrict__ y,
+                                                          const float* __restrict__ stat,
+                                                          const float* __restrict__ gamma,
+                                                          const float* __restrict__ beta,
+                                                          __nv_bfloat16* __restrict__ out, uint8_t* __restrict__ idx) {
+  __shared__ uint4 tile[PT_R * PT_C * 8];
+  __shared__ float prm[4][64];
+  const int tq = (g.Q + PT_Q - 1) / PT_Q, tp = (g.P + PT_P - 1) / PT_P;
+  const int b = blockIdx.x;
+  const int n = b / (tp * tq), r0 = b % (tp * tq);
+  const int p0 = (r0 / tq) * PT_P, q0 = (r0 % tq) * PT_Q;
+  if (threadIdx.x < 64) {
+    prm[0][threadIdx.x] = gamma[threadIdx.x];
+    prm[1][threadIdx.x] = beta[threadIdx.x];
+    prm[2][threadIdx.x] = stat[threadIdx.x];
+    prm[3][threadIdx.x] = stat[64 + threadIdx.x];
+  }
+  __syncthreads();
+  const int h0 = 2 * p0 - 1, w0 = 2 * q0 - 1;
+  for (int e = threadIdx.x; e < PT_R * PT_C * 8; e += 256) {
+    const int cg = e & 7, pix = e >> 3;
+    const int h = h0 + pix / PT_C, w = w0 + pix % PT_C;
+    __nv_bfloat162 z2[4];
+    if (h >= 0 && h < g.H && w >= 0 && w < g.W) {
+      const V8 x = ld8(y + (((int64_t)n * g.H + h) * g.W + w) * 64 + cg * 8);
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        const int c = cg * 8 + k;
+        const float a0 = fmaxf(fmaf(prm[0][c], (x.v[k] - prm[2][c]) * prm[3][c], prm[1][c]), 0.f);
+        const float a1 = fmaxf(fmaf(prm[0][c + 1], (x.v[k + 1] - prm[2][c + 1]) * prm[3][c + 1], prm[1][c + 1]), 0.f);
+        z2[k / 2] = __floats2bfloat162_rn(a0, a1);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) z2[k] = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+    }
+    tile[e] = *reinterpret_cast<uint4*>(z2);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < PT_P * PT_Q * 8; e += 256) {
+    const int cg = e & 7, o = e >> 3;
+    const int p = p0 + o / PT_Q, q = q0 + o % PT_Q;
+    if (p >= g.P || q >= g.Q) continue;
+    float best[8];
+    uint8_t bi[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { best[k] = -INFINITY; bi[k] = 0; }
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+#pragma unroll
+      for (int v = 0; v < 3; ++v) {
+        const uint4 c4 = tile[((2 * (o / PT_Q) + u) * PT_C + 2 * (o % PT_Q) + v) * 8 + cg];
+        const __nv_bfloat162* z2 = reinterpret_cast<const __nv_bfloat162*>(&c4);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(z2[k]);
+          if (f.x > best[2 * k]) { best[2 * k] = f.x; bi[2 * k] = (uint8_t)(u * 3 + v); }
+          if (f.y > best[2 * k + 1]) { best[2 * k + 1] = f.y; bi[2 * k + 1] = (uint8_t)(u * 3 + v); }
+        }
+      }
+    V8 ov;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ov.v[k] = best[k];
+    const int64_t oo = (((int64_t)n * g.P + p) * g.Q + q) * 64 + cg * 8;
+    st8(out + oo, ov);
+    uint2 packed;
+    packed.x = bi[0] | (bi[1] << 8) | (bi[2] << 16) | ((uint32_t)bi[3] << 24);
+    packed.y = bi[4] | (bi[5] << 8) | (bi[6] << 16) | ((uint32_t)bi[7] << 24);
+    *reinterpret_cast<uint2*>(idx + oo) = packed;
+  }
+}
+
 enum { RP_Y, RP_STAT, RP_GAMMA, RP_BETA, RP_OUT, RP_IDX };
 template <typename T>
 Status bn_relu_pool_fwd_t(OpArgs& a) {
@@ -419,6 +497,15 @@ Status bn_relu_pool_fwd_t(OpArgs& a) {
   auto y = (const T*)a.p(RP_Y);
   if (!Ab(a, "stat_in")) OC_TRY(batch_stats<T>(a, (int64_t)g.N * g.H * g.W, g.C, y, (float*)a.p(RP_STAT)));
   const int64_t total = (int64_t)g.N * g.P * g.Q * (g.C / 8);
+  const char* et = std::getenv("OC_POOL_TILED");
+  if (sizeof(T) == 2 && g.C == 64 && g.r == 3 && g.st == 2 && g.pad == 1 && !(et && et[0] == '0')) {
+    const int64_t blocks = (int64_t)g.N * ((g.P + PT_P - 1) / PT_P) * ((g.Q + PT_Q - 1) / PT_Q);
+    bn_relu_pool_tiled<<<(unsigned)blocks, 256, 0, a.stream>>>(
+        g, (const __nv_bfloat16*)y, (const float*)a.p(RP_STAT), (const float*)a.p(RP_GAMMA),
+        (const float*)a.p(RP_BETA), (__nv_bfloat16*)a.p(RP_OUT), (uint8_t*)a.p(RP_IDX));
+    OC_LAUNCH_CHECK(a);
+    return Status::ok();
+  }
   bn_relu_pool<T><<<grid_for(total, 256, 2), 256, 0, a.stream>>>(g, y, (const float*)a.p(RP_STAT),
                                                                  (const float*)a.p(RP_GAMMA),
                                                                  (const float*)a.p(RP_BETA), (T*)a.p(RP_OUT),
