@@ -843,8 +843,10 @@ __global__ void __launch_bounds__(256) pbn_partial_blk(PoolGeom g, const T* __re
   }
 }
 
+// (256, 3): 80 registers instead of 121 — three blocks per SM; measured 8 % faster
+// despite a small stack spill (the same bound made pbn_partial_blk 27 % slower)
 template <typename T>
-__global__ void __launch_bounds__(256) pbn_apply_blk(PoolGeom g, const T* __restrict__ gp,
+__global__ void __launch_bounds__(256, 3) pbn_apply_blk(PoolGeom g, const T* __restrict__ gp,
                                                      const uint8_t* __restrict__ idx, T* y,
                                                      const float* __restrict__ stat, const float* __restrict__ gamma,
                                                      const float* __restrict__ beta, const float* __restrict__ dgamma,
