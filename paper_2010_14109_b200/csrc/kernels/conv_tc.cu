@@ -448,7 +448,11 @@ bool conv_tma_ok(const ConvGeom& g, int mode);
 Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* wb, int kpad,
                       __nv_bfloat16* y, bool accumulate, int nst = 0, float* stat_part = nullptr,
                       int* stat_slots = nullptr);
-constexpr int kStatSlotsMax = 148 * 4;   // epilogue statistics slots per launch (CTA × epilogue warp)
+namespace tma {
+int stat_slots_max();   // epilogue statistics slots per launch (CTA × epilogue warp)
+int sm_count();
+int grid_cap(int ctas);   // OC_CONV_MAX_CTAS (tests)
+}  // namespace tma
 Status bn_stats_from_parts(OpArgs& a, int nslots, int64_t rows, int C, const float* part, float* stat);
 Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* wt,
                       __nv_bfloat16* dx, bool accumulate, int nst = 0);
@@ -867,7 +871,7 @@ size_t conv_tc_ws(const ConvGeom& g0, int mode) {
 size_t conv_tc_stat_ws(const ConvGeom& g0) {
   const Narrow nw = narrow_of(g0);
   const int64_t nsl = (g0.N + nw.slice - 1) / nw.slice;
-  return align256((size_t)nsl * kStatSlotsMax * 2 * g0.K * 4);
+  return align256((size_t)nsl * tma::stat_slots_max() * 2 * g0.K * 4);
 }
 
 Status conv_fprop_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* x, const float* w, __nv_bfloat16* y,
@@ -983,7 +987,7 @@ Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* dy, con
     // persistent kernel: at most two units per SM, balanced (floor, not ceil)
     const int64_t tiles = ((int64_t)g.R * g.S * g.C + BM - 1) / BM * (g.K / BN);
     const int64_t kbs = ((int64_t)gs.N * g.P * g.Q + BKE - 1) / BKE;
-    int64_t s2 = (2 * 148) / tiles;
+    int64_t s2 = (2 * (int64_t)tma::grid_cap(tma::sm_count())) / tiles;
     s2 = s2 < 1 ? 1 : (s2 > kbs ? kbs : s2);
     splits = (int)(s2 < splits ? s2 : splits);
   }

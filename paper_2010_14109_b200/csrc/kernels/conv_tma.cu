@@ -527,6 +527,21 @@ int max_pairs() {
   return n;
 }
 
+// Upper bound on the persistent grid, read at every launch (OC_CONV_MAX_CTAS,
+// tests only): with a few CTAs every CTA loops over many work units, so the
+// parity tests reach the persistent-loop regime the full-size step runs in
+// (mbarrier phase wrap, TMEM double-buffer alternation, stat slots summed
+// across units) on shapes the oracle finishes in seconds.
+int grid_cap(int ctas) {
+  const char* e = std::getenv("OC_CONV_MAX_CTAS");
+  const int cap = e ? std::atoi(e) : 0;
+  return (cap > 0 && cap < ctas) ? cap : ctas;
+}
+
+// epilogue statistics slots one launch may write (CTA x epilogue warp); the
+// BN-statistics workspace is sized from this (conv_tc_stat_ws)
+int stat_slots_max() { return sm_count() * 4; }
+
 Status encode_fail(CUresult r, const char* what) { return cu_status(r, what); }
 
 // NHWC bf16 activation [N][H][W][C] gathered for an output grid Pd × Qd
@@ -607,10 +622,15 @@ Status launch_mt(OpArgs& a, Params P, int* stat_slots = nullptr) {
   const int units = P.num_m * P.num_n * (MODE == WGRAD ? P.splits : 1);
   if (units == 0) return Status::ok();
   int ctas = std::min(units, CG == 1 ? sm_count() : max_pairs());   // CTAs, or pairs
+  ctas = CG == 1 ? grid_cap(ctas) : std::max(1, grid_cap(2 * ctas) / 2);
   if (P.stat_part) {
     // fused statistics: whole groups of num_n CTAs (pairs), 4·CG slots per group member
-    ctas = ctas / P.num_n * P.num_n;
-    if (ctas == 0) return Status::make(OC_E_INVARIANT, "conv: statistics epilogue needs num_n CTAs");
+    // (units = num_m · num_n >= num_n, so a capped grid rounds up to one group)
+    ctas = std::max(ctas / P.num_n, 1) * P.num_n;
+    if (ctas > (CG == 1 ? sm_count() : max_pairs()))
+      return Status::make(OC_E_INVARIANT, "conv: statistics epilogue needs num_n CTAs");
+    if (ctas / P.num_n * 4 * CG > stat_slots_max())
+      return Status::make(OC_E_INVARIANT, "conv: more statistics slots than the workspace holds");
     if (stat_slots) *stat_slots = ctas / P.num_n * 4 * CG;
   }
   if (a.ktimer) a.ktimer->begin(a.stream);
@@ -1297,7 +1317,7 @@ Status conv_stem_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const
     cudaFuncSetAttribute(stem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     attr = true;
   }
-  const int ctas = std::min(P.units, sm_count());
+  const int ctas = grid_cap(std::min(P.units, sm_count()));
   if (stat_part && stat_slots) *stat_slots = ctas * 4;
   if (a.ktimer) a.ktimer->begin(a.stream);
   stem_kernel<<<ctas, NTHREADS, SMEM, a.stream>>>(P);
@@ -1344,7 +1364,7 @@ Status conv_halo3_tma(OpArgs& a, int N, int Hm, int Wm, const __nv_bfloat16* in,
     cudaFuncSetAttribute(halo3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, H3SMEM);
     attr = true;
   }
-  const int ctas = std::min(P.units, sm_count());
+  const int ctas = grid_cap(std::min(P.units, sm_count()));
   if (stat_part && stat_slots) *stat_slots = ctas * 4;
   if (a.ktimer) a.ktimer->begin(a.stream);
   halo3_kernel<<<ctas, NTHREADS, H3SMEM, a.stream>>>(P);

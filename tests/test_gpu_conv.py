@@ -2,7 +2,8 @@
 CUDA-core fallback) with the oracle's direct-definition convolution, through
 the C-ABI executor on one-function graphs: several tiles, ragged M tails,
 stride 1 and 2, 1×1 and 3×3 filters, 64- and 128-wide N tiles, dgrad
-accumulation and the deterministic split-K wgrad."""
+accumulation and the deterministic split-K wgrad.  bf16 outputs within
+north_star's 1e-3 relative L2, fp32 weight gradients within 1e-5."""
 import json
 
 import numpy as np
@@ -96,7 +97,7 @@ def test_conv_fwd(g):
     y = _run(doc, total, {"x": _bits(x), "w": w}, "y", np.uint16)
     y = _from_bits(y, (N, P, Q, K))
     ref = nm.round_bf16(nm.conv2d(x.float().numpy().astype(np.float64), nm.round_bf16(w.astype(np.float64)), st, pad))
-    assert nm.rel_l2(y, ref) < 2e-3
+    assert nm.rel_l2(y, ref) < 1e-3
     assert np.max(np.abs(y - ref)) <= 2 ** -7 * np.max(np.abs(ref)) + 1e-6
 
 
@@ -117,7 +118,7 @@ def test_conv_dgrad(g, accumulate):
     if accumulate:
         ref = ref + old.float().numpy()
     ref = nm.round_bf16(ref)
-    assert nm.rel_l2(dx, ref) < 2e-3
+    assert nm.rel_l2(dx, ref) < 1e-3
 
 
 @pytest.mark.gpu
