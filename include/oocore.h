@@ -123,6 +123,12 @@ uint32_t oc_graph_fn_position(const oc_graph* g, uint32_t decl_index);
 uint64_t oc_graph_in_core_peak(const oc_graph* g);
 /* Σ distinct variable bytes and max_i bytes(distinct V̂_i). */
 void oc_graph_footprint(const oc_graph* g, uint64_t* total_bytes, uint64_t* max_function_bytes);
+/* Bytes of the executor's compute workspace for this graph: the largest
+ * per-function scratch of its ops (bf16 weight copies, re-laid-out narrow
+ * input slices, split-K partials, reduction partials).  Allocated once per
+ * executor outside the swap pool (like a cuDNN workspace), so a physical
+ * device budget B_p = pinned bytes + pool + this.  0 for graphs without ops. */
+uint64_t oc_graph_workspace_bytes(const oc_graph* g);
 
 /* --------------------------------------------------------------- planning
  * The schedule-window greedy of P:91-93 / Fig.2:
@@ -343,7 +349,32 @@ int oc_run_step(oc_exec* x, oc_step_metrics* out, oc_err* err);
 /* Per-event timeline of the last step as JSON lines (S:358 format):
  * {"t0":ms,"t1":ms,"stream":"compute|h2d|d2h","id":"<fn or var>"} */
 int oc_exec_timeline(oc_exec* x, char* buf, size_t cap, size_t* need);
+/* Switch the per-event timeline on or off for later steps (the executor must
+ * have been created with options.timeline = 1, which creates the events;
+ * OC_E_ARG otherwise).  Off: steps replay the captured CUDA graph when
+ * options.use_graph is set; on: steps are issued eagerly with events, so one
+ * executor serves both the timed and the instrumented passes of a bench. */
+int oc_exec_set_timeline(oc_exec* x, int on);
 void oc_exec_destroy(oc_exec* x);
+
+/* ---------------------------------------------------- layer-local inspection
+ * Test infrastructure for the layer-local parity harness
+ * (tests/test_gpu_layerwise.py): the out-of-core step's functions are the
+ * ordinary training step's, so each f_i can be checked on its own —
+ * its outputs against the definition applied to the values it read.
+ * With a hook set, oc_run_step issues the step eagerly (no CUDA-graph
+ * capture), synchronises the device before and after the kernels of each
+ * function f_i and calls hook(user, i, 0) before them and hook(user, i, 1)
+ * after them (i = execution position, oc_graph_fn_position).  Inside the hook
+ * oc_exec_read_var copies the current device bytes of a variable of V̂_i —
+ * resident by construction (swap-ins complete before f_i) — or of a
+ * pinned variable to host memory (blocking cudaMemcpy; `host` is caller
+ * memory of at least `bytes`).  Errors: OC_E_ARG (unknown variable, not
+ * resident, bytes larger than the variable), OC_E_CUDA.  hook = NULL removes
+ * it.  Not for timed runs. */
+typedef void (*oc_fn_hook)(void* user, uint32_t fn, int phase);
+int oc_exec_set_hook(oc_exec* x, oc_fn_hook hook, void* user);
+int oc_exec_read_var(oc_exec* x, uint32_t var, void* host, uint64_t bytes, oc_err* err);
 
 /* ---------------------------------------------------- data parallel (NCCL)
  * Functions with op {"kind":"allreduce", ...} sum their pinned gradient

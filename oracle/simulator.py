@@ -120,6 +120,8 @@ def simulate_exec(g, seq, sch, placements, mode, fn_ms, h2d_gbs, d2h_gbs, h2d_us
             rel_iv.append((u[1][0], u[1][1], t))
 
     stall = []
+    events = []        # timeline in the executor's format (oc_exec_timeline): slot / dep ids
+    slot = dep = 0
     for i in range(n):
         t_wait = 0.0
         for v in sch.wait_out[i]:
@@ -132,10 +134,13 @@ def simulate_exec(g, seq, sch, placements, mode, fn_ms, h2d_gbs, d2h_gbs, h2d_us
             t = max(h2d_free, mem_ready(u))
             if kind == "h2d":
                 t = max(t, host_ready.get(v, 0.0))
+                t0 = t
                 t = t + (h2d_us * 1e-3 + b[v] / (h2d_gbs * 1e6))
+                events.append({"t0": t0, "t1": t, "stream": "h2d", "slot": slot, "fn": i, "var": v})
             h2d_free = t
             ready[v] = t
             held[v] = u
+            slot += 1
         need = 0.0
         for v in set(seq.occ[seq.l[i]:seq.e[i] + 1]):
             if not g.pinned[v]:
@@ -143,17 +148,21 @@ def simulate_exec(g, seq, sch, placements, mode, fn_ms, h2d_gbs, d2h_gbs, h2d_us
         start = max(end_prev, t_wait, need)
         stall.append(start - end_prev)
         end = start + fn_ms[i]
+        events.append({"t0": start, "t1": end, "stream": "compute", "fn": i})
         for v, dirty in zip(sch.reserve_out[i], sch.reserve_dirty[i]):
             t = max(d2h_free, end)
             if dirty or not elide_clean:
+                t0 = t
                 t = t + (d2h_us * 1e-3 + b[v] / (d2h_gbs * 1e6))
                 host_ready[v] = t
+                events.append({"t0": t0, "t1": t, "stream": "d2h", "dep": dep, "fn": i, "var": v})
             d2h_free = t
             out_done[v] = t
+            dep += 1
         for v in sch.free[i]:
             release(held.pop(v), end)
         end_prev = end
     makespan = end_prev
     for v in sch.end_wait:
         makespan = max(makespan, out_done[v])
-    return {"makespan_ms": makespan, "stall_ms": stall}
+    return {"makespan_ms": makespan, "stall_ms": stall, "events": events}

@@ -86,6 +86,7 @@ class oc_step_metrics(C.Structure):
 
 P = C.c_void_p
 E = C.POINTER(oc_err)
+OC_FN_HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_uint32, C.c_int)
 _SIGS = {
     "oc_strerror": (C.c_char_p, [C.c_int]),
     "oc_abi_version": (C.c_int, []),
@@ -102,6 +103,7 @@ _SIGS = {
     "oc_graph_fn_position": (C.c_uint32, [P, C.c_uint32]),
     "oc_graph_in_core_peak": (C.c_uint64, [P]),
     "oc_graph_footprint": (None, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "oc_graph_workspace_bytes": (C.c_uint64, [P]),
     "oc_plan_schedule": (C.c_int, [P, C.POINTER(oc_plan_params), C.POINTER(P), E]),
     "oc_schedule_destroy": (None, [P]),
     "oc_min_feasible_budget": (C.c_uint64, [P, C.c_uint64]),
@@ -127,6 +129,9 @@ _SIGS = {
     "oc_run_step": (C.c_int, [P, C.POINTER(oc_step_metrics), E]),
     "oc_exec_timeline": (C.c_int, [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "oc_exec_destroy": (None, [P]),
+    "oc_exec_set_timeline": (C.c_int, [P, C.c_int]),
+    "oc_exec_set_hook": (C.c_int, [P, OC_FN_HOOK, P]),
+    "oc_exec_read_var": (C.c_int, [P, C.c_uint32, P, C.c_uint64, E]),
     "oc_nccl_unique_id": (C.c_int, [P, E]),
     "oc_exec_attach_nccl": (C.c_int, [P, P, C.c_int, C.c_int, E]),
 }
@@ -246,6 +251,9 @@ class Graph:
 
     def in_core_peak(self):
         return lib().oc_graph_in_core_peak(self.h)
+
+    def workspace_bytes(self):
+        return lib().oc_graph_workspace_bytes(self.h)
 
     def footprint(self):
         t, m = C.c_uint64(), C.c_uint64()

@@ -117,6 +117,18 @@ double inter_len(const std::vector<Interval>& A, const std::vector<Interval>& B)
 
 }  // namespace
 
+// the largest per-function workspace of the graph's ops (oc_graph_workspace_bytes)
+size_t graph_workspace(const Graph& g) {
+  size_t ws = 0;
+  for (const Function& f : g.fns) {
+    if (f.op.kind != JVal::OBJ) continue;
+    const OpDesc* d = find_op(f.op.gets("kind"));
+    const JVal* attrs = f.op.get("attrs");
+    if (d && d->workspace && attrs) ws = std::max(ws, d->workspace(*attrs));
+  }
+  return ws;
+}
+
 struct Exec {
   int device = 0;
   const Graph* g = nullptr;
@@ -148,6 +160,7 @@ struct Exec {
   // timeline (opt.timeline)
   std::vector<cudaEvent_t> tl_fn0, tl_fn1, tl_in0, tl_in1, tl_out0, tl_out1;
   std::vector<uint8_t> tl_in_used, tl_out_used;
+  std::vector<int32_t> tl_in_ref, tl_out_ref;   // slot / departure whose events time this one (pack kernels)
   std::vector<KernelTimer> tl_k;   // per function: the contraction kernel launches
   // NCCL
   void* nccl_lib = nullptr;
@@ -155,6 +168,10 @@ struct Exec {
   void* nccl_allreduce = nullptr;
   void* nccl_destroy = nullptr;
   uint64_t step_index = 0;
+  // layer-local inspection hook (oc_exec_set_hook; tests only)
+  oc_fn_hook hook = nullptr;
+  void* hook_user = nullptr;
+  bool tl_created = false;   // timeline events exist (created with opt.timeline)
 
   Status create(int dev, const Graph* graph, const Schedule* sch, MemPool* m, const oc_streams& st,
                 const oc_exec_options* o);
@@ -341,7 +358,7 @@ Status Exec::create(int dev, const Graph* graph, const Schedule* sch, MemPool* m
   }
 
   // ops
-  size_t ws_need = 0;
+  size_t ws_need = graph_workspace(*g);
   for (uint32_t i = 0; i < n; ++i) {
     const Function& f = g->fns[i];
     if (f.op.kind != JVal::OBJ) continue;  // a function without compute (planner-only graphs)
@@ -381,8 +398,6 @@ Status Exec::create(int dev, const Graph* graph, const Schedule* sch, MemPool* m
         fns[i].role_vars[r].push_back(v);
       }
     }
-    const JVal* attrs = f.op.get("attrs");
-    if (d->workspace && attrs) ws_need = std::max(ws_need, d->workspace(*attrs));
   }
   ws_bytes = ws_need;
   if (ws_bytes) OC_CUDA(cudaMalloc(&ws, ws_bytes));
@@ -407,6 +422,7 @@ Status Exec::create(int dev, const Graph* graph, const Schedule* sch, MemPool* m
     OC_TRY(mk(tl_out0, deps.size(), true));
     OC_TRY(mk(tl_out1, deps.size(), true));
     tl_k.resize(n);
+    tl_created = true;
   }
   return Status::ok();
 }
@@ -428,6 +444,10 @@ Status Exec::run(oc_step_metrics* out) {
   uint32_t n_h2d = 0, n_d2h = 0, n_kernels = 0;
   tl_in_used.assign(slots.size(), 0);
   tl_out_used.assign(deps.size(), 0);
+  tl_in_ref.resize(slots.size());
+  tl_out_ref.resize(deps.size());
+  for (size_t k = 0; k < slots.size(); ++k) tl_in_ref[k] = (int32_t)k;
+  for (size_t k = 0; k < deps.size(); ++k) tl_out_ref[k] = (int32_t)k;
   auto ev_of = [&](const Ref& r) { return r.type == Ref::DONE ? ev_done[r.idx] : ev_out[r.idx]; };
 
   // The whole step is issued by `issue`: eagerly, or once into a CUDA graph
@@ -490,6 +510,7 @@ Status Exec::run(oc_step_metrics* out) {
       for (const Arrival& a : F.in) {
         Slot& sl = slots[a.slot];
         if (!sl.packed) continue;
+        if (opt.timeline) { tl_in_used[a.slot] = 1; tl_in_ref[a.slot] = first; }
         OC_CUDA(cudaEventRecord(ev_in[a.slot], hs));
         vars[sl.var].cur_slot = (int32_t)a.slot;
         vars[sl.var].need_wait = true;
@@ -512,6 +533,10 @@ Status Exec::run(oc_step_metrics* out) {
           xv.need_wait = false;
         }
       }
+    if (hook) {
+      OC_CUDA(cudaDeviceSynchronize());
+      hook(hook_user, i, 0);
+    }
     if (opt.timeline) OC_CUDA(cudaEventRecord(tl_fn0[i], cs));
     if (X.op) {
       OpArgs oa;
@@ -540,6 +565,10 @@ Status Exec::run(oc_step_metrics* out) {
       }
       n_kernels += oa.n_kernels;
     }
+    if (hook) {
+      OC_CUDA(cudaDeviceSynchronize());
+      hook(hook_user, i, 1);
+    }
     if (opt.timeline) OC_CUDA(cudaEventRecord(tl_fn1[i], cs));
     OC_CUDA(cudaEventRecord(ev_done[i], cs));
     // (c) reserved swap-outs after f_i; small ones through one pack kernel (A7)
@@ -548,14 +577,19 @@ Status Exec::run(oc_step_metrics* out) {
       if (ds2) OC_CUDA(cudaStreamWaitEvent(ds2, ev_done[i], 0));
     }
     if (X.pout_n) {
-      const uint32_t first = X.dep_reserve[0];
+      uint32_t first = X.dep_reserve[0];   // the pack kernel is timed on its first packed departure
+      for (uint32_t d : X.dep_reserve)
+        if (deps[d].packed) { first = d; break; }
       if (opt.timeline) { OC_CUDA(cudaEventRecord(tl_out0[first], ds)); tl_out_used[first] = 1; }
       OC_TRY(pack_launch(pack_tab + X.pout_off, (int)X.pout_n, ds));
       if (opt.timeline) OC_CUDA(cudaEventRecord(tl_out1[first], ds));
       ++n_d2h;
       ++n_kernels;
       for (uint32_t d : X.dep_reserve)
-        if (deps[d].packed) bytes_d2h += vars[deps[d].var].bytes;
+        if (deps[d].packed) {
+          bytes_d2h += vars[deps[d].var].bytes;
+          if (opt.timeline) { tl_out_used[d] = 1; tl_out_ref[d] = (int32_t)first; }
+        }
     }
     for (uint32_t d : X.dep_reserve) {
       const Dep& D = deps[d];
@@ -588,7 +622,7 @@ Status Exec::run(oc_step_metrics* out) {
   return Status::ok();
   };
 
-  if (opt.use_graph && !gexec && step_index >= 1 && !opt.timeline) {
+  if (opt.use_graph && !gexec && step_index >= 1 && !opt.timeline && !hook) {
     const uint64_t maps_before = mem->n_driver_map;
     OC_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
     Status st = issue();
@@ -602,7 +636,7 @@ Status Exec::run(oc_step_metrics* out) {
     g_bytes_h2d = bytes_h2d; g_bytes_d2h = bytes_d2h; g_n_h2d = n_h2d; g_n_d2h = n_d2h; g_n_kernels = n_kernels;
   }
   OC_CUDA(cudaEventRecord(ev_start, cs));
-  if (gexec) {
+  if (gexec && !hook && !opt.timeline) {
     OC_CUDA(cudaGraphLaunch(gexec, cs));
     bytes_h2d = g_bytes_h2d; bytes_d2h = g_bytes_d2h; n_h2d = g_n_h2d; n_d2h = g_n_d2h; n_kernels = g_n_kernels;
   } else {
@@ -731,6 +765,43 @@ int oc_run_step(oc_exec* x, oc_step_metrics* out, oc_err* err) {
   return st.code;
 }
 
+uint64_t oc_graph_workspace_bytes(const oc_graph* g) { return g ? graph_workspace(g->g) : 0; }
+
+int oc_exec_set_timeline(oc_exec* x, int on) {
+  if (!x || (on && !x->x.tl_created)) return OC_E_ARG;
+  x->x.opt.timeline = on ? 1 : 0;
+  return OC_OK;
+}
+
+int oc_exec_set_hook(oc_exec* x, oc_fn_hook hook, void* user) {
+  if (!x) return OC_E_ARG;
+  x->x.hook = hook;
+  x->x.hook_user = user;
+  return OC_OK;
+}
+
+int oc_exec_read_var(oc_exec* x, uint32_t var, void* host, uint64_t bytes, oc_err* err) {
+  if (!x || !host || var >= x->x.vars.size() || bytes > x->x.vars[var].bytes) {
+    Status::make(OC_E_ARG, "oc_exec_read_var: unknown variable or size").fill(err);
+    return OC_E_ARG;
+  }
+  void* d = x->x.addr_of(var);
+  if (!d) {
+    Status e = Status::make(OC_E_ARG, "oc_exec_read_var: variable " + x->x.g->var_names[var] + " is not resident");
+    e.var = var;
+    e.fill(err);
+    return OC_E_ARG;
+  }
+  cudaSetDevice(x->x.device);
+  cudaError_t ce = cudaMemcpy(host, d, bytes, cudaMemcpyDeviceToHost);
+  if (ce != cudaSuccess) {
+    Status s = cuda_status(ce, "oc_exec_read_var");
+    s.fill(err);
+    return s.code;
+  }
+  return OC_OK;
+}
+
 int oc_exec_timeline(oc_exec* xh, char* buf, size_t cap, size_t* need) {
   if (!xh) return OC_E_ARG;
   Exec& X = xh->x;
@@ -740,16 +811,26 @@ int oc_exec_timeline(oc_exec* xh, char* buf, size_t cap, size_t* need) {
     for (uint32_t i = 0; i < X.fns.size(); ++i)
       if (X.fns[i].op)
         o << "{\"t0\":" << t(X.tl_fn0[i]) << ",\"t1\":" << t(X.tl_fn1[i]) << ",\"stream\":\"compute\",\"id\":\""
-          << X.g->fns[i].name << "\",\"k_ms\":" << (i < X.tl_k.size() ? X.tl_k[i].ms() : 0.0f)
+          << X.g->fns[i].name << "\",\"fn\":" << i << ",\"k_ms\":" << (i < X.tl_k.size() ? X.tl_k[i].ms() : 0.0f)
           << ",\"k_n\":" << (i < X.tl_k.size() ? X.tl_k[i].used / 2 : 0) << "}\n";
+    // transfers: "slot" = arrival slot (allocator-replay order), "fn" = the
+    // function whose step (a) issued it; departures: "fn" = the function after
+    // which the swap-out was reserved (c), "slot" = the slot it leaves;
+    // "packed": moved by that function's pack/unpack kernel (one interval)
     for (size_t k = 0; k < X.slots.size(); ++k)
-      if (k < X.tl_in_used.size() && X.tl_in_used[k])
-        o << "{\"t0\":" << t(X.tl_in0[k]) << ",\"t1\":" << t(X.tl_in1[k]) << ",\"stream\":\"h2d\",\"id\":\""
-          << X.g->var_names[X.slots[k].var] << "\"}\n";
+      if (k < X.tl_in_used.size() && X.tl_in_used[k]) {
+        const int32_t r = X.tl_in_ref[k];
+        o << "{\"t0\":" << t(X.tl_in0[r]) << ",\"t1\":" << t(X.tl_in1[r]) << ",\"stream\":\"h2d\",\"id\":\""
+          << X.g->var_names[X.slots[k].var] << "\",\"slot\":" << k << ",\"fn\":" << X.slots[k].fn
+          << ",\"packed\":" << (X.slots[k].packed ? 1 : 0) << "}\n";
+      }
     for (size_t k = 0; k < X.deps.size(); ++k)
-      if (k < X.tl_out_used.size() && X.tl_out_used[k])
-        o << "{\"t0\":" << t(X.tl_out0[k]) << ",\"t1\":" << t(X.tl_out1[k]) << ",\"stream\":\"d2h\",\"id\":\""
-          << X.g->var_names[X.deps[k].var] << "\"}\n";
+      if (k < X.tl_out_used.size() && X.tl_out_used[k]) {
+        const int32_t r = X.tl_out_ref[k];
+        o << "{\"t0\":" << t(X.tl_out0[r]) << ",\"t1\":" << t(X.tl_out1[r]) << ",\"stream\":\"d2h\",\"id\":\""
+          << X.g->var_names[X.deps[k].var] << "\",\"dep\":" << k << ",\"fn\":" << X.deps[k].fn
+          << ",\"slot\":" << X.deps[k].slot << ",\"packed\":" << (X.deps[k].packed ? 1 : 0) << "}\n";
+      }
   }
   std::string j = o.str();
   if (need) *need = j.size();

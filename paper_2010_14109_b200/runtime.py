@@ -92,6 +92,12 @@ class OutOfCoreStep:
         B.check(B.lib().oc_run_step(self.exec, C.byref(m), C.byref(err)), err)
         return {k: getattr(m, k) for k, _ in B.oc_step_metrics._fields_}
 
+    def set_timeline(self, on):
+        """Per-event timeline on/off for the next steps (created with timeline=True)."""
+        rc = B.lib().oc_exec_set_timeline(self.exec, 1 if on else 0)
+        if rc != B.OC_OK:
+            raise RuntimeError("set_timeline: the executor was created without timeline events")
+
     def timeline(self):
         need = C.c_size_t()
         B.lib().oc_exec_timeline(self.exec, None, 0, C.byref(need))
@@ -103,6 +109,26 @@ class OutOfCoreStep:
         s = B.oc_mem_stats()
         B.lib().oc_mem_get_stats(self.mem, C.byref(s))
         return {k: getattr(s, k) for k, _ in B.oc_mem_stats._fields_}
+
+    # ------------------------------------------------ layer-local inspection
+    def set_hook(self, fn):
+        """fn(position, phase) is called before (0) and after (1) the kernels of
+        each function, device synchronised, eager issue (oc_exec_set_hook).
+        None removes it."""
+        if fn is None:
+            self._hook = B.OC_FN_HOOK()
+        else:
+            self._hook = B.OC_FN_HOOK(lambda user, i, phase: fn(int(i), int(phase)))
+        B.check(B.lib().oc_exec_set_hook(self.exec, self._hook, None), B.oc_err())
+
+    def read_device(self, name, dtype=np.uint8):
+        """Current device bytes of a resident (or pinned) variable (oc_exec_read_var)."""
+        n = self.var_bytes[name]
+        out = np.empty(n, dtype=np.uint8)
+        err = B.oc_err()
+        B.check(B.lib().oc_exec_read_var(self.exec, self.id[name], out.ctypes.data_as(C.c_void_p), n,
+                                         C.byref(err)), err)
+        return out.view(dtype)
 
     def attach_nccl(self, uid_bytes, rank, nranks):
         err = B.oc_err()
