@@ -1,23 +1,35 @@
 """Benchmark of the out-of-core training step (BASELINE.json metric:
 "samples/sec at k× in-budget batch vs in-core; host-link GB/s; overlap %").
 
-Default workload (N=1): configs[1] — ResNet-18, 224×224 synthetic images,
-batch 256, budget fixed at 25% of the in-core footprint F_peak (reading Z21),
-schedule-window = the largest feasible (Z12), VA allocator with 2 MiB chunks.
-One step = forward + backward + update of the whole network through the
-C-ABI (oc_run_step), inputs swapped in from pinned host memory as part of the
-schedule.
+Default workload (N=1): configs[2] — ResNet-50, 224×224 synthetic images,
+per GPU a fixed PHYSICAL device budget B_p = 8 GiB ("else
+B = 8 GiB"; the paper's fixed 16 GB V100) that holds everything the
+step puts on the device: pinned variables + the VA swap pool + the
+executor's compute workspace.  b0 = the largest batch whose in-core step
+(footprint F_peak + workspace) fits B_p; the step runs at the paper's
+1440-equivalent batch round(1440/190 · b0) (7.5× over the
+in-core maximum).  The scheduler budget B_s is the largest one whose
+allocator replay fits the pool B_p − pinned − workspace (Fig.3's "maximum
+defined memory budget"), window 0 (the measured best on this
+link-bound step), VA allocator with 2 MiB chunks.  One step = forward +
+backward + update of the whole network through the C-ABI (oc_run_step),
+inputs and parameters swapped in from pinned host memory as part of the
+schedule.  Retention = samples/s ÷ in-core samples/s at b0 (the paper's
+55 % = 321/581).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config r18|r50|mlp] [--mode va|best|first]
+                    [--config r50|r18|mlp|unet|r1001|biggan|densenet] [--mode va|best|first]
 
-Multi-GPU: one process per GPU (torchrun), each replica with its own budget,
-pool and host link (weak scaling); gradients averaged with NCCL inside the
-step.  Rank 0 prints ONE JSON line.
+--config r18: configs[1] (ResNet-18 b=256, B_p = 25 % of the in-core footprint).
+Multi-GPU: one process per GPU (torchrun; `--gpus N` spawns it when
+WORLD_SIZE is unset), each replica with its own budget, pool and host link
+(weak scaling); gradients averaged with NCCL inside the step.  Rank 0 prints
+ONE JSON line.
 """
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -29,8 +41,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 MiB = 1 << 20
+GiB = 1 << 30
 PCIE5_X16_GBS = 63.0          # 32 GT/s × 16 × 128/130 / 8, per direction
 FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # derived peak for FFMA kernels
+PAPER_MULTIPLE = 1440 / 190   # batch 1440 = 7.5× the in-core maximum 190
 
 
 def parse():
@@ -39,64 +53,83 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="r18", choices=["r18", "r50", "r1001", "mlp", "biggan", "unet", "densenet"])
+    ap.add_argument("--config", default="r50", choices=["r50", "r18", "r1001", "mlp", "biggan", "unet", "densenet"])
     ap.add_argument("--mode", default="va", choices=["va", "best", "first"])
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--phys-gib", type=float, default=8.0, help="r50: physical device budget per GPU (GiB)")
+    ap.add_argument("--multiple", type=float, default=PAPER_MULTIPLE, help="r50: batch = multiple × b0")
     ap.add_argument("--budget-frac", type=float, default=None,
-                    help="budget as a fraction of F_peak (default: 0.125 for configs[3] U-Net, else 0.25)")
+                    help="other configs: physical budget as a fraction of the in-core footprint "
+                         "(default 0.125 for configs[3] U-Net, else 0.25)")
     ap.add_argument("--chunk-mib", type=int, default=2)
+    ap.add_argument("--bucket-mib", type=int, default=25,
+                    help="N > 1: gradient allreduce bucket size (one ncclGroup on the comm stream per bucket)")
     ap.add_argument("--no-incore", action="store_true")
-    ap.add_argument("--window", default="auto", help="auto (timed probes) | model (makespan model, F4) | max | <bytes>")
+    ap.add_argument("--window", default=None,
+                    help="auto (timed probes) | model (makespan model, F4) | max | <bytes>; default 0 for r50, "
+                         "auto otherwise")
     ap.add_argument("--no-graph", action="store_true", help="issue every step eagerly (no CUDA graph replay)")
     ap.add_argument("--policy", default="paper", choices=["paper", "vdnn", "lms"],
                     help="swap-timing window: the paper's byte window, or the prior-art function-distance "
                          "window (vdnn = 1 function ahead, lms = --distance functions ahead; SURVEY F1)")
     ap.add_argument("--distance", type=int, default=3, help="lms policy: functions of look-ahead")
+    ap.add_argument("--trigger", default="release", choices=["release", "paper"],
+                    help="arrival trigger: at the release of the reused memory (executor default) or at the "
+                         "end of f_{i-1} as the paper's Fig.2 (P:91)")
     a = ap.parse_args()
     if a.budget_frac is None:
         a.budget_frac = 0.125 if a.config == "unet" else 0.25
+    if a.window is None:
+        a.window = "0" if a.config == "r50" else "auto"
     return a
 
 
-def config(args):
+# ----------------------------------------------------------------- workloads
+def spec_for(args, batch=None):
     from synth import nets
-    if args.config == "mlp":
-        spec = nets.mlp6()
-        return spec, {"workload": "configs[0] 6-layer MLP fp32 b=8, 4 MiB budget", "budget": 4 * MiB}
-    if args.config == "r50":
-        b = args.batch or 256
-        spec = nets.resnet(50, batch=b)
-        return spec, {"workload": f"ResNet-50 224x224 b={b} at {args.budget_frac:.2f} of F_peak"}
-    if args.config == "densenet":
-        # the paper's second family (Fig.4/5), DenseNet-121 224²
-        b = args.batch or 128
-        spec = nets.densenet(batch=b)
-        return spec, {"workload": f"F3 DenseNet-121 224x224 b={b} at {args.budget_frac:.2f} of F_peak"}
-    if args.config == "unet":
-        # configs[3]: U-Net 1024² b=8 at 1/8 of F_peak (pass --budget-frac 0.125)
-        b = args.batch or 8
-        spec = nets.unet(batch=b, image=1024)
-        return spec, {"workload": f"configs[3] U-Net 1024x1024 base 64 depth 4, 19 classes, b={b} at "
-                                  f"{args.budget_frac:.3f} of F_peak"}
-    if args.config == "biggan":
-        b = args.batch or 32
-        spec = nets.biggan(batch=b)
-        return spec, {"workload": f"configs[4] BigGAN-style 128x128 ch=96 GAN step (D-step + G-step) b={b} at "
-                                  f"{args.budget_frac:.2f} of F_peak"}
-    if args.config == "r1001":
-        # b=256: every activation is >= 2 MiB (one VA chunk); tensors below one
-        # chunk (parameters, optimizer state, BN statistics) stay resident (Z26)
-        b = args.batch or 256
-        spec = nets.preact_resnet(1001, batch=b)
-        return spec, {"workload": f"configs[4] pre-activation ResNet-1001 32x32 b={b} at {args.budget_frac:.2f} "
-                                  "of F_peak, tensors < 1 VA chunk pinned", "pin_below": args.chunk_mib * MiB}
-    b = args.batch or 256
-    spec = nets.resnet(18, batch=b)
-    # tensors under 1 MiB (BN parameters, small weights and their optimizer
-    # state: 12.9 MB) stay resident (Z26): ~140 fewer sub-MB copies per step,
-    # which run far below the link rate (tools/link_profile.py)
-    return spec, {"workload": f"configs[1] ResNet-18 224x224 b={b}, budget {args.budget_frac:.2f} x in-core footprint, "
-                              "tensors < 1 MiB pinned", "pin_below": 1 << 20}
+    c = args.config
+    if c == "mlp":
+        return nets.mlp6()
+    if c == "r50":
+        return nets.resnet(50, batch=batch or args.batch or 256)
+    if c == "densenet":      # the paper's second family (Fig.4/5), DenseNet-121 224²
+        return nets.densenet(batch=batch or args.batch or 128)
+    if c == "unet":          # configs[3]: U-Net 1024² b=8
+        return nets.unet(batch=batch or args.batch or 8, image=1024)
+    if c == "biggan":
+        return nets.biggan(batch=batch or args.batch or 32)
+    if c == "r1001":
+        return nets.preact_resnet(1001, batch=batch or args.batch or 256)
+    return nets.resnet(18, batch=batch or args.batch or 256)
+
+
+def pin_below_for(args):
+    # tensors under one threshold (BN parameters, small weights, their optimizer
+    # state) stay resident (Z26); R50 keeps the paper-literal
+    # all-swappable graph (Table 1)
+    return {"r18": MiB, "r1001": args.chunk_mib * MiB}.get(args.config, 0)
+
+
+def workload_name(args, spec, B_p, b0):
+    c = args.config
+    if c == "r50":
+        return (f"configs[2] ResNet-50 224x224 b={spec['batch']} = {spec['batch'] / b0:.2f} x b0 (b0 = {b0}, the "
+                f"in-core maximum under B_p = {B_p / GiB:.2f} GiB physical per GPU)")
+    if c == "r18":
+        return (f"configs[1] ResNet-18 224x224 b={spec['batch']}, physical budget {args.budget_frac:.2f} x in-core "
+                "footprint, tensors < 1 MiB pinned")
+    if c == "mlp":
+        return "configs[0] 6-layer MLP fp32 b=8, 4 MiB scheduler budget"
+    if c == "unet":
+        return (f"configs[3] U-Net 1024x1024 base 64 depth 4, 19 classes, b={spec['batch']} at "
+                f"{args.budget_frac:.3f} of the in-core footprint")
+    if c == "biggan":
+        return (f"configs[4] BigGAN-style 128x128 ch=96 GAN step (D-step + G-step) b={spec['batch']} at "
+                f"{args.budget_frac:.2f} of the in-core footprint")
+    if c == "r1001":
+        return (f"configs[4] pre-activation ResNet-1001 32x32 b={spec['batch']} at {args.budget_frac:.2f} of the "
+                "in-core footprint, tensors < 1 VA chunk pinned")
+    return f"F3 DenseNet-121 224x224 b={spec['batch']} at {args.budget_frac:.2f} of the in-core footprint"
 
 
 class Clocks:
@@ -141,41 +174,119 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def trainable_batch(spec_fn, budget, lo=1, hi=4096, params="pinned"):
-    """Largest batch whose IN-CORE footprint fits `budget` (bisection on the
-    planner's F_peak) — the denominator of the trainable-batch multiple."""
+# ----------------------------------------------------------- memory budgets
+def in_core_device_bytes(spec):
+    """Device bytes of the IN-CORE step: F_peak with parameters, gradients and
+    momentum resident, plus the executor workspace."""
     from paper_2010_14109_b200 import binding as B
     from paper_2010_14109_b200 import graphs
+    doc, _ = graphs.build(spec, params="pinned")
+    G = B.Graph(doc)
+    return G.in_core_peak() + G.workspace_bytes()
 
-    def fits(b):
-        doc, _ = graphs.build(spec_fn(b), params=params)
-        return B.Graph(doc).in_core_peak() <= budget
-    if not fits(lo):
+
+def trainable_batch(spec_fn, phys, lo=1, hi=8192):
+    """b0: the largest batch whose in-core step fits `phys` device bytes
+    (bisection) — the denominator of the trainable-batch multiple."""
+    if in_core_device_bytes(spec_fn(lo)) > phys:
         return 0
     while lo < hi:
         mid = (lo + hi + 1) // 2
-        if fits(mid):
+        if in_core_device_bytes(spec_fn(mid)) <= phys:
             lo = mid
         else:
             hi = mid - 1
     return lo
 
 
-def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None, pack=64 << 10, use_graph=False,
-               distance=0):
-    import torch
+def fit_budget(G, pool, mode, chunk, W=0, distance=0):
+    """Largest scheduler budget B_s whose allocator replay fits a swap pool of
+    `pool` physical bytes (Fig.3 'maximum defined memory budget'); None if
+    even the minimum feasible budget does not fit."""
     from paper_2010_14109_b200 import binding as B
+    m = {"va": B.OC_ALLOC_VA, "best": B.OC_ALLOC_ARENA_BEST, "first": B.OC_ALLOC_ARENA_FIRST}[mode]
+    lo = G.min_feasible_budget(W, distance=distance) if distance else G.min_feasible_budget(W)
+
+    def fits(b):
+        return G.plan(b, W, m, chunk_bytes=chunk, phys_bytes=pool, allow_oom=True,
+                      distance=distance).stats()["oom_fn"] < 0
+    if not fits(lo):
+        return None
+    pinned = G.plan(lo, W, m, chunk_bytes=chunk, phys_bytes=pool, allow_oom=True, distance=distance).stats()[
+        "pinned_bytes"]
+    hi = pinned + pool + 1
+    if fits(hi):
+        return hi
+    while hi - lo > MiB:
+        mid = (lo + hi) // 2
+        if fits(mid):
+            lo = mid
+        else:
+            hi = mid
+    return lo
+
+
+def host_ram_bytes():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def host_copy_bytes(doc, sched_json):
+    """Pinned host bytes the executor allocates: persistent swappable
+    variables and every variable the schedule ever swaps out."""
+    d = json.loads(doc)
+    s = json.loads(sched_json)
+    need = {i for i, v in enumerate(d["variables"]) if v.get("persistent") and not v.get("pinned")}
+    for f in s["fn"]:
+        need.update(f["reserve_out"])
+    return sum((d["variables"][i]["bytes"] + 255) // 256 * 256 for i in need)
+
+
+def link_probe(nbytes=256 * MiB):
+    """Pinned host <-> device copy bandwidth on this box, per direction and
+    duplex (GB/s, CUDA events): the link roofline's denominators."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    out = {}
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        best = 1e9
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s1):
+                e0.record()
+                fn()
+                e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out[name] = nbytes / (best / 1e3) / 1e9
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with torch.cuda.stream(s1):
+        d.copy_(h, non_blocking=True)
+    with torch.cuda.stream(s2):
+        h2.copy_(d2, non_blocking=True)
+    torch.cuda.synchronize()
+    out["duplex"] = 2 * nbytes / (time.perf_counter() - t0) / 1e9
+    return out
+
+
+# ----------------------------------------------------------------- setup
+def new_step(spec, info, doc, budget, mode, chunk, phys, window, timeline=False, pack=64 << 10, use_graph=False,
+             distance=0, trigger=0):
+    import torch
     from paper_2010_14109_b200.runtime import OutOfCoreStep
     from synth import nets
-    G = B.Graph(doc)
-    W = window if window is not None else G.max_feasible_window(budget)
-    # VA physical pool: scheduler budget + chunk rounding headroom (Eq.2: IF < N_max·m_c)
-    probe = G.plan(budget, W, B.OC_ALLOC_VA if mode == "va" else B.OC_ALLOC_ARENA_BEST, chunk_bytes=chunk,
-                   phys_bytes=budget * 4, allow_oom=True, distance=distance)
-    ps = probe.stats()
-    phys = ps["peak_phys"] + chunk if mode == "va" else max(ps["peak_phys"], 1)
-    st = OutOfCoreStep(doc, budget, W, mode=mode, chunk_bytes=chunk, phys_bytes=phys, timeline=timeline,
-                       pack_threshold=pack, use_graph=use_graph, distance=distance)
+    st = OutOfCoreStep(doc, budget, window, mode=mode, chunk_bytes=chunk, phys_bytes=phys, timeline=timeline,
+                       pack_threshold=pack, use_graph=use_graph, distance=distance, trigger=trigger)
     if "G" in spec:          # GAN step: noise, real images, G and D parameters
         pG, pD = nets.make_gan_params(spec)
         z1, z2, xr = nets.make_gan_inputs(spec)
@@ -186,18 +297,30 @@ def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None,
             for k, v in pp.items():
                 st.write(info[net]["params"][k], v)
                 st.write(info[net]["momentum"][k], np.zeros_like(v))
-        return st, W, phys
+        return st
     x, y = nets.make_inputs(spec)
     p = nets.make_params(spec)
-    if spec["mode"] == "bf16":
-        xb = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy()
-    else:
-        xb = x
-    st.write(info["x"], xb)
+    st.write(info["x"], torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy()
+             if spec["mode"] == "bf16" else x)
     st.write(info["labels"], y)
     for k, v in p.items():
         st.write(info["params"][k], v)
         st.write(info["momentum"][k], np.zeros_like(v))
+    return st
+
+
+def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None, pack=64 << 10, use_graph=False,
+               distance=0):
+    """Scheduler budget -> executor with the pool sized to the replay's
+    physical peak (tools: sweeps that fix B_s rather than B_p)."""
+    from paper_2010_14109_b200 import binding as B
+    G = B.Graph(doc)
+    W = window if window is not None else G.max_feasible_window(budget)
+    probe = G.plan(budget, W, B.OC_ALLOC_VA if mode == "va" else B.OC_ALLOC_ARENA_BEST, chunk_bytes=chunk,
+                   phys_bytes=budget * 4, allow_oom=True, distance=distance)
+    ps = probe.stats()
+    phys = ps["peak_phys"] + chunk if mode == "va" else max(ps["peak_phys"], 1)
+    st = new_step(spec, info, doc, budget, mode, chunk, phys, W, timeline, pack, use_graph, distance)
     return st, W, phys
 
 
@@ -220,152 +343,231 @@ def conv_flops(doc):
     return fl
 
 
+def time_steps(st, steps, warmup, world):
+    import torch
+    import torch.distributed as dist
+    for _ in range(warmup):
+        st.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0.record(st.streams[0])
+    mets = [st.step() for _ in range(steps)]
+    e1.record(st.streams[0])
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    return e0.elapsed_time(e1), (t1 - t0) * 1e3, mets
+
+
+def max_over_ranks(vals, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64)
+    if world > 1:
+        t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = t.cpu()
+    return [float(x) for x in t]
+
+
+def attach(st, rank, world):
+    import torch.distributed as dist
+    from paper_2010_14109_b200.runtime import nccl_unique_id
+    if world <= 1:
+        return
+    uid = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    st.attach_nccl(uid[0], rank, world)
+
+
+def in_core_rate(args, spec, rank, world, chunk, steps):
+    """In-core step at this spec's batch: no swapping at all — parameters,
+    gradients and momentum device-resident, budget = F_peak, W = 0, best-fit
+    arena; NCCL attached for N > 1 (same exchange as the out-of-core step);
+    samples/s over all ranks from the max-over-ranks device time."""
+    import torch
+    from paper_2010_14109_b200 import binding as B
+    from paper_2010_14109_b200 import graphs
+    torch.cuda.empty_cache()
+    doc_p, info_p = graphs.build(spec, params="pinned", inputs="host")
+    G_p = B.Graph(doc_p)
+    F_p = G_p.in_core_peak()
+    # the best-fit arena's carved peak (fragmentation included) sizes the slab
+    slab = G_p.plan(F_p, 0, B.OC_ALLOC_ARENA_BEST, chunk_bytes=chunk, phys_bytes=1 << 50,
+                    allow_oom=True).stats()["peak_phys"]
+    st2 = new_step(spec, info_p, doc_p, F_p, "best", chunk, slab, 0, use_graph=not args.no_graph)
+    attach(st2, rank, world)
+    ms, _, _ = time_steps(st2, max(3, steps // 2), max(1, args.warmup), world)
+    st2.close()
+    ms = max_over_ranks([ms], world)[0]
+    return spec["batch"] * world * max(3, steps // 2) / (ms / 1e3)
+
+
+# ------------------------------------------------------------------ our arm
 def run_ours(args, rank, world):
     import torch
     import torch.distributed as dist
     from paper_2010_14109_b200 import binding as B
     from paper_2010_14109_b200 import graphs
-    from paper_2010_14109_b200.runtime import nccl_unique_id
     from synth import nets
 
-    spec, cfg = config(args)
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
     chunk = args.chunk_mib * MiB
-    params = "persistent"
-    doc, info = graphs.build(spec, params=params, inputs="host", pin_below=cfg.get("pin_below", 0))
-    G = B.Graph(doc)
-    F_peak = G.in_core_peak()
-    budget = cfg.get("budget") or int(F_peak * args.budget_frac)
-    # schedule-window: the paper's single hyperparameter, "decided experimentally"
-    # (P:120-style); auto = best of a few fractions of the largest feasible W
-    wmax = G.max_feasible_window(budget)
-    window_probe = []
     dist_ = {"paper": 0, "vdnn": 1, "lms": args.distance}[args.policy]
-    if dist_:
-        W_sel = 0
-    elif args.window == "auto":
-        best = None
-        for wf in (0.0, 0.25, 0.5, 1.0):
-            Wc = int(wmax * wf)
-            stc, _, _ = setup_step(spec, info, doc, budget, args.mode, chunk, timeline=False, window=Wc)
-            stc.step()
-            ms = float(np.mean([stc.step()["step_ms"] for _ in range(2)]))
-            stc.close()
-            window_probe.append({"window": Wc, "ms": ms})
-            if best is None or ms < best[1]:
-                best = (Wc, ms)
-        W_sel = best[0]
-    elif args.window == "model":
-        # F4: choose W with the makespan model instead of timed probes — one
-        # instrumented step gives the per-function compute times (independent
-        # of the schedule), oc_simulate ranks 16 candidate windows
-        stc, _, _ = setup_step(spec, info, doc, budget, args.mode, chunk, timeline=True, window=0)
-        stc.step()
-        mc = stc.step()
-        bh = mc["bytes_h2d"] / max(mc["h2d_busy_ms"], 1e-9) / 1e6 or 55.6
-        bd = mc["bytes_d2h"] / max(mc["d2h_busy_ms"], 1e-9) / 1e6 or 57.3
-        fid = [f["id"] for f in json.loads(doc)["functions"]]
-        dur = {}
-        for ev in stc.timeline():
-            if ev["stream"] == "compute":
-                dur[ev["id"]] = dur.get(ev["id"], 0.0) + (ev["t1"] - ev["t0"])
-        stc.close()
-        fn_ms = [dur.get(f, 0.0) for f in fid]
-        best = None
-        for k in range(16):
-            Wc = int(wmax * k / 15)
-            sc = G.plan(budget, Wc, B.OC_ALLOC_VA if args.mode == "va" else B.OC_ALLOC_ARENA_BEST,
-                        chunk_bytes=chunk, phys_bytes=budget * 4, allow_oom=True)
-            pred = sc.simulate(fn_ms, bh, bd, 0.0, 0.0, True, model=1)["makespan_ms"]
-            window_probe.append({"window": Wc, "predicted_ms": pred})
-            if best is None or pred < best[1]:
-                best = (Wc, pred)
-        W_sel = best[0]
-    elif args.window == "max":
-        W_sel = wmax
+    trigger = 1 if args.trigger == "paper" else 0
+    mode = args.mode
+    ram = host_ram_bytes()
+    notes = []
+
+    # ---- physical budget, batch, scheduler budget
+    b0 = None
+    if args.config == "mlp":
+        spec = spec_for(args)
+        doc, info = graphs.build(spec, params="persistent", inputs="host")
+        G = B.Graph(doc)
+        F_peak, ws = G.in_core_peak(), G.workspace_bytes()
+        W0 = 0
+        B_s = 4 * MiB   # configs[0]: the scheduler budget itself (all variables swappable)
+        probe = G.plan(B_s, B.OC_WINDOW_MAX_FEASIBLE, B.OC_ALLOC_ARENA_BEST if mode != "va" else B.OC_ALLOC_VA,
+                       chunk_bytes=chunk, phys_bytes=B_s * 64, allow_oom=True).stats()
+        pinned = probe["pinned_bytes"]
+        pool = probe["peak_phys"] + (chunk if mode == "va" else 0)
+        B_p = pinned + pool + ws
     else:
-        W_sel = int(args.window)
+        B_p = None
+        for attempt in range(6):
+            if args.config == "r50":
+                B_p = B_p or int(args.phys_gib * GiB)
+                b0 = trainable_batch(lambda b: spec_for(args, b), B_p)
+                spec = spec_for(args, args.batch or max(1, int(round(args.multiple * b0))))
+            else:
+                spec = spec_for(args)
+            doc, info = graphs.build(spec, params="persistent", inputs="host", pin_below=pin_below_for(args),
+                                     dp_bucket_bytes=(args.bucket_mib * MiB if world > 1 and "G" not in spec else 0))
+            G = B.Graph(doc)
+            F_peak, ws = G.in_core_peak(), G.workspace_bytes()
+            if args.config != "r50":
+                B_p = B_p or int(args.budget_frac * (F_peak + ws))
+                b0 = trainable_batch(lambda b: spec_for(args, b), B_p) if "G" not in spec else None
+            probe = G.plan(G.min_feasible_budget(0), 0, B.OC_ALLOC_VA, chunk_bytes=chunk, phys_bytes=1 << 50,
+                           allow_oom=True).stats()
+            pinned = probe["pinned_bytes"]
+            pool = B_p - pinned - ws
+            pool = pool // chunk * chunk if mode == "va" else pool
+            if pool <= 0:
+                raise RuntimeError(f"physical budget {B_p} B cannot hold pinned {pinned} + workspace {ws}")
+            if args.config != "r50" and fit_budget(G, pool, mode, chunk, 0) is None:
+                # the fraction is below what any schedule can run in once the pinned
+                # bytes, the workspace and the allocator's granularity are counted:
+                # raise B_p to the smallest physical budget that runs, and say so
+                lo, hi = B_p, int(F_peak + ws)
+                while hi - lo > MiB:
+                    mid = (lo + hi) // 2
+                    pm = (mid - pinned - ws) // chunk * chunk if mode == "va" else mid - pinned - ws
+                    if pm > 0 and fit_budget(G, pm, mode, chunk, 0) is not None:
+                        hi = mid
+                    else:
+                        lo = mid
+                notes.append(f"{args.budget_frac:.3f} x footprint = {B_p} B cannot hold the minimum feasible "
+                             f"schedule + pinned + workspace; B_p raised to {hi} B = "
+                             f"{hi / (F_peak + ws):.3f} x footprint")
+                B_p = hi
+                pool = (B_p - pinned - ws) // chunk * chunk if mode == "va" else B_p - pinned - ws
+            host_est = sum(v["bytes"] for v in json.loads(doc)["variables"] if not v.get("pinned"))
+            if world > 1 and ram and world * host_est > 0.8 * ram and args.config == "r50" and not args.batch:
+                # SURVEY H7: N replicas share the host's RAM — shrink the per-GPU budget until they fit
+                B_p = int(B_p * 0.8 * ram / (world * host_est) * 0.95)
+                notes.append(f"B_p scaled to {B_p / GiB:.2f} GiB so that {world} x host copies fit host RAM")
+                continue
+            break
+        W0 = 0
+    # schedule-window: the paper's single hyperparameter, "decided experimentally"
+    window_probe = []
+    if args.config == "mlp":
+        B_s_of = {}
+        W_sel = int(args.window) if args.window.isdigit() else G.max_feasible_window(B_s)
+    else:
+        B_s0 = fit_budget(G, pool, mode, chunk, 0, dist_)
+        if B_s0 is None:
+            raise RuntimeError(f"no scheduler budget fits the {pool} B pool (min feasible "
+                               f"{G.min_feasible_budget(0)} B)")
+        wmax = G.max_feasible_window(B_s0)
+        if dist_:
+            W_sel = 0
+        elif args.window == "auto":
+            best = None
+            for wf in (0.0, 0.25, 0.5, 1.0):
+                Wc = int(wmax * wf)
+                Bc = fit_budget(G, pool, mode, chunk, Wc)
+                if Bc is None:
+                    continue
+                stc = new_step(spec, info, doc, Bc, mode, chunk, pool, Wc)
+                stc.step()
+                ms = float(np.mean([stc.step()["step_ms"] for _ in range(2)]))
+                stc.close()
+                window_probe.append({"window": Wc, "budget": Bc, "ms": ms})
+                if best is None or ms < best[1]:
+                    best = (Wc, ms)
+            W_sel = best[0]
+        elif args.window == "max":
+            W_sel = wmax
+        else:
+            W_sel = int(args.window)
+        B_s = fit_budget(G, pool, mode, chunk, W_sel, dist_)
     if world > 1:   # every replica runs the identical schedule (SURVEY §8(e))
         sel = [W_sel]
         dist.broadcast_object_list(sel, src=0)
         W_sel = sel[0]
-    # timed steps run without per-event instrumentation (timing events between
-    # back-to-back copies cost ~6% of the step); a second, instrumented pass
-    # below measures overlap, link busy time and the per-kernel durations
-    # the timed steps replay the step as one CUDA graph (captured after the first
-    # warm-up step memoised every VA mapping); --no-graph issues it eagerly
-    st, W, phys = setup_step(spec, info, doc, budget, args.mode, chunk, timeline=False, window=W_sel,
-                             use_graph=not args.no_graph, distance=dist_)
-    uid = None
+
+    # one executor serves the timed pass (CUDA-graph replay, no per-event
+    # timing) and the instrumented pass (timeline events, eager issue)
+    st = new_step(spec, info, doc, B_s, mode, chunk, pool, W_sel, timeline=True, use_graph=not args.no_graph,
+                  distance=dist_, trigger=trigger)
+    host_bytes = host_copy_bytes(doc, st.sched.json())
+    host_pool_bytes, host_numa = st.host_info()
     if world > 1:
-        # every replica must run the identical schedule: compare
-        # the canonical schedule bytes across ranks before the first step
         import hashlib
         hs = [None] * world
         dist.all_gather_object(hs, hashlib.sha256(st.sched.json().encode()).hexdigest())
         if len(set(hs)) != 1:
             raise RuntimeError(f"ranks planned different schedules: {hs}")
-        uid = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        st.attach_nccl(uid[0], rank, world)
-    for _ in range(args.warmup):
-        st.step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    mets = []
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    attach(st, rank, world)
+    st.set_timeline(False)
     with Clocks(dev) as clk:
-        torch.cuda.synchronize()
-        t_wall0 = time.perf_counter()
-        e0.record(st.streams[0])
-        for _ in range(args.steps):
-            mets.append(st.step())
-        e1.record(st.streams[0])
-        torch.cuda.synchronize()
-        t_wall1 = time.perf_counter()
-    if world > 1:
-        dist.barrier()
-    dev_ms = e0.elapsed_time(e1)
+        dev_ms, wall_ms, mets = time_steps(st, args.steps, args.warmup, world)
     loss = float(st.read(info["loss_g" if "G" in spec else "loss"])[0])
     ss = st.stats
     mstat = st.mem_stats()
     n_k = int(sum(m["n_kernels"] for m in mets))
     h2d = float(np.mean([m["bytes_h2d"] for m in mets]))
     d2h = float(np.mean([m["bytes_d2h"] for m in mets]))
+    # instrumented pass: same executor, CUDA events around every function and transfer
+    st.set_timeline(True)
+    st.step()
+    mets_i = [st.step() for _ in range(3)]
+    tl = st.timeline()
     st.close()
-    # instrumented pass: identical schedule, CUDA events around every function and transfer
-    sti, _, _ = setup_step(spec, info, doc, budget, args.mode, chunk, timeline=True, window=W_sel, distance=dist_)
-    if world > 1:
-        uid2 = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid2, src=0)
-        sti.attach_nccl(uid2[0], rank, world)
-    sti.step()
-    mets_i = [sti.step() for _ in range(3)]
-    tl = sti.timeline()
-    # makespan model (oc_simulate) fed with this pass's per-function
-    # compute durations and the measured link rates: predicted vs measured step
     fid = [f["id"] for f in json.loads(doc)["functions"]]
+    vbytes = {v["id"]: v["bytes"] for v in json.loads(doc)["variables"]}
     dur = {}
     for ev in tl:
         if ev["stream"] == "compute":
-            dur[ev["id"]] = dur.get(ev["id"], 0.0) + (ev["t1"] - ev["t0"])   # last instrumented step
+            dur[ev["id"]] = dur.get(ev["id"], 0.0) + (ev["t1"] - ev["t0"])
     fn_ms = [dur.get(f, 0.0) for f in fid]
-    # link rates calibrated on this pass: bytes over busy copy time per direction
     bw_h = float(np.mean([m["bytes_h2d"] / max(m["h2d_busy_ms"], 1e-9) for m in mets_i])) / 1e6
     bw_d = float(np.mean([m["bytes_d2h"] / max(m["d2h_busy_ms"], 1e-9) for m in mets_i])) / 1e6
-    bw_h = bw_h if bw_h > 1 else 55.6
-    bw_d = bw_d if bw_d > 1 else 57.3
-    sim = sti.sched.simulate(fn_ms, bw_h, bw_d, 0.0, 0.0, True, model=1)
-    sim0 = sti.sched.simulate(fn_ms, bw_h, bw_d, 0.0, 0.0, True, model=0)
-    sti.close()
-    ms = torch.tensor([dev_ms, (t_wall1 - t_wall0) * 1e3], dtype=torch.float64)
-    if world > 1:
-        ms = ms.cuda()
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-        ms = ms.cpu()
-    dev_ms, wall_ms = float(ms[0]), float(ms[1])
+    link = link_probe()
+    bw_h = bw_h if bw_h > 1 else link["h2d"]
+    bw_d = bw_d if bw_d > 1 else link["d2h"]
+    sim = st.sched.simulate(fn_ms, bw_h, bw_d, 0.0, 0.0, True, model=1)
+    sim0 = st.sched.simulate(fn_ms, bw_h, bw_d, 0.0, 0.0, True, model=0)
+    dev_ms, wall_ms = max_over_ranks([dev_ms, wall_ms], world)
     B_glob = spec["batch"] * world
     value = B_glob * args.steps / (dev_ms / 1e3)
     e2e = B_glob * args.steps / (wall_ms / 1e3)
@@ -375,6 +577,16 @@ def run_ours(args, rank, world):
     d2h_busy = float(np.mean([m["d2h_busy_ms"] for m in mets_i]))
     comp_busy = float(np.mean([m["compute_busy_ms"] for m in mets_i]))
     instr_step_ms = float(np.mean([m["step_ms"] for m in mets_i]))
+    # transfers by phase (forward = functions up to the loss): the practical
+    # link bound of a step whose forward drives D2H and backward drives H2D
+    loss_pos = max(i for i, f in enumerate(fid) if f.startswith(("loss", "d1.hinge", "d2.hinge")) or f == "loss")
+    ph = {"h2d_fwd": 0, "h2d_bwd": 0, "d2h_fwd": 0, "d2h_bwd": 0}
+    for ev in tl:
+        if ev["stream"] in ("h2d", "d2h"):
+            ph[f"{ev['stream']}_{'fwd' if ev['fn'] <= loss_pos else 'bwd'}"] += vbytes[ev["id"]]
+    t_duplex = max(h2d / (link["h2d"] * 1e9), d2h / (link["d2h"] * 1e9))
+    t_phase = max(ph["d2h_fwd"] / (link["d2h"] * 1e9), ph["h2d_fwd"] / (link["h2d"] * 1e9)) + \
+        max(ph["h2d_bwd"] / (link["h2d"] * 1e9), ph["d2h_bwd"] / (link["d2h"] * 1e9))
     # dominant contraction kernel from the per-function CUDA events of the instrumented pass
     fl = conv_flops(doc)
     per_kind = {}
@@ -384,32 +596,21 @@ def run_ours(args, rank, world):
         kind, f = fl[ev["id"]]
         a = per_kind.setdefault(kind, [0.0, 0.0, 0])
         a[0] += f
-        # the contraction kernels' own launch durations when recorded (k_ms),
-        # else the whole function (operand re-layout kernels included)
         if ev.get("k_n"):
             a[1] += ev["k_ms"] / 1e3
             a[2] += ev["k_n"]
         else:
             a[1] += (ev["t1"] - ev["t0"]) / 1e3
             a[2] += 1
-    # in-core reference at the same batch: no swapping at all — parameters,
-    # gradients and momentum device-resident (pinned), budget = F_peak, W = 0
-    incore = None
+    # in-core references
+    incore_b0 = incore_same = None
     if not args.no_incore and spec["mode"] == "bf16":
-        torch.cuda.empty_cache()
-        doc_p, info_p = graphs.build(spec, params="pinned", inputs="host")
-        F_p = B.Graph(doc_p).in_core_peak()
-        st2, _, _ = setup_step(spec, info_p, doc_p, F_p, "best", chunk, timeline=False, window=0)
-        for _ in range(max(1, args.warmup)):
-            st2.step()
-        torch.cuda.synchronize()
-        e0.record(st2.streams[0])
-        for _ in range(max(3, args.steps // 2)):
-            st2.step()
-        e1.record(st2.streams[0])
-        torch.cuda.synchronize()
-        incore = spec["batch"] * max(3, args.steps // 2) / (e0.elapsed_time(e1) / 1e3) * world
-        st2.close()
+        if args.config == "r50" and b0:
+            incore_b0 = in_core_rate(args, spec_for(args, b0), rank, world, chunk, args.steps)
+            if in_core_device_bytes(spec) < 0.85 * torch.cuda.get_device_properties(dev).total_memory:
+                incore_same = in_core_rate(args, spec, rank, world, chunk, args.steps)
+        else:
+            incore_same = in_core_rate(args, spec, rank, world, chunk, args.steps)
     if rank != 0:
         return None
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -421,77 +622,84 @@ def run_ours(args, rank, world):
         impl = os.environ.get("OC_CONV_IMPL", "tc")
         if impl == "simt" or kind.startswith("attn"):   # CUDA-core FFMA kernels
             roof = {"bound": "alu", "achieved": ach, "peak": FP32_SIMT_TFLOPS, "unit": "TFLOP/s",
-                    "frac": ach / FP32_SIMT_TFLOPS, "traffic": None, "kernel": kind, "launches": cnt, "timed": "CUDA events around each contraction kernel launch in the instrumented pass (operand re-layout kernels excluded)",
+                    "frac": ach / FP32_SIMT_TFLOPS, "traffic": None, "kernel": kind, "launches": cnt,
+                    "timed": "CUDA events around each contraction kernel launch in the instrumented pass",
                     "peak_source": "derived: 148 SM x 128 FFMA lanes x 2 x 1.965 GHz"}
         else:
             pk = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-            # DRAM bytes per launch of this kernel kind from the committed ncu capture of the step
-            tpath = os.path.join(ROOT, "profiles", "r01_conv_traffic.json")
+            tpath = os.path.join(ROOT, "profiles", f"r02_conv_traffic_{args.config}.json")
             traffic = None
-            if os.path.exists(tpath) and args.config == "r18":
+            if os.path.exists(tpath):
                 traffic = json.load(open(tpath)).get(kind, {}).get("bytes_per_launch")
             roof = {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
-                    "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, profiles/r01_conv_traffic.json)",
-                    "kernel": kind, "launches": cnt, "timed": "CUDA events around each contraction kernel launch in the instrumented pass (operand re-layout kernels excluded)",
+                    "traffic": traffic, "traffic_unit": f"DRAM bytes per launch (ncu --set full, {tpath[len(ROOT) + 1:]})",
+                    "kernel": kind, "launches": cnt,
+                    "timed": "CUDA events around each contraction kernel launch in the instrumented pass "
+                             "(operand re-layout kernels excluded)",
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"}
-    # step-level roofline: slower of compute at tensor peak and swap bytes over the link (NS)
     total_flops = sum(f for (_, f) in fl.values())
-    t_link = max(h2d / (55.6e9), d2h / (57.3e9))
     t_tc = total_flops / (peaks.get("bf16_tflops_sustained", 1395.5) * 1e12)
-    t_roof = max(t_link, t_tc)
-    train_mult = None
-    if args.config == "r18":
-        b0 = trainable_batch(lambda b: nets.resnet(18, batch=b), budget)
-        train_mult = spec["batch"] / b0 if b0 else None
+    incore_ref = incore_b0 or incore_same
     line = {
         "metric": "samples/sec at k x in-budget batch vs in-core; host-link GB/s; overlap %",
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16" if spec["mode"] == "bf16" else "f32", "data": "synthetic (seeded N(0,1) images, U labels)",
-        "config": dict(cfg, global_batch=B_glob, per_gpu_batch=spec["batch"], budget_bytes=budget,
-                       in_core_footprint_bytes=F_peak, window_bytes=W, window_max_feasible=wmax,
-                       window_selection=window_probe or args.window, allocator=args.mode, chunk_bytes=chunk,
-                       swap_policy=args.policy if not dist_ else f"{args.policy} (function distance {dist_})",
-                       phys_pool_bytes=phys, parallelism=f"dp{world}", cuda_graph_replay=not args.no_graph,
-                       l2_flush="inputs larger than L2 (activations GBs per step)"),
+        "config": {"workload": workload_name(args, spec, B_p, b0 or 1), "global_batch": B_glob,
+                   "per_gpu_batch": spec["batch"], "b0_in_core_max": b0,
+                   "physical_budget_bytes": B_p, "pinned_bytes": pinned, "workspace_bytes": ws,
+                   "swap_pool_bytes": pool, "scheduler_budget_bytes": B_s,
+                   "device_bytes_used": pinned + pool + ws,
+                   "in_core_footprint_bytes": F_peak, "window_bytes": W_sel, "window_selection": window_probe or
+                   args.window, "allocator": mode, "chunk_bytes": chunk,
+                   "swap_policy": args.policy if not dist_ else f"{args.policy} (function distance {dist_})",
+                   "arrival_trigger": args.trigger, "host_copy_bytes": host_bytes, "host_ram_bytes": ram,
+                   "host_pool_bytes": host_pool_bytes, "host_pool_numa_node": host_numa,
+                   "dp_bucket_bytes": args.bucket_mib * MiB if world > 1 else None,
+                   "parallelism": f"dp{world}", "cuda_graph_replay": not args.no_graph,
+                   "l2_flush": "inputs larger than L2 (activations GBs per step)", "notes": notes},
         "clocks": clk.summary(),
         "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "note": "wall clock around oc_run_step with host inputs/params swapped in and loss read back"},
+                "note": "wall clock around oc_run_step: host inputs/parameters swapped in, loss written back, "
+                        "every step"},
         "gpu_launches": n_k,
         "roofline": roof,
-        "step_roofline": {"t_link_ms": t_link * 1e3, "t_tensor_ms": t_tc * 1e3, "bound": "host-link" if t_link > t_tc
-                          else "tensor", "frac": t_roof / (step_ms / 1e3)},
+        "link_roofline": {"t_duplex_ms": t_duplex * 1e3, "t_phase_separated_ms": t_phase * 1e3,
+                          "frac_duplex": t_duplex * 1e3 / step_ms, "frac_phase_separated": t_phase * 1e3 / step_ms,
+                          "bytes_by_phase": ph, "measured_gbs": link, "pcie5_x16_gbs_per_dir": PCIE5_X16_GBS,
+                          "t_tensor_ms": t_tc * 1e3,
+                          "note": "duplex = max(h2d/BW_h2d, d2h/BW_d2h); phase-separated = forward transfers then "
+                                  "backward transfers, each direction-limited (SURVEY H1)"},
         "host_link": {"h2d_gbs_step": h2d / (step_ms / 1e3) / 1e9, "d2h_gbs_step": d2h / (step_ms / 1e3) / 1e9,
                       "h2d_gbs_busy": (h2d / (h2d_busy / 1e3) / 1e9) if h2d_busy else None,
                       "d2h_gbs_busy": (d2h / (d2h_busy / 1e3) / 1e9) if d2h_busy else None,
-                      "pcie5_x16_gbs_per_dir": PCIE5_X16_GBS, "measured_pinned_gbs": {"h2d": 55.6, "d2h": 57.3}},
+                      "pcie5_x16_gbs_per_dir": PCIE5_X16_GBS, "measured_pinned_gbs": link},
         "overlap_pct": 100 * overlap,
         "makespan_model": {"predicted_ms": sim["makespan_ms"], "predicted_boundary_ms": sim0["makespan_ms"],
-                           "compute_ms": sim["compute_ms"],
-                           "stall_ms": sim["stall_ms"],
+                           "compute_ms": sim["compute_ms"], "stall_ms": sim["stall_ms"],
                            "link_gbs": {"h2d": bw_h, "d2h": bw_d, "source": "bytes / busy copy time of the "
-                                                                           "instrumented pass"},
-                           "note": "oc_simulate on this schedule with the instrumented pass's per-function times; "
-                                   "compare instrumented_pass.ms_per_step; model 1 = executor ordering, "
-                                   "boundary = the paper's function-boundary semantics"},
+                                                                           "instrumented pass"}},
         "instrumented_pass": {"steps": 3, "ms_per_step": instr_step_ms,
                               "note": "overlap, busy times and kernel durations come from this pass (CUDA events "
-                                      "around every function and transfer); the timed steps run without them"},
+                                      "around every function and transfer); the timed steps replay a CUDA graph"},
         "compute_busy_ms": comp_busy,
-        "in_core_samples_per_s": incore,
-        "fraction_of_in_core": (value / incore) if incore else None,
-        "trainable_batch_multiple": train_mult,
+        "in_core_samples_per_s": incore_ref,
+        "in_core_same_batch_samples_per_s": incore_same,
+        "fraction_of_in_core": (value / incore_ref) if incore_ref else None,
+        "trainable_batch_multiple": (spec["batch"] / b0) if b0 else None,
         "schedule": {k: ss[k] for k in ("bytes_h2d", "bytes_alloc", "bytes_d2h", "bytes_d2h_dirty", "peak_sched",
                                         "peak_phys", "if_peak", "n_max")},
         "vmm": {k: mstat[k] for k in ("n_driver_map", "n_map_calls", "n_map_memo_hits", "map_us")},
         "loss": loss,
-        "paper_context": "V100 ResNet-50 b=1440 (7.5x physical memory) at 55% of in-core speed (PAPER.md P:10)",
+        "paper_context": "V100 16 GB, fp32: ResNet-50 b=1440 (7.5x the in-core maximum 190) at 321 images/s = "
+                         "55% of in-core 581 (PAPER.md P:10, Table 1 P:135-137)",
     }
-    if rank == 0 and args.config != "mlp":
+    if args.config != "mlp":
         line["cpu_baseline"] = cpu_baseline(args)
     return line
 
 
+# ------------------------------------------------------------ oracle (CPU)
 def oracle_sample(args):
     """The oracle's bounded sample of the configured workload: (one-step
     callable, samples per step, time scale to the real sample, description)."""
@@ -521,13 +729,16 @@ def oracle_sample(args):
     return (lambda: nm.train_step(spec, p, x, y)), spec["batch"], scale, note + " (numpy float64 oracle)"
 
 
-def cpu_baseline(args, steps=1):
-    """The oracle on a bounded sample of the same workload, on all host cores."""
+def cpu_baseline(args, min_s=10.0):
+    """The oracle on a bounded sample of the same workload, on all host cores
+    (repeated steps until ~10 s of CPU work)."""
     cores = len(os.sched_getaffinity(0))
     fn, batch, scale, note = oracle_sample(args)
     t0 = time.perf_counter()
-    for _ in range(steps):
+    steps = 0
+    while steps == 0 or (time.perf_counter() - t0 < min_s and steps < 50):
         fn()
+        steps += 1
     dt = (time.perf_counter() - t0) * scale
     return {"value": batch * steps / dt, "unit": "samples/s", "cores": cores, "kind": "oracle",
             "sample": f"{note}, {steps} step(s)"}
@@ -544,17 +755,30 @@ def run_reference(args):
         fn()
     dt = (time.perf_counter() - t0) * scale
     v = batch * args.steps / dt
-    _, cfg = config(args)
     return {"impl": "reference", "metric": "samples/sec at k x in-budget batch vs in-core; host-link GB/s; overlap %",
             "value": v, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "config": cfg,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {note} (bounded CPU sample of the GPU arm's workload)"},
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "oracle", "sample": note},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def spawn(args):
+    """`--gpus N` without a torchrun environment: launch N ranks (one per GPU)."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     if args.impl == "reference":

@@ -326,6 +326,15 @@ typedef struct oc_exec_options {
                               the step's issue — copies, event waits, kernels, NCCL — into a
                               CUDA graph once and replay it every later step; ignored with
                               timeline */
+  uint32_t trigger;        /* when step (a)'s swap-ins of f_i start on the H2D stream:
+                              0 = as soon as the memory they reuse is released (the
+                                  previous occupant's last use or swap-out) and their
+                                  host copy is complete — the executor's default;
+                              1 = the paper's trigger ("We trigger Swap-in
+                                  operations at a function f_i", Fig.2): also after
+                                  f_{i-1} has finished and the swap-outs f_i waits for
+                                  in (b) are complete — the boundary semantics of
+                                  oc_simulate model 0 */
 } oc_exec_options;
 
 typedef struct oc_step_metrics {
@@ -345,6 +354,10 @@ int oc_exec_create(int device, const oc_graph* g, const oc_schedule* s, oc_mem* 
                    oc_err* err);
 int oc_exec_bind_device(oc_exec* x, uint32_t var, void* dev_ptr, oc_err* err);
 int oc_exec_host_ptr(oc_exec* x, uint32_t var, void** host_ptr, oc_err* err);
+/* The executor's pinned host pool: its size, and the NUMA node its pages were
+ * placed on (the GPU's PCIe-local node read from sysfs, MPOL_PREFERRED), or -1
+ * when the node is unknown and the pool came from cudaHostAlloc. */
+int oc_exec_host_info(oc_exec* x, uint64_t* host_bytes, int* numa_node);
 int oc_run_step(oc_exec* x, oc_step_metrics* out, oc_err* err);
 /* Per-event timeline of the last step as JSON lines (S:358 format):
  * {"t0":ms,"t1":ms,"stream":"compute|h2d|d2h","id":"<fn or var>"} */
@@ -384,6 +397,21 @@ int oc_exec_read_var(oc_exec* x, uint32_t var, void* host, uint64_t bytes, oc_er
 int oc_nccl_unique_id(void* out_128_bytes, oc_err* err);
 int oc_exec_attach_nccl(oc_exec* x, const void* unique_id_128_bytes, int rank, int nranks,
                         oc_err* err);
+/* A caller-provided communicator instead of NCCL (other transports; the
+ * multi-process tests exchange through torch.distributed gloo): fn(user, buf,
+ * count, stream) must replace the `count` fp32 values at device address `buf`
+ * by their mean over the replicas, ordered after the work already issued on
+ * `stream` (a cudaStream_t), and return 0 (non-zero -> OC_E_NCCL).  Steps then
+ * run eagerly (no CUDA-graph capture).  The user pointer is borrowed.
+ *
+ * With a communicator attached (NCCL or custom) every allreduce function — a
+ * bucket of gradients, graphs.build(dp_bucket_bytes=...) — runs on the
+ * executor's communication stream, forked from the compute stream after its
+ * inputs; everything that consumes the bucket (its SGD, swap-outs, reuse of
+ * its memory) waits for the exchange, while the compute stream continues with
+ * the next layers' backward.  NCCL buckets are one ncclGroup. */
+typedef int (*oc_allreduce_fn)(void* user, void* buf, uint64_t count, void* stream);
+int oc_exec_attach_comm(oc_exec* x, oc_allreduce_fn fn, void* user, oc_err* err);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -73,7 +73,7 @@ class oc_streams(C.Structure):
 
 class oc_exec_options(C.Structure):
     _fields_ = [("timeline", C.c_uint32), ("elide_clean", C.c_uint32), ("check", C.c_uint32),
-                ("pack_threshold", C.c_uint32), ("use_graph", C.c_uint32)]
+                ("pack_threshold", C.c_uint32), ("use_graph", C.c_uint32), ("trigger", C.c_uint32)]
 
 
 class oc_step_metrics(C.Structure):
@@ -87,6 +87,7 @@ class oc_step_metrics(C.Structure):
 P = C.c_void_p
 E = C.POINTER(oc_err)
 OC_FN_HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_uint32, C.c_int)
+OC_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
 _SIGS = {
     "oc_strerror": (C.c_char_p, [C.c_int]),
     "oc_abi_version": (C.c_int, []),
@@ -126,6 +127,7 @@ _SIGS = {
                                  C.POINTER(P), E]),
     "oc_exec_bind_device": (C.c_int, [P, C.c_uint32, P, E]),
     "oc_exec_host_ptr": (C.c_int, [P, C.c_uint32, C.POINTER(P), E]),
+    "oc_exec_host_info": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]),
     "oc_run_step": (C.c_int, [P, C.POINTER(oc_step_metrics), E]),
     "oc_exec_timeline": (C.c_int, [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "oc_exec_destroy": (None, [P]),
@@ -134,6 +136,7 @@ _SIGS = {
     "oc_exec_read_var": (C.c_int, [P, C.c_uint32, P, C.c_uint64, E]),
     "oc_nccl_unique_id": (C.c_int, [P, E]),
     "oc_exec_attach_nccl": (C.c_int, [P, P, C.c_int, C.c_int, E]),
+    "oc_exec_attach_comm": (C.c_int, [P, OC_ALLREDUCE_FN, P, E]),
 }
 
 _lib = None

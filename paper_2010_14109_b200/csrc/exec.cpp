@@ -23,6 +23,10 @@
 #include <cstring>
 #include <dlfcn.h>
 #include <sstream>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+#include <fstream>
 
 #include "mem.hpp"
 #include "ops.hpp"
@@ -69,6 +73,7 @@ struct XVar {
   int64_t host_off = -1;
   int32_t cur_slot = -1;
   bool need_wait = false;
+  int32_t async_fn = -1;           // produced by an allreduce still running on the comm stream
 };
 
 struct XFn {
@@ -78,6 +83,65 @@ struct XFn {
   std::vector<uint32_t> dep_reserve;             // departure ids reserved after f_i
   uint32_t pin_off = 0, pin_n = 0;               // unpack entries (small arrivals) in pack_tab
   uint32_t pout_off = 0, pout_n = 0;             // pack entries (small departures)
+  bool is_allreduce = false;                     // gradient exchange (comm stream when attached)
+};
+
+// NUMA node of a GPU's PCIe root (sysfs), -1 if unknown
+int gpu_numa_node(int dev) {
+  char bus[64] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), dev) != cudaSuccess) return -1;
+  std::string b(bus);
+  for (char& c : b) c = (char)std::tolower((unsigned char)c);
+  std::ifstream f("/sys/bus/pci/devices/" + b + "/numa_node");
+  int n = -1;
+  if (!(f >> n)) return -1;
+  return n;
+}
+
+// The pinned host pool on the GPU's NUMA node (each replica's
+// host copies local to its PCIe link): anonymous pages with a preferred-node
+// policy (mbind), faulted in there, then page-locked and mapped for the
+// device (cudaHostRegister).  Falls back to cudaHostAlloc when the node is
+// unknown or any step fails.
+struct HostPool {
+  char* p = nullptr;
+  uint64_t bytes = 0;
+  int node = -1;
+  bool registered = false;
+  Status alloc(int dev, uint64_t n) {
+    bytes = n;
+    node = gpu_numa_node(dev);
+    if (node >= 0 && node < 1024) {
+      void* m = mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+      if (m != MAP_FAILED) {
+        unsigned long mask[16] = {0};
+        mask[node / 64] |= 1UL << (node % 64);
+        const long rc = syscall(SYS_mbind, m, n, 1 /* MPOL_PREFERRED */, mask, 1024, 0);
+        std::memset(m, 0, n);   // fault the pages in on the preferred node
+        if (rc == 0 && cudaHostRegister(m, n, cudaHostRegisterPortable | cudaHostRegisterMapped) == cudaSuccess) {
+          p = (char*)m;
+          registered = true;
+          return Status::ok();
+        }
+        (void)cudaGetLastError();
+        munmap(m, n);
+      }
+      node = -1;
+    }
+    OC_CUDA(cudaHostAlloc((void**)&p, n, cudaHostAllocPortable | cudaHostAllocMapped));
+    std::memset(p, 0, n);
+    return Status::ok();
+  }
+  void release() {
+    if (!p) return;
+    if (registered) {
+      cudaHostUnregister(p);
+      munmap(p, bytes);
+    } else {
+      cudaFreeHost(p);
+    }
+    p = nullptr;
+  }
 };
 
 struct Interval { double a, b; };
@@ -154,6 +218,7 @@ struct Exec {
   bool have_prev = false;
   char* host = nullptr;
   uint64_t host_bytes = 0;
+  HostPool host_pool;
   void* ws = nullptr;
   size_t ws_bytes = 0;
   PackEntry* pack_tab = nullptr;   // device copy of all pack/unpack entries (static addresses)
@@ -167,6 +232,24 @@ struct Exec {
   void* nccl_comm = nullptr;
   void* nccl_allreduce = nullptr;
   void* nccl_destroy = nullptr;
+  void* nccl_group_start = nullptr, *nccl_group_end = nullptr;
+  oc_allreduce_fn comm_fn = nullptr;   // custom communicator (tests, other transports)
+  void* comm_user = nullptr;
+  // gradient exchange on its own stream: an allreduce function f_i (a bucket of
+  // gradients) runs on comm_s, forked from the compute stream after f_i's
+  // inputs are produced; ev_done[i] is recorded on comm_s, so every consumer of
+  // the bucket (the SGD placed one bucket later, swap-outs, memory reuse) waits
+  // for the exchange while the compute stream runs the next layers' backward
+  cudaStream_t comm_s = nullptr;
+  cudaEvent_t ev_cfork = nullptr, ev_cjoin = nullptr;
+  Status ensure_comm_stream() {
+    if (comm_s) return Status::ok();
+    OC_CUDA(cudaSetDevice(device));
+    OC_CUDA(cudaStreamCreateWithFlags(&comm_s, cudaStreamNonBlocking));
+    OC_CUDA(cudaEventCreateWithFlags(&ev_cfork, cudaEventDisableTiming));
+    OC_CUDA(cudaEventCreateWithFlags(&ev_cjoin, cudaEventDisableTiming));
+    return Status::ok();
+  }
   uint64_t step_index = 0;
   // layer-local inspection hook (oc_exec_set_hook; tests only)
   oc_fn_hook hook = nullptr;
@@ -232,8 +315,8 @@ Status Exec::create(int dev, const Graph* graph, const Schedule* sch, MemPool* m
     }
   if (host_bytes) {
     // mapped: the pack/unpack kernel addresses it directly (UVA: same pointer on the device)
-    OC_CUDA(cudaHostAlloc((void**)&host, host_bytes, cudaHostAllocPortable | cudaHostAllocMapped));
-    std::memset(host, 0, host_bytes);
+    OC_TRY(host_pool.alloc(dev, host_bytes));
+    host = host_pool.p;
   }
 
   // departures
@@ -370,6 +453,7 @@ Status Exec::create(int dev, const Graph* graph, const Schedule* sch, MemPool* m
       return e;
     }
     fns[i].op = d;
+    fns[i].is_allreduce = kind == "allreduce";
     const JVal* args = f.op.get("args");
     fns[i].role_vars.resize(d->roles.size());
     for (size_t r = 0; r < d->roles.size(); ++r) {
@@ -437,6 +521,7 @@ Status Exec::run(oc_step_metrics* out) {
     }
     vars[v].cur_slot = -1;
     vars[v].need_wait = false;
+    vars[v].async_fn = -1;
   }
   const double t_host0 = now_ms();
   const double map0 = mem->map_us, unmap0 = mem->unmap_us;
@@ -472,13 +557,22 @@ Status Exec::run(oc_step_metrics* out) {
       OC_CUDA(cudaStreamWaitEvent(cs, ev_out[X.dep_of_wait[k]], 0));
       vars[F.wait_out[k]].cur_slot = -1;  // swapped out: no longer resident
     }
-    // (a) arrivals; small H2D arrivals go through one unpack kernel (A7)
+    // (a) arrivals; small H2D arrivals go through one unpack kernel (A7).
+    // Paper trigger (opt.trigger = 1): the arrivals of f_i are issued at the
+    // function boundary — after f_{i-1} and the swap-outs waited in (b).
+    auto paper_gate = [&](cudaStream_t h) -> Status {
+      if (opt.trigger != 1) return Status::ok();
+      if (i > 0) OC_CUDA(cudaStreamWaitEvent(h, ev_done[i - 1], 0));
+      for (int32_t d : X.dep_of_wait) OC_CUDA(cudaStreamWaitEvent(h, ev_out[d], 0));
+      return Status::ok();
+    };
     for (const Arrival& a : F.in) {
       Slot& sl = slots[a.slot];
       if (s->alloc.mode == OC_ALLOC_VA) OC_TRY(mem->bind(sl.span, sl.chunks));
       if (sl.packed) continue;
       cudaStream_t h = (hs2 && sl.kind == ARRIVE_H2D && (n_hcopy++ & 1)) ? hs2 : hs;
       for (const Ref& r : sl.waits) OC_CUDA(cudaStreamWaitEvent(h, ev_of(r), 0));
+      OC_TRY(paper_gate(h));
       if (sl.kind == ARRIVE_H2D) {
         if (sl.host_dep >= 0) OC_CUDA(cudaStreamWaitEvent(h, ev_out[sl.host_dep], 0));
         XVar& xv = vars[sl.var];
@@ -502,6 +596,7 @@ Status Exec::run(oc_step_metrics* out) {
         if (sl.host_dep >= 0) OC_CUDA(cudaStreamWaitEvent(hs, ev_out[sl.host_dep], 0));
         bytes_h2d += vars[sl.var].bytes;
       }
+      OC_TRY(paper_gate(hs));
       if (opt.timeline) { OC_CUDA(cudaEventRecord(tl_in0[first], hs)); tl_in_used[first] = 1; }
       OC_TRY(pack_launch(pack_tab + X.pin_off, (int)X.pin_n, hs));
       if (opt.timeline) OC_CUDA(cudaEventRecord(tl_in1[first], hs));
@@ -521,6 +616,10 @@ Status Exec::run(oc_step_metrics* out) {
     for (int pass = 0; pass < 2; ++pass)
       for (uint32_t v : (pass == 0 ? f.in : f.out)) {
         XVar& xv = vars[v];
+        if (xv.async_fn >= 0) {   // a gradient bucket still being exchanged
+          OC_CUDA(cudaStreamWaitEvent(cs, ev_done[xv.async_fn], 0));
+          xv.async_fn = -1;
+        }
         if (xv.pinned) continue;
         if (xv.cur_slot < 0) {
           Status e = Status::make(OC_E_INVARIANT, "variable " + g->var_names[v] + " not resident at " + f.name);
@@ -537,7 +636,13 @@ Status Exec::run(oc_step_metrics* out) {
       OC_CUDA(cudaDeviceSynchronize());
       hook(hook_user, i, 0);
     }
-    if (opt.timeline) OC_CUDA(cudaEventRecord(tl_fn0[i], cs));
+    const bool on_comm = X.is_allreduce && comm_s && (nccl_comm || comm_fn);
+    cudaStream_t fs = on_comm ? comm_s : cs;
+    if (on_comm) {
+      OC_CUDA(cudaEventRecord(ev_cfork, cs));
+      OC_CUDA(cudaStreamWaitEvent(comm_s, ev_cfork, 0));
+    }
+    if (opt.timeline) OC_CUDA(cudaEventRecord(tl_fn0[i], fs));
     if (X.op) {
       OpArgs oa;
       oa.ptr.resize(X.role_vars.size());
@@ -550,9 +655,13 @@ Status Exec::run(oc_step_metrics* out) {
       oa.attrs = f.op.get("attrs");
       oa.ws = ws;
       oa.ws_bytes = ws_bytes;
-      oa.stream = cs;
+      oa.stream = fs;
       oa.nccl_comm = nccl_comm;
       oa.nccl_allreduce = nccl_allreduce;
+      oa.nccl_group_start = nccl_group_start;
+      oa.nccl_group_end = nccl_group_end;
+      oa.comm_fn = comm_fn;
+      oa.comm_user = comm_user;
       if (opt.timeline) {
         tl_k[i].used = 0;
         oa.ktimer = &tl_k[i];
@@ -569,8 +678,10 @@ Status Exec::run(oc_step_metrics* out) {
       OC_CUDA(cudaDeviceSynchronize());
       hook(hook_user, i, 1);
     }
-    if (opt.timeline) OC_CUDA(cudaEventRecord(tl_fn1[i], cs));
-    OC_CUDA(cudaEventRecord(ev_done[i], cs));
+    if (opt.timeline) OC_CUDA(cudaEventRecord(tl_fn1[i], fs));
+    OC_CUDA(cudaEventRecord(ev_done[i], fs));
+    if (on_comm)
+      for (uint32_t v : f.out) vars[v].async_fn = (int32_t)i;
     // (c) reserved swap-outs after f_i; small ones through one pack kernel (A7)
     if (!X.dep_reserve.empty()) {
       OC_CUDA(cudaStreamWaitEvent(ds, ev_done[i], 0));
@@ -613,6 +724,10 @@ Status Exec::run(oc_step_metrics* out) {
     for (uint32_t v : F.free) vars[v].cur_slot = -1;
   }
   for (int32_t d : end_deps) OC_CUDA(cudaStreamWaitEvent(cs, ev_out[d], 0));
+  if (comm_s) {   // the step ends when its last gradient exchange has
+    OC_CUDA(cudaEventRecord(ev_cjoin, comm_s));
+    OC_CUDA(cudaStreamWaitEvent(cs, ev_cjoin, 0));
+  }
   if (hs2) {   // join the extra copy streams (their work is already complete or awaited)
     OC_CUDA(cudaEventRecord(ev_join[0], hs2));
     OC_CUDA(cudaEventRecord(ev_join[1], ds2));
@@ -622,7 +737,7 @@ Status Exec::run(oc_step_metrics* out) {
   return Status::ok();
   };
 
-  if (opt.use_graph && !gexec && step_index >= 1 && !opt.timeline && !hook) {
+  if (opt.use_graph && !gexec && step_index >= 1 && !opt.timeline && !hook && !comm_fn) {
     const uint64_t maps_before = mem->n_driver_map;
     OC_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
     Status st = issue();
@@ -636,7 +751,7 @@ Status Exec::run(oc_step_metrics* out) {
     g_bytes_h2d = bytes_h2d; g_bytes_d2h = bytes_d2h; g_n_h2d = n_h2d; g_n_d2h = n_d2h; g_n_kernels = n_kernels;
   }
   OC_CUDA(cudaEventRecord(ev_start, cs));
-  if (gexec && !hook && !opt.timeline) {
+  if (gexec && !hook && !opt.timeline && !comm_fn) {
     OC_CUDA(cudaGraphLaunch(gexec, cs));
     bytes_h2d = g_bytes_h2d; bytes_d2h = g_bytes_d2h; n_h2d = g_n_h2d; n_d2h = g_n_d2h; n_kernels = g_n_kernels;
   } else {
@@ -669,10 +784,11 @@ Status Exec::run(oc_step_metrics* out) {
       };
       for (uint32_t i = 0; i < n; ++i)
         if (fns[i].op) C.push_back(iv(tl_fn0[i], tl_fn1[i]));
+      // packed transfers share their kernel's events (tl_*_ref); the unions dedupe them
       for (size_t k = 0; k < slots.size(); ++k)
-        if (tl_in_used[k]) H.push_back(iv(tl_in0[k], tl_in1[k]));
+        if (tl_in_used[k]) H.push_back(iv(tl_in0[tl_in_ref[k]], tl_in1[tl_in_ref[k]]));
       for (size_t k = 0; k < deps.size(); ++k)
-        if (tl_out_used[k]) D.push_back(iv(tl_out0[k], tl_out1[k]));
+        if (tl_out_used[k]) D.push_back(iv(tl_out0[tl_out_ref[k]], tl_out1[tl_out_ref[k]]));
       T = H;
       T.insert(T.end(), D.begin(), D.end());
       out->compute_busy_ms = union_len(C);
@@ -681,6 +797,7 @@ Status Exec::run(oc_step_metrics* out) {
       double tl = union_len(T);
       out->overlap_frac = tl > 0 ? inter_len(T, C) / tl : 1.0;
       out->stall_ms = out->step_ms - out->compute_busy_ms;
+      (void)cudaGetLastError();   // timing queries are best effort; leave no sticky error behind
     }
   }
   return Status::ok();
@@ -708,10 +825,14 @@ void Exec::destroy() {
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (gexec) cudaGraphExecDestroy(gexec);
   if (ev_end) cudaEventDestroy(ev_end);
-  if (host) cudaFreeHost(host);
+  host_pool.release();
+  host = nullptr;
   if (ws) cudaFree(ws);
   if (pack_tab) cudaFree(pack_tab);
   if (nccl_comm && nccl_destroy) ((int (*)(void*))nccl_destroy)(nccl_comm);
+  if (comm_s) cudaStreamDestroy(comm_s);
+  if (ev_cfork) cudaEventDestroy(ev_cfork);
+  if (ev_cjoin) cudaEventDestroy(ev_cjoin);
 }
 
 }  // namespace oc
@@ -766,6 +887,13 @@ int oc_run_step(oc_exec* x, oc_step_metrics* out, oc_err* err) {
 }
 
 uint64_t oc_graph_workspace_bytes(const oc_graph* g) { return g ? graph_workspace(g->g) : 0; }
+
+int oc_exec_host_info(oc_exec* x, uint64_t* host_bytes, int* numa_node) {
+  if (!x) return OC_E_ARG;
+  if (host_bytes) *host_bytes = x->x.host_bytes;
+  if (numa_node) *numa_node = x->x.host_pool.node;
+  return OC_OK;
+}
 
 int oc_exec_set_timeline(oc_exec* x, int on) {
   if (!x || (on && !x->x.tl_created)) return OC_E_ARG;
@@ -875,13 +1003,27 @@ int oc_exec_attach_nccl(oc_exec* xh, const void* uid, int rank, int nranks, oc_e
   auto init = (nccl_init_rank_t)dlsym(h, "ncclCommInitRank");
   X.nccl_allreduce = dlsym(h, "ncclAllReduce");
   X.nccl_destroy = dlsym(h, "ncclCommDestroy");
+  X.nccl_group_start = dlsym(h, "ncclGroupStart");
+  X.nccl_group_end = dlsym(h, "ncclGroupEnd");
   if (!init || !X.nccl_allreduce) { Status::make(OC_E_NCCL, "NCCL symbols missing").fill(err); return OC_E_NCCL; }
   cudaSetDevice(X.device);
   nccl_uid id;
   std::memcpy(&id, uid, sizeof(id));
   int r = init(&X.nccl_comm, nranks, id, rank);
   if (r) { Status s = Status::make(OC_E_NCCL, "ncclCommInitRank failed"); s.cuda = r; s.fill(err); return OC_E_NCCL; }
-  return OC_OK;
+  Status st = X.ensure_comm_stream();
+  st.fill(err);
+  return st.code;
+}
+
+int oc_exec_attach_comm(oc_exec* xh, oc_allreduce_fn fn, void* user, oc_err* err) {
+  if (!xh || !fn) return OC_E_ARG;
+  Exec& X = xh->x;
+  X.comm_fn = fn;
+  X.comm_user = user;
+  Status st = X.ensure_comm_stream();
+  st.fill(err);
+  return st.code;
 }
 
 }  // extern "C"

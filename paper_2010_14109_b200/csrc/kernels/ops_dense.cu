@@ -167,34 +167,48 @@ Status softmax_ce(OpArgs& a) {
 size_t softmax_ce_ws(const JVal& at) { return (size_t)at.geti("M") * 4; }
 
 // ---------------------------------------------------------------- SGD
-// v ← μ v + g ; w ← w − lr v  (fp32 state; vectorised, grid-stride)
-__global__ void sgd_kernel(int64_t n, float* __restrict__ w, const float* __restrict__ g, float* __restrict__ v,
-                           float lr, float mu) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  if ((((uintptr_t)w | (uintptr_t)g | (uintptr_t)v) & 15) == 0) {
-    int64_t n4 = n / 4;
-    for (int64_t k = i; k < n4; k += stride) {
-      float4 gw = reinterpret_cast<const float4*>(g)[k];
-      float4 vv = reinterpret_cast<float4*>(v)[k];
-      float4 ww = reinterpret_cast<float4*>(w)[k];
-      vv.x = fmaf(mu, vv.x, gw.x); vv.y = fmaf(mu, vv.y, gw.y);
-      vv.z = fmaf(mu, vv.z, gw.z); vv.w = fmaf(mu, vv.w, gw.w);
-      ww.x = fmaf(-lr, vv.x, ww.x); ww.y = fmaf(-lr, vv.y, ww.y);
-      ww.z = fmaf(-lr, vv.z, ww.z); ww.w = fmaf(-lr, vv.w, ww.w);
-      reinterpret_cast<float4*>(v)[k] = vv;
-      reinterpret_cast<float4*>(w)[k] = ww;
-    }
-    for (int64_t k = n4 * 4 + i; k < n; k += stride) {
-      float vk = fmaf(mu, v[k], g[k]);
-      v[k] = vk;
-      w[k] = fmaf(-lr, vk, w[k]);
-    }
-  } else {
-    for (int64_t k = i; k < n; k += stride) {
-      float vk = fmaf(mu, v[k], g[k]);
-      v[k] = vk;
-      w[k] = fmaf(-lr, vk, w[k]);
+// v ← μ v + g ; w ← w − lr v  (fp32 state).  Multi-tensor: one launch updates
+// up to kSgdMax tensors of a function; the tensor table travels
+// by value in the kernel parameters (addresses are fixed per step, so a CUDA
+// graph replays it), each block takes chunks of 16 KB of one tensor.
+constexpr int kSgdMax = 48;
+constexpr int64_t kSgdChunk = 4096;   // elements per block-chunk
+struct SgdTab {
+  float* w[kSgdMax];
+  const float* g[kSgdMax];
+  float* v[kSgdMax];
+  int64_t n[kSgdMax];
+  int32_t first_chunk[kSgdMax + 1];   // prefix sums of chunks per tensor
+  int count;
+};
+
+__global__ void __launch_bounds__(256) sgd_multi(const __grid_constant__ SgdTab T, float lr, float mu) {
+  for (int c = blockIdx.x; c < T.first_chunk[T.count]; c += gridDim.x) {
+    int t = 0;
+    while (T.first_chunk[t + 1] <= c) ++t;
+    const int64_t base = (int64_t)(c - T.first_chunk[t]) * kSgdChunk;
+    const int64_t end = min(T.n[t], base + kSgdChunk);
+    float* __restrict__ w = T.w[t];
+    const float* __restrict__ g = T.g[t];
+    float* __restrict__ v = T.v[t];
+    if (((((uintptr_t)w | (uintptr_t)g | (uintptr_t)v) & 15) == 0) && ((end - base) & 3) == 0) {
+      for (int64_t k = base + 4 * threadIdx.x; k < end; k += 4 * blockDim.x) {
+        float4 gw = *reinterpret_cast<const float4*>(g + k);
+        float4 vv = *reinterpret_cast<float4*>(v + k);
+        float4 ww = *reinterpret_cast<float4*>(w + k);
+        vv.x = fmaf(mu, vv.x, gw.x); vv.y = fmaf(mu, vv.y, gw.y);
+        vv.z = fmaf(mu, vv.z, gw.z); vv.w = fmaf(mu, vv.w, gw.w);
+        ww.x = fmaf(-lr, vv.x, ww.x); ww.y = fmaf(-lr, vv.y, ww.y);
+        ww.z = fmaf(-lr, vv.z, ww.z); ww.w = fmaf(-lr, vv.w, ww.w);
+        *reinterpret_cast<float4*>(v + k) = vv;
+        *reinterpret_cast<float4*>(w + k) = ww;
+      }
+    } else {
+      for (int64_t k = base + threadIdx.x; k < end; k += blockDim.x) {
+        const float vk = fmaf(mu, v[k], g[k]);
+        v[k] = vk;
+        w[k] = fmaf(-lr, vk, w[k]);
+      }
     }
   }
 }
@@ -204,24 +218,56 @@ Status sgd(OpArgs& a) {
   const float lr = (float)Ad(a, "lr"), mu = (float)Ad(a, "momentum");
   const size_t cnt = a.ptr[G_W].size();
   if (a.ptr[G_G].size() != cnt || a.ptr[G_M].size() != cnt) return Status::make(OC_E_INVALID, "sgd: role lengths differ");
-  for (size_t t = 0; t < cnt; ++t) {
-    int64_t n = (int64_t)(a.bytes[G_W][t] / 4);
-    sgd_kernel<<<grid_for(n, 256, 4), 256, 0, a.stream>>>(n, (float*)a.ptr[G_W][t], (const float*)a.ptr[G_G][t],
-                                                          (float*)a.ptr[G_M][t], lr, mu);
+  for (size_t t0 = 0; t0 < cnt; t0 += kSgdMax) {
+    SgdTab T{};
+    T.count = (int)std::min<size_t>(kSgdMax, cnt - t0);
+    T.first_chunk[0] = 0;
+    for (int t = 0; t < T.count; ++t) {
+      T.w[t] = (float*)a.ptr[G_W][t0 + t];
+      T.g[t] = (const float*)a.ptr[G_G][t0 + t];
+      T.v[t] = (float*)a.ptr[G_M][t0 + t];
+      T.n[t] = (int64_t)(a.bytes[G_W][t0 + t] / 4);
+      T.first_chunk[t + 1] = T.first_chunk[t] + (int32_t)((T.n[t] + kSgdChunk - 1) / kSgdChunk);
+    }
+    if (T.first_chunk[T.count] == 0) continue;
+    const int grid = std::min(T.first_chunk[T.count], 4 * kNumSMs);
+    sgd_multi<<<grid, 256, 0, a.stream>>>(T, lr, mu);
     OC_LAUNCH_CHECK(a);
   }
   return Status::ok();
 }
 
 // ---------------------------------------------------------------- all-reduce
+// Mean of the replicas' gradients: NCCL (ncclAvg; one
+// ncclGroup per bucket — the tensors of one allreduce function), or the
+// attached custom communicator, one call per tensor.  The executor launches
+// it on its communication stream (a.stream) when a communicator is attached.
 typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_group_t)();
 Status allreduce(OpArgs& a) {
+  if (a.comm_fn) {
+    for (size_t t = 0; t < a.ptr[0].size(); ++t)
+      if (a.comm_fn(a.comm_user, a.ptr[0][t], a.bytes[0][t] / 4, (void*)a.stream))
+        return Status::make(OC_E_NCCL, "custom allreduce failed");
+    return Status::ok();
+  }
   if (!a.nccl_comm) return Status::ok();  // single replica
   auto f = (nccl_allreduce_t)a.nccl_allreduce;
+  const bool grp = a.nccl_group_start && a.nccl_group_end && a.ptr[0].size() > 1;
+  if (grp) ((nccl_group_t)a.nccl_group_start)();
   for (size_t t = 0; t < a.ptr[0].size(); ++t) {
-    // ncclFloat32 = 7, ncclAvg = 4: mean of the replicas' gradients
+    // ncclFloat32 = 7, ncclAvg = 4
     int r = f(a.ptr[0][t], a.ptr[0][t], a.bytes[0][t] / 4, 7, 4, a.nccl_comm, a.stream);
-    if (r) { Status s = Status::make(OC_E_NCCL, "ncclAllReduce failed"); s.cuda = r; return s; }
+    if (r) {
+      if (grp) ((nccl_group_t)a.nccl_group_end)();
+      Status s = Status::make(OC_E_NCCL, "ncclAllReduce failed");
+      s.cuda = r;
+      return s;
+    }
+  }
+  if (grp) {
+    int r = ((nccl_group_t)a.nccl_group_end)();
+    if (r) { Status s = Status::make(OC_E_NCCL, "ncclGroupEnd failed"); s.cuda = r; return s; }
   }
   return Status::ok();
 }

@@ -62,6 +62,9 @@ struct OpArgs {
   cudaStream_t stream = nullptr;
   void* nccl_comm = nullptr;     // attached communicator (allreduce)
   void* nccl_allreduce = nullptr;
+  void* nccl_group_start = nullptr, *nccl_group_end = nullptr;   // one NCCL group per bucket
+  oc_allreduce_fn comm_fn = nullptr;   // custom communicator (oc_exec_attach_comm)
+  void* comm_user = nullptr;
   uint32_t n_kernels = 0;        // incremented by launch()
   void* p(size_t role, size_t k = 0) const {
     return (role < ptr.size() && k < ptr[role].size()) ? ptr[role][k] : nullptr;

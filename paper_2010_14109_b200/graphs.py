@@ -26,17 +26,22 @@ F32, BF16, I32, U8 = 4, 2, 4, 1
 
 
 class Builder:
-    def __init__(self):
+    def __init__(self, dp_bucket_bytes=0):
         self.vars = []
         self.fns = []
         self.meta = {}
         self._names = set()
+        self._bytes = {}
+        # data-parallel gradient buckets: see _update
+        self.dp_bucket = dp_bucket_bytes
+        self.dp_pending, self.dp_prev, self.dp_nbytes, self.dp_count, self.dp_spec = [], [], 0, 0, None
 
     def var(self, name, nbytes, persistent=False, pinned=False, **meta):
         assert name not in self._names, name
         self._names.add(name)
         self.vars.append({"id": name, "bytes": int(max(1, nbytes)), "persistent": bool(persistent),
                           "pinned": bool(pinned)})
+        self._bytes[name] = int(max(1, nbytes))
         self.meta[name] = meta
         return name
 
@@ -48,10 +53,12 @@ class Builder:
                                 "attrs": attrs}})
 
     def doc(self):
+        if self.dp_bucket:
+            _dp_flush(self, final=True)
         return json.dumps({"variables": self.vars, "functions": self.fns}, separators=(",", ":"))
 
 
-def build(spec, params="persistent", inputs="host", pin_below=0):
+def build(spec, params="persistent", inputs="host", pin_below=0, dp_bucket_bytes=0):
     """Returns (graph document JSON, info dict).  info maps roles to variable
     names: params (name -> var), momentum, grads, x, labels, loss, shapes.
 
@@ -59,14 +66,24 @@ def build(spec, params="persistent", inputs="host", pin_below=0):
     inputs and loss) are pinned — resident for the whole step, charged to the
     budget, never swapped (Z26: the LMS-style size threshold; with VA
     chunks of m_c bytes a tensor far below m_c would otherwise map a whole
-    chunk, Eq.1)."""
+    chunk, Eq.1).
+
+    dp_bucket_bytes: data-parallel replicas — gradients are
+    averaged in buckets of about this many bytes, one allreduce function per
+    bucket placed right after the backward of its last layer, and the bucket's
+    SGD update (one multi-tensor function) one bucket later, so that with a
+    communicator attached the exchange of bucket k runs on the executor's
+    communication stream while the backward of bucket k+1 computes.  0: one
+    allreduce + SGD pair per layer right after its backward (single replica)."""
     if "G" in spec:                       # GAN step (configs[4], graphs_gan.py)
         from .graphs_gan import build_gan
+        if dp_bucket_bytes:
+            raise ValueError("gradient buckets: not for the GAN step (D's update must precede the G-step)")
         return build_gan(spec, params, inputs)
     if any(l["type"] != "linear" for l in spec["layers"]):
-        doc, info = _build_convnet(spec, params, inputs)
+        doc, info = _build_convnet(spec, params, inputs, dp_bucket_bytes)
     else:
-        doc, info = _build_mlp(spec, params, inputs)
+        doc, info = _build_mlp(spec, params, inputs, dp_bucket_bytes)
     if pin_below:
         d = json.loads(doc)
         keep = {info["x"], info["labels"], info["loss"]}
@@ -89,9 +106,37 @@ def _pvars(b, spec, pshapes, params):
     return P, Mo, G
 
 
+def _dp_flush(b, final=False):
+    """Emit the pending bucket's allreduce, then the previous bucket's SGD
+    (and at the end of the step the last bucket's SGD too)."""
+    if b.dp_pending:
+        gs = [G[n] for (_, P, Mo, G, names) in b.dp_pending for n in names]
+        b.fn(f"allreduce.bucket{b.dp_count}", "allreduce", {"bufs": gs}, {"bucket": b.dp_count}, gs, gs)
+        b.dp_count += 1
+    groups = [b.dp_prev] + ([b.dp_pending] if final else [])
+    for grp in groups:
+        if not grp:
+            continue
+        ws = [P[n] for (_, P, Mo, G, names) in grp for n in names]
+        gs = [G[n] for (_, P, Mo, G, names) in grp for n in names]
+        ms = [Mo[n] for (_, P, Mo, G, names) in grp for n in names]
+        b.fn(f"sgd.{grp[0][0]}..{grp[-1][0]}", "sgd", {"w": ws, "g": gs, "m": ms},
+             {"lr": b.dp_spec["sgd"]["lr"], "momentum": b.dp_spec["sgd"]["momentum"]}, ws + gs + ms, ws + ms)
+    b.dp_prev = [] if final else b.dp_pending
+    b.dp_pending, b.dp_nbytes = [], 0
+
+
 def _update(b, spec, layer, P, Mo, G, names):
     """Per-layer gradient all-reduce (a no-op on one replica) and SGD update,
-    placed right after the layer's backward function."""
+    placed right after the layer's backward function — or, with gradient
+    buckets (build(dp_bucket_bytes=...)), the layer joins the open bucket."""
+    if b.dp_bucket:
+        b.dp_spec = spec
+        b.dp_pending.append((layer, P, Mo, G, names))
+        b.dp_nbytes += sum(b._bytes[G[n]] for n in names)
+        if b.dp_nbytes >= b.dp_bucket:
+            _dp_flush(b)
+        return
     gs = [G[n] for n in names]
     b.fn(f"allreduce.{layer}", "allreduce", {"bufs": gs}, {}, gs, gs)
     ws, ms = [P[n] for n in names], [Mo[n] for n in names]
@@ -99,8 +144,8 @@ def _update(b, spec, layer, P, Mo, G, names):
          {"lr": spec["sgd"]["lr"], "momentum": spec["sgd"]["momentum"]}, ws + gs + ms, ws + ms)
 
 
-def _build_mlp(spec, params, inputs):
-    b = Builder()
+def _build_mlp(spec, params, inputs, dp_bucket_bytes=0):
+    b = Builder(dp_bucket_bytes)
     M = spec["batch"]
     act = F32 if spec["mode"] == "fp32" else BF16
     dt = "f32" if spec["mode"] == "fp32" else "bf16"
@@ -151,6 +196,6 @@ def _build_mlp(spec, params, inputs):
     return b.doc(), info
 
 
-def _build_convnet(spec, params, inputs):
+def _build_convnet(spec, params, inputs, dp_bucket_bytes=0):
     from . import graphs_conv
-    return graphs_conv.build_convnet(spec, params, inputs)
+    return graphs_conv.build_convnet(spec, params, inputs, dp_bucket_bytes)

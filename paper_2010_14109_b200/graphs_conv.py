@@ -25,10 +25,10 @@ from synth import nets
 from .graphs import BF16, F32, I32, U8, Builder, _pvars, _update
 
 
-def build_convnet(spec, params="pinned", inputs="host"):
+def build_convnet(spec, params="pinned", inputs="host", dp_bucket_bytes=0):
     # bf16 storage (tcgen05 convs) or the fp32 parity mode (CUDA-core convs, no TF32)
     ACT, DT = (BF16, "bf16") if spec["mode"] == "bf16" else (F32, "f32")
-    b = Builder()
+    b = Builder(dp_bucket_bytes)
     Nb = spec["batch"]
     shapes, pshapes = nets.tensor_shapes(spec)
     pin_in = inputs == "pinned"

@@ -17,7 +17,7 @@ _NP = {"f32": np.float32, "i32": np.int32, "u8": np.uint8, "bf16": np.uint16}
 class OutOfCoreStep:
     def __init__(self, doc, budget, window=B.OC_WINDOW_MAX_FEASIBLE, mode="va", chunk_bytes=40 << 20,
                  phys_bytes=0, device=0, timeline=False, elide_clean=True, align=512, meta=None,
-                 pack_threshold=64 << 10, use_graph=False, distance=0):
+                 pack_threshold=64 << 10, use_graph=False, distance=0, trigger=0):
         if not torch.cuda.is_available():
             raise RuntimeError("OutOfCoreStep needs a CUDA device (no CPU fallback)")
         self.device = device
@@ -47,7 +47,7 @@ class OutOfCoreStep:
         self.exec = B.P()
         ss = B.oc_streams(self.streams[0].cuda_stream, self.streams[1].cuda_stream, self.streams[2].cuda_stream)
         opt = B.oc_exec_options(1 if timeline else 0, 1 if elide_clean else 0, 0, int(pack_threshold),
-                                1 if use_graph else 0)
+                                1 if use_graph else 0, int(trigger))
         B.check(B.lib().oc_exec_create(device, self.graph.h, self.sched.h, self.mem, C.byref(ss), C.byref(opt),
                                        C.byref(self.exec), C.byref(err)), err)
         # device-resident (pinned) variables live in torch tensors bound to the executor
@@ -92,6 +92,12 @@ class OutOfCoreStep:
         B.check(B.lib().oc_run_step(self.exec, C.byref(m), C.byref(err)), err)
         return {k: getattr(m, k) for k, _ in B.oc_step_metrics._fields_}
 
+    def host_info(self):
+        """(pinned host pool bytes, NUMA node of its pages or -1)."""
+        n, node = C.c_uint64(), C.c_int()
+        B.lib().oc_exec_host_info(self.exec, C.byref(n), C.byref(node))
+        return n.value, node.value
+
     def set_timeline(self, on):
         """Per-event timeline on/off for the next steps (created with timeline=True)."""
         rc = B.lib().oc_exec_set_timeline(self.exec, 1 if on else 0)
@@ -134,6 +140,13 @@ class OutOfCoreStep:
         err = B.oc_err()
         buf = C.create_string_buffer(bytes(uid_bytes), 128)
         B.check(B.lib().oc_exec_attach_nccl(self.exec, buf, rank, nranks, C.byref(err)), err)
+
+    def attach_comm(self, fn):
+        """Custom communicator (oc_exec_attach_comm): fn(dev_ptr, count, stream)
+        averages `count` fp32 values at the device address over the replicas."""
+        self._comm = B.OC_ALLREDUCE_FN(lambda user, buf, count, stream: int(fn(buf, int(count), stream) or 0))
+        err = B.oc_err()
+        B.check(B.lib().oc_exec_attach_comm(self.exec, self._comm, None, C.byref(err)), err)
 
     def close(self):
         if getattr(self, "exec", None):

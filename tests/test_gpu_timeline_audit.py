@@ -20,11 +20,11 @@ from synth import nets
 MiB = 1 << 20
 
 
-def _run_and_audit(spec, budget, mode, phys, chunk=2 * MiB, pack=64 << 10, pin_below=0, steps=2):
+def _run_and_audit(spec, budget, mode, phys, chunk=2 * MiB, pack=64 << 10, pin_below=0, steps=2, trigger=0):
     from paper_2010_14109_b200.runtime import OutOfCoreStep
     doc, info = graphs.build(spec, params="persistent", inputs="host", pin_below=pin_below)
     st = OutOfCoreStep(doc, budget, B.OC_WINDOW_MAX_FEASIBLE, mode=mode, chunk_bytes=chunk, phys_bytes=phys,
-                       timeline=True, pack_threshold=pack)
+                       timeline=True, pack_threshold=pack, trigger=trigger)
     x, y = nets.make_inputs(spec)
     p = nets.make_params(spec)
     st.write(info["x"], x.astype(np.float32) if spec["mode"] == "fp32"
@@ -45,7 +45,7 @@ def _run_and_audit(spec, budget, mode, phys, chunk=2 * MiB, pack=64 << 10, pin_b
     assert met["bytes_d2h"] > 0 and met["bytes_h2d"] > 0
     n_h2d = sum(1 for e in tl if e["stream"] == "h2d")
     assert n_h2d == sum(1 for i in range(g.n_fns) for _, k in o.ins[i] if k == "h2d")
-    return TA.audit(g, o, pl, mode, tl, align=512)
+    return TA.audit(g, o, pl, mode, tl, align=512, paper_trigger=trigger == 1)
 
 
 @pytest.mark.gpu
@@ -58,6 +58,13 @@ def test_mlp_timeline(mode, phys, pack):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["va", "best"])
+def test_mlp_timeline_paper_trigger(mode):
+    bad = _run_and_audit(nets.mlp6(), 4 * MiB, mode, 8 * MiB if mode == "best" else 512 * MiB, trigger=1)
+    assert bad == [], bad[:10]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["va", "best"])
 def test_resnet_timelines(mode):
     for spec in (nets.tiny_resnet(batch=4, image=16, classes=10),
                  nets.resnet(18, batch=8, image=64, classes=10, mode="fp32")):
@@ -65,6 +72,7 @@ def test_resnet_timelines(mode):
         G = B.Graph(doc)
         budget = max(G.min_feasible_budget(0), G.in_core_peak() // 4)
         probe = G.plan(budget, B.OC_WINDOW_MAX_FEASIBLE, B.OC_ALLOC_VA if mode == "va" else B.OC_ALLOC_ARENA_BEST,
-                       chunk_bytes=2 * MiB, phys_bytes=budget * 8, allow_oom=True).stats()
-        bad = _run_and_audit(spec, budget, mode, probe["peak_phys"] + 2 * MiB)
-        assert bad == [], bad[:10]
+                       chunk_bytes=2 * MiB, phys_bytes=1 << 40, allow_oom=True).stats()
+        for trigger in (0, 1):
+            bad = _run_and_audit(spec, budget, mode, probe["peak_phys"] + 2 * MiB, trigger=trigger)
+            assert bad == [], (trigger, bad[:10])

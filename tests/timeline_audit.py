@@ -21,6 +21,9 @@ clock):
   R3 swap-out    every D2H starts after the function it was reserved after ends
   R4 write-back  an H2D of a variable starts after the latest earlier D2H of
                  the same variable ended (the host copy it reads is complete)
+  R5 trigger     (paper trigger mode only, oc_exec_options.trigger = 1) every
+                 H2D issued by f_i's step (a) starts after f_{i-1} ended
+                 (P:91 "We trigger Swap-in operations at a function f_i")
 
 Test helper (tests/ only); returns a list of violation strings."""
 
@@ -38,7 +41,7 @@ def _overlap(u, w):
     return u[1][0] < w[1][1] and w[1][0] < u[1][1]
 
 
-def audit(g, sch, placements, mode, timeline, align=512):
+def audit(g, sch, placements, mode, timeline, align=512, paper_trigger=False):
     n = len(sch.ins)
     uses = [set(g.uses(i)) for i in range(n)]
     comp = {e["fn"]: (e["t0"], e["t1"]) for e in timeline if e["stream"] == "compute"}
@@ -106,6 +109,13 @@ def audit(g, sch, placements, mode, timeline, align=512):
             prev = [d for d, (i, u) in enumerate(deps) if u == v and i < s["fn"] and d in d2h]
             if prev and d2h[prev[-1]]["t1"] > h2d[k]["t0"]:
                 bad.append(f"R4 slot {k} ({g.var_names[v]}): H2D starts before its write-back ended")
+    # R5
+    if paper_trigger:
+        for k, e in h2d.items():
+            i = e["fn"]
+            if i > 0 and i - 1 in comp and e["t0"] < comp[i - 1][1]:
+                bad.append(f"R5 slot {k}: H2D issued by f{i} starts {e['t0']:.4f} before f{i - 1} ends "
+                           f"{comp[i - 1][1]:.4f}")
     # R3
     for d, (i, v) in enumerate(deps):
         if d in d2h and i in comp and d2h[d]["t0"] < comp[i][1]:
