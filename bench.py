@@ -310,7 +310,7 @@ def new_step(spec, info, doc, budget, mode, chunk, phys, window, timeline=False,
 
 
 def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None, pack=64 << 10, use_graph=False,
-               distance=0):
+               distance=0, trigger=0):
     """Scheduler budget -> executor with the pool sized to the replay's
     physical peak (tools: sweeps that fix B_s rather than B_p)."""
     from paper_2010_14109_b200 import binding as B
@@ -320,7 +320,7 @@ def setup_step(spec, info, doc, budget, mode, chunk, timeline=True, window=None,
                    phys_bytes=budget * 4, allow_oom=True, distance=distance)
     ps = probe.stats()
     phys = ps["peak_phys"] + chunk if mode == "va" else max(ps["peak_phys"], 1)
-    st = new_step(spec, info, doc, budget, mode, chunk, phys, W, timeline, pack, use_graph, distance)
+    st = new_step(spec, info, doc, budget, mode, chunk, phys, W, timeline, pack, use_graph, distance, trigger)
     return st, W, phys
 
 
@@ -594,14 +594,19 @@ def run_ours(args, rank, world):
         if ev["stream"] != "compute" or ev["id"] not in fl:
             continue
         kind, f = fl[ev["id"]]
-        a = per_kind.setdefault(kind, [0.0, 0.0, 0])
+        a = per_kind.setdefault(kind, [0.0, 0.0, 0, 0.0, []])
         a[0] += f
         if ev.get("k_n"):
-            a[1] += ev["k_ms"] / 1e3
+            # in-kernel span (%globaltimer, first CTA start to last CTA end) when probed, else the events
+            a[1] += (ev.get("k_span_ms") or ev["k_ms"]) / 1e3
             a[2] += ev["k_n"]
+            a[3] += ev["k_ms"] / 1e3
+            if ev.get("k_mhz"):
+                a[4].append(ev["k_mhz"])
         else:
             a[1] += (ev["t1"] - ev["t0"]) / 1e3
             a[2] += 1
+            a[3] += (ev["t1"] - ev["t0"]) / 1e3
     # in-core references
     incore_b0 = incore_same = None
     if not args.no_incore and spec["mode"] == "bf16":
@@ -617,7 +622,7 @@ def run_ours(args, rank, world):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
     roof = None
     if per_kind:
-        kind, (flops, secs, cnt) = max(per_kind.items(), key=lambda kv: kv[1][1])
+        kind, (flops, secs, cnt, ev_secs, mhz) = max(per_kind.items(), key=lambda kv: kv[1][1])
         ach = flops / secs / 1e12
         impl = os.environ.get("OC_CONV_IMPL", "tc")
         if impl == "simt" or kind.startswith("attn"):   # CUDA-core FFMA kernels
@@ -634,8 +639,10 @@ def run_ours(args, rank, world):
             roof = {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
                     "traffic": traffic, "traffic_unit": f"DRAM bytes per launch (ncu --set full, {tpath[len(ROOT) + 1:]})",
                     "kernel": kind, "launches": cnt,
-                    "timed": "CUDA events around each contraction kernel launch in the instrumented pass "
-                             "(operand re-layout kernels excluded)",
+                    "timed": "in-kernel %globaltimer span of each contraction launch (first CTA start to last CTA "
+                             "end) in the instrumented pass, operand re-layout kernels excluded",
+                    "achieved_event_timed": flops / ev_secs / 1e12 if ev_secs else None,
+                    "sm_mhz_in_kernels": float(np.median(mhz)) if mhz else None,
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"}
     total_flops = sum(f for (_, f) in fl.values())
     t_tc = total_flops / (peaks.get("bf16_tflops_sustained", 1395.5) * 1e12)

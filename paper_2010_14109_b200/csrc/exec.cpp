@@ -930,6 +930,16 @@ int oc_exec_read_var(oc_exec* x, uint32_t var, void* host, uint64_t bytes, oc_er
   return OC_OK;
 }
 
+// the launch probes of f_i's contraction kernels: Σ in-kernel spans and the SM clock
+static std::string probe_json(const Exec& X, uint32_t i) {
+  if (i >= X.tl_k.size() || !X.tl_k[i].dprobe) return "";
+  double span = 0, mhz = 0;
+  X.tl_k[i].probe_summary(span, mhz);
+  std::ostringstream o;
+  o << ",\"k_span_ms\":" << span << ",\"k_mhz\":" << mhz;
+  return o.str();
+}
+
 int oc_exec_timeline(oc_exec* xh, char* buf, size_t cap, size_t* need) {
   if (!xh) return OC_E_ARG;
   Exec& X = xh->x;
@@ -940,7 +950,7 @@ int oc_exec_timeline(oc_exec* xh, char* buf, size_t cap, size_t* need) {
       if (X.fns[i].op)
         o << "{\"t0\":" << t(X.tl_fn0[i]) << ",\"t1\":" << t(X.tl_fn1[i]) << ",\"stream\":\"compute\",\"id\":\""
           << X.g->fns[i].name << "\",\"fn\":" << i << ",\"k_ms\":" << (i < X.tl_k.size() ? X.tl_k[i].ms() : 0.0f)
-          << ",\"k_n\":" << (i < X.tl_k.size() ? X.tl_k[i].used / 2 : 0) << "}\n";
+          << ",\"k_n\":" << (i < X.tl_k.size() ? X.tl_k[i].used / 2 : 0) << probe_json(X, i) << "}\n";
     // transfers: "slot" = arrival slot (allocator-replay order), "fn" = the
     // function whose step (a) issued it; departures: "fn" = the function after
     // which the swap-out was reserved (c), "slot" = the slot it leaves;

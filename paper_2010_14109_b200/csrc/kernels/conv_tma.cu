@@ -78,6 +78,7 @@ struct Params {
   // (n, h', w') is dx pixel (n, h'·dst + ph, w'·dst + pw) of an Ho × Wo map
   int Sw, r0, s0, dst, ph, pw, Ho, Wo;
   FastDiv fQ, fP, fCb, fS;
+  unsigned long long* probe;   // launch probe (timeline mode), or null
 };
 
 __device__ __forceinline__ void base_of(const Params& P, int pix, int& w, int& h, int& n) {
@@ -110,6 +111,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  KProbe kp;
+  if (threadIdx.x == 0) probe_begin(kp);
 
   if (NCH) {
     // taps past R·S are never loaded; their (weight-zero) A columns must hold
@@ -502,6 +505,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
     if (CG == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
     else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
   }
+  if (threadIdx.x == 0) probe_end(P.probe, kp);
 }
 
 int sm_count() {
@@ -633,7 +637,10 @@ Status launch_mt(OpArgs& a, Params P, int* stat_slots = nullptr) {
       return Status::make(OC_E_INVARIANT, "conv: more statistics slots than the workspace holds");
     if (stat_slots) *stat_slots = ctas / P.num_n * 4 * CG;
   }
-  if (a.ktimer) a.ktimer->begin(a.stream);
+  if (a.ktimer) {
+    P.probe = a.ktimer->probe_slot(a.stream);
+    a.ktimer->begin(a.stream);
+  }
   if (CG == 1) {
     kern<<<ctas, NTHREADS, smem, a.stream>>>(P);
   } else {
@@ -750,6 +757,7 @@ struct Params {
   CUtensorMap ty;   // y [N][P][Q][64] bf16, box {64, 8, 4, 1}, SWIZZLE_128B
   int tq, tpq, units, pad;
   float* stat_part;   // fused BN statistics: part[slot][2][64]
+  unsigned long long* probe;
 };
 
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint64_t* b, int c0, int c1, int c2,
@@ -763,6 +771,8 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
 
 __global__ void __launch_bounds__(NTHREADS, 1) stem_kernel(const __grid_constant__ Params P) {
   constexpr uint32_t TCOLS = 128;   // two 64-column accumulators
+  KProbe kp;
+  if (threadIdx.x == 0) probe_begin(kp);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* bsm = smem;
@@ -922,6 +932,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) stem_kernel(const __grid_constant
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
   }
+  if (threadIdx.x == 0) probe_end(P.probe, kp);
 }
 
 // Weight gradient of the same stem, halo-gathered: dW'[(t, c)][k] = Σ_pixels
@@ -944,10 +955,13 @@ struct WParams {
   CUtensorMap tdy;  // dY [N][P][Q][64] box {64, 8, 16, 1}, SWIZZLE_128B
   int tq, tpq, units, pad, accumulate;
   float* part;      // [gridDim.x][256][64]
+  unsigned long long* probe;
 };
 
 __global__ void __launch_bounds__(NTHREADS, 1) stem_wgrad_kernel(const __grid_constant__ WParams P) {
   constexpr uint32_t TCOLS = 256;   // four 64-column accumulators (j = 0..3)
+  KProbe kp;
+  if (threadIdx.x == 0) probe_begin(kp);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + WNSTG * WSTAGE);
@@ -1051,6 +1065,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) stem_wgrad_kernel(const __grid_co
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
   }
+  if (threadIdx.x == 0) probe_end(P.probe, kp);
 }
 
 // 3×3 stride-1 pad-1 convs with 64 input and 64 output channels (ResNet's
@@ -1319,7 +1334,10 @@ Status conv_stem_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const
   }
   const int ctas = grid_cap(std::min(P.units, sm_count()));
   if (stat_part && stat_slots) *stat_slots = ctas * 4;
-  if (a.ktimer) a.ktimer->begin(a.stream);
+  if (a.ktimer) {
+    P.probe = a.ktimer->probe_slot(a.stream);
+    a.ktimer->begin(a.stream);
+  }
   stem_kernel<<<ctas, NTHREADS, SMEM, a.stream>>>(P);
   if (a.ktimer) a.ktimer->end(a.stream);
   OC_LAUNCH_CHECK(a);
@@ -1526,7 +1544,10 @@ Status conv_stem_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x,
     cudaFuncSetAttribute(stem_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WSMEM);
     attr = true;
   }
-  if (a.ktimer) a.ktimer->begin(a.stream);
+  if (a.ktimer) {
+    P.probe = a.ktimer->probe_slot(a.stream);
+    a.ktimer->begin(a.stream);
+  }
   stem_wgrad_kernel<<<splits, NTHREADS, WSMEM, a.stream>>>(P);   // every CTA writes its partial (zeros if idle)
   if (a.ktimer) a.ktimer->end(a.stream);
   OC_LAUNCH_CHECK(a);

@@ -22,6 +22,32 @@ struct FastDiv {
   }
 };
 
+// Launch probe (timeline mode): each CTA's thread 0 reads %globaltimer and
+// clock64 at entry and exit; probe[0] = earliest start, probe[1] = latest end
+// (ns), probe[2] = Σ SM cycles, probe[3] = Σ ns over the CTAs — so the launch's
+// span and the SM clock it actually ran at (Σcycles / Σns) are known without
+// host-side events (in-step vs isolated kernel times).
+struct KProbe {
+  unsigned long long t0, c0;
+};
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void probe_begin(KProbe& k) {
+  k.t0 = gtimer_ns();
+  k.c0 = clock64();
+}
+__device__ __forceinline__ void probe_end(unsigned long long* p, const KProbe& k) {
+  if (!p) return;
+  const unsigned long long t1 = gtimer_ns(), c1 = clock64();
+  atomicMin(p, k.t0);
+  atomicMax(p + 1, t1);
+  atomicAdd(p + 2, c1 - k.c0);
+  atomicAdd(p + 3, t1 - k.t0);
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -8,6 +8,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -22,6 +23,39 @@ namespace oc {
 struct KernelTimer {
   std::vector<cudaEvent_t> ev;   // 2 per launch, created on demand, reused every step
   size_t used = 0;
+  // in-kernel launch probes (tc_util.cuh KProbe): 4 u64 per launch, kMaxProbes launches
+  static constexpr size_t kMaxProbes = 64;
+  unsigned long long* dprobe = nullptr;
+  unsigned long long* probe_slot(cudaStream_t s) {
+    const size_t k = used / 2;
+    if (k >= kMaxProbes) return nullptr;
+    if (!dprobe && cudaMalloc((void**)&dprobe, kMaxProbes * 4 * sizeof(unsigned long long)) != cudaSuccess) {
+      dprobe = nullptr;
+      return nullptr;
+    }
+    unsigned long long* p = dprobe + 4 * k;
+    cudaMemsetAsync(p, 0xFF, 8, s);
+    cudaMemsetAsync(p + 1, 0, 24, s);
+    return p;
+  }
+  // Σ launch spans (ms) and the SM clock the launches ran at (MHz), after the step
+  void probe_summary(double& span_ms, double& mhz) const {
+    span_ms = 0;
+    mhz = 0;
+    const size_t n = std::min(used / 2, kMaxProbes);
+    if (!dprobe || n == 0) return;
+    std::vector<unsigned long long> h(4 * n);
+    if (cudaMemcpy(h.data(), dprobe, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return;
+    double clk = 0, ns = 0;
+    for (size_t k = 0; k < n; ++k) {
+      if (h[4 * k + 1] < h[4 * k]) continue;   // launch without a probe
+      span_ms += (double)(h[4 * k + 1] - h[4 * k]) * 1e-6;
+      clk += (double)h[4 * k + 2];
+      ns += (double)h[4 * k + 3];
+    }
+    mhz = ns > 0 ? clk / ns * 1e3 : 0;
+  }
   void begin(cudaStream_t s) {
     if (used + 2 > ev.size())
       for (int k = 0; k < 2; ++k) {
@@ -48,6 +82,8 @@ struct KernelTimer {
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     ev.clear();
     used = 0;
+    if (dprobe) cudaFree(dprobe);
+    dprobe = nullptr;
   }
 };
 

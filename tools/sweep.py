@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--packs", default="65536", help="pack/unpack thresholds in bytes (0 = copy engines only)")
     ap.add_argument("--pin-below", type=int, default=0, help="pin variables smaller than this (bytes, Z26)")
     ap.add_argument("--distances", default="", help="also run the prior-art function-distance windows (F1), e.g. 1,2,4")
+    ap.add_argument("--triggers", default="0", help="arrival triggers: 0 = at memory release (executor), "
+                                                     "1 = the paper's f_{i-1} boundary (P:91); e.g. 0,1")
     a = ap.parse_args()
     import numpy as np
     from paper_2010_14109_b200 import binding as B
@@ -46,11 +48,12 @@ def main():
             for ch in [int(c) for c in a.chunks.split(",")]:
                 runs = [(float(x), int(p), 0) for x in a.wfracs.split(",") for p in a.packs.split(",")]
                 runs += [(0.0, int(a.packs.split(",")[0]), int(d)) for d in a.distances.split(",") if d]
-                for wf, pk, dd in runs:
+                runs = [r + (int(t),) for r in runs for t in a.triggers.split(",")]
+                for wf, pk, dd, trg in runs:
                     W = int(wmax * wf)
                     try:
                         st, W, phys = bench.setup_step(spec, info, doc, budget, mode, ch << 20, timeline=True,
-                                                       window=W, pack=pk, distance=dd)
+                                                       window=W, pack=pk, distance=dd, trigger=trg)
                     except Exception as e:  # noqa: BLE001
                         print(json.dumps({"frac": frac, "mode": mode, "chunk_mib": ch, "wfrac": wf, "distance": dd,
                                           "error": str(e)[:200]}), flush=True)
@@ -74,6 +77,7 @@ def main():
                     m["predicted_boundary_ms"] = st.sched.simulate(fm, bh, bd, 0.0, 0.0, True)["makespan_ms"]
                     print(json.dumps({"frac": frac, "budget": budget, "mode": mode, "chunk_mib": ch, "wfrac": wf,
                                       "pack": pk, "policy": "paper" if not dd else f"distance {dd}",
+                                      "trigger": ("release", "paper")[trg],
                                       "window": W, "phys": phys, "samples_per_s": a.batch / m["step_ms"] * 1e3,
                                       **m, "peak_phys": st.stats["peak_phys"], "if_peak": st.stats["if_peak"],
                                       "map_us_total": mem["map_us"]}), flush=True)
