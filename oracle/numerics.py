@@ -70,23 +70,25 @@ def rounder(mode):
 # ------------------------------------------------------------------ layers
 
 
-def conv2d(x, w, stride, pad):
-    """x [N,H,W,C], w [K,R,S,C] -> y [N,P,Q,K] (definition above)."""
+def conv2d(x, w, stride, pad, dil=1):
+    """x [N,H,W,C], w [K,R,S,C] -> y [N,P,Q,K] (definition above; dilation d:
+    tap (r, s) reads x[n, p·st − pad + d·r, q·st − pad + d·s, c], the atrous
+    convolution of DeepLab)."""
     N, H, W, C = x.shape
     K, R, S, _ = w.shape
-    P = (H + 2 * pad - R) // stride + 1
-    Q = (W + 2 * pad - S) // stride + 1
+    P = (H + 2 * pad - dil * (R - 1) - 1) // stride + 1
+    Q = (W + 2 * pad - dil * (S - 1) - 1) // stride + 1
     xp = np.zeros((N, H + 2 * pad, W + 2 * pad, C))
     xp[:, pad:pad + H, pad:pad + W, :] = x
     y = np.zeros((N, P, Q, K))
     for r in range(R):
         for s in range(S):
-            patch = xp[:, r:r + stride * P:stride, s:s + stride * Q:stride, :]
+            patch = xp[:, dil * r:dil * r + stride * P:stride, dil * s:dil * s + stride * Q:stride, :]
             y += patch @ w[:, r, s, :].T
     return y
 
 
-def conv2d_backward(x, w, dy, stride, pad):
+def conv2d_backward(x, w, dy, stride, pad, dil=1):
     """Returns (dx, dw) for conv2d."""
     N, H, W, C = x.shape
     K, R, S, _ = w.shape
@@ -98,10 +100,107 @@ def conv2d_backward(x, w, dy, stride, pad):
     dy2 = dy.reshape(-1, K)
     for r in range(R):
         for s in range(S):
-            patch = xp[:, r:r + stride * P:stride, s:s + stride * Q:stride, :]
+            sl = (slice(None), slice(dil * r, dil * r + stride * P, stride), slice(dil * s, dil * s + stride * Q, stride))
+            patch = xp[sl]
             dw[:, r, s, :] = dy2.T @ patch.reshape(-1, C)
-            dxp[:, r:r + stride * P:stride, s:s + stride * Q:stride, :] += dy @ w[:, r, s, :]
+            dxp[sl] += dy @ w[:, r, s, :]
     return dxp[:, pad:pad + H, pad:pad + W, :], dw
+
+
+def conv_transpose2d(x, w, stride, pad, out_hw):
+    """Transposed convolution (Pix2PixHD's upsampling layers): the adjoint of
+    the conv2d that maps an out_hw map to x's map, x [N,H,W,C_in],
+    w [C_in,R,S,K_out] read as that conv's KRSC weight (K = C_in)."""
+    N = x.shape[0]
+    dx, _ = conv2d_backward(np.zeros((N, out_hw[0], out_hw[1], w.shape[3])), w, x, stride, pad)
+    return dx
+
+
+def conv_transpose2d_backward(x, w, g, stride, pad):
+    """(dx, dw) of conv_transpose2d: dx = conv2d(g, w) (the forward conv),
+    dw = that conv's weight gradient with x in the role of its dy."""
+    dx = conv2d(g, w, stride, pad)
+    _, dw = conv2d_backward(g, w, x, stride, pad)
+    return dx, dw
+
+
+def bilinear_coeffs(n_in, n_out):
+    """1-D bilinear interpolation weights, half-pixel centres (PyTorch
+    align_corners=False): output i samples input coordinate
+    src = max((i + 0.5)·n_in/n_out − 0.5, 0); i0 = floor(src),
+    i1 = min(i0 + 1, n_in − 1), weights (1 − λ, λ), λ = src − i0."""
+    src = np.maximum((np.arange(n_out) + 0.5) * (n_in / n_out) - 0.5, 0.0)
+    i0 = np.minimum(np.floor(src).astype(np.int64), n_in - 1)
+    i1 = np.minimum(i0 + 1, n_in - 1)
+    lam = src - i0
+    return i0, i1, lam
+
+
+def upsample_bilinear(x, out_hw):
+    """x [N,H,W,C] -> [N,Ho,Wo,C]: separable bilinear interpolation (rows, then columns)."""
+    r0, r1, a = bilinear_coeffs(x.shape[1], out_hw[0])
+    c0, c1, b = bilinear_coeffs(x.shape[2], out_hw[1])
+    rows = x[:, r0] * (1 - a)[None, :, None, None] + x[:, r1] * a[None, :, None, None]
+    return rows[:, :, c0] * (1 - b)[None, None, :, None] + rows[:, :, c1] * b[None, None, :, None]
+
+
+def upsample_bilinear_backward(g, in_hw):
+    """Adjoint of upsample_bilinear: each output's gradient scattered to its
+    four source pixels with the same weights."""
+    N, Ho, Wo, C = g.shape
+    r0, r1, a = bilinear_coeffs(in_hw[0], Ho)
+    c0, c1, b = bilinear_coeffs(in_hw[1], Wo)
+    rows = np.zeros((N, Ho, in_hw[1], C))
+    np.add.at(rows, (slice(None), slice(None), c0), g * (1 - b)[None, None, :, None])
+    np.add.at(rows, (slice(None), slice(None), c1), g * b[None, None, :, None])
+    dx = np.zeros((N, in_hw[0], in_hw[1], C))
+    np.add.at(dx, (slice(None), r0), rows * (1 - a)[None, :, None, None])
+    np.add.at(dx, (slice(None), r1), rows * a[None, :, None, None])
+    return dx
+
+
+def reflect_index(n, p):
+    """Source index of each padded position of a length-n axis padded by p on
+    both sides with reflection (the edge value not repeated: ... 2 1 | 0 1 2 ...)."""
+    k = np.arange(-p, n + p)
+    k = np.where(k < 0, -k, k)
+    return np.where(k >= n, 2 * (n - 1) - k, k)
+
+
+def reflect_pad(x, p):
+    """[N,H,W,C] -> [N,H+2p,W+2p,C] (Pix2PixHD's ReflectionPad2d)."""
+    return x[:, reflect_index(x.shape[1], p)][:, :, reflect_index(x.shape[2], p)]
+
+
+def reflect_pad_backward(g, p):
+    N, Hp, Wp, C = g.shape
+    H, W = Hp - 2 * p, Wp - 2 * p
+    rows = np.zeros((N, Hp, W, C))
+    np.add.at(rows, (slice(None), slice(None), reflect_index(W, p)), g)
+    dx = np.zeros((N, H, W, C))
+    np.add.at(dx, (slice(None), reflect_index(H, p)), rows)
+    return dx
+
+
+def instance_norm(x):
+    """Per sample and channel over the H·W positions (Pix2PixHD's
+    InstanceNorm2d, no affine): x̂ = (x − μ_nc)/√(σ²_nc + eps), biased variance.
+    Returns (x̂, rstd [N,1,1,C])."""
+    mu = x.mean(axis=(1, 2), keepdims=True)
+    var = ((x - mu) ** 2).mean(axis=(1, 2), keepdims=True)
+    rstd = 1.0 / np.sqrt(var + BN_EPS)
+    return (x - mu) * rstd, rstd
+
+
+def instance_norm_backward(xhat, rstd, dz):
+    """dx = rstd·(dz − mean_hw(dz) − x̂·mean_hw(dz·x̂))."""
+    return rstd * (dz - dz.mean(axis=(1, 2), keepdims=True) - xhat * (dz * xhat).mean(axis=(1, 2), keepdims=True))
+
+
+def l1_loss(y, t):
+    """L = mean |y − t|; dL/dy = sign(y − t)/count (sign(0) = 0)."""
+    d = y - t
+    return float(np.abs(d).mean()), np.sign(d) / d.size
 
 
 def conv_transpose2x2(x, w):
@@ -240,7 +339,7 @@ class _Net:
                 if lay.get("reshape"):
                     out = out.reshape([xin.shape[0]] + list(lay["reshape"]))
             elif t == "conv":
-                out = rnd(conv2d(xin, wcopy[nm + ".W"], lay["stride"], lay["pad"]))
+                out = rnd(conv2d(xin, wcopy[nm + ".W"], lay["stride"], lay["pad"], lay.get("dil", 1)))
                 if lay.get("in2"):
                     # conv over the concatenation [in, in2] = conv(in, W) + conv(in2, W2);
                     # contributions to one stored tensor accumulate in order with a
@@ -248,6 +347,17 @@ class _Net:
                     out = rnd(out + conv2d(acts[lay["in2"]], wcopy[nm + ".W2"], lay["stride"], lay["pad"]))
             elif t == "convT":
                 out = rnd(conv_transpose2x2(xin, wcopy[nm + ".W"]))
+            elif t == "tconv":
+                out = rnd(conv_transpose2d(xin, wcopy[nm + ".W"], lay["stride"], lay["pad"], lay["_out_hw"]))
+            elif t == "in":
+                xhat, rstd = instance_norm(xin)
+                z = np.maximum(xhat, 0.0) if lay["relu"] else xhat
+                out = rnd(z)
+                saved[nm] = (xhat, rstd)
+            elif t == "reflect_pad":
+                out = reflect_pad(xin, lay["pad"])
+            elif t == "upsample_bilinear":
+                out = rnd(upsample_bilinear(xin, lay["size"]))
             elif t == "bn":
                 axes = tuple(range(xin.ndim - 1))
                 mu = xin.mean(axis=axes)
@@ -265,7 +375,7 @@ class _Net:
                 out, arg = maxpool(xin, lay["r"], lay["stride"], lay["pad"])
                 saved[nm] = arg
             elif t == "gap":
-                out = rnd(xin.mean(axis=(1, 2)))
+                out = rnd(xin.mean(axis=(1, 2), keepdims=bool(lay.get("keepdims"))))
             elif t == "add":                      # residual sum
                 out = rnd(xin + acts[lay["in2"]])
             elif t == "relu":
@@ -325,7 +435,7 @@ class _Net:
                 if need_dx:
                     acc(lay["in"], (dz @ wcopy[nm + ".W"]).reshape(xin.shape))
             elif t == "conv":
-                dx, dw = conv2d_backward(xin, wcopy[nm + ".W"], g, lay["stride"], lay["pad"])
+                dx, dw = conv2d_backward(xin, wcopy[nm + ".W"], g, lay["stride"], lay["pad"], lay.get("dil", 1))
                 pg(nm + ".W", dw)
                 if need_dx:
                     acc(lay["in"], dx)
@@ -337,6 +447,22 @@ class _Net:
                 dx, dw = conv_transpose2x2_backward(xin, wcopy[nm + ".W"], g)
                 pg(nm + ".W", dw)
                 acc(lay["in"], dx)
+            elif t == "tconv":
+                dx, dw = conv_transpose2d_backward(xin, wcopy[nm + ".W"], g, lay["stride"], lay["pad"])
+                pg(nm + ".W", dw)
+                if need_dx:
+                    acc(lay["in"], dx)
+            elif t == "in":
+                xhat, rstd = saved[nm]
+                dz = g * (acts[lay["out"]] > 0) if lay["relu"] else g
+                if need_dx:
+                    acc(lay["in"], instance_norm_backward(xhat, rstd, dz))
+            elif t == "reflect_pad":
+                if need_dx:
+                    acc(lay["in"], reflect_pad_backward(g, lay["pad"]))
+            elif t == "upsample_bilinear":
+                if need_dx:
+                    acc(lay["in"], upsample_bilinear_backward(g, xin.shape[1:3]))
             elif t == "bn":
                 xhat, rstd = saved[nm]
                 out = acts[lay["out"]]
@@ -352,7 +478,8 @@ class _Net:
                 acc(lay["in"], maxpool_backward(g, saved[nm], xin.shape, lay["r"], lay["stride"], lay["pad"]))
             elif t == "gap":
                 H, W = xin.shape[1], xin.shape[2]
-                acc(lay["in"], np.broadcast_to(g[:, None, None, :] / (H * W), xin.shape))
+                g4 = g.reshape(g.shape[0], 1, 1, -1)
+                acc(lay["in"], np.broadcast_to(g4 / (H * W), xin.shape))
             elif t == "add":
                 acc(lay["in"], g)
                 acc(lay["in2"], g)
@@ -415,12 +542,20 @@ def train_step(spec, params, x, labels, momentum=None):
     """One step.  `params`: dict name -> fp32 array (masters); `momentum`:
     dict or None (zeros).  Returns dict with loss, grads, new params, new
     momentum and the stored activations (for inspection)."""
+    _attach_out_hw(spec)
     net = _Net(spec["layers"], params, spec["mode"])
     rnd, r32 = net.rnd, net.r32
     acts = {"x": rnd(np.asarray(x, np.float64))}
-    pix = spec["loss"]["type"] == "softmax_ce_pix"
+    pix = spec["loss"]["type"] in ("softmax_ce_pix", "l1")
     saved = net.forward(acts, fp32_out=() if pix else (spec["loss"]["in"],))
-    if pix:
+    if spec["loss"]["type"] == "l1":
+        # L1 to a target image (the synthetic stand-in for Pix2PixHD's losses);
+        # the output and its gradient are act-dtype tensors, the target is
+        # stored in the act dtype
+        z = acts[spec["loss"]["in"]]
+        loss, dz = l1_loss(z, rnd(np.asarray(labels, np.float64)).reshape(z.shape))
+        G = {spec["loss"]["in"]: rnd(dz)}
+    elif pix:
         # per-pixel cross-entropy over the channel axis, mean over all pixels;
         # the logits are a conv output (act dtype) and so is their gradient
         z = acts[spec["loss"]["in"]]
@@ -434,6 +569,17 @@ def train_step(spec, params, x, labels, momentum=None):
     net.backward(acts, saved, G, grads)
     new_p, new_m = _sgd(spec, params, grads, momentum, r32)
     return {"loss": float(loss), "grads": grads, "params": new_p, "momentum": new_m, "acts": acts}
+
+
+def _attach_out_hw(spec):
+    """Output sizes of the transposed convs (from the layer list's shapes)."""
+    if not any(l["type"] == "tconv" for l in spec["layers"]):
+        return
+    from synth import nets
+    shapes, _ = nets.tensor_shapes(spec)
+    for lay in spec["layers"]:
+        if lay["type"] == "tconv":
+            lay["_out_hw"] = tuple(shapes[lay["out"]][:2])
 
 
 def hinge_d(s, n_real):

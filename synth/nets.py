@@ -215,8 +215,9 @@ def net_shapes(layers, in_name, in_shape):
             shapes[lay["out"]] = list(lay["reshape"]) if lay.get("reshape") else [lay["features"]]
         elif t == "conv":
             H, W, C = ish
-            P = (H + 2 * lay["pad"] - lay["r"]) // lay["stride"] + 1
-            Q = (W + 2 * lay["pad"] - lay["s"]) // lay["stride"] + 1
+            d = lay.get("dil", 1)
+            P = (H + 2 * lay["pad"] - d * (lay["r"] - 1) - 1) // lay["stride"] + 1
+            Q = (W + 2 * lay["pad"] - d * (lay["s"] - 1) - 1) // lay["stride"] + 1
             params[lay["name"] + ".W"] = [lay["k"], lay["r"], lay["s"], C]
             if lay.get("in2"):          # second input channel group (concat-conv)
                 H2, W2, C2 = shapes[lay["in2"]]
@@ -227,6 +228,18 @@ def net_shapes(layers, in_name, in_shape):
             H, W, C = ish
             params[lay["name"] + ".W"] = [C, 2, 2, lay["k"]]
             shapes[lay["out"]] = [2 * H, 2 * W, lay["k"]]
+        elif t == "tconv":             # transposed conv, weight [C_in, r, r, K_out]
+            H, W, C = ish
+            Ho = (H - 1) * lay["stride"] - 2 * lay["pad"] + lay["r"] + lay.get("out_pad", 0)
+            Wo = (W - 1) * lay["stride"] - 2 * lay["pad"] + lay["r"] + lay.get("out_pad", 0)
+            params[lay["name"] + ".W"] = [C, lay["r"], lay["r"], lay["k"]]
+            shapes[lay["out"]] = [Ho, Wo, lay["k"]]
+        elif t == "in":                 # instance norm (no affine parameters)
+            shapes[lay["out"]] = list(ish)
+        elif t == "reflect_pad":
+            shapes[lay["out"]] = [ish[0] + 2 * lay["pad"], ish[1] + 2 * lay["pad"], ish[2]]
+        elif t == "upsample_bilinear":
+            shapes[lay["out"]] = [lay["size"][0], lay["size"][1], ish[2]]
         elif t == "bn":
             C = ish[-1]
             params[lay["name"] + ".gamma"] = [C]
@@ -238,7 +251,7 @@ def net_shapes(layers, in_name, in_shape):
             Q = (W + 2 * lay["pad"] - lay["r"]) // lay["stride"] + 1
             shapes[lay["out"]] = [P, Q, C]
         elif t == "gap":
-            shapes[lay["out"]] = [ish[-1]]
+            shapes[lay["out"]] = [1, 1, ish[-1]] if lay.get("keepdims") else [ish[-1]]
         elif t == "add":
             assert shapes[lay["in2"]] == ish, (lay["name"], shapes[lay["in2"]], ish)
             shapes[lay["out"]] = list(ish)
@@ -274,6 +287,10 @@ def make_inputs(spec, seed_x=0, seed_y=1):
     if len(spec["input"]) == 3 and spec["input"][2] == 8:
         x[..., 3:] = 0.0
     ysize = b
+    if spec.get("loss", {}).get("type") == "l1":   # a target image ~ N(0,1) of the output's shape
+        shp, _ = tensor_shapes(spec)
+        y = np.random.default_rng(seed_y).standard_normal([b] + shp[spec["loss"]["in"]]).astype(np.float32)
+        return x, y
     if spec.get("loss", {}).get("type") == "softmax_ce_pix":   # one label per pixel
         ysize = [b] + list(spec["input"][:2])
     y = np.random.default_rng(seed_y).integers(0, spec["classes"], size=ysize).astype(np.int32)
@@ -457,3 +474,127 @@ def make_gan_inputs(spec, seed=0):
 def make_gan_params(spec, seed=2):
     _, gp, _, dp = gan_shapes(spec)
     return make_params(spec, seed, gp), make_params(spec, seed + 1, dp)
+
+
+def deeplabv3plus(batch=4, image=513, classes=21, mode="bf16", width=64, rates=(6, 12, 18), aspp=256, low=48,
+                  blocks=(3, 4, 6, 3)):
+    """DeepLabv3+ (the paper's third family, PASCAL VOC 513²) on a
+    ResNet-50 backbone at output stride 16: layer4 keeps stride 1 and dilates
+    its 3×3 convs by 2; ASPP over the stride-16 features (1×1 conv, three 3×3
+    atrous convs at `rates`, image pooling: global average → 1×1 conv → BN-ReLU
+    → bilinear back to the map), concatenated and projected by a 1×1 conv; the
+    decoder upsamples ×4 (bilinear), concatenates the 1×1-reduced stride-4
+    features, two 3×3 convs, a 1×1 classifier and a bilinear upsample to the
+    input size; per-pixel softmax cross-entropy.  Every conv is followed by
+    BN(-ReLU).  Synthetic shapes: the backbone is ResNet-50 rather than the
+    paper's (unstated) one."""
+    L = []
+
+    def conv(name, i, o, k, r, st, pad, dil=1):
+        L.append({"type": "conv", "name": name, "in": i, "out": o, "k": k, "r": r, "s": r, "stride": st, "pad": pad,
+                  "dil": dil})
+
+    def bn(name, i, o, relu, res=None):
+        L.append({"type": "bn", "name": name, "in": i, "out": o, "relu": relu, "residual": res})
+
+    def cbr(name, i, o, k, r=1, dil=1):
+        conv(name + "_c", i, name + "_y", k, r, 1, dil * (r - 1) // 2, dil)
+        bn(name + "_bn", name + "_y", o, True)
+
+    conv("conv1", "x", "c1", width, 7, 2, 3)
+    bn("bn1", "c1", "a1", True)
+    L.append({"type": "maxpool", "name": "pool1", "in": "a1", "out": "p1", "r": 3, "stride": 2, "pad": 1})
+    prev, ch = "p1", width
+    for si, nb in enumerate(blocks):
+        planes = width * (2 ** si)
+        for bi in range(nb):
+            st = 2 if (bi == 0 and si in (1, 2)) else 1        # output stride 16: layer4 not strided
+            dil = 2 if si == 3 else 1
+            pre = f"l{si + 1}b{bi}"
+            out_ch = planes * 4
+            res = prev
+            if st != 1 or ch != out_ch:
+                conv(pre + "_dsc", prev, pre + "_dy", out_ch, 1, st, 0)
+                bn(pre + "_dsbn", pre + "_dy", pre + "_ds", False)
+                res = pre + "_ds"
+            conv(pre + "_c1", prev, pre + "_y1", planes, 1, 1, 0)
+            bn(pre + "_bn1", pre + "_y1", pre + "_a1", True)
+            conv(pre + "_c2", pre + "_a1", pre + "_y2", planes, 3, st, dil, dil)
+            bn(pre + "_bn2", pre + "_y2", pre + "_a2", True)
+            conv(pre + "_c3", pre + "_a2", pre + "_y3", out_ch, 1, 1, 0)
+            bn(pre + "_bn3", pre + "_y3", pre + "_out", True, res)
+            prev, ch = pre + "_out", out_ch
+    low_feat = "l1b%d_out" % (blocks[0] - 1)
+    shapes, _ = net_shapes(L, "x", [image, image, 3])
+    fh, fw = shapes[prev][:2]
+    lh, lw = shapes[low_feat][:2]
+    # ASPP
+    cbr("aspp0", prev, "aspp0_o", aspp)
+    for j, r in enumerate(rates):
+        cbr(f"aspp{j + 1}", prev, f"aspp{j + 1}_o", aspp, 3, r)
+    L.append({"type": "gap", "name": "aspp_gap", "in": prev, "out": "aspp_g", "keepdims": True})
+    cbr("aspp_pool", "aspp_g", "aspp_p", aspp)
+    L.append({"type": "upsample_bilinear", "name": "aspp_up", "in": "aspp_p", "out": "aspp4_o", "size": [fh, fw]})
+    cat = "aspp0_o"
+    for j in range(1, 5):
+        L.append({"type": "concat", "name": f"aspp_cat{j}", "in": cat, "in2": f"aspp{j}_o", "out": f"aspp_cat{j}"})
+        cat = f"aspp_cat{j}"
+    cbr("aspp_proj", cat, "aspp_out", aspp)
+    # decoder
+    L.append({"type": "upsample_bilinear", "name": "dec_up", "in": "aspp_out", "out": "dec_u", "size": [lh, lw]})
+    cbr("dec_low", low_feat, "dec_l", low)
+    L.append({"type": "concat", "name": "dec_cat", "in": "dec_u", "in2": "dec_l", "out": "dec_c"})
+    cbr("dec1", "dec_c", "dec1_o", aspp, 3)
+    cbr("dec2", "dec1_o", "dec2_o", aspp, 3)
+    conv("cls", "dec2_o", "cls_o", classes, 1, 1, 0)
+    L.append({"type": "upsample_bilinear", "name": "cls_up", "in": "cls_o", "out": "logits", "size": [image, image]})
+    return {"name": "deeplabv3plus", "mode": mode, "batch": batch, "input": [image, image, 3], "classes": classes,
+            "sgd": {"lr": 0.01, "momentum": 0.9}, "layers": L, "loss": {"type": "softmax_ce_pix", "in": "logits"}}
+
+
+def pix2pixhd(batch=1, image=(512, 1024), ngf=64, n_down=4, n_blocks=9, in_ch=3, out_ch=3, mode="bf16"):
+    """Pix2PixHD's global generator (the paper's second family, Cityscapes
+    512×1024): ReflectionPad 3 → conv 7×7 → IN-ReLU; n_down stride-2
+    3×3 convs doubling the channels (IN-ReLU); n_blocks residual blocks
+    (reflection pad 1, conv 3×3, IN-ReLU, reflection pad 1, conv 3×3, IN, + x);
+    n_down transposed 3×3 stride-2 convs (output padding 1) halving the
+    channels (IN-ReLU); ReflectionPad 3 → conv 7×7 → tanh.  IN = instance
+    norm without affine parameters.  Trained here against an L1 loss to a
+    synthetic target image (the multi-scale discriminator, feature-matching and
+    VGG losses of Pix2PixHD are not modelled: synthetic shapes of the
+    generator's step)."""
+    L = []
+    H, W = image
+
+    def conv(name, i, o, k, r, st, pad):
+        L.append({"type": "conv", "name": name, "in": i, "out": o, "k": k, "r": r, "s": r, "stride": st,
+                  "pad": pad})
+
+    L.append({"type": "reflect_pad", "name": "pad0", "in": "x", "out": "x_p", "pad": 3})
+    conv("c0", "x_p", "c0_y", ngf, 7, 1, 0)
+    L.append({"type": "in", "name": "in0", "in": "c0_y", "out": "a0", "relu": True})
+    prev, ch = "a0", ngf
+    for i in range(n_down):
+        conv(f"down{i}", prev, f"down{i}_y", ch * 2, 3, 2, 1)
+        L.append({"type": "in", "name": f"down{i}_in", "in": f"down{i}_y", "out": f"down{i}_o", "relu": True})
+        prev, ch = f"down{i}_o", ch * 2
+    for b in range(n_blocks):
+        pre = f"res{b}"
+        L.append({"type": "reflect_pad", "name": pre + "_p1", "in": prev, "out": pre + "_xp1", "pad": 1})
+        conv(pre + "_c1", pre + "_xp1", pre + "_y1", ch, 3, 1, 0)
+        L.append({"type": "in", "name": pre + "_in1", "in": pre + "_y1", "out": pre + "_a1", "relu": True})
+        L.append({"type": "reflect_pad", "name": pre + "_p2", "in": pre + "_a1", "out": pre + "_xp2", "pad": 1})
+        conv(pre + "_c2", pre + "_xp2", pre + "_y2", ch, 3, 1, 0)
+        L.append({"type": "in", "name": pre + "_in2", "in": pre + "_y2", "out": pre + "_n2", "relu": False})
+        L.append({"type": "add", "name": pre + "_add", "in": prev, "in2": pre + "_n2", "out": pre + "_out"})
+        prev = pre + "_out"
+    for i in range(n_down):
+        L.append({"type": "tconv", "name": f"up{i}", "in": prev, "out": f"up{i}_y", "k": ch // 2, "r": 3,
+                  "stride": 2, "pad": 1, "out_pad": 1})
+        L.append({"type": "in", "name": f"up{i}_in", "in": f"up{i}_y", "out": f"up{i}_o", "relu": True})
+        prev, ch = f"up{i}_o", ch // 2
+    L.append({"type": "reflect_pad", "name": "padf", "in": prev, "out": "pf", "pad": 3})
+    conv("cf", "pf", "cf_y", out_ch, 7, 1, 0)
+    L.append({"type": "tanh", "name": "tanh", "in": "cf_y", "out": "out"})
+    return {"name": "pix2pixhd", "mode": mode, "batch": batch, "input": [H, W, in_ch], "classes": out_ch,
+            "sgd": {"lr": 0.01, "momentum": 0.9}, "layers": L, "loss": {"type": "l1", "in": "out"}}
