@@ -87,7 +87,7 @@ def conv_fwd(a, ins):
     rnd = _rnd(a)
     x = ins["x"].reshape(N, H, W, C)
     w = ins["w"].reshape(K, R, S, C)
-    c = nm.conv2d(x, rnd(w), st, pad)
+    c = nm.conv2d(x, rnd(w), st, pad, a.get("dil", 1))
     y = rnd(ins["y"].reshape(N, P, Q, K) + c) if a.get("accumulate") else rnd(c)
     out = {"y": y}
     if a.get("bn_stat"):
@@ -100,7 +100,7 @@ def conv_dgrad(a, ins):
     rnd = _rnd(a)
     dy = ins["dy"].reshape(N, P, Q, K)
     w = ins["w"].reshape(K, R, S, C)
-    dx, _ = nm.conv2d_backward(np.zeros((N, H, W, C)), rnd(w), dy, st, pad)
+    dx, _ = nm.conv2d_backward(np.zeros((N, H, W, C)), rnd(w), dy, st, pad, a.get("dil", 1))
     if a.get("accumulate"):
         return {"dx": rnd(ins["dx"].reshape(N, H, W, C) + dx)}
     return {"dx": rnd(dx)}
@@ -110,8 +110,23 @@ def conv_wgrad(a, ins):
     N, H, W, C, K, R, S, st, pad, P, Q = _geom(a)
     x = ins["x"].reshape(N, H, W, C)
     dy = ins["dy"].reshape(N, P, Q, K)
-    _, dw = nm.conv2d_backward(x, np.zeros((K, R, S, C)), dy, st, pad)
+    _, dw = nm.conv2d_backward(x, np.zeros((K, R, S, C)), dy, st, pad, a.get("dil", 1))
     return {"dw": r32(dw)}
+
+
+# transposed convs: attrs describe the conv g they invert (g's input = the
+# big map, its output = the small map, its KRSC weight = the convT weight)
+def convT_fwd(a, ins):
+    return {"y": conv_dgrad(a, {"dy": ins["x"], "w": ins["w"]})["dx"]}
+
+
+def convT_dgrad(a, ins):
+    out = conv_fwd(dict(a, bn_stat=False), {"x": ins["dy"], "w": ins["w"], "y": ins.get("dx")})
+    return {"dx": out["y"]}
+
+
+def convT_wgrad(a, ins):
+    return conv_wgrad(a, {"x": ins["dy"], "dy": ins["x"]})
 
 
 def _bn_out(a, y2, stat, gamma, beta, res):
@@ -266,9 +281,102 @@ def allreduce(a, ins):
     return {"bufs": list(ins["bufs"])}
 
 
+def _acc(a, ins, role, val, shape):
+    rnd = _rnd(a)
+    if a.get("accumulate"):
+        return rnd(ins[role].reshape(shape) + val)
+    return rnd(val)
+
+
+def upsample_bilinear_fwd(a, ins):
+    x = ins["x"].reshape(a["N"], a["H"], a["W"], a["C"])
+    return {"y": _rnd(a)(nm.upsample_bilinear(x, (a["Ho"], a["Wo"])))}
+
+
+def upsample_bilinear_bwd(a, ins):
+    g = ins["g"].reshape(a["N"], a["Ho"], a["Wo"], a["C"])
+    shape = (a["N"], a["H"], a["W"], a["C"])
+    return {"dx": _acc(a, ins, "dx", nm.upsample_bilinear_backward(g, (a["H"], a["W"])), shape)}
+
+
+def reflect_pad_fwd(a, ins):
+    return {"y": nm.reflect_pad(ins["x"].reshape(a["N"], a["H"], a["W"], a["C"]), a["pad"])}
+
+
+def reflect_pad_bwd(a, ins):
+    p = a["pad"]
+    g = ins["g"].reshape(a["N"], a["H"] + 2 * p, a["W"] + 2 * p, a["C"])
+    return {"dx": _acc(a, ins, "dx", nm.reflect_pad_backward(g, p), (a["N"], a["H"], a["W"], a["C"]))}
+
+
+def _in_stat(x):
+    mu = x.mean(axis=1)
+    var = ((x - mu[:, None, :]) ** 2).mean(axis=1)
+    return r32(np.stack([mu, 1.0 / np.sqrt(var + nm.BN_EPS)], axis=1))   # [N, 2, C]
+
+
+def instnorm_fwd(a, ins):
+    N, HW, C = a["N"], a["HW"], a["C"]
+    x = ins["x"].reshape(N, HW, C)
+    st = _in_stat(x)
+    xh = (x - st[:, 0:1, :]) * st[:, 1:2, :]
+    return {"stat": st, "out": _rnd(a)(np.maximum(xh, 0.0) if a.get("relu") else xh)}
+
+
+def instnorm_bwd(a, ins):
+    N, HW, C = a["N"], a["HW"], a["C"]
+    x = ins["x"].reshape(N, HW, C)
+    st = ins["stat"].reshape(N, 2, C)
+    xh = (x - st[:, 0:1, :]) * st[:, 1:2, :]
+    g = ins["g"].reshape(N, HW, C)
+    dz = g * (xh > 0) if a.get("relu") else g
+    dx = st[:, 1:2, :] * (dz - dz.mean(axis=1, keepdims=True) - xh * (dz * xh).mean(axis=1, keepdims=True))
+    return {"dx": _acc(a, ins, "dx", dx, (N, HW, C))}
+
+
+def tanh_fwd(a, ins):
+    return {"y": _rnd(a)(np.tanh(ins["x"]))}
+
+
+def tanh_bwd(a, ins):
+    return {"dx": _acc(a, ins, "dx", ins["g"] * (1.0 - ins["y"] * ins["y"]), ins["g"].shape)}
+
+
+def add_fwd(a, ins):
+    return {"out": _rnd(a)(ins["a"] + ins["b"])}
+
+
+def concat_ch_fwd(a, ins):
+    rows, Ca, Cb = a["rows"], a["Ca"], a["Cb"]
+    return {"out": np.concatenate([ins["a"].reshape(rows, Ca), ins["b"].reshape(rows, Cb)], axis=1)}
+
+
+def concat_ch_bwd(a, ins):
+    rows, Ca, Cb = a["rows"], a["Ca"], a["Cb"]
+    g = ins["g"].reshape(rows, Ca + Cb)
+    rnd = _rnd(a)
+    da = rnd(ins["da"].reshape(rows, Ca) + g[:, :Ca]) if a.get("acc_a") else g[:, :Ca]
+    db = rnd(ins["db"].reshape(rows, Cb) + g[:, Ca:]) if a.get("acc_b") else g[:, Ca:]
+    return {"da": da, "db": db}
+
+
+def softmax_ce_pix(a, ins):
+    rows, K = a["rows"], a["K"]
+    loss, dz = nm.softmax_ce(ins["logits"].reshape(rows, K), ins["labels"].astype(np.int64).reshape(rows))
+    return {"loss": r32(np.array([loss])), "dlogits": _rnd(a)(dz)}
+
+
+def l1_loss(a, ins):
+    loss, dy = nm.l1_loss(ins["y"], ins["target"])
+    return {"loss": r32(np.array([loss])), "dy": _rnd(a)(dy)}
+
+
 OPS = {f.__name__: f for f in (conv_fwd, conv_dgrad, conv_wgrad, bn_fwd, bn_bwd_reduce, bn_bwd_apply,
                                bn_relu_pool_fwd, pool_bn_bwd_reduce, pool_bn_bwd_apply, gap_fwd, gap_bwd,
-                               linear_fwd, linear_bwd, softmax_ce, sgd, allreduce)}
+                               linear_fwd, linear_bwd, softmax_ce, sgd, allreduce, convT_fwd, convT_dgrad,
+                               convT_wgrad, upsample_bilinear_fwd, upsample_bilinear_bwd, reflect_pad_fwd,
+                               reflect_pad_bwd, instnorm_fwd, instnorm_bwd, tanh_fwd, tanh_bwd, add_fwd,
+                               concat_ch_fwd, concat_ch_bwd, softmax_ce_pix, l1_loss)}
 LIST_ROLES = {"sgd": ("w", "g", "m"), "allreduce": ("bufs",)}
 
 

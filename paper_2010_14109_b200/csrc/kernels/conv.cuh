@@ -13,17 +13,26 @@ struct ConvGeom {
                   // "pad_slice"; 0 = as many as fit 32 MiB)
   int nopadh;     // kernel geometry of the folded stem: no vertical padding
                   // (the vertical taps live in the channels), pad is horizontal only
+  int dil;        // dilation (atrous conv, DeepLabv3+): tap (r, s) reads input pixel
+                  // (p·st − pad + dil·r, q·st − pad + dil·s); 0 or 1 = none (attrs "dil")
 };
+__host__ __device__ inline int dil_of(const ConvGeom& g) { return g.dil > 1 ? g.dil : 1; }
 
 inline ConvGeom conv_geom(const OpArgs& a) {
-  return ConvGeom{(int)A(a, "N"), (int)A(a, "H"), (int)A(a, "W"), (int)A(a, "C"), (int)A(a, "K"), (int)A(a, "R"),
-                  (int)A(a, "S"), (int)A(a, "stride"), (int)A(a, "pad"), (int)A(a, "P"), (int)A(a, "Q"),
-                  (int)A(a, "Cw", A(a, "C")), (int)A(a, "pad_slice", 0)};
+  ConvGeom g{(int)A(a, "N"), (int)A(a, "H"), (int)A(a, "W"), (int)A(a, "C"), (int)A(a, "K"), (int)A(a, "R"),
+             (int)A(a, "S"), (int)A(a, "stride"), (int)A(a, "pad"), (int)A(a, "P"), (int)A(a, "Q"),
+             (int)A(a, "Cw", A(a, "C")), (int)A(a, "pad_slice", 0)};
+  g.nopadh = 0;
+  g.dil = (int)A(a, "dil", 1);
+  return g;
 }
 inline ConvGeom conv_geom(const JVal& j) {
-  return ConvGeom{(int)j.geti("N"), (int)j.geti("H"), (int)j.geti("W"), (int)j.geti("C"), (int)j.geti("K"),
-                  (int)j.geti("R"), (int)j.geti("S"), (int)j.geti("stride"), (int)j.geti("pad"), (int)j.geti("P"),
-                  (int)j.geti("Q"), (int)j.geti("Cw", j.geti("C")), (int)j.geti("pad_slice", 0)};
+  ConvGeom g{(int)j.geti("N"), (int)j.geti("H"), (int)j.geti("W"), (int)j.geti("C"), (int)j.geti("K"),
+             (int)j.geti("R"), (int)j.geti("S"), (int)j.geti("stride"), (int)j.geti("pad"), (int)j.geti("P"),
+             (int)j.geti("Q"), (int)j.geti("Cw", j.geti("C")), (int)j.geti("pad_slice", 0)};
+  g.nopadh = 0;
+  g.dil = (int)j.geti("dil", 1);
+  return g;
 }
 
 // CUDA-core implicit GEMM (conv_simt.cu); T = __nv_bfloat16 or float

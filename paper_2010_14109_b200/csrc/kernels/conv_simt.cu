@@ -3,10 +3,11 @@
 // shapes outside the tcgen05 tiling; also the cross-check of conv_tc.cu.
 // NHWC activations of type T (bf16 or fp32), KRSC fp32 weight masters rounded
 // to T on load (the act-dtype weight copy of the numerics contract).
-//   fprop  y[m=(n,p,q), k]   = Σ_{(r,s,c)} x[n, p·st−pad+r, q·st−pad+s, c] · W[k,r,s,c]
-//   dgrad  dx[m=(n,h,w), c]  = Σ_{(r,s,k)} dy[n, (h+pad−r)/st, (w+pad−s)/st, k] · W[k,r,s,c]
+//   fprop  y[m=(n,p,q), k]   = Σ_{(r,s,c)} x[n, p·st−pad+d·r, q·st−pad+d·s, c] · W[k,r,s,c]
+//   dgrad  dx[m=(n,h,w), c]  = Σ_{(r,s,k)} dy[n, (h+pad−d·r)/st, (w+pad−d·s)/st, k] · W[k,r,s,c]
 //                              (terms with a non-integer or out-of-range index vanish)
-//   wgrad  dW[k, (r,s,c)]    = Σ_{m=(n,p,q)} dy[m,k] · x[n, p·st−pad+r, q·st−pad+s, c]
+//   wgrad  dW[k, (r,s,c)]    = Σ_{m=(n,p,q)} dy[m,k] · x[n, p·st−pad+d·r, q·st−pad+d·s, c]
+//   (d = dilation, 1 unless the atrous convs of DeepLabv3+)
 //          deterministic split-K over m: fixed partial slices, fixed-order sum
 #include "conv.cuh"
 
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(256) conv_simt(ConvGeom g, const T* __restrict
             const int q = (int)(gm % g.Q);
             const int64_t t = gm / g.Q;
             const int p = (int)(t % g.P), n = (int)(t / g.P);
-            const int h = p * g.st - g.pad + r, ww = q * g.st - g.pad + s;
+            const int h = p * g.st - g.pad + dil_of(g) * r, ww = q * g.st - g.pad + dil_of(g) * s;
             if (h >= 0 && h < g.H && ww >= 0 && ww < g.W) v = ld_f(a_src + (((int64_t)n * g.H + h) * g.W + ww) * g.C + c);
           } else if (MODE == 1) {
             const int k = (int)(gk % g.K);
@@ -60,7 +61,7 @@ __global__ void __launch_bounds__(256) conv_simt(ConvGeom g, const T* __restrict
             const int ww = (int)(gm % g.W);
             const int64_t t = gm / g.W;
             const int h = (int)(t % g.H), n = (int)(t / g.H);
-            const int pn = h + g.pad - r, qn = ww + g.pad - s;
+            const int pn = h + g.pad - dil_of(g) * r, qn = ww + g.pad - dil_of(g) * s;
             if (pn >= 0 && qn >= 0 && pn % g.st == 0 && qn % g.st == 0) {
               const int p = pn / g.st, q = qn / g.st;
               if (p < g.P && q < g.Q) v = ld_f(a_src + (((int64_t)n * g.P + p) * g.Q + q) * g.K + k);
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(256) conv_simt(ConvGeom g, const T* __restrict
             const int q = (int)(gk % g.Q);
             const int64_t t = gk / g.Q;
             const int p = (int)(t % g.P), n = (int)(t / g.P);
-            const int h = p * g.st - g.pad + r, ww = q * g.st - g.pad + s;
+            const int h = p * g.st - g.pad + dil_of(g) * r, ww = q * g.st - g.pad + dil_of(g) * s;
             if (h >= 0 && h < g.H && ww >= 0 && ww < g.W) v = ld_f(b_src + (((int64_t)n * g.H + h) * g.W + ww) * g.C + c);
           }
         }

@@ -478,6 +478,8 @@ bool conv_tc_ok(const ConvGeom& g, int mode) {
   if ((int64_t)g.N * g.H * g.W * ((g.C + 63) / 64 * 64) >= (1ll << 31) ||
       (int64_t)g.N * g.P * g.Q * ((g.K + 63) / 64 * 64) >= (1ll << 31))
     return false;
+  if (dil_of(g) > 1)   // atrous convs: the TMA kernels with dilated im2col offsets, 64-channel operands
+    return g.C % 64 == 0 && g.K % 64 == 0 && g.Cw == g.C && conv_tma_enabled() && (mode != DGRAD || g.st == 1);
   if (pad_path(g, mode)) return true;
   // zero-padded activation channels (Cw < C) only on the 16-byte-chunk paths
   if (g.Cw != g.C && (g.C % 8 != 0 || g.Cw > g.C || mode == DGRAD)) return false;

@@ -79,6 +79,7 @@ struct Params {
   int Sw, r0, s0, dst, ph, pw, Ho, Wo;
   FastDiv fQ, fP, fCb, fS;
   unsigned long long* probe;   // launch probe (timeline mode), or null
+  int dil;                     // im2col tap offsets × dil (atrous convs); 0/1 = none
 };
 
 __device__ __forceinline__ void base_of(const Params& P, int pix, int& w, int& h, int& n) {
@@ -215,7 +216,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
               for (int j = 0; j < nrb; ++j) {
                 const int blk = rb0 + j;
                 const int tap = (int)P.fCb.div((uint32_t)blk), cb = blk - tap * (P.Cr / 64);
-                const int r = (int)P.fS.div((uint32_t)tap), s = tap - r * P.S;
+                const int dl = P.dil > 1 ? P.dil : 1;
+                const int r = (int)P.fS.div((uint32_t)tap) * dl, s = (tap - (r / dl) * P.S) * dl;
                 tma_load_im2col_pair(a + j * ATOM, &P.ta, fb, cb * 64, pw, ph, pn, (uint16_t)s, (uint16_t)r);
               }
 #pragma unroll
@@ -226,7 +228,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
               for (int j = 0; j < nrb; ++j) {
                 const int blk = rb0 + j;
                 const int tap = (int)P.fCb.div((uint32_t)blk), cb = blk - tap * (P.Cr / 64);
-                const int r = (int)P.fS.div((uint32_t)tap), s = tap - r * P.S;
+                const int dl = P.dil > 1 ? P.dil : 1;
+                const int r = (int)P.fS.div((uint32_t)tap) * dl, s = (tap - (r / dl) * P.S) * dl;
                 tma_load_im2col(a + j * ATOM, &P.ta, &full[sg], cb * 64, pw, ph, pn, (uint16_t)s, (uint16_t)r);
               }
 #pragma unroll
@@ -249,8 +252,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
             tma_load_2d(b, &P.tb, &full[sg], kb * BK, nt * BN);
           } else {
             const int tap = (int)P.fCb.div((uint32_t)kb), cb = kb - tap * (P.Cr / 64);
-            const int r = (int)P.fS.div((uint32_t)tap), s = tap - r * P.S;
-            const int btap = MODE == DGRAD ? (P.r0 + P.dst * (P.R - 1 - r)) * P.Sw + P.s0 + P.dst * (P.S - 1 - s) : tap;
+            const int r0_ = (int)P.fS.div((uint32_t)tap), s0_ = tap - r0_ * P.S;
+            const int btap = MODE == DGRAD ? (P.r0 + P.dst * (P.R - 1 - r0_)) * P.Sw + P.s0 + P.dst * (P.S - 1 - s0_)
+                                           : tap;
+            const int dl = P.dil > 1 ? P.dil : 1;
+            const int r = r0_ * dl, s = s0_ * dl;   // im2col offsets (dilated taps)
             if (CG == 2) {
               // both CTAs' bytes land on the leader's barrier
               const uint32_t fb = mapa(smem_u32(&full[sg]), 0);
@@ -1288,7 +1294,8 @@ bool conv_tma_enabled() {
 // which kernel geometries the TMA kernels take (after the narrow-input re-layout)
 bool conv_tma_ok(const ConvGeom& g, int mode) {
   if (!conv_tma_enabled()) return false;
-  if (g.pad > 127 || g.R > 64 || g.S > 64 || g.st > 8) return false;
+  if (g.pad > 127 || g.R > 64 || g.S > 64 || g.st > 8 || dil_of(g) * (g.R - 1) > 127) return false;
+  if (dil_of(g) > 1 && (g.C % 64 != 0 || (mode == DGRAD && g.st != 1))) return false;
   if (g.nopadh && mode == DGRAD) return false;
   if (mode == FPROP) return g.K % 64 == 0 && (g.C % 64 == 0 || g.C == 8 || g.C == 16);
   if (mode == DGRAD) return g.C % 64 == 0 && g.K % 64 == 0;
@@ -1392,7 +1399,8 @@ Status conv_halo3_tma(OpArgs& a, int N, int Hm, int Wm, const __nv_bfloat16* in,
 }
 
 bool halo3_geom(const ConvGeom& g) {
-  return g.C == 64 && g.K == 64 && g.R == 3 && g.S == 3 && g.st == 1 && g.pad == 1 && !g.nopadh && g.P == g.H &&
+  return g.C == 64 && g.K == 64 && g.R == 3 && g.S == 3 && g.st == 1 && g.pad == 1 && !g.nopadh && dil_of(g) == 1 &&
+         g.P == g.H &&
          g.Q == g.W && halo3_enabled() && tstore_enabled();
 }
 
@@ -1402,7 +1410,7 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
                       __nv_bfloat16* y, bool accumulate, int nst, float* stat_part, int* stat_slots) {
   if (stat_slots) *stat_slots = 0;
   if (g.C == 16 && g.R == 4 && g.S == 4 && g.st == 1 && !g.nopadh && g.K == 64 && kpad == 256 && g.P % 16 == 0 &&
-      g.Q % 8 == 0 && !accumulate && !nst && tstore_enabled() && stem_enabled())
+      g.Q % 8 == 0 && !accumulate && !nst && tstore_enabled() && stem_enabled() && dil_of(g) == 1)
     return conv_stem_tma(a, g, x, wb, kpad, y, stat_part, stat_slots);
   if (halo3_geom(g) && kpad == 576 && !accumulate && !nst)
     return conv_halo3_tma(a, g.N, g.H, g.W, x, wb, y, false, stat_part, stat_slots);
@@ -1436,6 +1444,7 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   P.R = g.R;
   P.S = g.S;
   P.Cr = g.C;
+  P.dil = dil_of(g);
   fill(P);
   int* ss = nullptr;
   if (stat_part && P.tstore && !nst && !accumulate) {
@@ -1474,8 +1483,10 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
       if (Hp <= 0 || Wp <= 0) continue;
       if (nr == 0 || ns == 0) continue;   // zero (cleared above) or unchanged (accumulating)
       // dy row of (h', tap i') is h' − pad'' + i' with pad'' = nr − 1 − (ph + pad − r0)/st
+      // (dilation d, stride 1 only: tap i' reads dy row h' − (d·(nr − 1) − pad) + d·i')
+      const int dl = dil_of(g);
       const int dh = (ph + g.pad - r0) / g.st, dw = (pw + g.pad - s0) / g.st;
-      const int padh = nr > 0 ? nr - 1 - dh : 0, padw = ns > 0 ? ns - 1 - dw : 0;
+      const int padh = nr > 0 ? dl * (nr - 1) - dh : 0, padw = ns > 0 ? dl * (ns - 1) - dw : 0;
       Status st = make_im2col(&P.ta, dy, g.N, g.P, g.Q, g.K, 64, BM, Hp, Wp, 1, padh, padw);
       if (!st.good()) return st;
       const Tile tile = choose_tile(g.N * Hp * Wp, g.C, std::max(1, nr * ns * g.K / BK));
@@ -1509,6 +1520,7 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
       P.pw = pw;
       P.Ho = g.H;
       P.Wo = g.W;
+      P.dil = dl;
       fill(P);
       st = launch_tile<DGRAD>(a, P, tile);
       if (!st.good()) return st;
@@ -1558,7 +1570,7 @@ Status conv_stem_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x,
 Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
                       int splits, int kb_per_split, bool accumulate) {
   if (g.C == 16 && g.R == 4 && g.S == 4 && g.st == 1 && !g.nopadh && g.K == 64 && g.P % 16 == 0 && g.Q % 8 == 0 &&
-      splits >= 1 && splits <= 1024 && stem_enabled())
+      splits >= 1 && splits <= 1024 && stem_enabled() && dil_of(g) == 1)
     return conv_stem_wgrad_tma(a, g, x, dy, part, splits, accumulate);
   Params P{};
   const int nch = g.C == 16 ? 16 : 0;
@@ -1594,6 +1606,7 @@ Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   P.R = g.R;
   P.S = g.S;
   P.Cr = g.C;
+  P.dil = dil_of(g);
   fill(P);
   if (nch) return BN == 128 ? launch<WGRAD, 128, 16>(a, P) : launch<WGRAD, 64, 16>(a, P);
   if (pbn == 256) {

@@ -12,7 +12,8 @@ namespace oc {
   X(kPoolBnBwdApply) X(kGapFwd) X(kGapBwd) X(kAddFwd) X(kMaxpoolFwd) X(kMaxpoolBwd) X(kSoftmaxCEPix) X(kConvTFwd) \
   X(kConvTDgrad) X(kConvTWgrad) X(kUpsample2Fwd) X(kUpsample2Bwd) X(kAvgpool2Fwd) X(kAvgpool2Bwd) \
   X(kReluFwd) X(kReluBwd) X(kTanhFwd) X(kTanhBwd) X(kConcatBatch) X(kScaleAddFwd) X(kScaleAddBwd) X(kAttnFwd) \
-  X(kAttnBwd) X(kHingeD) X(kHingeG) X(kConcatChFwd) X(kConcatChBwd)
+  X(kAttnBwd) X(kHingeD) X(kHingeG) X(kConcatChFwd) X(kConcatChBwd) X(kUpsampleBilinearFwd)                  \
+  X(kUpsampleBilinearBwd) X(kInstnormFwd) X(kInstnormBwd) X(kReflectPadFwd) X(kReflectPadBwd) X(kL1Loss)
 
 #define OC_DECL(n) extern const OpDesc n;
 OC_OPS(OC_DECL)

@@ -34,8 +34,13 @@ def build_convnet(spec, params="pinned", inputs="host", dp_bucket_bytes=0):
     pin_in = inputs == "pinned"
     x = b.var("x", Nb * int(np.prod(spec["input"])) * ACT, persistent=not pin_in, pinned=pin_in,
               shape=[Nb] + spec["input"], dtype=DT)
-    ylen = Nb * (int(np.prod(spec["input"][:2])) if spec["loss"]["type"] == "softmax_ce_pix" else 1)
-    y = b.var("labels", ylen * I32, persistent=not pin_in, pinned=pin_in, shape=[ylen], dtype="i32")
+    if spec["loss"]["type"] == "l1":   # the target image (act dtype) of the L1 loss
+        tshape = shapes[spec["loss"]["in"]]
+        y = b.var("labels", Nb * int(np.prod(tshape)) * ACT, persistent=not pin_in, pinned=pin_in,
+                  shape=[Nb] + tshape, dtype=DT)
+    else:
+        ylen = Nb * (int(np.prod(spec["input"][:2])) if spec["loss"]["type"] == "softmax_ce_pix" else 1)
+        y = b.var("labels", ylen * I32, persistent=not pin_in, pinned=pin_in, shape=[ylen], dtype="i32")
     P, Mo, G = _pvars(b, spec, pshapes, params)
     layers = spec["layers"]
 
@@ -77,6 +82,8 @@ def build_convnet(spec, params="pinned", inputs="host", dp_bucket_bytes=0):
             attrs = {"dtype": DT, "N": Nb, "H": H, "W": W, "C": C, "K": K, "R": lay["r"], "S": lay["s"],
                      "stride": lay["stride"],
                      "pad": lay["pad"], "P": Pq, "Q": Qq}
+            if lay.get("dil", 1) > 1:
+                attrs["dil"] = lay["dil"]
             lay["_attrs"] = attrs
             if nm in bn_of_conv:
                 bnm = bn_of_conv[nm]
@@ -104,6 +111,37 @@ def build_convnet(spec, params="pinned", inputs="host", dp_bucket_bytes=0):
             lay["_attrs"] = attrs
             b.fn(f"fwd.{nm}", "convT_fwd", {"x": t[lay["in"]], "w": P[nm + ".W"], "y": t[lay["out"]]}, attrs,
                  [t[lay["in"]], P[nm + ".W"]], [t[lay["out"]]])
+        elif ty == "tconv":
+            # transposed conv (Pix2PixHD): the data gradient of the conv from the
+            # output map to the input map (convT_* ops, virtual conv attrs)
+            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
+            H, W, C = shapes[lay["in"]]
+            Ho, Wo, Ko = shapes[lay["out"]]
+            attrs = {"dtype": DT, "N": Nb, "H": Ho, "W": Wo, "C": Ko, "K": C, "R": lay["r"], "S": lay["r"],
+                     "stride": lay["stride"], "pad": lay["pad"], "P": H, "Q": W}
+            lay["_attrs"] = attrs
+            b.fn(f"fwd.{nm}", "convT_fwd", {"x": t[lay["in"]], "w": P[nm + ".W"], "y": t[lay["out"]]}, attrs,
+                 [t[lay["in"]], P[nm + ".W"]], [t[lay["out"]]])
+        elif ty == "in":
+            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
+            H, W, C = shapes[lay["in"]]
+            stat[nm] = b.var(f"stat.{nm}", Nb * 2 * C * F32, shape=[Nb, 2, C], dtype="f32")
+            lay["_attrs"] = {"dtype": DT, "N": Nb, "HW": H * W, "C": C, "relu": lay["relu"]}
+            b.fn(f"fwd.{nm}", "instnorm_fwd", {"x": t[lay["in"]], "out": t[lay["out"]], "stat": stat[nm]},
+                 lay["_attrs"], [t[lay["in"]]], [t[lay["out"]], stat[nm]])
+        elif ty in ("reflect_pad", "upsample_bilinear"):
+            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
+            H, W, C = shapes[lay["in"]]
+            Ho, Wo, _ = shapes[lay["out"]]
+            lay["_attrs"] = {"dtype": DT, "N": Nb, "H": H, "W": W, "C": C, "pad": lay.get("pad", 0), "Ho": Ho,
+                             "Wo": Wo}
+            b.fn(f"fwd.{nm}", ty + "_fwd", {"x": t[lay["in"]], "y": t[lay["out"]]}, lay["_attrs"], [t[lay["in"]]],
+                 [t[lay["out"]]])
+        elif ty == "tanh":
+            t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
+            lay["_attrs"] = {"dtype": DT, "n": Nb * int(np.prod(shapes[lay["out"]]))}
+            b.fn(f"fwd.{nm}", "tanh_fwd", {"x": t[lay["in"]], "y": t[lay["out"]]}, lay["_attrs"], [t[lay["in"]]],
+                 [t[lay["out"]]])
         elif ty == "maxpool":
             t[lay["out"]] = b.var(lay["out"], nbytes(lay["out"]), shape=[Nb] + shapes[lay["out"]], dtype=DT)
             idx[nm] = b.var(f"idx.{nm}", nbytes(lay["out"], U8), shape=[Nb] + shapes[lay["out"]], dtype="u8")
@@ -182,7 +220,12 @@ def build_convnet(spec, params="pinned", inputs="host", dp_bucket_bytes=0):
     loss = b.var("loss", F32, persistent=True, shape=[], dtype="f32")
     logits = t[spec["loss"]["in"]]
     g = {}   # tensor -> variable holding its gradient
-    if spec["loss"]["type"] == "softmax_ce_pix":
+    if spec["loss"]["type"] == "l1":
+        lt = spec["loss"]["in"]
+        g[lt] = b.var("grad." + lt, nbytes(lt), shape=[Nb] + shapes[lt], dtype=DT)
+        b.fn("loss", "l1_loss", {"y": logits, "target": y, "loss": loss, "dy": g[lt]},
+             {"dtype": DT, "n": Nb * int(np.prod(shapes[lt]))}, [logits, y], [loss, g[lt]])
+    elif spec["loss"]["type"] == "softmax_ce_pix":
         # per-pixel CE over the channel axis of a conv output (act dtype in and out)
         lt = spec["loss"]["in"]
         g[lt] = b.var("grad.logits", nbytes(lt), shape=[Nb] + shapes[lt], dtype=DT)
@@ -297,6 +340,43 @@ def build_convnet(spec, params="pinned", inputs="host", dp_bucket_bytes=0):
             b.fn(f"bwd.{nm}.dgrad", "convT_dgrad", {"dy": gv, "w": P[nm + ".W"], "dx": dx},
                  dict(lay["_attrs"], accumulate=acc), ins, [dx])
             _update(b, spec, nm, P, Mo, G, [nm + ".W"])
+        elif ty == "tconv":
+            src = lay["in"]
+            b.fn(f"bwd.{nm}.wgrad", "convT_wgrad", {"dy": gv, "x": t[src], "dw": G[nm + ".W"]}, lay["_attrs"],
+                 [gv, t[src]], [G[nm + ".W"]])
+            acc = src in g
+            if acc:
+                dx = g[src]
+                ins = [gv, P[nm + ".W"], dx]
+            else:
+                dx = b.var(f"grad.{src}", nbytes(src), shape=[Nb] + shapes[src], dtype=DT)
+                ins = [gv, P[nm + ".W"]]
+                g[src] = dx
+            b.fn(f"bwd.{nm}.dgrad", "convT_dgrad", {"dy": gv, "w": P[nm + ".W"], "dx": dx},
+                 dict(lay["_attrs"], accumulate=acc), ins, [dx])
+            _update(b, spec, nm, P, Mo, G, [nm + ".W"])
+        elif ty in ("in", "reflect_pad", "upsample_bilinear", "tanh"):
+            src = lay["in"]
+            if src == "x":
+                continue
+            acc = src in g
+            if acc:
+                dx = g[src]
+            else:
+                dx = b.var(f"grad.{src}", nbytes(src), shape=[Nb] + shapes[src], dtype=DT)
+                g[src] = dx
+            at = dict(lay["_attrs"], accumulate=acc)
+            if ty == "in":
+                args = {"g": gv, "x": t[src], "stat": stat[nm], "dx": dx}
+                ins = [gv, t[src], stat[nm]]
+            elif ty == "tanh":
+                args = {"g": gv, "y": t[lay["out"]], "dx": dx}
+                ins = [gv, t[lay["out"]]]
+            else:
+                args = {"g": gv, "dx": dx}
+                ins = [gv]
+            b.fn(f"bwd.{nm}", {"in": "instnorm", "tanh": "tanh"}.get(ty, ty) + "_bwd", args, at,
+                 ins + ([dx] if acc else []), [dx])
         elif ty == "avgpool2":
             src = lay["in"]
             acc = src in g

@@ -29,7 +29,8 @@ def _chain(spec):
     x, y = nets.make_inputs(spec)
     p = nets.make_params(spec)
     rnd = nm.rounder(spec["mode"])
-    vals = {info["x"]: rnd(np.asarray(x, np.float64)), info["labels"]: np.asarray(y, np.int64)}
+    lab = rnd(np.asarray(y, np.float64)) if spec["loss"]["type"] == "l1" else np.asarray(y, np.int64)
+    vals = {info["x"]: rnd(np.asarray(x, np.float64)), info["labels"]: lab}
     for k, v in p.items():
         vals[info["params"][k]] = np.asarray(v, np.float64)
         vals[info["momentum"][k]] = np.zeros(np.asarray(v).shape)
@@ -42,6 +43,12 @@ def _chain(spec):
     (nets.tiny_resnet(batch=4, image=16, classes=10, mode="fp32"), 1e-6),
     (nets.resnet(18, batch=8, image=64, classes=10, mode="fp32"), 1e-5),
     (nets.tiny_resnet(batch=4, image=16, classes=10, mode="bf16"), 1e-3),
+    # F3 families (the paper's Fig.4/5 networks): atrous convs, ASPP, bilinear
+    # decoder; reflection padding, instance norm, transposed convs, tanh, L1
+    (nets.deeplabv3plus(batch=4, image=33, classes=3, width=8, rates=(2, 3, 4), aspp=8, low=8,
+                        blocks=(1, 1, 1, 1), mode="fp32"), 1e-5),
+    (nets.pix2pixhd(batch=2, image=(16, 32), ngf=8, n_down=2, n_blocks=1, mode="fp32"), 1e-5),
+    (nets.pix2pixhd(batch=2, image=(16, 32), ngf=8, n_down=2, n_blocks=1, mode="bf16"), 1e-3),
 ])
 def test_graph_chain_equals_train_step(spec, tol):
     vals, info, ref, p = _chain(spec)
@@ -58,7 +65,8 @@ def test_graph_chain_equals_train_step(spec, tol):
 
 def test_every_conv_graph_op_kind_has_a_definition():
     import json
-    for spec in (nets.resnet(18, batch=2, image=32), nets.resnet(50, batch=2, image=32), nets.tiny_resnet()):
+    for spec in (nets.resnet(18, batch=2, image=32), nets.resnet(50, batch=2, image=32), nets.tiny_resnet(),
+                 nets.deeplabv3plus(batch=2, image=65), nets.pix2pixhd(batch=1, image=(32, 64), ngf=8)):
         doc, _ = graphs.build(spec, params="pinned")
         kinds = {f["op"]["kind"] for f in json.loads(doc)["functions"]}
         assert kinds <= set(layerwise.OPS), kinds - set(layerwise.OPS)
