@@ -53,7 +53,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="r50", choices=["r50", "r18", "r1001", "mlp", "biggan", "unet", "densenet"])
+    ap.add_argument("--config", default="r50",
+                    choices=["r50", "r18", "r1001", "mlp", "biggan", "unet", "densenet", "deeplab", "pix2pix"])
     ap.add_argument("--mode", default="va", choices=["va", "best", "first"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--phys-gib", type=float, default=8.0, help="r50: physical device budget per GPU (GiB)")
@@ -100,6 +101,10 @@ def spec_for(args, batch=None):
         return nets.biggan(batch=batch or args.batch or 32)
     if c == "r1001":
         return nets.preact_resnet(1001, batch=batch or args.batch or 256)
+    if c == "deeplab":       # DeepLabv3+ on PASCAL-VOC-sized 513² images
+        return nets.deeplabv3plus(batch=batch or args.batch or 16)
+    if c == "pix2pix":       # Pix2PixHD global generator on Cityscapes-sized 512×1024
+        return nets.pix2pixhd(batch=batch or args.batch or 4)
     return nets.resnet(18, batch=batch or args.batch or 256)
 
 
@@ -129,6 +134,12 @@ def workload_name(args, spec, B_p, b0):
     if c == "r1001":
         return (f"configs[4] pre-activation ResNet-1001 32x32 b={spec['batch']} at {args.budget_frac:.2f} of the "
                 "in-core footprint, tensors < 1 VA chunk pinned")
+    if c == "deeplab":
+        return (f"F3 DeepLabv3+ (ResNet-50, output stride 16) 513x513 b={spec['batch']} at {args.budget_frac:.2f} "
+                "of the in-core footprint")
+    if c == "pix2pix":
+        return (f"F3 Pix2PixHD global generator 512x1024 b={spec['batch']} (L1 loss) at {args.budget_frac:.2f} of "
+                "the in-core footprint")
     return f"F3 DenseNet-121 224x224 b={spec['batch']} at {args.budget_frac:.2f} of the in-core footprint"
 
 
@@ -727,6 +738,13 @@ def oracle_sample(args):
     elif args.config == "densenet":
         spec = nets.densenet(batch=1)
         scale, note = 1.0, "densenet121 batch 1 per step"
+    elif args.config == "deeplab":
+        spec = nets.deeplabv3plus(batch=2, image=257)
+        scale, note = 2.0, ("deeplabv3plus batch 2 on a 257x257 crop, time scaled by the 4x pixel count to one "
+                            "513x513 sample pair (extrapolated)")
+    elif args.config == "pix2pix":
+        spec = nets.pix2pixhd(batch=1, image=(128, 256))
+        scale, note = 16.0, "pix2pixhd batch 1 on a 128x256 crop, time scaled by the 16x pixel count (extrapolated)"
     else:
         spec = {"r50": lambda: nets.resnet(50, batch=1), "r1001": lambda: nets.preact_resnet(1001, batch=2)}.get(
             args.config, lambda: nets.resnet(18, batch=2))()

@@ -110,7 +110,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* ldbar = tempty + 2;        // accumulate epilogue: old-output box loads (warp q, buffer b) -> 2q + b
+  uint32_t* tmem_slot = (uint32_t*)(ldbar + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   KProbe kp;
   if (threadIdx.x == 0) probe_begin(kp);
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
     tma_prefetch(&P.tb);
     for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4 * CG); }
+    for (int b = 0; b < 8; ++b) mbar_init(&ldbar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -341,6 +343,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
       float ssum[BN / 64][2], ssq[BN / 64][2];
 #pragma unroll
       for (int jb = 0; jb < BN / 64; ++jb) ssum[jb][0] = ssum[jb][1] = ssq[jb][0] = ssq[jb][1] = 0.f;
+      uint32_t ldph = 0;   // accumulate: phase bits of this warp's two box-load barriers
       for (int u = u0; u < units; u += ustep, ++lt) {
         int mt, nt, z, kb0, nk;
         unit_of(u, mt, nt, z, kb0, nk);
@@ -360,14 +363,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");   // this buffer's last store read
             __syncwarp();
             const uint32_t sb = smem_u32(stg) + (uint32_t)(q * 2 + (sc & 1)) * 4096u;
+            if (P.accumulate) {
+              // out = rnd(old + acc): the old box arrives by TMA in the same
+              // swizzled staging layout the store uses (rows past M zero-filled)
+              uint64_t* lb = &ldbar[q * 2 + (sc & 1)];
+              if (lane == 0) {
+                mbar_expect_tx(lb, 4096);
+                tma_load_2d(sb, &P.tc, lb, nt * BN + j0, row0);
+              }
+              mbar_wait(lb, (ldph >> (sc & 1)) & 1);
+              ldph ^= 1u << (sc & 1);
+            }
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               uint32_t w[4];
+              uint32_t old[4] = {0u, 0u, 0u, 0u};
+              if (P.accumulate)
+                asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(old[0]), "=r"(old[1]), "=r"(old[2]), "=r"(old[3])
+                             : "r"(sb + lane * 128 + ((c ^ (lane & 7)) << 4))
+                             : "memory");
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const uint32_t lo = c < 4 ? v0[c * 8 + 2 * e] : v1[(c - 4) * 8 + 2 * e];
                 const uint32_t hi = c < 4 ? v0[c * 8 + 2 * e + 1] : v1[(c - 4) * 8 + 2 * e + 1];
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(nk ? __uint_as_float(lo) : 0.f, nk ? __uint_as_float(hi) : 0.f);
+                float flo = nk ? __uint_as_float(lo) : 0.f, fhi = nk ? __uint_as_float(hi) : 0.f;
+                if (P.accumulate) {
+                  const float2 o2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&old[e]));
+                  flo += o2.x;
+                  fhi += o2.y;
+                }
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(flo, fhi);
                 w[e] = *reinterpret_cast<uint32_t*>(&h2);
               }
               asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sb + lane * 128 + ((c ^ (lane & 7)) << 4)),
@@ -1428,7 +1454,7 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   P.out = y;
   P.nst = nst;
   P.accumulate = accumulate ? 1 : 0;
-  st = set_tstore(P, y, g.N * g.P * g.Q, nst ? nst : g.K, !accumulate);
+  st = set_tstore(P, y, g.N * g.P * g.Q, nst ? nst : g.K, true);
   if (!st.good()) return st;
   P.M = g.N * g.P * g.Q;
   P.N = g.K;
@@ -1496,7 +1522,7 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
       P.out = dx;
       P.nst = nst;
       P.accumulate = accumulate ? 1 : 0;
-      st = set_tstore(P, dx, g.N * Hp * Wp, nst ? nst : g.C, !accumulate && g.st == 1);
+      st = set_tstore(P, dx, g.N * Hp * Wp, nst ? nst : g.C, g.st == 1);
       if (!st.good()) return st;
       P.M = g.N * Hp * Wp;
       P.N = g.C;

@@ -54,6 +54,9 @@ def run_layerwise(spec, budget_frac=0.25, pin_below=MiB, mode="va", window=0, ch
     p = nets.make_params(spec)
     st.write(info["x"], x.astype(np.float32) if spec["mode"] == "fp32"
              else torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy())
+    if spec["loss"]["type"] == "l1":   # the target image, stored in the act dtype
+        y = y.astype(np.float32) if spec["mode"] == "fp32" else \
+            torch.from_numpy(np.ascontiguousarray(y, np.float32)).to(torch.bfloat16).view(torch.int16).numpy()
     st.write(info["labels"], y)
     for k, v in p.items():
         st.write(info["params"][k], v)

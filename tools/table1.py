@@ -1,5 +1,5 @@
 """Table-1 / Fig.3-shaped sweep on B200 (Table 1 P:127-143,
-Fig.3): ResNet-50 224², batch swept at Table 1's batch/190 ratios
+Fig.3; --net densenet|deeplab|pix2pix: the Fig.4/5 families): ResNet-50 224², batch swept at Table 1's batch/190 ratios
 around the in-core maximum b0 under a fixed physical memory B_p, three rows:
   in-core      (no swapping; only batches whose in-core footprint fits B_p)
   schedule     window schedule + caching best-fit arena (the frameworks' default)
@@ -50,6 +50,8 @@ def max_budget(G, phys, mode, chunk, W=0):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--depth", type=int, default=50)
+    ap.add_argument("--net", default="resnet", choices=["resnet", "densenet", "deeplab", "pix2pix"],
+                    help="resnet (Table 1) or the paper's Fig.4/5 families (SURVEY F3)")
     ap.add_argument("--phys-gib", type=float, default=8.0)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--chunk-mib", type=int, default=40)
@@ -62,12 +64,14 @@ def main():
     from synth import nets
     phys = int(a.phys_gib * (1 << 30))
     chunk = a.chunk_mib << 20
-    b0 = bench.trainable_batch(lambda b: nets.resnet(a.depth, batch=b), phys)
+    make = {"resnet": lambda b: nets.resnet(a.depth, batch=b), "densenet": lambda b: nets.densenet(batch=b),
+            "deeplab": lambda b: nets.deeplabv3plus(batch=b), "pix2pix": lambda b: nets.pix2pixhd(batch=b)}[a.net]
+    b0 = bench.trainable_batch(make, phys)
     print(json.dumps({"b0_in_core_max": b0, "phys_bytes": phys, "chunk_bytes": chunk}), flush=True)
     ratios = [float(r) for r in a.ratios.split(",")] if a.ratios else RATIOS
     for r in ratios:
         b = max(1, int(round(b0 * r)))
-        spec = nets.resnet(a.depth, batch=b)
+        spec = make(b)
         doc, info = graphs.build(spec, params="persistent")
         G = B.Graph(doc)
         F = G.in_core_peak()
