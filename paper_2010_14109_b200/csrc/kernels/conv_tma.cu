@@ -363,7 +363,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");   // this buffer's last store read
             __syncwarp();
             const uint32_t sb = smem_u32(stg) + (uint32_t)(q * 2 + (sc & 1)) * 4096u;
-            if (P.accumulate) {
+            if (!P.accumulate) {
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const uint32_t lo = c < 4 ? v0[c * 8 + 2 * e] : v1[(c - 4) * 8 + 2 * e];
+                  const uint32_t hi = c < 4 ? v0[c * 8 + 2 * e + 1] : v1[(c - 4) * 8 + 2 * e + 1];
+                  __nv_bfloat162 h2 =
+                      __floats2bfloat162_rn(nk ? __uint_as_float(lo) : 0.f, nk ? __uint_as_float(hi) : 0.f);
+                  w[e] = *reinterpret_cast<uint32_t*>(&h2);
+                }
+                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sb + lane * 128 + ((c ^ (lane & 7)) << 4)),
+                             "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                             : "memory");
+              }
+            } else {
               // out = rnd(old + acc): the old box arrives by TMA in the same
               // swizzled staging layout the store uses (rows past M zero-filled)
               uint64_t* lb = &ldbar[q * 2 + (sc & 1)];
@@ -373,32 +389,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
               }
               mbar_wait(lb, (ldph >> (sc & 1)) & 1);
               ldph ^= 1u << (sc & 1);
-            }
+              uint32_t old[8][4];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              uint32_t w[4];
-              uint32_t old[4] = {0u, 0u, 0u, 0u};
-              if (P.accumulate)
+              for (int c = 0; c < 8; ++c)
                 asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                             : "=r"(old[0]), "=r"(old[1]), "=r"(old[2]), "=r"(old[3])
+                             : "=r"(old[c][0]), "=r"(old[c][1]), "=r"(old[c][2]), "=r"(old[c][3])
                              : "r"(sb + lane * 128 + ((c ^ (lane & 7)) << 4))
                              : "memory");
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const uint32_t lo = c < 4 ? v0[c * 8 + 2 * e] : v1[(c - 4) * 8 + 2 * e];
-                const uint32_t hi = c < 4 ? v0[c * 8 + 2 * e + 1] : v1[(c - 4) * 8 + 2 * e + 1];
-                float flo = nk ? __uint_as_float(lo) : 0.f, fhi = nk ? __uint_as_float(hi) : 0.f;
-                if (P.accumulate) {
-                  const float2 o2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&old[e]));
-                  flo += o2.x;
-                  fhi += o2.y;
+              for (int c = 0; c < 8; ++c) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const uint32_t lo = c < 4 ? v0[c * 8 + 2 * e] : v1[(c - 4) * 8 + 2 * e];
+                  const uint32_t hi = c < 4 ? v0[c * 8 + 2 * e + 1] : v1[(c - 4) * 8 + 2 * e + 1];
+                  const float2 o2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&old[c][e]));
+                  __nv_bfloat162 h2 = __floats2bfloat162_rn((nk ? __uint_as_float(lo) : 0.f) + o2.x,
+                                                            (nk ? __uint_as_float(hi) : 0.f) + o2.y);
+                  w[e] = *reinterpret_cast<uint32_t*>(&h2);
                 }
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(flo, fhi);
-                w[e] = *reinterpret_cast<uint32_t*>(&h2);
+                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sb + lane * 128 + ((c ^ (lane & 7)) << 4)),
+                             "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                             : "memory");
               }
-              asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sb + lane * 128 + ((c ^ (lane & 7)) << 4)),
-                           "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
-                           : "memory");
             }
             fence_async_smem();
             __syncwarp();
