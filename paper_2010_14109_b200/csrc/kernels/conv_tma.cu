@@ -95,7 +95,9 @@ __device__ __forceinline__ void base_of(const Params& P, int pix, int& w, int& h
 // CG = 2: CTA pairs (cta_group::2).  A unit is MT tiles of 256 rows (CTA rank
 // r holds rows 128·r .. 128·r + 127 of each) × BN columns; each CTA stages its
 // own A rows and B columns [BN/2·r, BN/2·(r+1)), rank 0 issues 256 × BN MMAs.
-template <int MODE, int BN, int NCH, int MT, int CG = 1>
+// ACC: the TMA-store epilogue accumulates into the existing output (P.accumulate
+// with P.tstore) — a separate instantiation, so the plain epilogue's code is unchanged
+template <int MODE, int BN, int NCH, int MT, int CG = 1, bool ACC = false>
 __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_constant__ Params P) {
   static_assert(CG == 1 || (NCH == 0 && (MODE != WGRAD || BN / CG >= 64)), "CTA pairs: 64-channel pixels; wgrad: whole 64-column B atoms per CTA");
   constexpr int KB = kblock(MODE);              // K extent of a stage (elements, or wgrad pixels)
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");   // this buffer's last store read
             __syncwarp();
             const uint32_t sb = smem_u32(stg) + (uint32_t)(q * 2 + (sc & 1)) * 4096u;
-            if (!P.accumulate) {
+            if constexpr (!ACC) {
 #pragma unroll
               for (int c = 0; c < 8; ++c) {
                 uint32_t w[4];
@@ -660,12 +662,15 @@ int conv_mt() {
 template <int MODE, int BN, int NCH, int MT, int CG = 1>
 Status launch_mt(OpArgs& a, Params P, int* stat_slots = nullptr) {
   constexpr int smem = tma_smem(BN / CG, MT, kblock(MODE));
-  auto kern = conv_tma_kernel<MODE, BN, NCH, MT, CG>;
-  static bool attr = false;
-  if (!attr) {
+  auto kern = conv_tma_kernel<MODE, BN, NCH, MT, CG, false>;
+  if constexpr (MODE != WGRAD && NCH == 0)
+    if (P.accumulate && P.tstore) kern = conv_tma_kernel<MODE, BN, NCH, MT, CG, true>;
+  static bool attr[2] = {false, false};
+  const int ai = (P.accumulate && P.tstore) ? 1 : 0;
+  if (!attr[ai]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (CG == 2) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-    attr = true;
+    attr[ai] = true;
   }
   P.num_m = (P.M + BM * MT * CG - 1) / (BM * MT * CG);   // super-tiles of MT × (128·CG) rows
   const int units = P.num_m * P.num_n * (MODE == WGRAD ? P.splits : 1);
@@ -1467,7 +1472,8 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   P.out = y;
   P.nst = nst;
   P.accumulate = accumulate ? 1 : 0;
-  st = set_tstore(P, y, g.N * g.P * g.Q, nst ? nst : g.K, true);
+  // (the accumulating TMA epilogue is instantiated for 64-channel pixels only)
+  st = set_tstore(P, y, g.N * g.P * g.Q, nst ? nst : g.K, !(accumulate && nch));
   if (!st.good()) return st;
   P.M = g.N * g.P * g.Q;
   P.N = g.K;
