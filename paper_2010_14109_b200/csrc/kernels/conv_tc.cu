@@ -473,19 +473,7 @@ bool pad_path(const ConvGeom& g, int mode) {
   return g.K % 64 != 0 || (g.C % 64 != 0 && !nch);
 }
 
-bool conv_tc_ok(const ConvGeom& g, int mode) {
-  // 32-bit element indices of the activations (the 64-bit tensor offsets are formed per row)
-  if ((int64_t)g.N * g.H * g.W * ((g.C + 63) / 64 * 64) >= (1ll << 31) ||
-      (int64_t)g.N * g.P * g.Q * ((g.K + 63) / 64 * 64) >= (1ll << 31))
-    return false;
-  if (dil_of(g) > 1)   // atrous convs: the TMA kernels with dilated im2col offsets, 64-channel operands
-    return g.C % 64 == 0 && g.K % 64 == 0 && g.Cw == g.C && conv_tma_enabled() && (mode != DGRAD || g.st == 1);
-  if (pad_path(g, mode)) return true;
-  // zero-padded activation channels (Cw < C) only on the 16-byte-chunk paths
-  if (g.Cw != g.C && (g.C % 8 != 0 || g.Cw > g.C || mode == DGRAD)) return false;
-  if (mode == DGRAD) return g.K % 64 == 0 && g.C % 64 == 0 && (g.st == 1 || g.st == 2);
-  return g.K % 64 == 0;
-}
+bool conv_tc_ok(const ConvGeom& g, int mode);
 
 namespace {
 
@@ -563,6 +551,34 @@ Narrow narrow_of(const ConvGeom& g) {
   n.slice_bytes = align256((size_t)(n.slice * per));
   return n;
 }
+
+}  // namespace
+
+bool conv_tc_ok(const ConvGeom& g, int mode) {
+  // 32-bit element indices: the TMA kernels address rows (output pixels) with
+  // 32-bit indices and let the tensor maps form the byte offsets, so they need
+  // only M = images · P · Q < 2^31 per launch (narrow inputs run one
+  // re-laid-out slice of images per launch); the cp.async kernels also form
+  // 32-bit element offsets of whole activation tensors
+  const Narrow nw = narrow_of(g);
+  const int64_t nimg = nw.on ? nw.slice : g.N;
+  const bool tma = conv_tma_ok(nw.gk, mode) || pad_path(g, mode);
+  if (tma) {
+    if (nimg * g.P * g.Q >= (1ll << 31) || (int64_t)g.N * g.H * g.W >= (1ll << 31)) return false;
+  } else if ((int64_t)g.N * g.H * g.W * ((g.C + 63) / 64 * 64) >= (1ll << 31) ||
+             (int64_t)g.N * g.P * g.Q * ((g.K + 63) / 64 * 64) >= (1ll << 31)) {
+    return false;
+  }
+  if (dil_of(g) > 1)   // atrous convs: the TMA kernels with dilated im2col offsets, 64-channel operands
+    return g.C % 64 == 0 && g.K % 64 == 0 && g.Cw == g.C && conv_tma_enabled() && (mode != DGRAD || g.st == 1);
+  if (pad_path(g, mode)) return true;
+  // zero-padded activation channels (Cw < C) only on the 16-byte-chunk paths
+  if (g.Cw != g.C && (g.C % 8 != 0 || g.Cw > g.C || mode == DGRAD)) return false;
+  if (mode == DGRAD) return g.K % 64 == 0 && g.C % 64 == 0 && (g.st == 1 || g.st == 2);
+  return g.K % 64 == 0;
+}
+
+namespace {
 
 __global__ void pad_pixels(int64_t rows, int C, int C8, const __nv_bfloat16* __restrict__ x,
                            __nv_bfloat16* __restrict__ out) {

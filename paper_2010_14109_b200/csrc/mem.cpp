@@ -169,6 +169,30 @@ void MemPool::poll_deferred() {
   }
 }
 
+cudaEvent_t MemPool::take_event() {
+  if (!ev_pool.empty()) {
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
+}
+
+void MemPool::poll_released() {
+  for (size_t k = 0; k < released.size();) {
+    if (cudaEventQuery(released[k].ev) == cudaSuccess) {
+      ev_pool.push_back(released[k].ev);
+      released[k] = released.back();
+      released.pop_back();
+      continue;
+    }
+    ++k;
+  }
+  (void)cudaGetLastError();   // cudaErrorNotReady from the queries is not an error
+}
+
 void MemPool::destroy() {
   cudaSetDevice(device);
   cudaDeviceSynchronize();
@@ -182,6 +206,8 @@ void MemPool::destroy() {
   for (auto& r : released)
     if (r.ev) cudaEventDestroy(r.ev);
   released.clear();
+  for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+  ev_pool.clear();
   for (uint32_t c = 0; c < chunk.size(); ++c) {
     if (chunk[c]) drv->MemRelease(chunk[c]);
     if (chunk_ev[c]) cudaEventDestroy(chunk_ev[c]);
@@ -291,14 +317,17 @@ int oc_map(oc_mem* m, uint64_t handle, void* consumer_stream, oc_span* out, oc_e
     P.live_if += s.m_a - s.m_r;
     P.if_peak = std::max(P.if_peak, P.live_if);
   } else {
-    // wait for every earlier occupant of the block's bytes
+    // wait for every earlier occupant of the block's bytes whose release is
+    // still in flight (completed releases are dropped first, so the list holds
+    // only in-flight ranges and does not grow with the number of maps)
+    P.poll_released();
     const uint64_t a = s.offset, b = s.offset + s.m_a;
     for (size_t k = 0; k < P.released.size();) {
       auto& r = P.released[k];
       if (r.start < b && a < r.end) {
         cudaStreamWaitEvent(cs, r.ev, 0);
         if (a <= r.start && r.end <= b) {  // fully covered: this block's release will imply it
-          cudaEventDestroy(r.ev);
+          P.ev_pool.push_back(r.ev);
           P.released[k] = P.released.back();
           P.released.pop_back();
           continue;
@@ -343,7 +372,7 @@ int oc_unmap(oc_mem* m, uint64_t handle, void* release_stream, oc_err* err) {
     MemPool::Released r;
     r.start = s.offset;
     r.end = s.offset + s.m_a;
-    cudaEventCreateWithFlags(&r.ev, cudaEventDisableTiming);
+    r.ev = P.take_event();
     cudaEventRecord(r.ev, rs);
     P.released.push_back(r);
   }

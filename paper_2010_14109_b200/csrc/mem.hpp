@@ -44,7 +44,10 @@ struct MemPool {
   CUmemGenericAllocationHandle slab_h = 0;
   ArenaPlacer placer;
   struct Released { uint64_t start, end; cudaEvent_t ev; };
-  std::vector<Released> released;
+  std::vector<Released> released;   // arena: byte ranges whose release has not completed yet
+  std::vector<cudaEvent_t> ev_pool;  // recycled release events
+  cudaEvent_t take_event();
+  void poll_released();              // drop (and recycle) releases whose event has completed
   // spans
   std::unordered_map<uint64_t, Span> spans;
   std::set<uint64_t> freed;

@@ -241,3 +241,23 @@ def test_bn_relu_pool_tiled(shape):
     at = zp[nn, 2 * pp + idx // 3, 2 * qq + idx % 3, cc]
     assert np.all(np.abs(at - ref) <= ulp)
     assert np.mean(idx != arg) < 1e-3
+
+
+@pytest.mark.gpu
+def test_stem_at_the_r50_bench_batch_sampled():
+    """The 7x7/2 stem at the R50 bench batch (1523 images: the whole input
+    exceeds 2^31 elements once padded to 64 channels, so the per-slice
+    tensor-core path must take it): sampled images against the oracle."""
+    N, H, C, K = 1523, 224, 3, 64
+    g = (N, H, H, C, K, 7, 2, 3)
+    rng = np.random.default_rng(41)
+    xs = rng.standard_normal((N, H, H, C)).astype(np.float32)
+    x = T.bf(xs)
+    w = (rng.standard_normal((K, 7, 7, C)) / np.sqrt(49 * C)).astype(np.float32)
+    doc, (P, Q), total = T._graph("conv_fwd", g)
+    y = T._run(doc, total, {"x": T._bits(x), "w": w}, "y", np.uint16).reshape(N, P * Q * K)
+    wr = nm.round_bf16(w.astype(np.float64))
+    for n in (0, 761, N - 1):
+        ref = nm.round_bf16(nm.conv2d(x[n:n + 1].float().numpy().astype(np.float64), wr, 2, 3))
+        got = T._from_bits(y[n], (1, P, Q, K))
+        assert nm.rel_l2(got, ref) < TOL_BF16, n

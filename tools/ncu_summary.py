@@ -10,6 +10,8 @@ def main(path):
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     hdr, data = rows[hi], rows[hi + 1:]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    mi = hdr.index("Metric Name") if "Metric Name" in hdr else None
+    data = [r for r in data if mi is None or r[mi] == "gpu__time_duration.sum"]
     scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
     agg = collections.defaultdict(lambda: [0.0, 0])
     for r in data:
