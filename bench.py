@@ -434,6 +434,10 @@ def run_ours(args, rank, world):
     trigger = 1 if args.trigger == "paper" else 0
     mode = args.mode
     ram = host_ram_bytes()
+    if world > 1:   # one decision for every replica (they must plan identical schedules)
+        r = [ram]
+        dist.broadcast_object_list(r, src=0)
+        ram = r[0]
     notes = []
 
     # ---- physical budget, batch, scheduler budget

@@ -225,8 +225,8 @@ def test_bf16_deep_net_gradients_are_chaotic():
         r0 = nm.train_step(spec, p, x, y)
         rng = np.random.default_rng(0)
 
-        def noisy(xx, w, st, pad):
-            yy = orig(xx, w, st, pad)
+        def noisy(xx, w, st, pad, dil=1):
+            yy = orig(xx, w, st, pad, dil)
             return yy * (1 + 1e-6 * rng.standard_normal(yy.shape)) if w.shape == shape else yy
         nm.conv2d = noisy
         try:
