@@ -488,15 +488,9 @@ size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 //     conv becomes a stride-1 R'×S' conv over X' with pad' = ⌈pad/2⌉ and
 //     W'[k][i][j][(a,b,c)] = W[k][2(i−pad')+a+pad][2(j−pad')+b+pad][c] (zero
 //     outside the filter): the same products, 4× fewer gathered boxes
-//   folded (space-to-depth with R' = 4, the 7×7/2 stem): the four vertical
-//     taps of X' move into the channels as well, X''[n][p][v][(i,a,b,c)] =
-//     X'[n][p+i−pad'][v][(a,b,c)] (64-channel, 128-byte pixels, zero outside),
-//     and the conv becomes a 1×S' conv with horizontal padding only over the
-//     standard 64-channel TMA path (SWIZZLE_128B boxes instead of 32-byte
-//     ones: the 16-tap gather was TMA-request bound), W''[k][j][(i,a,b,c)] = W'[k][i][j][(a,b,c)]
 //   otherwise: 8-channel (16-byte) pixels, zero past C
 struct Narrow {
-  bool on, s2d, fold;
+  bool on, s2d;
   ConvGeom g0;        // the op's geometry
   ConvGeom gk;        // the geometry the kernels run
   int64_t slice;      // images per slice
@@ -510,16 +504,8 @@ bool s2d_enabled() {
   }
   return env == 1;
 }
-// opt-in (OC_CONV_FOLD=1): measured on B200 at ResNet-18 b=256 the folded
-// stem runs at the speed of the 16-channel one (both gathers are L2→SM bound
-// at ~5.5 TB/s; the fold only moves the 16× re-read from 32-byte to 128-byte
-// rows) while writing 4× the workspace bytes
-bool fold_enabled() {
-  const char* e = std::getenv("OC_CONV_FOLD");
-  return e && e[0] == '1' && conv_tma_enabled();
-}
 Narrow narrow_of(const ConvGeom& g) {
-  Narrow n{g.C % 8 != 0, false, false, g, g, g.N, 0};
+  Narrow n{g.C % 8 != 0, false, g, g, g.N, 0};
   if (!n.on) return n;
   if (s2d_enabled() && g.st == 2 && g.C <= 4 && g.H % 2 == 0 && g.W % 2 == 0 && g.R == g.S) {
     n.s2d = true;
@@ -533,19 +519,12 @@ Narrow narrow_of(const ConvGeom& g) {
     n.gk.R = n.gk.S = R2;
     n.gk.st = 1;
     n.gk.pad = c;
-    if (R2 == 4 && g.C == 3 && g.P == g.H / 2 && fold_enabled()) {
-      n.fold = true;
-      n.gk.H = g.P;
-      n.gk.C = n.gk.Cw = 64;
-      n.gk.R = 1;
-      n.gk.nopadh = 1;
-    }
   } else {
     n.gk.C = (g.C + 7) / 8 * 8;
     n.gk.Cw = g.C;
   }
   const int64_t per = (int64_t)n.gk.H * n.gk.W * n.gk.C * 2;
-  n.slice = g.pad_slice > 0 ? g.pad_slice : ((n.fold ? 64ll : 32ll) << 20) / per;
+  n.slice = g.pad_slice > 0 ? g.pad_slice : (32ll << 20) / per;
   if (n.slice < 1) n.slice = 1;
   if (n.slice > g.N) n.slice = g.N;
   n.slice_bytes = align256((size_t)(n.slice * per));
@@ -626,46 +605,12 @@ __global__ void s2d_pixels(int rows, int H2, int W2, int C, const __nv_bfloat16*
   }
 }
 
-// X [n][H][W][3] -> X'' [n][P][W/2][64]: thread (n, u, v) builds the X' pixel
-// (rows 2u, 2u+1, columns 2v, 2v+1: two contiguous 12-byte runs, 4-byte
-// aligned) once and stores it as chunk i of the four X'' pixels (n, u+c2−i, v);
-// the virtual rows u < 0 and u >= H/2 store the zero chunks of the padding
-// grid: x over v (128 threads per block), y over (n, virtual row) — no 64-bit
-// index division in the hot loop
-__global__ void fold_pixels(int rows, int P, int H2, int W2, int c2, const __nv_bfloat16* __restrict__ x,
-                            __nv_bfloat16* __restrict__ out) {
-  const int U = H2 + 4 - 1;   // virtual rows −c2 .. H2 + 3 − c2 − 1
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  for (int y = blockIdx.y; v < W2 && y < rows; y += gridDim.y) {
-    const int u = y % U - c2;
-    const int64_t n = y / U;
-    uint4 lo = make_uint4(0u, 0u, 0u, 0u), hi = lo;
-    if (u >= 0 && u < H2) {
-      const uint32_t* r0 = reinterpret_cast<const uint32_t*>(x + ((n * 2 * H2 + 2 * u) * 2 * W2 + 2 * v) * 3);
-      const uint32_t* r1 = r0 + (int64_t)2 * W2 * 3 / 2;
-      lo = make_uint4(__ldg(r0), __ldg(r0 + 1), __ldg(r0 + 2), __ldg(r1));
-      hi = make_uint4(__ldg(r1 + 1), __ldg(r1 + 2), 0u, 0u);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int p = u + c2 - i;
-      if (p < 0 || p >= P) continue;
-      uint4* o = reinterpret_cast<uint4*>(out + (((n * P + p) * W2 + v) * 4 + i) * 16);
-      o[0] = lo;
-      o[1] = hi;
-    }
-  }
-}
 
 Status pad_slice(OpArgs& a, const Narrow& nw, int64_t n0, int64_t nn, const __nv_bfloat16* x,
                  __nv_bfloat16* buf) {
   const ConvGeom& g0 = nw.g0;
   const __nv_bfloat16* xs = x + n0 * g0.H * g0.W * g0.C;
-  if (nw.fold) {
-    const int rows = (int)(nn * (g0.H / 2 + 3));
-    const dim3 grid((nw.gk.W + 127) / 128, (unsigned)std::min(rows, 65535));
-    fold_pixels<<<grid, 128, 0, a.stream>>>(rows, nw.gk.H, g0.H / 2, nw.gk.W, nw.gk.pad, xs, buf);
-  } else if (nw.s2d) {
+  if (nw.s2d) {
     const int rows = (int)(nn * nw.gk.H);
     const dim3 grid((nw.gk.W + 127) / 128, (unsigned)std::min(rows, 65535));
     s2d_pixels<<<grid, 128, 0, a.stream>>>(rows, nw.gk.H, nw.gk.W, g0.C, xs, buf);
@@ -678,13 +623,12 @@ Status pad_slice(OpArgs& a, const Narrow& nw, int64_t n0, int64_t nn, const __nv
 }
 
 // W'[k][(i,j,(a,b,c))] (bf16, row pitch kpad) from W[k][R][S][C] for the space-to-depth conv
-// folded (R2 = 4): W''[k][(j,(i,a,b,c))], tap (i, j) at column j·64 + i·16
 __global__ void weight_bf16_s2d(const float* __restrict__ w, __nv_bfloat16* __restrict__ out, int K, int R, int S,
-                                int C, int R2, int S2, int c2, int pad, int kpad, int fold) {
+                                int C, int R2, int S2, int c2, int pad, int kpad) {
   const int64_t n = (int64_t)K * kpad;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int k = (int)(e / kpad), jj = (int)(e % kpad);
-    const int tap = fold ? (jj % 64 / 16) * S2 + jj / 64 : jj / 16, ch = jj % 16;
+    const int tap = jj / 16, ch = jj % 16;
     float v = 0.f;
     if (tap < R2 * S2 && ch < 4 * C) {
       const int i = tap / S2, j = tap % S2, ab = ch / C, c = ch % C;
@@ -701,7 +645,7 @@ __global__ void weight_bf16_s2d(const float* __restrict__ w, __nv_bfloat16* __re
 // then the 8 group sums are added in order (fixed: bitwise reproducible)
 __global__ void __launch_bounds__(256) wgrad_reduce_s2d(int splits, int RSC2, int K, const float* __restrict__ part,
                                                         float* __restrict__ dw, int R, int S, int C, int S2, int c2,
-                                                        int pad, int fold) {
+                                                        int pad) {
   __shared__ float sm[8][33];
   const int n = K * R * S * C;
   const int l = threadIdx.x & 31, gz = threadIdx.x >> 5;
@@ -716,8 +660,7 @@ __global__ void __launch_bounds__(256) wgrad_reduce_s2d(int splits, int RSC2, in
     s = t % S;
     r = t / S;
     const int tr = r + 2 * c2 - pad, ts = s + 2 * c2 - pad;
-    row = (fold ? (ts >> 1) * 64 + (tr >> 1) * 16 : ((tr >> 1) * S2 + (ts >> 1)) * 16) + ((tr & 1) * 2 + (ts & 1)) * C +
-          c;
+    row = ((tr >> 1) * S2 + (ts >> 1)) * 16 + ((tr & 1) * 2 + (ts & 1)) * C + c;
 #pragma unroll 4
     for (int z = gz; z < splits; z += 8) acc += part[((int64_t)z * RSC2 + row) * K + k];
   }
@@ -907,7 +850,7 @@ Status conv_fprop_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* x, cons
   bool fused = stat != nullptr;
   if (nw.s2d)
     weight_bf16_s2d<<<grid_for((int64_t)g.K * kpad, 256, 4), 256, 0, a.stream>>>(
-        w, wb, g.K, g0.R, g0.S, g0.C, nw.fold ? 4 : g.R, g.S, g.pad, g0.pad, kpad, nw.fold ? 1 : 0);
+        w, wb, g.K, g0.R, g0.S, g0.C, g.R, g.S, g.pad, g0.pad, kpad);
   else
     weight_bf16<<<grid_for((int64_t)g.K * kpad, 256, 1), 256, 0, a.stream>>>(w, wb, g.K, g.R * g.S, g.C, 0, kpad,
                                                                               g.Cw);
@@ -1047,7 +990,7 @@ Status conv_wgrad_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* dy, con
   }
   if (nw.s2d)
     wgrad_reduce_s2d<<<(unsigned)((g0.K * g0.R * g0.S * g0.C + 31) / 32), 256, 0, a.stream>>>(
-        splits, RSC, g.K, part, dw, g0.R, g0.S, g0.C, g.S, g.pad, g0.pad, nw.fold ? 1 : 0);
+        splits, RSC, g.K, part, dw, g0.R, g0.S, g0.C, g.S, g.pad, g0.pad);
   else
     wgrad_reduce<<<dim3((g.K + 31) / 32, (RSC + 31) / 32), 1024, 0, a.stream>>>(splits, RSC, g.K, g.C, g.Cw, part,
                                                                                dw);

@@ -1118,196 +1118,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) stem_wgrad_kernel(const __grid_co
   if (threadIdx.x == 0) probe_end(P.probe, kp);
 }
 
-// 3×3 stride-1 pad-1 convs with 64 input and 64 output channels (ResNet's
-// 64-wide stage: fprop, and dgrad as the same conv over dY with the taps
-// flipped) on the same halo tiles: per 16 × 8 output block and horizontal tap
-// j one box of 18 rows × 8 pixels × 64 channels (SWIZZLE_128B, 18 KB) serves
-// the three vertical taps (1024-byte offsets = one SW128 pattern repeat);
-// the 9 weight taps (72 KB) stay resident.  Operand traffic per tile: 54 KB
-// instead of 9 × 16 KB im2col boxes.
-constexpr int H3R = TH + 2;
-constexpr int H3COPY = H3R * TW * 128;         // 18432 B
-constexpr int H3STAGE = 3 * H3COPY;            // 55296 B
-constexpr int H3NSTG = 2;
-constexpr int H3W = 9 * 8192;                  // resident weights: 9 taps × 64 rows × 64 K
-constexpr int H3SMEM = H3W + H3NSTG * H3STAGE + STG_BYTES + 1024 + 256;
-
-struct H3Params {
-  CUtensorMap tx;   // input [N][H][W][64], box {64, 8, 18, 1}, SWIZZLE_128B
-  CUtensorMap tw;   // weights [64 rows][576] bf16, box {64, 64}, SWIZZLE_128B (tap t at column 64·t)
-  CUtensorMap ty;   // output [N][P][Q][64], box {64, 8, 4, 1}, SWIZZLE_128B
-  int tq, tpq, units, P, Q, flip;
-  float* stat_part;
-};
-
-__global__ void __launch_bounds__(NTHREADS, 1) halo3_kernel(const __grid_constant__ H3Params P) {
-  constexpr uint32_t TCOLS = 128;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* wsm = smem;
-  uint8_t* asm_ = smem + H3W;
-  uint8_t* stg = asm_ + H3NSTG * H3STAGE;
-  uint64_t* full = (uint64_t*)(stg + STG_BYTES);
-  uint64_t* empty = full + H3NSTG;
-  uint64_t* tfull = empty + H3NSTG;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* bfull = tempty + 2;
-  uint32_t* tmem_slot = (uint32_t*)(bfull + 1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&P.tx);
-    tma_prefetch(&P.tw);
-    for (int s = 0; s < H3NSTG; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
-    mbar_init(bfull, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TCOLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-  auto tile_of = [&](int u, int& n, int& p0, int& q0) {
-    n = u / P.tpq;
-    const int r = u - n * P.tpq;
-    const int tp = r / P.tq;
-    p0 = tp * TH;
-    q0 = (r - tp * P.tq) * TW;
-  };
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_expect_tx(bfull, H3W);
-      for (int t = 0; t < 9; ++t) tma_load_2d(smem_u32(wsm) + t * 8192, &P.tw, bfull, t * 64, 0);
-      uint32_t it = 0;
-      for (int u = blockIdx.x; u < P.units; u += gridDim.x, ++it) {
-        int n, p0, q0;
-        tile_of(u, n, p0, q0);
-        const int sg = (int)(it % H3NSTG);
-        if (it >= (uint32_t)H3NSTG) mbar_wait(&empty[sg], ((it / H3NSTG) - 1) & 1);
-        const uint32_t a = smem_u32(asm_) + sg * H3STAGE;
-        mbar_expect_tx(&full[sg], H3STAGE);
-#pragma unroll
-        for (int j = 0; j < 3; ++j) tma_load_4d(a + j * H3COPY, &P.tx, &full[sg], 0, q0 + j - 1, p0 - 1, n);
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t ID = idesc(64, false, false);
-    if (lane == 0) mbar_wait(bfull, 0);
-    __syncwarp();
-    uint32_t it = 0;
-    for (int u = blockIdx.x; u < P.units; u += gridDim.x, ++it) {
-      const uint32_t buf = it & 1;
-      if (it >= 2) mbar_wait(&tempty[buf], ((it >> 1) - 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int sg = (int)(it % H3NSTG);
-      mbar_wait(&full[sg], (it / H3NSTG) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (lane == 0) {
-        const uint32_t a = smem_u32(asm_) + sg * H3STAGE, w = smem_u32(wsm);
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            const int t = P.flip ? (2 - i) * 3 + (2 - j) : i * 3 + j;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16(tmem + buf * 64, sdesc(a + j * H3COPY + i * 1024 + k * 32, 16, 1024),
-                       sdesc(w + t * 8192 + k * 32, 16, 1024), ID, (i | j | k) ? 1u : 0u);
-          }
-        mma_commit(&empty[sg]);
-        mma_commit(&tfull[buf]);
-      }
-      __syncwarp();
-    }
-  } else {
-    const int q = warp & 3;
-    float s0a = 0.f, s1a = 0.f, q0a = 0.f, q1a = 0.f;
-    uint32_t lt = 0;
-    for (int u = blockIdx.x; u < P.units; u += gridDim.x, ++lt) {
-      int n, p0, q0;
-      tile_of(u, n, p0, q0);
-      const uint32_t buf = lt & 1;
-      mbar_wait(&tfull[buf], (lt >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t v0[32], v1[32];
-      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + buf * 64;
-      TMEM_LD32(ta, v0);
-      TMEM_LD32(ta + 32, v1);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      __syncwarp();
-      const uint32_t sb = smem_u32(stg) + (uint32_t)(q * 2 + (lt & 1)) * 4096u;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint32_t w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t lo = c < 4 ? v0[c * 8 + 2 * e] : v1[(c - 4) * 8 + 2 * e];
-          const uint32_t hi = c < 4 ? v0[c * 8 + 2 * e + 1] : v1[(c - 4) * 8 + 2 * e + 1];
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
-          w[e] = *reinterpret_cast<uint32_t*>(&h2);
-        }
-        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sb + lane * 128 + ((c ^ (lane & 7)) << 4)),
-                     "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
-                     : "memory");
-      }
-      fence_async_smem();
-      __syncwarp();
-      if (P.stat_part) {
-        // staged row r is output pixel (p0 + 4q + r/8, q0 + r%8): rows past the map are masked
-        const int pr = p0 + q * 4, vr = min(4, P.P - pr), vc = min(8, P.Q - q0);
-        const uint8_t* sbp = stg + (q * 2 + (lt & 1)) * 4096 + (lane & 3) * 4;
-        uint32_t wv[32];
-#pragma unroll
-        for (int r = 0; r < 32; ++r)
-          wv[r] = *reinterpret_cast<const uint32_t*>(sbp + r * 128 + ((((uint32_t)lane >> 2) ^ (uint32_t)(r & 7)) << 4));
-        float s0 = 0.f, s1 = 0.f, q0s = 0.f, q1s = 0.f;
-#pragma unroll
-        for (int r = 0; r < 32; ++r) {
-          float2 f = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wv[r]));
-          if ((r >> 3) >= vr || (r & 7) >= vc) f = make_float2(0.f, 0.f);
-          s0 += f.x;
-          s1 += f.y;
-          q0s = fmaf(f.x, f.x, q0s);
-          q1s = fmaf(f.y, f.y, q1s);
-        }
-        s0a += s0;
-        s1a += s1;
-        q0a += q0s;
-        q1a += q1s;
-      }
-      if (lane == 0) {
-        if (p0 + q * 4 < P.P)
-          asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(&P.ty),
-                       "r"(sb), "r"(0), "r"(q0), "r"(p0 + q * 4), "r"(n)
-                       : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-    }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    __syncwarp();
-    if (P.stat_part) {
-      float* pp = P.stat_part + (int64_t)(blockIdx.x * 4 + q) * 2 * 64;
-      *reinterpret_cast<float2*>(pp + 2 * lane) = make_float2(s0a, s1a);
-      *reinterpret_cast<float2*>(pp + 64 + 2 * lane) = make_float2(q0a, q1a);
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 1) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
-  }
-}
-
 Status encode_tiled(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
                     const cuuint32_t* box, CUtensorMapSwizzle sw) {
   Driver* d;
@@ -1395,59 +1205,6 @@ Status conv_stem_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const
   return Status::ok();
 }
 
-// opt-in (OC_CONV_HALO=1): in isolation 6 % faster than the im2col pair kernel
-// at ResNet-18 l1 shapes, but inside the out-of-core step (copy engines
-// streaming through HBM/L2 alongside) its two-stage pipeline exposes more
-// load latency and the step's fprop kernels measured 0.302 vs 0.342 of peak
-bool halo3_enabled() {
-  const char* e = std::getenv("OC_CONV_HALO");
-  return e && e[0] == '1';
-}
-
-// 3×3 / stride 1 / pad 1, 64 → 64 channels on halo tiles (namespace stem):
-// in [N][Hm][Wm][64] -> out [N][Hm][Wm][64]; w [64][576] bf16 (tap t at column
-// 64·t); flip: dgrad (taps reversed)
-Status conv_halo3_tma(OpArgs& a, int N, int Hm, int Wm, const __nv_bfloat16* in, const __nv_bfloat16* w,
-                      __nv_bfloat16* out, bool flip, float* stat_part, int* stat_slots) {
-  using namespace stem;
-  H3Params P{};
-  {
-    const cuuint64_t dims[4] = {64, (cuuint64_t)Wm, (cuuint64_t)Hm, (cuuint64_t)N};
-    const cuuint64_t strides[3] = {128, (cuuint64_t)Wm * 128, (cuuint64_t)Hm * Wm * 128};
-    const cuuint32_t box[4] = {64, TW, H3R, 1};
-    OC_TRY(encode_tiled(&P.tx, in, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B));
-    const cuuint32_t obox[4] = {64, TW, 4, 1};
-    OC_TRY(encode_tiled(&P.ty, out, 4, dims, strides, obox, CU_TENSOR_MAP_SWIZZLE_128B));
-  }
-  OC_TRY(make_tiled(&P.tw, w, 576, 64, 64));
-  P.tq = (Wm + TW - 1) / TW;
-  P.tpq = ((Hm + TH - 1) / TH) * P.tq;
-  P.units = N * P.tpq;
-  P.P = Hm;
-  P.Q = Wm;
-  P.flip = flip ? 1 : 0;
-  P.stat_part = stat_part;
-  if (P.units == 0) return Status::ok();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(halo3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, H3SMEM);
-    attr = true;
-  }
-  const int ctas = grid_cap(std::min(P.units, sm_count()));
-  if (stat_part && stat_slots) *stat_slots = ctas * 4;
-  if (a.ktimer) a.ktimer->begin(a.stream);
-  halo3_kernel<<<ctas, NTHREADS, H3SMEM, a.stream>>>(P);
-  if (a.ktimer) a.ktimer->end(a.stream);
-  OC_LAUNCH_CHECK(a);
-  return Status::ok();
-}
-
-bool halo3_geom(const ConvGeom& g) {
-  return g.C == 64 && g.K == 64 && g.R == 3 && g.S == 3 && g.st == 1 && g.pad == 1 && !g.nopadh && dil_of(g) == 1 &&
-         g.P == g.H &&
-         g.Q == g.W && halo3_enabled() && tstore_enabled();
-}
-
 // stat_part (optional): fused BN statistics of y (TMA-store epilogue only); on
 // return *stat_slots = the slots written (0: not fused, the caller reduces y)
 Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* wb, int kpad,
@@ -1456,8 +1213,6 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   if (g.C == 16 && g.R == 4 && g.S == 4 && g.st == 1 && !g.nopadh && g.K == 64 && kpad == 256 && g.P % 16 == 0 &&
       g.Q % 8 == 0 && !accumulate && !nst && tstore_enabled() && stem_enabled() && dil_of(g) == 1)
     return conv_stem_tma(a, g, x, wb, kpad, y, stat_part, stat_slots);
-  if (halo3_geom(g) && kpad == 576 && !accumulate && !nst)
-    return conv_halo3_tma(a, g.N, g.H, g.W, x, wb, y, false, stat_part, stat_slots);
   const int nch = g.C % 64 == 0 ? 0 : g.C;     // 8 or 16: narrow pixels, one tap per box
   Params P{};
   const int padh = g.nopadh ? 0 : g.pad;
@@ -1506,8 +1261,6 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
 // phase's filter taps; a phase no tap reaches gets zeros (or keeps dx when accumulating)
 Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* wt,
                       __nv_bfloat16* dx, bool accumulate, int nst) {
-  if (halo3_geom(g) && !accumulate && !nst)   // dx = 3×3 conv of dY with the taps flipped (Wt[c][(r,s)][k])
-    return conv_halo3_tma(a, g.N, g.H, g.W, dy, wt, dx, true, nullptr, nullptr);
   // phases no filter tap reaches (e.g. 3 of the 4 phases of a 1×1 stride-2 conv):
   // without accumulation their dx is zero — cleared once for the whole tensor
   bool tapless = false;

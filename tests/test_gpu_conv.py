@@ -168,19 +168,6 @@ def test_conv_tiles_dgrad(g, tile, monkeypatch):
     test_conv_dgrad(g, True)
 
 
-# the folded stem (OC_CONV_FOLD=1): space-to-depth pixels with the four
-# vertical taps in the channels, a 1x4 conv over 64-channel pixels
-FOLD_SHAPES = [(2, 16, 14, 3, 64, 7, 2, 3), (3, 18, 12, 3, 128, 7, 2, 3, 2)]
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("g", FOLD_SHAPES)
-def test_conv_folded_stem(g, monkeypatch):
-    monkeypatch.setenv("OC_CONV_FOLD", "1")
-    test_conv_fwd(g)
-    test_conv_wgrad(g)
-
-
 # weight gradient on CTA pairs (K divisible by 128: 256 (r,s,c) rows × 128 / 256
 # columns per pair) against single CTAs (OC_WGRAD_CG=1)
 WGRAD_PAIR_SHAPES = [
@@ -269,27 +256,4 @@ def test_conv_stem_halo(g, stem, monkeypatch):
 @pytest.mark.gpu
 @pytest.mark.parametrize("g", STEM_SHAPES[:2])
 def test_conv_stem_halo_fused_bn_stats(g, monkeypatch):
-    test_conv_fused_bn_stats(g, "", monkeypatch)
-
-
-# 3x3 / stride 1 / pad 1, 64 -> 64 channels on halo tiles (fprop, and dgrad
-# as the tap-flipped conv over dY); ragged 16 x 8 blocks at the bottom and
-# right edges; OC_CONV_HALO=0 runs the im2col kernels on the same shapes
-HALO_SHAPES = [(2, 9, 7, 64, 64, 3, 1, 1), (2, 33, 20, 64, 64, 3, 1, 1), (1, 16, 24, 64, 64, 3, 1, 1)]
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("halo", ["1", "0"])
-@pytest.mark.parametrize("g", HALO_SHAPES)
-def test_conv_halo3(g, halo, monkeypatch):
-    monkeypatch.setenv("OC_CONV_HALO", halo)
-    test_conv_fwd(g)
-    test_conv_dgrad(g, False)
-    test_conv_dgrad(g, True)
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("g", HALO_SHAPES[:2])
-def test_conv_halo3_fused_bn_stats(g, monkeypatch):
-    monkeypatch.setenv("OC_CONV_HALO", "1")
     test_conv_fused_bn_stats(g, "", monkeypatch)
