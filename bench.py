@@ -185,6 +185,51 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+class PcieSampler:
+    """Counter-backed host-link throughput during the timed region: NVML's PCIe
+    throughput counters (nvmlDeviceGetPcieThroughput, KB/s over 20 ms windows;
+    TX = device -> host, RX = host -> device), sampled every 25 ms on a thread —
+    an independent check of the CUDA-event-derived host-link GB/s."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.tx, self.rx = [], []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+        self.info = {}
+
+    def run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+            self.info = {"link_gen": pynvml.nvmlDeviceGetCurrPcieLinkGeneration(h),
+                         "link_width": pynvml.nvmlDeviceGetCurrPcieLinkWidth(h)}
+            while not self.stop.is_set():
+                self.tx.append(pynvml.nvmlDeviceGetPcieThroughput(h, pynvml.NVML_PCIE_UTIL_TX_BYTES))
+                self.rx.append(pynvml.nvmlDeviceGetPcieThroughput(h, pynvml.NVML_PCIE_UTIL_RX_BYTES))
+                self.stop.wait(0.025)
+        except Exception as e:  # noqa: BLE001
+            self.info["error"] = str(e)[:120]
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=5)
+
+    def summary(self):
+        if not self.tx:
+            return dict(self.info, samples=0)
+        kb = 1e3 / 1e9   # KB/s -> GB/s
+        return dict(self.info, samples=len(self.tx), d2h_gbs_mean=float(np.mean(self.tx)) * kb,
+                    h2d_gbs_mean=float(np.mean(self.rx)) * kb, d2h_gbs_p90=float(np.percentile(self.tx, 90)) * kb,
+                    h2d_gbs_p90=float(np.percentile(self.rx, 90)) * kb,
+                    source="NVML nvmlDeviceGetPcieThroughput (20 ms windows) during the timed steps")
+
+
 # ----------------------------------------------------------- memory budgets
 def in_core_device_bytes(spec):
     """Device bytes of the IN-CORE step: F_peak with parameters, gradients and
@@ -554,7 +599,7 @@ def run_ours(args, rank, world):
             raise RuntimeError(f"ranks planned different schedules: {hs}")
     attach(st, rank, world)
     st.set_timeline(False)
-    with Clocks(dev) as clk:
+    with Clocks(dev) as clk, PcieSampler(dev) as pcie:
         dev_ms, wall_ms, mets = time_steps(st, args.steps, args.warmup, world)
     loss = float(st.read(info["loss_g" if "G" in spec else "loss"])[0])
     ss = st.stats
@@ -695,7 +740,8 @@ def run_ours(args, rank, world):
         "host_link": {"h2d_gbs_step": h2d / (step_ms / 1e3) / 1e9, "d2h_gbs_step": d2h / (step_ms / 1e3) / 1e9,
                       "h2d_gbs_busy": (h2d / (h2d_busy / 1e3) / 1e9) if h2d_busy else None,
                       "d2h_gbs_busy": (d2h / (d2h_busy / 1e3) / 1e9) if d2h_busy else None,
-                      "pcie5_x16_gbs_per_dir": PCIE5_X16_GBS, "measured_pinned_gbs": link},
+                      "pcie5_x16_gbs_per_dir": PCIE5_X16_GBS, "measured_pinned_gbs": link,
+                      "nvml_pcie_counters": pcie.summary()},
         "overlap_pct": 100 * overlap,
         "makespan_model": {"predicted_ms": sim["makespan_ms"], "predicted_boundary_ms": sim0["makespan_ms"],
                            "compute_ms": sim["compute_ms"], "stall_ms": sim["stall_ms"],
