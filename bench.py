@@ -804,10 +804,23 @@ def oracle_sample(args):
     return (lambda: nm.train_step(spec, p, x, y)), spec["batch"], scale, note + " (numpy float64 oracle)"
 
 
+def oracle_threads():
+    """Threads the numpy oracle actually uses (the BLAS pool; torchrun sets
+    OMP_NUM_THREADS=1 for its workers)."""
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i["num_threads"] for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n:
+            return int(max(n))
+    except Exception:  # noqa: BLE001
+        pass
+    return len(os.sched_getaffinity(0))
+
+
 def cpu_baseline(args, min_s=10.0):
     """The oracle on a bounded sample of the same workload, on all host cores
     (repeated steps until ~10 s of CPU work)."""
-    cores = len(os.sched_getaffinity(0))
+    cores = oracle_threads()
     fn, batch, scale, note = oracle_sample(args)
     t0 = time.perf_counter()
     steps = 0
@@ -821,7 +834,7 @@ def cpu_baseline(args, min_s=10.0):
 
 def run_reference(args):
     """--impl reference: the CPU oracle as it stands, bounded sample per step."""
-    cores = len(os.sched_getaffinity(0))
+    cores = oracle_threads()
     fn, batch, scale, note = oracle_sample(args)
     for _ in range(args.warmup):
         fn()
