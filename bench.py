@@ -358,6 +358,8 @@ def new_step(spec, info, doc, budget, mode, chunk, phys, window, timeline=False,
     p = nets.make_params(spec)
     st.write(info["x"], torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy()
              if spec["mode"] == "bf16" else x)
+    if spec["loss"]["type"] == "l1" and spec["mode"] == "bf16":   # the L1 target image, act dtype
+        y = torch.from_numpy(y).to(torch.bfloat16).view(torch.int16).numpy()
     st.write(info["labels"], y)
     for k, v in p.items():
         st.write(info["params"][k], v)
