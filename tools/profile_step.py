@@ -13,7 +13,7 @@ import bench  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="r18")
+    ap.add_argument("--config", default="r18", help="r18 | r50 | any bench.py --config")
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--budget-frac", type=float, default=0.25)
     ap.add_argument("--mode", default="va")
@@ -22,7 +22,12 @@ def main():
     from paper_2010_14109_b200 import binding as B
     from paper_2010_14109_b200 import graphs
     from synth import nets
-    spec = nets.resnet(18 if a.config == "r18" else 50, batch=a.batch)
+    if a.config in ("r18", "r50"):
+        spec = nets.resnet(18 if a.config == "r18" else 50, batch=a.batch)
+    else:
+        class _A:
+            config, batch = a.config, a.batch
+        spec = bench.spec_for(_A())
     doc, info = graphs.build(spec, params="persistent")
     G = B.Graph(doc)
     F = G.in_core_peak()
