@@ -466,7 +466,11 @@ bool conv_tma_enabled();
 // workspace copies (operands) and zero-padded weights, only the real
 // channels stored (TMA kernels)
 bool pad_path(const ConvGeom& g, int mode) {
-  if (!conv_tma_enabled() || g.Cw != g.C || g.C % 8 || g.K % 8) return false;
+  // output channels the 8-wide rows do not divide (the 3-channel image a
+  // generator emits, a 21-class segmentation head) run through a padded
+  // output buffer (fprop) or a padded dY copy (dgrad / wgrad)
+  if (!conv_tma_enabled() || g.Cw != g.C || g.C % 8) return false;
+  if (g.K % 8) return dil_of(g) == 1;
   // 8/16-channel pixels are gathered natively by the fprop kernel, 16-channel ones by wgrad
   const bool nch = (mode == FPROP && (g.C == 8 || g.C == 16)) || (mode == WGRAD && g.C == 16);
   if (mode == DGRAD) return g.C % 64 != 0 || g.K % 64 != 0;
@@ -696,7 +700,8 @@ PadPlan pad_plan(const ConvGeom& g, int mode) {
   p.gk.C = p.gk.Cw = Cp;
   p.gk.K = Kp;
   p.pad_x = Cp != g.C && mode != DGRAD;
-  p.pad_y = Kp != g.K && mode != FPROP;
+  // dY copy for dgrad / wgrad; for fprop with K % 8 != 0 the same buffer holds the padded output
+  p.pad_y = Kp != g.K && (mode != FPROP || g.K % 8 != 0);
   const int64_t px = p.pad_x ? (int64_t)g.H * g.W * Cp * 2 : 0, py = p.pad_y ? (int64_t)g.P * g.Q * Kp * 2 : 0;
   if (px + py > 0) p.slice = std::max<int64_t>(1, std::min<int64_t>(g.N, (64ll << 20) / (px + py)));
   p.xbytes = align256((size_t)(p.slice * px));
@@ -713,7 +718,7 @@ int tma_wgrad_splits(const ConvGeom& gk, int64_t slice) {
 size_t pad_ws(const ConvGeom& g, int mode) {
   const PadPlan p = pad_plan(g, mode);
   const ConvGeom& k = p.gk;
-  if (mode == FPROP) return align256((size_t)k.K * kpad_of(k) * 2) + p.xbytes;
+  if (mode == FPROP) return align256((size_t)k.K * kpad_of(k) * 2) + p.xbytes + p.ybytes;
   if (mode == DGRAD) return align256((size_t)k.C * k.R * k.S * k.K * 2) + p.ybytes;
   return align256((size_t)tma_wgrad_splits(k, p.slice) * k.R * k.S * k.C * k.K * 4) + p.xbytes + p.ybytes;
 }
@@ -727,6 +732,20 @@ __global__ void weight_bf16_tpad(const float* __restrict__ w, __nv_bfloat16* __r
     const int64_t t = i / Kp;
     const int rs = (int)(t % RS), c = (int)(t / RS);
     out[i] = (c < C && k < K) ? __float2bfloat16_rn(w[((int64_t)k * RS + rs) * C + c]) : __float2bfloat16_rn(0.f);
+  }
+}
+
+// y[r][k] = yp[r][k] for k < K (or rnd(y + yp) when accumulating): the real
+// channels of a padded-output conv
+__global__ void unpad_pixels(int64_t rows, int K, int Kp, const __nv_bfloat16* __restrict__ yp,
+                             __nv_bfloat16* __restrict__ y, int acc) {
+  const int64_t n = rows * K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / K;
+    const int k = (int)(i - r * K);
+    float v = __bfloat162float(yp[r * Kp + k]);
+    if (acc) v += __bfloat162float(y[i]);
+    y[i] = __float2bfloat16_rn(v);
   }
 }
 
@@ -754,6 +773,15 @@ Status conv_fprop_pad(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
     if (pp.pad_x) {
       OC_TRY(pad_copy(a, nn * g.H * g.W, g.C, k.C, act, xbuf));
       act = xbuf;
+    }
+    if (pp.pad_y) {   // K % 8 != 0: all Kp channels into the workspace, then the real ones out
+      __nv_bfloat16* ybuf = (__nv_bfloat16*)((char*)xbuf + pp.xbytes);
+      OC_TRY(conv_fprop_tma(a, gs, act, wb, kpad, ybuf, false, 0));
+      const int64_t rows = nn * g.P * g.Q;
+      unpad_pixels<<<grid_for(rows * g.K, 256, 4), 256, 0, a.stream>>>(rows, g.K, k.K, ybuf,
+                                                                       y + n0 * g.P * g.Q * g.K, accumulate ? 1 : 0);
+      OC_LAUNCH_CHECK(a);
+      continue;
     }
     OC_TRY(conv_fprop_tma(a, gs, act, wb, kpad, y + n0 * g.P * g.Q * g.K, accumulate, g.K));
   }

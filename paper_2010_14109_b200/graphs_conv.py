@@ -238,6 +238,14 @@ def build_convnet(spec, params="pinned", inputs="host", dp_bucket_bytes=0):
         b.fn("loss", "softmax_ce", {"logits": logits, "labels": y, "loss": loss, "dlogits": g[spec["loss"]["in"]]},
              {"M": Nb, "N": spec["classes"]}, [logits, y], [loss, g[spec["loss"]["in"]]])
 
+    # tensors that carry no gradient: the input image and whatever parameter-free
+    # single-input layers derive from it alone (Pix2PixHD's reflection-padded
+    # input) — the conv reading one needs its weight gradient but no dgrad
+    nograd = {"x"}
+    for lay in layers:
+        if lay["type"] in ("reflect_pad", "upsample_bilinear", "tanh", "avgpool2", "in") and lay["in"] in nograd:
+            nograd.add(lay["out"])
+
     for lay in reversed(layers):
         nm, ty = lay["name"], lay["type"]
         if nm in skip:
@@ -312,7 +320,7 @@ def build_convnet(spec, params="pinned", inputs="host", dp_bucket_bytes=0):
                 at = {k: v for k, v in at.items() if k != "accumulate"}
                 b.fn(f"bwd.{nm}.wgrad{sfx}", "conv_wgrad", {"dy": dy, "x": t[src], "dw": G[wname]}, at,
                      [dy, t[src]], [G[wname]])
-                if src != "x":
+                if src not in nograd:
                     acc = src in g
                     if acc:
                         dx = g[src]
@@ -329,6 +337,9 @@ def build_convnet(spec, params="pinned", inputs="host", dp_bucket_bytes=0):
             src = lay["in"]
             b.fn(f"bwd.{nm}.wgrad", "convT_wgrad", {"dy": gv, "x": t[src], "dw": G[nm + ".W"]}, lay["_attrs"],
                  [gv, t[src]], [G[nm + ".W"]])
+            if src in nograd:
+                _update(b, spec, nm, P, Mo, G, [nm + ".W"])
+                continue
             acc = src in g
             if acc:
                 dx = g[src]
@@ -344,6 +355,9 @@ def build_convnet(spec, params="pinned", inputs="host", dp_bucket_bytes=0):
             src = lay["in"]
             b.fn(f"bwd.{nm}.wgrad", "convT_wgrad", {"dy": gv, "x": t[src], "dw": G[nm + ".W"]}, lay["_attrs"],
                  [gv, t[src]], [G[nm + ".W"]])
+            if src in nograd:
+                _update(b, spec, nm, P, Mo, G, [nm + ".W"])
+                continue
             acc = src in g
             if acc:
                 dx = g[src]
@@ -357,7 +371,7 @@ def build_convnet(spec, params="pinned", inputs="host", dp_bucket_bytes=0):
             _update(b, spec, nm, P, Mo, G, [nm + ".W"])
         elif ty in ("in", "reflect_pad", "upsample_bilinear", "tanh"):
             src = lay["in"]
-            if src == "x":
+            if src in nograd:
                 continue
             acc = src in g
             if acc:

@@ -34,6 +34,11 @@ PAD = [
     (2, 10, 9, 96, 96, 3, 2, 1),      # BigGAN-like 96 channels, stride 2 (dgrad phases)
     (2, 6, 6, 64, 24, 1, 1, 0),       # attention-like 64 -> 24
     (2, 8, 8, 24, 64, 3, 1, 1),       # 24 -> 64
+    # output channels not a multiple of 8: fprop stores through a padded
+    # workspace output, dgrad / wgrad read a padded dY copy
+    (2, 9, 8, 64, 3, 7, 1, 3),        # Pix2PixHD image head 64 -> 3, 7x7
+    (2, 6, 7, 64, 21, 1, 1, 0),       # DeepLabv3+ class head -> 21
+    (2, 10, 9, 32, 3, 3, 2, 1),       # K = 3, stride 2 (dgrad phases)
 ]
 
 
