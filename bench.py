@@ -401,6 +401,22 @@ def conv_flops(doc):
     return fl
 
 
+def attn_bytes(doc):
+    """Algorithmic HBM bytes per attention function (bf16 tensor-core path,
+    DESIGN.md §7): forward S written and read (fp32), P written and read
+    (bf16) = 12·L² per sample; backward P read twice, dS written once and read
+    twice = 16·L² per sample (the L-wide q, k, v, o tensors are < 2 % and left out)."""
+    d = json.loads(doc)
+    out = {}
+    for f in d["functions"]:
+        op = f.get("op") or {}
+        a = op.get("attrs", {})
+        if op.get("kind") in ("attn_fwd", "attn_bwd"):
+            nb, L = a.get("nb", a["N"]), a["L"]
+            out[f["id"]] = (12 if op["kind"] == "attn_fwd" else 16) * nb * L * L
+    return out
+
+
 def time_steps(st, steps, warmup, world):
     import torch
     import torch.distributed as dist
@@ -651,11 +667,14 @@ def run_ours(args, rank, world):
         max(ph["h2d_bwd"] / (link["h2d"] * 1e9), ph["d2h_bwd"] / (link["d2h"] * 1e9))
     # dominant contraction kernel from the per-function CUDA events of the instrumented pass
     fl = conv_flops(doc)
+    abytes = attn_bytes(doc)
     per_kind = {}
     for ev in tl:
         if ev["stream"] != "compute" or ev["id"] not in fl:
             continue
         kind, f = fl[ev["id"]]
+        if kind.startswith("attn") and spec["mode"] == "bf16":
+            f = abytes[ev["id"]]   # HBM-bound on the tensor-core path: bytes, not FLOPs
         a = per_kind.setdefault(kind, [0.0, 0.0, 0, 0.0, []])
         a[0] += f
         if ev.get("k_n"):
@@ -687,7 +706,15 @@ def run_ours(args, rank, world):
         kind, (flops, secs, cnt, ev_secs, mhz) = max(per_kind.items(), key=lambda kv: kv[1][1])
         ach = flops / secs / 1e12
         impl = os.environ.get("OC_CONV_IMPL", "tc")
-        if impl == "simt" or kind.startswith("attn"):   # CUDA-core FFMA kernels
+        if kind.startswith("attn") and spec["mode"] == "bf16":   # tensor-core products, HBM-bound
+            gbs = flops / secs / 1e9
+            roof = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": gbs / peaks["hbm_gbs"], "traffic": None, "kernel": kind, "launches": cnt,
+                    "algorithmic_bytes": "12·L² per sample forward, 16·L² backward (bench.attn_bytes)",
+                    "timed": "CUDA events around each attention function in the instrumented pass (all its "
+                             "kernels: products, softmax, split reductions)",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        elif impl == "simt" or kind.startswith("attn"):   # CUDA-core FFMA kernels
             roof = {"bound": "alu", "achieved": ach, "peak": FP32_SIMT_TFLOPS, "unit": "TFLOP/s",
                     "frac": ach / FP32_SIMT_TFLOPS, "traffic": None, "kernel": kind, "launches": cnt,
                     "timed": "CUDA events around each contraction kernel launch in the instrumented pass",

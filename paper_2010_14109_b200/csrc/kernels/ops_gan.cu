@@ -9,12 +9,16 @@
 // P = rnd(softmax_rows(S)) stored as an activation (the L×L map the config
 // is meant to swap), o = rnd(P v); backward dv = rnd(Pᵀ do), dP = do vᵀ
 // (fp32), dS = P ⊙ (dP − rowsum), rowsum_i = do_i·o_i, dq = rnd(dS k),
-// dk = rnd(dSᵀ q).  The products are the batched SIMT GEMM (gemm_simt.cuh);
-// samples go through the fp32 L×L workspace a few at a time.
+// dk = rnd(dSᵀ q).  bf16: the products run on the tensor cores (gemm_tc.cuh;
+// dS as an exact bf16 hi + lo pair); fp32 parity mode: the batched SIMT GEMM
+// (gemm_simt.cuh, exact FFMA).  Samples go through the fp32 L×L workspace a
+// few at a time.
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "gemm_simt.cuh"
+#include "gemm_tc.cuh"
 
 namespace oc {
 
@@ -262,6 +266,57 @@ __global__ void softmax_rows_k(int64_t rows, int L, const float* __restrict__ S,
   const float inv = 1.f / sum;
   for (int j = lane; j < L; j += 32) st_f(P + r * L + j, expf(s[j] - mx) * inv);
 }
+// the same, one pass: a row of L = 128·NCH values held in registers (float4
+// per lane per chunk), so S is read once
+template <typename T, int NCH>
+__global__ void softmax_rows_reg_k(int64_t rows, const float* __restrict__ S, T* __restrict__ P) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int lane = threadIdx.x & 31;
+  constexpr int L = 128 * NCH;
+  const float4* s = reinterpret_cast<const float4*>(S + r * L);
+  float4 v[NCH];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    v[c] = __ldcs(s + c * 32 + lane);
+    mx = fmaxf(mx, fmaxf(fmaxf(v[c].x, v[c].y), fmaxf(v[c].z, v[c].w)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    v[c] = make_float4(expf(v[c].x - mx), expf(v[c].y - mx), expf(v[c].z - mx), expf(v[c].w - mx));
+    sum += (v[c].x + v[c].y) + (v[c].z + v[c].w);
+  }
+  sum = warp_sum(sum);
+  const float inv = 1.f / sum;
+  T* p = P + r * L;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int j = (c * 32 + lane) * 4;
+    st_f(p + j, v[c].x * inv);
+    st_f(p + j + 1, v[c].y * inv);
+    st_f(p + j + 2, v[c].z * inv);
+    st_f(p + j + 3, v[c].w * inv);
+  }
+}
+template <typename T>
+void softmax_rows(OpArgs& a, int64_t rows, int L, const float* S, T* P) {
+  // 4-warp blocks: the 4096-wide rows hold ~170 registers per thread, so
+  // small blocks let three of them share an SM
+  const int g = (int)((rows + 3) / 4);
+  switch (L) {
+    case 4096: softmax_rows_reg_k<T, 32><<<g, 128, 0, a.stream>>>(rows, S, P); return;
+    case 2048: softmax_rows_reg_k<T, 16><<<g, 128, 0, a.stream>>>(rows, S, P); return;
+    case 1024: softmax_rows_reg_k<T, 8><<<g, 128, 0, a.stream>>>(rows, S, P); return;
+    case 512: softmax_rows_reg_k<T, 4><<<g, 128, 0, a.stream>>>(rows, S, P); return;
+    case 256: softmax_rows_reg_k<T, 2><<<g, 128, 0, a.stream>>>(rows, S, P); return;
+    case 128: softmax_rows_reg_k<T, 1><<<g, 128, 0, a.stream>>>(rows, S, P); return;
+    default: softmax_rows_k<T><<<(int)((rows + 7) / 8), 256, 0, a.stream>>>(rows, L, S, P);
+  }
+}
 // rs[row] = do[row] · o[row] (= rowsum(dP ⊙ P))
 template <typename T>
 __global__ void rowdot_k(int64_t rows, int d, const T* __restrict__ a, const T* __restrict__ b, float* __restrict__ out) {
@@ -284,6 +339,17 @@ int64_t attn_chunk(int64_t N, int64_t L) {
   const int64_t per = L * L * 4 + L * 4;
   int64_t c = (256ll << 20) / per;
   return std::max<int64_t>(1, std::min<int64_t>(N, c));
+}
+// tensor-core split-K partials of the products that reduce over L
+size_t attn_split_ws(int64_t N, int64_t L, int dq, int dv) {
+  const int64_t cn = attn_chunk(N, L);
+  tcg::Gemm pv{(int)L, dv, (int)L, (int)cn, nullptr, L, 1, L * L, false, nullptr, dv, 1, L * dv, nullptr, dv, L * dv,
+               false};
+  tcg::Gemm dvg{(int)L, dv, (int)L, (int)N, nullptr, 1, L, L * L, false, nullptr, dv, 1, L * dv, nullptr, dv, L * dv,
+                false};
+  tcg::Gemm dqg{(int)L, dq, (int)L, (int)cn, nullptr, L, 1, L * L, true, nullptr, dq, 1, L * dq, nullptr, dq, L * dq,
+                false};
+  return std::max({tcg::ws_bytes(pv), tcg::ws_bytes(dvg), tcg::ws_bytes(dqg)});
 }
 
 // ---------------------------------------------------------------- ops
@@ -424,10 +490,24 @@ Status attn_fwd_t(OpArgs& a) {
   const T* v = (const T*)a.p(AT_V) + s0 * L * dv;
   T *P = (T*)a.p(AT_P), *O = (T*)a.p(AT_O) + s0 * L * dv;
   const int64_t cn = attn_chunk(N, L);
-  if (a.ws_bytes < (size_t)(cn * L * L * 4)) return Status::make(OC_E_INVARIANT, "attn: workspace");
+  constexpr bool TC = std::is_same<T, __nv_bfloat16>::value;
+  const size_t sws = TC ? attn_split_ws(N, L, dq, dv) : 0;
+  if (a.ws_bytes < (size_t)(cn * L * L * 4 + cn * L * 4) + sws) return Status::make(OC_E_INVARIANT, "attn: workspace");
   float* S = (float*)a.ws;
+  void* part = (char*)a.ws + cn * L * L * 4 + cn * L * 4;
   for (int64_t n0 = 0; n0 < N; n0 += cn) {
     const int b = (int)std::min<int64_t>(cn, N - n0);
+    if (TC) {
+      // S = q kᵀ: A = q (K-major), B(k, n) = k[n][k] (K-major); fp32 out
+      OC_TRY(tcg::gemm(a, {(int)L, (int)L, dq, b, q + n0 * L * dq, dq, 1, L * dq, false, k + n0 * L * dq, 1, dq,
+                           L * dq, S, L, L * L, true}));
+      softmax_rows<T>(a, b * L, (int)L, S, P + n0 * L * L);
+      OC_LAUNCH_CHECK(a);
+      // o = P v: B(k, n) = v[k][n] (MN-major)
+      OC_TRY(tcg::gemm(a, {(int)L, dv, (int)L, b, P + n0 * L * L, L, 1, L * L, false, v + n0 * L * dv, dv, 1,
+                           L * dv, O + n0 * L * dv, dv, L * dv, false}, part, sws));
+      continue;
+    }
     // S = q kᵀ (fp32)
     OC_TRY((gemm<T, T, float, false>(a, (int)L, (int)L, dq, q + n0 * L * dq, dq, 1, nullptr, k + n0 * L * dq, 1, dq,
                                      S, L, 1, nullptr, false, false, b, L * dq, L * dq, L * L)));
@@ -449,14 +529,42 @@ Status attn_bwd_t(OpArgs& a) {
   const T *P = (const T*)a.p(AB_P), *O = (const T*)a.p(AB_O) + ov, *dO = (const T*)a.p(AB_DO) + ov;
   T *dQ = (T*)a.p(AB_DQ) + oq, *dK = (T*)a.p(AB_DK) + oq, *dV = (T*)a.p(AB_DV) + ov;
   const int64_t cn = attn_chunk(N, L);
-  if (a.ws_bytes < (size_t)(cn * L * L * 4 + cn * L * 4)) return Status::make(OC_E_INVARIANT, "attn: workspace");
+  constexpr bool TC = std::is_same<T, __nv_bfloat16>::value;
+  const size_t sws = TC ? attn_split_ws(N, L, dq, dv) : 0;
+  if (a.ws_bytes < (size_t)(cn * L * L * 4 + cn * L * 4) + sws) return Status::make(OC_E_INVARIANT, "attn: workspace");
   float* dS = (float*)a.ws;
   float* rs = dS + cn * L * L;
+  void* part = (char*)a.ws + cn * L * L * 4 + cn * L * 4;
   // dv = Pᵀ do (all samples in one batched launch)
-  OC_TRY((gemm<T, T, T, false>(a, (int)L, dv, (int)L, P, 1, L, nullptr, dO, dv, 1, dV, dv, 1, nullptr, false, false,
-                               (int)N, L * L, L * dv, L * dv)));
+  if (TC)   // A(m = j, k = i) = P[i][j] (MN-major), B(k = i, n) = do[i][n] (MN-major)
+    OC_TRY(tcg::gemm(a, {(int)L, dv, (int)L, (int)N, P, 1, L, L * L, false, dO, dv, 1, L * dv, dV, dv, L * dv, false},
+                     part, sws));
+  else
+    OC_TRY((gemm<T, T, T, false>(a, (int)L, dv, (int)L, P, 1, L, nullptr, dO, dv, 1, dV, dv, 1, nullptr, false, false,
+                                 (int)N, L * L, L * dv, L * dv)));
   for (int64_t n0 = 0; n0 < N; n0 += cn) {
     const int b = (int)std::min<int64_t>(cn, N - n0);
+    if (TC) {
+      rowdot_k<T><<<(int)((b * L + 7) / 8), 256, 0, a.stream>>>(b * L, dv, dO + n0 * L * dv, O + n0 * L * dv, rs);
+      OC_LAUNCH_CHECK(a);
+      // dS = P ⊙ (do vᵀ − rs) straight from the product's epilogue:
+      // A = do (K-major), B(k, n) = v[n][k] (K-major)
+      tcg::Gemm g{(int)L, (int)L, dv, b, dO + n0 * L * dv, dv, 1, L * dv, false, v + n0 * L * dv, 1, dv, L * dv,
+                  dS, L, L * L, true};
+      g.ep_p = (const __nv_bfloat16*)(P + n0 * L * L);
+      g.ldp = L;
+      g.p_b = L * L;
+      g.ep_rs = rs;
+      g.rs_b = L;
+      OC_TRY(tcg::gemm(a, g));
+      // dq = dS k: A = dS (K-major fp32), B(k, n) = k[k][n] (MN-major)
+      OC_TRY(tcg::gemm(a, {(int)L, dq, (int)L, b, dS, L, 1, L * L, true, k + n0 * L * dq, dq, 1, L * dq,
+                           dQ + n0 * L * dq, dq, L * dq, false}, part, sws));
+      // dk = dSᵀ q: A(m = j, k = i) = dS[i][j] (MN-major fp32), B(k = i, n) = q[i][n]
+      OC_TRY(tcg::gemm(a, {(int)L, dq, (int)L, b, dS, 1, L, L * L, true, q + n0 * L * dq, dq, 1, L * dq,
+                           dK + n0 * L * dq, dq, L * dq, false}, part, sws));
+      continue;
+    }
     // dP = do vᵀ (fp32), rowsum, dS = P ⊙ (dP − rs)
     OC_TRY((gemm<T, T, float, false>(a, (int)L, (int)L, dv, dO + n0 * L * dv, dv, 1, nullptr, v + n0 * L * dv, 1,
                                      dv, dS, L, 1, nullptr, false, false, b, L * dv, L * dv, L * L)));
@@ -475,7 +583,9 @@ Status attn_bwd_t(OpArgs& a) {
 size_t attn_ws(const JVal& at) {
   const int64_t N = at.geti("nb", at.geti("N")), L = at.geti("L");
   const int64_t cn = attn_chunk(N, L);
-  return (size_t)(cn * L * L * 4 + cn * L * 4);
+  const bool tc = at.gets("dtype", "bf16") != "f32";
+  return (size_t)(cn * L * L * 4 + cn * L * 4) +
+         (tc ? attn_split_ws(N, L, (int)at.geti("dq"), (int)at.geti("dv")) : 0);
 }
 
 OC_GAN_DISPATCH(upsample2_fwd)
