@@ -403,9 +403,10 @@ def conv_flops(doc):
 
 def attn_bytes(doc):
     """Algorithmic HBM bytes per attention function (bf16 tensor-core path,
-    DESIGN.md §7): forward S written and read (fp32), P written and read
-    (bf16) = 12·L² per sample; backward P read twice, dS written once and read
-    twice = 16·L² per sample (the L-wide q, k, v, o tensors are < 2 % and left out)."""
+    DESIGN.md §7): forward P written and read (bf16; the scores are recomputed,
+    never stored, when dq ≤ 64) = 4·L² per sample, else S written and read
+    (fp32) too = 12·L²; backward P read twice, dS written once and read twice =
+    16·L² per sample (the L-wide q, k, v, o tensors are < 2 % and left out)."""
     d = json.loads(doc)
     out = {}
     for f in d["functions"]:
@@ -413,7 +414,8 @@ def attn_bytes(doc):
         a = op.get("attrs", {})
         if op.get("kind") in ("attn_fwd", "attn_bwd"):
             nb, L = a.get("nb", a["N"]), a["L"]
-            out[f["id"]] = (12 if op["kind"] == "attn_fwd" else 16) * nb * L * L
+            per = (4 if a["dq"] <= 64 else 12) if op["kind"] == "attn_fwd" else 16
+            out[f["id"]] = per * nb * L * L
     return out
 
 

@@ -463,6 +463,267 @@ Status launch(OpArgs& a, const KP& p) {
 
 bool aligned(const void* p, int64_t bytes) { return ((uintptr_t)p % bytes) == 0; }
 
+
+// ---------------------------------------------------------------- fused attention probabilities
+struct AP {
+  int L, dq, js, jper;
+  const uint16_t* q;
+  const uint16_t* k;
+  int64_t sb;          // q / k batch stride (L·dq)
+  uint16_t* P;
+  float* pm;           // per-range row statistics [nb][js][L]
+  float* pl;
+  int vec;
+  int async_k;         // k rows 8-byte aligned (dq % 4 == 0): cp.async key tiles
+};
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int AT_N = 64;    // key columns per score tile (two TMEM buffers of 64 columns)
+constexpr int AT_NT = 256;
+constexpr int AT_KS = 4;    // key-tile ring slots (cp.async path)
+constexpr int AT_JS = 16;   // most key ranges per row (fixed-size statistics merge)  // 8 warps: warp w reads TMEM lanes 32·(w % 4).., columns 32·(w / 4).. of a tile
+
+// one 128-query block × one key range of one sample; pass 0 (WRITE = false):
+// running (max, Σexp) per row; pass 1: merge the ranges, write P.  Each thread
+// owns one query row (its TMEM lane) and one 32-column half of every tile;
+// exp(s − m) = 2^(s·log2e − m·log2e).  Warps 0-3 stage the operands.
+template <bool WRITE>
+__global__ void __launch_bounds__(AT_NT) attn_p_kernel(const __grid_constant__ AP p) {
+  constexpr int T_A = BM * BK * 2, T_B = AT_N * BK * 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  constexpr int T_P = BM * AT_N * 2;   // pass 1: a bf16 P tile staged for coalesced stores (two buffers)
+  uint8_t* pst = smem + T_A + AT_KS * T_B;
+  uint64_t* tfull = (uint64_t*)(pst + (WRITE ? 2 * T_P : 0));
+  uint32_t* tmem_slot = (uint32_t*)(tfull + 2);
+  float* xch = (float*)(tmem_slot + 2);   // pass 0: the second halves' (max, Σ) per row
+  const int warp = threadIdx.x >> 5, half = warp >> 2, lane = threadIdx.x & 31;
+  const bool stager = threadIdx.x < NT;
+  const int jr = blockIdx.x, i0 = blockIdx.y * BM, b = blockIdx.z, L = p.L;
+  const int rl = (warp & 3) * 32 + lane, row = i0 + rl;   // this thread's TMEM lane = query row
+  const int jbeg = jr * p.jper, jend = min(L, jbeg + p.jper);
+  const int T = jend > jbeg ? (jend - jbeg + AT_N - 1) / AT_N : 0;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tfull[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * AT_N));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  const uint16_t* qb = p.q + b * p.sb;
+  const uint16_t* kb_ = p.k + b * p.sb;
+  if (stager) {
+    Loader<BM, false> la;
+    la.init(qb, p.dq, 1, false, p.vec, i0, L, p.dq);
+    la.load(0, p.dq >= BK);
+    la.store(smem_u32(smem), 0);
+  }
+  // this row's statistics: running (pass 0) or merged over the ranges (pass 1)
+  float m = -INFINITY, l = 0.f;
+  if (WRITE && row < L) {
+    const float* pm = p.pm + (int64_t)b * p.js * L + row;
+    const float* pl = p.pl + (int64_t)b * p.js * L + row;
+    float zm[AT_JS], zl[AT_JS];
+#pragma unroll
+    for (int z = 0; z < AT_JS; ++z) {
+      zm[z] = z < p.js ? pm[(int64_t)z * L] : -INFINITY;
+      zl[z] = z < p.js ? pl[(int64_t)z * L] : 0.f;
+    }
+#pragma unroll
+    for (int z = 0; z < AT_JS; ++z) m = fmaxf(m, zm[z]);
+#pragma unroll
+    for (int z = 0; z < AT_JS; ++z)
+      if (zm[z] != -INFINITY) l += zl[z] * ex2((zm[z] - m) * kLog2e);
+  }
+  const float inv = 1.f / l;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t id = idesc_m(BM, AT_N, false, false);
+  const uint32_t a_s = smem_u32(smem);
+
+  Loader<AT_N, false> lb;
+  auto load_k = [&](int t) {
+    lb.init(kb_, p.dq, 1, false, p.vec, jbeg + t * AT_N, jend, p.dq);
+    lb.load(0, p.dq >= BK);
+  };
+  auto epilogue = [&](int u) {
+    mbar_wait(&tfull[u & 1], (u >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int j0 = jbeg + u * AT_N;
+    {
+      const int c4 = half;
+      uint32_t v[32];
+      TMEM_LD32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (u & 1) * AT_N + c4 * 32, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const int jc = j0 + c4 * 32;
+      const int nv = min(32, jend - jc);
+      if (!WRITE) {
+        if (row < L && nv > 0) {
+          float x[32];
+          if (nv == 32) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = fmaxf(__uint_as_float(v[e]), __uint_as_float(v[e + 16]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              x[e] = fmaxf(e < nv ? __uint_as_float(v[e]) : -INFINITY, e + 16 < nv ? __uint_as_float(v[e + 16]) : -INFINITY);
+          }
+#pragma unroll
+          for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+            for (int e = 0; e < w; ++e) x[e] = fmaxf(x[e], x[e + w]);
+          const float mn = fmaxf(m, x[0]), mL = mn * kLog2e;
+          float s4[4] = {0.f, 0.f, 0.f, 0.f};
+          if (nv == 32) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) s4[e & 3] += ex2(fmaf(__uint_as_float(v[e]), kLog2e, -mL));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (e < nv) s4[e & 3] += ex2(fmaf(__uint_as_float(v[e]), kLog2e, -mL));
+          }
+          l = (m == -INFINITY ? 0.f : l * ex2((m - mn) * kLog2e)) + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
+          m = mn;
+        }
+      } else {
+        // P for this row's 32 columns into the staging tile (row rl, 16-byte
+        // chunks 4·half .. 4·half + 3, swizzled by rl % 8), then the CTA stores
+        // the tile as whole 128-byte row segments
+        const uint32_t sb = smem_u32(pst) + (u & 1) * T_P;
+        if (row < L && nv > 0) {
+          const float mL = m * kLog2e;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float e8[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) e8[e] = ex2(fmaf(__uint_as_float(v[c * 8 + e]), kLog2e, -mL)) * inv;
+            const int ch = half * 4 + c;
+            sts128(sb + rl * 128 + ((ch ^ (rl & 7)) << 4),
+                   make_uint4(pack2(e8[0], e8[1]), pack2(e8[2], e8[3]), pack2(e8[4], e8[5]), pack2(e8[6], e8[7])));
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(AT_NT) : "memory");
+        const int ch = threadIdx.x & 7, col = j0 + ch * 8;
+#pragma unroll
+        for (int i = 0; i < BM * 8 / AT_NT; ++i) {
+          const int r = (threadIdx.x >> 3) + i * (AT_NT / 8), grow = i0 + r;
+          if (grow >= L || col >= jend) continue;
+          const uint4 w = lds128(sb + r * 128 + ((ch ^ (r & 7)) << 4));
+          uint16_t* pp = p.P + (int64_t)b * L * L + (int64_t)grow * L + col;
+          if (col + 8 <= jend && p.vec) {
+            *reinterpret_cast<uint4*>(pp) = w;
+          } else {
+            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (col + e < jend) pp[e] = (uint16_t)(ww[e >> 1] >> ((e & 1) * 16));
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  };
+
+  if (p.async_k) {
+    // key tiles through a ring of AT_KS shared-memory slots filled by cp.async
+    // (8-byte pieces, zero-filled past the range and past dq), AT_KS − 1 tiles ahead
+    auto issue_k = [&](int t) {
+      if (t < T) {
+        const uint32_t slot = a_s + T_A + (t % AT_KS) * T_B;
+        const int c = threadIdx.x & 7;
+#pragma unroll
+        for (int i = 0; i < AT_N * 8 / AT_NT; ++i) {
+          const int r = (threadIdx.x >> 3) + i * (AT_NT / 8), j = jbeg + t * AT_N + r;
+          const uint32_t dst = slot + r * 128 + ((c ^ (r & 7)) << 4);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int e0 = c * 8 + h * 4;
+            const bool ok = j < jend && e0 < p.dq;
+            const uint16_t* src = ok ? kb_ + (int64_t)j * p.dq + e0 : kb_;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst + h * 8), "l"(src), "r"(ok ? 8 : 0)
+                         : "memory");
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int t = 0; t < AT_KS - 1; ++t) issue_k(t);
+    for (int t = 0; t < T; ++t) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(AT_KS - 2) : "memory");
+      fence_async_smem();
+      __syncthreads();
+      const uint32_t bsm = a_s + T_A + (t % AT_KS) * T_B;
+      if (threadIdx.x == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < BK / 16; ++j)
+          mma_bf16(tmem + (t & 1) * AT_N, sdesc(a_s + j * 32, 16, 1024), sdesc(bsm + j * 32, 16, 1024), id,
+                   j > 0 ? 1u : 0u);
+        mma_commit(&tfull[t & 1]);
+      }
+      if (t >= 1) epilogue(t - 1);   // waits for MMA t − 1: its slot may be refilled
+      issue_k(t + AT_KS - 1);
+    }
+    if (T > 0) epilogue(T - 1);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  } else {
+  if (T > 0 && stager) load_k(0);
+  for (int t = 0; t < T; ++t) {
+    const uint32_t bsm = a_s + T_A + (t & 1) * T_B;
+    if (stager) lb.store(bsm, 0);   // the MMA that last read this buffer (t − 2) was waited for by epilogue(t − 2)
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < BK / 16; ++j)
+        mma_bf16(tmem + (t & 1) * AT_N, sdesc(a_s + j * 32, 16, 1024), sdesc(bsm + j * 32, 16, 1024), id,
+                 j > 0 ? 1u : 0u);
+      mma_commit(&tfull[t & 1]);
+    }
+    if (t + 1 < T && stager) load_k(t + 1);
+    if (t >= 1) epilogue(t - 1);
+  }
+  if (T > 0) epilogue(T - 1);
+  }
+  if (!WRITE) {   // merge the two column halves of each row, in fixed order
+    if (half) {
+      xch[rl] = m;
+      xch[BM + rl] = l;
+    }
+    __syncthreads();
+    if (!half && row < L) {
+      const float m1 = xch[rl], l1 = xch[BM + rl], mm = fmaxf(m, m1);
+      const float lm = (m == -INFINITY ? 0.f : l * ex2((m - mm) * kLog2e)) +
+                       (m1 == -INFINITY ? 0.f : l1 * ex2((m1 - mm) * kLog2e));
+      p.pm[((int64_t)b * p.js + jr) * L + row] = mm;
+      p.pl[((int64_t)b * p.js + jr) * L + row] = lm;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * AT_N));
+  }
+}
+
+int attn_js(int nb, int L) {
+  const int rb = (L + BM - 1) / BM, tiles = (L + AT_N - 1) / AT_N;
+  const int64_t ctas = (int64_t)rb * nb;
+  int js = (int)std::min<int64_t>(std::min(tiles, AT_JS), std::max<int64_t>(1, (4 * 148 + ctas - 1) / ctas));
+  return std::max(1, js);
+}
 }  // namespace
 
 int splits_of(const Gemm& g) {
@@ -545,6 +806,49 @@ Status gemm(OpArgs& a, const Gemm& g, void* ws, size_t ws_size) {
                                                                                 (__nv_bfloat16*)g.C, g.ldc, g.c_b);
     OC_LAUNCH_CHECK(a);
   }
+  return Status::ok();
+}
+
+}  // namespace tcg
+}  // namespace oc
+
+namespace oc {
+namespace tcg {
+
+size_t attn_softmax_ws(int nb, int L) { return (size_t)2 * nb * attn_js(nb, L) * L * 4; }
+
+Status attn_softmax(OpArgs& a, const __nv_bfloat16* q, const __nv_bfloat16* k, __nv_bfloat16* P, int nb, int L,
+                    int dq, void* ws, size_t ws_size) {
+  if (nb <= 0 || L <= 0) return Status::ok();
+  if (dq > BK) return Status::make(OC_E_UNSUPPORTED, "attn_softmax: dq > 64");
+  if (nb > 65535) return Status::make(OC_E_UNSUPPORTED, "attn_softmax: batch > 65535");
+  if (!ws || ws_size < attn_softmax_ws(nb, L)) return Status::make(OC_E_INVARIANT, "attn_softmax: workspace");
+  AP p{};
+  p.L = L;
+  p.dq = dq;
+  p.js = attn_js(nb, L);
+  p.jper = ((L + AT_N - 1) / AT_N + p.js - 1) / p.js * AT_N;
+  p.q = (const uint16_t*)q;
+  p.k = (const uint16_t*)k;
+  p.sb = (int64_t)L * dq;
+  p.P = (uint16_t*)P;
+  p.pm = (float*)ws;
+  p.pl = p.pm + (size_t)nb * p.js * L;
+  p.vec = aligned(q, 16) && aligned(k, 16) && aligned(P, 16) && dq % 8 == 0 && L % 8 == 0;
+  p.async_k = aligned(k, 8) && dq % 4 == 0;
+  constexpr int SMEM0 = BM * BK * 2 + AT_KS * AT_N * BK * 2 + 1024 + 64 + 2 * BM * 4;
+  constexpr int SMEM1 = SMEM0 + 2 * BM * AT_N * 2;
+  static bool attr = false;
+  if (!attr) {
+    OC_CUDA(cudaFuncSetAttribute(attn_p_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM0));
+    OC_CUDA(cudaFuncSetAttribute(attn_p_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM1));
+    attr = true;
+  }
+  dim3 grid(p.js, (L + BM - 1) / BM, nb);
+  attn_p_kernel<false><<<grid, AT_NT, SMEM0, a.stream>>>(p);
+  OC_LAUNCH_CHECK(a);
+  attn_p_kernel<true><<<grid, AT_NT, SMEM1, a.stream>>>(p);
+  OC_LAUNCH_CHECK(a);
   return Status::ok();
 }
 

@@ -50,5 +50,16 @@ size_t ws_bytes(const Gemm& g);
 // ws is smaller than ws_bytes(g)
 Status gemm(OpArgs& a, const Gemm& g, void* ws = nullptr, size_t ws_size = 0);
 
+// Attention probabilities without the fp32 score map: P[b] = rnd(softmax_rows(
+// q[b] k[b]ᵀ)) for q, k [nb, L, dq] bf16 (dq ≤ 64), P [nb, L, L] bf16.  Two
+// launches over (query block, key range): the first recomputes the scores on
+// the tensor cores and keeps per-row running (max, Σexp) for its key range;
+// the second merges the ranges' statistics in fixed order, recomputes the
+// scores and writes P = exp(s − max) / Σ.  Scores are never stored: HBM
+// traffic is P's write alone.  ws: attn_softmax_ws() bytes.
+size_t attn_softmax_ws(int nb, int L);
+Status attn_softmax(OpArgs& a, const __nv_bfloat16* q, const __nv_bfloat16* k, __nv_bfloat16* P, int nb, int L,
+                    int dq, void* ws, size_t ws_size);
+
 }  // namespace tcg
 }  // namespace oc

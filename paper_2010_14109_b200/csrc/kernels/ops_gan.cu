@@ -498,11 +498,17 @@ Status attn_fwd_t(OpArgs& a) {
   for (int64_t n0 = 0; n0 < N; n0 += cn) {
     const int b = (int)std::min<int64_t>(cn, N - n0);
     if (TC) {
-      // S = q kᵀ: A = q (K-major), B(k, n) = k[n][k] (K-major); fp32 out
-      OC_TRY(tcg::gemm(a, {(int)L, (int)L, dq, b, q + n0 * L * dq, dq, 1, L * dq, false, k + n0 * L * dq, 1, dq,
-                           L * dq, S, L, L * L, true}));
-      softmax_rows<T>(a, b * L, (int)L, S, P + n0 * L * L);
-      OC_LAUNCH_CHECK(a);
+      if (dq <= 64) {
+        // P straight from q, k: the scores are recomputed on the tensor cores, never stored
+        OC_TRY(tcg::attn_softmax(a, (const __nv_bfloat16*)(q + n0 * L * dq), (const __nv_bfloat16*)(k + n0 * L * dq),
+                                 (__nv_bfloat16*)(P + n0 * L * L), b, (int)L, dq, S, (size_t)(cn * L * L * 4)));
+      } else {
+        // S = q kᵀ: A = q (K-major), B(k, n) = k[n][k] (K-major); fp32 out
+        OC_TRY(tcg::gemm(a, {(int)L, (int)L, dq, b, q + n0 * L * dq, dq, 1, L * dq, false, k + n0 * L * dq, 1, dq,
+                             L * dq, S, L, L * L, true}));
+        softmax_rows<T>(a, b * L, (int)L, S, P + n0 * L * L);
+        OC_LAUNCH_CHECK(a);
+      }
       // o = P v: B(k, n) = v[k][n] (MN-major)
       OC_TRY(tcg::gemm(a, {(int)L, dv, (int)L, b, P + n0 * L * L, L, 1, L * L, false, v + n0 * L * dv, dv, 1,
                            L * dv, O + n0 * L * dv, dv, L * dv, false}, part, sws));
