@@ -46,6 +46,8 @@ struct KP {
   const float* ep_rs;
   int64_t rs_b;
   int ep_vec;
+  const float* bias;           // + bias[n], then ReLU if relu (unsplit calls)
+  int relu;
 };
 
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
@@ -89,8 +91,10 @@ __device__ __forceinline__ const T* chunk_src(const T* X, int64_t s_mn, int64_t 
 // and dk per K-block, and which chunks are wholly in range (vector load) or
 // wholly outside (zero) is known once.  Only chunks cut by the M, N or K edge,
 // or an operand whose rows are not 16-byte aligned, take the element-wise path.
-template <int ROWS, bool F32>
+// KIND 0: bf16; 1: fp32 split into bf16 hi + lo tiles; 2: fp32 rounded to bf16
+template <int ROWS, int KIND>
 struct Loader {
+  static constexpr bool F32 = KIND != 0;
   using T = typename std::conditional<F32, float, uint16_t>::type;
   static constexpr int IT = ROWS * BK / 8 / NT;
   const T* X;
@@ -187,12 +191,15 @@ struct Loader {
       }
     }
   }
-  // bf16: one tile; fp32: hi tile at `tile`, lo tile at `lo`
+  // bf16 / rounded fp32: one tile; split fp32: hi tile at `tile`, lo tile at `lo`
   __device__ __forceinline__ void store(uint32_t tile, uint32_t lo) const {
 #pragma unroll
     for (int i = 0; i < IT; ++i) {
       const uint32_t off = chunk_off(mn_major, r0 + i * rstep, c);
-      if constexpr (F32) {
+      if constexpr (KIND == 2) {
+        sts128(tile + off, make_uint4(pack2(f[i][0].x, f[i][0].y), pack2(f[i][0].z, f[i][0].w),
+                                      pack2(f[i][1].x, f[i][1].y), pack2(f[i][1].z, f[i][1].w)));
+      } else if constexpr (KIND == 1) {
         const float e8[8] = {f[i][0].x, f[i][0].y, f[i][0].z, f[i][0].w, f[i][1].x, f[i][1].y, f[i][1].z, f[i][1].w};
         uint32_t hw[4], lw[4];
 #pragma unroll
@@ -211,7 +218,7 @@ struct Loader {
   }
 };
 
-template <int BN, bool AF32, bool CF32>
+template <int BN, bool AF32, bool CF32, bool BF32>
 __global__ void __launch_bounds__(NT) gemm_tc_kernel(const __grid_constant__ KP P) {
   constexpr int A_T = BM * BK * 2, B_T = BN * BK * 2;
   constexpr int STAGE = A_T * (AF32 ? 2 : 1) + B_T;
@@ -245,10 +252,10 @@ __global__ void __launch_bounds__(NT) gemm_tc_kernel(const __grid_constant__ KP 
   const uint32_t id = idesc_m(BM, BN, a_mn, b_mn);
   const int nkb = (P.K + BK - 1) / BK, nfull = P.K / BK;
   const int kb0 = sp * P.kps, kb1 = min(nkb, kb0 + P.kps);
-  Loader<BM, AF32> la;
-  Loader<BN, false> lb;
-  la.init((const typename Loader<BM, AF32>::T*)P.A + bz * P.a_b, P.a_m, P.a_k, a_mn, P.a_vec, m0, P.M, P.K);
-  lb.init((const uint16_t*)P.B + bz * P.b_b, P.b_n, P.b_k, b_mn, P.b_vec, n0, P.N, P.K);
+  Loader<BM, AF32 ? 1 : 0> la;
+  Loader<BN, BF32 ? 2 : 0> lb;
+  la.init((const typename Loader<BM, AF32 ? 1 : 0>::T*)P.A + bz * P.a_b, P.a_m, P.a_k, a_mn, P.a_vec, m0, P.M, P.K);
+  lb.init((const typename Loader<BN, BF32 ? 2 : 0>::T*)P.B + bz * P.b_b, P.b_n, P.b_k, b_mn, P.b_vec, n0, P.N, P.K);
   if (kb0 < kb1) {
     la.load(kb0, kb0 < nfull);
     lb.load(kb0, kb0 < nfull);
@@ -359,6 +366,14 @@ __global__ void __launch_bounds__(NT) gemm_tc_kernel(const __grid_constant__ KP 
         float f[4] = {__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w)};
         if (row >= P.M || col >= P.N) continue;
         const int nv = P.N - col;
+        if (!split && P.bias) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) f[e] += e < nv ? P.bias[col + e] : 0.f;
+        }
+        if (!split && P.relu) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) f[e] = fmaxf(f[e], 0.f);
+        }
         if (ep) {   // dS = P ⊙ (dP − rs)
           f[0] = __uint_as_float(pc[i].x << 16) * (f[0] - rsv[i]);
           f[1] = __uint_as_float(pc[i].x & 0xffff0000u) * (f[1] - rsv[i]);
@@ -391,7 +406,11 @@ __global__ void __launch_bounds__(NT) gemm_tc_kernel(const __grid_constant__ KP 
       for (int c = 0; c < 32; c += 8) {
         float f[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = has_k ? __uint_as_float(v[c + e]) : 0.f;
+        for (int e = 0; e < 8; ++e) {
+          f[e] = has_k ? __uint_as_float(v[c + e]) : 0.f;
+          if (P.bias && c + e < nv) f[e] += P.bias[n0 + j0 + c + e];
+          if (P.relu) f[e] = fmaxf(f[e], 0.f);
+        }
         if (c + 8 <= nv && P.c_vec) {
           *reinterpret_cast<uint4*>(cp + c) =
               make_uint4(pack2(f[0], f[1]), pack2(f[2], f[3]), pack2(f[4], f[5]), pack2(f[6], f[7]));
@@ -427,7 +446,10 @@ __global__ void split_reduce_k(int64_t n, int M, int N, int splits, const float*
 
 // fp32 outputs (the L × L maps) take 128-column tiles: 128 TMEM columns per
 // CTA, so four CTAs share an SM and one's epilogue overlaps the others' loads
-int bn_of(const Gemm& g) { return g.N <= 64 ? 64 : (g.N <= 128 || g.c_f32) ? 128 : 256; }
+int bn_of(const Gemm& g) {
+  if (g.b_f32 || (g.a_f32 && g.c_f32)) return 128;   // the dense layers: one tile width
+  return g.N <= 64 ? 64 : (g.N <= 128 || g.c_f32) ? 128 : 256;
+}
 
 void plan_split(const Gemm& g, int& splits, int& kps) {
   const int nkb = (g.K + BK - 1) / BK;
@@ -435,7 +457,7 @@ void plan_split(const Gemm& g, int& splits, int& kps) {
   const int64_t tiles = (int64_t)((g.N + bn - 1) / bn) * ((g.M + BM - 1) / BM) * g.batch;
   const int64_t target = 2 * 148;
   splits = 1;
-  if (!g.ep_p && tiles < target && nkb >= 8) {
+  if (!g.ep_p && !g.no_split && !g.bias && !g.relu && tiles < target && nkb >= 8) {
     int64_t s = (target + tiles - 1) / tiles;
     s = std::min<int64_t>(s, nkb / 4);
     s = std::min<int64_t>(s, 65535 / std::max(1, g.batch));
@@ -445,11 +467,11 @@ void plan_split(const Gemm& g, int& splits, int& kps) {
   splits = std::max(1, (nkb + kps - 1) / kps);
 }
 
-template <int BN, bool AF32, bool CF32>
+template <int BN, bool AF32, bool CF32, bool BF32 = false>
 Status launch(OpArgs& a, const KP& p) {
   constexpr int STAGE = BM * BK * 2 * (AF32 ? 2 : 1) + BN * BK * 2;
   const int smem = std::max(p.ns * STAGE, STG) + 1024 + 64;
-  auto k = gemm_tc_kernel<BN, AF32, CF32>;
+  auto k = gemm_tc_kernel<BN, AF32, CF32, BF32>;
   static bool attr = false;
   if (!attr) {
     OC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, NS * STAGE + 1024 + 64));
@@ -522,7 +544,7 @@ __global__ void __launch_bounds__(AT_NT) attn_p_kernel(const __grid_constant__ A
   const uint16_t* qb = p.q + b * p.sb;
   const uint16_t* kb_ = p.k + b * p.sb;
   if (stager) {
-    Loader<BM, false> la;
+    Loader<BM, 0> la;
     la.init(qb, p.dq, 1, false, p.vec, i0, L, p.dq);
     la.load(0, p.dq >= BK);
     la.store(smem_u32(smem), 0);
@@ -552,7 +574,7 @@ __global__ void __launch_bounds__(AT_NT) attn_p_kernel(const __grid_constant__ A
   const uint32_t id = idesc_m(BM, AT_N, false, false);
   const uint32_t a_s = smem_u32(smem);
 
-  Loader<AT_N, false> lb;
+  Loader<AT_N, 0> lb;
   auto load_k = [&](int t) {
     lb.init(kb_, p.dq, 1, false, p.vec, jbeg + t * AT_N, jend, p.dq);
     lb.load(0, p.dq >= BK);
@@ -741,7 +763,6 @@ Status gemm(OpArgs& a, const Gemm& g, void* ws, size_t ws_size) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return Status::ok();
   if ((g.a_m != 1 && g.a_k != 1) || (g.b_k != 1 && g.b_n != 1))
     return Status::make(OC_E_UNSUPPORTED, "gemm_tc: an operand without a unit stride");
-  if (g.a_f32 && g.c_f32) return Status::make(OC_E_UNSUPPORTED, "gemm_tc: fp32 A with fp32 C");
   if (g.ep_p && !g.c_f32) return Status::make(OC_E_UNSUPPORTED, "gemm_tc: fused epilogue needs fp32 C");
   KP p{};
   p.M = g.M;
@@ -775,6 +796,9 @@ Status gemm(OpArgs& a, const Gemm& g, void* ws, size_t ws_size) {
   p.ep_rs = g.ep_rs;
   p.rs_b = g.rs_b;
   p.ep_vec = g.ep_p && aligned(g.ep_p, 8) && g.ldp % 4 == 0 && g.p_b % 4 == 0;
+  p.bias = g.bias;
+  p.relu = g.relu ? 1 : 0;
+  if (g.b_f32) p.b_vec = aligned(g.B, 16) && (p.b_mn ? g.b_k : g.b_n) % 4 == 0 && g.b_b % 4 == 0;
   if (p.splits > 1) {
     const size_t need = (size_t)p.splits * g.batch * g.M * g.N * 4;
     if (!ws || ws_size < need) return Status::make(OC_E_INVARIANT, "gemm_tc: split workspace");
@@ -784,7 +808,7 @@ Status gemm(OpArgs& a, const Gemm& g, void* ws, size_t ws_size) {
   const int BN = bn_of(g);
   Status st = Status::make(OC_E_UNSUPPORTED, "gemm_tc: no instantiation");
 #define OC_TCG(bn, af, cf) \
-  if (BN == bn && g.a_f32 == af && g.c_f32 == cf) st = launch<bn, af, cf>(a, p);
+  if (BN == bn && g.a_f32 == af && g.c_f32 == cf && !g.b_f32) st = launch<bn, af, cf>(a, p);
   OC_TCG(64, false, false)
   OC_TCG(128, false, false)
   OC_TCG(256, false, false)
@@ -794,7 +818,12 @@ Status gemm(OpArgs& a, const Gemm& g, void* ws, size_t ws_size) {
   OC_TCG(64, true, false)
   OC_TCG(128, true, false)
   OC_TCG(256, true, false)
+  OC_TCG(128, true, true)
 #undef OC_TCG
+  // dense layers: fp32 master weights rounded to bf16 as they are staged
+  if (g.b_f32 && !g.a_f32 && g.c_f32) st = launch<128, false, true, true>(a, p);
+  if (g.b_f32 && !g.a_f32 && !g.c_f32) st = launch<128, false, false, true>(a, p);
+  if (g.b_f32 && g.a_f32 && !g.c_f32) st = launch<128, true, false, true>(a, p);
   OC_TRY(st);
   if (p.splits > 1) {
     const int64_t n = (int64_t)g.batch * g.M * g.N;

@@ -1,5 +1,6 @@
-// Batched tcgen05 GEMM for the attention products of the GAN step (bf16
-// activations; ops_gan.cu): C[b] = A[b] · B[b], fp32 accumulation in TMEM.
+// Batched tcgen05 GEMM for the attention products of the GAN step and the
+// bf16 dense layers (ops_gan.cu, ops_dense.cu): C[b] = A[b] · B[b], fp32
+// accumulation in TMEM.
 //
 //   A(m, k) at A + b·a_b + m·a_m + k·a_k   (bf16, or fp32 split into bf16 hi + lo)
 //   B(k, n) at B + b·b_b + k·b_k + n·b_n   (bf16)
@@ -40,6 +41,12 @@ struct Gemm {
   int64_t ldp = 0, p_b = 0;
   const float* ep_rs = nullptr;
   int64_t rs_b = 0;
+  // dense layers: B fp32 (a master weight) rounded to bf16 as staged; bias[n]
+  // added and ReLU applied in the epilogue; no K split (no workspace)
+  bool b_f32 = false;
+  const float* bias = nullptr;
+  bool relu = false;
+  bool no_split = false;
 };
 
 // K splits the call will use (1 = none)

@@ -4,12 +4,13 @@
 // a step is bitwise reproducible whatever the swap schedule (swap
 // transparency).
 //
-// The GEMM here is a SIMT FFMA kernel: the fp32 parity mode must not use TF32
-// tensor cores, and the dense layers of the configs are tiny
-// (MLP 8×256×256, ResNet FC b×512×1000).  Convolutions — the dominant
-// contractions — run on tcgen05 (kernels/conv_tc.cu).
+// bf16 layers run their products on the tensor cores (gemm_tc.cuh: the fp32
+// master weight rounded to bf16 as it is staged, an fp32 logits gradient as an
+// exact bf16 hi + lo pair, bias / ReLU in the epilogue); the fp32 parity mode
+// and ReLU-masked gradients keep the SIMT FFMA kernel (no TF32).
 #include "common.cuh"
 #include "gemm_simt.cuh"
+#include "gemm_tc.cuh"
 
 namespace oc {
 
@@ -43,11 +44,15 @@ Status linear_fwd(OpArgs& a) {
   if (dt == "f32")
     return gemm<float, float, float, false>(a, M, N, K, (const float*)a.p(L_X), K, 1, nullptr, w, 1, K,
                                             (float*)a.p(L_Y), N, 1, b, relu, false);
-  if (Ab(a, "out_f32"))
-    return gemm<__nv_bfloat16, float, float, true>(a, M, N, K, (const __nv_bfloat16*)a.p(L_X), K, 1, nullptr, w,
-                                                   1, K, (float*)a.p(L_Y), N, 1, b, relu, false);
-  return gemm<__nv_bfloat16, float, __nv_bfloat16, true>(a, M, N, K, (const __nv_bfloat16*)a.p(L_X), K, 1, nullptr,
-                                                         w, 1, K, (__nv_bfloat16*)a.p(L_Y), N, 1, b, relu, false);
+  {
+    // y = x Wᵀ + b: A = x (K-major), B(k, n) = W[n][k] (fp32, rounded, K-major)
+    tcg::Gemm g{M, N, K, 1, a.p(L_X), K, 1, 0, false, w, 1, K, 0, a.p(L_Y), N, 0, Ab(a, "out_f32")};
+    g.b_f32 = true;
+    g.bias = b;
+    g.relu = relu;
+    g.no_split = true;
+    return tcg::gemm(a, g);
+  }
 }
 
 // roles: dy, y (ReLU mask source), x, w, dw, db, dx
@@ -63,6 +68,25 @@ Status linear_bwd(OpArgs& a) {
     // dy fp32 [M,N]; mask (if any) has dy's layout and type
     const float* dy = (const float*)a.p(LB_DY);
     const float* mask = relu ? (const float*)a.p(LB_Y) : nullptr;
+    if (dt != "f32" && !mask) {
+      // tensor cores: dW[n,k] = Σ_m dy[m,n] x[m,k] (A = dyᵀ, MN-major fp32 split; B = x, MN-major)
+      if (dw) {
+        tcg::Gemm g{N, K, M, 1, dy, 1, N, 0, true, a.p(LB_X), K, 1, 0, dw, K, 0, true};
+        g.no_split = true;
+        OC_TRY(tcg::gemm(a, g));
+      }
+      if (db) {
+        colsum<float><<<(N + 255) / 256, 256, 0, a.stream>>>(M, N, dy, nullptr, db);
+        OC_LAUNCH_CHECK(a);
+      }
+      if (a.p(LB_DX)) {   // dx = dy W: A = dy (K-major fp32 split), B(k, n) = W[k][n] (fp32 rounded, MN-major)
+        tcg::Gemm g{M, K, N, 1, dy, N, 1, 0, true, a.p(LB_W), K, 1, 0, a.p(LB_DX), K, 0, false};
+        g.b_f32 = true;
+        g.no_split = true;
+        OC_TRY(tcg::gemm(a, g));
+      }
+      return Status::ok();
+    }
     // dW[n,k] = Σ_m dz[m,n] x[m,k]  (dw / db null: data gradient only)
     if (dw && dt == "f32") {
       OC_TRY((gemm<float, float, float, false>(a, N, K, M, dy, 1, N, mask, (const float*)a.p(LB_X), K, 1, dw, K, 1,
@@ -89,6 +113,24 @@ Status linear_bwd(OpArgs& a) {
   // bf16 dy (hidden bf16 linear layers)
   const __nv_bfloat16* dy = (const __nv_bfloat16*)a.p(LB_DY);
   const __nv_bfloat16* mask = relu ? (const __nv_bfloat16*)a.p(LB_Y) : nullptr;
+  if (!mask) {
+    if (dw) {   // A = dyᵀ (MN-major bf16), B = x (MN-major)
+      tcg::Gemm g{N, K, M, 1, dy, 1, N, 0, false, a.p(LB_X), K, 1, 0, dw, K, 0, true};
+      g.no_split = true;
+      OC_TRY(tcg::gemm(a, g));
+    }
+    if (db) {
+      colsum<__nv_bfloat16><<<(N + 255) / 256, 256, 0, a.stream>>>(M, N, dy, nullptr, db);
+      OC_LAUNCH_CHECK(a);
+    }
+    if (a.p(LB_DX)) {
+      tcg::Gemm g{M, K, N, 1, dy, N, 1, 0, false, a.p(LB_W), K, 1, 0, a.p(LB_DX), K, 0, false};
+      g.b_f32 = true;
+      g.no_split = true;
+      OC_TRY(tcg::gemm(a, g));
+    }
+    return Status::ok();
+  }
   if (dw)
     OC_TRY((gemm<__nv_bfloat16, __nv_bfloat16, float, false>(a, N, K, M, dy, 1, N, mask,
                                                              (const __nv_bfloat16*)a.p(LB_X), K, 1, dw, K, 1,
