@@ -419,6 +419,40 @@ def attn_bytes(doc):
     return out
 
 
+def copy_rates(tl, vbytes):
+    """Per-copy host-link rates of the instrumented pass: bytes-weighted
+    quantiles of bytes / duration per direction, and the share of each
+    direction's busy time during which the other direction was also copying
+    (a duplex PCIe link shares its bandwidth: ~50 GB/s each way when both run)."""
+    out = {}
+    iv = {"h2d": [], "d2h": []}
+    for ev in tl:
+        if ev["stream"] in iv and ev["t1"] > ev["t0"]:
+            iv[ev["stream"]].append((ev["t0"], ev["t1"], vbytes.get(ev["id"], 0)))
+    for d, lst in iv.items():
+        if not lst:
+            continue
+        rates = sorted(((b / ((t1 - t0) * 1e-3) / 1e9, b) for t0, t1, b in lst), key=lambda x: x[0])
+        tot = sum(b for _, b in rates)
+        q, acc = {}, 0
+        for r, b in rates:
+            acc += b
+            for k in (0.1, 0.5, 0.9):
+                if f"p{int(k * 100)}" not in q and acc >= k * tot:
+                    q[f"p{int(k * 100)}"] = round(r, 2)
+        other = sorted((t0, t1) for t0, t1, _ in iv["d2h" if d == "h2d" else "h2d"])
+        both = 0.0
+        for t0, t1, _ in lst:
+            for o0, o1 in other:
+                if o0 >= t1:
+                    break
+                both += max(0.0, min(t1, o1) - max(t0, o0))
+        busy = sum(t1 - t0 for t0, t1, _ in lst)
+        out[d] = {"copies": len(lst), "gbs_bytes_weighted": q, "gbs_sum_of_copies": round(tot / (busy * 1e-3) / 1e9, 2),
+                  "share_with_other_direction": round(both / busy, 3) if busy else None}
+    return out
+
+
 def time_steps(st, steps, warmup, world):
     import torch
     import torch.distributed as dist
@@ -642,6 +676,7 @@ def run_ours(args, rank, world):
     fn_ms = [dur.get(f, 0.0) for f in fid]
     bw_h = float(np.mean([m["bytes_h2d"] / max(m["h2d_busy_ms"], 1e-9) for m in mets_i])) / 1e6
     bw_d = float(np.mean([m["bytes_d2h"] / max(m["d2h_busy_ms"], 1e-9) for m in mets_i])) / 1e6
+    copy_diag = copy_rates(tl, vbytes)
     link = link_probe()
     bw_h = bw_h if bw_h > 1 else link["h2d"]
     bw_d = bw_d if bw_d > 1 else link["d2h"]
@@ -772,7 +807,7 @@ def run_ours(args, rank, world):
                       "h2d_gbs_busy": (h2d / (h2d_busy / 1e3) / 1e9) if h2d_busy else None,
                       "d2h_gbs_busy": (d2h / (d2h_busy / 1e3) / 1e9) if d2h_busy else None,
                       "pcie5_x16_gbs_per_dir": PCIE5_X16_GBS, "measured_pinned_gbs": link,
-                      "nvml_pcie_counters": pcie.summary()},
+                      "nvml_pcie_counters": pcie.summary(), "per_copy": copy_diag},
         "overlap_pct": 100 * overlap,
         "makespan_model": {"predicted_ms": sim["makespan_ms"], "predicted_boundary_ms": sim0["makespan_ms"],
                            "compute_ms": sim["compute_ms"], "stall_ms": sim["stall_ms"],
