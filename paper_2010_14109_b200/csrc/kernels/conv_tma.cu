@@ -50,12 +50,18 @@ __host__ __device__ constexpr int kblock(int mode) { return mode == 2 ? WKB : BK
 // stages: as many as fit 192 KB (at most 8); fprop / dgrad add 32 KB of
 // epilogue staging (two 32-row × 64-column bf16 boxes per epilogue warp)
 constexpr int STG_BYTES = 8 * 4096;
+// accumulating epilogue: the old output boxes stream through two more 4 KB
+// buffers per epilogue warp, loaded two boxes ahead (the ring gives up 32 KB)
+constexpr int OLD_BYTES = 8 * 4096;
 __host__ __device__ constexpr int tma_stage_bytes(int bn, int mt, int kb) { return mt * BM * kb * 2 + bn * kb * 2; }
-__host__ __device__ constexpr int tma_stages(int bn, int mt, int kb) {
-  return (192 * 1024) / tma_stage_bytes(bn, mt, kb) < 8 ? (192 * 1024) / tma_stage_bytes(bn, mt, kb) : 8;
+__host__ __device__ constexpr int tma_stages(int bn, int mt, int kb, bool acc = false) {
+  return (192 * 1024 - (acc ? OLD_BYTES : 0)) / tma_stage_bytes(bn, mt, kb) < 8
+             ? (192 * 1024 - (acc ? OLD_BYTES : 0)) / tma_stage_bytes(bn, mt, kb)
+             : 8;
 }
-__host__ __device__ constexpr int tma_smem(int bn, int mt, int kb) {
-  return tma_stages(bn, mt, kb) * tma_stage_bytes(bn, mt, kb) + (kb == WKB ? 0 : STG_BYTES) + 1024 + 256;
+__host__ __device__ constexpr int tma_smem(int bn, int mt, int kb, bool acc = false) {
+  return tma_stages(bn, mt, kb, acc) * tma_stage_bytes(bn, mt, kb) + (kb == WKB ? 0 : STG_BYTES) +
+         (acc ? OLD_BYTES : 0) + 1024 + 256;
 }
 
 struct Params {
@@ -102,17 +108,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
   static_assert(CG == 1 || (NCH == 0 && (MODE != WGRAD || BN / CG >= 64)), "CTA pairs: 64-channel pixels; wgrad: whole 64-column B atoms per CTA");
   constexpr int KB = kblock(MODE);              // K extent of a stage (elements, or wgrad pixels)
   constexpr int ATOM = KB * 128;                 // wgrad: one 64-wide MN-major atom column
-  constexpr int NST = tma_stages(BN / CG, MT, KB);
+  constexpr int NST = tma_stages(BN / CG, MT, KB, ACC);
+  static_assert(NST >= 2, "conv_tma: at least two ring stages");
   constexpr int A_TILE = BM * KB * 2, A_BYTES = MT * A_TILE, B_BYTES = (BN / CG) * KB * 2, STAGE = A_BYTES + B_BYTES;
   constexpr uint32_t TCOLS = 2 * MT * BN;   // two accumulator sets of MT tiles × BN columns
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* stg = smem + NST * STAGE;   // epilogue staging (fprop / dgrad)
-  uint64_t* full = (uint64_t*)(stg + (MODE == WGRAD ? 0 : STG_BYTES));
+  uint8_t* obuf = stg + STG_BYTES;     // ACC: old-output boxes (warp q, buffer b) at (2q + b) · 4 KB
+  uint64_t* full = (uint64_t*)(stg + (MODE == WGRAD ? 0 : STG_BYTES) + (ACC ? OLD_BYTES : 0));
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
-  uint64_t* ldbar = tempty + 2;        // accumulate epilogue: old-output box loads (warp q, buffer b) -> 2q + b
+  uint64_t* ldbar = tempty + 2;        // accumulate epilogue: old-output box loads into obuf (warp q, buffer b) -> 2q + b
   uint32_t* tmem_slot = (uint32_t*)(ldbar + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   KProbe kp;
@@ -345,7 +353,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
       float ssum[BN / 64][2], ssq[BN / 64][2];
 #pragma unroll
       for (int jb = 0; jb < BN / 64; ++jb) ssum[jb][0] = ssum[jb][1] = ssq[jb][0] = ssq[jb][1] = 0.f;
-      uint32_t ldph = 0;   // accumulate: phase bits of this warp's two box-load barriers
+      // ACC: this warp's boxes form one stream over its tiles (box s = tile
+      // lt, box b of NB, s = lt·NB + b); box s+2 is loaded into obuf buffer
+      // s & 1 as soon as box s has been consumed, so each load has two boxes
+      // of epilogue work (and the next tile's MMA wait) to arrive in
+      constexpr int NB = MT * (BN / 64);
+      auto issue_old = [&](uint32_t sidx) {
+        const int uu = u0 + (int)(sidx / NB) * ustep;
+        if (uu >= units) return;
+        int mt_, nt_, z_, kb0_, nk_;
+        unit_of(uu, mt_, nt_, z_, kb0_, nk_);
+        const int bb = (int)(sidx % NB), t_ = bb / (BN / 64), j_ = (bb % (BN / 64)) * 64;
+        uint64_t* lb = &ldbar[q * 2 + (sidx & 1)];
+        mbar_expect_tx(lb, 4096);
+        tma_load_2d(smem_u32(obuf) + (uint32_t)(q * 2 + (sidx & 1)) * 4096u, &P.tc, lb, nt_ * BN + j_,
+                    ((mt_ * MT + t_) * CG + (int)rank) * BM + q * 32);
+      };
+      if (ACC && lane == 0) {
+        issue_old(0);
+        if (NB > 1 || u0 + ustep < units) issue_old(1);
+      }
       for (int u = u0; u < units; u += ustep, ++lt) {
         int mt, nt, z, kb0, nk;
         unit_of(u, mt, nt, z, kb0, nk);
@@ -382,21 +409,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
                              : "memory");
               }
             } else {
-              // out = rnd(old + acc): the old box arrives by TMA in the same
-              // swizzled staging layout the store uses (rows past M zero-filled)
-              uint64_t* lb = &ldbar[q * 2 + (sc & 1)];
-              if (lane == 0) {
-                mbar_expect_tx(lb, 4096);
-                tma_load_2d(sb, &P.tc, lb, nt * BN + j0, row0);
-              }
-              mbar_wait(lb, (ldph >> (sc & 1)) & 1);
-              ldph ^= 1u << (sc & 1);
+              // out = rnd(old + acc): the old box arrived by TMA (issued two
+              // boxes earlier) in the swizzled layout the store uses (rows past M zero-filled)
+              const uint32_t ob = smem_u32(obuf) + (uint32_t)(q * 2 + (sc & 1)) * 4096u;
+              mbar_wait(&ldbar[q * 2 + (sc & 1)], (sc >> 1) & 1);
               uint32_t old[8][4];
 #pragma unroll
               for (int c = 0; c < 8; ++c)
                 asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
                              : "=r"(old[c][0]), "=r"(old[c][1]), "=r"(old[c][2]), "=r"(old[c][3])
-                             : "r"(sb + lane * 128 + ((c ^ (lane & 7)) << 4))
+                             : "r"(ob + lane * 128 + ((c ^ (lane & 7)) << 4))
                              : "memory");
 #pragma unroll
               for (int c = 0; c < 8; ++c) {
@@ -417,6 +439,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tma_kernel(const __grid_cons
             }
             fence_async_smem();
             __syncwarp();
+            if (ACC && lane == 0) issue_old(sc + 2);   // obuf (sc & 1) consumed: load box sc + 2 into it
             if (P.stat_part) {
               // column sums of the 32 staged rows (conflict-free: the swizzle
               // spreads a row's eight 16-byte chunks over all banks); rows past M are zero
@@ -661,10 +684,13 @@ int conv_mt() {
 
 template <int MODE, int BN, int NCH, int MT, int CG = 1>
 Status launch_mt(OpArgs& a, Params P, int* stat_slots = nullptr) {
-  constexpr int smem = tma_smem(BN / CG, MT, kblock(MODE));
+  int smem = tma_smem(BN / CG, MT, kblock(MODE));
   auto kern = conv_tma_kernel<MODE, BN, NCH, MT, CG, false>;
   if constexpr (MODE != WGRAD && NCH == 0)
-    if (P.accumulate && P.tstore) kern = conv_tma_kernel<MODE, BN, NCH, MT, CG, true>;
+    if (P.accumulate && P.tstore) {
+      kern = conv_tma_kernel<MODE, BN, NCH, MT, CG, true>;
+      smem = tma_smem(BN / CG, MT, kblock(MODE), true);
+    }
   static bool attr[2] = {false, false};
   const int ai = (P.accumulate && P.tstore) ? 1 : 0;
   if (!attr[ai]) {

@@ -14,7 +14,7 @@
 // dz = g·[out>0], dβ = Σdz, dγ = Σdz·x̂, dy = γ·rstd·(dz − dβ/n − x̂·dγ/n).
 // Algorithmic bytes per launch = one read of every input + one write of every
 // output (roofline: HBM).
-#include "common.cuh"
+#include "tc_util.cuh"
 
 namespace oc {
 
@@ -412,55 +412,120 @@ __global__ void bn_relu_pool(PoolGeom g, const T* __restrict__ y, const float* _
   }
 }
 
-// The stem geometry (3×3, stride 2, pad 1, bf16, C = 64) tiled: a block takes
-// 4 × 16 output pixels, stages their 9 × 33 input pixels in shared memory with
-// BN-ReLU applied and rounded once per element (padding as −inf, which never
-// wins the first-max rule), then each thread pools from shared memory — y is
-// read about once instead of 9 BN evaluations per output.
-constexpr int PT_P = 4, PT_Q = 16, PT_R = 2 * PT_P + 1, PT_C = 2 * PT_Q + 1;
-__global__ void __launch_bounds__(256) bn_relu_pool_tiled(PoolGeom g, const __nv_bfloat16* __restrict__ y,
-                                                          const float* __restrict__ stat,
-                                                          const float* __restrict__ gamma,
-                                                          const float* __restrict__ beta,
-                                                          __nv_bfloat16* __restrict__ out, uint8_t* __restrict__ idx) {
-  __shared__ uint4 tile[PT_R * PT_C * 8];
-  __shared__ float prm[4][64];
-  const int tq = (g.Q + PT_Q - 1) / PT_Q, tp = (g.P + PT_P - 1) / PT_P;
-  const int b = blockIdx.x;
-  const int n = b / (tp * tq), r0 = b % (tp * tq);
-  const int p0 = (r0 / tq) * PT_P, q0 = (r0 % tq) * PT_Q;
-  if (threadIdx.x < 64) {
-    prm[0][threadIdx.x] = gamma[threadIdx.x];
-    prm[1][threadIdx.x] = beta[threadIdx.x];
-    prm[2][threadIdx.x] = stat[threadIdx.x];
-    prm[3][threadIdx.x] = stat[64 + threadIdx.x];
-  }
+// ---- stem geometry (3×3 / stride 2 / pad 1 over an even H × W map, P = H/2,
+// Q = W/2) staged by whole image rows: NHWC makes an image row one contiguous
+// W·C·sizeof(T) run, so a block's operands arrive as a few 1-D bulk copies
+// (cp.async.bulk, completion on one mbarrier) — every byte in flight at once
+// without registers, which the per-thread 16-byte loads of the round-1
+// kernels (0.26-0.39 of HBM) did not reach.
+inline bool stem_pool(const PoolGeom& g) {
+  return g.r == 3 && g.st == 2 && g.pad == 1 && g.H % 2 == 0 && g.W % 2 == 0 && g.P == g.H / 2 && g.Q == g.W / 2;
+}
+constexpr int kRowSmemMax = 200 * 1024;
+template <typename T>
+inline bool rows_fit(const PoolGeom& g, int bytes) {
+  return stem_pool(g) && g.C % 8 == 0 && 256 % (g.C / 8) == 0 && ((size_t)g.Q * g.C) % 16 == 0 &&
+         ((size_t)g.W * g.C * sizeof(T)) % 16 == 0 && bytes <= kRowSmemMax;
+}
+template <typename T>
+inline int fwd_rows_smem(const PoolGeom& g) { return 3 * g.W * g.C * (int)sizeof(T) + 16; }
+// one stage of the backward: y rows 2i, 2i+1; gp and idx rows i, i+1
+template <typename T>
+__host__ __device__ inline int bwd_stage_bytes(const PoolGeom& g) {
+  return 2 * g.W * g.C * (int)sizeof(T) + 2 * g.Q * g.C * (int)sizeof(T) + 2 * g.Q * g.C;
+}
+
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(tcu::smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bar_init_one(uint64_t* bar) {
+  tcu::mbar_init(bar, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// out[n,p,q,c] = max over the 3×3 window of rnd(relu(bn(y))) (first max, row-major
+// taps, padding excluded); block = one output row p: input rows 2p−1..2p+1 are
+// bulk-loaded, BN-ReLU-rounded once per element in place (the missing row −1 as
+// −inf, which never wins the first-max rule), then pooled from shared memory
+template <typename T>
+__global__ void __launch_bounds__(256) bn_relu_pool_rows(PoolGeom g, const T* __restrict__ y,
+                                                         const float* __restrict__ stat,
+                                                         const float* __restrict__ gamma,
+                                                         const float* __restrict__ beta, T* __restrict__ out,
+                                                         uint8_t* __restrict__ idx) {
+  extern __shared__ __align__(128) uint8_t rsm[];
+  T* rows = reinterpret_cast<T*>(rsm);
+  const int C = g.C, gC = C / 8, W = g.W;
+  const int rowe = W * C;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(rsm + 3 * rowe * sizeof(T));
+  const int n = blockIdx.x / g.P, p = blockIdx.x % g.P, h0 = 2 * p - 1;
+  if (threadIdx.x == 0) bar_init_one(bar);
   __syncthreads();
-  const int h0 = 2 * p0 - 1, w0 = 2 * q0 - 1;
-  for (int e = threadIdx.x; e < PT_R * PT_C * 8; e += 256) {
-    const int cg = e & 7, pix = e >> 3;
-    const int h = h0 + pix / PT_C, w = w0 + pix % PT_C;
-    __nv_bfloat162 z2[4];
-    if (h >= 0 && h < g.H && w >= 0 && w < g.W) {
-      const V8 x = ld8(y + (((int64_t)n * g.H + h) * g.W + w) * 64 + cg * 8);
+  if (threadIdx.x == 0) {
+    const uint32_t rb = (uint32_t)(rowe * sizeof(T));
+    tcu::mbar_expect_tx(bar, (h0 < 0 ? 2u : 3u) * rb);
+    for (int r = h0 < 0 ? 1 : 0; r < 3; ++r)
+      bulk_load(tcu::smem_u32(rows) + r * rb, y + ((int64_t)n * g.H + h0 + r) * rowe, rb, bar);
+  }
+  const int cg = threadIdx.x % gC;   // fixed: 256 is a multiple of C/8
+  float gm[8], bt[8], mu[8], rs[8];
 #pragma unroll
-      for (int k = 0; k < 8; k += 2) {
-        const int c = cg * 8 + k;
-        const float a0 = fmaxf(fmaf(prm[0][c], (x.v[k] - prm[2][c]) * prm[3][c], prm[1][c]), 0.f);
-        const float a1 = fmaxf(fmaf(prm[0][c + 1], (x.v[k + 1] - prm[2][c + 1]) * prm[3][c + 1], prm[1][c + 1]), 0.f);
-        z2[k / 2] = __floats2bfloat162_rn(a0, a1);
-      }
+  for (int k = 0; k < 8; ++k) {
+    const int c = cg * 8 + k;
+    gm[k] = gamma[c]; bt[k] = beta[c]; mu[k] = stat[c]; rs[k] = stat[C + c];
+  }
+  tcu::mbar_wait(bar, 0);
+  for (int e = threadIdx.x; e < 3 * W * gC; e += 256) {
+    T* at = rows + (int64_t)e * 8;
+    V8 z;
+    if (h0 + e / (W * gC) >= 0) {
+      const V8 x = ld8(at);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) z.v[k] = fmaxf(fmaf(gm[k], (x.v[k] - mu[k]) * rs[k], bt[k]), 0.f);
     } else {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) z2[k] = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+      for (int k = 0; k < 8; ++k) z.v[k] = -INFINITY;
     }
-    tile[e] = *reinterpret_cast<uint4*>(z2);
+    st8(at, z);   // rounded to T once per element
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < PT_P * PT_Q * 8; e += 256) {
-    const int cg = e & 7, o = e >> 3;
-    const int p = p0 + o / PT_Q, q = q0 + o % PT_Q;
-    if (p >= g.P || q >= g.Q) continue;
+  for (int e = threadIdx.x; e < g.Q * gC; e += 256) {
+    const int q = e / gC;
+    const int64_t oo = (((int64_t)n * g.P + p) * g.Q + q) * C + cg * 8;
+    if constexpr (sizeof(T) == 2) {
+      // bf16 pairs: z > best as a 16-bit lane mask, max, and the tap index
+      // selected per lane (exact: comparisons of stored bf16 values), about a
+      // third of the instructions of the per-channel fp32 loop (the kernel is
+      // issue-bound, ncu: SM throughput 80 % at 0.35 of HBM)
+      __nv_bfloat162 best[4];
+      uint32_t bi[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) { best[k] = __floats2bfloat162_rn(-INFINITY, -INFINITY); bi[k] = 0; }
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+          const int w = 2 * q - 1 + v;
+          if (w < 0) continue;
+          const uint4 c4 = *reinterpret_cast<const uint4*>(rows + ((int64_t)u * W + w) * C + cg * 8);
+          const __nv_bfloat162* z2 = reinterpret_cast<const __nv_bfloat162*>(&c4);
+          const uint32_t tap2 = (uint32_t)(u * 3 + v) * 0x00010001u;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t m = __hgt2_mask(z2[k], best[k]);
+            best[k] = __hmax2(z2[k], best[k]);
+            bi[k] = (m & tap2) | (~m & bi[k]);
+          }
+        }
+      *reinterpret_cast<uint4*>(out + oo) = *reinterpret_cast<const uint4*>(best);
+      uint2 packed;
+      packed.x = __byte_perm(bi[0], bi[1], 0x6420);
+      packed.y = __byte_perm(bi[2], bi[3], 0x6420);
+      *reinterpret_cast<uint2*>(idx + oo) = packed;
+      continue;
+    }
     float best[8];
     uint8_t bi[8];
 #pragma unroll
@@ -469,20 +534,17 @@ __global__ void __launch_bounds__(256) bn_relu_pool_tiled(PoolGeom g, const __nv
     for (int u = 0; u < 3; ++u)
 #pragma unroll
       for (int v = 0; v < 3; ++v) {
-        const uint4 c4 = tile[((2 * (o / PT_Q) + u) * PT_C + 2 * (o % PT_Q) + v) * 8 + cg];
-        const __nv_bfloat162* z2 = reinterpret_cast<const __nv_bfloat162*>(&c4);
+        const int w = 2 * q - 1 + v;
+        if (w < 0) continue;
+        const V8 z = ld8(rows + ((int64_t)u * W + w) * C + cg * 8);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 f = __bfloat1622float2(z2[k]);
-          if (f.x > best[2 * k]) { best[2 * k] = f.x; bi[2 * k] = (uint8_t)(u * 3 + v); }
-          if (f.y > best[2 * k + 1]) { best[2 * k + 1] = f.y; bi[2 * k + 1] = (uint8_t)(u * 3 + v); }
-        }
+        for (int k = 0; k < 8; ++k)
+          if (z.v[k] > best[k]) { best[k] = z.v[k]; bi[k] = (uint8_t)(u * 3 + v); }
       }
-    V8 ov;
+    V8 o;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) ov.v[k] = best[k];
-    const int64_t oo = (((int64_t)n * g.P + p) * g.Q + q) * 64 + cg * 8;
-    st8(out + oo, ov);
+    for (int k = 0; k < 8; ++k) o.v[k] = best[k];
+    st8(out + oo, o);
     uint2 packed;
     packed.x = bi[0] | (bi[1] << 8) | (bi[2] << 16) | ((uint32_t)bi[3] << 24);
     packed.y = bi[4] | (bi[5] << 8) | (bi[6] << 16) | ((uint32_t)bi[7] << 24);
@@ -497,12 +559,15 @@ Status bn_relu_pool_fwd_t(OpArgs& a) {
   auto y = (const T*)a.p(RP_Y);
   if (!Ab(a, "stat_in")) OC_TRY(batch_stats<T>(a, (int64_t)g.N * g.H * g.W, g.C, y, (float*)a.p(RP_STAT)));
   const int64_t total = (int64_t)g.N * g.P * g.Q * (g.C / 8);
-  const char* et = std::getenv("OC_POOL_TILED");
-  if (sizeof(T) == 2 && g.C == 64 && g.r == 3 && g.st == 2 && g.pad == 1 && !(et && et[0] == '0')) {
-    const int64_t blocks = (int64_t)g.N * ((g.P + PT_P - 1) / PT_P) * ((g.Q + PT_Q - 1) / PT_Q);
-    bn_relu_pool_tiled<<<(unsigned)blocks, 256, 0, a.stream>>>(
-        g, (const __nv_bfloat16*)y, (const float*)a.p(RP_STAT), (const float*)a.p(RP_GAMMA),
-        (const float*)a.p(RP_BETA), (__nv_bfloat16*)a.p(RP_OUT), (uint8_t*)a.p(RP_IDX));
+  if (rows_fit<T>(g, fwd_rows_smem<T>(g))) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(bn_relu_pool_rows<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmemMax);
+      attr = true;
+    }
+    bn_relu_pool_rows<T><<<(unsigned)(g.N * g.P), 256, fwd_rows_smem<T>(g), a.stream>>>(
+        g, y, (const float*)a.p(RP_STAT), (const float*)a.p(RP_GAMMA), (const float*)a.p(RP_BETA), (T*)a.p(RP_OUT),
+        (uint8_t*)a.p(RP_IDX));
     OC_LAUNCH_CHECK(a);
     return Status::ok();
   }
@@ -740,29 +805,55 @@ __global__ void __launch_bounds__(256) pbn_apply(PoolGeom g, const T* __restrict
   }
 }
 
-// 3×3 / stride-2 / pad-1 pool over an even H × W map (the stem): a thread
-// owns the 2×2 input block (2i..2i+1, 2j..2j+1) × 8 channels, which only the
-// windows (i|i+1, j|j+1) reach; each window's argmax tap lands in at most one
-// of the four pixels.  Windows are visited in (p, q) ascending order, the order
-// pooled_grad8 sums them in, so the routed gradients are bitwise the same.
+// Backward of the stem's BN-ReLU-maxpool, staged by image row pairs: unit
+// (n, i) = input rows 2i, 2i+1, which only the windows of pooled rows i and
+// i+1 reach.  A stage holds the two y rows, and gp / idx rows i, i+1 (row i+1
+// absent for the last pair).  Thread item (j, cg) owns the 2×2 input block
+// (2i..2i+1, 2j..2j+1) × 8 channels; windows are visited in (p, q) ascending
+// order — the order pooled_grad8 sums them in, so the routed gradients are
+// bitwise those of the generic kernels.
 template <typename T>
-__device__ __forceinline__ void pool_block_grad(const PoolGeom& g, int n, int i, int j, int cg, const T* __restrict__ gp,
-                                                const uint8_t* __restrict__ idx, float ga[4][8]) {
+struct RowStage {
+  T* y;          // [2][W][C]
+  T* gp;         // [2][Q][C]
+  uint8_t* ix;   // [2][Q][C]
+  __device__ RowStage(uint8_t* base, const PoolGeom& g) {
+    y = reinterpret_cast<T*>(base);
+    gp = y + 2 * g.W * g.C;
+    ix = reinterpret_cast<uint8_t*>(gp + 2 * g.Q * g.C);
+  }
+};
+// thread 0: bulk loads of unit u = n·P + i into the stage, completion on bar
+template <typename T>
+__device__ __forceinline__ void issue_rows(const PoolGeom& g, int64_t u, const RowStage<T>& s, uint64_t* bar,
+                                           const T* __restrict__ y, const T* __restrict__ gp,
+                                           const uint8_t* __restrict__ idx) {
+  const int i = (int)(u % g.P);
+  const int two = i + 1 < g.P ? 2 : 1;
+  const uint32_t yb = 2u * g.W * g.C * sizeof(T), gb = (uint32_t)(g.Q * g.C * sizeof(T)), ib = (uint32_t)(g.Q * g.C);
+  tcu::mbar_expect_tx(bar, yb + two * (gb + ib));
+  bulk_load(tcu::smem_u32(s.y), y + u * 2 * g.W * g.C, yb, bar);   // rows 2i, 2i+1 of image n = rows 2u, 2u+1
+  bulk_load(tcu::smem_u32(s.gp), gp + u * g.Q * g.C, two * gb, bar);
+  bulk_load(tcu::smem_u32(s.ix), idx + u * g.Q * g.C, two * ib, bar);
+}
+// routed gradient of the 2×2 block (2i.., 2j..) from the staged windows (rows i, i+1)
+template <typename T>
+__device__ __forceinline__ void block_grad_smem(const PoolGeom& g, bool last_row, int j, int cg,
+                                                const RowStage<T>& s, float ga[4][8]) {
 #pragma unroll
   for (int px = 0; px < 4; ++px)
 #pragma unroll
     for (int k = 0; k < 8; ++k) ga[px][k] = 0.f;
 #pragma unroll
   for (int wi = 0; wi < 2; ++wi) {
-    const int p = i + wi;
-    if (p >= g.P) continue;
+    if (wi == 1 && last_row) continue;
 #pragma unroll
     for (int wj = 0; wj < 2; ++wj) {
       const int q = j + wj;
       if (q >= g.Q) continue;
-      const int64_t oo = (((int64_t)n * g.P + p) * g.Q + q) * g.C + cg * 8;
-      const uint2 packed = *reinterpret_cast<const uint2*>(idx + oo);
-      const V8 gv = ld8(gp + oo);
+      const int o = (wi * g.Q + q) * g.C + cg * 8;
+      const uint2 packed = *reinterpret_cast<const uint2*>(s.ix + o);
+      const V8 gv = ld8(s.gp + o);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t tap = ((k < 4 ? packed.x : packed.y) >> (8 * (k & 3))) & 0xff;
@@ -780,43 +871,48 @@ __device__ __forceinline__ void pool_block_grad(const PoolGeom& g, int n, int i,
     for (int k = 0; k < 8; ++k) ga[px][k] = rnd<T>(ga[px][k]);
 }
 
-inline bool stem_pool(const PoolGeom& g) {
-  return g.r == 3 && g.st == 2 && g.pad == 1 && g.H % 2 == 0 && g.W % 2 == 0 && g.P == g.H / 2 && g.Q == g.W / 2;
-}
-
+// dγ, dβ partials: grid = stat_blocks(rows) persistent blocks, each over a
+// contiguous chunk of row pairs through a two-stage ring (the next pair's
+// copies in flight while this one is reduced); fixed chunking and fixed-order
+// block sums keep the result bitwise reproducible
 template <typename T>
-__global__ void __launch_bounds__(256) pbn_partial_blk(PoolGeom g, const T* __restrict__ gp,
-                                                       const uint8_t* __restrict__ idx, const T* __restrict__ y,
-                                                       const float* __restrict__ stat,
-                                                       const float* __restrict__ gamma,
-                                                       const float* __restrict__ beta, float* __restrict__ part) {
+__global__ void __launch_bounds__(256, 2) pbn_partial_rows(PoolGeom g, const T* __restrict__ gp,
+                                                        const uint8_t* __restrict__ idx, const T* __restrict__ y,
+                                                        const float* __restrict__ stat,
+                                                        const float* __restrict__ gamma,
+                                                        const float* __restrict__ beta, float* __restrict__ part) {
+  extern __shared__ __align__(128) uint8_t rsm[];
   const int C = g.C, gC = C / 8, tpr = 256 / gC;
-  const int t = threadIdx.x, cg = t % gC, rr = t / gC;
-  const int64_t units = (int64_t)g.N * g.P * g.Q;           // 2×2 input blocks
+  const int t = threadIdx.x, cg = t % gC;
+  const int sb = bwd_stage_bytes<T>(g);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(rsm + 2 * sb);
+  const int64_t units = (int64_t)g.N * g.P;
   const int64_t chunk = (units + gridDim.x - 1) / gridDim.x;
   const int64_t u0 = blockIdx.x * chunk, u1 = min(units, u0 + chunk);
+  if (t == 0) { bar_init_one(&bar[0]); bar_init_one(&bar[1]); }
+  __syncthreads();
+  if (t == 0)
+    for (int k = 0; k < 2; ++k)
+      if (u0 + k < u1) issue_rows<T>(g, u0 + k, RowStage<T>(rsm + k * sb, g), &bar[k], y, gp, idx);
   float s[8] = {}, q[8] = {};
   float mu[8], rs[8], gm[8], bt[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const int c = (cg * 8 + k) % C;
-    mu[k] = stat[c];
-    rs[k] = stat[C + c];
-    gm[k] = gamma[c];
-    bt[k] = beta[c];
+    const int c = cg * 8 + k;
+    mu[k] = stat[c]; rs[k] = stat[C + c]; gm[k] = gamma[c]; bt[k] = beta[c];
   }
-  if (rr < tpr)
-    for (int64_t u = u0 + rr; u < u1; u += tpr) {
-      const uint32_t t1 = g.fQ.div((uint32_t)u);
-      const int j = (int)((uint32_t)u - t1 * g.Q);
-      const uint32_t n = g.fP.div(t1);
-      const int i = (int)(t1 - n * g.P);
+  for (int64_t u = u0; u < u1; ++u) {
+    const int k2 = (int)((u - u0) & 1);
+    tcu::mbar_wait(&bar[k2], (uint32_t)(((u - u0) >> 1) & 1));
+    const RowStage<T> S(rsm + k2 * sb, g);
+    const bool last_row = (int)(u % g.P) + 1 >= g.P;
+    for (int e = t; e < g.Q * gC; e += 256) {
+      const int j = e / gC;
       float ga[4][8];
-      pool_block_grad<T>(g, (int)n, i, j, cg, gp, idx, ga);
+      block_grad_smem<T>(g, last_row, j, cg, S, ga);
 #pragma unroll
       for (int px = 0; px < 4; ++px) {
-        const int64_t o = (((int64_t)n * g.H + 2 * i + (px >> 1)) * g.W + 2 * j + (px & 1)) * C + cg * 8;
-        const V8 yv = ld8(y + o);
+        const V8 yv = ld8(S.y + ((px >> 1) * g.W + 2 * j + (px & 1)) * C + cg * 8);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const float xh = (yv.v[k] - mu[k]) * rs[k];
@@ -827,7 +923,13 @@ __global__ void __launch_bounds__(256) pbn_partial_blk(PoolGeom g, const T* __re
         }
       }
     }
-  extern __shared__ float sm[];
+    __syncthreads();   // stage k2 fully read
+    if (t == 0 && u + 2 < u1) {
+      tcu::fence_async_smem();
+      issue_rows<T>(g, u + 2, S, &bar[k2], y, gp, idx);
+    }
+  }
+  float* sm = reinterpret_cast<float*>(rsm);   // the stages are idle now
 #pragma unroll
   for (int k = 0; k < 8; ++k) { sm[t * 16 + k] = s[k]; sm[t * 16 + 8 + k] = q[k]; }
   __syncthreads();
@@ -843,50 +945,66 @@ __global__ void __launch_bounds__(256) pbn_partial_blk(PoolGeom g, const T* __re
   }
 }
 
-// (256, 3): 80 registers instead of 121 — three blocks per SM; measured 8 % faster
-// despite a small stack spill (the same bound made pbn_partial_blk 27 % slower)
+// dy = γ·rstd·(dz − dβ/n − x̂·dγ/n) written over y: persistent blocks over
+// contiguous chunks of row pairs through the same two-stage ring; a block
+// reads only its own staged copy of its rows of y, so the in-place global
+// write never races a reader
 template <typename T>
-__global__ void __launch_bounds__(256, 3) pbn_apply_blk(PoolGeom g, const T* __restrict__ gp,
-                                                     const uint8_t* __restrict__ idx, T* y,
-                                                     const float* __restrict__ stat, const float* __restrict__ gamma,
-                                                     const float* __restrict__ beta, const float* __restrict__ dgamma,
-                                                     const float* __restrict__ dbeta, float inv_n) {
-  const int C = g.C, gC = C / 8, tpr = 256 / gC;
-  const int cg = threadIdx.x % gC, rr = threadIdx.x / gC;
-  if (rr >= tpr) return;
+__global__ void __launch_bounds__(256, 2) pbn_apply_rows(PoolGeom g, const T* __restrict__ gp,
+                                                         const uint8_t* __restrict__ idx, T* y,
+                                                         const float* __restrict__ stat,
+                                                         const float* __restrict__ gamma,
+                                                         const float* __restrict__ beta,
+                                                         const float* __restrict__ dgamma,
+                                                         const float* __restrict__ dbeta, float inv_n) {
+  extern __shared__ __align__(128) uint8_t rsm[];
+  const int C = g.C, gC = C / 8;
+  const int t = threadIdx.x, cg = t % gC;
+  const int sb = bwd_stage_bytes<T>(g);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(rsm + 2 * sb);
+  const int64_t units = (int64_t)g.N * g.P;
+  const int64_t chunk = (units + gridDim.x - 1) / gridDim.x;
+  const int64_t u0 = blockIdx.x * chunk, u1 = min(units, u0 + chunk);
+  if (t == 0) { bar_init_one(&bar[0]); bar_init_one(&bar[1]); }
+  __syncthreads();
+  if (t == 0)
+    for (int k = 0; k < 2; ++k)
+      if (u0 + k < u1) issue_rows<T>(g, u0 + k, RowStage<T>(rsm + k * sb, g), &bar[k], y, gp, idx);
   float mu[8], rs[8], gm[8], bt[8], dg[8], db[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int c = cg * 8 + k;
-    mu[k] = stat[c];
-    rs[k] = stat[C + c];
-    gm[k] = gamma[c];
-    bt[k] = beta[c];
-    dg[k] = dgamma[c];
-    db[k] = dbeta[c];
+    mu[k] = stat[c]; rs[k] = stat[C + c]; gm[k] = gamma[c]; bt[k] = beta[c]; dg[k] = dgamma[c]; db[k] = dbeta[c];
   }
-  const int64_t units = (int64_t)g.N * g.P * g.Q;
-  const int64_t stride = (int64_t)gridDim.x * tpr;
-  for (int64_t u = (int64_t)blockIdx.x * tpr + rr; u < units; u += stride) {
-    const uint32_t t1 = g.fQ.div((uint32_t)u);
-    const int j = (int)((uint32_t)u - t1 * g.Q);
-    const uint32_t n = g.fP.div(t1);
-    const int i = (int)(t1 - n * g.P);
-    float ga[4][8];
-    pool_block_grad<T>(g, (int)n, i, j, cg, gp, idx, ga);
+  for (int64_t u = u0; u < u1; ++u) {
+    const int k2 = (int)((u - u0) & 1);
+    tcu::mbar_wait(&bar[k2], (uint32_t)(((u - u0) >> 1) & 1));
+    const RowStage<T> S(rsm + k2 * sb, g);
+    const bool last_row = (int)(u % g.P) + 1 >= g.P;
+    T* yo = y + u * 2 * g.W * C;
+    for (int e = t; e < g.Q * gC; e += 256) {
+      const int j = e / gC;
+      float ga[4][8];
+      block_grad_smem<T>(g, last_row, j, cg, S, ga);
 #pragma unroll
-    for (int px = 0; px < 4; ++px) {
-      const int64_t o = (((int64_t)n * g.H + 2 * i + (px >> 1)) * g.W + 2 * j + (px & 1)) * C + cg * 8;
-      const V8 yv = ld8(y + o);
-      V8 dy;
+      for (int px = 0; px < 4; ++px) {
+        const int o = ((px >> 1) * g.W + 2 * j + (px & 1)) * C + cg * 8;
+        const V8 yv = ld8(S.y + o);
+        V8 dy;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float xh = (yv.v[k] - mu[k]) * rs[k];
-        const float z = fmaf(gm[k], xh, bt[k]);
-        const float dz = z > 0.f ? ga[px][k] : 0.f;
-        dy.v[k] = gm[k] * rs[k] * (dz - db[k] * inv_n - xh * dg[k] * inv_n);
+        for (int k = 0; k < 8; ++k) {
+          const float xh = (yv.v[k] - mu[k]) * rs[k];
+          const float z = fmaf(gm[k], xh, bt[k]);
+          const float dz = z > 0.f ? ga[px][k] : 0.f;
+          dy.v[k] = gm[k] * rs[k] * (dz - db[k] * inv_n - xh * dg[k] * inv_n);
+        }
+        st8(yo + o, dy);
       }
-      st8(y + o, dy);   // in place: each thread reads only its own four pixels of y
+    }
+    __syncthreads();   // stage k2 fully read
+    if (t == 0 && u + 2 < u1) {
+      tcu::fence_async_smem();
+      issue_rows<T>(g, u + 2, S, &bar[k2], y, gp, idx);
     }
   }
 }
@@ -898,10 +1016,17 @@ Status pool_bn_bwd_reduce_t(OpArgs& a) {
   const int64_t rows = (int64_t)g.N * g.H * g.W;
   const int nblk = stat_blocks(rows);
   if (a.ws_bytes < (size_t)nblk * 2 * g.C * 4) return Status::make(OC_E_INVARIANT, "pool_bn_bwd: workspace too small");
-  if (stem_pool(g))
-    pbn_partial_blk<T><<<nblk, 256, 256 * 16 * 4, a.stream>>>(
+  const int sb2 = 2 * bwd_stage_bytes<T>(g) + 16;
+  if (rows_fit<T>(g, sb2) && 256 * 16 * 4 <= sb2) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(pbn_partial_rows<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmemMax);
+      attr = true;
+    }
+    pbn_partial_rows<T><<<nblk, 256, sb2, a.stream>>>(
         g, (const T*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX), (const T*)a.p(PB_Y), (const float*)a.p(PB_STAT),
         (const float*)a.p(PB_GAMMA), (const float*)a.p(PB_BETA), (float*)a.ws);
+  }
   else
     pbn_partial<T><<<nblk, 256, 256 * 16 * 4, a.stream>>>(
         g, (const T*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX), (const T*)a.p(PB_Y), (const float*)a.p(PB_STAT),
@@ -917,11 +1042,19 @@ Status pool_bn_bwd_apply_t(OpArgs& a) {
   PoolGeom g = geom(a);
   const int64_t rows = (int64_t)g.N * g.H * g.W;
   if (g.C % 8 || g.C > 2048) return Status::make(OC_E_UNSUPPORTED, "pool_bn: C must be a multiple of 8 and <= 2048");
-  if (stem_pool(g))
-    pbn_apply_blk<T><<<rowgroup_blocks(rows / 4, g.C), 256, 0, a.stream>>>(
+  const int sb1 = 2 * bwd_stage_bytes<T>(g) + 16;
+  if (rows_fit<T>(g, sb1)) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(pbn_apply_rows<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmemMax);
+      attr = true;
+    }
+    const int64_t units = (int64_t)g.N * g.P;
+    pbn_apply_rows<T><<<(unsigned)std::min<int64_t>(units, 2 * 148), 256, sb1, a.stream>>>(
         g, (const T*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX), (T*)a.p(PB_Y), (const float*)a.p(PB_STAT),
         (const float*)a.p(PB_GAMMA), (const float*)a.p(PB_BETA), (const float*)a.p(PB_DGAMMA),
         (const float*)a.p(PB_DBETA), 1.f / (float)rows);
+  }
   else
     pbn_apply<T><<<rowgroup_blocks(rows, g.C), 256, 0, a.stream>>>(
         g, (const T*)a.p(PB_G), (const uint8_t*)a.p(PB_IDX), (T*)a.p(PB_Y), (const float*)a.p(PB_STAT),

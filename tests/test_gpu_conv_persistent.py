@@ -200,8 +200,9 @@ def _pool_graph(N, H, W, C):
 @pytest.mark.gpu
 @pytest.mark.parametrize("shape", [(16, 112, 112, 64), (3, 37, 23, 64)])
 def test_bn_relu_pool_tiled(shape):
-    """The stem's fused BN-apply + ReLU + 3x3/2 max pool (bn_relu_pool_tiled,
-    the C = 64 bf16 hot-path kernel) against the definition: BN with the given
+    """The stem's fused BN-apply + ReLU + 3x3/2 max pool (bn_relu_pool_rows,
+    the row-staged hot-path kernel, for the even 112^2 map; the generic kernel
+    for the odd one) against the definition: BN with the given
     batch statistics (fp32 [mu; rstd]), ReLU, bf16 storage rounding, max over
     the window, first maximum in row-major tap order (oracle maxpool).  The
     kernel evaluates gamma*(y-mu)*rstd+beta in fp32, the oracle in fp64, so a
@@ -261,3 +262,75 @@ def test_stem_at_the_r50_bench_batch_sampled():
         ref = nm.round_bf16(nm.conv2d(x[n:n + 1].float().numpy().astype(np.float64), wr, 2, 3))
         got = T._from_bits(y[n], (1, P, Q, K))
         assert nm.rel_l2(got, ref) < TOL_BF16, n
+
+
+# -------------------------------------------------- stem BN-ReLU-maxpool backward (row-staged kernels)
+def _pool_bwd_graph(kind, N, H, W, C):
+    P, Q = (H + 2 - 3) // 2 + 1, (W + 2 - 3) // 2 + 1
+    v = lambda n, b: {"id": n, "bytes": int(b), "pinned": True}
+    vars_ = [v("g", N * P * Q * C * 2), v("idx", N * P * Q * C), v("y", N * H * W * C * 2), v("stat", 2 * C * 4),
+             v("gamma", C * 4), v("beta", C * 4), v("dgamma", C * 4), v("dbeta", C * 4)]
+    attrs = {"dtype": "bf16", "N": N, "H": H, "W": W, "C": C, "r": 3, "stride": 2, "pad": 1, "P": P, "Q": Q}
+    args = {k: k for k in ("g", "idx", "y", "stat", "gamma", "beta", "dgamma", "dbeta")}
+    if kind == "reduce":
+        fn = {"id": "f", "in": ["g", "idx", "y", "stat", "gamma", "beta"], "out": ["dgamma", "dbeta"],
+              "op": {"kind": "pool_bn_bwd_reduce", "args": args, "attrs": attrs}}
+    else:
+        fn = {"id": "f", "in": ["g", "idx", "y", "stat", "gamma", "beta", "dgamma", "dbeta"], "out": ["y"],
+              "op": {"kind": "pool_bn_bwd_apply", "args": args, "attrs": attrs}}
+    return json.dumps({"variables": vars_, "functions": [fn]}), (P, Q), sum(x["bytes"] for x in vars_), attrs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(32, 112, 112, 64), (3, 20, 36, 64), (2, 21, 23, 64)])
+def test_pool_bn_backward(shape):
+    """The stem's BN-ReLU-maxpool backward (pool_bn_bwd_reduce: dgamma, dbeta;
+    pool_bn_bwd_apply: dy over y) against oracle/layerwise.py's definitions on
+    the same bf16 inputs, argmax taps from the oracle's own forward pool.  The
+    even stem shapes run the row-staged kernels (bulk-copied row pairs through
+    a two-stage ring; 32 × 112² gives every persistent block several row pairs,
+    so the ring's phases wrap), the odd shape the generic kernels.  bf16
+    tolerance 1e-3 relative L2 (north_star)."""
+    from oracle import layerwise as LW
+    from paper_2010_14109_b200.runtime import OutOfCoreStep
+    N, H, W, C = shape
+    rng = np.random.default_rng(23)
+    y = T.bf(rng.standard_normal((N, H, W, C)) * 1.5 + 0.3)
+    yf = y.float().numpy().astype(np.float64)
+    mu = yf.reshape(-1, C).mean(0)
+    rstd = 1.0 / np.sqrt(yf.reshape(-1, C).var(0) + nm.BN_EPS)
+    stat = np.stack([mu, rstd]).astype(np.float32)
+    gamma = (1.0 + 0.1 * rng.standard_normal(C)).astype(np.float32)
+    beta = (0.1 * rng.standard_normal(C)).astype(np.float32)
+    st64 = stat.astype(np.float64)
+    z = nm.round_bf16(np.maximum(gamma * (yf - st64[0]) * st64[1] + beta, 0.0))
+    _, arg = nm.maxpool(z, 3, 2, 1)
+    P, Q = arg.shape[1:3]
+    g = T.bf(rng.standard_normal((N, P, Q, C)))
+    gf = g.float().numpy().astype(np.float64)
+    ins = {"g": gf, "idx": arg.astype(np.uint8), "y": yf, "stat": st64, "gamma": gamma.astype(np.float64),
+           "beta": beta.astype(np.float64)}
+    doc, _, total, attrs = _pool_bwd_graph("reduce", N, H, W, C)
+    ref = LW.apply("pool_bn_bwd_reduce", attrs, ins)
+    s = OutOfCoreStep(doc, total, 0, mode="best", phys_bytes=4096)
+    for k, a in (("g", T._bits(g)), ("idx", arg.astype(np.uint8)), ("y", T._bits(y)), ("stat", stat),
+                 ("gamma", gamma), ("beta", beta)):
+        s.write(k, a)
+    s.step()
+    dgamma, dbeta = s.read("dgamma", np.float32), s.read("dbeta", np.float32)
+    s.close()
+    assert nm.rel_l2(dgamma, ref["dgamma"]) < TOL_BF16
+    assert nm.rel_l2(dbeta, ref["dbeta"]) < TOL_BF16
+    # apply, from the oracle's dgamma / dbeta (the kernel is tested on its own)
+    dg32, db32 = ref["dgamma"].astype(np.float32), ref["dbeta"].astype(np.float32)
+    doc, _, total, attrs = _pool_bwd_graph("apply", N, H, W, C)
+    ref_dy = LW.apply("pool_bn_bwd_apply", attrs, dict(ins, dgamma=dg32.astype(np.float64),
+                                                         dbeta=db32.astype(np.float64)))["y"]
+    s = OutOfCoreStep(doc, total, 0, mode="best", phys_bytes=4096)
+    for k, a in (("g", T._bits(g)), ("idx", arg.astype(np.uint8)), ("y", T._bits(y)), ("stat", stat),
+                 ("gamma", gamma), ("beta", beta), ("dgamma", dg32), ("dbeta", db32)):
+        s.write(k, a)
+    s.step()
+    dy = T._from_bits(s.read("y", np.uint16), (N, H, W, C))
+    s.close()
+    assert nm.rel_l2(dy, ref_dy.reshape(N, H, W, C)) < TOL_BF16

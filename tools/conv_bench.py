@@ -46,6 +46,10 @@ def graph(kind, s):
     elif kind == "dgrad":
         vs, args, ins, outs = [v("dy", ys), v("w", ws), v("dx", xs)], {"dy": "dy", "w": "w", "dx": "dx"}, ["dy", "w"], ["dx"]
         op = "conv_dgrad"
+    elif kind == "dgrad_acc":   # dx = rnd(dx + dgrad): the residual-gradient accumulation of a bottleneck
+        vs, args, ins, outs = [v("dy", ys), v("w", ws), v("dx", xs)], {"dy": "dy", "w": "w", "dx": "dx"}, ["dy", "w", "dx"], ["dx"]
+        op = "conv_dgrad"
+        at = dict(at, accumulate=True)
     else:
         vs, args, ins, outs = [v("dy", ys), v("x", xs), v("dw", ws)], {"dy": "dy", "x": "x", "dw": "dw"}, ["dy", "x"], ["dw"]
         op = "conv_wgrad"
@@ -67,7 +71,7 @@ def main():
     peak = peaks.get("bf16_tflops", 1642.7)
     for name in a.shapes.split(","):
         for kind in a.passes.split(","):
-            if name.startswith("stem") and kind == "dgrad":
+            if name.startswith("stem") and kind.startswith("dgrad"):
                 continue
             doc, total, flops = graph(kind, SHAPES_ALL[name])
             st = OutOfCoreStep(doc, total, 0, mode="best", phys_bytes=4096)
@@ -75,7 +79,7 @@ def main():
             for vname, t in st.dev.items():
                 if vname in ("w",):
                     t.view(torch.float32).copy_(torch.from_numpy(rng.standard_normal(t.numel() // 4).astype(np.float32) * 0.05))
-                elif vname in ("x", "dy"):
+                elif vname in ("x", "dy", "dx"):
                     t.view(torch.bfloat16).copy_(torch.from_numpy(rng.standard_normal(t.numel() // 2).astype(np.float32)))
             st.step()
             ms = float(np.median([st.step()["step_ms"] for _ in range(a.reps)]))
