@@ -401,6 +401,61 @@ def conv_flops(doc):
     return fl
 
 
+def _union(iv):
+    out = []
+    for a, b in sorted(iv):
+        if out and a <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], b)
+        else:
+            out.append([a, b])
+    return out
+
+
+def compute_under_transfer(tl):
+    """|T ∩ C| / |C| of one instrumented step's timeline: the share of the
+    compute time that runs while a transfer is in flight (the executor's
+    overlap_frac is the other ratio, |T ∩ C| / |T|)."""
+    C = _union([(e["t0"], e["t1"]) for e in tl if e["stream"] == "compute"])
+    T = _union([(e["t0"], e["t1"]) for e in tl if e["stream"] in ("h2d", "d2h")])
+    inter, j = 0.0, 0
+    for a, b in C:
+        while j < len(T) and T[j][1] <= a:
+            j += 1
+        k = j
+        while k < len(T) and T[k][0] < b:
+            inter += max(0.0, min(b, T[k][1]) - max(a, T[k][0]))
+            k += 1
+    c = sum(b - a for a, b in C)
+    return inter / c if c > 0 else None
+
+
+def conv_bytes(doc):
+    """Algorithmic HBM bytes per convolution function: one read of each
+    operand and one write of the result (bf16 activations and weights, fp32
+    weight gradient), plus one read of the result when the epilogue
+    accumulates into it."""
+    d = json.loads(doc)
+    out = {}
+    for f in d["functions"]:
+        op = f.get("op") or {}
+        a = op.get("attrs", {})
+        k = op.get("kind")
+        if k not in ("conv_fwd", "conv_dgrad", "conv_wgrad"):
+            continue
+        e = 2 if a.get("dtype", "bf16") == "bf16" else 4
+        x = a["N"] * a["H"] * a["W"] * a["C"] * e
+        y = a["N"] * a["P"] * a["Q"] * a["K"] * e
+        w = a["K"] * a["R"] * a["S"] * a["C"]
+        acc = 1 if a.get("accumulate") else 0
+        if k == "conv_fwd":
+            out[f["id"]] = x + w * e + y * (1 + acc)
+        elif k == "conv_dgrad":
+            out[f["id"]] = y + w * e + x * (1 + acc)
+        else:
+            out[f["id"]] = y + x + w * 4
+    return out
+
+
 def attn_bytes(doc):
     """Algorithmic HBM bytes per attention function (bf16 tensor-core path,
     DESIGN.md §7): forward P written and read (bf16; the scores are recomputed,
@@ -688,6 +743,7 @@ def run_ours(args, rank, world):
     e2e = B_glob * args.steps / (wall_ms / 1e3)
     step_ms = dev_ms / args.steps
     overlap = float(np.mean([m["overlap_frac"] for m in mets_i]))
+    cut = compute_under_transfer(tl)
     h2d_busy = float(np.mean([m["h2d_busy_ms"] for m in mets_i]))
     d2h_busy = float(np.mean([m["d2h_busy_ms"] for m in mets_i]))
     comp_busy = float(np.mean([m["compute_busy_ms"] for m in mets_i]))
@@ -705,7 +761,13 @@ def run_ours(args, rank, world):
     # dominant contraction kernel from the per-function CUDA events of the instrumented pass
     fl = conv_flops(doc)
     abytes = attn_bytes(doc)
+    cbytes = conv_bytes(doc)
     per_kind = {}
+    per_launch = {}   # kind -> [Σ max(FLOPs/tensor peak, bytes/HBM peak) s, Σ measured s, Σ HBM-bound s]
+    per_shape = {}
+    fattrs = {f["id"]: (f.get("op") or {}).get("attrs", {}) for f in json.loads(doc)["functions"]}
+    pk_ = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     for ev in tl:
         if ev["stream"] != "compute" or ev["id"] not in fl:
             continue
@@ -714,6 +776,22 @@ def run_ours(args, rank, world):
             f = abytes[ev["id"]]   # HBM-bound on the tensor-core path: bytes, not FLOPs
         a = per_kind.setdefault(kind, [0.0, 0.0, 0, 0.0, []])
         a[0] += f
+        if ev["id"] in cbytes and spec["mode"] == "bf16":
+            t_tc_ = f / (pk_.get("bf16_tflops_sustained", 1395.5) * 1e12)
+            t_hbm_ = cbytes[ev["id"]] / (pk_.get("hbm_gbs", 6549.8) * 1e9)
+            pl = per_launch.setdefault(kind, [0.0, 0.0, 0.0])
+            pl[0] += max(t_tc_, t_hbm_)
+            pl[1] += (ev.get("k_span_ms") or ev.get("k_ms") or (ev["t1"] - ev["t0"])) / 1e3
+            pl[2] += t_hbm_ if t_hbm_ > t_tc_ else 0.0
+            at_ = fattrs[ev["id"]]
+            key_ = f'{at_["C"]}>{at_["K"]} {at_["R"]}x{at_["S"]}/{at_["stride"]} {at_["H"]}x{at_["W"]}' + \
+                (" acc" if at_.get("accumulate") else "")
+            sh = per_shape.setdefault(kind, {}).setdefault(key_, [0.0, 0.0, 0.0, 0.0, 0])
+            sh[0] += (ev.get("k_span_ms") or ev.get("k_ms") or (ev["t1"] - ev["t0"])) / 1e3
+            sh[1] += f
+            sh[2] += cbytes[ev["id"]]
+            sh[3] += max(t_tc_, t_hbm_)
+            sh[4] += 1
         if ev.get("k_n"):
             # in-kernel span (%globaltimer, first CTA start to last CTA end) when probed, else the events
             a[1] += (ev.get("k_span_ms") or ev["k_ms"]) / 1e3
@@ -768,6 +846,17 @@ def run_ours(args, rank, world):
                     "timed": "in-kernel %globaltimer span of each contraction launch (first CTA start to last CTA "
                              "end) in the instrumented pass, operand re-layout kernels excluded",
                     "achieved_event_timed": flops / ev_secs / 1e12 if ev_secs else None,
+                    "per_launch_roofline": None if kind not in per_launch else {
+                        "frac": per_launch[kind][0] / per_launch[kind][1],
+                        "hbm_bound_share_of_bound_time": per_launch[kind][2] / per_launch[kind][0],
+                        "definition": "Σ over this kind's launches of max(FLOPs / sustained bf16 peak, algorithmic "
+                                      "bytes / HBM peak) ÷ Σ of their measured spans: short-reduction 1x1 "
+                                      "convolutions are HBM-bound, so `frac` (FLOP rate ÷ tensor peak) "
+                                      "understates how close the kind runs to its roofline"},
+                    "by_shape": None if kind not in per_shape else [
+                        {"shape": k_, "launches": v_[4], "ms": v_[0] * 1e3, "tflops": v_[1] / v_[0] / 1e12,
+                         "gbs": v_[2] / v_[0] / 1e9, "frac_of_roofline": v_[3] / v_[0]}
+                        for k_, v_ in sorted(per_shape[kind].items(), key=lambda kv: -kv[1][0])[:12]],
                     "sm_mhz_in_kernels": float(np.median(mhz)) if mhz else None,
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"}
     total_flops = sum(f for (_, f) in fl.values())
@@ -809,6 +898,9 @@ def run_ours(args, rank, world):
                       "pcie5_x16_gbs_per_dir": PCIE5_X16_GBS, "measured_pinned_gbs": link,
                       "nvml_pcie_counters": pcie.summary(), "per_copy": copy_diag},
         "overlap_pct": 100 * overlap,
+        "overlap_definition": "|transfer ∩ compute| / |transfer| (executor timeline unions); the compute side "
+                              "is compute_under_transfer_pct",
+        "compute_under_transfer_pct": None if cut is None else 100 * cut,
         "makespan_model": {"predicted_ms": sim["makespan_ms"], "predicted_boundary_ms": sim0["makespan_ms"],
                            "compute_ms": sim["compute_ms"], "stall_ms": sim["stall_ms"],
                            "link_gbs": {"h2d": bw_h, "d2h": bw_d, "source": "bytes / busy copy time of the "

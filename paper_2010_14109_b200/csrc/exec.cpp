@@ -199,11 +199,6 @@ struct Exec {
   const Schedule* s = nullptr;
   MemPool* mem = nullptr;
   cudaStream_t cs = nullptr, hs = nullptr, ds = nullptr;
-  // optional second copy stream per direction (OC_COPY_STREAMS=2): consecutive
-  // transfers alternate between the two, so one copy's setup overlaps the
-  // previous copy; every dependency is an explicit event, so order is free
-  cudaStream_t hs2 = nullptr, ds2 = nullptr;
-  cudaEvent_t ev_join[2] = {nullptr, nullptr};
   oc_exec_options opt{};
   std::vector<XVar> vars;
   std::vector<XFn> fns;
@@ -278,12 +273,6 @@ Status Exec::create(int dev, const Graph* graph, const Schedule* sch, MemPool* m
   ds = (cudaStream_t)st.d2h;
   if (o) opt = *o;
   OC_CUDA(cudaSetDevice(dev));
-  if (const char* e = std::getenv("OC_COPY_STREAMS"); e && e[0] == '2') {
-    OC_CUDA(cudaStreamCreateWithFlags(&hs2, cudaStreamNonBlocking));
-    OC_CUDA(cudaStreamCreateWithFlags(&ds2, cudaStreamNonBlocking));
-    OC_CUDA(cudaEventCreateWithFlags(&ev_join[0], cudaEventDisableTiming));
-    OC_CUDA(cudaEventCreateWithFlags(&ev_join[1], cudaEventDisableTiming));
-  }
   if (s->replay.oom_fn >= 0) return Status::make(OC_E_DEVICE_OOM, "schedule's allocator replay ran out of memory");
   const auto& am = s->alloc;
   if (am.mode != m->model.mode) return Status::make(OC_E_ARG, "schedule and memory pool use different allocator modes");
@@ -544,11 +533,6 @@ Status Exec::run(oc_step_metrics* out) {
   OC_CUDA(cudaEventRecord(ev_fork, cs));
   OC_CUDA(cudaStreamWaitEvent(hs, ev_fork, 0));
   OC_CUDA(cudaStreamWaitEvent(ds, ev_fork, 0));
-  if (hs2) {
-    OC_CUDA(cudaStreamWaitEvent(hs2, ev_fork, 0));
-    OC_CUDA(cudaStreamWaitEvent(ds2, ev_fork, 0));
-  }
-  uint32_t n_hcopy = 0, n_dcopy = 0;
   for (uint32_t i = 0; i < n; ++i) {
     const FnSchedule& F = s->fn[i];
     XFn& X = fns[i];
@@ -570,7 +554,7 @@ Status Exec::run(oc_step_metrics* out) {
       Slot& sl = slots[a.slot];
       if (s->alloc.mode == OC_ALLOC_VA) OC_TRY(mem->bind(sl.span, sl.chunks));
       if (sl.packed) continue;
-      cudaStream_t h = (hs2 && sl.kind == ARRIVE_H2D && (n_hcopy++ & 1)) ? hs2 : hs;
+      cudaStream_t h = hs;
       for (const Ref& r : sl.waits) OC_CUDA(cudaStreamWaitEvent(h, ev_of(r), 0));
       OC_TRY(paper_gate(h));
       if (sl.kind == ARRIVE_H2D) {
@@ -683,10 +667,7 @@ Status Exec::run(oc_step_metrics* out) {
     if (on_comm)
       for (uint32_t v : f.out) vars[v].async_fn = (int32_t)i;
     // (c) reserved swap-outs after f_i; small ones through one pack kernel (A7)
-    if (!X.dep_reserve.empty()) {
-      OC_CUDA(cudaStreamWaitEvent(ds, ev_done[i], 0));
-      if (ds2) OC_CUDA(cudaStreamWaitEvent(ds2, ev_done[i], 0));
-    }
+    if (!X.dep_reserve.empty()) OC_CUDA(cudaStreamWaitEvent(ds, ev_done[i], 0));
     if (X.pout_n) {
       uint32_t first = X.dep_reserve[0];   // the pack kernel is timed on its first packed departure
       for (uint32_t d : X.dep_reserve)
@@ -711,7 +692,6 @@ Status Exec::run(oc_step_metrics* out) {
       }
       cudaStream_t dsk = ds;
       if (D.dirty || !opt.elide_clean) {
-        if (ds2 && (n_dcopy++ & 1)) dsk = ds2;
         if (opt.timeline) { OC_CUDA(cudaEventRecord(tl_out0[d], dsk)); tl_out_used[d] = 1; }
         OC_CUDA(cudaMemcpyAsync(host + xv.host_off, addr_of(D.var), xv.bytes, cudaMemcpyDeviceToHost, dsk));
         if (opt.timeline) OC_CUDA(cudaEventRecord(tl_out1[d], dsk));
@@ -727,12 +707,6 @@ Status Exec::run(oc_step_metrics* out) {
   if (comm_s) {   // the step ends when its last gradient exchange has
     OC_CUDA(cudaEventRecord(ev_cjoin, comm_s));
     OC_CUDA(cudaStreamWaitEvent(cs, ev_cjoin, 0));
-  }
-  if (hs2) {   // join the extra copy streams (their work is already complete or awaited)
-    OC_CUDA(cudaEventRecord(ev_join[0], hs2));
-    OC_CUDA(cudaEventRecord(ev_join[1], ds2));
-    OC_CUDA(cudaStreamWaitEvent(cs, ev_join[0], 0));
-    OC_CUDA(cudaStreamWaitEvent(cs, ev_join[1], 0));
   }
   return Status::ok();
   };
@@ -806,11 +780,6 @@ Status Exec::run(oc_step_metrics* out) {
 void Exec::destroy() {
   cudaSetDevice(device);
   cudaDeviceSynchronize();
-  if (hs2) cudaStreamDestroy(hs2);
-  if (ds2) cudaStreamDestroy(ds2);
-  for (auto& e : ev_join)
-    if (e) cudaEventDestroy(e), e = nullptr;
-  hs2 = ds2 = nullptr;
   for (auto& k : tl_k) k.destroy();
   for (auto& sl : slots) {
     if (sl.span.va) {

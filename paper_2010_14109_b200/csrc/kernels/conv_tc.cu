@@ -459,7 +459,6 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
 Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
                       int splits, int kb_per_split, bool accumulate);
 
-bool conv_tma_enabled();
 
 // channel counts the 64-wide tiles do not divide (e.g. ResNet-1001's 16/32,
 // BigGAN's 96, attention's 12-48): zero-padded to multiples of 64 in
@@ -469,7 +468,7 @@ bool pad_path(const ConvGeom& g, int mode) {
   // output channels the 8-wide rows do not divide (the 3-channel image a
   // generator emits, a 21-class segmentation head) run through a padded
   // output buffer (fprop) or a padded dY copy (dgrad / wgrad)
-  if (!conv_tma_enabled() || g.Cw != g.C || g.C % 8) return false;
+  if (g.Cw != g.C || g.C % 8) return false;
   if (g.K % 8) return dil_of(g) == 1;
   // 8/16-channel pixels are gathered natively by the fprop kernel, 16-channel ones by wgrad
   const bool nch = (mode == FPROP && (g.C == 8 || g.C == 16)) || (mode == WGRAD && g.C == 16);
@@ -500,18 +499,10 @@ struct Narrow {
   int64_t slice;      // images per slice
   size_t slice_bytes;
 };
-bool s2d_enabled() {
-  static int env = -1;
-  if (env < 0) {
-    const char* e = std::getenv("OC_CONV_S2D");
-    env = (e && e[0] == '0') ? 0 : 1;
-  }
-  return env == 1;
-}
 Narrow narrow_of(const ConvGeom& g) {
   Narrow n{g.C % 8 != 0, false, g, g, g.N, 0};
   if (!n.on) return n;
-  if (s2d_enabled() && g.st == 2 && g.C <= 4 && g.H % 2 == 0 && g.W % 2 == 0 && g.R == g.S) {
+  if (g.st == 2 && g.C <= 4 && g.H % 2 == 0 && g.W % 2 == 0 && g.R == g.S) {
     n.s2d = true;
     const int c = (g.pad + 1) / 2;
     int R2 = 1;
@@ -553,7 +544,7 @@ bool conv_tc_ok(const ConvGeom& g, int mode) {
     return false;
   }
   if (dil_of(g) > 1)   // atrous convs: the TMA kernels with dilated im2col offsets, 64-channel operands
-    return g.C % 64 == 0 && g.K % 64 == 0 && g.Cw == g.C && conv_tma_enabled() && (mode != DGRAD || g.st == 1);
+    return g.C % 64 == 0 && g.K % 64 == 0 && g.Cw == g.C && (mode != DGRAD || g.st == 1);
   if (pad_path(g, mode)) return true;
   // zero-padded activation channels (Cw < C) only on the 16-byte-chunk paths
   if (g.Cw != g.C && (g.C % 8 != 0 || g.Cw > g.C || mode == DGRAD)) return false;

@@ -595,8 +595,6 @@ int max_pairs() {
   static int n = 0;
   if (!n) {
     n = sm_count() / 2;
-    const char* e = std::getenv("OC_CONV_PAIRS");
-    if (e && std::atoi(e) > 0) n = std::atoi(e);
   }
   return n;
 }
@@ -652,14 +650,10 @@ Status make_tiled(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows
   return r == CUDA_SUCCESS ? Status::ok() : encode_fail(r, "cuTensorMapEncodeTiled");
 }
 
-bool tstore_enabled() {
-  const char* e = std::getenv("OC_CONV_TSTORE");
-  return !(e && e[0] == '0');
-}
 // the TMA-store epilogue for row-contiguous bf16 outputs that are not accumulated
 Status set_tstore(Params& P, void* out, int rows, int cols_stored, bool ok) {
   P.tstore = 0;
-  if (!ok || !tstore_enabled() || cols_stored % 8) return Status::ok();
+  if (!ok || cols_stored % 8) return Status::ok();
   Status st = make_tiled(&P.tc, out, (uint64_t)cols_stored, (uint64_t)rows, 32);
   if (!st.good()) return st;
   P.tstore = 1;
@@ -673,14 +667,7 @@ void fill(Params& P) {
   P.fS.init(P.S);
 }
 
-int conv_mt() {
-  static int mt = 0;
-  if (!mt) {
-    const char* e = std::getenv("OC_CONV_MT");
-    mt = (e && e[0] == '1') ? 1 : 2;
-  }
-  return mt;
-}
+int conv_mt() { return 2; }
 
 template <int MODE, int BN, int NCH, int MT, int CG = 1>
 Status launch_mt(OpArgs& a, Params P, int* stat_slots = nullptr) {
@@ -1162,18 +1149,8 @@ Status encode_tiled(CUtensorMap* m, const void* base, int rank, const cuuint64_t
 
 using namespace tma;
 
-bool conv_tma_enabled() {
-  static int env = -1;
-  if (env < 0) {
-    const char* e = std::getenv("OC_CONV_TMA");
-    env = (e && e[0] == '0') ? 0 : 1;
-  }
-  return env == 1;
-}
-
 // which kernel geometries the TMA kernels take (after the narrow-input re-layout)
 bool conv_tma_ok(const ConvGeom& g, int mode) {
-  if (!conv_tma_enabled()) return false;
   if (g.pad > 127 || g.R > 64 || g.S > 64 || g.st > 8 || dil_of(g) * (g.R - 1) > 127) return false;
   if (dil_of(g) > 1 && (g.C % 64 != 0 || (mode == DGRAD && g.st != 1))) return false;
   if (g.nopadh && mode == DGRAD) return false;
@@ -1237,7 +1214,7 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
                       __nv_bfloat16* y, bool accumulate, int nst, float* stat_part, int* stat_slots) {
   if (stat_slots) *stat_slots = 0;
   if (g.C == 16 && g.R == 4 && g.S == 4 && g.st == 1 && !g.nopadh && g.K == 64 && kpad == 256 && g.P % 16 == 0 &&
-      g.Q % 8 == 0 && !accumulate && !nst && tstore_enabled() && stem_enabled() && dil_of(g) == 1)
+      g.Q % 8 == 0 && !accumulate && !nst && stem_enabled() && dil_of(g) == 1)
     return conv_stem_tma(a, g, x, wb, kpad, y, stat_part, stat_slots);
   const int nch = g.C % 64 == 0 ? 0 : g.C;     // 8 or 16: narrow pixels, one tap per box
   Params P{};

@@ -79,8 +79,7 @@ Status conv_fwd(OpArgs& a) {
   float* stat = (float*)a.p(CF_STAT);
   if (!stat) return fprop(a, g, a.p(CF_X), (const float*)a.p(CF_W), a.p(CF_Y), acc);
   bool done = false;
-  const char* ef = std::getenv("OC_FUSED_STATS");   // "0": reduce y in a separate pass (A/B measurements)
-  if (!(ef && ef[0] == '0') && !f32(a) && !force_simt(&a) && conv_tc_ok(g, 0) && !acc) {
+  if (!f32(a) && !force_simt(&a) && conv_tc_ok(g, 0) && !acc) {
     OC_TRY(conv_fprop_tc(a, g, (const __nv_bfloat16*)a.p(CF_X), (const float*)a.p(CF_W), (__nv_bfloat16*)a.p(CF_Y),
                          false, stat, &done));
   } else {

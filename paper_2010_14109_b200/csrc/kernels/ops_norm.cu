@@ -836,34 +836,50 @@ __device__ __forceinline__ void issue_rows(const PoolGeom& g, int64_t u, const R
   bulk_load(tcu::smem_u32(s.gp), gp + u * g.Q * g.C, two * gb, bar);
   bulk_load(tcu::smem_u32(s.ix), idx + u * g.Q * g.C, two * ib, bar);
 }
-// routed gradient of the 2×2 block (2i.., 2j..) from the staged windows (rows i, i+1)
+// routed gradient of the 2×2 block (2i.., 2j..) from the staged windows (rows
+// i, i+1), pixel by pixel: with stride 2 and pad 1 each block pixel is reached
+// by fixed (window, tap) pairs — (0,0) ← (i,j) tap 4; (0,1) ← (i,j) 5,
+// (i,j+1) 3; (1,0) ← (i,j) 7, (i+1,j) 1; (1,1) ← (i,j) 8, (i,j+1) 6, (i+1,j) 2,
+// (i+1,j+1) 0 — summed in that (p, q) ascending order, the order pooled_grad8
+// uses; 9 compare-adds per channel instead of decoding every window's taps
 template <typename T>
 __device__ __forceinline__ void block_grad_smem(const PoolGeom& g, bool last_row, int j, int cg,
                                                 const RowStage<T>& s, float ga[4][8]) {
+  const bool has_r = !last_row, has_c = j + 1 < g.Q;
+  const int o00 = j * g.C + cg * 8, o01 = o00 + g.C, o10 = o00 + g.Q * g.C, o11 = o10 + g.C;
+  const uint2 i00 = *reinterpret_cast<const uint2*>(s.ix + o00);
+  const uint2 i01 = has_c ? *reinterpret_cast<const uint2*>(s.ix + o01) : make_uint2(~0u, ~0u);
+  const uint2 i10 = has_r ? *reinterpret_cast<const uint2*>(s.ix + o10) : make_uint2(~0u, ~0u);
+  const uint2 i11 = has_r && has_c ? *reinterpret_cast<const uint2*>(s.ix + o11) : make_uint2(~0u, ~0u);
+  const V8 g00 = ld8(s.gp + o00);
+  V8 g01, g10, g11;
 #pragma unroll
-  for (int px = 0; px < 4; ++px)
+  for (int k = 0; k < 8; ++k) g01.v[k] = g10.v[k] = g11.v[k] = 0.f;
+  if (has_c) g01 = ld8(s.gp + o01);
+  if (has_r) g10 = ld8(s.gp + o10);
+  if (has_r && has_c) g11 = ld8(s.gp + o11);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) ga[px][k] = 0.f;
-#pragma unroll
-  for (int wi = 0; wi < 2; ++wi) {
-    if (wi == 1 && last_row) continue;
-#pragma unroll
-    for (int wj = 0; wj < 2; ++wj) {
-      const int q = j + wj;
-      if (q >= g.Q) continue;
-      const int o = (wi * g.Q + q) * g.C + cg * 8;
-      const uint2 packed = *reinterpret_cast<const uint2*>(s.ix + o);
-      const V8 gv = ld8(s.gp + o);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t tap = ((k < 4 ? packed.x : packed.y) >> (8 * (k & 3))) & 0xff;
-        const int u = (int)((tap * 11) >> 5), v = (int)tap - 3 * u;   // tap / 3, tap % 3 for tap < 9
-        const int dr = 2 * wi - 1 + u, dc = 2 * wj - 1 + v;           // row / col inside the 2×2 block
-#pragma unroll
-        for (int px = 0; px < 4; ++px)
-          if (dr == (px >> 1) && dc == (px & 1)) ga[px][k] += gv.v[k];
-      }
-    }
+  for (int k = 0; k < 8; ++k) {
+    const int sh = 8 * (k & 3);
+    const uint32_t t00 = ((k < 4 ? i00.x : i00.y) >> sh) & 0xff, t01 = ((k < 4 ? i01.x : i01.y) >> sh) & 0xff;
+    const uint32_t t10 = ((k < 4 ? i10.x : i10.y) >> sh) & 0xff, t11 = ((k < 4 ? i11.x : i11.y) >> sh) & 0xff;
+    float a = 0.f;
+    if (t00 == 4) a += g00.v[k];
+    ga[0][k] = a;
+    a = 0.f;
+    if (t00 == 5) a += g00.v[k];
+    if (t01 == 3) a += g01.v[k];
+    ga[1][k] = a;
+    a = 0.f;
+    if (t00 == 7) a += g00.v[k];
+    if (t10 == 1) a += g10.v[k];
+    ga[2][k] = a;
+    a = 0.f;
+    if (t00 == 8) a += g00.v[k];
+    if (t01 == 6) a += g01.v[k];
+    if (t10 == 2) a += g10.v[k];
+    if (t11 == 0) a += g11.v[k];
+    ga[3][k] = a;
   }
 #pragma unroll
   for (int px = 0; px < 4; ++px)

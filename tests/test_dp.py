@@ -118,3 +118,43 @@ def test_nccl_single_rank_step_identical():
         st.close()
     for k in p:
         assert np.array_equal(outs[0][k], outs[1][k]), k
+
+
+@pytest.mark.gpu
+def test_nccl_single_rank_bucketed_resnet_identical():
+    """The bench's N > 1 configuration on one rank: a bf16 tiny ResNet with
+    bucketed allreduce functions (graphs.build(dp_bucket_bytes=...), one
+    ncclGroup per bucket on the executor's communication stream, SGD one
+    bucket later) under a swap-forcing budget; a one-rank NCCL communicator
+    makes every exchange an identity, so the step equals the step without a
+    communicator bitwise — the NCCL plumbing (dlopen, unique id, comm init,
+    group calls, comm-stream ordering) runs on the GPU."""
+    from paper_2010_14109_b200 import binding as B
+    from paper_2010_14109_b200 import graphs
+    from paper_2010_14109_b200.runtime import OutOfCoreStep, nccl_unique_id
+    spec = nets.tiny_resnet(batch=4, image=16, classes=10)
+    doc, info = graphs.build(spec, params="persistent", dp_bucket_bytes=16 << 10)
+    assert sum(1 for f in json.loads(doc)["functions"] if f["op"]["kind"] == "allreduce") > 1
+    G = B.Graph(doc)
+    budget = max(G.min_feasible_budget(0), int(G.in_core_peak() * 0.5))
+    x, y = nets.make_inputs(spec)
+    p = nets.make_params(spec)
+    phys = G.plan(budget, 0, B.OC_ALLOC_VA, chunk_bytes=2 << 20, phys_bytes=8 * budget + (1 << 30),
+                  allow_oom=True).stats()["peak_phys"] + (2 << 20)
+    xb = torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(torch.bfloat16).view(torch.int16).numpy()
+    outs = []
+    for use_nccl in (False, True):
+        st = OutOfCoreStep(doc, budget, 0, mode="va", chunk_bytes=2 << 20, phys_bytes=phys)
+        if use_nccl:
+            st.attach_nccl(nccl_unique_id(), 0, 1)
+        st.write(info["x"], xb)
+        st.write(info["labels"], y)
+        for k, v in p.items():
+            st.write(info["params"][k], v)
+            st.write(info["momentum"][k], np.zeros_like(v))
+        m = st.step()
+        assert m["bytes_d2h"] > 0
+        outs.append({k: st.read(info["params"][k]) for k in p})
+        st.close()
+    for k in p:
+        assert np.array_equal(outs[0][k], outs[1][k]), k
