@@ -142,9 +142,21 @@ __global__ void splitk_reduce(int splits, int64_t n, const float* __restrict__ p
 
 }  // namespace
 
+// split count the workspace is sized for (two CTAs per SM, at most 64)
 int wgrad_splits_simt(const ConvGeom& g) {
   const int64_t tiles = ((g.K + BM - 1) / BM) * (((int64_t)g.R * g.S * g.C + BN - 1) / BN);
   return (int)std::max<int64_t>(1, std::min<int64_t>(64, 296 / std::max<int64_t>(1, tiles)));
+}
+// split count a launch uses: about four CTAs per SM, each split at least 8
+// K-blocks deep, as many as the workspace it was given holds (a weight
+// gradient with few (k, r, s, c) outputs — the 3-channel first conv of
+// ResNet-1001, one tile — ran 64 splits on 64 SMs for 1 ms)
+int wgrad_splits_run(const ConvGeom& g, size_t ws_bytes) {
+  const int64_t tiles = ((g.K + BM - 1) / BM) * (((int64_t)g.R * g.S * g.C + BN - 1) / BN);
+  const int64_t depth = std::max<int64_t>(1, (int64_t)g.N * g.P * g.Q / (8 * BK));
+  const int64_t fit = (int64_t)(ws_bytes / ((size_t)g.K * g.R * g.S * g.C * 4));
+  const int64_t want = std::min<int64_t>(std::min<int64_t>(1024, depth), 4 * 148 / std::max<int64_t>(1, tiles));
+  return (int)std::max<int64_t>(std::min<int64_t>(wgrad_splits_simt(g), fit), std::min(want, fit));
 }
 
 template <typename T>
@@ -169,7 +181,7 @@ Status conv_dgrad_simt(OpArgs& a, const ConvGeom& g, const T* dy, const float* w
 
 template <typename T>
 Status conv_wgrad_simt(OpArgs& a, const ConvGeom& g, const T* dy, const T* x, float* dw) {
-  const int splits = wgrad_splits_simt(g);
+  const int splits = std::max(1, wgrad_splits_run(g, a.ws_bytes));
   const int64_t Kg = (int64_t)g.N * g.P * g.Q;
   int64_t step = (Kg + splits - 1) / splits;
   step = (step + BK - 1) / BK * BK;
