@@ -468,7 +468,18 @@ bool pad_path(const ConvGeom& g, int mode) {
   // output channels the 8-wide rows do not divide (the 3-channel image a
   // generator emits, a 21-class segmentation head) run through a padded
   // output buffer (fprop) or a padded dY copy (dgrad / wgrad)
-  if (g.Cw != g.C || g.C % 8) return false;
+  if (g.Cw != g.C) return false;
+  if (g.C % 8) {
+    // a narrow input (an image): fprop gathers it natively (Narrow); its data
+    // gradient (a discriminator's image input in a generator step) is computed
+    // into a 64-channel padded workspace output and the real channels copied
+    // (or added) out; its weight gradient, when K needs padding too, reads a
+    // 16-channel padded copy of X (the native 16-channel wgrad gather)
+    if (dil_of(g) != 1) return false;
+    if (mode == DGRAD) return g.st == 1 || g.st == 2;
+    if (mode == WGRAD) return g.K % 64 != 0 && g.C < 16;
+    return false;
+  }
   if (g.K % 8) return dil_of(g) == 1;
   // 8/16-channel pixels are gathered natively by the fprop kernel, 16-channel ones by wgrad
   const bool nch = (mode == FPROP && (g.C == 8 || g.C == 16)) || (mode == WGRAD && g.C == 16);
@@ -681,22 +692,27 @@ int up64(int c) { return (c + 63) / 64 * 64; }
 struct PadPlan {
   ConvGeom gk;             // padded geometry (full batch)
   bool pad_x, pad_y;       // X (C channels) / dY (K channels) need a padded copy
+  bool pad_out;            // dgrad of a narrow input: dX computed Cp wide in the workspace, real channels copied out
   int64_t slice;
-  size_t xbytes, ybytes;   // per-slice copy bytes
+  size_t xbytes, ybytes, obytes;   // per-slice copy / padded-output bytes
 };
 PadPlan pad_plan(const ConvGeom& g, int mode) {
-  PadPlan p{g, false, false, g.N, 0, 0};
+  PadPlan p{g, false, false, false, g.N, 0, 0, 0};
   const bool nch = (mode == FPROP && (g.C == 8 || g.C == 16)) || (mode == WGRAD && g.C == 16);
-  const int Cp = (g.C % 64 == 0 || nch) ? g.C : up64(g.C), Kp = up64(g.K);
+  const bool narrow_w = mode == WGRAD && g.C % 8 != 0 && g.C < 16;   // X padded to the 16-channel gather
+  const int Cp = (g.C % 64 == 0 || nch) ? g.C : (narrow_w ? 16 : up64(g.C)), Kp = up64(g.K);
   p.gk.C = p.gk.Cw = Cp;
   p.gk.K = Kp;
   p.pad_x = Cp != g.C && mode != DGRAD;
   // dY copy for dgrad / wgrad; for fprop with K % 8 != 0 the same buffer holds the padded output
   p.pad_y = Kp != g.K && (mode != FPROP || g.K % 8 != 0);
+  p.pad_out = mode == DGRAD && g.C % 8 != 0;
   const int64_t px = p.pad_x ? (int64_t)g.H * g.W * Cp * 2 : 0, py = p.pad_y ? (int64_t)g.P * g.Q * Kp * 2 : 0;
-  if (px + py > 0) p.slice = std::max<int64_t>(1, std::min<int64_t>(g.N, (64ll << 20) / (px + py)));
+  const int64_t po = p.pad_out ? (int64_t)g.H * g.W * Cp * 2 : 0;
+  if (px + py + po > 0) p.slice = std::max<int64_t>(1, std::min<int64_t>(g.N, (64ll << 20) / (px + py + po)));
   p.xbytes = align256((size_t)(p.slice * px));
   p.ybytes = align256((size_t)(p.slice * py));
+  p.obytes = align256((size_t)(p.slice * po));
   return p;
 }
 int tma_wgrad_splits(const ConvGeom& gk, int64_t slice) {
@@ -710,7 +726,7 @@ size_t pad_ws(const ConvGeom& g, int mode) {
   const PadPlan p = pad_plan(g, mode);
   const ConvGeom& k = p.gk;
   if (mode == FPROP) return align256((size_t)k.K * kpad_of(k) * 2) + p.xbytes + p.ybytes;
-  if (mode == DGRAD) return align256((size_t)k.C * k.R * k.S * k.K * 2) + p.ybytes;
+  if (mode == DGRAD) return align256((size_t)k.C * k.R * k.S * k.K * 2) + p.ybytes + p.obytes;
   return align256((size_t)tma_wgrad_splits(k, p.slice) * k.R * k.S * k.C * k.K * 4) + p.xbytes + p.ybytes;
 }
 
@@ -796,6 +812,20 @@ Status conv_dgrad_pad(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
     if (pp.pad_y) {
       OC_TRY(pad_copy(a, nn * g.P * g.Q, g.K, k.K, act, ybuf));
       act = ybuf;
+    }
+    if (pp.pad_out) {
+      // narrow dX: all Cp channels into the workspace, then the real ones out;
+      // accumulating, the old dX is padded into the workspace first and the
+      // kernel's epilogue adds to it (one rounding of old + dgrad, as the
+      // direct path; adding a rounded dgrad afterwards would round twice)
+      __nv_bfloat16* obuf = (__nv_bfloat16*)((char*)ybuf + pp.ybytes);
+      __nv_bfloat16* dxs = dx + n0 * g.H * g.W * g.C;
+      const int64_t rows = nn * g.H * g.W;
+      if (accumulate) OC_TRY(pad_copy(a, rows, g.C, k.C, dxs, obuf));
+      OC_TRY(conv_dgrad_tma(a, gs, act, wt, obuf, accumulate, k.C));
+      unpad_pixels<<<grid_for(rows * g.C, 256, 4), 256, 0, a.stream>>>(rows, g.C, k.C, obuf, dxs, 0);
+      OC_LAUNCH_CHECK(a);
+      continue;
     }
     OC_TRY(conv_dgrad_tma(a, gs, act, wt, dx + n0 * g.H * g.W * g.C, accumulate, g.C));
   }

@@ -106,8 +106,19 @@ def test_conv_fwd(g):
     assert np.max(np.abs(y - ref)) <= 2 ** -7 * np.max(np.abs(ref)) + 1e-6
 
 
+# narrow inputs (an image) in the backward: the data gradient through a
+# 64-channel padded workspace output (real channels copied or added out), the
+# weight gradient through a 16-channel padded copy of X when K needs padding
+NARROW_BWD = [
+    (2, 12, 10, 3, 96, 3, 1, 1),      # BigGAN discriminator input conv 3 -> 96
+    (2, 9, 8, 3, 96, 1, 1, 0),        # ... and its 1x1 shortcut
+    (3, 10, 9, 5, 64, 3, 2, 1),       # 5 channels, stride 2 (dgrad phases)
+    (2, 11, 7, 3, 16, 3, 1, 1),       # ResNet-1001 input conv 3 -> 16
+]
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("g", SHAPES[:5] + PAD)
+@pytest.mark.parametrize("g", SHAPES[:5] + PAD + NARROW_BWD)
 @pytest.mark.parametrize("accumulate", [False, True])
 def test_conv_dgrad(g, accumulate):
     N, H, W, C, K, R, st, pad = g[:8]
@@ -127,7 +138,7 @@ def test_conv_dgrad(g, accumulate):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("g", SHAPES + PAD)
+@pytest.mark.parametrize("g", SHAPES + PAD + NARROW_BWD)
 def test_conv_wgrad(g):
     N, H, W, C, K, R, st, pad = g[:8]
     rng = np.random.default_rng(3)
