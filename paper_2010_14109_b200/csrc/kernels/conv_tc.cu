@@ -445,9 +445,13 @@ void fill_divs(Params& P) {
 using namespace tc;
 
 bool conv_tma_ok(const ConvGeom& g, int mode);
+// cmem (optional): channels per pixel of the gathered tensor in memory (x for
+// fprop / wgrad, dY for dgrad) when it is narrower than the kernel's padded
+// channel count — the tensor map's channel extent, so the channels past it
+// arrive as the TMA engine's zero fill instead of through a padded copy
 Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* wb, int kpad,
                       __nv_bfloat16* y, bool accumulate, int nst = 0, float* stat_part = nullptr,
-                      int* stat_slots = nullptr);
+                      int* stat_slots = nullptr, int cmem = 0);
 namespace tma {
 int stat_slots_max();   // epilogue statistics slots per launch (CTA × epilogue warp)
 int sm_count();
@@ -455,9 +459,10 @@ int grid_cap(int ctas);   // OC_CONV_MAX_CTAS (tests)
 }  // namespace tma
 Status bn_stats_from_parts(OpArgs& a, int nslots, int64_t rows, int C, const float* part, float* stat);
 Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* wt,
-                      __nv_bfloat16* dx, bool accumulate, int nst = 0);
+                      __nv_bfloat16* dx, bool accumulate, int nst = 0, int cmem = 0);
+// cmem: channels per pixel of x in memory; kmem: of dY (0 = the geometry's own)
 Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
-                      int splits, int kb_per_split, bool accumulate);
+                      int splits, int kb_per_split, bool accumulate, int cmem = 0, int kmem = 0);
 
 
 // channel counts the 64-wide tiles do not divide (e.g. ResNet-1001's 16/32,
@@ -703,9 +708,13 @@ PadPlan pad_plan(const ConvGeom& g, int mode) {
   const int Cp = (g.C % 64 == 0 || nch) ? g.C : (narrow_w ? 16 : up64(g.C)), Kp = up64(g.K);
   p.gk.C = p.gk.Cw = Cp;
   p.gk.K = Kp;
-  p.pad_x = Cp != g.C && mode != DGRAD;
+  // an operand of >= 64 channels whose pixels are 16-byte rows is read in
+  // place (the tensor map's channel extent is its own, the TMA engine zero-fills
+  // the padding channels); narrower ones get a padded copy
+  const bool x_direct = g.C % 8 == 0 && g.C >= 64, y_direct = g.K % 8 == 0 && g.K >= 64;
+  p.pad_x = Cp != g.C && mode != DGRAD && !x_direct;
   // dY copy for dgrad / wgrad; for fprop with K % 8 != 0 the same buffer holds the padded output
-  p.pad_y = Kp != g.K && (mode != FPROP || g.K % 8 != 0);
+  p.pad_y = Kp != g.K && (mode == FPROP ? g.K % 8 != 0 : !y_direct);
   p.pad_out = mode == DGRAD && g.C % 8 != 0;
   const int64_t px = p.pad_x ? (int64_t)g.H * g.W * Cp * 2 : 0, py = p.pad_y ? (int64_t)g.P * g.Q * Kp * 2 : 0;
   const int64_t po = p.pad_out ? (int64_t)g.H * g.W * Cp * 2 : 0;
@@ -777,20 +786,22 @@ Status conv_fprop_pad(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
     ConvGeom gs = k;
     gs.N = (int)nn;
     const __nv_bfloat16* act = x + n0 * g.H * g.W * g.C;
+    int cmem = g.C;
     if (pp.pad_x) {
       OC_TRY(pad_copy(a, nn * g.H * g.W, g.C, k.C, act, xbuf));
       act = xbuf;
+      cmem = k.C;
     }
     if (pp.pad_y) {   // K % 8 != 0: all Kp channels into the workspace, then the real ones out
       __nv_bfloat16* ybuf = (__nv_bfloat16*)((char*)xbuf + pp.xbytes);
-      OC_TRY(conv_fprop_tma(a, gs, act, wb, kpad, ybuf, false, 0));
+      OC_TRY(conv_fprop_tma(a, gs, act, wb, kpad, ybuf, false, 0, nullptr, nullptr, cmem));
       const int64_t rows = nn * g.P * g.Q;
       unpad_pixels<<<grid_for(rows * g.K, 256, 4), 256, 0, a.stream>>>(rows, g.K, k.K, ybuf,
                                                                        y + n0 * g.P * g.Q * g.K, accumulate ? 1 : 0);
       OC_LAUNCH_CHECK(a);
       continue;
     }
-    OC_TRY(conv_fprop_tma(a, gs, act, wb, kpad, y + n0 * g.P * g.Q * g.K, accumulate, g.K));
+    OC_TRY(conv_fprop_tma(a, gs, act, wb, kpad, y + n0 * g.P * g.Q * g.K, accumulate, g.K, nullptr, nullptr, cmem));
   }
   return Status::ok();
 }
@@ -809,9 +820,11 @@ Status conv_dgrad_pad(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
     ConvGeom gs = k;
     gs.N = (int)nn;
     const __nv_bfloat16* act = dy + n0 * g.P * g.Q * g.K;
+    int kmem = g.K;
     if (pp.pad_y) {
       OC_TRY(pad_copy(a, nn * g.P * g.Q, g.K, k.K, act, ybuf));
       act = ybuf;
+      kmem = k.K;
     }
     if (pp.pad_out) {
       // narrow dX: all Cp channels into the workspace, then the real ones out;
@@ -822,12 +835,12 @@ Status conv_dgrad_pad(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
       __nv_bfloat16* dxs = dx + n0 * g.H * g.W * g.C;
       const int64_t rows = nn * g.H * g.W;
       if (accumulate) OC_TRY(pad_copy(a, rows, g.C, k.C, dxs, obuf));
-      OC_TRY(conv_dgrad_tma(a, gs, act, wt, obuf, accumulate, k.C));
+      OC_TRY(conv_dgrad_tma(a, gs, act, wt, obuf, accumulate, k.C, kmem));
       unpad_pixels<<<grid_for(rows * g.C, 256, 4), 256, 0, a.stream>>>(rows, g.C, k.C, obuf, dxs, 0);
       OC_LAUNCH_CHECK(a);
       continue;
     }
-    OC_TRY(conv_dgrad_tma(a, gs, act, wt, dx + n0 * g.H * g.W * g.C, accumulate, g.C));
+    OC_TRY(conv_dgrad_tma(a, gs, act, wt, dx + n0 * g.H * g.W * g.C, accumulate, g.C, kmem));
   }
   return Status::ok();
 }
@@ -846,15 +859,18 @@ Status conv_wgrad_pad(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
     gs.N = (int)nn;
     const __nv_bfloat16* xa = x + n0 * g.H * g.W * g.C;
     const __nv_bfloat16* ya = dy + n0 * g.P * g.Q * g.K;
+    int cmem = g.C, kmem = g.K;
     if (pp.pad_x) {
       OC_TRY(pad_copy(a, nn * g.H * g.W, g.C, k.C, xa, xbuf));
       xa = xbuf;
+      cmem = k.C;
     }
     if (pp.pad_y) {
       OC_TRY(pad_copy(a, nn * g.P * g.Q, g.K, k.K, ya, ybuf));
       ya = ybuf;
+      kmem = k.K;
     }
-    OC_TRY(conv_wgrad_tma(a, gs, xa, ya, part, splits, 0, sl > 0));
+    OC_TRY(conv_wgrad_tma(a, gs, xa, ya, part, splits, 0, sl > 0, cmem, kmem));
   }
   wgrad_reduce<<<dim3((k.K + 31) / 32, (RSCp + 31) / 32), 1024, 0, a.stream>>>(splits, RSCp, k.K, k.C, g.C, part, dw,
                                                                               g.K);

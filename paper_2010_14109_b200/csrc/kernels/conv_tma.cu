@@ -1211,7 +1211,7 @@ Status conv_stem_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const
 // stat_part (optional): fused BN statistics of y (TMA-store epilogue only); on
 // return *stat_slots = the slots written (0: not fused, the caller reduces y)
 Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* wb, int kpad,
-                      __nv_bfloat16* y, bool accumulate, int nst, float* stat_part, int* stat_slots) {
+                      __nv_bfloat16* y, bool accumulate, int nst, float* stat_part, int* stat_slots, int cmem) {
   if (stat_slots) *stat_slots = 0;
   if (g.C == 16 && g.R == 4 && g.S == 4 && g.st == 1 && !g.nopadh && g.K == 64 && kpad == 256 && g.P % 16 == 0 &&
       g.Q % 8 == 0 && !accumulate && !nst && stem_enabled() && dil_of(g) == 1)
@@ -1219,7 +1219,7 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   const int nch = g.C % 64 == 0 ? 0 : g.C;     // 8 or 16: narrow pixels, one tap per box
   Params P{};
   const int padh = g.nopadh ? 0 : g.pad;
-  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, nch ? nch : 64, BM, g.P, g.Q, g.st, padh, g.pad,
+  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, cmem > 0 ? cmem : g.C, nch ? nch : 64, BM, g.P, g.Q, g.st, padh, g.pad,
                           nch == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE
                                    : (nch == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B));
   if (!st.good()) return st;
@@ -1263,7 +1263,7 @@ Status conv_fprop_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
 // valid taps: dx[(n,h',w')][C] = im2col_{pad''}(dy) · Wt_bf16[C][(r,s,K)]ᵀ at the
 // phase's filter taps; a phase no tap reaches gets zeros (or keeps dx when accumulating)
 Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, const __nv_bfloat16* wt,
-                      __nv_bfloat16* dx, bool accumulate, int nst) {
+                      __nv_bfloat16* dx, bool accumulate, int nst, int cmem) {
   // phases no filter tap reaches (e.g. 3 of the 4 phases of a 1×1 stride-2 conv):
   // without accumulation their dx is zero — cleared once for the whole tensor
   bool tapless = false;
@@ -1288,7 +1288,7 @@ Status conv_dgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* dy, con
       const int dl = dil_of(g);
       const int dh = (ph + g.pad - r0) / g.st, dw = (pw + g.pad - s0) / g.st;
       const int padh = nr > 0 ? dl * (nr - 1) - dh : 0, padw = ns > 0 ? dl * (ns - 1) - dw : 0;
-      Status st = make_im2col(&P.ta, dy, g.N, g.P, g.Q, g.K, 64, BM, Hp, Wp, 1, padh, padw);
+      Status st = make_im2col(&P.ta, dy, g.N, g.P, g.Q, cmem > 0 ? cmem : g.K, 64, BM, Hp, Wp, 1, padh, padw);
       if (!st.good()) return st;
       const Tile tile = choose_tile(g.N * Hp * Wp, g.C, std::max(1, nr * ns * g.K / BK));
       const int BN = tile.bn;
@@ -1369,14 +1369,14 @@ Status conv_stem_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x,
 
 // wgrad partials part[z][R·S·C][K] over pixel blocks [z·kbps, (z+1)·kbps)
 Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, const __nv_bfloat16* dy, float* part,
-                      int splits, int kb_per_split, bool accumulate) {
+                      int splits, int kb_per_split, bool accumulate, int cmem, int kmem) {
   if (g.C == 16 && g.R == 4 && g.S == 4 && g.st == 1 && !g.nopadh && g.K == 64 && g.P % 16 == 0 && g.Q % 8 == 0 &&
       splits >= 1 && splits <= 1024 && stem_enabled() && dil_of(g) == 1)
     return conv_stem_wgrad_tma(a, g, x, dy, part, splits, accumulate);
   Params P{};
   const int nch = g.C == 16 ? 16 : 0;
   const int padh = g.nopadh ? 0 : g.pad;
-  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, g.C, nch ? 16 : 64, WKB, g.P, g.Q, g.st, padh, g.pad,
+  Status st = make_im2col(&P.ta, x, g.N, g.H, g.W, cmem > 0 ? cmem : g.C, nch ? 16 : 64, WKB, g.P, g.Q, g.st, padh, g.pad,
                           nch ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B);
   if (!st.good()) return st;
   const int BN = g.K % 128 == 0 ? 128 : 64;
@@ -1387,7 +1387,7 @@ Status conv_wgrad_tma(OpArgs& a, const ConvGeom& g, const __nv_bfloat16* x, cons
   const char* ecg = std::getenv("OC_WGRAD_CG");
   const bool force = ecg && ecg[0] == '2', off = ecg && ecg[0] == '1';
   const int pbn = (nch || off) ? 0 : (g.K % 256 == 0 ? 256 : ((force && g.K % 128 == 0) ? 128 : 0));
-  st = make_tiled(&P.tb, dy, (uint64_t)g.K, (uint64_t)g.N * g.P * g.Q, WKB);
+  st = make_tiled(&P.tb, dy, (uint64_t)(kmem > 0 ? kmem : g.K), (uint64_t)g.N * g.P * g.Q, WKB);
   if (!st.good()) return st;
   P.out = part;
   P.accumulate = accumulate ? 1 : 0;

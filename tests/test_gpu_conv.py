@@ -31,7 +31,10 @@ SHAPES = [  # N, H, W, C, K, R, stride, pad
 PAD = [
     (2, 9, 7, 32, 16, 3, 1, 1),       # ResNet-1001-like 32 -> 16
     (3, 8, 8, 16, 32, 1, 1, 0),       # 16 -> 32, 1x1 (fprop gathers 16-ch pixels)
-    (2, 10, 9, 96, 96, 3, 2, 1),      # BigGAN-like 96 channels, stride 2 (dgrad phases)
+    (2, 10, 9, 96, 96, 3, 2, 1),      # BigGAN-like 96 channels, stride 2 (dgrad phases): X and dY read in
+                                      # place, the TMA engine zero-fills channels 96..127
+    (2, 9, 8, 160, 96, 3, 1, 1),      # DenseNet-like 160 -> 96, both operands read in place
+    (3, 8, 7, 224, 128, 1, 1, 0),     # DenseNet bottleneck 1x1 224 -> 128
     (2, 6, 6, 64, 24, 1, 1, 0),       # attention-like 64 -> 24
     (2, 8, 8, 24, 64, 3, 1, 1),       # 24 -> 64
     # output channels not a multiple of 8: fprop stores through a padded
