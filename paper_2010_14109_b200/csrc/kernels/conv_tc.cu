@@ -711,7 +711,7 @@ PadPlan pad_plan(const ConvGeom& g, int mode) {
   // an operand of >= 64 channels whose pixels are 16-byte rows is read in
   // place (the tensor map's channel extent is its own, the TMA engine zero-fills
   // the padding channels); narrower ones get a padded copy
-  const bool x_direct = g.C % 8 == 0 && g.C >= 64, y_direct = g.K % 8 == 0 && g.K >= 64;
+  const bool x_direct = g.C % 8 == 0 && g.C >= 16, y_direct = g.K % 8 == 0 && g.K >= 16;
   p.pad_x = Cp != g.C && mode != DGRAD && !x_direct;
   // dY copy for dgrad / wgrad; for fprop with K % 8 != 0 the same buffer holds the padded output
   p.pad_y = Kp != g.K && (mode == FPROP ? g.K % 8 != 0 : !y_direct);
