@@ -542,6 +542,14 @@ Narrow narrow_of(const ConvGeom& g) {
   return n;
 }
 
+// forward conv of a narrow input whose output width K is a multiple of 8 but
+// not of 64 (a discriminator's 3 -> 96 input conv): the kernels run Kp =
+// up64(K) weight rows (zero past K) and store the first K columns (nst); 0 = n/a
+int narrow_fprop_kp(const Narrow& nw, const ConvGeom& g0) {
+  if (!nw.on || nw.s2d || g0.K % 64 == 0 || g0.K % 8 != 0) return 0;
+  return (g0.K + 63) / 64 * 64;
+}
+
 }  // namespace
 
 bool conv_tc_ok(const ConvGeom& g, int mode) {
@@ -552,7 +560,10 @@ bool conv_tc_ok(const ConvGeom& g, int mode) {
   // 32-bit element offsets of whole activation tensors
   const Narrow nw = narrow_of(g);
   const int64_t nimg = nw.on ? nw.slice : g.N;
-  const bool tma = conv_tma_ok(nw.gk, mode) || pad_path(g, mode);
+  ConvGeom gk = nw.gk;
+  const int kp = mode == FPROP ? narrow_fprop_kp(nw, g) : 0;
+  if (kp) gk.K = kp;
+  const bool tma = conv_tma_ok(gk, mode) || pad_path(g, mode);
   if (tma) {
     if (nimg * g.P * g.Q >= (1ll << 31) || (int64_t)g.N * g.H * g.W >= (1ll << 31)) return false;
   } else if ((int64_t)g.N * g.H * g.W * ((g.C + 63) / 64 * 64) >= (1ll << 31) ||
@@ -565,6 +576,7 @@ bool conv_tc_ok(const ConvGeom& g, int mode) {
   // zero-padded activation channels (Cw < C) only on the 16-byte-chunk paths
   if (g.Cw != g.C && (g.C % 8 != 0 || g.Cw > g.C || mode == DGRAD)) return false;
   if (mode == DGRAD) return g.K % 64 == 0 && g.C % 64 == 0 && (g.st == 1 || g.st == 2);
+  if (kp) return tma;
   return g.K % 64 == 0;
 }
 
@@ -890,7 +902,8 @@ size_t conv_tc_ws(const ConvGeom& g0, int mode) {
     const int64_t nsl = (g.N + nw.slice - 1) / nw.slice;
     return align256((size_t)wgrad_splits(gs, wgrad_bn(g)) * g.R * g.S * g.C * g.K * 4) + nw.slice_bytes;
   }
-  return align256((size_t)g.K * kpad_of(g) * 2) + nw.slice_bytes;
+  const int kp = mode == FPROP ? narrow_fprop_kp(nw, g0) : 0;
+  return align256((size_t)(kp ? kp : g.K) * kpad_of(g) * 2) + nw.slice_bytes;
 }
 
 // partial-sum region of the fused BN statistics: one set of slots per image slice
@@ -905,20 +918,22 @@ Status conv_fprop_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* x, cons
   if (stat_done) *stat_done = false;
   if (pad_path(g0, FPROP)) return conv_fprop_pad(a, g0, x, w, y, accumulate);
   const Narrow nw = narrow_of(g0);
-  const ConvGeom& g = nw.gk;
+  const int kp = narrow_fprop_kp(nw, g0);
+  ConvGeom g = nw.gk;
+  if (kp) g.K = kp;   // weight rows past the real K are zero; only the first K columns are stored
   __nv_bfloat16* wb = (__nv_bfloat16*)a.ws;
   const int kpad = kpad_of(g);
   __nv_bfloat16* xbuf = (__nv_bfloat16*)((char*)a.ws + align256((size_t)g.K * kpad * 2));
   // fused statistics: slices append their epilogue slots (part[slot][2][K]) after the conv workspace
   float* part = stat ? (float*)((char*)a.ws + conv_tc_ws(g0, FPROP)) : nullptr;
   int nslots = 0;
-  bool fused = stat != nullptr;
+  bool fused = stat != nullptr && !kp;   // stored columns ≠ computed ones: statistics in a separate pass
   if (nw.s2d)
     weight_bf16_s2d<<<grid_for((int64_t)g.K * kpad, 256, 4), 256, 0, a.stream>>>(
         w, wb, g.K, g0.R, g0.S, g0.C, g.R, g.S, g.pad, g0.pad, kpad);
   else
     weight_bf16<<<grid_for((int64_t)g.K * kpad, 256, 1), 256, 0, a.stream>>>(w, wb, g.K, g.R * g.S, g.C, 0, kpad,
-                                                                              g.Cw);
+                                                                              g.Cw, g0.K);
   OC_LAUNCH_CHECK(a);
   for (int64_t n0 = 0; n0 < g.N; n0 += nw.slice) {
     const int64_t nn = g.N - n0 < nw.slice ? g.N - n0 : nw.slice;
@@ -932,7 +947,7 @@ Status conv_fprop_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* x, cons
       P.act = xbuf;
     }
     P.wgt = wb;
-    P.out = y + n0 * g.P * g.Q * g.K;
+    P.out = y + n0 * g.P * g.Q * g0.K;
     P.M = (int)(nn * g.P * g.Q);
     P.N = g.K;
     P.kpad = kpad;
@@ -942,13 +957,14 @@ Status conv_fprop_tc(OpArgs& a, const ConvGeom& g0, const __nv_bfloat16* x, cons
     P.accumulate = accumulate ? 1 : 0;
     if (conv_tma_ok(P.g, FPROP)) {
       int sl = 0;
-      Status st = conv_fprop_tma(a, P.g, P.act, wb, kpad, (__nv_bfloat16*)P.out, accumulate, 0,
+      Status st = conv_fprop_tma(a, P.g, P.act, wb, kpad, (__nv_bfloat16*)P.out, accumulate, kp ? g0.K : 0,
                                  fused ? part + (size_t)nslots * 2 * g.K : nullptr, fused ? &sl : nullptr);
       if (!st.good()) return st;
       if (sl == 0) fused = false;
       nslots += sl;
       continue;
     }
+    if (kp) return Status::make(OC_E_INVARIANT, "conv: padded-K narrow fprop needs the TMA kernels");
     fused = false;
     fill_divs(P);
     const dim3 grid((P.M + BM - 1) / BM, g.K / (g.K % 128 == 0 ? 128 : 64), 1);

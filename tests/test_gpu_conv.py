@@ -94,8 +94,20 @@ def _from_bits(a, shape):
     return torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).float().numpy().reshape(shape).astype(np.float64)
 
 
+# narrow inputs (an image) whose output width is not a multiple of 64: the
+# forward runs 64-multiple weight rows and stores the real columns; the data gradient through a
+# 64-channel padded workspace output (real channels copied or added out), the
+# weight gradient through a 16-channel padded copy of X when K needs padding
+NARROW_BWD = [
+    (2, 12, 10, 3, 96, 3, 1, 1),      # BigGAN discriminator input conv 3 -> 96
+    (2, 9, 8, 3, 96, 1, 1, 0),        # ... and its 1x1 shortcut
+    (3, 10, 9, 5, 64, 3, 2, 1),       # 5 channels, stride 2 (dgrad phases)
+    (2, 11, 7, 3, 16, 3, 1, 1),       # ResNet-1001 input conv 3 -> 16
+]
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("g", SHAPES + PAD)
+@pytest.mark.parametrize("g", SHAPES + PAD + NARROW_BWD)
 def test_conv_fwd(g):
     N, H, W, C, K, R, st, pad = g[:8]
     rng = np.random.default_rng(1)
@@ -107,17 +119,6 @@ def test_conv_fwd(g):
     ref = nm.round_bf16(nm.conv2d(x.float().numpy().astype(np.float64), nm.round_bf16(w.astype(np.float64)), st, pad))
     assert nm.rel_l2(y, ref) < 1e-3
     assert np.max(np.abs(y - ref)) <= 2 ** -7 * np.max(np.abs(ref)) + 1e-6
-
-
-# narrow inputs (an image) in the backward: the data gradient through a
-# 64-channel padded workspace output (real channels copied or added out), the
-# weight gradient through a 16-channel padded copy of X when K needs padding
-NARROW_BWD = [
-    (2, 12, 10, 3, 96, 3, 1, 1),      # BigGAN discriminator input conv 3 -> 96
-    (2, 9, 8, 3, 96, 1, 1, 0),        # ... and its 1x1 shortcut
-    (3, 10, 9, 5, 64, 3, 2, 1),       # 5 channels, stride 2 (dgrad phases)
-    (2, 11, 7, 3, 16, 3, 1, 1),       # ResNet-1001 input conv 3 -> 16
-]
 
 
 @pytest.mark.gpu
@@ -218,6 +219,7 @@ STAT_CASES = [
     ((3, 11, 10, 64, 128, 3, 2, 1), ""),
     ((3, 17, 16, 3, 64, 7, 2, 3, 2), ""),      # stem: space-to-depth slices of 2 images
     ((2, 15, 13, 3, 64, 7, 2, 3), ""),         # 8-channel pixels
+    ((2, 12, 10, 3, 96, 3, 1, 1), ""),         # narrow input, K = 96 (padded weight rows; statistics pass)
     ((2, 9, 7, 64, 64, 3, 1, 1), "simt"),
 ]
 
