@@ -458,7 +458,10 @@ void plan_split(const Gemm& g, int& splits, int& kps) {
   const int64_t target = 2 * 148;
   splits = 1;
   if (!g.ep_p && !g.no_split && !g.bias && !g.relu && tiles < target && nkb >= 8) {
-    int64_t s = (target + tiles - 1) / tiles;
+    // whole waves: at most two CTAs per SM fit (shared memory), so rounding the
+    // split count up would start a second, mostly idle wave (384 CTAs for 296
+    // slots, ncu: a 1.3-wave dS product at 0.28 of HBM); rounding down keeps one
+    int64_t s = std::max<int64_t>(1, target / tiles);
     s = std::min<int64_t>(s, nkb / 4);
     s = std::min<int64_t>(s, 65535 / std::max(1, g.batch));
     splits = (int)std::max<int64_t>(1, s);
