@@ -746,7 +746,9 @@ __global__ void __launch_bounds__(AT_NT) attn_p_kernel(const __grid_constant__ A
 int attn_js(int nb, int L) {
   const int rb = (L + BM - 1) / BM, tiles = (L + AT_N - 1) / AT_N;
   const int64_t ctas = (int64_t)rb * nb;
-  int js = (int)std::min<int64_t>(std::min(tiles, AT_JS), std::max<int64_t>(1, (4 * 148 + ctas - 1) / ctas));
+  // two CTAs fit per SM: at most two whole waves (rounding the range count up
+  // had left a 0.27-full third wave, ncu: 2.27 waves per SM)
+  int js = (int)std::min<int64_t>(std::min(tiles, AT_JS), std::max<int64_t>(1, (4 * 148) / ctas));
   return std::max(1, js);
 }
 }  // namespace
